@@ -1,0 +1,113 @@
+"""End-to-end acceptance checks against the oracle — TEST INFRASTRUCTURE.
+
+These turn BASELINE.json's north-star correctness statement into executable checks
+(readings R1-R16).  With tol_j = 1e-5 * (||q_i||^2 + ||c_j||^2)
+(fp64 norms, the north star's "relative 1e-5 of (||q||^2 + ||c||^2)"):
+
+* E2E-1 "pinned rows exact": a row is pinned iff
+  max_{r<k}(D64[s_r] + tol_{s_r}) < min_{r>=k}(D64[s_r] - tol_{s_r}) in the oracle's
+  order s; on a pinned row the returned index SET equals the oracle's.
+* E2E-2 "tolerance-consistent" (every row): each returned distance within tol of
+  D64; each returned j has D64[j] <= D64[s_{k-1}] + tol_j + tol_{s_{k-1}}; no
+  non-returned j has D64[j] < D64[s_{k-1}] - tol_j - tol_{s_{k-1}}; indices distinct,
+  in range, no self in graph mode; the list is sorted by (distance, index).
+* E2E-3 "integer grid exact" is a plain equality with the oracle's R32 lists and
+  needs no helper.
+
+All comparisons are in the squared-distance domain; for the Euclidean metric the
+returned d_E is mapped back with the +-1 ulp sqrt widening of SURVEY §8(c).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+REL_TOL = 1e-5  # BASELINE.json north_star: "within relative 1e-5 of (||q||^2 + ||c||^2)"
+_ULP = 2.0 ** -23
+
+
+def _sorted_by_order(idx, dist):
+    """True iff (dist, idx) is non-decreasing under the (value, index) order."""
+    d = dist.astype(np.float64)
+    for a in range(len(idx) - 1):
+        if d[a] > d[a + 1] or (d[a] == d[a + 1] and idx[a] >= idx[a + 1]):
+            return False
+    return True
+
+
+def check_rows(gpu_idx, gpu_dist, D64sq, qn, cn, rows, k, metric=0, graph=False):
+    """Run E2E-1 and E2E-2 on sampled rows.
+
+    gpu_idx/gpu_dist: R×k results of the CUDA path for the query rows ``rows``;
+    D64sq: R×N fp64 SQUARED distances from oracle.dist_rows(metric=L2SQ);
+    qn: fp64 ||q||^2 of the R query rows; cn: fp64 ||c||^2 of all N corpus rows.
+    Returns dict(n_rows, n_pinned, failures=[str]).
+    """
+    R, N = D64sq.shape
+    failures = []
+    n_pinned = 0
+    for r in range(R):
+        i = int(rows[r])
+        D = D64sq[r].copy()
+        valid = np.ones(N, bool)
+        if graph:
+            valid[i] = False
+        tol = REL_TOL * (qn[r] + cn)
+        cand = np.nonzero(valid)[0]
+        order = cand[np.lexsort((cand, D[cand]))]  # oracle order s: (D64, idx)
+        kth = order[k - 1]
+        gi = np.asarray(gpu_idx[r], np.int64)
+        gd = np.asarray(gpu_dist[r], np.float64)
+        tag = f"row {i}"
+        if np.any(gi < 0) or np.any(gi >= N):
+            failures.append(f"{tag}: index out of range")
+            continue
+        if len(np.unique(gi)) != k:
+            failures.append(f"{tag}: duplicate indices")
+            continue
+        if graph and np.any(gi == i):
+            failures.append(f"{tag}: contains self")
+            continue
+        if not _sorted_by_order(gi, gd):
+            failures.append(f"{tag}: list not sorted by (distance, index)")
+        S = D[gi]
+        t = tol[gi]
+        if metric == 0:
+            bad = np.abs(gd - S) > t
+        else:
+            lo = np.sqrt(np.maximum(0.0, S - t)) * (1 - _ULP)
+            hi = np.sqrt(S + t) * (1 + _ULP)
+            bad = (gd < lo) | (gd > hi)
+        if np.any(bad):
+            j = int(gi[np.argmax(bad)])
+            failures.append(f"{tag}: distance of {j} outside tolerance")
+        if np.any(S > D[kth] + t + tol[kth]):
+            failures.append(f"{tag}: returned a neighbour beyond the k-th + tolerance")
+        ret = np.zeros(N, bool)
+        ret[gi] = True
+        missed = valid & ~ret & (D < D[kth] - tol - tol[kth])
+        if np.any(missed):
+            failures.append(f"{tag}: missed neighbour {int(np.nonzero(missed)[0][0])}")
+        top, rest = order[:k], order[k:]
+        pinned = len(rest) == 0 or np.max(D[top] + tol[top]) < np.min(D[rest] - tol[rest])
+        if pinned:
+            n_pinned += 1
+            if set(gi.tolist()) != set(top.tolist()):
+                failures.append(f"{tag}: pinned row index set differs from the oracle")
+    return {"n_rows": R, "n_pinned": n_pinned, "failures": failures}
+
+
+def check_distances(D_gpu, D64sq, qn, cn, metric=0):
+    """a-S3 parity: |D_gpu - D64| <= 1e-5 (||q_i||^2 + ||c_j||^2) elementwise.
+
+    Returns (max ratio |err| / tol, number of violations)."""
+    tol = REL_TOL * (qn[:, None] + cn[None, :])
+    G = np.asarray(D_gpu, np.float64)
+    if metric == 0:
+        err = np.abs(G - D64sq)
+        ratio = err / np.maximum(tol, 1e-300)
+        return float(ratio.max(initial=0.0)), int((err > tol).sum())
+    lo = np.sqrt(np.maximum(0.0, D64sq - tol)) * (1 - _ULP)
+    hi = np.sqrt(D64sq + tol) * (1 + _ULP)
+    bad = (G < lo) | (G > hi)
+    err = np.abs(G * G - D64sq)
+    return float((err / np.maximum(tol, 1e-300)).max(initial=0.0)), int(bad.sum())
