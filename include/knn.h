@@ -1,0 +1,151 @@
+/* knn.h — C ABI of libknn.so: B200-native (sm_100a) brute-force k-NN search and
+ * k-NN-graph construction, the data-parallel hot path of arXiv 1309.5478
+ * ("Fast k-NNG construction with GPU-based quick multi-select").
+ *
+ * Problem statement (§Introduction): given a corpus of N points and a set
+ * of M query points, k-NN finds for each query the k nearest corpus points; in the
+ * k-NN graph (k-NNG) every corpus point is also a query.  Method:
+ * (1) the M×N distance matrix, computed as a matrix product (PAPER.md:73-83,
+ *     d^2 = ||x||^2 + ||y||^2 - 2 x.y), then
+ * (2) a per-row multi-select of the k smallest distances and their indices
+ *     ("GPU-based quick multi-select").
+ *
+ * Conventions (all entry points)
+ *  - Layout: point sets are row-major fp32, one point per row, row stride = d
+ *    ("vector-contiguous"; the paper's vectors are the columns of X).
+ *    Outputs are M×k row-major: out_idx[i*k + r] (int32), out_dist[i*k + r] (fp32).
+ *  - Order: each output row is sorted ascending by the total order
+ *        (distance ascending, -0 == +0, NaN after +inf; ties by smaller index)
+ *    (readings R1, R2, R6).  Results are deterministic and bit-identical
+ *    across runs, launch configurations and GPU shardings.
+ *  - Pointers: every float / int pointer argument is a DEVICE pointer on the ctx's
+ *    device unless stated otherwise; `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).  The caller owns all inputs and outputs; the
+ *    library never frees or retains caller pointers after return.  Workspace is owned
+ *    by the ctx, grown on demand, freed by knn_ctx_destroy.
+ *  - Errors: status codes only, never exceptions/aborts across the ABI.  Argument
+ *    errors are detected before any launch.  On error outputs are unspecified and
+ *    knn_last_error(ctx) describes the failure.
+ *  - Threading: a ctx is not thread-safe; distinct ctxs are independent.
+ */
+#ifndef KNN_B200_H
+#define KNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNN_ABI_VERSION 1
+
+typedef struct knn_ctx* knn_ctx_t;
+
+/* Distance metrics.  L2SQ = d^2, L2 = d_E = sqrt(d^2)
+ * (PAPER.md:61).  COSINE / PEARSON are NEXT work: KNN_ERR_UNSUPPORTED. */
+typedef enum { KNN_L2SQ = 0, KNN_L2 = 1, KNN_COSINE = 2, KNN_PEARSON = 3 } knn_metric;
+
+typedef enum {
+    KNN_OK = 0,
+    KNN_ERR_ARG = 1,          /* invalid argument (sizes, k range, null pointer, alignment) */
+    KNN_ERR_UNSUPPORTED = 2,  /* valid request the library does not implement (metric, k > 1024) */
+    KNN_ERR_NONFINITE = 3,    /* input holds NaN/inf, or a squared norm >= FLT_MAX/4 (R8) */
+    KNN_ERR_OOM = 4,          /* device workspace allocation failed */
+    KNN_ERR_CUDA = 5,         /* a CUDA runtime/driver call failed */
+    KNN_ERR_NCCL = 6,         /* reserved for collective failures */
+    KNN_ERR_INTERNAL = 7
+} knn_status;
+
+/* "No self exclusion" value for the self_shift arguments below. */
+#define KNN_NO_SELF INT64_MIN
+/* Largest supported k. */
+#define KNN_MAX_K 1024
+
+int         knn_abi_version(void);
+/* Create a context bound to CUDA device `device`. */
+knn_status  knn_ctx_create(int device, knn_ctx_t* out);
+knn_status  knn_ctx_destroy(knn_ctx_t ctx);
+/* Message for the last non-OK status of this ctx (static storage inside ctx). */
+const char* knn_last_error(knn_ctx_t ctx);
+
+/* ---------------------------------------------------------------- top level ------
+ * Blocking: return after the work queued on `stream` has completed, so the status is
+ * final (including KNN_ERR_NONFINITE from the input validation of knn_rownorms).
+ *
+ * knn_graph: the k-NNG of X (N×d).  Row i lists the k nearest OTHER points of x_i:
+ * self is excluded by position (reading R3), so 1 <= k <= min(N-1, 1024).
+ * metric: KNN_L2SQ or KNN_L2.  out_idx/out_dist: N×k. */
+knn_status knn_graph(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
+                     int32_t metric, int32_t* out_idx, float* out_dist, void* stream);
+
+/* knn_search: for each of the M queries Q (M×d), its k nearest points of X (N×d) under
+ * squared Euclidean distance (the north-star signature knn_search(query, M, corpus, N,
+ * d, k)).  1 <= k <= min(N, 1024).  out_idx/out_dist: M×k. */
+knn_status knn_search(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                      int32_t d, int32_t k, int32_t* out_idx, float* out_dist, void* stream);
+
+/* knn_search_block: the general block both sharded drivers are built from.  Query i of
+ * Q against corpus point j of X, with
+ *   - self exclusion by position: pair (i, j) is dropped when j == i + self_shift
+ *     (self_shift = KNN_NO_SELF: nothing dropped).  A row whose valid corpus points
+ *     number fewer than k is padded with (+inf, excluded index) entries, which sort
+ *     after every finite distance;
+ *   - idx_offset added to every returned index (global index of X's first row).
+ * 1 <= k <= min(N, 1024).  metric KNN_L2SQ / KNN_L2.  Blocking, like knn_graph. */
+knn_status knn_search_block(knn_ctx_t ctx, const float* Q, int64_t M, const float* X,
+                            int64_t N, int32_t d, int32_t k, int32_t metric,
+                            int64_t self_shift, int64_t idx_offset,
+                            int32_t* out_idx, float* out_dist, void* stream);
+
+/* Same computation with HOST input/output buffers (pageable or pinned): copies Q and X
+ * to the device, runs knn_search_block, copies the M×k results back; all inside the
+ * call.  This is the end-to-end entry point a host application uses. */
+knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
+                                 const float* X_host, int64_t N, int32_t d, int32_t k,
+                                 int32_t metric, int64_t self_shift, int64_t idx_offset,
+                                 int32_t* out_idx_host, float* out_dist_host, void* stream);
+
+/* ---------------------------------------------------------------- building blocks --
+ * Stream-ordered (asynchronous): they validate arguments, enqueue kernels on `stream`
+ * and return.  Used by the tests and the benchmark. */
+
+/* ||x_j||^2 = sum_t x_j[t]^2 for j < N, accumulated in fp64, rounded to fp32
+ * (norms by reduction; reading R15).  out_sqn: N floats.
+ * Also writes *out_flag (device int32, may be NULL) = 1 when some x is non-finite or
+ * some ||x||^2 >= FLT_MAX/4, else leaves it unchanged (caller zeroes it). */
+knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, float* out_sqn,
+                        int32_t* out_flag, void* stream);
+
+/* The distance matrix: for i < M, j < N
+ *   D[i*ldD + j] = max(||q_i||^2 + ||x_j||^2 - 2 q_i.x_j, 0)   (metric KNN_L2SQ)
+ *                 sqrt of that                                (metric KNN_L2)
+ * with the dot products from the FP32-accurate split tensor-core GEMM
+ * and +inf where j == i + self_shift.  ldD >= N.  D: M×ldD floats. */
+knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                         int32_t d, int32_t metric, int64_t self_shift, float* D, int64_t ldD,
+                         void* stream);
+
+/* The per-row multi-select: for each row i < M of D (row stride ldD,
+ * N columns), the k smallest (D[i,j], j) under the total order above, written sorted.
+ * Values are written canonicalised (-0 -> +0, NaN -> +NaN).  1 <= k <= min(N, 1024),
+ * ldD >= N.  Exact: bit-identical to sorting the row. */
+knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64_t ldD,
+                      int32_t k, int32_t* out_idx, float* out_dist, void* stream);
+
+/* k-way merge of partial lists ("Batch execution will obviously require
+ * merging of results"): part_dist / part_idx are G blocks laid out [G][M][k]; list g's
+ * indices are shifted by offsets_host[g] (a HOST array of G int64) before the merge.
+ * Output: the first k of the union under the total order (global index tie-break),
+ * M×k.  Equal to the unsharded select when the G lists come from contiguous column
+ * shards.  1 <= G <= 64, 1 <= k <= 1024. */
+knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_idx, int32_t G,
+                     int64_t M, int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                     float* out_dist, void* stream);
+
+/* Number of kernel launches this ctx has issued so far (for benchmarks). */
+int64_t knn_launch_count(knn_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNN_B200_H */

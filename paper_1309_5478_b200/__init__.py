@@ -12,6 +12,6 @@ __all__ = ["datagen", "knn"]
 
 def __getattr__(name):
     if name == "knn":
-        from . import knn
-        return knn
+        import importlib
+        return importlib.import_module(__name__ + ".knn")
     raise AttributeError(name)

@@ -1,0 +1,415 @@
+// api.cu — host runtime behind the C ABI of include/knn.h: argument validation,
+// workspace management, plan choice and the orchestration of the hot path
+//   a-S2 prep (norms + split)  ->  a-S3 distance GEMM  ->  a-S4 per-row select
+// over bounded row blocks of the distance matrix.  No kernels live here.
+#include "../../include/knn.h"
+#include "internal.cuh"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+struct knn_ctx {
+    int device = 0;
+    int num_sms = 148;
+    bool tc_ok = false;
+    int gemm_mode = 0;  // 0 = tensor-core split GEMM, 1 = SIMT FFMA (KNN_GEMM=simt)
+    std::string err;
+    void* ws = nullptr;  // compute workspace
+    size_t ws_size = 0;
+    void* io = nullptr;  // device copies for the host-buffer entry point
+    size_t io_size = 0;
+    int32_t* flag_host = nullptr;  // pinned
+    int64_t launches = 0;
+    size_t d_budget = (size_t)4 << 30;  // bytes of distance-matrix block per launch pair
+};
+
+namespace {
+
+using knn::ceil_div;
+using knn::round_up;
+
+knn_status fail(knn_ctx* c, knn_status st, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return st;
+}
+
+#define KNN_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(ctx, KNN_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define KNN_TRY(call)                  \
+    do {                               \
+        knn_status s_ = (call);        \
+        if (s_ != KNN_OK) return s_;   \
+    } while (0)
+
+knn_status ensure(knn_ctx* ctx, void** buf, size_t* size, size_t need) {
+    if (need <= *size) return KNN_OK;
+    if (*buf) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return fail(ctx, KNN_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+        cudaFree(*buf);
+        *buf = nullptr;
+        *size = 0;
+    }
+    size_t sz = need + (need >> 3);
+    if (cudaMalloc(buf, sz) != cudaSuccess) {
+        cudaGetLastError();
+        if (cudaMalloc(buf, need) != cudaSuccess) {
+            cudaGetLastError();
+            *buf = nullptr;
+            return fail(ctx, KNN_ERR_OOM, "cannot allocate %zu bytes of workspace", need);
+        }
+        sz = need;
+    }
+    *size = sz;
+    return KNN_OK;
+}
+
+// Bump allocator over a workspace region (256-byte aligned slices).
+struct Carve {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = round_up((int64_t)off, 256);
+        T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+knn_status set_device(knn_ctx* ctx) {
+    KNN_CUDA(cudaSetDevice(ctx->device));
+    return KNN_OK;
+}
+
+bool metric_ok(knn_ctx* ctx, int32_t metric, knn_status* st) {
+    if (metric == KNN_L2SQ || metric == KNN_L2) return true;
+    if (metric == KNN_COSINE || metric == KNN_PEARSON)
+        *st = fail(ctx, KNN_ERR_UNSUPPORTED, "metric %d (cosine/pearson) is not implemented yet",
+                   metric);
+    else
+        *st = fail(ctx, KNN_ERR_ARG, "unknown metric %d", metric);
+    return false;
+}
+
+// Split operands of one point set, produced by prep.
+struct Prepared {
+    float* sqn;
+    float* rs;
+    __half* hi;
+    __half* lo;
+};
+
+// Queue the whole hot path for one block problem; asynchronous on `s`.
+knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                     int32_t d, int32_t k, int32_t metric, int64_t self_shift, int64_t idx_offset,
+                     int32_t* out_idx, float* out_dist, cudaStream_t s) {
+    const bool same = (Q == X) && (M == N);
+    const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    const int64_t ldD = round_up(N, 4);
+    int64_t rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldD * sizeof(float)));
+    rows_blk = rows_blk < 128 ? 128 : (rows_blk / 128) * 128;
+    if (rows_blk > M) rows_blk = M;
+
+    auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
+        flag = c.take<int32_t>(4);
+        auto prep = [&](Prepared& p, int64_t n) {
+            p.sqn = c.take<float>(n);
+            p.rs = c.take<float>(n);
+            p.hi = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
+            p.lo = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
+        };
+        prep(px, N);
+        if (same) pq = px; else prep(pq, M);
+        D = c.take<float>((size_t)rows_blk * ldD);
+    };
+    Carve probe{nullptr};
+    Prepared pq{}, px{};
+    float* D = nullptr;
+    int32_t* flag = nullptr;
+    layout(probe, pq, px, D, flag);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve, pq, px, D, flag);
+
+    KNN_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+    ctx->launches++;
+    if (!same) {
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
+        ctx->launches++;
+    }
+    for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
+        const int64_t R = (M - r0) < rows_blk ? (M - r0) : rows_blk;
+        const int64_t shift = self_shift == KNN_NO_SELF ? KNN_NO_SELF : self_shift + r0;
+        if (tc) {
+            knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
+                               px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+            KNN_CUDA(knn::launch_dist_tc(op, metric, shift, D, ldD, ctx->num_sms, s));
+        } else {
+            KNN_CUDA(knn::launch_dist_simt(Q + r0 * d, pq.sqn + r0, R, X, px.sqn, N, d, metric,
+                                           shift, D, ldD, s));
+        }
+        ctx->launches++;
+        KNN_CUDA(knn::launch_select(D, R, N, ldD, k, idx_offset, out_idx + r0 * k,
+                                    out_dist + r0 * k, s));
+        ctx->launches++;
+    }
+    return KNN_OK;
+}
+
+knn_status finish_blocking(knn_ctx* ctx, cudaStream_t s) {
+    // The flag is the first slice of the workspace (see run_block's layout).
+    int32_t* flag = static_cast<int32_t*>(ctx->ws);
+    KNN_CUDA(cudaMemcpyAsync(ctx->flag_host, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    KNN_CUDA(cudaStreamSynchronize(s));
+    if (*ctx->flag_host)
+        return fail(ctx, KNN_ERR_NONFINITE,
+                    "input contains NaN/inf or a vector with ||x||^2 >= FLT_MAX/4");
+    return KNN_OK;
+}
+
+knn_status check_block_args(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                            int32_t d, int32_t k, int32_t metric, int64_t self_shift,
+                            int64_t idx_offset, const void* out_idx, const void* out_dist) {
+    knn_status st = KNN_OK;
+    if (!metric_ok(ctx, metric, &st)) return st;
+    if (N < 1 || M < 0 || d < 1) return fail(ctx, KNN_ERR_ARG, "bad sizes M=%lld N=%lld d=%d",
+                                             (long long)M, (long long)N, d);
+    if (N > INT32_MAX || M > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M and N must be < 2^31");
+    if (idx_offset < 0 || idx_offset + N - 1 > INT32_MAX)
+        return fail(ctx, KNN_ERR_ARG, "idx_offset + N must fit int32");
+    if (k < 1 || k > N) return fail(ctx, KNN_ERR_ARG, "k=%d outside [1, N=%lld]", k, (long long)N);
+    if (k > KNN_MAX_K) return fail(ctx, KNN_ERR_UNSUPPORTED, "k=%d > %d", k, KNN_MAX_K);
+    if (M > 0 && (!Q || !X || !out_idx || !out_dist)) return fail(ctx, KNN_ERR_ARG, "null pointer");
+    (void)self_shift;
+    return KNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int knn_abi_version(void) { return KNN_ABI_VERSION; }
+
+knn_status knn_ctx_create(int device, knn_ctx_t* out) {
+    if (!out) return KNN_ERR_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return KNN_ERR_CUDA;
+    }
+    knn_ctx* c = new knn_ctx();
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return KNN_ERR_CUDA;
+    }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->tc_ok = knn::tc_supported();
+    const char* g = getenv("KNN_GEMM");
+    if (g && strcmp(g, "simt") == 0) c->gemm_mode = 1;
+    const char* b = getenv("KNN_D_BUDGET_MB");
+    if (b) c->d_budget = (size_t)atoll(b) << 20;
+    if (cudaMallocHost(&c->flag_host, sizeof(int32_t)) != cudaSuccess) {
+        delete c;
+        return KNN_ERR_CUDA;
+    }
+    *out = c;
+    return KNN_OK;
+}
+
+knn_status knn_ctx_destroy(knn_ctx_t ctx) {
+    if (!ctx) return KNN_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->io) cudaFree(ctx->io);
+    if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
+    delete ctx;
+    return KNN_OK;
+}
+
+const char* knn_last_error(knn_ctx_t ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+knn_status knn_search_block(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                            int32_t d, int32_t k, int32_t metric, int64_t self_shift,
+                            int64_t idx_offset, int32_t* out_idx, float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    KNN_TRY(check_block_args(ctx, Q, M, X, N, d, k, metric, self_shift, idx_offset, out_idx,
+                             out_dist));
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    KNN_TRY(run_block(ctx, Q, M, X, N, d, k, metric, self_shift, idx_offset, out_idx, out_dist, s));
+    return finish_blocking(ctx, s);
+}
+
+knn_status knn_graph(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
+                     int32_t metric, int32_t* out_idx, float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (N >= 1 && k > N - 1)
+        return fail(ctx, KNN_ERR_ARG, "knn_graph needs k <= N-1 (k=%d, N=%lld)", k, (long long)N);
+    return knn_search_block(ctx, X, N, X, N, d, k, metric, 0, 0, out_idx, out_dist, stream);
+}
+
+knn_status knn_search(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                      int32_t d, int32_t k, int32_t* out_idx, float* out_dist, void* stream) {
+    return knn_search_block(ctx, Q, M, X, N, d, k, KNN_L2SQ, KNN_NO_SELF, 0, out_idx, out_dist,
+                            stream);
+}
+
+knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
+                                 const float* X_host, int64_t N, int32_t d, int32_t k,
+                                 int32_t metric, int64_t self_shift, int64_t idx_offset,
+                                 int32_t* out_idx_host, float* out_dist_host, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    KNN_TRY(check_block_args(ctx, Q_host, M, X_host, N, d, k, metric, self_shift, idx_offset,
+                             out_idx_host, out_dist_host));
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool same = Q_host == X_host && M == N;
+    auto layout = [&](Carve& c, float*& q, float*& x, int32_t*& oi, float*& od) {
+        x = c.take<float>((size_t)N * d);
+        q = same ? x : c.take<float>((size_t)M * d);
+        oi = c.take<int32_t>((size_t)M * k);
+        od = c.take<float>((size_t)M * k);
+    };
+    Carve probe{nullptr};
+    float *q, *x, *od;
+    int32_t* oi;
+    layout(probe, q, x, oi, od);
+    KNN_TRY(ensure(ctx, &ctx->io, &ctx->io_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->io)};
+    layout(carve, q, x, oi, od);
+    KNN_CUDA(cudaMemcpyAsync(x, X_host, (size_t)N * d * sizeof(float), cudaMemcpyHostToDevice, s));
+    if (!same)
+        KNN_CUDA(cudaMemcpyAsync(q, Q_host, (size_t)M * d * sizeof(float), cudaMemcpyHostToDevice, s));
+    KNN_TRY(run_block(ctx, q, M, x, N, d, k, metric, self_shift, idx_offset, oi, od, s));
+    KNN_CUDA(cudaMemcpyAsync(out_idx_host, oi, (size_t)M * k * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+    KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)M * k * sizeof(float),
+                             cudaMemcpyDeviceToHost, s));
+    return finish_blocking(ctx, s);
+}
+
+knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, float* out_sqn,
+                        int32_t* out_flag, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (N < 0 || d < 1) return fail(ctx, KNN_ERR_ARG, "bad sizes");
+    if (N > 0 && (!X || !out_sqn)) return fail(ctx, KNN_ERR_ARG, "null pointer");
+    if (N == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    KNN_CUDA(knn::launch_prep(X, N, d, 0, out_sqn, nullptr, nullptr, nullptr, out_flag,
+                              static_cast<cudaStream_t>(stream)));
+    ctx->launches++;
+    return KNN_OK;
+}
+
+knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
+                         int32_t d, int32_t metric, int64_t self_shift, float* D, int64_t ldD,
+                         void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    knn_status st = KNN_OK;
+    if (!metric_ok(ctx, metric, &st)) return st;
+    if (M < 0 || N < 1 || d < 1 || ldD < N) return fail(ctx, KNN_ERR_ARG, "bad sizes");
+    if (M > INT32_MAX || N > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M and N must be < 2^31");
+    if (M > 0 && (!Q || !X || !D)) return fail(ctx, KNN_ERR_ARG, "null pointer");
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool same = (Q == X) && (M == N);
+    const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    auto layout = [&](Carve& c, Prepared& pq, Prepared& px, int32_t*& flag) {
+        flag = c.take<int32_t>(4);
+        auto prep = [&](Prepared& p, int64_t n) {
+            p.sqn = c.take<float>(n);
+            p.rs = c.take<float>(n);
+            p.hi = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
+            p.lo = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
+        };
+        prep(px, N);
+        if (same) pq = px; else prep(pq, M);
+    };
+    Carve probe{nullptr};
+    Prepared pq{}, px{};
+    int32_t* flag;
+    layout(probe, pq, px, flag);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve, pq, px, flag);
+    KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+    ctx->launches++;
+    if (!same) {
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
+        ctx->launches++;
+    }
+    if (tc) {
+        knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        KNN_CUDA(knn::launch_dist_tc(op, metric, self_shift, D, ldD, ctx->num_sms, s));
+    } else {
+        KNN_CUDA(knn::launch_dist_simt(Q, pq.sqn, M, X, px.sqn, N, d, metric, self_shift, D, ldD, s));
+    }
+    ctx->launches++;
+    return KNN_OK;
+}
+
+knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
+                      int32_t* out_idx, float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (M < 0 || N < 1 || ldD < N) return fail(ctx, KNN_ERR_ARG, "bad sizes");
+    if (N > INT32_MAX || M > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M and N must be < 2^31");
+    if (k < 1 || k > N) return fail(ctx, KNN_ERR_ARG, "k=%d outside [1, N]", k);
+    if (k > KNN_MAX_K) return fail(ctx, KNN_ERR_UNSUPPORTED, "k=%d > %d", k, KNN_MAX_K);
+    if (M > 0 && (!D || !out_idx || !out_dist)) return fail(ctx, KNN_ERR_ARG, "null pointer");
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    KNN_CUDA(knn::launch_select(D, M, N, ldD, k, 0, out_idx, out_dist,
+                                static_cast<cudaStream_t>(stream)));
+    ctx->launches++;
+    return KNN_OK;
+}
+
+knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_idx, int32_t G,
+                     int64_t M, int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                     float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (G < 1 || G > 64 || M < 0) return fail(ctx, KNN_ERR_ARG, "bad G=%d or M", G);
+    if (M > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M must be < 2^31");
+    if (k < 1) return fail(ctx, KNN_ERR_ARG, "k=%d < 1", k);
+    if (k > KNN_MAX_K) return fail(ctx, KNN_ERR_UNSUPPORTED, "k=%d > %d", k, KNN_MAX_K);
+    if (M > 0 && (!part_dist || !part_idx || !offsets_host || !out_idx || !out_dist))
+        return fail(ctx, KNN_ERR_ARG, "null pointer");
+    for (int g = 0; g < G; ++g)
+        if (offsets_host[g] < 0 || offsets_host[g] > INT32_MAX)
+            return fail(ctx, KNN_ERR_ARG, "offset %d out of range", g);
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    KNN_CUDA(knn::launch_merge(part_dist, part_idx, G, M, k, offsets_host, out_idx, out_dist,
+                               static_cast<cudaStream_t>(stream)));
+    ctx->launches++;
+    return KNN_OK;
+}
+
+}  // extern "C"

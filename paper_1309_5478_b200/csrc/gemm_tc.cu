@@ -1,0 +1,395 @@
+// gemm_tc.cu — a-S3: the distance matrix as a dense contraction on the 5th-generation
+// tensor cores (tcgen05 + TMEM + TMA), FP32-accurate, with the distance assembly fused
+// into the epilogue.
+//
+// Paper: "the n×m dot products x_i.y_j ... are easily formulated as a matrix product
+// X^T Y"; "d^2_ij = ||x_i||^2 + ||y_j||^2 - 2 x_i.y_j";
+// d_E = sqrt(d^2).  The paper used a library SGEMM on Fermi FP32 cores.
+//
+// B200 design:
+//  * Operands are the per-vector power-of-two-scaled fp16 halves of prep.cu:
+//    s_q q = qh + ql,  s_x x = xh + xl.  The dot is recovered FP32-accurately from three
+//    fp16 products with fp32 accumulation in TMEM:  ql.xh + qh.xl + qh.xh  (the
+//    dropped ql.xl and the split residuals are <= ~3*2^-22 relative per term), issued
+//    as three K-segments of one accumulation, smallest terms first.  fp16 runs at twice
+//    the TF32 tensor rate, so this costs what 1.5 TF32 passes would (vs 3 for 3xTF32).
+//  * Warp-specialised persistent kernel, one CTA per SM, 6 warps:
+//      warp 0  TMA producer: per K-block loads qh, ql (BM×BK) and xh, xl (BN×BK) tiles,
+//              swizzled K-major, into a STAGES-deep ring (each stage feeds 3 MMA
+//              segments, so the hi tiles are loaded once and used twice);
+//      warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16);
+//      warps 2-5 epilogue: tcgen05.ld (32x32b.x32) -> registers -> fused distance
+//              assembly -> streaming 128-bit stores of the fp32 distance row.
+//    The accumulator is double-buffered in TMEM (2 × 256 columns), so the epilogue of
+//    tile t overlaps the MMAs of tile t+1.
+//  * Epilogue (per element): acc*(-2 rs_q) is exact (power-of-two scale), so
+//      D = max(fma(acc * (-2 rs_q), rs_x, ||q||^2 + ||x||^2), 0) + 0
+//    rounds once; +0 canonicalises -0 (R6); sqrt for L2; +inf on the excluded self pair.
+#include "internal.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace knn {
+namespace {
+
+constexpr int BM = 128;          // rows per tile (TMEM lanes)
+constexpr int BN = 256;          // columns per tile (TMEM columns per accumulator)
+constexpr int BK = 64;           // fp16 K elements per stage = one 128-byte swizzle row
+constexpr int STAGES = 2;
+constexpr int UMMA_K = 16;
+constexpr int THREADS = 192;
+constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (16 KB)
+constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (32 KB)
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands
+constexpr int TMEM_COLS = 512;   // 2 accumulators × BN fp32 columns
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, cols*/ +
+                           2 * BN * 2 * 4 /*column norms/scales, double buffered*/;
+constexpr int GROUP_M = 16;      // tile-order swizzle: 16 row blocks share a column sweep
+
+// Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
+// [4,6) D format = F32 (1); [7,10) A = F16 (0); [10,13) B = F16 (0); bit 15/16 = 0:
+// both K-major; [17,23) N>>3; [24,29) M>>4.
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+// ------------------------------------------------------------ PTX wrappers ----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+// Shared-memory matrix descriptor, K-major, 128-byte swizzle (PTX ISA "Matrix
+// descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
+// [32,46) SBO>>4 = 1024 B between 8-row core-matrix groups; [46,48) version = 1;
+// [49,52) base offset = 0 (tiles are 1024-aligned); [61,64) layout = 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+
+struct TileMap {
+    int64_t n_mb, n_nb;
+    __device__ __forceinline__ void get(int64_t t, int64_t& mb, int64_t& nb) const {
+        const int64_t per_group = (int64_t)GROUP_M * n_nb;
+        const int64_t g = t / per_group;
+        const int64_t r = t - g * per_group;
+        const int64_t m0 = g * GROUP_M;
+        const int64_t gm = (n_mb - m0) < GROUP_M ? (n_mb - m0) : GROUP_M;
+        mb = m0 + r % gm;
+        nb = r / gm;
+    }
+};
+
+struct EpiArgs {
+    const float* qn; const float* q_rs; int64_t M;
+    const float* xn; const float* x_rs; int64_t N;
+    int32_t metric; int64_t self_shift; float* D; int64_t ldD;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
+               const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
+               int num_kb, TileMap tiles, int64_t num_tiles, EpiArgs ep) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint8_t* stage_base = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    float* col_n = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);  // [2][BN]
+    float* col_s = col_n + 2 * BN;                                                  // [2][BN]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qh)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ql)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_xh)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_xl)));
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer --------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int64_t mb, nb;
+                tiles.get(t, mb, nb);
+                const int row_a = (int)(mb * BM), row_b = (int)(nb * BN);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                    const uint32_t fb = full0 + 8 * stage;
+                    mbar_expect_tx(fb, STAGE_BYTES);
+                    const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                    tma_load_2d(sb, &map_qh, fb, kb * BK, row_a);
+                    tma_load_2d(sb + A_BYTES, &map_ql, fb, kb * BK, row_a);
+                    tma_load_2d(sb + 2 * A_BYTES, &map_xh, fb, kb * BK, row_b);
+                    tma_load_2d(sb + 2 * A_BYTES + B_BYTES, &map_xl, fb, kb * BK, row_b);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer ----------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+                const int buf = it & 1;
+                const uint32_t tphase = (it >> 1) & 1;
+                mbar_wait(tempty0 + 8 * buf, tphase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + buf * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(full0 + 8 * stage, phase);
+                    tc_fence_after();
+                    const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                    const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + 2 * A_BYTES,
+                                   xl = sb + 2 * A_BYTES + B_BYTES;
+                    // three K-segments, smallest terms first: ql.xh, qh.xl, qh.xh
+                    const uint32_t sa[3] = {ql, qh, qh};
+                    const uint32_t sbx[3] = {xh, xl, xh};
+                    #pragma unroll
+                    for (int seg = 0; seg < 3; ++seg) {
+                        #pragma unroll
+                        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                            const uint32_t acc = (kb | seg | kk) != 0;
+                            tc_mma(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2),
+                                   sdesc(sbx[seg] + kk * UMMA_K * 2), acc);
+                        }
+                    }
+                    tc_commit(empty0 + 8 * stage);  // frees the smem stage when MMAs finish
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(tfull0 + 8 * buf);  // accumulator ready for the epilogue
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------ epilogue (4 warps) --
+        const int quad = warp & 3;             // TMEM lane quadrant this warp may access
+        const int etid = threadIdx.x - 64;     // 0..127
+        const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+            int64_t mb, nb;
+            tiles.get(t, mb, nb);
+            const int buf = it & 1;
+            const uint32_t tphase = (it >> 1) & 1;
+            const int64_t n0 = nb * BN;
+            // stage the tile's column norms and scales (double-buffered by `buf`)
+            float* cn = col_n + buf * BN;
+            float* cs = col_s + buf * BN;
+            for (int c = etid; c < BN; c += 128) {
+                const int64_t j = n0 + c;
+                cn[c] = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
+                cs[c] = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+            }
+            named_bar(1, 128);
+            const int64_t row = mb * BM + quad * 32 + lane;
+            const bool row_ok = row < ep.M;
+            const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
+            const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
+            const int64_t self_col = row + ep.self_shift;  // wraps harmlessly for KNN_NO_SELF
+            float* drow = ep.D + row * ep.ldD + n0;
+
+            mbar_wait(tfull0 + 8 * buf, tphase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+            #pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t r[32];
+                tmem_ld32(taddr + ch * 32, r);
+                if (ch == BN / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                }
+                if (!row_ok) continue;
+                float v[32];
+                #pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int cc = ch * 32 + c;
+                    float dd = fmaf(__uint_as_float(r[c]) * cq, cs[cc], qn + cn[cc]);
+                    dd = fmaxf(dd, 0.0f) + 0.0f;
+                    if (ep.metric == 1) dd = sqrtf(dd);
+                    if (n0 + cc == self_col) dd = __int_as_float(0x7F800000);
+                    v[c] = dd;
+                }
+                const int64_t c0 = n0 + ch * 32;
+                if (vec_ok && c0 + 32 <= ep.N) {
+                    #pragma unroll
+                    for (int c = 0; c < 32; c += 4)
+                        st_cs4(drow + ch * 32 + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+                } else {
+                    #pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (c0 + c < ep.N) drow[ch * 32 + c] = v[c];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS));
+    }
+}
+
+// ------------------------------------------------------------ host side -------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_once;
+
+void init_encode() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+        cudaGetLastError();
+}
+
+bool make_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)d_pad, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d_pad * 2};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool tc_supported() {
+    std::call_once(g_once, init_encode);
+    if (!g_encode) return false;
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0;
+}
+
+cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_shift, float* D,
+                           int64_t ldD, int num_sms, cudaStream_t s) {
+    if (op.M == 0 || op.N == 0) return cudaSuccess;
+    std::call_once(g_once, init_encode);
+    if (!g_encode) return cudaErrorNotSupported;
+    CUtensorMap mqh, mql, mxh, mxl;
+    if (!make_map(&mqh, op.q_hi, op.M, op.d_pad, BM) || !make_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !make_map(&mxh, op.x_hi, op.N, op.d_pad, BN) || !make_map(&mxl, op.x_lo, op.N, op.d_pad, BN))
+        return cudaErrorInvalidValue;
+    TileMap tiles{ceil_div(op.M, BM), ceil_div(op.N, BN)};
+    const int64_t num_tiles = tiles.n_mb * tiles.n_nb;
+    const int grid = (int)(num_tiles < num_sms ? num_tiles : num_sms);
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD};
+    cudaError_t e = cudaFuncSetAttribute(dist_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    dist_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, op.d_pad / BK, tiles,
+                                                     num_tiles, ep);
+    return cudaGetLastError();
+}
+
+}  // namespace knn

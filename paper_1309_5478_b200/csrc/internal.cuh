@@ -1,0 +1,60 @@
+// internal.cuh — shared device helpers and launcher declarations of libknn.so.
+// Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace knn {
+
+constexpr int kMaxK = 1024;
+constexpr uint32_t kKeyMax = 0xFFFFFFFFu;  // larger than every key (used as "accept all")
+
+// Order-preserving map float -> uint32 for the total order of include/knn.h:
+// -0 == +0 (reading R6), every NaN -> +NaN, which sorts after +inf.
+__device__ __forceinline__ uint32_t ukey(float x) {
+    uint32_t b = __float_as_uint(x);
+    b = (b == 0x80000000u) ? 0u : b;                       // -0 -> +0
+    b = ((b & 0x7FFFFFFFu) > 0x7F800000u) ? 0x7FC00000u : b;  // NaN -> +NaN
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ukey_to_float(uint32_t u) {
+    uint32_t b = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    return __uint_as_float(b);
+}
+
+__host__ __device__ constexpr int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// The K padding of the split operands: one 128-byte swizzle atom of fp16 = 64 elements.
+constexpr int kSplitKAlign = 64;
+
+// ---------------------------------------------------------------- launchers --------
+// prep.cu: row norms (fp64 accumulate) + non-finite flag; optionally the scaled fp16
+// hi/lo split for the tensor-core GEMM (hi/lo may be null).
+cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
+                        float* rscale, __half* hi, __half* lo, int32_t* flag, cudaStream_t s);
+
+// gemm_simt.cu: FP32 FFMA distance GEMM with the fused epilogue.
+cudaError_t launch_dist_simt(const float* Q, const float* qn, int64_t M, const float* X,
+                             const float* xn, int64_t N, int32_t d, int32_t metric,
+                             int64_t self_shift, float* D, int64_t ldD, cudaStream_t s);
+
+// gemm_tc.cu: tcgen05 3-pass split-fp16 distance GEMM with the fused epilogue.
+struct TcOperands {
+    const __half* q_hi; const __half* q_lo; const float* qn; const float* q_rs; int64_t M;
+    const __half* x_hi; const __half* x_lo; const float* xn; const float* x_rs; int64_t N;
+    int32_t d_pad;
+};
+cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_shift, float* D,
+                           int64_t ldD, int num_sms, cudaStream_t s);
+bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
+
+// select.cu
+cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
+                          int64_t idx_offset, int32_t* out_idx, float* out_dist, cudaStream_t s);
+cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
+                         int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                         float* out_dist, cudaStream_t s);
+
+}  // namespace knn

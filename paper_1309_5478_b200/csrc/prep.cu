@@ -1,0 +1,91 @@
+// prep.cu — a-S2: row norms + input validation + split of the operands for the
+// FP32-accurate tensor-core GEMM.
+//
+// Paper: "we compute the vector norms of the vectors in X,Y using a combination of a
+// transform iterator and reduction_by_key ... The transform iterator generates the
+// square of individual elements and feeds the result into the reduction_by_key function
+// which in turn computes the square of the vector norms".  Here one warp
+// reduces one vector: squares accumulated in fp64 (reading R15), rounded to fp32.
+//
+// In the same pass (one HBM read of X) it writes, for the GEMM of gemm_tc.cu, each
+// vector scaled by a power of two s = 2^sh chosen so that max|x|*s lies in [2^14, 2^15),
+// split into two fp16 halves:  hi = fp16(x*s),  lo = fp16(x*s - hi).
+// x*s = hi + lo + r with |r| <= 2^-22 |x*s|, so hi.hi + hi.lo + lo.hi reproduces every
+// product to ~3*2^-22 relative, and rscale = 2^-sh undoes the scale
+// exactly in the epilogue.  Rows are zero-padded to d_pad (a multiple of 64) so TMA
+// boxes of 64 fp16 (= one 128-byte swizzle atom) tile K exactly.
+//
+// Validation (reading R8): flag = 1 if any x is NaN/inf or
+// ||x||^2 >= FLT_MAX/4 (which bounds every distance below FLT_MAX).
+#include "internal.cuh"
+
+#include <cfloat>
+
+namespace knn {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
+            float* __restrict__ sqn, float* __restrict__ rscale, __half* __restrict__ hi,
+            __half* __restrict__ lo, int32_t* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (row >= N) return;
+    const float* x = X + row * (int64_t)d;
+
+    double s = 0.0;
+    float amax = 0.0f;
+    bool finite = true;
+    for (int t = lane; t < d; t += 32) {
+        float v = __ldg(x + t);
+        finite &= isfinite(v);
+        amax = fmaxf(amax, fabsf(v));
+        s += (double)v * (double)v;
+    }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
+    }
+    finite = __all_sync(0xFFFFFFFFu, finite);
+    const float n2 = (float)s;
+    if (lane == 0) {
+        sqn[row] = n2;
+        if (flag && (!finite || !(s < (double)(FLT_MAX / 4)))) *flag = 1;
+    }
+    if (hi == nullptr) return;
+
+    // sh such that amax * 2^sh in [2^14, 2^15); frexp: amax = m 2^e, m in [0.5, 1).
+    int e = 0;
+    int sh = 0;
+    if (amax > 0.0f && finite) {
+        frexpf(amax, &e);
+        sh = 15 - e;
+    }
+    // 2^sh may exceed the fp32 range for subnormal-only rows: apply it in two exact steps.
+    const int sh1 = sh > 120 ? 120 : sh;
+    const float s1 = ldexpf(1.0f, sh1), s2 = ldexpf(1.0f, sh - sh1);
+    if (lane == 0) rscale[row] = ldexpf(1.0f, -sh);
+    __half* h = hi + row * (int64_t)d_pad;
+    __half* l = lo + row * (int64_t)d_pad;
+    for (int t = lane; t < d_pad; t += 32) {
+        float v = (t < d && finite) ? __ldg(x + t) * s1 * s2 : 0.0f;
+        __half vh = __float2half_rn(v);
+        h[t] = vh;
+        l[t] = __float2half_rn(v - __half2float(vh));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
+                        float* rscale, __half* hi, __half* lo, int32_t* flag, cudaStream_t s) {
+    if (N == 0) return cudaSuccess;
+    dim3 grid((unsigned)ceil_div(N, kWarpsPerBlock));
+    prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace knn

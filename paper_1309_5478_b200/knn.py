@@ -1,0 +1,252 @@
+"""Thin ctypes binding of libknn.so (include/knn.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module converts
+torch tensors / numpy arrays to pointers, passes the current CUDA stream, and turns
+status codes into exceptions.  A missing library is a hard error: there is no CPU path.
+Function names follow the C ABI (``knn_graph`` -> ``graph`` ...).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libknn.so")
+
+L2SQ, L2, COSINE, PEARSON = 0, 1, 2, 3
+NO_SELF = -(2 ** 63)  # KNN_NO_SELF
+MAX_K = 1024
+
+STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_NONFINITE",
+          4: "KNN_ERR_OOM", 5: "KNN_ERR_CUDA", 6: "KNN_ERR_NCCL", 7: "KNN_ERR_INTERNAL"}
+
+# every symbol include/knn.h declares
+SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
+           "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
+           "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count"]
+
+
+class KnnError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class KnnLibraryMissing(ImportError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+_ctx = {}
+
+
+def load_library():
+    """Load libknn.so (built by `make` / __graft_entry__.build()); raise if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise KnnLibraryMissing(
+                f"{LIB_PATH} not found: build it with `make` or __graft_entry__.build(); "
+                "there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        st = ctypes.c_int
+        sig = {
+            "knn_abi_version": (ctypes.c_int, []),
+            "knn_ctx_create": (st, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+            "knn_ctx_destroy": (st, [p]),
+            "knn_last_error": (ctypes.c_char_p, [p]),
+            "knn_launch_count": (i64, [p]),
+            "knn_graph": (st, [p, p, i64, i32, i32, i32, p, p, p]),
+            "knn_search": (st, [p, p, i64, p, i64, i32, i32, p, p, p]),
+            "knn_search_block": (st, [p, p, i64, p, i64, i32, i32, i32, i64, i64, p, p, p]),
+            "knn_search_block_host": (st, [p, p, i64, p, i64, i32, i32, i32, i64, i64, p, p, p]),
+            "knn_rownorms": (st, [p, p, i64, i32, p, p, p]),
+            "knn_distances": (st, [p, p, i64, p, i64, i32, i32, i64, p, i64, p]),
+            "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
+            "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(lib, name)
+            f.restype, f.argtypes = res, args
+        _lib = lib
+        return lib
+
+
+def context(device=None):
+    """The per-process knn_ctx of a CUDA device (created on first use)."""
+    import torch
+    lib = load_library()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    with _lock:
+        if dev not in _ctx:
+            h = ctypes.c_void_p()
+            rc = lib.knn_ctx_create(dev, ctypes.byref(h))
+            if rc != 0:
+                raise KnnError(rc, f"knn_ctx_create({dev}) failed")
+            _ctx[dev] = h
+        return _ctx[dev]
+
+
+def _check(rc, ctx):
+    if rc != 0:
+        raise KnnError(rc, load_library().knn_last_error(ctx).decode())
+
+
+def _dev_ptr(t, dtype, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _outputs(rows, k, device):
+    import torch
+    return (torch.empty((rows, k), dtype=torch.int32, device=device),
+            torch.empty((rows, k), dtype=torch.float32, device=device))
+
+
+def graph(X, k, metric=L2SQ, stream=None):
+    """k-NNG of X (N×d fp32 CUDA tensor): (idx N×k int32, dist N×k fp32), self excluded."""
+    import torch
+    N, d = X.shape
+    ctx = context(X.device.index)
+    idx, dist = _outputs(N, k, X.device)
+    rc = load_library().knn_graph(ctx, _dev_ptr(X, torch.float32, "X"), N, d, k, metric,
+                                  ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                  _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def search(Q, X, k, stream=None):
+    """For each query row of Q, its k nearest rows of X (squared Euclidean)."""
+    import torch
+    M, d = Q.shape
+    N = X.shape[0]
+    ctx = context(Q.device.index)
+    idx, dist = _outputs(M, k, Q.device)
+    rc = load_library().knn_search(ctx, _dev_ptr(Q, torch.float32, "Q"), M,
+                                   _dev_ptr(X, torch.float32, "X"), N, d, k,
+                                   ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                   _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def search_block(Q, X, k, metric=L2SQ, self_shift=NO_SELF, idx_offset=0, out=None, stream=None):
+    """knn_search_block: self pair j == i + self_shift excluded; idx_offset added."""
+    import torch
+    M, d = Q.shape
+    N = X.shape[0]
+    ctx = context(Q.device.index)
+    idx, dist = out if out is not None else _outputs(M, k, Q.device)
+    rc = load_library().knn_search_block(
+        ctx, _dev_ptr(Q, torch.float32, "Q"), M, _dev_ptr(X, torch.float32, "X"), N, d, k, metric,
+        self_shift, idx_offset, _dev_ptr(idx, torch.int32, "out_idx"),
+        _dev_ptr(dist, torch.float32, "out_dist"), _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def search_block_host(Q, X, k, metric=L2SQ, self_shift=NO_SELF, idx_offset=0, out=None,
+                      device=None, stream=None):
+    """knn_search_block_host: numpy (ideally pinned) host inputs and outputs; the
+    host<->device copies happen inside the call."""
+    Q = np.ascontiguousarray(Q, np.float32)
+    X = Q if X is Q else np.ascontiguousarray(X, np.float32)
+    M, d = Q.shape
+    N = X.shape[0]
+    ctx = context(device)
+    if out is None:
+        out = (np.empty((M, k), np.int32), np.empty((M, k), np.float32))
+    idx, dist = out
+    rc = load_library().knn_search_block_host(
+        ctx, Q.ctypes.data_as(ctypes.c_void_p), M, X.ctypes.data_as(ctypes.c_void_p), N, d, k,
+        metric, self_shift, idx_offset, idx.ctypes.data_as(ctypes.c_void_p),
+        dist.ctypes.data_as(ctypes.c_void_p), _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def rownorms(X, stream=None):
+    """(||x||^2 fp32 per row, non-finite flag int32[1])."""
+    import torch
+    N, d = X.shape
+    ctx = context(X.device.index)
+    out = torch.empty(N, dtype=torch.float32, device=X.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=X.device)
+    rc = load_library().knn_rownorms(ctx, _dev_ptr(X, torch.float32, "X"), N, d,
+                                     ctypes.c_void_p(out.data_ptr()),
+                                     ctypes.c_void_p(flag.data_ptr()), _stream(stream))
+    _check(rc, ctx)
+    return out, flag
+
+
+def distances(Q, X, metric=L2SQ, self_shift=NO_SELF, ldD=None, stream=None):
+    """The M×N distance matrix (M×ldD storage; returns the M×N view)."""
+    import torch
+    M, d = Q.shape
+    N = X.shape[0]
+    ldD = N if ldD is None else ldD
+    ctx = context(Q.device.index)
+    D = torch.empty((M, ldD), dtype=torch.float32, device=Q.device)
+    rc = load_library().knn_distances(ctx, _dev_ptr(Q, torch.float32, "Q"), M,
+                                      _dev_ptr(X, torch.float32, "X"), N, d, metric, self_shift,
+                                      ctypes.c_void_p(D.data_ptr()), ldD, _stream(stream))
+    _check(rc, ctx)
+    return D[:, :N]
+
+
+def select(D, k, N=None, stream=None):
+    """Per-row k smallest of D (M×ldD fp32 CUDA tensor; first N columns), sorted."""
+    import torch
+    M, ld = D.shape
+    N = ld if N is None else N
+    if not D.is_contiguous():
+        raise ValueError("D must be contiguous (use the N argument for a column prefix)")
+    ctx = context(D.device.index)
+    idx, dist = _outputs(M, k, D.device)
+    rc = load_library().knn_select(ctx, _dev_ptr(D, torch.float32, "D"), M, N, ld, k,
+                                   ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                   _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def merge(part_dist, part_idx, offsets, stream=None):
+    """Merge G partial lists ([G][M][k] CUDA tensors), list g's indices + offsets[g]."""
+    import torch
+    G, M, k = part_dist.shape
+    offs = np.ascontiguousarray(offsets, np.int64)
+    if offs.shape != (G,):
+        raise ValueError("offsets must have G entries")
+    ctx = context(part_dist.device.index)
+    idx, dist = _outputs(M, k, part_dist.device)
+    rc = load_library().knn_merge(ctx, _dev_ptr(part_dist, torch.float32, "part_dist"),
+                                  _dev_ptr(part_idx, torch.int32, "part_idx"), G, M, k,
+                                  offs.ctypes.data_as(ctypes.c_void_p),
+                                  ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                  _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def launch_count(device=None):
+    return int(load_library().knn_launch_count(context(device)))

@@ -1,0 +1,247 @@
+"""a-S2 / a-S3 / end-to-end parity of the CUDA path against the oracle.
+
+Tolerances come from BASELINE.json's north star: distances within 1e-5 of
+(||q||^2 + ||c||^2) of the fp64 value; neighbour lists checked with E2E-1/2 (oracle.checks)
+and, on integer-grid data where every correct implementation is exact, bit-identical
+to the oracle (E2E-3).  Sizes span several GEMM tiles (128×256) with ragged tails; the
+BASELINE configs run at full size on sampled rows."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import checks
+from paper_1309_5478_b200 import datagen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def knn():
+    from paper_1309_5478_b200 import knn as k
+    return k
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------ a-S2 -------------
+def test_rownorms():
+    X = datagen.points(3001, 77, "gauss", seed=1)
+    sqn, flag = knn().rownorms(cuda(X))
+    ref = oracle.sqnorms(X)
+    assert np.array_equal(sqn.cpu().numpy(), ref.astype(np.float32))  # fp64 acc, one rounding
+    assert int(flag.item()) == 0
+    G = datagen.points(500, 1024, "grid", seed=2)
+    assert np.array_equal(knn().rownorms(cuda(G))[0].cpu().numpy(), oracle.sqnorms(G).astype(np.float32))
+    X[17, 3] = np.nan
+    assert int(knn().rownorms(cuda(X))[1].item()) == 1
+
+
+# ------------------------------------------------------------------ a-S3 -------------
+@pytest.mark.parametrize("M,N,d,dist", [(300, 517, 32, "uniform"), (129, 1000, 1, "gauss"),
+                                        (257, 300, 3, "uniform"), (1000, 777, 100, "clusters"),
+                                        (256, 2048, 256, "gauss"), (130, 513, 1000, "uniform"),
+                                        (64, 4000, 128, "clusters")])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_distances_within_tolerance(M, N, d, dist, metric):
+    Q = datagen.points(M, d, dist, seed=M + d)
+    X = datagen.points(N, d, dist, seed=N + d + 1)
+    D = knn().distances(cuda(Q), cuda(X), metric=metric).cpu().numpy()
+    D64 = oracle.dist_rows(Q, X)
+    ratio, bad = checks.check_distances(D, D64, oracle.sqnorms(Q), oracle.sqnorms(X), metric)
+    assert bad == 0, f"max |err|/tol = {ratio}"
+
+
+def test_distances_integer_grid_exact():
+    # all norms/dots are integers < 2^24: the split GEMM and epilogue are exact
+    Q = datagen.points(200, 1024, "grid", seed=3)
+    X = datagen.points(333, 1024, "grid", seed=4)
+    D = knn().distances(cuda(Q), cuda(X)).cpu().numpy()
+    assert np.array_equal(D, oracle.dist_rows(Q, X).astype(np.float32))
+
+
+def test_distances_self_exclusion_and_ld():
+    X = datagen.points(400, 16, "uniform", seed=5)
+    D = knn().distances(cuda(X), cuda(X), self_shift=0, ldD=404).cpu().numpy()
+    assert np.all(np.isinf(np.diag(D)))
+    off = ~np.eye(400, dtype=bool)
+    ratio, bad = checks.check_distances(np.where(off, D, 0), np.where(off, oracle.dist_rows(X, X), 0),
+                                        oracle.sqnorms(X), oracle.sqnorms(X))
+    assert bad == 0
+    D2 = knn().distances(cuda(X[:100]), cuda(X), self_shift=50).cpu().numpy()
+    assert all(np.isinf(D2[i, i + 50]) for i in range(100))
+
+
+def test_distances_scale_extremes():
+    # per-vector power-of-two scaling keeps tiny and huge vectors FP32-accurate
+    g = np.random.Generator(np.random.Philox(6))
+    X = g.standard_normal((300, 64)).astype(np.float32)
+    X[:100] *= np.float32(1e-20)
+    X[100:200] *= np.float32(1e15)
+    D = knn().distances(cuda(X), cuda(X)).cpu().numpy()
+    n = oracle.sqnorms(X)
+    ratio, bad = checks.check_distances(D, oracle.dist_rows(X, X), n, n)
+    assert bad == 0, ratio
+
+
+# ------------------------------------------------------------------ end to end -------
+def run_graph(X, k, metric=0):
+    i, d = knn().graph(cuda(X), k, metric=metric)
+    return i.cpu().numpy(), d.cpu().numpy()
+
+
+def e2e_check(Q, X, gi, gd, k, rows, graph, metric=0, min_pinned=0.0):
+    D64 = oracle.dist_rows(Q, X, rows=rows)
+    res = checks.check_rows(gi[rows], gd[rows], D64, oracle.sqnorms(Q[rows]), oracle.sqnorms(X),
+                            rows, k, metric=metric, graph=graph)
+    assert res["failures"] == [], res["failures"][:5]
+    assert res["n_pinned"] >= min_pinned * len(rows)
+    return res
+
+
+def test_c1_graph_all_rows():
+    cfg = datagen.CONFIGS["C1"]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, np.arange(cfg.N), True, min_pinned=0.9)
+
+
+def test_c1_graph_l2_metric():
+    cfg = datagen.CONFIGS["C1"]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k, metric=1)
+    e2e_check(X, X, gi, gd, cfg.k, np.arange(0, cfg.N, 3), True, metric=1)
+
+
+@pytest.mark.parametrize("N,d,k", [(2000, 64, 50), (5000, 1024, 1024), (3333, 7, 100)])
+def test_integer_grid_graph_exact(N, d, k):
+    # E2E-3: the full lists (indices, order, distances) equal the oracle's R32 exactly
+    X = datagen.points(N, d, "grid", seed=N + d)
+    gi, gd = run_graph(X, k)
+    rows = np.arange(0, N, max(1, N // 300))
+    ref = oracle.knn(X, X, k, rows=rows, graph=True)
+    assert np.array_equal(gi[rows], ref["idx32"])
+    assert np.array_equal(gd[rows], ref["dist32"])
+
+
+def _sample_rows(M, n, seed):
+    g = np.random.Generator(np.random.Philox(seed))
+    rows = np.unique(np.concatenate([[0, 1, M - 2, M - 1], g.integers(0, M, n)]))
+    return rows
+
+
+def test_c2_graph_full_size():
+    cfg = datagen.CONFIGS["C2"]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 200, 1), True)
+
+
+def test_c3_search_full_size():
+    cfg = datagen.CONFIGS["C3"]
+    Q, X = datagen.config_inputs(cfg)
+    i, d = knn().search(cuda(Q), cuda(X), cfg.k)
+    e2e_check(Q, X, i.cpu().numpy(), d.cpu().numpy(), cfg.k, _sample_rows(cfg.M, 40, 2), False,
+              min_pinned=0.5)
+
+
+def test_headline_graph_full_size():
+    cfg = datagen.HEADLINE
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 40, 3), True, min_pinned=0.5)
+
+
+def test_c4_graph_large_k_full_size():
+    cfg = datagen.CONFIGS["C4"]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 12, 4), True)
+
+
+def test_c5_graph_single_gpu_full_size():
+    cfg = datagen.CONFIGS["C5"]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 12, 5), True)
+
+
+def test_corpus_shards_plus_merge_equal_graph():
+    # Par-2 on one GPU: column shards with global self exclusion and idx offsets, then
+    # the k-way merge, must equal the unsharded graph bit-for-bit.
+    X = datagen.points(5000, 48, "gauss", seed=7)
+    k = 20
+    ref_i, ref_d = run_graph(X, k)
+    Xt = cuda(X)
+    bounds = [0, 1250, 2500, 3750, 5000]
+    parts = [knn().search_block(Xt, Xt[a:b].contiguous(), k, self_shift=-a, idx_offset=a)
+             for a, b in zip(bounds[:-1], bounds[1:])]
+    pi = torch.stack([p[0] for p in parts])
+    pd = torch.stack([p[1] for p in parts])
+    i, d = knn().merge(pd, pi, np.zeros(4, np.int64))
+    assert np.array_equal(i.cpu().numpy(), ref_i)
+    assert np.array_equal(d.cpu().numpy(), ref_d)
+
+
+def test_query_shards_equal_graph():
+    # Par-1 on one GPU: row blocks with self_shift = row offset
+    X = datagen.points(3000, 40, "uniform", seed=8)
+    k = 10
+    ref_i, ref_d = run_graph(X, k)
+    Xt = cuda(X)
+    got = [knn().search_block(Xt[a:a + 1000].contiguous(), Xt, k, self_shift=a)
+           for a in (0, 1000, 2000)]
+    assert np.array_equal(torch.cat([g[0] for g in got]).cpu().numpy(), ref_i)
+    assert np.array_equal(torch.cat([g[1] for g in got]).cpu().numpy(), ref_d)
+
+
+def test_host_entry_point_equals_device():
+    X = datagen.points(2500, 32, "clusters", seed=9)
+    k = 12
+    ref_i, ref_d = run_graph(X, k)
+    hi, hd = knn().search_block_host(X, X, k, self_shift=0)
+    assert np.array_equal(hi, ref_i) and np.array_equal(hd, ref_d)
+
+
+def test_deterministic_and_small_row_blocks(monkeypatch):
+    X = datagen.points(4000, 64, "uniform", seed=10)
+    a = run_graph(X, 16)
+    b = run_graph(X, 16)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_errors():
+    k = knn()
+    X = cuda(datagen.points(10, 4, "uniform", seed=11))
+    with pytest.raises(k.KnnError) as e:
+        k.graph(X, 10)
+    assert e.value.status == 1
+    with pytest.raises(k.KnnError) as e:
+        k.graph(X, 3, metric=2)
+    assert e.value.status == 2
+    big = cuda(datagen.points(2000, 4, "uniform", seed=12))
+    with pytest.raises(k.KnnError) as e:
+        k.graph(big, 1025)
+    assert e.value.status == 2
+    bad = datagen.points(10, 4, "uniform", seed=13)
+    bad[3, 1] = np.inf
+    with pytest.raises(k.KnnError) as e:
+        k.graph(cuda(bad), 3)
+    assert e.value.status == 3
+
+
+def test_simt_cross_check_path():
+    # The FFMA path (KNN_GEMM=simt) in a fresh process must pass the same tolerance.
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "from oracle import checks\n"
+        "from paper_1309_5478_b200 import knn, datagen\n"
+        "Q = datagen.points(300, 100, 'gauss', seed=1); X = datagen.points(700, 100, 'gauss', seed=2)\n"
+        "D = knn.distances(torch.from_numpy(Q).cuda(), torch.from_numpy(X).cuda()).cpu().numpy()\n"
+        "r, bad = checks.check_distances(D, oracle.dist_rows(Q, X), oracle.sqnorms(Q), oracle.sqnorms(X))\n"
+        "assert bad == 0, r\n")
+    env = dict(os.environ, KNN_GEMM="simt")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)

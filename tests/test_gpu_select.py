@@ -1,0 +1,143 @@
+"""a-S4 / a-S6 parity: the CUDA select and merge vs the oracle, bit-exact.
+
+The select runs on fp32 matrices the oracle (or the seeded generators) produced and must
+return exactly the oracle's (index, value) lists: sorted by (value, index), -0 == +0,
+NaN after +inf (include/knn.h).  Shapes span several chunks and ragged tails."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1309_5478_b200 import datagen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def knn():
+    from paper_1309_5478_b200 import knn as k
+    return k
+
+
+def gpu_select(D, k, ld=None):
+    M, N = D.shape
+    if ld is None:
+        Dt = torch.from_numpy(np.ascontiguousarray(D)).cuda()
+        return [t.cpu().numpy() for t in knn().select(Dt, k)]
+    buf = np.zeros((M, ld), np.float32)
+    buf[:, :N] = D
+    Dt = torch.from_numpy(buf).cuda()
+    return [t.cpu().numpy() for t in knn().select(Dt, k, N=N)]
+
+
+def assert_same(got, ref):
+    gi, gd = got
+    ri, rd = ref
+    assert np.array_equal(gi, ri), f"first index mismatch at {np.argwhere(gi != ri)[:3]}"
+    assert np.array_equal(gd.view(np.uint32), rd.view(np.uint32))
+
+
+@pytest.mark.parametrize("N", [1, 31, 33, 1000, 2048, 2049, 4097, 16385])
+@pytest.mark.parametrize("k", [1, 8, 31, 32, 33, 255, 256, 1000, 1024])
+def test_select_uniform(N, k):
+    if k > N:
+        pytest.skip("k > N")
+    D = datagen.keys(24, N, "uniform", seed=N * 7 + k)
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("kind", ["dup256", "descending", "ascending", "equal"])
+@pytest.mark.parametrize("k", [1, 32, 33, 1024])
+def test_select_adversarial(kind, k):
+    D = datagen.keys(8, 9000, kind, seed=11)
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+def test_select_special_values():
+    g = np.random.Generator(np.random.Philox(3))
+    D = g.standard_normal((16, 3000)).astype(np.float32)
+    D[:, ::7] = 0.0
+    D[:, 3::7] = -0.0
+    D[:, 5::11] = np.inf
+    D[:, 6::13] = -np.inf
+    D[:, 2::17] = np.nan
+    D[:, 9::19] = -np.nan
+    for k in (1, 40, 1024):
+        assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+    # a row with fewer finite values than k
+    E = np.full((3, 500), np.inf, np.float32)
+    E[:, :10] = np.arange(10, dtype=np.float32)
+    assert_same(gpu_select(E, 64), oracle.select_f32(E, 64))
+
+
+@pytest.mark.parametrize("ld_extra", [1, 3])
+def test_select_unaligned_rows(ld_extra):
+    D = datagen.keys(10, 5001, "uniform", seed=5)
+    assert_same(gpu_select(D, 50, ld=5001 + ld_extra), oracle.select_f32(D, 50))
+
+
+def test_select_full_row_and_k_equals_n():
+    D = datagen.keys(5, 700, "dup256", seed=6)
+    assert_same(gpu_select(D, 700), oracle.select_f32(D, 700))
+
+
+def test_select_on_oracle_distance_matrix():
+    # north star: "The GPU select, run on the oracle's own distance matrix, must return
+    # bit-identical indices" — D32 = fp32(D64) rows of a clustered k-NNG (C2 shape family).
+    X = datagen.points(6000, 64, "clusters", seed=datagen.BASE_SEED + 2)
+    rows = np.arange(0, 6000, 97)
+    D32 = oracle.dist_rows(X, X, rows=rows).astype(np.float32)
+    for r, i in enumerate(rows):
+        D32[r, i] = np.inf  # graph mode: self excluded by position
+    ref = oracle.knn(X, X, 16, rows=rows, graph=True)
+    got = gpu_select(D32, 16)
+    assert np.array_equal(got[0], ref["idx32"])
+    assert np.array_equal(got[1], ref["dist32"])
+
+
+def test_select_many_rows_full_size():
+    # the select at a bench-sized row length (65536) on a sample of rows
+    D = datagen.keys(64, 65536, "uniform", seed=9)
+    assert_same(gpu_select(D, 32), oracle.select_f32(D, 32))
+
+
+def test_select_deterministic():
+    D = datagen.keys(32, 20000, "dup256", seed=10)
+    a, b = gpu_select(D, 100), gpu_select(D, 100)
+    assert_same(a, b)
+
+
+# ------------------------------------------------------------------ merge -----------
+def _sorted_lists(G, M, k, seed, dup=False):
+    g = np.random.Generator(np.random.Philox(seed))
+    vals = (g.integers(0, 50, size=(G, M, k)) / 8.0 if dup else g.random((G, M, k))).astype(np.float32)
+    idx = g.integers(0, 10000, size=(G, M, k)).astype(np.int32)
+    for a in range(G):
+        for r in range(M):
+            o = np.lexsort((idx[a, r], vals[a, r]))
+            vals[a, r], idx[a, r] = vals[a, r][o], idx[a, r][o]
+    return vals, idx
+
+
+@pytest.mark.parametrize("G,k", [(1, 1), (2, 32), (8, 32), (8, 1024), (3, 1000), (64, 16)])
+@pytest.mark.parametrize("dup", [False, True])
+def test_merge_parity(G, k, dup):
+    M = 40
+    vals, idx = _sorted_lists(G, M, k, seed=G * 1000 + k, dup=dup)
+    offsets = np.arange(G, dtype=np.int64) * 10000
+    ref = oracle.merge(vals, idx, offsets)
+    got = knn().merge(torch.from_numpy(vals).cuda(), torch.from_numpy(idx).cuda(), offsets)
+    assert_same([t.cpu().numpy() for t in got], ref)
+
+
+def test_merge_of_column_shards_equals_unsharded_select():
+    D = datagen.keys(50, 10000, "dup256", seed=12)
+    k = 64
+    bounds = [0, 2500, 5000, 7500, 10000]
+    pd, pi = [], []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        i, d = gpu_select(D[:, a:b], k)
+        pd.append(d)
+        pi.append(i)
+    got = knn().merge(torch.from_numpy(np.stack(pd)).cuda(), torch.from_numpy(np.stack(pi)).cuda(),
+                      bounds[:-1])
+    assert_same([t.cpu().numpy() for t in got], oracle.select_f32(D, k))
