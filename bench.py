@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Headline benchmark (BASELINE.json "metric"): k-NNG points/s at N=65536, d=256, k=32.
+
+A step is one pass of the whole hot path over the workload: row norms + split (a-S2),
+distance GEMM (a-S3) and per-row select (a-S4) for all N query rows; under torchrun the
+query rows are sharded over the ranks (Par-1: rank 0's points are broadcast, results
+all-gathered, both inside the step).  Inputs are resident in HBM when a step starts;
+L2 is flushed (256 MiB write, untimed) before every timed step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config H|C1..C5]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every field)."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-NNG points/sec at N=65536,d=256,k=32 (1/2/4/8 B200); select GB/s; GEMM tensor util"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="H", help="H (headline) or C1..C5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU seconds of the oracle cpu_baseline sample")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback"}
+
+
+def get_config(name):
+    from paper_1309_5478_b200 import datagen
+    return datagen.HEADLINE if name == "H" else datagen.CONFIGS[name]
+
+
+def workload_name(cfg):
+    mode = "k-NNG" if cfg.mode == "graph" else f"k-NN search M={cfg.M}"
+    return f"{mode} N={cfg.N} d={cfg.d} k={cfg.k} {cfg.dist} fp32 (squared L2)"
+
+
+# ------------------------------------------------------------------ clocks ----------
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons, n_load = [], None, set(), 0
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                clk, mx, util = float(parts[0]), float(parts[1]), float(parts[2])
+            except ValueError:
+                continue
+            smax = mx
+            if util >= 50:
+                n_load += 1
+                sm.append(clk)
+                for nm, v in zip(names, parts[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples_under_load": n_load}
+
+
+# ------------------------------------------------------------------ CPU oracle ------
+def oracle_rows_per_s(X, k, graph, target_s, threads):
+    """Time the oracle (as it stands) on a bounded sample of query rows."""
+    import numpy as np
+    import oracle
+    N = X.shape[0]
+    g = np.random.Generator(np.random.Philox(4242))
+    rows = g.choice(N, size=min(N, threads), replace=False)
+    t0 = time.perf_counter()
+    oracle.knn(X, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
+    t1 = time.perf_counter() - t0
+    R = int(min(N, max(len(rows), len(rows) * target_s / max(t1, 1e-3))))
+    R = max(threads, (R // threads) * threads)
+    rows = g.choice(N, size=min(N, R), replace=False)
+    t0 = time.perf_counter()
+    oracle.knn(X, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
+    dt = time.perf_counter() - t0
+    return len(rows) / dt, len(rows), dt
+
+
+def run_reference(args):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    from paper_1309_5478_b200 import datagen
+    cfg = get_config(args.config)
+    Q, X = datagen.config_inputs(cfg)
+    threads = oracle.default_threads()
+    graph = cfg.mode == "graph"
+    # one step = a bounded sample of the workload's query rows (same rows every step)
+    g = np.random.Generator(np.random.Philox(4243))
+    per_step = max(threads, 2 * threads)
+    rows = g.choice(cfg.M, size=min(cfg.M, per_step), replace=False)
+
+    def step():
+        oracle.knn(Q, X, cfg.k, rows=rows, graph=graph, threads=threads, want_r32=False)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = len(rows) * args.steps / dt
+    sample = (f"{len(rows)} seeded query rows of the {cfg.M}-row workload per step "
+              f"(fp64 direct distances to all {cfg.N} points + full std::sort per row)")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "N": cfg.N, "d": cfg.d, "k": cfg.k,
+                   "sample_rows_per_step": len(rows)},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ ours ------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1309_5478_b200 import datagen, knn, sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = get_config(args.config)
+    if cfg.mode != "graph":
+        raise SystemExit("bench.py times the k-NNG workloads (H, C1, C2, C4, C5)")
+    N, d, k = cfg.N, cfg.d, cfg.k
+    X_host = datagen.points(N, d, cfg.dist, cfg.seed) if rank == 0 else None
+    X = torch.from_numpy(X_host).to(dev) if rank == 0 else torch.empty((N, d), device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+
+    def step():
+        return sharded.graph_query_sharded(X, k, broadcast=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    assert knn.gemm_path() == 0 or os.environ.get("KNN_GEMM") == "simt", "tensor-core path expected"
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    knn.profile_enable(True)
+    launches0 = knn.launch_count()
+    stream = torch.cuda.current_stream()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()  # evict L2 (untimed)
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        barrier()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    launches = knn.launch_count() - launches0
+    prof = {kname: knn.profile_read(kname) for kname in ("prep", "gemm", "select")}
+    knn.profile_enable(False)
+    clocks = sampler.stop()
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = N / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (per-launch averages over the timed region)
+    peaks = load_peaks()
+    R_local = sharded.block_range(N, world, rank)[1] - sharded.block_range(N, world, rank)[0]
+    d_pad = -(-d // 64) * 64
+    g_ms, g_n = prof["gemm"]
+    s_ms, s_n = prof["select"]
+    p_ms, p_n = prof["prep"]
+    gemm_avg = g_ms / max(g_n, 1)
+    sel_avg = s_ms / max(s_n, 1)
+    gemm_launches_per_step = max(g_n // args.steps, 1)
+    rows_per_gemm = R_local / gemm_launches_per_step
+    # tensor work the split GEMM must issue: 3 fp16 products per multiply-add
+    tensor_flop = 3 * 2.0 * rows_per_gemm * N * d_pad
+    useful_flop = 2.0 * rows_per_gemm * N * d
+    sel_bytes = rows_per_gemm * (N * 4.0 + k * 8.0)  # read the rows + write k (idx, dist)
+    gemm_roof = {"kernel": "dist_tc_kernel (a-S3)", "bound": "tensor",
+                 "achieved": tensor_flop / (gemm_avg * 1e-3) / 1e12,
+                 "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                 "peak_kind": f"fp16 dense = bf16 {peaks['source']} sustained",
+                 "useful_tflops": useful_flop / (gemm_avg * 1e-3) / 1e12,
+                 "avg_launch_ms": gemm_avg, "traffic": None}
+    gemm_roof["frac"] = gemm_roof["achieved"] / gemm_roof["peak"]
+    sel_roof = {"kernel": "select_rows_kernel (a-S4)", "bound": "hbm",
+                "achieved": sel_bytes / (sel_avg * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "avg_launch_ms": sel_avg, "traffic": None}
+    sel_roof["frac"] = sel_roof["achieved"] / sel_roof["peak"]
+    dominant, other = (gemm_roof, sel_roof) if g_ms >= s_ms else (sel_roof, gemm_roof)
+    roofline = dict(dominant)
+    roofline["other"] = other
+    roofline["step_share"] = {"gemm": g_ms / total_ms, "select": s_ms / total_ms,
+                              "prep": p_ms / total_ms}
+
+    # ---- e2e: the public host-buffer API, H2D of the inputs and D2H of the results inside
+    e2e = None
+    if not args.no_e2e:
+        lo, hi = sharded.block_range(N, world, rank)
+        Xh = torch.empty((N, d), dtype=torch.float32, pin_memory=True)
+        if rank == 0:
+            Xh.copy_(torch.from_numpy(X_host))
+        else:
+            Xh.copy_(X.cpu())
+        Xn = Xh.numpy()
+        oi = torch.empty((hi - lo, k), dtype=torch.int32, pin_memory=True).numpy()
+        od = torch.empty((hi - lo, k), dtype=torch.float32, pin_memory=True).numpy()
+        Qn = Xn[lo:hi]
+
+        def e2e_step():
+            knn.search_block_host(Qn, Xn, k, self_shift=lo, out=(oi, od))
+
+        for _ in range(2):
+            e2e_step()
+        e_ms = 0.0
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            e_ms += (time.perf_counter() - t0) * 1e3
+            barrier()
+        e_ms /= max(3, args.steps // 2)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": N / (float(te.item()) / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": int(N * d * 4), "d2h_bytes_per_step": int((hi - lo) * k * 8),
+               "api": "knn_search_block_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        threads = oracle.default_threads()
+        rps, R, dt = oracle_rows_per_s(X_host, k, True, args.cpu_seconds, threads)
+        cpu = {"value": rps, "unit": "points/s", "cores": threads, "kind": "oracle",
+               "sample": f"{R} seeded query rows of the N={N} k-NNG ({dt:.1f} s; fp64 direct "
+                         f"distances + full std::sort per row)"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "N": N, "d": d, "k": k,
+                       "sharding": "query rows (Par-1): bcast X, per-rank rows, all-gather",
+                       "gemm": "tcgen05 3-pass split-fp16 (FP32-accurate), fp32 accumulate",
+                       "l2": "flushed before every timed step (256 MiB write, untimed)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "select_gbs": sel_roof["achieved"],
+            "gemm_useful_tflops": gemm_roof["useful_tflops"],
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

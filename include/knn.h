@@ -142,8 +142,23 @@ knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_
                      int64_t M, int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                      float* out_dist, void* stream);
 
-/* Number of kernel launches this ctx has issued so far (for benchmarks). */
+/* ---------------------------------------------------------------- introspection ----
+ * Number of kernel launches this ctx has issued so far (for benchmarks). */
 int64_t knn_launch_count(knn_ctx_t ctx);
+
+/* Which distance-GEMM plan this ctx uses: 0 = tcgen05 split-fp16 tensor-core GEMM
+ * (gemm_tc.cu), 1 = SIMT FP32 FFMA (gemm_simt.cu; selected by env KNN_GEMM=simt at
+ * ctx creation, or when the device is not sm_100). */
+int knn_gemm_path(knn_ctx_t ctx);
+
+/* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by
+ * CUDA events recorded on the launch stream.  knn_profile_enable(ctx, 1) also resets
+ * the counters.  knn_profile_read waits for the recorded events and returns the summed
+ * duration (ms) and the launch count of one kernel class. */
+typedef enum { KNN_KERNEL_PREP = 0, KNN_KERNEL_GEMM = 1, KNN_KERNEL_SELECT = 2,
+               KNN_KERNEL_MERGE = 3 } knn_kernel;
+knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on);
+knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 struct knn_ctx {
     int device = 0;
@@ -24,6 +26,13 @@ struct knn_ctx {
     int32_t* flag_host = nullptr;  // pinned
     int64_t launches = 0;
     size_t d_budget = (size_t)4 << 30;  // bytes of distance-matrix block per launch pair
+    // per-kernel event timing (knn_profile_*)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> ev_pool;
+    struct Pending { int kind; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    double prof_ms[4] = {0, 0, 0, 0};
+    int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -92,6 +101,52 @@ struct Carve {
     }
 };
 
+cudaEvent_t take_event(knn_ctx* ctx) {
+    if (!ctx->ev_pool.empty()) {
+        cudaEvent_t e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Bracket one launch with events when profiling; usage:
+//   Timed t(ctx, KIND, s); launch...; t.done();
+struct Timed {
+    knn_ctx* ctx; int kind; cudaStream_t s; cudaEvent_t a = nullptr;
+    Timed(knn_ctx* c, int k, cudaStream_t st) : ctx(c), kind(k), s(st) {
+        if (ctx->prof_on) {
+            a = take_event(ctx);
+            cudaEventRecord(a, s);
+        }
+    }
+    void done() {
+        ctx->launches++;
+        if (!a) return;
+        cudaEvent_t b = take_event(ctx);
+        cudaEventRecord(b, s);
+        ctx->pending.push_back({kind, a, b});
+        a = nullptr;
+    }
+};
+
+void drain_profile(knn_ctx* ctx) {
+    for (auto& p : ctx->pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.b);
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            ctx->prof_ms[p.kind] += ms;
+            ctx->prof_n[p.kind] += 1;
+        }
+        cudaGetLastError();
+        ctx->ev_pool.push_back(p.a);
+        ctx->ev_pool.push_back(p.b);
+    }
+    ctx->pending.clear();
+}
+
 knn_status set_device(knn_ctx* ctx) {
     KNN_CUDA(cudaSetDevice(ctx->device));
     return KNN_OK;
@@ -149,15 +204,20 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     layout(carve, pq, px, D, flag);
 
     KNN_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
-    KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
-    ctx->launches++;
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+        t.done();
+    }
     if (!same) {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
         KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
-        ctx->launches++;
+        t.done();
     }
     for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
         const int64_t R = (M - r0) < rows_blk ? (M - r0) : rows_blk;
         const int64_t shift = self_shift == KNN_NO_SELF ? KNN_NO_SELF : self_shift + r0;
+        Timed tg(ctx, KNN_KERNEL_GEMM, s);
         if (tc) {
             knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
                                px.hi, px.lo, px.sqn, px.rs, N, d_pad};
@@ -166,10 +226,11 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             KNN_CUDA(knn::launch_dist_simt(Q + r0 * d, pq.sqn + r0, R, X, px.sqn, N, d, metric,
                                            shift, D, ldD, s));
         }
-        ctx->launches++;
+        tg.done();
+        Timed ts(ctx, KNN_KERNEL_SELECT, s);
         KNN_CUDA(knn::launch_select(D, R, N, ldD, k, idx_offset, out_idx + r0 * k,
                                     out_dist + r0 * k, s));
-        ctx->launches++;
+        ts.done();
     }
     return KNN_OK;
 }
@@ -240,6 +301,8 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
     if (!ctx) return KNN_ERR_ARG;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
+    drain_profile(ctx);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->io) cudaFree(ctx->io);
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
@@ -250,6 +313,32 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
 const char* knn_last_error(knn_ctx_t ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+int knn_gemm_path(knn_ctx_t ctx) {
+    if (!ctx) return -1;
+    return (ctx->gemm_mode == 0 && ctx->tc_ok) ? 0 : 1;
+}
+
+knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on) {
+    if (!ctx) return KNN_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    drain_profile(ctx);
+    for (int i = 0; i < 4; ++i) {
+        ctx->prof_ms[i] = 0;
+        ctx->prof_n[i] = 0;
+    }
+    ctx->prof_on = on != 0;
+    return KNN_OK;
+}
+
+knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches) {
+    if (!ctx || kernel < 0 || kernel > 3 || !total_ms || !launches) return KNN_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    drain_profile(ctx);
+    *total_ms = ctx->prof_ms[kernel];
+    *launches = ctx->prof_n[kernel];
+    return KNN_OK;
+}
 
 knn_status knn_search_block(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,
                             int32_t d, int32_t k, int32_t metric, int64_t self_shift,
@@ -320,9 +409,10 @@ knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, flo
     if (N > 0 && (!X || !out_sqn)) return fail(ctx, KNN_ERR_ARG, "null pointer");
     if (N == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
+    Timed t(ctx, KNN_KERNEL_PREP, static_cast<cudaStream_t>(stream));
     KNN_CUDA(knn::launch_prep(X, N, d, 0, out_sqn, nullptr, nullptr, nullptr, out_flag,
                               static_cast<cudaStream_t>(stream)));
-    ctx->launches++;
+    t.done();
     return KNN_OK;
 }
 
@@ -359,19 +449,24 @@ knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* 
     KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve, pq, px, flag);
-    KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
-    ctx->launches++;
-    if (!same) {
-        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
-        ctx->launches++;
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+        t.done();
     }
+    if (!same) {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
+        t.done();
+    }
+    Timed tg(ctx, KNN_KERNEL_GEMM, s);
     if (tc) {
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
         KNN_CUDA(knn::launch_dist_tc(op, metric, self_shift, D, ldD, ctx->num_sms, s));
     } else {
         KNN_CUDA(knn::launch_dist_simt(Q, pq.sqn, M, X, px.sqn, N, d, metric, self_shift, D, ldD, s));
     }
-    ctx->launches++;
+    tg.done();
     return KNN_OK;
 }
 
@@ -385,9 +480,10 @@ knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64
     if (M > 0 && (!D || !out_idx || !out_dist)) return fail(ctx, KNN_ERR_ARG, "null pointer");
     if (M == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
+    Timed t(ctx, KNN_KERNEL_SELECT, static_cast<cudaStream_t>(stream));
     KNN_CUDA(knn::launch_select(D, M, N, ldD, k, 0, out_idx, out_dist,
                                 static_cast<cudaStream_t>(stream)));
-    ctx->launches++;
+    t.done();
     return KNN_OK;
 }
 
@@ -406,9 +502,10 @@ knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_
             return fail(ctx, KNN_ERR_ARG, "offset %d out of range", g);
     if (M == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
+    Timed t(ctx, KNN_KERNEL_MERGE, static_cast<cudaStream_t>(stream));
     KNN_CUDA(knn::launch_merge(part_dist, part_idx, G, M, k, offsets_host, out_idx, out_dist,
                                static_cast<cudaStream_t>(stream)));
-    ctx->launches++;
+    t.done();
     return KNN_OK;
 }
 

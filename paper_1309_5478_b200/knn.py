@@ -26,7 +26,9 @@ STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_N
 # every symbol include/knn.h declares
 SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
-           "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count"]
+           "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
+           "knn_gemm_path", "knn_profile_enable", "knn_profile_read"]
+KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3}
 
 
 class KnnError(RuntimeError):
@@ -71,6 +73,10 @@ def load_library():
             "knn_distances": (st, [p, p, i64, p, i64, i32, i32, i64, p, i64, p]),
             "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
+            "knn_gemm_path": (ctypes.c_int, [p]),
+            "knn_profile_enable": (st, [p, i32]),
+            "knn_profile_read": (st, [p, i32, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_int64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -250,3 +256,22 @@ def merge(part_dist, part_idx, offsets, stream=None):
 
 def launch_count(device=None):
     return int(load_library().knn_launch_count(context(device)))
+
+
+def gemm_path(device=None):
+    """0 = tcgen05 split-fp16 tensor-core GEMM, 1 = SIMT FFMA."""
+    return int(load_library().knn_gemm_path(context(device)))
+
+
+def profile_enable(on=True, device=None):
+    ctx = context(device)
+    _check(load_library().knn_profile_enable(ctx, 1 if on else 0), ctx)
+
+
+def profile_read(kernel, device=None):
+    """(summed device ms, launches) of one kernel class since profile_enable."""
+    ctx = context(device)
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    _check(load_library().knn_profile_read(ctx, KERNELS[kernel], ctypes.byref(ms),
+                                           ctypes.byref(n)), ctx)
+    return ms.value, n.value

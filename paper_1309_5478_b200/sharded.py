@@ -1,0 +1,145 @@
+"""Multi-GPU drivers: one process per GPU, torch.distributed (NCCL) for the plumbing.
+
+Two shardings of the brute-force k-NN (the paper is single-GPU and names
+"batch execution with data partitioning ... merging of results" as future work,
+PAPER.md:102):
+
+* ``graph_query_sharded`` (Par-1): query rows are independent.  Rank 0's dataset is
+  broadcast once over NVLink, each rank runs the whole hot path (norms -> GEMM ->
+  select) on its contiguous block of ceil(N/G) query rows against all N points, and the
+  M×k results are all-gathered.  The only exchanges are the input broadcast and the
+  output gather; there is no collective inside the hot path.
+* ``graph_corpus_sharded`` (Par-2): corpus columns are split in G contiguous blocks;
+  every rank computes partial top-k lists of ALL rows against its block (global self
+  exclusion and global indices via knn_search_block's self_shift / idx_offset), an
+  all-to-all hands each rank the G partial lists of its own row block, the k-way merge
+  kernel (knn_merge) produces its final rows, and an all-gather assembles the graph.
+  Equal to the unsharded graph bit-for-bit: (distance, index) is a total order and the
+  shards are contiguous index ranges.
+
+The per-rank compute is injected (``compute`` / ``merge``) so the same orchestration is
+exercised by the world-size-2 gloo tests on CPU with oracle stand-ins; by default it is
+the CUDA library (there is no CPU fallback in the product path).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def block_range(n: int, parts: int, r: int):
+    """Contiguous block r of ceil(n/parts)-sized blocks of range(n): [lo, hi)."""
+    per = -(-n // parts)
+    lo = min(n, r * per)
+    return lo, min(n, lo + per)
+
+
+def _default_compute(Q, X, k, metric, self_shift, idx_offset):
+    from . import knn
+    return knn.search_block(Q, X, k, metric=metric, self_shift=self_shift, idx_offset=idx_offset)
+
+
+def _default_merge(part_dist, part_idx, offsets):
+    from . import knn
+    return knn.merge(part_dist, part_idx, offsets)
+
+
+def _world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def broadcast_points(X, group=None, src=0):
+    """Broadcast rank `src`'s N×d point set (in place on every rank)."""
+    dist.broadcast(X, src=src, group=group)
+    return X
+
+
+def graph_query_sharded(X, k, metric=0, group=None, compute=None, broadcast=True):
+    """k-NNG of X with the query rows sharded over the ranks of `group` (Par-1).
+
+    X: N×d fp32 tensor on this rank's device, valid on rank 0 (broadcast here unless
+    broadcast=False).  Returns the full (idx N×k int32, dist N×k fp32) on every rank."""
+    compute = compute or _default_compute
+    G, r = _world(group)
+    N = X.shape[0]
+    if broadcast and G > 1:
+        broadcast_points(X, group)
+    per = -(-N // G)
+    lo, hi = block_range(N, G, r)
+    out_i = torch.zeros((per, k), dtype=torch.int32, device=X.device)
+    out_d = torch.full((per, k), float("inf"), dtype=torch.float32, device=X.device)
+    if hi > lo:
+        i, d = compute(X[lo:hi], X, k, metric, lo, 0)  # self pair: column lo + i
+        out_i[: hi - lo] = i
+        out_d[: hi - lo] = d
+    if G == 1:
+        return out_i[:N], out_d[:N]
+    all_i = torch.empty((G * per, k), dtype=torch.int32, device=X.device)
+    all_d = torch.empty((G * per, k), dtype=torch.float32, device=X.device)
+    dist.all_gather_into_tensor(all_i, out_i, group=group)
+    dist.all_gather_into_tensor(all_d, out_d, group=group)
+    return all_i[:N], all_d[:N]
+
+
+def search_query_sharded(Q, X, k, group=None, compute=None, broadcast=True):
+    """k-NN search with the query rows sharded (Par-1); Q and X valid on rank 0."""
+    compute = compute or _default_compute
+    G, r = _world(group)
+    M = Q.shape[0]
+    if broadcast and G > 1:
+        broadcast_points(X, group)
+        broadcast_points(Q, group)
+    per = -(-M // G)
+    lo, hi = block_range(M, G, r)
+    out_i = torch.zeros((per, k), dtype=torch.int32, device=X.device)
+    out_d = torch.full((per, k), float("inf"), dtype=torch.float32, device=X.device)
+    if hi > lo:
+        i, d = compute(Q[lo:hi], X, k, 0, -(2 ** 63), 0)
+        out_i[: hi - lo] = i
+        out_d[: hi - lo] = d
+    if G == 1:
+        return out_i[:M], out_d[:M]
+    all_i = torch.empty((G * per, k), dtype=torch.int32, device=X.device)
+    all_d = torch.empty((G * per, k), dtype=torch.float32, device=X.device)
+    dist.all_gather_into_tensor(all_i, out_i, group=group)
+    dist.all_gather_into_tensor(all_d, out_d, group=group)
+    return all_i[:M], all_d[:M]
+
+
+def graph_corpus_sharded(X, k, metric=0, group=None, compute=None, merge=None, broadcast=True):
+    """k-NNG of X with the corpus columns sharded over the ranks (Par-2).
+
+    Needs k <= the smallest column block.  Returns the full graph on every rank."""
+    compute = compute or _default_compute
+    merge = merge or _default_merge
+    G, r = _world(group)
+    N = X.shape[0]
+    if broadcast and G > 1:
+        broadcast_points(X, group)
+    c0, c1 = block_range(N, G, r)
+    if min(block_range(N, G, g)[1] - block_range(N, G, g)[0] for g in range(G)) < k:
+        raise ValueError("corpus sharding needs k <= N/G")
+    per = -(-N // G)
+    # partial lists of every row against columns [c0, c1), rows padded to G*per
+    part_i = torch.zeros((G * per, k), dtype=torch.int32, device=X.device)
+    part_d = torch.full((G * per, k), float("inf"), dtype=torch.float32, device=X.device)
+    i, d = compute(X, X[c0:c1], k, metric, -c0, c0)  # self: global column c0 + j == row i
+    part_i[:N] = i
+    part_d[:N] = d
+    if G == 1:
+        return merge(part_d[None, :N], part_i[None, :N], np.zeros(1, np.int64))
+    # all-to-all: rank g receives, from every rank, the partial lists of rows block g
+    recv_i = torch.empty_like(part_i)
+    recv_d = torch.empty_like(part_d)
+    dist.all_to_all_single(recv_i, part_i, group=group)
+    dist.all_to_all_single(recv_d, part_d, group=group)
+    # recv[s*per:(s+1)*per] = rank s's lists for this rank's rows -> [G][per][k]
+    mi, md = merge(recv_d.view(G, per, k), recv_i.view(G, per, k), np.zeros(G, np.int64))
+    all_i = torch.empty((G * per, k), dtype=torch.int32, device=X.device)
+    all_d = torch.empty((G * per, k), dtype=torch.float32, device=X.device)
+    dist.all_gather_into_tensor(all_i, mi.contiguous(), group=group)
+    dist.all_gather_into_tensor(all_d, md.contiguous(), group=group)
+    return all_i[:N], all_d[:N]
