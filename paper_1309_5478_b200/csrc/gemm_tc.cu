@@ -18,14 +18,16 @@
 //              swizzled K-major, into a STAGES-deep ring (each stage feeds 3 MMA
 //              segments, so the hi tiles are loaded once and used twice);
 //      warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16);
-//      warps 2-5 epilogue: tcgen05.ld (32x32b.x32) -> registers -> fused distance
-//              assembly -> streaming 128-bit stores of the fp32 distance row.
+//      warps 2-9 epilogue: tcgen05.ld (32x32b.x32) -> registers -> fused distance
+//              assembly -> streaming 128-bit stores of the fp32 distance row.  Two
+//              warps per TMEM lane quadrant (32 rows), each owning half the columns.
 //    The accumulator is double-buffered in TMEM (2 × 256 columns), so the epilogue of
 //    tile t overlaps the MMAs of tile t+1.
 //  * Epilogue (per element): acc*(-2 rs_q) is exact (power-of-two scale), so
 //      D = max(fma(acc * (-2 rs_q), rs_x, ||q||^2 + ||x||^2), 0) + 0
 //    rounds once; +0 canonicalises -0 (R6); sqrt for L2; +inf on the excluded self pair.
 #include "internal.cuh"
+#include "ptx.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -40,13 +42,13 @@ constexpr int BN = 256;          // columns per tile (TMEM columns per accumulat
 constexpr int BK = 64;           // fp16 K elements per stage = one 128-byte swizzle row
 constexpr int STAGES = 2;
 constexpr int UMMA_K = 16;
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;     // 2 per TMEM lane quadrant, each owning BN/2 columns
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (16 KB)
 constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (32 KB)
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands
 constexpr int TMEM_COLS = 512;   // 2 accumulators × BN fp32 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, cols*/ +
-                           2 * BN * 2 * 4 /*column norms/scales, double buffered*/;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/;
 constexpr int GROUP_M = 16;      // tile-order swizzle: 16 row blocks share a column sweep
 
 // Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
@@ -54,29 +56,6 @@ constexpr int GROUP_M = 16;      // tile-order swizzle: 16 row blocks share a co
 // both K-major; [17,23) N>>3; [24,29) M>>4.
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
-// ------------------------------------------------------------ PTX wrappers ----------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
     asm volatile(
@@ -84,12 +63,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -123,9 +96,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
                  "f"(d)
@@ -151,18 +121,19 @@ struct EpiArgs {
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
 };
 
+template <int METRIC>
 __global__ void __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                int num_kb, TileMap tiles, int64_t num_tiles, EpiArgs ep) {
     extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
+    __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* stage_base = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-    float* col_n = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);  // [2][BN]
-    float* col_s = col_n + 2 * BN;                                                  // [2][BN]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
@@ -175,7 +146,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+            mbar_init(tempty0 + 8 * b, EPI_WARPS);  // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qh)));
@@ -261,9 +232,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------ epilogue (4 warps) --
-        const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-        const int etid = threadIdx.x - 64;     // 0..127
+        // ------------------------------------------------------ epilogue (8 warps) --
+        const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;           // which BN/2 columns it owns
+        const int etid = threadIdx.x - 64;          // 0..255
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int it = 0;
         for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
@@ -273,53 +245,70 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
             // stage the tile's column norms and scales (double-buffered by `buf`)
-            float* cn = col_n + buf * BN;
-            float* cs = col_s + buf * BN;
-            for (int c = etid; c < BN; c += 128) {
-                const int64_t j = n0 + c;
-                cn[c] = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
-                cs[c] = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+            {
+                const int64_t j = n0 + etid;
+                col_n[buf][etid] = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
+                col_s[buf][etid] = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
             }
-            named_bar(1, 128);
-            const int64_t row = mb * BM + quad * 32 + lane;
+            named_bar(1, 32 * EPI_WARPS);
+            const int64_t row0 = mb * BM + quad * 32;
+            const int64_t row = row0 + lane;
             const bool row_ok = row < ep.M;
             const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
             const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
-            const int64_t self_col = row + ep.self_shift;  // wraps harmlessly for KNN_NO_SELF
-            float* drow = ep.D + row * ep.ldD + n0;
+            const int64_t c_lo = n0 + half * (BN / 2);
+            // does this warp's 32x(BN/2) block touch the excluded self pairs?
+            const bool diag = ep.self_shift != INT64_MIN &&
+                              row0 + ep.self_shift < c_lo + BN / 2 && row0 + 31 + ep.self_shift >= c_lo;
+            const int64_t self_col = row + ep.self_shift;
+            float* drow = ep.D + row * ep.ldD;
 
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + half * (BN / 2);
             #pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
+            for (int ch = 0; ch < BN / 64; ++ch) {
                 uint32_t r[32];
                 tmem_ld32(taddr + ch * 32, r);
-                if (ch == BN / 32 - 1) {
+                if (ch == BN / 64 - 1) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
                 }
-                if (!row_ok) continue;
+                const int cb = half * (BN / 2) + ch * 32;  // first column of the chunk in the tile
+                const float4* cn4 = reinterpret_cast<const float4*>(&col_n[buf][cb]);
+                const float4* cs4 = reinterpret_cast<const float4*>(&col_s[buf][cb]);
                 float v[32];
                 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const int cc = ch * 32 + c;
-                    float dd = fmaf(__uint_as_float(r[c]) * cq, cs[cc], qn + cn[cc]);
-                    dd = fmaxf(dd, 0.0f) + 0.0f;
-                    if (ep.metric == 1) dd = sqrtf(dd);
-                    if (n0 + cc == self_col) dd = __int_as_float(0x7F800000);
-                    v[c] = dd;
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const float4 nn = cn4[c4];
+                    const float4 ss = cs4[c4];
+                    const float na[4] = {nn.x, nn.y, nn.z, nn.w};
+                    const float sa4[4] = {ss.x, ss.y, ss.z, ss.w};
+                    #pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = 4 * c4 + e;
+                        float dd = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
+                        dd = fmaxf(dd, 0.0f) + 0.0f;
+                        if (METRIC == 1) dd = sqrtf(dd);
+                        v[c] = dd;
+                    }
                 }
-                const int64_t c0 = n0 + ch * 32;
+                const int64_t c0 = n0 + cb;
+                if (diag) {
+                    #pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
+                }
+                if (!row_ok) continue;
                 if (vec_ok && c0 + 32 <= ep.N) {
                     #pragma unroll
                     for (int c = 0; c < 32; c += 4)
-                        st_cs4(drow + ch * 32 + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+                        st_cs4(drow + c0 + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
                 } else {
                     #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                        if (c0 + c < ep.N) drow[ch * 32 + c] = v[c];
+                        if (c0 + c < ep.N) drow[c0 + c] = v[c];
                 }
             }
         }
@@ -384,11 +373,10 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int64_t num_tiles = tiles.n_mb * tiles.n_nb;
     const int grid = (int)(num_tiles < num_sms ? num_tiles : num_sms);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD};
-    cudaError_t e = cudaFuncSetAttribute(dist_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
+    auto kern = metric == 1 ? dist_tc_kernel<1> : dist_tc_kernel<0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    dist_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, op.d_pad / BK, tiles,
-                                                     num_tiles, ep);
+    kern<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, op.d_pad / BK, tiles, num_tiles, ep);
     return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@
 // correctly rejected by the strict "< T" test.  The merge sees lists in arbitrary index
 // order and uses the composite test (key, index) < (T, T_idx).
 #include "internal.cuh"
+#include "ptx.cuh"
 
 #include <climits>
 
@@ -37,6 +38,13 @@ struct Scal {
     uint32_t bin, before, neq;
     int kept;
 };
+
+// Barrier over the THREADS consumer threads 0..THREADS-1 of the CTA (named barrier 1), so
+// that a producer warp outside them never takes part.
+template <int THREADS>
+__device__ __forceinline__ void csync() {
+    named_bar(1, THREADS);
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -54,14 +62,14 @@ __device__ void radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt, 
                            uint32_t rank, uint32_t* hist, Scal* sc) {
     const int tid = threadIdx.x;
     for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
-    __syncthreads();
+    csync<THREADS>();
     for (int i = tid; i < cnt; i += THREADS) {
         uint32_t key = ckey[i];
         uint32_t v = on_idx ? cidx[i] : key;
         bool ok = on_idx ? (key == key_eq) : true;
         if (ok && (v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
     }
-    __syncthreads();
+    csync<THREADS>();
     if (tid < 32) {
         const int lane = tid;
         uint32_t c[8], sum = 0;
@@ -90,7 +98,7 @@ __device__ void radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt, 
             }
         }
     }
-    __syncthreads();
+    csync<THREADS>();
 }
 
 // Exact selection of the k best (key, idx) among cnt >= k candidates.  Writes them
@@ -124,7 +132,7 @@ __device__ void block_select_k(const uint32_t* ckey, const uint32_t* cidx, int c
     // Compaction of the kept side with the paper's ballot/popc primitive.
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) sc->kept = 0;
-    __syncthreads();
+    csync<THREADS>();
     for (int b = warp * 32; b < cnt; b += THREADS) {
         int i = b + lane;
         bool p = false;
@@ -146,7 +154,7 @@ __device__ void block_select_k(const uint32_t* ckey, const uint32_t* cidx, int c
             }
         }
     }
-    __syncthreads();
+    csync<THREADS>();
 }
 
 // Bitonic sort of KP (power of two) pairs by (key, idx) ascending.
@@ -165,7 +173,7 @@ __device__ void block_bitonic(uint32_t* key, uint32_t* idx, int KP) {
                     idx[i] = ij; idx[j] = ii;
                 }
             }
-            __syncthreads();
+            csync<THREADS>();
         }
     }
 }
@@ -188,7 +196,7 @@ __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int
         kkey[i] = 0xFFFFFFFFu;
         kidx[i] = 0xFFFFFFFFu;
     }
-    __syncthreads();
+    csync<THREADS>();
     block_bitonic<THREADS>(kkey, kidx, KP);
     for (int r = threadIdx.x; r < k; r += THREADS) {
         out_idx[r] = (int32_t)((int64_t)kidx[r] + idx_offset);
@@ -217,8 +225,38 @@ __device__ __forceinline__ float f4get(const float4& v, int c) {
 // Element e = 4*j + c of a thread in the chunk at `base` sits at column
 //   VEC:  base + 4*(j*THREADS + tid) + c        (one float4 per j)
 //   else: base + (4*j + c)*THREADS + tid        (coalesced scalars)
+// The next chunk is loaded into registers while the current one is filtered.  A warp
+// first tests its 32*EPT elements against the float image tf of the threshold (exact for
+// every non-NaN key once T is a finite/inf key); only warps holding a survivor run the
+// key transform and the ballot/popc compaction.
 template <int THREADS, int VPT, bool VEC>
-__global__ void __launch_bounds__(THREADS)
+__device__ __forceinline__ void load_chunk(float4 (&v)[VPT], const float* __restrict__ rp,
+                                           int64_t N, int64_t base, int tid) {
+    #pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        if (VEC) {
+            const int64_t c0 = base + 4 * ((int64_t)j * THREADS + tid);
+            v[j] = c0 < N ? ld_stream4(rp + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            float t[4];
+            #pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int64_t cc = base + (int64_t)(4 * j + c) * THREADS + tid;
+                t[c] = cc < N ? ld_stream1(rp + cc) : 0.0f;
+            }
+            v[j] = make_float4(t[0], t[1], t[2], t[3]);
+        }
+    }
+}
+
+template <int THREADS, bool VEC>
+__device__ __forceinline__ int64_t elem_col(int64_t base, int e, int tid) {
+    return VEC ? base + 4 * ((int64_t)(e >> 2) * THREADS + tid) + (e & 3)
+               : base + (int64_t)e * THREADS + tid;
+}
+
+template <int THREADS, int VPT, bool VEC>
+__global__ void __maxnreg__(80)
 select_rows_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k, int cap, int KP,
                    int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
                    float* __restrict__ out_dist) {
@@ -238,69 +276,65 @@ select_rows_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k, i
     const float* rp = D + row * ldD;
     if (tid == 0) s_count = 0;
     uint32_t T = kKeyMax;
-
-    auto col = [&](int64_t base, int e) -> int64_t {
-        return VEC ? base + 4 * ((int64_t)(e >> 2) * THREADS + tid) + (e & 3)
-                   : base + (int64_t)e * THREADS + tid;
-    };
-    auto load = [&](float4* v, int64_t base) {
-        #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            if (VEC) {
-                int64_t c0 = col(base, 4 * j);
-                v[j] = c0 < N ? ld_stream4(rp + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-                float t[4];
-                #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    int64_t cc = col(base, 4 * j + c);
-                    t[c] = cc < N ? ld_stream1(rp + cc) : 0.0f;
-                }
-                v[j] = make_float4(t[0], t[1], t[2], t[3]);
-            }
-        }
-    };
+    float tf = 0.0f;
+    bool fast = false;  // T is the key of a non-NaN value: the float test is exact
 
     float4 cur[VPT], nxt[VPT];
-    load(cur, 0);
+    load_chunk<THREADS, VPT, VEC>(cur, rp, N, 0, tid);
     __syncthreads();
     for (int64_t base = 0; base < N; base += CHUNK) {
-        if (base + CHUNK < N) load(nxt, base + CHUNK);
+        if (base + CHUNK < N) load_chunk<THREADS, VPT, VEC>(nxt, rp, N, base + CHUNK, tid);
         const bool full = base + CHUNK <= N;
-        uint32_t pm = 0;
-        #pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            bool ok = ukey(f4get(cur[e >> 2], e & 3)) < T;
-            if (!full) ok = ok && col(base, e) < N;
-            pm |= (uint32_t)ok << e;
+        bool any = !(fast && full);
+        if (!any) {
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j)
+                any |= (cur[j].x < tf) | (cur[j].y < tf) | (cur[j].z < tf) | (cur[j].w < tf);
         }
-        int my = __popc(pm);
         bool over = false;
-        if (__any_sync(FULL, my != 0)) {
+        if (__any_sync(FULL, any)) {
+            uint32_t pm = 0;
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+                #pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    bool ok = ukey(c4[c]) < T;
+                    if (!full) ok = ok && elem_col<THREADS, VEC>(base, 4 * j + c, tid) < N;
+                    pm |= (uint32_t)ok << (4 * j + c);
+                }
+            }
+            const int my = __popc(pm);
             // warp-inclusive scan of the per-thread survivor counts, one shared atomic
             // per warp (the paper's counters g_< kept in shared memory)
             int incl = my;
             #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int n = __shfl_up_sync(FULL, incl, o);
+                const int n = __shfl_up_sync(FULL, incl, o);
                 if (lane >= o) incl += n;
             }
             const int wtot = __shfl_sync(FULL, incl, 31);
-            int wbase = 0;
-            if (lane == 31) wbase = atomicAdd(&s_count, wtot);
-            wbase = __shfl_sync(FULL, wbase, 31);
-            over = wbase + wtot > limit;
-            int off = wbase + incl - my;
-            #pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                if (pm & (1u << e)) {
-                    ckey[off] = ukey(f4get(cur[e >> 2], e & 3));
-                    cidx[off] = (uint32_t)col(base, e);
-                    ++off;
+            if (wtot) {
+                int wbase = 0;
+                if (lane == 31) wbase = atomicAdd(&s_count, wtot);
+                wbase = __shfl_sync(FULL, wbase, 31);
+                over = wbase + wtot > limit;
+                int off = wbase + incl - my;
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+                    #pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (pm & (1u << (4 * j + c))) {
+                            ckey[off] = ukey(c4[c]);
+                            cidx[off] = (uint32_t)elem_col<THREADS, VEC>(base, 4 * j + c, tid);
+                            ++off;
+                        }
+                    }
                 }
             }
         }
-        if (__syncthreads_or(over)) {
+        if (named_bar_or(1, THREADS, over)) {
             uint32_t tk, ti;
             block_select_k<THREADS>(ckey, cidx, s_count, k, kkey, kidx, hist, &sc, false, tk, ti);
             for (int i = tid; i < k; i += THREADS) {
@@ -309,7 +343,9 @@ select_rows_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k, i
             }
             if (tid == 0) s_count = k;
             T = tk;
-            __syncthreads();
+            fast = T <= 0xFF800000u;  // key of a non-NaN value (<= +inf)
+            tf = ukey_to_float(T);
+            csync<THREADS>();
         }
         #pragma unroll
         for (int j = 0; j < VPT; ++j) cur[j] = nxt[j];
@@ -317,6 +353,594 @@ select_rows_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k, i
     __syncthreads();
     block_finish<THREADS>(ckey, cidx, s_count, k, KP, kkey, kidx, hist, &sc, idx_offset,
                           out_idx + row * k, out_dist + row * k);
+}
+
+// ------------------------------------------------------------------ ballot append ----
+// The paper's partition primitive applied per 32-element segment: for
+// element slot e of every lane, B = __ballot(x < T); a lane with its bit set stores its
+// element at base + popc(B & lanemask_lt); the warp advances by popc(B).  Slots whose vote
+// is empty are skipped warp-uniformly, so a chunk with a handful of survivors costs ~3
+// instructions per slot.  In `fast` mode the test is the float compare x < tf, exact for
+// every key once T is the key of a non-NaN value; otherwise the order-preserving key test.
+// `col(e)` gives the column of slot e; positions >= N are rejected when !full.
+// Returns the number appended (warp-uniform).
+template <int J0, int NJ, int VPT, class ColF>
+__device__ __forceinline__ int warp_append_generic(const float4 (&cur)[VPT], uint32_t Tlim, bool full,
+                                                   int64_t N, ColF col, uint32_t* ckey,
+                                                   uint32_t* cidx, int base) {
+    const uint32_t lt = lanemask_lt();
+    int added = 0;
+    #pragma unroll
+    for (int j = J0; j < J0 + NJ; ++j) {
+        const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+        #pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t u = ukey(c4[c]);
+            bool ok = u < Tlim;
+            if (!full) ok = ok && col(4 * j + c) < N;
+            const uint32_t m = __ballot_sync(FULL, ok);
+            if (m) {
+                if (ok) {
+                    const int pos = base + added + __popc(m & lt);
+                    ckey[pos] = u;
+                    cidx[pos] = (uint32_t)col(4 * j + c);
+                }
+                added += __popc(m);
+            }
+        }
+    }
+    return added;
+}
+
+// Steady state (full chunk, threshold the key of a non-NaN value): one vote per float4
+// group on min(group) < tf, then per-element votes only inside groups holding a survivor.
+template <int J0, int NJ, int VPT, class ColF>
+__device__ __forceinline__ int warp_append_fast(const float4 (&cur)[VPT], float tf, ColF col,
+                                                uint32_t* ckey, uint32_t* cidx, int base) {
+    const uint32_t lt = lanemask_lt();
+    int added = 0;
+    #pragma unroll
+    for (int j = J0; j < J0 + NJ; ++j) {
+        const float mn = fminf(fminf(cur[j].x, cur[j].y), fminf(cur[j].z, cur[j].w));
+        if (!__any_sync(FULL, mn < tf)) continue;
+        const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+        #pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const bool ok = c4[c] < tf;
+            const uint32_t m = __ballot_sync(FULL, ok);
+            if (m) {
+                if (ok) {
+                    const int pos = base + added + __popc(m & lt);
+                    ckey[pos] = ukey(c4[c]);
+                    cidx[pos] = (uint32_t)col(4 * j + c);
+                }
+                added += __popc(m);
+            }
+        }
+    }
+    return added;
+}
+
+// Block variant: slots with a non-empty vote reserve space in the CTA-shared buffer with
+// one atomicAdd by the lowest voting lane.  Returns true if the buffer grew past `limit`.
+template <int VPT, class ColF>
+__device__ __forceinline__ bool block_append(const float4 (&cur)[VPT], uint32_t T, float tf, bool fast,
+                                             bool full, int64_t N, ColF col, uint32_t* ckey,
+                                             uint32_t* cidx, int* s_count, int limit) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    bool over = false;
+    #pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+        #pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float x = c4[c];
+            bool ok = fast ? (x < tf) : (ukey(x) < T);
+            if (!full) ok = ok && col(4 * j + c) < N;
+            const uint32_t m = __ballot_sync(FULL, ok);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                int wb = 0;
+                if (lane == leader) wb = atomicAdd(s_count, __popc(m));
+                wb = __shfl_sync(FULL, wb, leader);
+                if (ok) {
+                    const int pos = wb + __popc(m & lt);
+                    ckey[pos] = ukey(x);
+                    cidx[pos] = (uint32_t)col(4 * j + c);
+                }
+                over |= wb + __popc(m) > limit;
+            }
+        }
+    }
+    return over;
+}
+
+// ------------------------------------------------------------------ ring select ------
+// Persistent CTAs, one row at a time: a producer warp streams the row in CHUNK-element
+// slices through a STAGES-deep shared-memory ring with 1-D bulk async copies (the TMA
+// engine; completion on mbarriers), prefetching across row boundaries, so the bytes in
+// flight do not depend on registers; CTHREADS consumer threads filter each slice with the
+// running threshold and compact survivors with ballot/popc exactly as above.
+// Requires 16-byte aligned rows (ldD % 4 == 0, aligned D).
+template <int CTHREADS, int CHUNK, int STAGES>
+__global__ void __launch_bounds__(CTHREADS + 32, 1)
+select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int cap,
+                   int KP, int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
+                   float* __restrict__ out_dist) {
+    constexpr int VPT = CHUNK / CTHREADS / 4;  // float4 per consumer thread per slice
+    static_assert(VPT * 4 * CTHREADS == CHUNK, "CHUNK must be a multiple of 4*CTHREADS");
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)STAGES * CHUNK);  // full, empty
+    uint32_t* ckey = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
+    uint32_t* cidx = ckey + cap;
+    uint32_t* kkey = cidx + cap;
+    uint32_t* kidx = kkey + KP;
+    uint32_t* hist = kidx + KP;
+    __shared__ Scal sc;
+    __shared__ int s_count;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const int64_t nchunk = ceil_div(N, CHUNK);
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, CTHREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CTHREADS / 32) {
+        // -------------------------------------------------------- producer warp ------
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+                const float* rp = D + row * ldD;
+                for (int64_t c = 0; c < nchunk; ++c) {
+                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                    const int64_t elems = (N - c * CHUNK) < CHUNK ? (N - c * CHUNK) : CHUNK;
+                    const uint32_t bytes = (uint32_t)round_up(elems * 4, 16);
+                    mbar_expect_tx(full0 + 8 * stage, bytes);
+                    bulk_load_evict_first(smem_u32(ring + (size_t)stage * CHUNK), rp + c * CHUNK,
+                                          bytes, full0 + 8 * stage, pol);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers ----------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+        if (tid == 0) s_count = 0;
+        uint32_t T = kKeyMax;
+        float tf = 0.0f;
+        bool fast = false;
+        csync<CTHREADS>();
+        for (int64_t c = 0; c < nchunk; ++c) {
+            const int64_t base = c * CHUNK;
+            mbar_wait(full0 + 8 * stage, phase);
+            const float4* buf = reinterpret_cast<const float4*>(ring + (size_t)stage * CHUNK);
+            float4 cur[VPT];
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) cur[j] = buf[j * CTHREADS + tid];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * stage);  // slot may be refilled
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+            const bool full = base + CHUNK <= N;
+            bool any = !(fast && full);
+            if (!any) {
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j)
+                    any |= (cur[j].x < tf) | (cur[j].y < tf) | (cur[j].z < tf) | (cur[j].w < tf);
+            }
+            bool over = false;
+            if (__any_sync(FULL, any))
+                over = block_append<VPT>(
+                    cur, T, tf, fast, full, N,
+                    [&](int e) -> int64_t { return base + 4 * ((e >> 2) * CTHREADS + tid) + (e & 3); },
+                    ckey, cidx, &s_count, limit);
+            if (named_bar_or(1, CTHREADS, over)) {
+                uint32_t tk, ti;
+                block_select_k<CTHREADS>(ckey, cidx, s_count, k, kkey, kidx, hist, &sc, false, tk, ti);
+                for (int i = tid; i < k; i += CTHREADS) {
+                    ckey[i] = kkey[i];
+                    cidx[i] = kidx[i];
+                }
+                if (tid == 0) s_count = k;
+                T = tk;
+                fast = T <= 0xFF800000u;
+                tf = ukey_to_float(T);
+                csync<CTHREADS>();
+            }
+        }
+        csync<CTHREADS>();
+        block_finish<CTHREADS>(ckey, cidx, s_count, k, KP, kkey, kidx, hist, &sc, idx_offset,
+                               out_idx + row * k, out_dist + row * k);
+        csync<CTHREADS>();
+    }
+}
+
+// ------------------------------------------------------------------ warp select ------
+// The paper's warp-per-query mode ("Each array is handled by a single
+// thread warp ... synchronized by default"; >= 1024 queries saturate the
+// GPU) made B200-native for k <= 128: one warp owns one row and runs the whole select —
+// threshold filter, ballot/popc compaction into a warp-private shared buffer, exact radix
+// rebuild, final register bitonic sort — with warp-synchronous code only, so no CTA
+// barrier ever couples rows.  The row is streamed through a warp-private ring of 1-D
+// bulk async copies (TMA engine) that lane 0 keeps WS stages ahead, across row
+// boundaries, so one row's rebuild/sort tail overlaps the other warps' streaming.
+constexpr int WSEL_K = 128;      // largest k of the warp path
+constexpr int WSEL_C = 1024;     // floats per ring stage (4 KB)
+constexpr int WSEL_S = 3;        // ring stages per warp
+constexpr int WSEL_WARPS = 4;    // warps (rows in flight) per CTA
+constexpr int WSEL_SUB = 256;    // elements appended between buffer checks
+
+__host__ __device__ constexpr int64_t wsel_slab_bytes(int cap) {
+    return round_up((int64_t)WSEL_S * WSEL_C * 4 + WSEL_S * 8 + (int64_t)(2 * cap + 2 * WSEL_K + 256) * 4,
+                    128);
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Warp radix pass: histogram of digit `shift` (of key, or of idx among key == key_eq)
+// over cnt warp-private candidates; returns the bin holding the rank-th value and the
+// counts below / in it (warp-uniform).
+__device__ __forceinline__ void warp_radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt,
+                                                bool on_idx, uint32_t key_eq, uint32_t prefix,
+                                                uint32_t mask, int shift, uint32_t rank,
+                                                uint32_t* hist, uint32_t& bin, uint32_t& before,
+                                                uint32_t& neq) {
+    const int lane = threadIdx.x & 31;
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane + 32 * i] = 0;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+        const uint32_t key = ckey[i];
+        const uint32_t v = on_idx ? cidx[i] : key;
+        const bool ok = on_idx ? (key == key_eq) : true;
+        if (ok && (v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t c[8], sum = 0;
+    #pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        c[j] = hist[lane * 8 + j];
+        sum += c[j];
+    }
+    uint32_t incl = sum;
+    #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += n;
+    }
+    const uint32_t excl = incl - sum;
+    const uint32_t hit = __ballot_sync(FULL, excl < rank && rank <= incl);
+    const int src = __ffs(hit) - 1;
+    uint32_t b = 0, bef = 0, eq = 0;
+    if (lane == src) {
+        uint32_t run = excl;
+        bool found = false;
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (!found && run + c[j] >= rank) {
+                b = lane * 8 + j;
+                bef = run;
+                eq = c[j];
+                found = true;
+            }
+            if (!found) run += c[j];
+        }
+    }
+    bin = __shfl_sync(FULL, b, src);
+    before = __shfl_sync(FULL, bef, src);
+    neq = __shfl_sync(FULL, eq, src);
+    __syncwarp();
+}
+
+// Keep exactly the k best (key, idx) of cnt >= k warp-private candidates, compacted into
+// okey/oidx[0, k); returns the key of the k-th best.  The radix passes start below the
+// key bits all candidates share (warp AND/OR reduction), so the first digit is not the
+// degenerate one of a narrow value range.
+__device__ __noinline__ uint32_t warp_select_k(const uint32_t* ckey, const uint32_t* cidx, int cnt,
+                                               int k, uint32_t* okey, uint32_t* oidx,
+                                               uint32_t* hist) {
+    const int lane = threadIdx.x & 31;
+    uint32_t andv = 0xFFFFFFFFu, orv = 0;
+    for (int i = lane; i < cnt; i += 32) {
+        const uint32_t v = ckey[i];
+        andv &= v;
+        orv |= v;
+    }
+    andv = __reduce_and_sync(FULL, andv);
+    orv = __reduce_or_sync(FULL, orv);
+    const uint32_t diff = andv ^ orv;
+    uint32_t rank = (uint32_t)k, neq = (uint32_t)cnt, bin, before;
+    uint32_t prefix = andv, mask = 0xFFFFFFFFu;
+    if (diff) {
+        const int hb = 31 - __clz(diff);
+        mask = hb == 31 ? 0u : ~((2u << hb) - 1u);
+        prefix = andv & mask;
+        for (int hi = hb; hi >= 0; hi -= 8) {
+            const int shift = hi >= 7 ? hi - 7 : 0;
+            warp_radix_pass(ckey, cidx, cnt, false, 0, prefix, mask, shift, rank, hist, bin, before, neq);
+            rank -= before;
+            const uint32_t wmask = ((2u << (hi - shift)) - 1u) << shift;  // digit bits
+            prefix |= (bin << shift) & wmask;
+            mask |= wmask;
+        }
+    }
+    const uint32_t Tkey = prefix;
+    uint32_t Tidx = 0xFFFFFFFFu;
+    if (neq > rank) {
+        uint32_t p2 = 0, m2 = 0;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            warp_radix_pass(ckey, cidx, cnt, true, Tkey, p2, m2, shift, rank, hist, bin, before, neq);
+            rank -= before;
+            p2 |= bin << shift;
+            m2 |= 0xFFu << shift;
+        }
+        Tidx = p2;
+    }
+    int base = 0;
+    for (int b = 0; b < cnt; b += 32) {
+        const int i = b + lane;
+        bool p = false;
+        uint32_t kk = 0, ii = 0;
+        if (i < cnt) {
+            kk = ckey[i];
+            ii = cidx[i];
+            p = kk < Tkey || (kk == Tkey && ii <= Tidx);
+        }
+        const uint32_t m = __ballot_sync(FULL, p);
+        if (p) {
+            const int pos = base + __popc(m & lanemask_lt());
+            okey[pos] = kk;
+            oidx[pos] = ii;
+        }
+        base += __popc(m);
+    }
+    __syncwarp();
+    return Tkey;
+}
+
+// Bitonic sort of R*32 (key, idx) pairs held as 64-bit words, element e = r*32 + lane.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[R]) {
+    const int lane = threadIdx.x & 31;
+    #pragma unroll
+    for (int size = 2; size <= 32 * R; size <<= 1) {
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                const int rs = stride / 32;
+                #pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int rp = r ^ rs;
+                    if (rp > r) {
+                        const int e = r * 32 + lane;
+                        const bool asc = (e & size) == 0;
+                        const uint64_t a = v[r], b = v[rp];
+                        const bool sw = asc ? (a > b) : (a < b);
+                        v[r] = sw ? b : a;
+                        v[rp] = sw ? a : b;
+                    }
+                }
+            } else {
+                #pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int e = r * 32 + lane;
+                    const uint64_t o = __shfl_xor_sync(FULL, v[r], stride);
+                    const bool asc = (e & size) == 0;
+                    const bool lower = (lane & stride) == 0;
+                    const bool take_min = (lower == asc);
+                    v[r] = take_min ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+                }
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_write(const uint32_t* key, const uint32_t* idx, int k,
+                                                int64_t idx_offset, int32_t* out_idx,
+                                                float* out_dist) {
+    const int lane = threadIdx.x & 31;
+    uint64_t v[R];
+    #pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = r * 32 + lane;
+        v[r] = e < k ? ((uint64_t)key[e] << 32 | idx[e]) : ~0ull;
+    }
+    warp_bitonic<R>(v);
+    #pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = r * 32 + lane;
+        if (e < k) {
+            out_idx[e] = (int32_t)((int64_t)(uint32_t)v[r] + idx_offset);
+            out_dist[e] = ukey_to_float((uint32_t)(v[r] >> 32));
+        }
+    }
+}
+
+// Reduce the warp's candidate buffer to exactly its k best, in place; returns the
+// k-th best key (the new strict threshold).  Out of line: it runs a few times per row.
+__device__ __noinline__ uint32_t warp_rebuild(uint32_t* ckey, uint32_t* cidx, int count, int k,
+                                              uint32_t* kkey, uint32_t* kidx, uint32_t* hist) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t t = warp_select_k(ckey, cidx, count, k, kkey, kidx, hist);
+    for (int i = lane; i < k; i += 32) {
+        ckey[i] = kkey[i];
+        cidx[i] = kidx[i];
+    }
+    __syncwarp();
+    return t;
+}
+
+template <int R>
+__global__ void __maxnreg__(128)
+select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int cap,
+                   int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
+                   float* __restrict__ out_dist) {
+    constexpr int VPT = WSEL_C / 128;      // float4 per lane per stage (8)
+    constexpr int SUBJ = WSEL_SUB / 128;   // float4 per lane per append sub-group (2)
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per-warp slab: ring | full barriers | candidates key, idx | kept key, idx | hist
+    uint8_t* my = smem_raw + wsel_slab_bytes(cap) * warp;
+    float* ring = reinterpret_cast<float*>(my);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + WSEL_S * WSEL_C);
+    uint32_t* ckey = reinterpret_cast<uint32_t*>(bars + WSEL_S);
+    uint32_t* cidx = ckey + cap;
+    uint32_t* kkey = cidx + cap;
+    uint32_t* kidx = kkey + WSEL_K;
+    uint32_t* hist = kidx + WSEL_K;
+    const uint32_t full0 = smem_u32(bars);
+    const uint32_t ring0 = smem_u32(ring);
+
+    const int64_t gw = (int64_t)blockIdx.x * WSEL_WARPS + warp;
+    const int64_t nw = (int64_t)gridDim.x * WSEL_WARPS;
+    const int64_t nchunk = ceil_div(N, WSEL_C);
+    if (lane == 0) {
+        for (int s = 0; s < WSEL_S; ++s) mbar_init(full0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // producer state (lane 0): next chunk to issue
+    int64_t prow = gw, pc = 0;
+    const float* psrc = D + gw * ldD;
+    const uint32_t last_bytes = (uint32_t)round_up((N - (nchunk - 1) * WSEL_C) * 4, 16);
+    auto issue = [&](int stage) {
+        if (prow >= M) return;
+        const uint32_t bytes = pc == nchunk - 1 ? last_bytes : (uint32_t)(WSEL_C * 4);
+        mbar_expect_tx(full0 + 8 * stage, bytes);
+        bulk_load(ring0 + stage * (WSEL_C * 4), psrc, bytes, full0 + 8 * stage);
+        psrc += WSEL_C;
+        if (++pc == nchunk) {
+            pc = 0;
+            prow += nw;
+            psrc = D + prow * ldD;
+        }
+    };
+    if (lane == 0)
+        for (int st = 0; st < WSEL_S; ++st) issue(st);
+
+    int stage = 0;
+    uint32_t parity = 0;
+    for (int64_t row = gw; row < M; row += nw) {
+        uint32_t Tlim = kKeyMax;  // accept keys u < Tlim
+        float tf = 0.0f;
+        bool fast = false;
+        int count = 0;
+        auto rebuild = [&]() {
+            const uint32_t t = warp_rebuild(ckey, cidx, count, k, kkey, kidx, hist);
+            count = k;
+            Tlim = t;  // later elements have larger indices: strict
+            fast = t <= 0xFF800000u;
+            tf = ukey_to_float(t);
+        };
+        for (int64_t c = 0; c < nchunk; ++c) {
+            mbar_wait(full0 + 8 * stage, parity);
+            const float4* buf = reinterpret_cast<const float4*>(ring + stage * WSEL_C);
+            float4 cur[VPT];
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) cur[j] = buf[j * 32 + lane];
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue(stage);  // refill this slot (the reads above are complete)
+            }
+            if (++stage == WSEL_S) {
+                stage = 0;
+                parity ^= 1;
+            }
+            const int64_t base = c * WSEL_C;
+            const bool full = base + WSEL_C <= N;
+            const int lane_ = lane;
+            auto col = [&](int e) -> int64_t { return base + 4 * ((e >> 2) * 32 + lane_) + (e & 3); };
+            if (fast && full) {
+                // steady state: tree minimum over the lane's 32 elements, one vote
+                float m[VPT];
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j)
+                    m[j] = fminf(fminf(cur[j].x, cur[j].y), fminf(cur[j].z, cur[j].w));
+                #pragma unroll
+                for (int w = VPT / 2; w > 0; w >>= 1)
+                    #pragma unroll
+                    for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
+                if (!__any_sync(FULL, m[0] < tf)) continue;
+                // append in WSEL_SUB-element sub-groups (columns increase with the group),
+                // rebuilding whenever the buffer passes `limit`
+#define KNN_FAST_SG(J)                                                                  \
+    count += warp_append_fast<J, SUBJ>(cur, tf, col, ckey, cidx, count);                \
+    if (count > limit) rebuild();
+                KNN_FAST_SG(0) KNN_FAST_SG(2) KNN_FAST_SG(4) KNN_FAST_SG(6)
+#undef KNN_FAST_SG
+                continue;
+            }
+            const bool first = (c == 0 && full);
+            if (first) {
+                // Initial threshold from the first chunk: split each lane's 32 elements into
+                // R groups; t0 = the largest of the 32R group minima (keys).  At least
+                // 32R >= k elements are <= t0, so every element > t0 is beaten by k others:
+                // keep u <= t0 in this chunk and u < t0 afterwards (larger indices).
+                constexpr int GS = (WSEL_C / 32) / R;  // elements per group
+                uint32_t t0 = 0;
+                #pragma unroll
+                for (int g = 0; g < R; ++g) {
+                    uint32_t mn = 0xFFFFFFFFu;
+                    #pragma unroll
+                    for (int e = g * GS; e < (g + 1) * GS; ++e) {
+                        const float4& f = cur[e >> 2];
+                        const float x = (e & 3) == 0 ? f.x : (e & 3) == 1 ? f.y : (e & 3) == 2 ? f.z : f.w;
+                        mn = min(mn, ukey(x));
+                    }
+                    t0 = max(t0, mn);
+                }
+                t0 = __reduce_max_sync(FULL, t0);
+                Tlim = t0 + 1;
+            }
+            // generic path: first / partial chunks, or a NaN / unset threshold
+            bool rebuilt = false;
+#define KNN_GEN_SG(J)                                                                   \
+    count += warp_append_generic<J, SUBJ>(cur, Tlim, full, N, col, ckey, cidx, count);  \
+    if (count > limit) {                                                                \
+        rebuild();                                                                      \
+        rebuilt = true;                                                                 \
+    }
+            KNN_GEN_SG(0) KNN_GEN_SG(2) KNN_GEN_SG(4) KNN_GEN_SG(6)
+#undef KNN_GEN_SG
+            if (first && !rebuilt) {  // later chunks: strict u < t0
+                Tlim -= 1;
+                fast = Tlim <= 0xFF800000u;
+                tf = ukey_to_float(Tlim);
+            }
+        }
+        const uint32_t* fk = ckey;
+        const uint32_t* fi = cidx;
+        if (count > k) {
+            warp_select_k(ckey, cidx, count, k, kkey, kidx, hist);
+            fk = kkey;
+            fi = kidx;
+        }
+        warp_sort_write<R>(fk, fi, k, idx_offset, out_idx + row * k, out_dist + row * k);
+        __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ merge kernel -----
@@ -384,7 +1008,7 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
                     ++off;
                 }
         }
-        if (__syncthreads_or(over)) {
+        if (named_bar_or(1, THREADS, over)) {
             uint32_t tk, ti;
             block_select_k<THREADS>(ckey, cidx, s_count, k, kkey, kidx, hist, &sc, true, tk, ti);
             for (int i = tid; i < k; i += THREADS) {
@@ -394,7 +1018,7 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
             if (tid == 0) s_count = k;
             T = tk;
             Ti = ti;
-            __syncthreads();
+            csync<THREADS>();
         }
     }
     __syncthreads();
@@ -418,30 +1042,74 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
                           int64_t idx_offset, int32_t* out_idx, float* out_dist, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
-    constexpr int THREADS = 256, VPT = 2, CHUNK = THREADS * VPT * 4;
     const int KP = next_pow2(k);
+    const bool aligned = (ldD % 4 == 0) && ((reinterpret_cast<uintptr_t>(D) & 15) == 0);
+    cudaError_t e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (aligned && k <= WSEL_K && M >= 4 * (int64_t)sms) {
+        // warp per row: enough rows to give every SM >= 4 warps
+        const int limit = (int)round_up(k + 64 > 2 * k ? k + 64 : 2 * k, 32);
+        const int cap = WSEL_SUB + limit;
+        const size_t smem = (size_t)wsel_slab_bytes(cap) * WSEL_WARPS;
+        auto pick = [&](auto kern) -> cudaError_t {
+            cudaError_t e2;
+            if ((e2 = set_smem(kern, smem)) != cudaSuccess) return e2;
+            int per_sm = 0;
+            if ((e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WSEL_WARPS, smem)) != cudaSuccess)
+                return e2;
+            int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+            const int64_t need = ceil_div(M, WSEL_WARPS);
+            if (grid > need) grid = need;
+            kern<<<(unsigned)grid, 32 * WSEL_WARPS, smem, s>>>(D, M, N, ldD, k, cap, limit, idx_offset,
+                                                               out_idx, out_dist);
+            return cudaGetLastError();
+        };
+        if (k <= 32) return pick(select_warp_kernel<1>);
+        if (k <= 64) return pick(select_warp_kernel<2>);
+        return pick(select_warp_kernel<4>);
+    }
+    if (aligned) {
+        constexpr int CT = 256, CHUNK = 4096, STAGES = 4;
+        int cap, limit;
+        if (N <= CHUNK) {
+            cap = (int)round_up(N, 32);
+            limit = INT_MAX;
+        } else {
+            limit = (int)round_up(k + 256 > 2 * k ? k + 256 : 2 * k, 32);
+            cap = CHUNK + limit;
+        }
+        const size_t smem = (size_t)STAGES * CHUNK * 4 + 2 * STAGES * 8 +
+                            (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
+        auto kern = select_ring_kernel<CT, CHUNK, STAGES>;
+        if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
+        int per_sm = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT + 32, smem)) != cudaSuccess)
+            return e;
+        int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+        if (grid > M) grid = M;
+        kern<<<(unsigned)grid, CT + 32, smem, s>>>(D, M, N, ldD, k, cap, KP, limit, idx_offset,
+                                                  out_idx, out_dist);
+        return cudaGetLastError();
+    }
+    constexpr int THREADS = 256, VPT = 4, CHUNK = THREADS * VPT * 4;
     int cap, limit;
     if (N <= CHUNK) {  // whole row fits: no rebuild during the stream
         cap = (int)round_up(N, 32);
         limit = INT_MAX;
     } else {
-        cap = CHUNK + (int)round_up(k > CHUNK ? k : CHUNK, 32);
-        limit = cap - CHUNK;
+        // Rebuild as soon as more than max(2k, k + 256) candidates are buffered: the
+        // first chunk (accepted whole) sets the threshold right away, after which a
+        // random-order row adds ~k ln(N/CHUNK) survivors in total.
+        limit = (int)round_up(k + 256 > 2 * k ? k + 256 : 2 * k, 32);
+        cap = CHUNK + limit;
     }
     const size_t smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
-    const bool vec = (ldD % 4 == 0) && ((reinterpret_cast<uintptr_t>(D) & 15) == 0);
-    cudaError_t e;
-    if (vec) {
-        auto kern = select_rows_kernel<THREADS, VPT, true>;
-        if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
-        kern<<<(unsigned)M, THREADS, smem, s>>>(D, N, ldD, k, cap, KP, limit, idx_offset, out_idx,
-                                               out_dist);
-    } else {
-        auto kern = select_rows_kernel<THREADS, VPT, false>;
-        if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
-        kern<<<(unsigned)M, THREADS, smem, s>>>(D, N, ldD, k, cap, KP, limit, idx_offset, out_idx,
-                                               out_dist);
-    }
+    auto kern = select_rows_kernel<THREADS, VPT, false>;
+    if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
+    kern<<<(unsigned)M, THREADS, smem, s>>>(D, N, ldD, k, cap, KP, limit, idx_offset, out_idx,
+                                           out_dist);
     return cudaGetLastError();
 }
 

@@ -141,3 +141,36 @@ def test_merge_of_column_shards_equals_unsharded_select():
     got = knn().merge(torch.from_numpy(np.stack(pd)).cuda(), torch.from_numpy(np.stack(pi)).cuda(),
                       bounds[:-1])
     assert_same([t.cpu().numpy() for t in got], oracle.select_f32(D, k))
+
+
+# ------------------------------------------------------------------ warp-per-row path --
+# knn_select runs one warp per row when k <= 128 and there are >= 4 rows per SM
+# (M >= 592 on B200); these cover that plan with ragged rows and adversarial keys.
+@pytest.mark.parametrize("N", [1, 33, 1000, 1024, 1025, 4097, 20000])
+@pytest.mark.parametrize("k", [1, 31, 32, 33, 64, 65, 128])
+def test_warp_select_uniform(N, k):
+    if k > N:
+        pytest.skip("k > N")
+    D = datagen.keys(700, N, "uniform", seed=N * 13 + k)
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("kind", ["dup256", "descending", "ascending", "equal"])
+@pytest.mark.parametrize("k", [1, 32, 100, 128])
+def test_warp_select_adversarial(kind, k):
+    D = datagen.keys(640, 5000, kind, seed=21)
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+def test_warp_select_special_values():
+    g = np.random.Generator(np.random.Philox(23))
+    D = g.standard_normal((800, 3000)).astype(np.float32)
+    D[:, ::7] = 0.0
+    D[:, 3::7] = -0.0
+    D[:, 5::11] = np.inf
+    D[:, 6::13] = -np.inf
+    D[:, 2::17] = np.nan
+    D[::3, :] = np.inf  # rows with few / no finite keys
+    D[::3, :5] = 1.0
+    for k in (1, 17, 128):
+        assert_same(gpu_select(D, k), oracle.select_f32(D, k))
