@@ -15,6 +15,7 @@
 //    the TF32 tensor rate, so this costs what 1.5 TF32 passes would (vs 3 for 3xTF32).
 //  * Warp-specialised persistent kernel, one CTA per SM, 6 warps:
 //      warp 0  TMA producer: per K-block loads qh, ql (BM×BK) and xh, xl (BN×BK) tiles,
+//              (the xh, xl halves multicast across the CTA pair of the cluster),
 //              swizzled K-major, into a STAGES-deep ring (each stage feeds 3 MMA
 //              segments, so the hi tiles are loaded once and used twice);
 //      warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16);
@@ -32,6 +33,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 namespace knn {
@@ -39,8 +41,9 @@ namespace {
 
 constexpr int BM = 128;          // rows per tile (TMEM lanes)
 constexpr int BN = 256;          // columns per tile (TMEM columns per accumulator)
-constexpr int BK = 64;           // fp16 K elements per stage = one 128-byte swizzle row
-constexpr int STAGES = 2;
+constexpr int BK = 32;           // fp16 K elements per stage = one 64-byte swizzle row
+constexpr int SWZ = BK * 2;      // swizzle span in bytes (64)
+constexpr int STAGES = 3;
 constexpr int UMMA_K = 16;
 constexpr int EPI_WARPS = 8;     // 2 per TMEM lane quadrant, each owning BN/2 columns
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
@@ -48,8 +51,11 @@ constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (16 KB)
 constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (32 KB)
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands
 constexpr int TMEM_COLS = 512;   // 2 accumulators × BN fp32 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/;
-constexpr int GROUP_M = 16;      // tile-order swizzle: 16 row blocks share a column sweep
+constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 output chunk (TMA-store staging)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 1024 /*align*/ +
+                           1024 /*barriers*/;
+constexpr int GROUP_M = 8;       // tile-order swizzle: 8 row-block pairs share a column sweep
+constexpr int CLUSTER = 2;       // CTA pair along M: the B operand is TMA-multicast to both
 
 // Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
 // [4,6) D format = F32 (1); [7,10) A = F16 (0); [10,13) B = F16 (0); bit 15/16 = 0:
@@ -64,6 +70,48 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
+// Multicast variant: the box lands at the same smem offset in every CTA of ctaMask and
+// completes tx bytes on the mbarrier at the same offset in each of them.
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+// Commit this CTA's prior MMAs to the mbarrier at `bar` in every CTA of ctaMask.
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(src)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -76,13 +124,15 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
-// Shared-memory matrix descriptor, K-major, 128-byte swizzle (PTX ISA "Matrix
+// Shared-memory matrix descriptor, K-major, SWZ-byte swizzle (PTX ISA "Matrix
 // descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
-// [32,46) SBO>>4 = 1024 B between 8-row core-matrix groups; [46,48) version = 1;
-// [49,52) base offset = 0 (tiles are 1024-aligned); [61,64) layout = 2 (SWIZZLE_128B).
+// [32,46) SBO>>4 = 8 rows * SWZ bytes between 8-row core-matrix groups; [46,48)
+// version = 1; [49,52) base offset = 0 (tiles are 1024-aligned); [61,64) layout:
+// 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B.
+constexpr uint64_t SDESC_LAYOUT = SWZ == 128 ? 2 : SWZ == 64 ? 4 : 6;
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) |
+           ((uint64_t)((8 * SWZ) >> 4) << 32) | ((uint64_t)1 << 46) | (SDESC_LAYOUT << 61);
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -102,15 +152,18 @@ __device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, floa
                  : "memory");
 }
 
+// Work unit of a 2-CTA cluster: a pair of row blocks (2*mp, 2*mp+1) against one column
+// block nb; CTA rank r of the pair computes row block 2*mp + r.  Units are ordered in
+// groups of GROUP_M pairs sweeping all column blocks (L2 reuse of the B panel).
 struct TileMap {
-    int64_t n_mb, n_nb;
-    __device__ __forceinline__ void get(int64_t t, int64_t& mb, int64_t& nb) const {
+    int64_t n_mp, n_nb;  // row-block pairs, column blocks
+    __device__ __forceinline__ void get(int64_t t, int64_t& mp, int64_t& nb) const {
         const int64_t per_group = (int64_t)GROUP_M * n_nb;
         const int64_t g = t / per_group;
         const int64_t r = t - g * per_group;
         const int64_t m0 = g * GROUP_M;
-        const int64_t gm = (n_mb - m0) < GROUP_M ? (n_mb - m0) : GROUP_M;
-        mb = m0 + r % gm;
+        const int64_t gm = (n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M;
+        mp = m0 + r % gm;
         nb = r / gm;
     }
 };
@@ -122,16 +175,18 @@ struct EpiArgs {
 };
 
 template <int METRIC>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
-               int num_kb, TileMap tiles, int64_t num_tiles, EpiArgs ep) {
+               const __grid_constant__ CUtensorMap map_d, int use_tma_store, int num_kb,
+               TileMap tiles, int64_t num_tiles, EpiArgs ep) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
     __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* stage_base = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + EPI_WARPS * 2 * STG_BYTES);
     // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
@@ -142,7 +197,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, CLUSTER);  // both CTAs' MMAs must release a stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
@@ -161,28 +216,32 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // barriers of both CTAs initialised before any multicast
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t crank = cluster_rank();
+    const int64_t cid = blockIdx.x / CLUSTER, ncl = gridDim.x / CLUSTER;
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer --------
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-                int64_t mb, nb;
-                tiles.get(t, mb, nb);
-                const int row_a = (int)(mb * BM), row_b = (int)(nb * BN);
+            for (int64_t t = cid; t < num_tiles; t += ncl) {
+                int64_t mp, nb;
+                tiles.get(t, mp, nb);
+                const int row_a = (int)((2 * mp + crank) * BM);
+                const int row_b = (int)(nb * BN + crank * (BN / 2));  // this CTA's half of B
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t fb = full0 + 8 * stage;
                     mbar_expect_tx(fb, STAGE_BYTES);
                     const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                    const uint32_t boff = crank * (B_BYTES / 2);
                     tma_load_2d(sb, &map_qh, fb, kb * BK, row_a);
                     tma_load_2d(sb + A_BYTES, &map_ql, fb, kb * BK, row_a);
-                    tma_load_2d(sb + 2 * A_BYTES, &map_xh, fb, kb * BK, row_b);
-                    tma_load_2d(sb + 2 * A_BYTES + B_BYTES, &map_xl, fb, kb * BK, row_b);
+                    tma_load_2d_mc(sb + 2 * A_BYTES + boff, &map_xh, fb, kb * BK, row_b, 0x3);
+                    tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + boff, &map_xl, fb, kb * BK, row_b, 0x3);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -197,7 +256,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+            for (int64_t t = cid; t < num_tiles; t += ncl, ++it) {
                 const int buf = it & 1;
                 const uint32_t tphase = (it >> 1) & 1;
                 mbar_wait(tempty0 + 8 * buf, tphase ^ 1);
@@ -221,7 +280,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                                    sdesc(sbx[seg] + kk * UMMA_K * 2), acc);
                         }
                     }
-                    tc_commit(empty0 + 8 * stage);  // frees the smem stage when MMAs finish
+                    // frees the smem stage (in both CTAs: B halves were multicast) when done
+                    tc_commit_mc(empty0 + 8 * stage, 0x3);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -237,10 +297,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         const int half = (warp - 2) >> 2;           // which BN/2 columns it owns
         const int etid = threadIdx.x - 64;          // 0..255
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
+        int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
-        for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-            int64_t mb, nb;
-            tiles.get(t, mb, nb);
+        for (int64_t t = cid; t < num_tiles; t += ncl, ++it) {
+            int64_t mp, nb;
+            tiles.get(t, mp, nb);
+            const int64_t mb = 2 * mp + crank;
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
@@ -300,6 +362,26 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     for (int c = 0; c < 32; ++c)
                         if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
                 }
+                if (use_tma_store) {
+                    // stage the 32x32 chunk in 128B-swizzled smem (row = lane: 16-byte
+                    // unit u of the row lives at unit u ^ (row & 7)), then one TMA store;
+                    // rows >= M / columns >= N are clipped by the TMA unit.
+                    if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store read
+                    __syncwarp();
+                    const uint32_t sbuf = smem_u32(stg_base + ((warp - 2) * 2 + sbsel) * STG_BYTES);
+                    #pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        sts128(sbuf + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
+                               v[4 * u + 2], v[4 * u + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&map_d, sbuf, (int)c0, (int)row0);
+                        bulk_commit();
+                    }
+                    sbsel ^= 1;
+                    continue;
+                }
                 if (!row_ok) continue;
                 if (vec_ok && c0 + 32 <= ep.N) {
                     #pragma unroll
@@ -312,9 +394,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 }
             }
         }
+        if (use_tma_store && lane == 0) bulk_wait_all();
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -336,15 +419,30 @@ void init_encode() {
         cudaGetLastError();
 }
 
+// Output map: fp32 D (rows x N, row stride ldD), 32x32 boxes, 128B swizzle (the staging
+// layout of the epilogue).
+bool make_dmap(CUtensorMap* m, float* D, int64_t rows, int64_t N, int64_t ldD) {
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ldD * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)d_pad, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)d_pad * 2};
     cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle swz = SWZ == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : SWZ == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims,
-                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -367,16 +465,22 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     if (!g_encode) return cudaErrorNotSupported;
     CUtensorMap mqh, mql, mxh, mxl;
     if (!make_map(&mqh, op.q_hi, op.M, op.d_pad, BM) || !make_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
-        !make_map(&mxh, op.x_hi, op.N, op.d_pad, BN) || !make_map(&mxl, op.x_lo, op.N, op.d_pad, BN))
+        !make_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) || !make_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
-    TileMap tiles{ceil_div(op.M, BM), ceil_div(op.N, BN)};
-    const int64_t num_tiles = tiles.n_mb * tiles.n_nb;
-    const int grid = (int)(num_tiles < num_sms ? num_tiles : num_sms);
+    TileMap tiles{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+    const int64_t num_tiles = tiles.n_mp * tiles.n_nb;  // work units per CTA pair
+    const int64_t pairs = num_tiles < num_sms / CLUSTER ? num_tiles : num_sms / CLUSTER;
+    const int grid = (int)(pairs * CLUSTER);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD};
     auto kern = metric == 1 ? dist_tc_kernel<1> : dist_tc_kernel<0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    kern<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, op.d_pad / BK, tiles, num_tiles, ep);
+    CUtensorMap md;
+    const bool tma_store = (ldD % 4) == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0 &&
+                           make_dmap(&md, D, op.M, op.N, ldD);
+    if (!tma_store) memset(&md, 0, sizeof md);
+    kern<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, tma_store ? 1 : 0, op.d_pad / BK,
+                                           tiles, num_tiles, ep);
     return cudaGetLastError();
 }
 
