@@ -67,6 +67,8 @@ def graph_query_sharded(X, k, metric=0, group=None, compute=None, broadcast=True
     N = X.shape[0]
     if broadcast and G > 1:
         broadcast_points(X, group)
+    if G == 1:
+        return compute(X, X, k, metric, 0, 0)
     per = -(-N // G)
     lo, hi = block_range(N, G, r)
     out_i = torch.zeros((per, k), dtype=torch.int32, device=X.device)
@@ -75,8 +77,6 @@ def graph_query_sharded(X, k, metric=0, group=None, compute=None, broadcast=True
         i, d = compute(X[lo:hi], X, k, metric, lo, 0)  # self pair: column lo + i
         out_i[: hi - lo] = i
         out_d[: hi - lo] = d
-    if G == 1:
-        return out_i[:N], out_d[:N]
     all_i = torch.empty((G * per, k), dtype=torch.int32, device=X.device)
     all_d = torch.empty((G * per, k), dtype=torch.float32, device=X.device)
     dist.all_gather_into_tensor(all_i, out_i, group=group)
