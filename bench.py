@@ -276,6 +276,17 @@ def run_ours(args):
                 "achieved": sel_bytes / (sel_avg * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "avg_launch_ms": sel_avg, "traffic": None}
     sel_roof["frac"] = sel_roof["achieved"] / sel_roof["peak"]
+    # DRAM traffic per launch from the committed ncu capture (profiles/traffic.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        gemm_roof["traffic"] = tr.get("dist_tc_kernel")
+        sel_roof["traffic"] = tr.get("select_warp_kernel")
+        gemm_roof["traffic_source"] = sel_roof["traffic_source"] = tr.get("_source")
+    except Exception:
+        pass
+    gemm_roof["algorithmic_bytes"] = rows_per_gemm * (-(-N // 4) * 4) * 4.0 + (rows_per_gemm + N) * d_pad * 4.0
+    sel_roof["algorithmic_bytes"] = sel_bytes
     dominant, other = (gemm_roof, sel_roof) if g_ms >= s_ms else (sel_roof, gemm_roof)
     roofline = dict(dominant)
     roofline["other"] = other

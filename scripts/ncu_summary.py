@@ -38,3 +38,19 @@ def summarise(path):
 if __name__ == "__main__":
     for p in sys.argv[1:]:
         print(summarise(p))
+
+
+def traffic(path):
+    """{kernel base name: dram read+write bytes per launch} from one report."""
+    raw = subprocess.check_output(["ncu", "-i", path, "--page", "raw", "--csv"], text=True)
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    out = {}
+    for vals in rows[2:]:
+        d = dict(zip(hdr, vals))
+        u = dict(zip(hdr, units))
+        name = re.sub(r"^void ", "", d["Kernel Name"]).split("(")[0].split("::")[-1].split("<")[0]
+        tot = sum(float(d[m]) * scale[u[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        out[name] = tot
+    return out
