@@ -12,7 +12,7 @@ ORACLE    := oracle/liboracle.so
 
 all: $(LIB) $(ORACLE)
 
-$(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/internal.cuh $(SRC_DIR)/ptx.cuh include/knn.h
+$(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/internal.cuh $(SRC_DIR)/ptx.cuh $(SRC_DIR)/tc_common.cuh $(SRC_DIR)/warpsel.cuh include/knn.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; exit 1)
 

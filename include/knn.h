@@ -150,13 +150,17 @@ int64_t knn_launch_count(knn_ctx_t ctx);
  * (gemm_tc.cu), 1 = SIMT FP32 FFMA (gemm_simt.cu; selected by env KNN_GEMM=simt at
  * ctx creation, or when the device is not sm_100). */
 int knn_gemm_path(knn_ctx_t ctx);
+/* Whether the top-level calls use the fused GEMM+select plan (fused.cu; the distance
+ * matrix never reaches HBM) for this k: tensor-core path, k <= 32, and env KNN_FUSED
+ * not "0" at ctx creation.  Results are bit-identical to the materialised plan. */
+int knn_fused_plan(knn_ctx_t ctx, int32_t k);
 
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by
  * CUDA events recorded on the launch stream.  knn_profile_enable(ctx, 1) also resets
  * the counters.  knn_profile_read waits for the recorded events and returns the summed
  * duration (ms) and the launch count of one kernel class. */
 typedef enum { KNN_KERNEL_PREP = 0, KNN_KERNEL_GEMM = 1, KNN_KERNEL_SELECT = 2,
-               KNN_KERNEL_MERGE = 3 } knn_kernel;
+               KNN_KERNEL_MERGE = 3, KNN_KERNEL_FUSED = 4 } knn_kernel;
 knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on);
 knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches);
 

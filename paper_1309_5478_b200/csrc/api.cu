@@ -31,8 +31,9 @@ struct knn_ctx {
     std::vector<cudaEvent_t> ev_pool;
     struct Pending { int kind; cudaEvent_t a, b; };
     std::vector<Pending> pending;
-    double prof_ms[4] = {0, 0, 0, 0};
-    int64_t prof_n[4] = {0, 0, 0, 0};
+    bool fused_ok = true;  // env KNN_FUSED=0 disables the fused plan
+    double prof_ms[5] = {0, 0, 0, 0, 0};
+    int64_t prof_n[5] = {0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -176,11 +177,14 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                      int32_t* out_idx, float* out_dist, cudaStream_t s) {
     const bool same = (Q == X) && (M == N);
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
+    const bool fused = knn_fused_plan(ctx, k) == 1;
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
     const int64_t ldD = round_up(N, 4);
     int64_t rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldD * sizeof(float)));
     rows_blk = rows_blk < 128 ? 128 : (rows_blk / 128) * 128;
     if (rows_blk > M) rows_blk = M;
+    const int S = fused ? (int)knn::fused_actual_splits(N, knn::fused_splits(M, N, ctx->num_sms)) : 1;
+    if (fused) rows_blk = 0;  // no distance block
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -198,10 +202,19 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     Prepared pq{}, px{};
     float* D = nullptr;
     int32_t* flag = nullptr;
-    layout(probe, pq, px, D, flag);
+    int32_t* part_i = nullptr;
+    float* part_d = nullptr;
+    auto layout_all = [&](Carve& c) {
+        layout(c, pq, px, D, flag);
+        if (fused && S > 1) {
+            part_i = c.take<int32_t>((size_t)S * M * k);
+            part_d = c.take<float>((size_t)S * M * k);
+        }
+    };
+    layout_all(probe);
     KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
     Carve carve{static_cast<char*>(ctx->ws)};
-    layout(carve, pq, px, D, flag);
+    layout_all(carve);
 
     KNN_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     {
@@ -213,6 +226,21 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         Timed t(ctx, KNN_KERNEL_PREP, s);
         KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
         t.done();
+    }
+    if (fused) {
+        knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        Timed tf(ctx, KNN_KERNEL_FUSED, s);
+        KNN_CUDA(knn::launch_knn_fused(op, metric, self_shift, k, idx_offset, S,
+                                       S > 1 ? part_i : out_idx, S > 1 ? part_d : out_dist,
+                                       ctx->num_sms, s));
+        tf.done();
+        if (S > 1) {
+            int64_t zeros[64] = {0};
+            Timed tm(ctx, KNN_KERNEL_MERGE, s);
+            KNN_CUDA(knn::launch_merge(part_d, part_i, S, M, k, zeros, out_idx, out_dist, s));
+            tm.done();
+        }
+        return KNN_OK;
     }
     for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
         const int64_t R = (M - r0) < rows_blk ? (M - r0) : rows_blk;
@@ -287,6 +315,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     c->tc_ok = knn::tc_supported();
     const char* g = getenv("KNN_GEMM");
     if (g && strcmp(g, "simt") == 0) c->gemm_mode = 1;
+    const char* fz = getenv("KNN_FUSED");
+    if (fz && strcmp(fz, "0") == 0) c->fused_ok = false;
     const char* b = getenv("KNN_D_BUDGET_MB");
     if (b) c->d_budget = (size_t)atoll(b) << 20;
     if (cudaMallocHost(&c->flag_host, sizeof(int32_t)) != cudaSuccess) {
@@ -314,6 +344,11 @@ const char* knn_last_error(knn_ctx_t ctx) { return ctx ? ctx->err.c_str() : "nul
 
 int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
+int knn_fused_plan(knn_ctx_t ctx, int32_t k) {
+    if (!ctx) return -1;
+    return (ctx->gemm_mode == 0 && ctx->tc_ok && ctx->fused_ok && k >= 1 && k <= knn::fused_max_k()) ? 1 : 0;
+}
+
 int knn_gemm_path(knn_ctx_t ctx) {
     if (!ctx) return -1;
     return (ctx->gemm_mode == 0 && ctx->tc_ok) ? 0 : 1;
@@ -323,7 +358,7 @@ knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on) {
     if (!ctx) return KNN_ERR_ARG;
     cudaSetDevice(ctx->device);
     drain_profile(ctx);
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
         ctx->prof_ms[i] = 0;
         ctx->prof_n[i] = 0;
     }
@@ -332,7 +367,7 @@ knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on) {
 }
 
 knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches) {
-    if (!ctx || kernel < 0 || kernel > 3 || !total_ms || !launches) return KNN_ERR_ARG;
+    if (!ctx || kernel < 0 || kernel > 4 || !total_ms || !launches) return KNN_ERR_ARG;
     cudaSetDevice(ctx->device);
     drain_profile(ctx);
     *total_ms = ctx->prof_ms[kernel];

@@ -27,10 +27,8 @@
 //  * Epilogue (per element): acc*(-2 rs_q) is exact (power-of-two scale), so
 //      D = max(fma(acc * (-2 rs_q), rs_x, ||q||^2 + ||x||^2), 0) + 0
 //    rounds once; +0 canonicalises -0 (R6); sqrt for L2; +inf on the excluded self pair.
-#include "internal.cuh"
-#include "ptx.cuh"
+#include "tc_common.cuh"
 
-#include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <cstring>
@@ -39,134 +37,14 @@
 namespace knn {
 namespace {
 
-constexpr int BM = 128;          // rows per tile (TMEM lanes)
-constexpr int BN = 256;          // columns per tile (TMEM columns per accumulator)
-constexpr int BK = 32;           // fp16 K elements per stage = one 64-byte swizzle row
-constexpr int SWZ = BK * 2;      // swizzle span in bytes (64)
+using namespace tc;
+
 constexpr int STAGES = 3;
-constexpr int UMMA_K = 16;
 constexpr int EPI_WARPS = 8;     // 2 per TMEM lane quadrant, each owning BN/2 columns
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
-constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (16 KB)
-constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (32 KB)
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands
-constexpr int TMEM_COLS = 512;   // 2 accumulators × BN fp32 columns
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 output chunk (TMA-store staging)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 1024 /*align*/ +
                            1024 /*barriers*/;
-constexpr int GROUP_M = 8;       // tile-order swizzle: 8 row-block pairs share a column sweep
-constexpr int CLUSTER = 2;       // CTA pair along M: the B operand is TMA-multicast to both
-
-// Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
-// [4,6) D format = F32 (1); [7,10) A = F16 (0); [10,13) B = F16 (0); bit 15/16 = 0:
-// both K-major; [17,23) N>>3; [24,29) M>>4.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                            int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-        : "memory");
-}
-// Multicast variant: the box lands at the same smem offset in every CTA of ctaMask and
-// completes tx bytes on the mbarrier at the same offset in each of them.
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                               int c0, int c1, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
-        : "memory");
-}
-// Commit this CTA's prior MMAs to the mbarrier at `bar` in every CTA of ctaMask.
-__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(bar), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-            reinterpret_cast<uint64_t>(map)),
-        "r"(c0), "r"(c1), "r"(src)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
-    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
-}
-// Shared-memory matrix descriptor, K-major, SWZ-byte swizzle (PTX ISA "Matrix
-// descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
-// [32,46) SBO>>4 = 8 rows * SWZ bytes between 8-row core-matrix groups; [46,48)
-// version = 1; [49,52) base offset = 0 (tiles are 1024-aligned); [61,64) layout:
-// 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B.
-constexpr uint64_t SDESC_LAYOUT = SWZ == 128 ? 2 : SWZ == 64 ? 4 : 6;
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) |
-           ((uint64_t)((8 * SWZ) >> 4) << 32) | ((uint64_t)1 << 46) | (SDESC_LAYOUT << 61);
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
-                 "f"(d)
-                 : "memory");
-}
-
-// Work unit of a 2-CTA cluster: a pair of row blocks (2*mp, 2*mp+1) against one column
-// block nb; CTA rank r of the pair computes row block 2*mp + r.  Units are ordered in
-// groups of GROUP_M pairs sweeping all column blocks (L2 reuse of the B panel).
-struct TileMap {
-    int64_t n_mp, n_nb;  // row-block pairs, column blocks
-    __device__ __forceinline__ void get(int64_t t, int64_t& mp, int64_t& nb) const {
-        const int64_t per_group = (int64_t)GROUP_M * n_nb;
-        const int64_t g = t / per_group;
-        const int64_t r = t - g * per_group;
-        const int64_t m0 = g * GROUP_M;
-        const int64_t gm = (n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M;
-        mp = m0 + r % gm;
-        nb = r / gm;
-    }
-};
 
 struct EpiArgs {
     const float* qn; const float* q_rs; int64_t M;
@@ -179,7 +57,7 @@ __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                const __grid_constant__ CUtensorMap map_d, int use_tma_store, int num_kb,
-               TileMap tiles, int64_t num_tiles, EpiArgs ep) {
+               TileSched sched, EpiArgs ep) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
     __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
@@ -187,109 +65,23 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     uint8_t* stage_base = smem;
     uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
     uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + EPI_WARPS * 2 * STG_BYTES);
-    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    const Bars b{smem_u32(bars), smem_u32(bars + STAGES), smem_u32(bars + 2 * STAGES),
+                 smem_u32(bars + 2 * STAGES + 2)};
+    const uint32_t tfull0 = b.tfull0, tempty0 = b.tempty0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
-    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
-
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, CLUSTER);  // both CTAs' MMAs must release a stage
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, EPI_WARPS);  // one arrive per epilogue warp
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qh)));
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ql)));
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_xh)));
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_xl)));
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    cluster_sync_all();  // barriers of both CTAs initialised before any multicast
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = setup(bars, STAGES, EPI_WARPS, tmem_slot, &map_qh, 1);
     const uint32_t crank = cluster_rank();
     const int64_t cid = blockIdx.x / CLUSTER, ncl = gridDim.x / CLUSTER;
 
     if (warp == 0) {
-        // ------------------------------------------------------ TMA producer --------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t t = cid; t < num_tiles; t += ncl) {
-                int64_t mp, nb;
-                tiles.get(t, mp, nb);
-                const int row_a = (int)((2 * mp + crank) * BM);
-                const int row_b = (int)(nb * BN + crank * (BN / 2));  // this CTA's half of B
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
-                    const uint32_t fb = full0 + 8 * stage;
-                    mbar_expect_tx(fb, STAGE_BYTES);
-                    const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
-                    const uint32_t boff = crank * (B_BYTES / 2);
-                    tma_load_2d(sb, &map_qh, fb, kb * BK, row_a);
-                    tma_load_2d(sb + A_BYTES, &map_ql, fb, kb * BK, row_a);
-                    tma_load_2d_mc(sb + 2 * A_BYTES + boff, &map_xh, fb, kb * BK, row_b, 0x3);
-                    tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + boff, &map_xl, fb, kb * BK, row_b, 0x3);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
+        if (lane == 0)
+            producer_loop<STAGES>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched, num_kb,
+                                  crank, cid, ncl);
         __syncwarp();
     } else if (warp == 1) {
-        // ------------------------------------------------------ MMA issuer ----------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            for (int64_t t = cid; t < num_tiles; t += ncl, ++it) {
-                const int buf = it & 1;
-                const uint32_t tphase = (it >> 1) & 1;
-                mbar_wait(tempty0 + 8 * buf, tphase ^ 1);
-                tc_fence_after();
-                const uint32_t tmem_d = tmem_base + buf * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    mbar_wait(full0 + 8 * stage, phase);
-                    tc_fence_after();
-                    const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
-                    const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + 2 * A_BYTES,
-                                   xl = sb + 2 * A_BYTES + B_BYTES;
-                    // three K-segments, smallest terms first: ql.xh, qh.xl, qh.xh
-                    const uint32_t sa[3] = {ql, qh, qh};
-                    const uint32_t sbx[3] = {xh, xl, xh};
-                    #pragma unroll
-                    for (int seg = 0; seg < 3; ++seg) {
-                        #pragma unroll
-                        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                            const uint32_t acc = (kb | seg | kk) != 0;
-                            tc_mma(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2),
-                                   sdesc(sbx[seg] + kk * UMMA_K * 2), acc);
-                        }
-                    }
-                    // frees the smem stage (in both CTAs: B halves were multicast) when done
-                    tc_commit_mc(empty0 + 8 * stage, 0x3);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-                tc_commit(tfull0 + 8 * buf);  // accumulator ready for the epilogue
-            }
-        }
+        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl);
         __syncwarp();
     } else {
         // ------------------------------------------------------ epilogue (8 warps) --
@@ -299,10 +91,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
-        for (int64_t t = cid; t < num_tiles; t += ncl, ++it) {
-            int64_t mp, nb;
-            tiles.get(t, mp, nb);
-            const int64_t mb = 2 * mp + crank;
+        for (int64_t t = cid; t < sched.units(); t += ncl, ++it) {
+            const tc::Unit w = sched.get(t);
+            const int64_t nb = w.nb0;
+            const int64_t mb = 2 * w.mp + crank;
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
@@ -396,13 +188,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
     }
-    tc_fence_before();
-    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(TMEM_COLS));
-    }
+    teardown(tmem_base);
 }
 
 // ------------------------------------------------------------ host side -------------
@@ -419,9 +205,13 @@ void init_encode() {
         cudaGetLastError();
 }
 
+}  // namespace
+
 // Output map: fp32 D (rows x N, row stride ldD), 32x32 boxes, 128B swizzle (the staging
 // layout of the epilogue).
-bool make_dmap(CUtensorMap* m, float* D, int64_t rows, int64_t N, int64_t ldD) {
+bool tc_make_output_map(CUtensorMap* m, float* D, int64_t rows, int64_t N, int64_t ldD) {
+    std::call_once(g_once, init_encode);
+    if (!g_encode) return false;
     cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ldD * 4};
     cuuint32_t box[2] = {32, 32};
@@ -432,7 +222,9 @@ bool make_dmap(CUtensorMap* m, float* D, int64_t rows, int64_t N, int64_t ldD) {
     return r == CUDA_SUCCESS;
 }
 
-bool make_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, int box_rows) {
+bool tc_make_operand_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, int box_rows) {
+    std::call_once(g_once, init_encode);
+    if (!g_encode) return false;
     cuuint64_t dims[2] = {(cuuint64_t)d_pad, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)d_pad * 2};
     cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
@@ -445,8 +237,6 @@ bool make_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, i
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
-
-}  // namespace
 
 bool tc_supported() {
     std::call_once(g_once, init_encode);
@@ -464,10 +254,12 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     std::call_once(g_once, init_encode);
     if (!g_encode) return cudaErrorNotSupported;
     CUtensorMap mqh, mql, mxh, mxl;
-    if (!make_map(&mqh, op.q_hi, op.M, op.d_pad, BM) || !make_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
-        !make_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) || !make_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
-    TileMap tiles{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+    TileSched tiles{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
     const int64_t num_tiles = tiles.n_mp * tiles.n_nb;  // work units per CTA pair
     const int64_t pairs = num_tiles < num_sms / CLUSTER ? num_tiles : num_sms / CLUSTER;
     const int grid = (int)(pairs * CLUSTER);
@@ -477,10 +269,10 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     if (e != cudaSuccess) return e;
     CUtensorMap md;
     const bool tma_store = (ldD % 4) == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0 &&
-                           make_dmap(&md, D, op.M, op.N, ldD);
+                           tc_make_output_map(&md, D, op.M, op.N, ldD);
     if (!tma_store) memset(&md, 0, sizeof md);
     kern<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, tma_store ? 1 : 0, op.d_pad / BK,
-                                           tiles, num_tiles, ep);
+                                           tiles, ep);
     return cudaGetLastError();
 }
 

@@ -50,6 +50,18 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
                            int64_t ldD, int num_sms, cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
+// fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial
+// lists [S][M][k] (final lists when S == 1).
+int fused_max_k();
+int fused_splits(int64_t M, int64_t N, int num_sms);  // requested S
+inline int64_t fused_actual_splits(int64_t N, int S) {
+    const int64_t n_nb = ceil_div(N, 256);
+    return ceil_div(n_nb, ceil_div(n_nb, S));
+}
+cudaError_t launch_knn_fused(const TcOperands& op, int32_t metric, int64_t self_shift, int32_t k,
+                             int64_t idx_offset, int S, int32_t* out_idx, float* out_dist,
+                             int num_sms, cudaStream_t s);
+
 // select.cu
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
                           int64_t idx_offset, int32_t* out_idx, float* out_dist, cudaStream_t s);

@@ -1,0 +1,291 @@
+// tc_common.cuh — the shared tcgen05 mainloop of the distance GEMMs (materialised
+// gemm_tc.cu and fused fused.cu): tile constants, PTX wrappers, work schedulers, the TMA
+// producer loop and the single-thread MMA issuer loop.  See gemm_tc.cu for the design.
+#pragma once
+#include "internal.cuh"
+#include "ptx.cuh"
+
+#include <cuda.h>
+
+namespace knn {
+namespace tc {
+
+constexpr int BM = 128;          // rows per tile (TMEM lanes)
+constexpr int BN = 256;          // columns per tile (TMEM columns per accumulator)
+constexpr int BK = 32;           // fp16 K elements per stage = one 64-byte swizzle row
+constexpr int SWZ = BK * 2;      // swizzle span in bytes (64)
+constexpr int UMMA_K = 16;
+constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (8 KB)
+constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (16 KB)
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands (48 KB)
+constexpr int TMEM_COLS = 512;   // 2 accumulators x BN fp32 columns
+constexpr int CLUSTER = 2;       // CTA pair along M: the B operand is TMA-multicast to both
+constexpr int GROUP_M = 8;       // tile order: 8 row-block pairs share a column sweep
+
+// Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
+// [4,6) D format = F32 (1); [7,10) A = F16 (0); [10,13) B = F16 (0); bit 15/16 = 0:
+// both K-major; [17,23) N>>3; [24,29) M>>4.
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+// Multicast variant: the box lands at the same smem offset in every CTA of ctaMask and
+// completes tx bytes on the mbarrier at the same offset in each of them.
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+// Commit this CTA's prior MMAs to the mbarrier at `bar` in every CTA of ctaMask.
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(src)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+// Shared-memory matrix descriptor, K-major, SWZ-byte swizzle (PTX ISA "Matrix
+// descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
+// [32,46) SBO>>4 = 8 rows * SWZ bytes between 8-row core-matrix groups; [46,48)
+// version = 1; [49,52) base offset = 0 (tiles are 1024-aligned); [61,64) layout:
+// 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B.
+constexpr uint64_t SDESC_LAYOUT = SWZ == 128 ? 2 : SWZ == 64 ? 4 : 6;
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) |
+           ((uint64_t)((8 * SWZ) >> 4) << 32) | ((uint64_t)1 << 46) | (SDESC_LAYOUT << 61);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+
+// Work unit of a 2-CTA cluster: a pair of row blocks (2*mp, 2*mp+1) against one column
+// block nb; CTA rank r of the pair computes row block 2*mp + r.  Units are ordered in
+// groups of GROUP_M pairs sweeping all column blocks (L2 reuse of the B panel).
+
+// ------------------------------------------------------------------ schedulers -------
+// A work unit of a 2-CTA cluster: the row-block pair mp (CTA rank r computes row block
+// 2*mp + r) against column blocks [nb0, nb1).
+struct Unit {
+    int64_t mp, nb0, nb1;
+};
+
+// Materialised GEMM: one tile per unit, groups of GROUP_M pairs sweep all column blocks.
+struct TileSched {
+    int64_t n_mp, n_nb;
+    __device__ __forceinline__ int64_t units() const { return n_mp * n_nb; }
+    __device__ __forceinline__ Unit get(int64_t t) const {
+        const int64_t per_group = (int64_t)GROUP_M * n_nb;
+        const int64_t g = t / per_group;
+        const int64_t r = t - g * per_group;
+        const int64_t m0 = g * GROUP_M;
+        const int64_t gm = (n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M;
+        const int64_t nb = r / gm;
+        return {m0 + r % gm, nb, nb + 1};
+    }
+};
+
+// Fused GEMM+select: a unit is a row-block pair against one of S column splits; units of
+// the same split are consecutive so concurrent clusters sweep the same B panel.
+struct SplitSched {
+    int64_t n_mp, n_nb, S, per;  // per = column blocks per split
+    __device__ __forceinline__ int64_t units() const { return n_mp * S; }
+    __device__ __forceinline__ Unit get(int64_t u) const {
+        const int64_t s = u / n_mp;
+        const int64_t nb0 = s * per;
+        const int64_t nb1 = nb0 + per < n_nb ? nb0 + per : n_nb;
+        return {u % n_mp, nb0, nb1};
+    }
+};
+
+// ------------------------------------------------------------------ mainloop ---------
+// Barriers: full[s] (1 arrival + tx bytes), empty[s] (CLUSTER arrivals: both CTAs' MMAs),
+// tfull[2] (MMA commit), tempty[2] (one arrival per epilogue warp).
+struct Bars {
+    uint32_t full0, empty0, tfull0, tempty0;
+};
+
+// TMA producer (one elected thread): per K-block, the CTA's own qh/ql rows and its half of
+// the xh/xl rows multicast to both CTAs of the pair.
+template <int STAGES, class Sched>
+__device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const CUtensorMap* map_ql,
+                                              const CUtensorMap* map_xh, const CUtensorMap* map_xl,
+                                              uint8_t* stage_base, const Bars& b, const Sched& sched,
+                                              int num_kb, uint32_t crank, int64_t cid, int64_t ncl) {
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t u = cid; u < sched.units(); u += ncl) {
+        const Unit w = sched.get(u);
+        const int row_a = (int)((2 * w.mp + crank) * BM);
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb) {
+            const int row_b = (int)(nb * BN + crank * (BN / 2));  // this CTA's half of B
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(b.empty0 + 8 * stage, phase ^ 1);
+                const uint32_t fb = b.full0 + 8 * stage;
+                mbar_expect_tx(fb, STAGE_BYTES);
+                const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                const uint32_t boff = crank * (B_BYTES / 2);
+                tma_load_2d(sb, map_qh, fb, kb * BK, row_a);
+                tma_load_2d(sb + A_BYTES, map_ql, fb, kb * BK, row_a);
+                tma_load_2d_mc(sb + 2 * A_BYTES + boff, map_xh, fb, kb * BK, row_b, 0x3);
+                tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + boff, map_xl, fb, kb * BK, row_b, 0x3);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+}
+
+// Single-thread MMA issuer: per tile, waits for a free TMEM accumulator, then per K-block
+// issues the three split segments (ql.xh, qh.xl, qh.xh; smallest first) and frees the
+// stage in both CTAs; finally signals the epilogue.
+template <int STAGES, class Sched>
+__device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, const Sched& sched,
+                                         int num_kb, uint32_t tmem_base, int64_t cid, int64_t ncl) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t u = cid; u < sched.units(); u += ncl) {
+        const Unit w = sched.get(u);
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb, ++it) {
+            const int buf = it & 1;
+            const uint32_t tphase = (it >> 1) & 1;
+            mbar_wait(b.tempty0 + 8 * buf, tphase ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + buf * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(b.full0 + 8 * stage, phase);
+                tc_fence_after();
+                const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + 2 * A_BYTES,
+                               xl = sb + 2 * A_BYTES + B_BYTES;
+                const uint32_t sa[3] = {ql, qh, qh};
+                const uint32_t sbx[3] = {xh, xl, xh};
+                #pragma unroll
+                for (int seg = 0; seg < 3; ++seg) {
+                    #pragma unroll
+                    for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                        const uint32_t acc = (kb | seg | kk) != 0;
+                        tc_mma(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2), sdesc(sbx[seg] + kk * UMMA_K * 2),
+                               acc);
+                    }
+                }
+                tc_commit_mc(b.empty0 + 8 * stage, 0x3);  // stage free in both CTAs
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            tc_commit(b.tfull0 + 8 * buf);  // accumulator ready for the epilogue
+        }
+    }
+}
+
+// Barrier init (one thread), TMEM allocation (warp 1), cluster-wide sync.
+__device__ __forceinline__ uint32_t setup(uint64_t* bars, int stages, int epi_warps,
+                                         uint32_t* tmem_slot, const CUtensorMap* maps, int nmaps) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages);
+    const uint32_t tfull0 = smem_u32(bars + 2 * stages), tempty0 = smem_u32(bars + 2 * stages + 2);
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, CLUSTER);  // both CTAs' MMAs must release a stage
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, epi_warps);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < nmaps; ++i)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps + i)));
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // barriers of both CTAs initialised before any multicast
+    tc_fence_after();
+    return *tmem_slot;
+}
+
+__device__ __forceinline__ void teardown(uint32_t tmem_base) {
+    tc_fence_before();
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+    if ((threadIdx.x >> 5) == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS));
+    }
+}
+
+}  // namespace tc
+
+// host helpers (gemm_tc.cu)
+bool tc_make_operand_map(CUtensorMap* m, const __half* base, int64_t rows, int32_t d_pad, int box_rows);
+bool tc_make_output_map(CUtensorMap* m, float* D, int64_t rows, int64_t N, int64_t ldD);
+
+}  // namespace knn

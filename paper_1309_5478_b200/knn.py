@@ -27,8 +27,8 @@ STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_N
 SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
-           "knn_gemm_path", "knn_profile_enable", "knn_profile_read"]
-KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3}
+           "knn_gemm_path", "knn_fused_plan", "knn_profile_enable", "knn_profile_read"]
+KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
 
 class KnnError(RuntimeError):
@@ -74,6 +74,7 @@ def load_library():
             "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
+            "knn_fused_plan": (ctypes.c_int, [p, i32]),
             "knn_profile_enable": (st, [p, i32]),
             "knn_profile_read": (st, [p, i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_int64)]),
@@ -261,6 +262,11 @@ def launch_count(device=None):
 def gemm_path(device=None):
     """0 = tcgen05 split-fp16 tensor-core GEMM, 1 = SIMT FFMA."""
     return int(load_library().knn_gemm_path(context(device)))
+
+
+def fused_plan(k, device=None):
+    """1 if the top-level calls run the fused GEMM+select plan for this k."""
+    return int(load_library().knn_fused_plan(context(device), k))
 
 
 def profile_enable(on=True, device=None):

@@ -245,3 +245,48 @@ def test_simt_cross_check_path():
     env = dict(os.environ, KNN_GEMM="simt")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
+
+
+# ------------------------------------------------------------------ a-S5 fused -------
+# The fused GEMM+select (k <= 32) must equal knn_distances + knn_select (the
+# materialised building blocks) bit-for-bit: same distance expression, exact select.
+@pytest.mark.parametrize("M,N,d,k", [(300, 300, 3, 1), (1000, 1000, 64, 8), (2500, 2500, 33, 32),
+                                     (5000, 5000, 200, 31), (777, 4099, 128, 16)])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_fused_equals_materialised(M, N, d, k, metric):
+    kn = knn()
+    X = datagen.points(N, d, "clusters", seed=N + d)
+    Xt = cuda(X)
+    if M == N:
+        assert kn.fused_plan(k) == 1
+        gi, gd = kn.graph(Xt, k, metric=metric)
+        D = kn.distances(Xt, Xt, metric=metric, self_shift=0)
+    else:
+        Q = cuda(datagen.points(M, d, "gauss", seed=M))
+        gi, gd = kn.search_block(Q, Xt, k, metric=metric)
+        D = kn.distances(Q, Xt, metric=metric)
+    ri, rd = kn.select(D.contiguous(), k)
+    assert torch.equal(gi, ri)
+    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_fused_many_splits_long_rows():
+    # few query rows against a long corpus: the fused plan splits columns and merges
+    kn = knn()
+    Q = cuda(datagen.points(2000, 256, "uniform", seed=31))
+    X = cuda(datagen.points(65536, 256, "uniform", seed=32))
+    gi, gd = kn.search_block(Q, X, 32)
+    ri, rd = kn.select(kn.distances(Q, X).contiguous(), 32)
+    assert torch.equal(gi, ri) and torch.equal(gd, rd)
+
+
+def test_fused_self_shift_and_offsets():
+    kn = knn()
+    X = datagen.points(3000, 24, "gauss", seed=33)
+    Xt = cuda(X)
+    ref_i, ref_d = kn.graph(Xt, 20)
+    parts = [kn.search_block(Xt, Xt[a:b].contiguous(), 20, self_shift=-a, idx_offset=a)
+             for a, b in ((0, 1000), (1000, 2000), (2000, 3000))]
+    i, d = kn.merge(torch.stack([p[1] for p in parts]), torch.stack([p[0] for p in parts]),
+                    np.zeros(3, np.int64))
+    assert torch.equal(i, ref_i) and torch.equal(d, ref_d)
