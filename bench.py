@@ -34,6 +34,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="H", help="H (headline) or C1..C5")
+    ap.add_argument("--plan", default="auto", choices=["auto", "fused", "materialised"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -215,6 +216,8 @@ def run_ours(args):
             dist.barrier()
 
     assert knn.gemm_path() == 0 or os.environ.get("KNN_GEMM") == "simt", "tensor-core path expected"
+    knn.set_plan({"auto": knn.PLAN_AUTO, "fused": knn.PLAN_FUSED,
+                  "materialised": knn.PLAN_MATERIALISED}[args.plan])
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -239,7 +242,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
     launches = knn.launch_count() - launches0
-    prof = {kname: knn.profile_read(kname) for kname in ("prep", "gemm", "select")}
+    prof = {kname: knn.profile_read(kname) for kname in ("prep", "gemm", "select", "merge", "fused")}
     knn.profile_enable(False)
     clocks = sampler.stop()
 
@@ -252,46 +255,68 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (per-launch averages over the timed region)
     peaks = load_peaks()
-    R_local = sharded.block_range(N, world, rank)[1] - sharded.block_range(N, world, rank)[0]
+    lo_r, hi_r = sharded.block_range(N, world, rank)
+    R_local = hi_r - lo_r
     d_pad = -(-d // 64) * 64
-    g_ms, g_n = prof["gemm"]
-    s_ms, s_n = prof["select"]
-    p_ms, p_n = prof["prep"]
-    gemm_avg = g_ms / max(g_n, 1)
-    sel_avg = s_ms / max(s_n, 1)
-    gemm_launches_per_step = max(g_n // args.steps, 1)
-    rows_per_gemm = R_local / gemm_launches_per_step
-    # tensor work the split GEMM must issue: 3 fp16 products per multiply-add
-    tensor_flop = 3 * 2.0 * rows_per_gemm * N * d_pad
-    useful_flop = 2.0 * rows_per_gemm * N * d
-    sel_bytes = rows_per_gemm * (N * 4.0 + k * 8.0)  # read the rows + write k (idx, dist)
-    gemm_roof = {"kernel": "dist_tc_kernel (a-S3)", "bound": "tensor",
-                 "achieved": tensor_flop / (gemm_avg * 1e-3) / 1e12,
-                 "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                 "peak_kind": f"fp16 dense = bf16 {peaks['source']} sustained",
-                 "useful_tflops": useful_flop / (gemm_avg * 1e-3) / 1e12,
-                 "avg_launch_ms": gemm_avg, "traffic": None}
-    gemm_roof["frac"] = gemm_roof["achieved"] / gemm_roof["peak"]
-    sel_roof = {"kernel": "select_rows_kernel (a-S4)", "bound": "hbm",
-                "achieved": sel_bytes / (sel_avg * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "avg_launch_ms": sel_avg, "traffic": None}
-    sel_roof["frac"] = sel_roof["achieved"] / sel_roof["peak"]
-    # DRAM traffic per launch from the committed ncu capture (profiles/traffic.json)
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f)
-        gemm_roof["traffic"] = tr.get("dist_tc_kernel")
-        sel_roof["traffic"] = tr.get("select_warp_kernel")
-        gemm_roof["traffic_source"] = sel_roof["traffic_source"] = tr.get("_source")
+            traffic = json.load(f)
     except Exception:
-        pass
-    gemm_roof["algorithmic_bytes"] = rows_per_gemm * (-(-N // 4) * 4) * 4.0 + (rows_per_gemm + N) * d_pad * 4.0
-    sel_roof["algorithmic_bytes"] = sel_bytes
-    dominant, other = (gemm_roof, sel_roof) if g_ms >= s_ms else (sel_roof, gemm_roof)
-    roofline = dict(dominant)
-    roofline["other"] = other
-    roofline["step_share"] = {"gemm": g_ms / total_ms, "select": s_ms / total_ms,
+        traffic = {}
+
+    def tensor_roof(name, kernel, ms, n, rows_per_launch):
+        avg = ms / max(n, 1)
+        flop = 3 * 2.0 * rows_per_launch * N * d_pad  # 3 fp16 products per multiply-add
+        useful = 2.0 * rows_per_launch * N * d
+        r = {"kernel": name, "bound": "tensor", "achieved": flop / (avg * 1e-3) / 1e12,
+             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+             "peak_kind": f"fp16 dense = bf16 {peaks['source']} sustained",
+             "useful_tflops": useful / (avg * 1e-3) / 1e12, "avg_launch_ms": avg,
+             "launches": n, "traffic": traffic.get(kernel),
+             "traffic_source": traffic.get("_source")}
+        r["frac"] = r["achieved"] / r["peak"]
+        return r
+
+    def hbm_roof(name, kernel, ms, n, bytes_per_launch):
+        avg = ms / max(n, 1)
+        r = {"kernel": name, "bound": "hbm", "achieved": bytes_per_launch / (avg * 1e-3) / 1e9,
+             "peak": peaks["hbm_gbs"], "unit": "GB/s", "avg_launch_ms": avg, "launches": n,
+             "algorithmic_bytes": bytes_per_launch, "traffic": traffic.get(kernel),
+             "traffic_source": traffic.get("_source")}
+        r["frac"] = r["achieved"] / r["peak"]
+        return r
+
+    rooflines = []
+    f_ms, f_n = prof["fused"]
+    g_ms, g_n = prof["gemm"]
+    s_ms, s_n = prof["select"]
+    m_ms, m_n = prof["merge"]
+    p_ms, p_n = prof["prep"]
+    if f_n:
+        rooflines.append((f_ms, tensor_roof("knn_fused_kernel (a-S5: a-S3 GEMM + a-S4 select in the epilogue)",
+                                            "knn_fused_kernel", f_ms, f_n, R_local)))
+    if g_n:
+        gl = max(g_n // args.steps, 1)
+        rooflines.append((g_ms, tensor_roof("dist_tc_kernel (a-S3)", "dist_tc_kernel", g_ms, g_n, R_local / gl)))
+    if s_n:
+        sl = max(s_n // args.steps, 1)
+        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4)", "select_warp_kernel", s_ms, s_n,
+                                         R_local / sl * (N * 4.0 + k * 8.0))))
+    if m_n:
+        # partial lists per row merged (fused split-N, same rule as fused.cu's fused_splits)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        n_mp, n_nb, ncl = -(-(-(-R_local // 128)) // 2), -(-N // 256), sms // 2
+        best = min(range(1, min(8, n_nb) + 1), key=lambda S: (-(-n_mp * S // ncl)) * (-(-n_nb // S)) * 100 + S)
+        S = -(-n_nb // (-(-n_nb // best)))
+        rooflines.append((m_ms, hbm_roof("merge_kernel (a-S6)", "merge_kernel", m_ms, m_n,
+                                         R_local * k * 8.0 * (S + 1))))
+    rooflines.sort(key=lambda x: -x[0])
+    roofline = dict(rooflines[0][1])
+    roofline["others"] = [r for _, r in rooflines[1:]]
+    roofline["step_share"] = {"fused": f_ms / total_ms, "gemm": g_ms / total_ms,
+                              "select": s_ms / total_ms, "merge": m_ms / total_ms,
                               "prep": p_ms / total_ms}
+    roofline["plan"] = "fused GEMM+select" if f_n else "materialised distances + select"
 
     # ---- e2e: the public host-buffer API, H2D of the inputs and D2H of the results inside
     e2e = None
@@ -353,8 +378,7 @@ def run_ours(args):
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": launches,
-            "select_gbs": sel_roof["achieved"],
-            "gemm_useful_tflops": gemm_roof["useful_tflops"],
+            "plan": roofline["plan"],
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -150,9 +150,14 @@ int64_t knn_launch_count(knn_ctx_t ctx);
  * (gemm_tc.cu), 1 = SIMT FP32 FFMA (gemm_simt.cu; selected by env KNN_GEMM=simt at
  * ctx creation, or when the device is not sm_100). */
 int knn_gemm_path(knn_ctx_t ctx);
-/* Whether the top-level calls use the fused GEMM+select plan (fused.cu; the distance
- * matrix never reaches HBM) for this k: tensor-core path, k <= 32, and env KNN_FUSED
- * not "0" at ctx creation.  Results are bit-identical to the materialised plan. */
+/* Plan of the top-level calls: KNN_PLAN_AUTO (default; currently the materialised
+ * distances + select plan, which measures faster on B200), KNN_PLAN_FUSED (fused.cu:
+ * GEMM with the select in its epilogue, the distance matrix never reaches HBM; used for
+ * k <= 32 on the tensor-core path), KNN_PLAN_MATERIALISED.  Env KNN_FUSED=1 / 0 at ctx
+ * creation selects FUSED / MATERIALISED.  All plans give bit-identical results. */
+typedef enum { KNN_PLAN_AUTO = 0, KNN_PLAN_FUSED = 1, KNN_PLAN_MATERIALISED = 2 } knn_plan;
+knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
+/* 1 if the top-level calls run the fused plan for this k under the current setting. */
 int knn_fused_plan(knn_ctx_t ctx, int32_t k);
 
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by

@@ -31,7 +31,7 @@ struct knn_ctx {
     std::vector<cudaEvent_t> ev_pool;
     struct Pending { int kind; cudaEvent_t a, b; };
     std::vector<Pending> pending;
-    bool fused_ok = true;  // env KNN_FUSED=0 disables the fused plan
+    int plan = KNN_PLAN_AUTO;  // knn_set_plan / env KNN_FUSED
     double prof_ms[5] = {0, 0, 0, 0, 0};
     int64_t prof_n[5] = {0, 0, 0, 0, 0};
 };
@@ -316,7 +316,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     const char* g = getenv("KNN_GEMM");
     if (g && strcmp(g, "simt") == 0) c->gemm_mode = 1;
     const char* fz = getenv("KNN_FUSED");
-    if (fz && strcmp(fz, "0") == 0) c->fused_ok = false;
+    if (fz && strcmp(fz, "0") == 0) c->plan = KNN_PLAN_MATERIALISED;
+    if (fz && strcmp(fz, "1") == 0) c->plan = KNN_PLAN_FUSED;
     const char* b = getenv("KNN_D_BUDGET_MB");
     if (b) c->d_budget = (size_t)atoll(b) << 20;
     if (cudaMallocHost(&c->flag_host, sizeof(int32_t)) != cudaSuccess) {
@@ -346,7 +347,16 @@ int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
 int knn_fused_plan(knn_ctx_t ctx, int32_t k) {
     if (!ctx) return -1;
-    return (ctx->gemm_mode == 0 && ctx->tc_ok && ctx->fused_ok && k >= 1 && k <= knn::fused_max_k()) ? 1 : 0;
+    return (ctx->gemm_mode == 0 && ctx->tc_ok && ctx->plan == KNN_PLAN_FUSED && k >= 1 &&
+            k <= knn::fused_max_k()) ? 1 : 0;
+}
+
+knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (plan < KNN_PLAN_AUTO || plan > KNN_PLAN_MATERIALISED)
+        return fail(ctx, KNN_ERR_ARG, "unknown plan %d", plan);
+    ctx->plan = plan;
+    return KNN_OK;
 }
 
 int knn_gemm_path(knn_ctx_t ctx) {

@@ -11,15 +11,16 @@
 //    split-fp16 tcgen05 MMAs into a double-buffered TMEM accumulator.
 //  * Work unit = a row-block pair against one of S column splits; the CTA keeps the state
 //    of its 128 rows for the whole split.
-//  * 4 epilogue warps; thread = one query row (its TMEM lane).  Per 32-column chunk: the
-//    same distance expression as the materialised epilogue (so the results are
-//    bit-identical to distances + select), then the row's running threshold test
-//    (v < T, T = key of the row's current k-th best; columns arrive in increasing order so
-//    the strict test is exact), survivors appended to the row's shared-memory list.  A
-//    list past `limit` is rebuilt by the whole warp (exact warp radix select, warpsel.cuh),
-//    one row at a time, which lowers that row's T.
-//  * End of unit: per row, exact k + register bitonic sort, written as the final lists
-//    (S = 1) or as partial lists merged by knn_merge (S > 1).
+//  * 4 epilogue warps; thread = one query row (its TMEM lane).  Each row keeps a sorted
+//    best-32 list in shared memory (threshold T = its k-th entry) and an unsorted survivor
+//    buffer.  Per 32-column chunk: the unclamped distance u (its clamp max(u,0)+0 is the
+//    materialised value, so u < T whenever that value is; for L2 the test runs against
+//    RU(T^2)), one min-vote per chunk, one vote per column that holds a survivor, and the
+//    survivor's exact value (same expression as gemm_tc.cu, hence bit-identical results)
+//    appended to its row's buffer.  A buffer past 32 entries is folded into the sorted
+//    list by the whole warp (bitonic sort of 32 + merge, warpsel.cuh), lowering T.
+//  * End of unit: fold the rest; the first k list entries are the row's answer, written
+//    as final lists (S = 1) or as partial lists merged by knn_merge (S > 1).
 #include "tc_common.cuh"
 #include "warpsel.cuh"
 
@@ -34,12 +35,12 @@ constexpr int FSTAGES = 2;
 constexpr int FEPI_WARPS = 4;                 // one thread per row of the 128-row block
 constexpr int FTHREADS = 64 + 32 * FEPI_WARPS;
 constexpr int FK = 32;                        // largest k of the fused plan
-constexpr int FCAP = 96;                      // row list capacity (limit + one chunk)
-constexpr int FLIMIT = FCAP - 32;             // rebuild when a list holds more
-constexpr int LIST_BYTES = FCAP * BM * 4;     // one of key / idx lists, [FCAP][BM]
-constexpr int SCR_WORDS = 2 * FK + 256;       // per warp: kept key, idx + histogram
-constexpr int FSMEM_BYTES = FSTAGES * STAGE_BYTES + 2 * LIST_BYTES + FEPI_WARPS * SCR_WORDS * 4 +
-                            1024 /*align*/ + 1024 /*barriers*/;
+constexpr int FCAP = 64;                      // survivor buffer per row (folded when > 32)
+constexpr int BMP = BM + 1;                   // padded row stride of the survivor buffers
+constexpr int BEST_BYTES = BM * 32 * 8;       // sorted best-32 per row, [BM][32] x u64
+constexpr int BUF_BYTES = FCAP * BMP * 4;     // one of key / idx buffers, [FCAP][BMP]
+constexpr int FSMEM_BYTES = FSTAGES * STAGE_BYTES + BEST_BYTES + 2 * BUF_BYTES + 1024 /*align*/ +
+                            1024 /*barriers*/;
 
 struct FusedArgs {
     const float* qn; const float* q_rs; int64_t M;
@@ -58,10 +59,10 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
     __shared__ __align__(16) float col_s[2][BN];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* stage_base = smem;
-    uint32_t* lkey = reinterpret_cast<uint32_t*>(smem + FSTAGES * STAGE_BYTES);  // [FCAP][BM]
-    uint32_t* lidx = lkey + FCAP * BM;
-    uint32_t* scratch = lidx + FCAP * BM;                                         // [warps][SCR]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + FEPI_WARPS * SCR_WORDS);
+    uint64_t* best = reinterpret_cast<uint64_t*>(smem + FSTAGES * STAGE_BYTES);  // [BM][32]
+    uint32_t* bkey = reinterpret_cast<uint32_t*>(best + BM * 32);                 // [FCAP][BMP]
+    uint32_t* bidx = bkey + FCAP * BMP;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bidx + FCAP * BMP);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * FSTAGES + 4);
     const Bars b{smem_u32(bars), smem_u32(bars + FSTAGES), smem_u32(bars + 2 * FSTAGES),
                  smem_u32(bars + 2 * FSTAGES + 2)};
@@ -81,13 +82,30 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
         __syncwarp();
     } else {
         // -------------------------------------------------------- epilogue -----------
+        // Each thread owns one row: a sorted best-32 list best[row][:] (key << 32 | idx;
+        // threshold = its (k-1)-th entry) and an unsorted survivor buffer; a buffer with
+        // more than 32 entries is folded into the list by the whole warp (warp_merge32).
         const int quad = warp & 3;           // TMEM lane quadrant = rows quad*32 .. +32
         const int etid = threadIdx.x - 64;   // 0..127
         const int rl = quad * 32 + lane;     // this thread's row within the block
-        uint32_t* kkey = scratch + (warp - 2) * SCR_WORDS;
-        uint32_t* kidx = kkey + FK;
-        uint32_t* hist = kidx + FK;
         const int k = a.k;
+        const float kInf = __int_as_float(0x7F800000);
+        // fold row rr's survivor buffer (all lanes); returns the row's new threshold
+        auto fold = [&](int rr, int n) -> float {
+            const int rrl = quad * 32 + rr;
+            uint64_t L = best[rrl * 32 + lane];
+            for (int o = 0; o < n; o += 32)
+                L = ws::warp_merge32<BMP>(L, bkey + o * BMP + rrl, bidx + o * BMP + rrl,
+                                          n - o < 32 ? n - o : 32);
+            best[rrl * 32 + lane] = L;
+            const uint32_t tk = (uint32_t)(__shfl_sync(ws::FULL, L, k - 1) >> 32);
+            __syncwarp();
+            if (tk == 0xFFFFFFFFu) return kInf;
+            const float t = ukey_to_float(tk);
+            // the filter runs on squared distances: for L2, sqrt(x) < t implies x < t^2 <=
+            // RU(t*t), so rounding the square up never rejects a true neighbour
+            return METRIC == 1 ? __fmul_ru(t, t) : t;
+        };
         int it = 0;
         for (int64_t u = cid; u < sched.units(); u += ncl) {
             const Unit w = sched.get(u);
@@ -98,7 +116,9 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
             const float cq = row_ok ? -2.0f * __ldg(a.q_rs + row) : 0.0f;
             const int64_t self_col = row + a.self_shift;  // wraps harmlessly for no-self
             int cnt = 0;
-            float tf = __int_as_float(0x7F800000);  // accept every finite distance
+            float tf = kInf;  // accept every finite distance until k are known
+            for (int rr = 0; rr < 32; ++rr) best[(quad * 32 + rr) * 32 + lane] = ~0ull;
+            __syncwarp();
             for (int64_t nb = w.nb0; nb < w.nb1; ++nb, ++it) {
                 const int buf = it & 1;
                 const uint32_t tphase = (it >> 1) & 1;
@@ -127,6 +147,8 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
                     const int cb = ch * 32;
                     const float4* cn4 = reinterpret_cast<const float4*>(&col_n[buf][cb]);
                     const float4* cs4 = reinterpret_cast<const float4*>(&col_s[buf][cb]);
+                    // unclamped distance u: the materialised value is max(u, 0) + 0, so
+                    // u < tf whenever that value is < tf (no false negatives).
                     float v[32];
                     #pragma unroll
                     for (int c4 = 0; c4 < 8; ++c4) {
@@ -137,17 +159,14 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
                         #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int c = 4 * c4 + e;
-                            float dd = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
-                            dd = fmaxf(dd, 0.0f) + 0.0f;
-                            if (METRIC == 1) dd = sqrtf(dd);
-                            v[c] = dd;
+                            v[c] = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
                         }
                     }
                     const int64_t c0 = n0 + cb;
                     if (diag || tail) {
                         #pragma unroll
                         for (int c = 0; c < 32; ++c)
-                            if (c0 + c == self_col || c0 + c >= a.N) v[c] = __int_as_float(0x7F800000);
+                            if (c0 + c == self_col || c0 + c >= a.N) v[c] = kInf;
                     }
                     float m[16];
                     #pragma unroll
@@ -157,67 +176,54 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
                         #pragma unroll
                         for (int c = 0; c < wdt; ++c) m[c] = fminf(m[c], m[c + wdt]);
                     if (!__any_sync(ws::FULL, m[0] < tf)) continue;
-                    // append this row's survivors (each thread owns its row's list)
+                    // per column: the rows (lanes) holding a survivor append it to their own
+                    // buffer; columns without any survivor cost one vote
                     #pragma unroll
                     for (int c = 0; c < 32; ++c) {
-                        if (v[c] < tf) {
-                            lkey[cnt * BM + rl] = __float_as_uint(v[c]) | 0x80000000u;  // ukey(v >= 0)
-                            lidx[cnt * BM + rl] = (uint32_t)(c0 + c);
-                            ++cnt;
+                        const bool ok = v[c] < tf;
+                        if (__any_sync(ws::FULL, ok)) {
+                            if (ok) {
+                                float dd = fmaxf(v[c], 0.0f) + 0.0f;
+                                if (METRIC == 1) dd = sqrtf(dd);
+                                bkey[cnt * BMP + rl] = __float_as_uint(dd) | 0x80000000u;  // ukey(dd >= 0)
+                                bidx[cnt * BMP + rl] = (uint32_t)(c0 + c);
+                                ++cnt;
+                            }
                         }
                     }
-                    uint32_t need = __ballot_sync(ws::FULL, cnt > FLIMIT);
+                    uint32_t need = __ballot_sync(ws::FULL, cnt > 32);
                     if (need) {
                         __syncwarp();
                         while (need) {
                             const int rr = __ffs(need) - 1;
                             need &= need - 1;
                             const int n = __shfl_sync(ws::FULL, cnt, rr);
-                            const int rrl = quad * 32 + rr;
-                            const uint32_t t = ws::warp_select_k<BM>(lkey + rrl, lidx + rrl, n, k, kkey,
-                                                                     kidx, hist);
-                            for (int i = lane; i < k; i += 32) {
-                                lkey[i * BM + rrl] = kkey[i];
-                                lidx[i * BM + rrl] = kidx[i];
-                            }
-                            __syncwarp();
+                            const float t = fold(rr, n);
                             if (lane == rr) {
-                                cnt = k;
-                                tf = ukey_to_float(t);
+                                cnt = 0;
+                                tf = t;
                             }
                         }
                     }
                 }
             }
-            // ---- end of unit: exact k, sort, write each of the warp's 32 rows
+            // ---- end of unit: fold what is left, write the first k of each sorted list
             __syncwarp();
             const int64_t split = w.nb0 / sched.per;
             for (int rr = 0; rr < 32; ++rr) {
                 const int64_t grow = row0 + rr;
                 if (grow >= a.M) break;
                 const int n = __shfl_sync(ws::FULL, cnt, rr);
-                const int rrl = quad * 32 + rr;
-                if (n > k) {
-                    ws::warp_select_k<BM>(lkey + rrl, lidx + rrl, n, k, kkey, kidx, hist);
-                } else {
-                    if (lane < n) {
-                        kkey[lane] = lkey[lane * BM + rrl];
-                        kidx[lane] = lidx[lane * BM + rrl];
-                    }
-                    __syncwarp();
-                }
-                const int e = lane;  // k <= 32: one element per lane
-                uint64_t vv[1] = {e < (n < k ? n : k) ? ((uint64_t)kkey[e] << 32 | kidx[e]) : ~0ull};
-                __syncwarp();
-                ws::warp_bitonic<1>(vv);
-                if (e < k) {
-                    const size_t o = ((size_t)split * a.M + grow) * k + e;
-                    const uint32_t key = (uint32_t)(vv[0] >> 32);
+                if (n > 0) fold(rr, n);
+                const uint64_t L = best[(quad * 32 + rr) * 32 + lane];
+                if (lane < k) {
+                    const size_t o = ((size_t)split * a.M + grow) * k + lane;
+                    const uint32_t key = (uint32_t)(L >> 32);
                     if (key == 0xFFFFFFFFu) {  // fewer than k columns in this split
                         a.out_idx[o] = -1;
-                        a.out_dist[o] = __int_as_float(0x7F800000);
+                        a.out_dist[o] = kInf;
                     } else {
-                        a.out_idx[o] = (int32_t)((int64_t)(uint32_t)vv[0] + a.idx_offset);
+                        a.out_idx[o] = (int32_t)((int64_t)(uint32_t)L + a.idx_offset);
                         a.out_dist[o] = ukey_to_float(key);
                     }
                 }

@@ -18,13 +18,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Wait for the phase with the given parity to complete.  The suspend-time hint lets the
+// hardware park the waiting thread instead of spinning (a spinning producer / MMA warp
+// otherwise steals issue slots from the epilogue warps of its SM sub-partition).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {

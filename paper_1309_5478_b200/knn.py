@@ -27,7 +27,9 @@ STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_N
 SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
-           "knn_gemm_path", "knn_fused_plan", "knn_profile_enable", "knn_profile_read"]
+           "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_profile_enable",
+           "knn_profile_read"]
+PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
 
@@ -75,6 +77,7 @@ def load_library():
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
             "knn_fused_plan": (ctypes.c_int, [p, i32]),
+            "knn_set_plan": (st, [p, i32]),
             "knn_profile_enable": (st, [p, i32]),
             "knn_profile_read": (st, [p, i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_int64)]),
@@ -262,6 +265,13 @@ def launch_count(device=None):
 def gemm_path(device=None):
     """0 = tcgen05 split-fp16 tensor-core GEMM, 1 = SIMT FFMA."""
     return int(load_library().knn_gemm_path(context(device)))
+
+
+def set_plan(plan, device=None):
+    """PLAN_AUTO (default), PLAN_FUSED (GEMM with the select in its epilogue, k <= 32) or
+    PLAN_MATERIALISED; all give bit-identical results."""
+    ctx = context(device)
+    _check(load_library().knn_set_plan(ctx, int(plan)), ctx)
 
 
 def fused_plan(k, device=None):

@@ -253,8 +253,16 @@ def test_simt_cross_check_path():
 @pytest.mark.parametrize("M,N,d,k", [(300, 300, 3, 1), (1000, 1000, 64, 8), (2500, 2500, 33, 32),
                                      (5000, 5000, 200, 31), (777, 4099, 128, 16)])
 @pytest.mark.parametrize("metric", [0, 1])
-def test_fused_equals_materialised(M, N, d, k, metric):
+@pytest.fixture
+def fused_plan():
     kn = knn()
+    kn.set_plan(kn.PLAN_FUSED)
+    yield kn
+    kn.set_plan(kn.PLAN_AUTO)
+
+
+def test_fused_equals_materialised(M, N, d, k, metric, fused_plan):
+    kn = fused_plan
     X = datagen.points(N, d, "clusters", seed=N + d)
     Xt = cuda(X)
     if M == N:
@@ -270,9 +278,9 @@ def test_fused_equals_materialised(M, N, d, k, metric):
     assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
 
 
-def test_fused_many_splits_long_rows():
+def test_fused_many_splits_long_rows(fused_plan):
     # few query rows against a long corpus: the fused plan splits columns and merges
-    kn = knn()
+    kn = fused_plan
     Q = cuda(datagen.points(2000, 256, "uniform", seed=31))
     X = cuda(datagen.points(65536, 256, "uniform", seed=32))
     gi, gd = kn.search_block(Q, X, 32)
@@ -280,8 +288,9 @@ def test_fused_many_splits_long_rows():
     assert torch.equal(gi, ri) and torch.equal(gd, rd)
 
 
-def test_fused_self_shift_and_offsets():
-    kn = knn()
+def test_fused_self_shift_and_offsets(fused_plan):
+    kn = fused_plan
+    assert kn.fused_plan(20) == 1
     X = datagen.points(3000, 24, "gauss", seed=33)
     Xt = cuda(X)
     ref_i, ref_d = kn.graph(Xt, 20)
@@ -290,3 +299,11 @@ def test_fused_self_shift_and_offsets():
     i, d = kn.merge(torch.stack([p[1] for p in parts]), torch.stack([p[0] for p in parts]),
                     np.zeros(3, np.int64))
     assert torch.equal(i, ref_i) and torch.equal(d, ref_d)
+
+
+@pytest.mark.parametrize("cfg_name", ["C1", "C2"])
+def test_fused_plan_e2e(cfg_name, fused_plan):
+    cfg = datagen.CONFIGS[cfg_name]
+    X, _ = datagen.config_inputs(cfg)
+    gi, gd = run_graph(X, cfg.k)
+    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 100, 9), True)
