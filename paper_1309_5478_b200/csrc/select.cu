@@ -599,6 +599,16 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Fold `count` buffered candidates into the sorted best-32 register list L (one entry per
+// lane), 32 at a time.  Out of line to keep the streaming loop small in the I-cache.
+__device__ __noinline__ uint64_t warp_fold32(uint64_t L, const uint32_t* ckey, const uint32_t* cidx,
+                                             int count) {
+    for (int o = 0; o < count; o += 32)
+        L = ws::warp_merge32<1>(L, ckey + o, cidx + o, count - o < 32 ? count - o : 32);
+    __syncwarp();
+    return L;
+}
+
 // Reduce the warp's candidate buffer to exactly its k best, in place; returns the
 // k-th best key (the new strict threshold).  Out of line: it runs a few times per row.
 __device__ __noinline__ uint32_t warp_rebuild(uint32_t* ckey, uint32_t* cidx, int count, int k,
@@ -668,12 +678,29 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
         float tf = 0.0f;
         bool fast = false;
         int count = 0;
-        auto rebuild = [&]() {
-            const uint32_t t = warp_rebuild(ckey, cidx, count, k, kkey, kidx, hist);
-            count = k;
-            Tlim = t;  // later elements have larger indices: strict
-            fast = t <= 0xFF800000u;
-            tf = ukey_to_float(t);
+        // k <= 32 (R == 1): the row's best 32 live sorted in registers, one entry per lane
+        // (key << 32 | idx); survivors are folded in 32 at a time (warp_merge32).  Larger
+        // k: exact radix rebuild of the buffer to its k best.  Either way the threshold
+        // only decreases and later elements (larger indices) are tested strictly.
+        uint64_t L = ~0ull;
+        auto rebuild = [&]() -> bool {
+            if constexpr (R == 1) {
+                L = warp_fold32(L, ckey, cidx, count);
+                count = 0;
+                const uint32_t tk = (uint32_t)(__shfl_sync(FULL, L, k - 1) >> 32);
+                if (tk == 0xFFFFFFFFu) return false;  // fewer than k seen so far
+                Tlim = tk;
+                fast = tk <= 0xFF800000u;
+                tf = ukey_to_float(tk);
+                return true;
+            } else {
+                const uint32_t t = warp_rebuild(ckey, cidx, count, k, kkey, kidx, hist);
+                count = k;
+                Tlim = t;  // later elements have larger indices: strict
+                fast = t <= 0xFF800000u;
+                tf = ukey_to_float(t);
+                return true;
+            }
         };
         for (int64_t c = 0; c < nchunk; ++c) {
             mbar_wait(full0 + 8 * stage, parity);
@@ -740,10 +767,7 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             bool rebuilt = false;
 #define KNN_GEN_SG(J)                                                                   \
     count += warp_append_generic<J, SUBJ>(cur, Tlim, full, N, col, ckey, cidx, count);  \
-    if (count > limit) {                                                                \
-        rebuild();                                                                      \
-        rebuilt = true;                                                                 \
-    }
+    if (count > limit) rebuilt |= rebuild();
             KNN_GEN_SG(0) KNN_GEN_SG(2) KNN_GEN_SG(4) KNN_GEN_SG(6)
 #undef KNN_GEN_SG
             if (first && !rebuilt) {  // later chunks: strict u < t0
@@ -752,14 +776,22 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
                 tf = ukey_to_float(Tlim);
             }
         }
-        const uint32_t* fk = ckey;
-        const uint32_t* fi = cidx;
-        if (count > k) {
-            ws::warp_select_k<1>(ckey, cidx, count, k, kkey, kidx, hist);
-            fk = kkey;
-            fi = kidx;
+        if constexpr (R == 1) {
+            if (count > 0) rebuild();
+            if (lane < k) {
+                out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)L + idx_offset);
+                out_dist[row * k + lane] = ukey_to_float((uint32_t)(L >> 32));
+            }
+        } else {
+            const uint32_t* fk = ckey;
+            const uint32_t* fi = cidx;
+            if (count > k) {
+                ws::warp_select_k<1>(ckey, cidx, count, k, kkey, kidx, hist);
+                fk = kkey;
+                fi = kidx;
+            }
+            ws::warp_sort_write<R>(fk, fi, k, idx_offset, out_idx + row * k, out_dist + row * k);
         }
-        ws::warp_sort_write<R>(fk, fi, k, idx_offset, out_idx + row * k, out_dist + row * k);
         __syncwarp();
     }
 }
@@ -871,8 +903,10 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (aligned && k <= WSEL_K && M >= 4 * (int64_t)sms) {
         // warp per row: enough rows to give every SM >= 4 warps
-        const int limit = (int)round_up(k + 64 > 2 * k ? k + 64 : 2 * k, 32);
-        const int cap = WSEL_SUB + limit;
+        // k <= 32 folds every 32 survivors into the sorted register list; larger k
+        // rebuilds the buffer once it passes max(2k, k + 64)
+        const int limit = k <= 32 ? 31 : (int)round_up(k + 64 > 2 * k ? k + 64 : 2 * k, 32);
+        const int cap = WSEL_SUB + limit + 1;
         const size_t smem = (size_t)wsel_slab_bytes(cap) * WSEL_WARPS;
         auto pick = [&](auto kern) -> cudaError_t {
             cudaError_t e2;

@@ -248,11 +248,6 @@ def test_simt_cross_check_path():
 
 
 # ------------------------------------------------------------------ a-S5 fused -------
-# The fused GEMM+select (k <= 32) must equal knn_distances + knn_select (the
-# materialised building blocks) bit-for-bit: same distance expression, exact select.
-@pytest.mark.parametrize("M,N,d,k", [(300, 300, 3, 1), (1000, 1000, 64, 8), (2500, 2500, 33, 32),
-                                     (5000, 5000, 200, 31), (777, 4099, 128, 16)])
-@pytest.mark.parametrize("metric", [0, 1])
 @pytest.fixture
 def fused_plan():
     kn = knn()
@@ -261,6 +256,11 @@ def fused_plan():
     kn.set_plan(kn.PLAN_AUTO)
 
 
+# The fused GEMM+select (k <= 32) must equal knn_distances + knn_select (the
+# materialised building blocks) bit-for-bit: same distance expression, exact select.
+@pytest.mark.parametrize("M,N,d,k", [(300, 300, 3, 1), (1000, 1000, 64, 8), (2500, 2500, 33, 32),
+                                     (5000, 5000, 200, 31), (777, 4099, 128, 16)])
+@pytest.mark.parametrize("metric", [0, 1])
 def test_fused_equals_materialised(M, N, d, k, metric, fused_plan):
     kn = fused_plan
     X = datagen.points(N, d, "clusters", seed=N + d)
