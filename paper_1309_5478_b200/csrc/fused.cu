@@ -75,10 +75,10 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
     if (warp == 0) {
         if (lane == 0)
             producer_loop<FSTAGES>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched, num_kb,
-                                   crank, cid, ncl);
+                                   crank, cid, ncl, a.self_shift);
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<FSTAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl);
+        if (lane == 0) mma_loop<FSTAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, a.self_shift);
         __syncwarp();
     } else {
         // -------------------------------------------------------- epilogue -----------
@@ -119,7 +119,10 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
             float tf = kInf;  // accept every finite distance until k are known
             for (int rr = 0; rr < 32; ++rr) best[(quad * 32 + rr) * 32 + lane] = ~0ull;
             __syncwarp();
-            for (int64_t nb = w.nb0; nb < w.nb1; ++nb, ++it) {
+            for (int64_t nb = w.nb0; nb < w.nb1; ++nb)
+            for (int pass = 0, cls = tile_class(w.mp, nb, a.self_shift); pass < tile_passes(cls);
+                 ++pass, ++it) {
+                const int tmask = tile_mask(cls, pass);  // mixed block: one side per pass
                 const int buf = it & 1;
                 const uint32_t tphase = (it >> 1) & 1;
                 const int64_t n0 = nb * BN;
@@ -163,10 +166,13 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
                         }
                     }
                     const int64_t c0 = n0 + cb;
-                    if (diag || tail) {
+                    if (diag || tail || tmask) {
                         #pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (c0 + c == self_col || c0 + c >= a.N) v[c] = kInf;
+                        for (int c = 0; c < 32; ++c) {
+                            const bool lower = row + a.self_shift > c0 + c;  // i+shift > j
+                            if (c0 + c == self_col || c0 + c >= a.N || (tmask && lower != (tmask == 2)))
+                                v[c] = kInf;
+                        }
                     }
                     float m[16];
                     #pragma unroll

@@ -78,10 +78,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     if (warp == 0) {
         if (lane == 0)
             producer_loop<STAGES>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched, num_kb,
-                                  crank, cid, ncl);
+                                  crank, cid, ncl, ep.self_shift);
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl);
+        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ep.self_shift);
         __syncwarp();
     } else {
         // ------------------------------------------------------ epilogue (8 warps) --
@@ -91,10 +91,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
-        for (int64_t t = cid; t < sched.units(); t += ncl, ++it) {
+        for (int64_t t = cid; t < sched.units(); t += ncl)
+        for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ep.self_shift);
+             pass < tile_passes(cls); ++pass, ++it) {
             const tc::Unit w = sched.get(t);
             const int64_t nb = w.nb0;
             const int64_t mb = 2 * w.mp + crank;
+            const int tmask = tile_mask(cls, pass);  // mixed block: keep one side only
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
@@ -153,6 +156,17 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int c = 0; c < 32; ++c)
                         if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
+                }
+                if (tmask) {
+                    // one orientation pass of a block straddling the diagonal: store only
+                    // the elements this orientation owns (rare; plain stores)
+                    if (!row_ok) continue;
+                    #pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const bool lower = row + ep.self_shift > c0 + c;  // i+shift > j
+                        if (c0 + c < ep.N && lower == (tmask == 2)) drow[c0 + c] = v[c];
+                    }
+                    continue;
                 }
                 if (use_tma_store) {
                     // stage the 32x32 chunk in 128B-swizzled smem (row = lane: 16-byte

@@ -156,6 +156,30 @@ struct SplitSched {
     }
 };
 
+// ------------------------------------------------------------------ orientation -------
+// Canonical orientation: the value of pair (query i, corpus j) is always
+// computed with the LOWER point index as the first split operand, so that when queries
+// and corpus are one point set (j == i + shift is the self pair) D[i][j] and D[j][i] are
+// the same bits in every plan.  Segment order O1 = (ql.xh, qh.xl, qh.xh) for i+shift < j,
+// O2 = (qh.xl, ql.xh, qh.xh) for i+shift > j (the same products in the transposed order).
+// A 256x256 pair block straddling the diagonal is computed twice, O1 keeping only
+// i+shift <= j and O2 keeping only i+shift > j.
+enum { TILE_ABOVE = 0, TILE_BELOW = 1, TILE_MIXED = 2 };
+__device__ __forceinline__ int tile_class(int64_t mp, int64_t nb, int64_t shift) {
+    if (shift == INT64_MIN) return TILE_ABOVE;
+    const int64_t r_lo = 2 * BM * mp + shift, r_hi = r_lo + 2 * BM - 1;  // shifted row range
+    const int64_t c_lo = nb * BN, c_hi = c_lo + BN - 1;
+    if (r_hi < c_lo) return TILE_ABOVE;
+    if (r_lo > c_hi) return TILE_BELOW;
+    return TILE_MIXED;
+}
+__device__ __forceinline__ int tile_passes(int cls) { return cls == TILE_MIXED ? 2 : 1; }
+__device__ __forceinline__ int tile_orient(int cls, int pass) { return cls == TILE_MIXED ? pass : cls; }
+// 0: keep all; 1: keep i+shift <= j (O1 pass of a mixed block); 2: keep i+shift > j
+__device__ __forceinline__ int tile_mask(int cls, int pass) {
+    return cls == TILE_MIXED ? 1 + pass : 0;
+}
+
 // ------------------------------------------------------------------ mainloop ---------
 // Barriers: full[s] (1 arrival + tx bytes), empty[s] (CLUSTER arrivals: both CTAs' MMAs),
 // tfull[2] (MMA commit), tempty[2] (one arrival per epilogue warp).
@@ -169,13 +193,15 @@ template <int STAGES, class Sched>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const CUtensorMap* map_ql,
                                               const CUtensorMap* map_xh, const CUtensorMap* map_xl,
                                               uint8_t* stage_base, const Bars& b, const Sched& sched,
-                                              int num_kb, uint32_t crank, int64_t cid, int64_t ncl) {
+                                              int num_kb, uint32_t crank, int64_t cid, int64_t ncl,
+                                              int64_t shift) {
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t u = cid; u < sched.units(); u += ncl) {
         const Unit w = sched.get(u);
         const int row_a = (int)((2 * w.mp + crank) * BM);
-        for (int64_t nb = w.nb0; nb < w.nb1; ++nb) {
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb)
+        for (int pass = 0; pass < tile_passes(tile_class(w.mp, nb, shift)); ++pass) {
             const int row_b = (int)(nb * BN + crank * (BN / 2));  // this CTA's half of B
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(b.empty0 + 8 * stage, phase ^ 1);
@@ -201,13 +227,16 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const C
 // stage in both CTAs; finally signals the epilogue.
 template <int STAGES, class Sched>
 __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, const Sched& sched,
-                                         int num_kb, uint32_t tmem_base, int64_t cid, int64_t ncl) {
+                                         int num_kb, uint32_t tmem_base, int64_t cid, int64_t ncl,
+                                         int64_t shift) {
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     for (int64_t u = cid; u < sched.units(); u += ncl) {
         const Unit w = sched.get(u);
-        for (int64_t nb = w.nb0; nb < w.nb1; ++nb, ++it) {
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb)
+        for (int pass = 0, cls = tile_class(w.mp, nb, shift); pass < tile_passes(cls); ++pass, ++it) {
+            const bool o2 = tile_orient(cls, pass) == TILE_BELOW;
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
             mbar_wait(b.tempty0 + 8 * buf, tphase ^ 1);
@@ -219,8 +248,9 @@ __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, con
                 const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
                 const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + 2 * A_BYTES,
                                xl = sb + 2 * A_BYTES + B_BYTES;
-                const uint32_t sa[3] = {ql, qh, qh};
-                const uint32_t sbx[3] = {xh, xl, xh};
+                // O1: ql.xh, qh.xl, qh.xh   O2: qh.xl, ql.xh, qh.xh  (smallest terms first)
+                const uint32_t sa[3] = {o2 ? qh : ql, o2 ? ql : qh, qh};
+                const uint32_t sbx[3] = {o2 ? xl : xh, o2 ? xh : xl, xh};
                 #pragma unroll
                 for (int seg = 0; seg < 3; ++seg) {
                     #pragma unroll

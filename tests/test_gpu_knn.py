@@ -307,3 +307,21 @@ def test_fused_plan_e2e(cfg_name, fused_plan):
     X, _ = datagen.config_inputs(cfg)
     gi, gd = run_graph(X, cfg.k)
     e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 100, 9), True)
+
+
+# ------------------------------------------------------------------ canonical orientation
+def test_distances_canonically_symmetric():
+    # With queries = corpus, every plan computes pair (i, j) with the lower index as the
+    # first split operand, so D is bit-symmetric, and row blocks with a self shift
+    # (query sharding) reproduce the same bits.
+    kn = knn()
+    X = datagen.points(1500, 100, "gauss", seed=40)
+    Xt = cuda(X)
+    D = kn.distances(Xt, Xt, self_shift=0).cpu().numpy()
+    off = ~np.eye(1500, dtype=bool)
+    assert np.array_equal(D.view(np.uint32)[off], D.T.view(np.uint32)[off])
+    assert np.all(np.isinf(np.diag(D)))
+    Db = kn.distances(Xt[300:1100].contiguous(), Xt, self_shift=300).cpu().numpy()
+    assert np.array_equal(Db.view(np.uint32), D[300:1100].view(np.uint32))
+    Dc = kn.distances(Xt, Xt[700:1400].contiguous(), self_shift=-700).cpu().numpy()
+    assert np.array_equal(Dc.view(np.uint32), D[:, 700:1400].view(np.uint32))
