@@ -159,6 +159,10 @@ typedef enum { KNN_PLAN_AUTO = 0, KNN_PLAN_FUSED = 1, KNN_PLAN_MATERIALISED = 2 
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
 /* 1 if the top-level calls run the fused plan for this k under the current setting. */
 int knn_fused_plan(knn_ctx_t ctx, int32_t k);
+/* Plan the last top-level call of this ctx executed: 0 = blocked distances + select,
+ * 1 = fused GEMM+select, 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
+ * each written directly and transposed) + select, -1 = none yet. */
+int knn_last_plan(knn_ctx_t ctx);
 
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by
  * CUDA events recorded on the launch stream.  knn_profile_enable(ctx, 1) also resets

@@ -32,6 +32,9 @@ struct knn_ctx {
     struct Pending { int kind; cudaEvent_t a, b; };
     std::vector<Pending> pending;
     int plan = KNN_PLAN_AUTO;  // knn_set_plan / env KNN_FUSED
+    bool sym_ok = true;        // env KNN_SYM=0 disables the symmetric k-NNG GEMM
+    int last_plan = -1;
+    size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
     double prof_ms[5] = {0, 0, 0, 0, 0};
     int64_t prof_n[5] = {0, 0, 0, 0, 0};
 };
@@ -185,6 +188,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     if (rows_blk > M) rows_blk = M;
     const int S = fused ? (int)knn::fused_actual_splits(N, knn::fused_splits(M, N, ctx->num_sms)) : 1;
     if (fused) rows_blk = 0;  // no distance block
+    // k-NNG with the transpose reuse of PAPER.md:83: only the upper triangle is multiplied
+    // (bit-identical to the other plans thanks to the canonical orientation)
+    const bool sym = !fused && tc && ctx->sym_ok && same && self_shift == 0 &&
+                     (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
+    if (sym) rows_blk = M;
+    ctx->last_plan = fused ? 1 : sym ? 2 : 0;
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -240,6 +249,16 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             KNN_CUDA(knn::launch_merge(part_d, part_i, S, M, k, zeros, out_idx, out_dist, s));
             tm.done();
         }
+        return KNN_OK;
+    }
+    if (sym) {
+        knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        Timed tg(ctx, KNN_KERNEL_GEMM, s);
+        KNN_CUDA(knn::launch_dist_tc_sym(op, metric, D, ldD, ctx->num_sms, s));
+        tg.done();
+        Timed ts(ctx, KNN_KERNEL_SELECT, s);
+        KNN_CUDA(knn::launch_select(D, M, N, ldD, k, idx_offset, out_idx, out_dist, s));
+        ts.done();
         return KNN_OK;
     }
     for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
@@ -318,6 +337,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     const char* fz = getenv("KNN_FUSED");
     if (fz && strcmp(fz, "0") == 0) c->plan = KNN_PLAN_MATERIALISED;
     if (fz && strcmp(fz, "1") == 0) c->plan = KNN_PLAN_FUSED;
+    const char* sy = getenv("KNN_SYM");
+    if (sy && strcmp(sy, "0") == 0) c->sym_ok = false;
     const char* b = getenv("KNN_D_BUDGET_MB");
     if (b) c->d_budget = (size_t)atoll(b) << 20;
     if (cudaMallocHost(&c->flag_host, sizeof(int32_t)) != cudaSuccess) {
@@ -358,6 +379,8 @@ knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan) {
     ctx->plan = plan;
     return KNN_OK;
 }
+
+int knn_last_plan(knn_ctx_t ctx) { return ctx ? ctx->last_plan : -1; }
 
 int knn_gemm_path(knn_ctx_t ctx) {
     if (!ctx) return -1;

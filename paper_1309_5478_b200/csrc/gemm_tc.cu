@@ -45,6 +45,8 @@ constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 output chunk (TMA-store staging)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 1024 /*align*/ +
                            1024 /*barriers*/;
+// SYM (symmetric k-NNG): each warp's two staging buffers hold the direct and the transposed
+// chunk of the same 32x32 block.
 
 struct EpiArgs {
     const float* qn; const float* q_rs; int64_t M;
@@ -52,12 +54,15 @@ struct EpiArgs {
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
 };
 
-template <int METRIC>
+template <int METRIC, bool SYM, class Sched>
 __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                const __grid_constant__ CUtensorMap map_d, int use_tma_store, int num_kb,
-               TileSched sched, EpiArgs ep) {
+               Sched sched, EpiArgs ep) {
+    // SYM: upper-triangle pair blocks only, O1 everywhere (every element has i < j or is
+    // mirrored from one), so the mainloop sees no self shift.
+    const int64_t ml_shift = SYM ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
     __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
@@ -78,10 +83,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     if (warp == 0) {
         if (lane == 0)
             producer_loop<STAGES>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched, num_kb,
-                                  crank, cid, ncl, ep.self_shift);
+                                  crank, cid, ncl, ml_shift);
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ep.self_shift);
+        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
         __syncwarp();
     } else {
         // ------------------------------------------------------ epilogue (8 warps) --
@@ -92,7 +97,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
         for (int64_t t = cid; t < sched.units(); t += ncl)
-        for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ep.self_shift);
+        for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ml_shift);
              pass < tile_passes(cls); ++pass, ++it) {
             const tc::Unit w = sched.get(t);
             const int64_t nb = w.nb0;
@@ -156,6 +161,49 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int c = 0; c < 32; ++c)
                         if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
+                }
+                if constexpr (SYM) {
+                    // chunk rows [row0, +32) x cols [c0, +32), both global.  Below the
+                    // diagonal: produced by the mirror chunk.  Above: stored directly and
+                    // transposed.  On it: lower triangle mirrored from the upper in smem.
+                    if (c0 < row0) continue;
+                    const uint32_t sd = smem_u32(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    const uint32_t st = sd + STG_BYTES;
+                    if (lane == 0) bulk_wait_read<0>();  // both buffers' previous stores read
+                    __syncwarp();
+                    #pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        sts128(sd + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
+                               v[4 * u + 2], v[4 * u + 3]);
+                    if (c0 == row0) {
+                        __syncwarp();
+                        float* sp = reinterpret_cast<float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                        for (int j = 0; j < lane; ++j)  // (lane, j) <- (j, lane)
+                            sp[lane * 32 + (((j >> 2) ^ (lane & 7)) << 2) + (j & 3)] =
+                                sp[j * 32 + (((lane >> 2) ^ (j & 7)) << 2) + (lane & 3)];
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&map_d, sd, (int)c0, (int)row0);
+                        bulk_commit();
+                    }
+                    if (c0 == row0) continue;
+                    if (lane == 0) bulk_wait_read<1>();  // transposed buffer's previous store read
+                    __syncwarp();
+                    #pragma unroll
+                    for (int j = 0; j < 32; ++j)  // element (row j, col lane) of the transpose
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) +
+                                                                   (lane & 3) * 4),
+                                     "f"(v[j])
+                                     : "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&map_d, st, (int)row0, (int)c0);
+                        bulk_commit();
+                    }
+                    continue;
                 }
                 if (tmask) {
                     // one orientation pass of a block straddling the diagonal: store only
@@ -278,7 +326,7 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int64_t pairs = num_tiles < num_sms / CLUSTER ? num_tiles : num_sms / CLUSTER;
     const int grid = (int)(pairs * CLUSTER);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD};
-    auto kern = metric == 1 ? dist_tc_kernel<1> : dist_tc_kernel<0>;
+    auto kern = metric == 1 ? dist_tc_kernel<1, false, TileSched> : dist_tc_kernel<0, false, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     CUtensorMap md;
@@ -287,6 +335,30 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     if (!tma_store) memset(&md, 0, sizeof md);
     kern<<<grid, THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, tma_store ? 1 : 0, op.d_pad / BK,
                                            tiles, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, int64_t ldD, int num_sms,
+                               cudaStream_t s) {
+    if (op.N == 0) return cudaSuccess;
+    if (op.M != op.N || ldD % 4 != 0 || (reinterpret_cast<uintptr_t>(D) & 15) != 0)
+        return cudaErrorInvalidValue;
+    CUtensorMap mqh, mql, mxh, mxl, md;
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2) ||
+        !tc_make_output_map(&md, D, op.N, op.N, ldD))
+        return cudaErrorInvalidValue;
+    SymSched sched{ceil_div(op.N, BN)};
+    const int64_t units = sched.n * (sched.n + 1) / 2;
+    const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD};
+    auto kern = metric == 1 ? dist_tc_kernel<1, true, SymSched> : dist_tc_kernel<0, true, SymSched>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 1, op.d_pad / BK,
+                                                                sched, ep);
     return cudaGetLastError();
 }
 

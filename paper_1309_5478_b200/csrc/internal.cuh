@@ -48,6 +48,10 @@ struct TcOperands {
 };
 cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_shift, float* D,
                            int64_t ldD, int num_sms, cudaStream_t s);
+// Symmetric k-NNG distances (queries = corpus, self excluded): the whole N x N matrix from
+// the upper triangle of 256x256 blocks, each also written transposed.
+cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, int64_t ldD,
+                               int num_sms, cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
 // fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial

@@ -143,6 +143,22 @@ struct TileSched {
     }
 };
 
+// Symmetric k-NNG (queries = corpus): the upper triangle of 256x256 pair blocks, nb >= mp,
+// row by row (consecutive units share the A panel); each block is also written transposed.
+struct SymSched {
+    int64_t n;  // pair blocks per side
+    __device__ __forceinline__ int64_t units() const { return n * (n + 1) / 2; }
+    __device__ __forceinline__ Unit get(int64_t u) const {
+        int64_t lo = 0, hi = n - 1;  // largest m with m*n - m(m-1)/2 <= u
+        while (lo < hi) {
+            const int64_t m = (lo + hi + 1) / 2;
+            if (m * n - m * (m - 1) / 2 <= u) lo = m; else hi = m - 1;
+        }
+        const int64_t nb = lo + (u - (lo * n - lo * (lo - 1) / 2));
+        return {lo, nb, nb + 1};
+    }
+};
+
 // Fused GEMM+select: a unit is a row-block pair against one of S column splits; units of
 // the same split are consecutive so concurrent clusters sweep the same B panel.
 struct SplitSched {

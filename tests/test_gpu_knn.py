@@ -325,3 +325,17 @@ def test_distances_canonically_symmetric():
     assert np.array_equal(Db.view(np.uint32), D[300:1100].view(np.uint32))
     Dc = kn.distances(Xt, Xt[700:1400].contiguous(), self_shift=-700).cpu().numpy()
     assert np.array_equal(Dc.view(np.uint32), D[:, 700:1400].view(np.uint32))
+
+
+@pytest.mark.parametrize("N,d,k,metric", [(3000, 64, 20, 0), (1000, 7, 100, 1), (4099, 256, 32, 0),
+                                          (700, 33, 1024 - 1024 + 699, 0)])
+def test_symmetric_graph_equals_unsymmetric(N, d, k, metric):
+    # knn_graph multiplies only the upper triangle (transpose reuse); the
+    # general block path (different pointers -> no symmetry) must give the same bits
+    kn = knn()
+    X = datagen.points(N, d, "clusters", seed=N + d)
+    Xt = cuda(X)
+    gi, gd = kn.graph(Xt, k, metric=metric)
+    ri, rd = kn.search_block(Xt, Xt.clone(), k, metric=metric, self_shift=0)
+    assert torch.equal(gi, ri)
+    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
