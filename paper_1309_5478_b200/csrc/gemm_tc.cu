@@ -96,6 +96,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
+        float pf_n = 0.0f, pf_s = 0.0f;  // next tile's column data, prefetched
+        bool pf_ok = false;
         for (int64_t t = cid; t < sched.units(); t += ncl)
         for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ml_shift);
              pass < tile_passes(cls); ++pass, ++it) {
@@ -106,11 +108,27 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
-            // stage the tile's column norms and scales (double-buffered by `buf`)
-            {
+            // stage the tile's column norms and scales (double-buffered by `buf`); they
+            // were loaded into registers one tile ahead, and the next tile's are issued now
+            if (!pf_ok) {
                 const int64_t j = n0 + etid;
-                col_n[buf][etid] = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
-                col_s[buf][etid] = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+                pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
+                pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+            }
+            col_n[buf][etid] = pf_n;
+            col_s[buf][etid] = pf_s;
+            pf_ok = false;
+            {
+                // next work item of this CTA (same unit's second pass, or the next unit)
+                int64_t tn = t;
+                bool again = pass + 1 < tile_passes(cls);
+                if (!again) tn = t + ncl;
+                if (tn < sched.units()) {
+                    const int64_t j = sched.get(tn).nb0 * BN + etid;
+                    pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
+                    pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+                    pf_ok = true;
+                }
             }
             named_bar(1, 32 * EPI_WARPS);
             const int64_t row0 = mb * BM + quad * 32;
