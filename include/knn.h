@@ -161,7 +161,13 @@ knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
 int knn_fused_plan(knn_ctx_t ctx, int32_t k);
 /* Plan the last top-level call of this ctx executed: 0 = blocked distances + select,
  * 1 = fused GEMM+select, 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
- * each written directly and transposed) + select, -1 = none yet. */
+ * each written directly and transposed) + select, 3 = pivot plan,
+ * symmetric (k <= 32, N >= 16384: per-row pivot = exact k-th distance over the first
+ * N/8 corpus points; the GEMM over the upper triangle keeps only elements <= pivot, for
+ * rows and, transposed, columns; exact select of the candidates — the quick multi-select
+ * partition of PAPER.md:56 applied at matrix scale), 4 = pivot plan, general block,
+ * -1 = none yet.  All plans give bit-identical results; a pivot call whose candidate
+ * buffer overflows (heavily tied data) is redone with the full matrix. */
 int knn_last_plan(knn_ctx_t ctx);
 
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by

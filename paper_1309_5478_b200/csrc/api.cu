@@ -33,6 +33,9 @@ struct knn_ctx {
     std::vector<Pending> pending;
     int plan = KNN_PLAN_AUTO;  // knn_set_plan / env KNN_FUSED
     bool sym_ok = true;        // env KNN_SYM=0 disables the symmetric k-NNG GEMM
+    bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
+    int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
+    int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;
     size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
     double prof_ms[5] = {0, 0, 0, 0, 0};
@@ -177,10 +180,17 @@ struct Prepared {
 // Queue the whole hot path for one block problem; asynchronous on `s`.
 knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
                      int32_t d, int32_t k, int32_t metric, int64_t self_shift, int64_t idx_offset,
-                     int32_t* out_idx, float* out_dist, cudaStream_t s) {
+                     int32_t* out_idx, float* out_dist, cudaStream_t s, bool allow_pivot = true) {
     const bool same = (Q == X) && (M == N);
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
     const bool fused = knn_fused_plan(ctx, k) == 1;
+    // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = exact k-th
+    // distance over a column sample, then the GEMM keeps only elements <= pivot.
+    const int64_t Ssamp = round_up(N / 8, 256);
+    const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
+                       ctx->plan != KNN_PLAN_MATERIALISED && Ssamp - 1 >= k;
+    const bool pivot_sym = pivot && same && self_shift == 0 && ctx->sym_ok;
+    const int32_t cap = ctx->pivot_cap;
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
     const int64_t ldD = round_up(N, 4);
     int64_t rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldD * sizeof(float)));
@@ -190,10 +200,17 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     if (fused) rows_blk = 0;  // no distance block
     // k-NNG with the transpose reuse of PAPER.md:83: only the upper triangle is multiplied
     // (bit-identical to the other plans thanks to the canonical orientation)
-    const bool sym = !fused && tc && ctx->sym_ok && same && self_shift == 0 &&
+    const bool sym = !fused && !pivot && tc && ctx->sym_ok && same && self_shift == 0 &&
                      (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
     if (sym) rows_blk = M;
-    ctx->last_plan = fused ? 1 : sym ? 2 : 0;
+    ctx->last_plan = fused ? 1 : pivot_sym ? 3 : pivot ? 4 : sym ? 2 : 0;
+    // pivot plan: the sample pass uses distance blocks of M' rows x Ssamp columns
+    const int64_t ldS = round_up(Ssamp, 4);
+    if (pivot) {
+        rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldS * sizeof(float)));
+        rows_blk = rows_blk < 128 ? 128 : (rows_blk / 128) * 128;
+        if (rows_blk > M) rows_blk = M;
+    }
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -205,7 +222,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         };
         prep(px, N);
         if (same) pq = px; else prep(pq, M);
-        D = c.take<float>((size_t)rows_blk * ldD);
+        D = c.take<float>((size_t)rows_blk * (pivot ? ldS : ldD));
     };
     Carve probe{nullptr};
     Prepared pq{}, px{};
@@ -213,11 +230,20 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int32_t* flag = nullptr;
     int32_t* part_i = nullptr;
     float* part_d = nullptr;
+    float* thr = nullptr;
+    int32_t* cnt = nullptr;
+    uint32_t *ckey = nullptr, *cidx = nullptr;
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
-        if (fused && S > 1) {
+        if ((fused && S > 1) || pivot) {
             part_i = c.take<int32_t>((size_t)S * M * k);
             part_d = c.take<float>((size_t)S * M * k);
+        }
+        if (pivot) {
+            thr = c.take<float>(M);
+            cnt = c.take<int32_t>(M);
+            ckey = c.take<uint32_t>((size_t)M * cap);
+            cidx = c.take<uint32_t>((size_t)M * cap);
         }
     };
     layout_all(probe);
@@ -249,6 +275,34 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             KNN_CUDA(knn::launch_merge(part_d, part_i, S, M, k, zeros, out_idx, out_dist, s));
             tm.done();
         }
+        return KNN_OK;
+    }
+    if (pivot) {
+        // 1. sample pass: exact k-NN of every query among the first Ssamp corpus points
+        for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
+            const int64_t R = (M - r0) < rows_blk ? (M - r0) : rows_blk;
+            const int64_t shift = self_shift == KNN_NO_SELF ? KNN_NO_SELF : self_shift + r0;
+            knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
+                               px.hi, px.lo, px.sqn, px.rs, Ssamp, d_pad};
+            Timed tg(ctx, KNN_KERNEL_GEMM, s);
+            KNN_CUDA(knn::launch_dist_tc(op, metric, shift, D, ldS, ctx->num_sms, s));
+            tg.done();
+            Timed ts(ctx, KNN_KERNEL_SELECT, s);
+            KNN_CUDA(knn::launch_select(D, R, Ssamp, ldS, k, 0, part_i + r0 * k, part_d + r0 * k, s));
+            ts.done();
+        }
+        // 2. pivots, 3. partition GEMM over the whole matrix, 4. exact select of candidates
+        Timed tp(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_pivot_prep(part_d, M, k, metric, thr, cnt, s));
+        tp.done();
+        knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        Timed tg(ctx, KNN_KERNEL_FUSED, s);
+        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
+                                           flag, ctx->num_sms, s));
+        tg.done();
+        Timed tc2(ctx, KNN_KERNEL_MERGE, s);
+        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, s));
+        tc2.done();
         return KNN_OK;
     }
     if (sym) {
@@ -287,9 +341,10 @@ knn_status finish_blocking(knn_ctx* ctx, cudaStream_t s) {
     int32_t* flag = static_cast<int32_t*>(ctx->ws);
     KNN_CUDA(cudaMemcpyAsync(ctx->flag_host, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     KNN_CUDA(cudaStreamSynchronize(s));
-    if (*ctx->flag_host)
+    if (*ctx->flag_host & 1)
         return fail(ctx, KNN_ERR_NONFINITE,
                     "input contains NaN/inf or a vector with ||x||^2 >= FLT_MAX/4");
+    if (*ctx->flag_host & 2) return KNN_ERR_INTERNAL;  // pivot candidates overflowed: redo
     return KNN_OK;
 }
 
@@ -337,6 +392,10 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     const char* fz = getenv("KNN_FUSED");
     if (fz && strcmp(fz, "0") == 0) c->plan = KNN_PLAN_MATERIALISED;
     if (fz && strcmp(fz, "1") == 0) c->plan = KNN_PLAN_FUSED;
+    const char* pv = getenv("KNN_PIVOT");
+    if (pv && strcmp(pv, "0") == 0) c->pivot_ok = false;
+    const char* pc = getenv("KNN_PIVOT_CAP");
+    if (pc) c->pivot_cap = atoi(pc) > 32 ? atoi(pc) : 32;
     const char* sy = getenv("KNN_SYM");
     if (sy && strcmp(sy, "0") == 0) c->sym_ok = false;
     const char* b = getenv("KNN_D_BUDGET_MB");
@@ -418,7 +477,14 @@ knn_status knn_search_block(knn_ctx_t ctx, const float* Q, int64_t M, const floa
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     KNN_TRY(run_block(ctx, Q, M, X, N, d, k, metric, self_shift, idx_offset, out_idx, out_dist, s));
-    return finish_blocking(ctx, s);
+    knn_status st = finish_blocking(ctx, s);
+    if (st == KNN_ERR_INTERNAL) {  // pivot plan overflowed (heavy ties): full matrix instead
+        ctx->pivot_redos++;
+        KNN_TRY(run_block(ctx, Q, M, X, N, d, k, metric, self_shift, idx_offset, out_idx, out_dist, s,
+                          false));
+        st = finish_blocking(ctx, s);
+    }
+    return st;
 }
 
 knn_status knn_graph(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
@@ -463,6 +529,15 @@ knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
     if (!same)
         KNN_CUDA(cudaMemcpyAsync(q, Q_host, (size_t)M * d * sizeof(float), cudaMemcpyHostToDevice, s));
     KNN_TRY(run_block(ctx, q, M, x, N, d, k, metric, self_shift, idx_offset, oi, od, s));
+    {
+        knn_status st0 = finish_blocking(ctx, s);
+        if (st0 == KNN_ERR_INTERNAL) {
+            ctx->pivot_redos++;
+            KNN_TRY(run_block(ctx, q, M, x, N, d, k, metric, self_shift, idx_offset, oi, od, s, false));
+        } else if (st0 != KNN_OK) {
+            return st0;
+        }
+    }
     KNN_CUDA(cudaMemcpyAsync(out_idx_host, oi, (size_t)M * k * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, s));
     KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)M * k * sizeof(float),

@@ -52,9 +52,31 @@ struct EpiArgs {
     const float* qn; const float* q_rs; int64_t M;
     const float* xn; const float* x_rs; int64_t N;
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
+    // PIVOT (partition epilogue): per-row pivots in the squared domain, candidate lists
+    const float* thr; int32_t* cnt; uint32_t* ckey; uint32_t* cidx; int32_t cap; int32_t* flag;
 };
 
-template <int METRIC, bool SYM, class Sched>
+// Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
+// materialised value max(u, 0) + 0 (+0 canonicalises -0), sqrt for L2.
+template <int METRIC>
+__device__ __forceinline__ float finalize_dist(float u) {
+    float dd = fmaxf(u, 0.0f) + 0.0f;
+    if (METRIC == 1) dd = sqrtf(dd);
+    return dd;
+}
+
+// Append candidate (key, column) to row r's list; counts overflow.
+__device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint32_t key, uint32_t col) {
+    const int pos = atomicAdd(ep.cnt + r, 1);
+    if (pos < ep.cap) {
+        ep.ckey[r * ep.cap + pos] = key;
+        ep.cidx[r * ep.cap + pos] = col;
+    } else {
+        *ep.flag |= 2;  // overflow: the caller redoes the problem with the full matrix
+    }
+}
+
+template <int METRIC, bool SYM, bool PIVOT, class Sched>
 __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -66,6 +88,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
     __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
+    __shared__ __align__(16) float col_t[PIVOT && SYM ? 2 : 1][BN];  // column pivots (SYM PIVOT)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* stage_base = smem;
     uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
@@ -96,7 +119,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
-        float pf_n = 0.0f, pf_s = 0.0f;  // next tile's column data, prefetched
+        float pf_n = 0.0f, pf_s = 0.0f, pf_t = 0.0f;  // next tile's column data, prefetched
         bool pf_ok = false;
         for (int64_t t = cid; t < sched.units(); t += ncl)
         for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ml_shift);
@@ -114,9 +137,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 const int64_t j = n0 + etid;
                 pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
                 pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+                if (PIVOT && SYM) pf_t = j < ep.N ? __ldg(ep.thr + j) : 0.0f;
             }
             col_n[buf][etid] = pf_n;
             col_s[buf][etid] = pf_s;
+            if constexpr (PIVOT && SYM) col_t[buf][etid] = pf_t;
             pf_ok = false;
             {
                 // next work item of this CTA (same unit's second pass, or the next unit)
@@ -127,6 +152,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     const int64_t j = sched.get(tn).nb0 * BN + etid;
                     pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
                     pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
+                    if (PIVOT && SYM) pf_t = j < ep.N ? __ldg(ep.thr + j) : 0.0f;
                     pf_ok = true;
                 }
             }
@@ -136,6 +162,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const bool row_ok = row < ep.M;
             const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
             const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
+            const float trow = PIVOT && row_ok ? __ldg(ep.thr + row) : -1.0f;  // row pivot
             const int64_t c_lo = n0 + half * (BN / 2);
             // does this warp's 32x(BN/2) block touch the excluded self pairs?
             const bool diag = ep.self_shift != INT64_MIN &&
@@ -168,10 +195,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int c = 4 * c4 + e;
-                        float dd = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
-                        dd = fmaxf(dd, 0.0f) + 0.0f;
-                        if (METRIC == 1) dd = sqrtf(dd);
-                        v[c] = dd;
+                        const float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
+                        v[c] = PIVOT ? u : finalize_dist<METRIC>(u);
                     }
                 }
                 const int64_t c0 = n0 + cb;
@@ -179,6 +204,50 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int c = 0; c < 32; ++c)
                         if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
+                }
+                if constexpr (PIVOT) {
+                    // Partition (quickselect): keep the elements at or below the
+                    // row's pivot as candidates; in SYM mode also the transposed element for
+                    // the column's row.  u is unclamped: max(u,0)+0 <= T implies u <= T.
+                    if (!row_ok) continue;
+                    if (SYM) {
+                        if (c0 < row0) continue;  // lower chunks: produced by their mirror
+                        if (c0 == row0) {        // diagonal chunk: keep col > row only
+                            #pragma unroll
+                            for (int c = 0; c < 32; ++c)
+                                if (c <= lane) v[c] = __int_as_float(0x7F800000);
+                        }
+                    } else if (tmask || diag) {
+                        #pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            const bool lower = row + ep.self_shift > c0 + c;
+                            if (c0 + c == self_col || (tmask && lower != (tmask == 2)))
+                                v[c] = __int_as_float(0x7F800000);
+                        }
+                    }
+                    if (c0 + 32 > ep.N) {
+                        #pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            if (c0 + c >= ep.N) v[c] = __int_as_float(0x7F800000);
+                    }
+                    const float* ct = &col_t[PIVOT && SYM ? buf : 0][cb];
+                    bool hit = false;
+                    #pragma unroll
+                    for (int c = 0; c < 32; ++c) hit |= (v[c] <= trow) | (SYM && v[c] <= ct[c]);
+                    if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+                    #pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const bool okr = v[c] <= trow;
+                        const bool okc = SYM && v[c] <= ct[c];
+                        if (__any_sync(0xFFFFFFFFu, okr || okc)) {
+                            if (okr || okc) {
+                                const uint32_t key = __float_as_uint(finalize_dist<METRIC>(v[c])) | 0x80000000u;
+                                if (okr) pivot_append(ep, row, key, (uint32_t)(c0 + c));
+                                if (okc) pivot_append(ep, c0 + c, key, (uint32_t)row);
+                            }
+                        }
+                    }
+                    continue;
                 }
                 if constexpr (SYM) {
                     // chunk rows [row0, +32) x cols [c0, +32), both global.  Below the
@@ -343,8 +412,9 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int64_t num_tiles = tiles.n_mp * tiles.n_nb;  // work units per CTA pair
     const int64_t pairs = num_tiles < num_sms / CLUSTER ? num_tiles : num_sms / CLUSTER;
     const int grid = (int)(pairs * CLUSTER);
-    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD};
-    auto kern = metric == 1 ? dist_tc_kernel<1, false, TileSched> : dist_tc_kernel<0, false, TileSched>;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD,
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+    auto kern = metric == 1 ? dist_tc_kernel<1, false, false, TileSched> : dist_tc_kernel<0, false, false, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     CUtensorMap md;
@@ -371,12 +441,50 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
     SymSched sched{ceil_div(op.N, BN)};
     const int64_t units = sched.n * (sched.n + 1) / 2;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD};
-    auto kern = metric == 1 ? dist_tc_kernel<1, true, SymSched> : dist_tc_kernel<0, true, SymSched>;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD,
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+    auto kern = metric == 1 ? dist_tc_kernel<1, true, false, SymSched> : dist_tc_kernel<0, true, false, SymSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 1, op.d_pad / BK,
                                                                 sched, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s) {
+    if (op.M == 0 || op.N == 0) return cudaSuccess;
+    if (sym && op.M != op.N) return cudaErrorInvalidValue;
+    CUtensorMap mqh, mql, mxh, mxl, md;
+    memset(&md, 0, sizeof md);
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
+        return cudaErrorInvalidValue;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, sym ? 0 : self_shift, nullptr, 0,
+               thr, cnt, ckey, cidx, cap, flag};
+    cudaError_t e;
+    if (sym) {
+        SymSched sched{ceil_div(op.N, BN)};
+        const int64_t units = sched.n * (sched.n + 1) / 2;
+        const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+        auto kern = metric == 1 ? dist_tc_kernel<1, true, true, SymSched> : dist_tc_kernel<0, true, true, SymSched>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+            return e;
+        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+                                                                    sched, ep);
+    } else {
+        TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+        const int64_t units = sched.n_mp * sched.n_nb;
+        const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+        auto kern = metric == 1 ? dist_tc_kernel<1, false, true, TileSched> : dist_tc_kernel<0, false, true, TileSched>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+            return e;
+        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+                                                                    sched, ep);
+    }
     return cudaGetLastError();
 }
 

@@ -52,6 +52,18 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
 // the upper triangle of 256x256 blocks, each also written transposed.
 cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, int64_t ldD,
                                int num_sms, cudaStream_t s);
+// Pivot (partition) plan: the GEMM keeps, per row, the elements at or below thr[row]
+// (squared domain) as candidates ckey/cidx[row*cap + i], i < cnt[row]; SYM also records
+// the transposed element for the column's row.  flag |= 2 on candidate overflow.
+cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
+// select.cu: pivots from a sample's k-th distances; exact select over candidate lists.
+cudaError_t launch_pivot_prep(const float* kth_dist, int64_t M, int32_t k, int32_t metric, float* thr,
+                              int32_t* cnt, cudaStream_t s);
+cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                    int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
+                                    int32_t* out_idx, float* out_dist, cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
 // fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial

@@ -879,6 +879,43 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
                           out_idx + row * k, out_dist + row * k);
 }
 
+// ------------------------------------------------------------------ pivot plan --------
+// Row pivots from the exact k-th distance of a column sample (an upper bound of the row's
+// k-th distance: the quickselect pivot of PAPER.md:56 chosen so that L >= K), in the
+// squared domain of the GEMM's filter (L2: RU(next(t)^2), so no true neighbour is rejected).
+__global__ void pivot_prep_kernel(const float* __restrict__ kth, int64_t M, int k, int metric,
+                                  float* __restrict__ thr, int32_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const float t = kth[i * k + k - 1];
+    // L2: every x with sqrt(x) rounding to <= t has sqrt(x) < next(t), so x <= RU(next(t)^2)
+    const float t1 = nextafterf(t, __int_as_float(0x7F800000));
+    thr[i] = metric == 1 ? __fmul_ru(t1, t1) : t;
+    cnt[i] = 0;
+}
+
+// Exact top-k (k <= 32) of each row's candidate list: warp per row, folds of 32.
+__global__ void __launch_bounds__(256)
+candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
+                        const uint32_t* __restrict__ cidx, int cap, int64_t M, int k,
+                        int64_t idx_offset, int32_t* __restrict__ out_idx,
+                        float* __restrict__ out_dist) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= M) return;
+    int n = cnt[row];
+    n = n < cap ? n : cap;
+    uint64_t L = ~0ull;
+    const uint32_t* rk = ckey + row * cap;
+    const uint32_t* ri = cidx + row * cap;
+    for (int o = 0; o < n; o += 32) L = ws::warp_merge32<1>(L, rk + o, ri + o, n - o < 32 ? n - o : 32);
+    if (lane < k) {
+        const uint32_t key = (uint32_t)(L >> 32);
+        out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)L + idx_offset);
+        out_dist[row * k + lane] = key == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(key);
+    }
+}
+
 int next_pow2(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -965,6 +1002,23 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
     if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
     kern<<<(unsigned)M, THREADS, smem, s>>>(D, N, ldD, k, cap, KP, limit, idx_offset, out_idx,
                                            out_dist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pivot_prep(const float* kth_dist, int64_t M, int32_t k, int32_t metric, float* thr,
+                              int32_t* cnt, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    pivot_prep_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, s>>>(kth_dist, M, k, metric, thr, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                    int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
+                                    int32_t* out_idx, float* out_dist, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    if (k > 32) return cudaErrorInvalidValue;
+    candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, ckey, cidx, cap, M, k, idx_offset,
+                                                                    out_idx, out_dist);
     return cudaGetLastError();
 }
 

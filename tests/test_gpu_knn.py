@@ -339,3 +339,58 @@ def test_symmetric_graph_equals_unsymmetric(N, d, k, metric):
     ri, rd = kn.search_block(Xt, Xt.clone(), k, metric=metric, self_shift=0)
     assert torch.equal(gi, ri)
     assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+# ------------------------------------------------------------------ pivot plan ---------
+@pytest.fixture
+def materialised_plan():
+    kn = knn()
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    yield kn
+    kn.set_plan(kn.PLAN_AUTO)
+
+
+@pytest.mark.parametrize("N,d,k,metric,dist", [(20000, 64, 32, 0, "uniform"), (17000, 128, 8, 1, "clusters"),
+                                               (16384, 3, 1, 0, "gauss")])
+def test_pivot_graph_equals_materialised(N, d, k, metric, dist):
+    kn = knn()
+    X = cuda(datagen.points(N, d, dist, seed=N + d + k))
+    gi, gd = kn.graph(X, k, metric=metric)
+    assert kn.last_plan() == 3
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(X, k, metric=metric)
+        assert kn.last_plan() != 3
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri)
+    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_pivot_search_blocks_equal_materialised():
+    kn = knn()
+    X = cuda(datagen.points(20000, 48, "gauss", seed=51))
+    Q = cuda(datagen.points(3000, 48, "gauss", seed=52))
+    gi, gd = kn.search_block(Q, X, 20)
+    assert kn.last_plan() == 4
+    ai, ad = kn.search_block(X[5000:9000].contiguous(), X, 16, self_shift=5000)
+    assert kn.last_plan() == 4
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.search_block(Q, X, 20)
+        bi, bd = kn.search_block(X[5000:9000].contiguous(), X, 16, self_shift=5000)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri) and torch.equal(gd, rd)
+    assert torch.equal(ai, bi) and torch.equal(ad, bd)
+
+
+def test_pivot_overflow_falls_back_exactly():
+    # integer grid in d=4: enormous numbers of tied distances overflow the candidate
+    # buffers; the call is redone on the full matrix and stays exact (E2E-3)
+    X = datagen.points(16384, 4, "grid", seed=53)
+    gi, gd = run_graph(X, 32)
+    rows = np.arange(0, 16384, 257)
+    ref = oracle.knn(X, X, 32, rows=rows, graph=True)
+    assert np.array_equal(gi[rows], ref["idx32"])
+    assert np.array_equal(gd[rows], ref["dist32"])

@@ -62,6 +62,16 @@ __global__ void warp_ring(const float* __restrict__ D, int64_t rows, int64_t row
     if (acc == 12345.f) out[0] = acc;
 }
 
+__global__ void stg_kernel(float4* __restrict__ p, size_t n4) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+    for (; i + 7 * st < n4; i += 8 * st) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + i + j * st), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    }
+}
+
 template <class F>
 float timeit(F f) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -76,7 +86,19 @@ int main() {
     float* out; cudaMalloc(&out, 4);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     size_t n4 = bytes / 16;
-  for (int pass = 0; pass < 3; ++pass) {
+    for (int bpsm : {2, 4, 8}) {
+        float ms = timeit([&] { stg_kernel<<<sms * bpsm, 256>>>((float4*)D, n4); });
+        printf("stg128 (write only) 256thr x %d CTA/SM: %.0f GB/s\n", bpsm, bytes / ms / 1e6);
+    }
+    {
+        float ms = timeit([&] { cudaMemsetAsync(D, 1, bytes); });
+        printf("cudaMemset (write only): %.0f GB/s\n", bytes / ms / 1e6);
+        float* E; cudaMalloc(&E, bytes);
+        ms = timeit([&] { cudaMemcpyAsync(E, D, bytes, cudaMemcpyDeviceToDevice); });
+        printf("cudaMemcpy D2D (read+write counted): %.0f GB/s\n", 2.0 * bytes / ms / 1e6);
+        cudaFree(E);
+    }
+  for (int pass = 0; pass < 1; ++pass) {
     if (pass == 1) { fill<<<sms * 8, 256>>>(D, bytes / 4); cudaDeviceSynchronize(); printf("--- random data\n"); }
     if (pass == 2) { int one = 1; cudaMemcpyToSymbol(g_policy_mode, &one, sizeof(int)); printf("--- random data + evict_first policy\n"); }
     for (int bpsm : {2, 4, 8}) {
