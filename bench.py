@@ -269,7 +269,8 @@ def run_ours(args):
     def tensor_roof(name, kernel, ms, n, rows_per_launch):
         avg = ms / max(n, 1)
         pairs = rows_per_launch * N
-        if plan_code == 2:  # symmetric: only the upper triangle of 256x256 blocks is multiplied
+        if plan_code in (2, 3) and kernel != "dist_tc_kernel_sample":
+            # symmetric: only the upper triangle of 256x256 blocks is multiplied
             nblk = -(-N // 256)
             pairs = nblk * (nblk + 1) / 2 * 256.0 * 256.0
         flop = 3 * 2.0 * pairs * d_pad  # 3 fp16 products per multiply-add
@@ -298,10 +299,23 @@ def run_ours(args):
     s_ms, s_n = prof["select"]
     m_ms, m_n = prof["merge"]
     p_ms, p_n = prof["prep"]
-    if f_n:
+    if f_n and plan_code in (3, 4):
+        rooflines.append((f_ms, tensor_roof(
+            "dist_tc_kernel<PIVOT%s> (a-S5: GEMM with the quickselect partition in its epilogue)"
+            % (",SYM" if plan_code == 3 else ""), "dist_tc_kernel", f_ms, f_n, R_local)))
+    elif f_n:
         rooflines.append((f_ms, tensor_roof("knn_fused_kernel (a-S5: a-S3 GEMM + a-S4 select in the epilogue)",
                                             "knn_fused_kernel", f_ms, f_n, R_local)))
-    if g_n:
+    if g_n and plan_code in (3, 4):
+        S_samp = -(-(N // 8) // 256) * 256
+        gr = tensor_roof("dist_tc_kernel (pivot sample pass: rows x first N/8 columns)",
+                         "dist_tc_kernel_sample", g_ms, g_n, R_local)
+        avg = g_ms / g_n
+        flop = 6.0 * R_local * S_samp * d_pad
+        gr.update({"achieved": flop / (avg * 1e-3) / 1e12, "useful_tflops": 2.0 * R_local * S_samp * d / (avg * 1e-3) / 1e12})
+        gr["frac"] = gr["achieved"] / gr["peak"]
+        rooflines.append((g_ms, gr))
+    elif g_n:
         gl = max(g_n // args.steps, 1)
         gr = tensor_roof("dist_tc_kernel (a-S3)", "dist_tc_kernel", g_ms, g_n, R_local / gl)
         if plan_code == 2:
@@ -318,9 +332,14 @@ def run_ours(args):
         rooflines.append((g_ms, gr))
     if s_n:
         sl = max(s_n // args.steps, 1)
-        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4)", "select_warp_kernel", s_ms, s_n,
-                                         R_local / sl * (N * 4.0 + k * 8.0))))
-    if m_n:
+        ncols = -(-(N // 8) // 256) * 256 if plan_code in (3, 4) else N
+        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4%s)" % (
+            ", pivot sample rows" if plan_code in (3, 4) else ""), "select_warp_kernel", s_ms, s_n,
+            R_local / sl * (ncols * 4.0 + k * 8.0))))
+    if m_n and plan_code in (3, 4):
+        rooflines.append((m_ms, hbm_roof("candidate_select_kernel (exact select of the partition)",
+                                         "candidate_select_kernel", m_ms, m_n, R_local * (4.0 + k * 8.0))))
+    elif m_n:
         # partial lists per row merged (fused split-N, same rule as fused.cu's fused_splits)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         n_mp, n_nb, ncl = -(-(-(-R_local // 128)) // 2), -(-N // 256), sms // 2
@@ -335,7 +354,9 @@ def run_ours(args):
                               "select": s_ms / total_ms, "merge": m_ms / total_ms,
                               "prep": p_ms / total_ms}
     roofline["plan"] = {0: "blocked distances + select", 1: "fused GEMM+select",
-                        2: "symmetric k-NNG distances (PAPER.md:83 transpose reuse) + select"}.get(
+                        2: "symmetric k-NNG distances (PAPER.md:83 transpose reuse) + select",
+                        3: "pivot (quickselect partition, PAPER.md:56) over the symmetric GEMM",
+                        4: "pivot (quickselect partition, PAPER.md:56) over the GEMM"}.get(
                             plan_code, "unknown")
 
     # ---- e2e: the public host-buffer API, H2D of the inputs and D2H of the results inside

@@ -65,6 +65,30 @@ __device__ __forceinline__ float finalize_dist(float u) {
     return dd;
 }
 
+// Candidates found by a warp are first pushed to a warp-local shared list (row, col, key)
+// and flushed to the global per-row lists 32 at a time, so the returning global atomics
+// run in parallel across lanes instead of one survivor at a time.
+constexpr int PEND_CAP = 320;  // 12-byte entries in one 4 KB staging buffer
+struct PendEntry {
+    uint32_t row, col, key;
+};
+__device__ __forceinline__ void pivot_append(const struct EpiArgs& ep, int64_t r, uint32_t key, uint32_t col);
+__device__ __forceinline__ void pivot_push(const struct EpiArgs& ep, PendEntry* pend, int* pcnt, int64_t r,
+                                           uint32_t col, uint32_t key) {
+    const int pos = atomicAdd(pcnt, 1);
+    if (pos < PEND_CAP) pend[pos] = {(uint32_t)r, col, key};
+    else pivot_append(ep, r, key, col);  // list full (adversarial ties): direct
+}
+__device__ __forceinline__ void pivot_flush(const struct EpiArgs& ep, PendEntry* pend, int* pcnt) {
+    const int lane = threadIdx.x & 31;
+    int n = *pcnt;
+    n = n < PEND_CAP ? n : PEND_CAP;
+    for (int i = lane; i < n; i += 32) pivot_append(ep, pend[i].row, pend[i].key, pend[i].col);
+    __syncwarp();
+    if (lane == 0) *pcnt = 0;
+    __syncwarp();
+}
+
 // Append candidate (key, column) to row r's list; counts overflow.
 __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint32_t key, uint32_t col) {
     const int pos = atomicAdd(ep.cnt + r, 1);
@@ -121,6 +145,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         int it = 0;
         float pf_n = 0.0f, pf_s = 0.0f, pf_t = 0.0f;  // next tile's column data, prefetched
         bool pf_ok = false;
+        // PIVOT: the warp's pending-candidate list lives in its second staging buffer
+        PendEntry* pend = reinterpret_cast<PendEntry*>(stg_base + ((warp - 2) * 2 + 1) * STG_BYTES);
+        __shared__ int pend_cnt[EPI_WARPS];
+        int* pcnt = &pend_cnt[warp - 2];
+        if (PIVOT && lane == 0) *pcnt = 0;
+        __syncwarp();
         for (int64_t t = cid; t < sched.units(); t += ncl)
         for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ml_shift);
              pass < tile_passes(cls); ++pass, ++it) {
@@ -209,7 +239,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     // Partition (quickselect): keep the elements at or below the
                     // row's pivot as candidates; in SYM mode also the transposed element for
                     // the column's row.  u is unclamped: max(u,0)+0 <= T implies u <= T.
-                    if (!row_ok) continue;
+                    if (!row_ok) {  // rows past M are masked, not skipped: the warp votes below
+                        #pragma unroll
+                        for (int c = 0; c < 32; ++c) v[c] = __int_as_float(0x7F800000);
+                    }
                     if (SYM) {
                         if (c0 < row0) continue;  // lower chunks: produced by their mirror
                         if (c0 == row0) {        // diagonal chunk: keep col > row only
@@ -231,22 +264,30 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             if (c0 + c >= ep.N) v[c] = __int_as_float(0x7F800000);
                     }
                     const float* ct = &col_t[PIVOT && SYM ? buf : 0][cb];
-                    bool hit = false;
+                    uint32_t hm = 0;  // this row's survivors in the chunk (row side or column side)
                     #pragma unroll
-                    for (int c = 0; c < 32; ++c) hit |= (v[c] <= trow) | (SYM && v[c] <= ct[c]);
-                    if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+                    for (int c = 0; c < 32; ++c)
+                        hm |= (uint32_t)((v[c] <= trow) | (SYM && v[c] <= ct[c])) << c;
+                    if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
+                    // stage the chunk's values (swizzled, conflict-free) so that each lane can
+                    // walk its own survivors with dynamic indices
+                    const uint32_t sv = smem_u32(stg_base + ((warp - 2) * 2) * STG_BYTES);
                     #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const bool okr = v[c] <= trow;
-                        const bool okc = SYM && v[c] <= ct[c];
-                        if (__any_sync(0xFFFFFFFFu, okr || okc)) {
-                            if (okr || okc) {
-                                const uint32_t key = __float_as_uint(finalize_dist<METRIC>(v[c])) | 0x80000000u;
-                                if (okr) pivot_append(ep, row, key, (uint32_t)(c0 + c));
-                                if (okc) pivot_append(ep, c0 + c, key, (uint32_t)row);
-                            }
-                        }
+                    for (int u = 0; u < 8; ++u)
+                        sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
+                               v[4 * u + 2], v[4 * u + 3]);
+                    __syncwarp();
+                    const float* svp = reinterpret_cast<const float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    while (hm) {
+                        const int c = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
+                        const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
+                        if (x <= trow) pivot_push(ep, pend, pcnt, row, (uint32_t)(c0 + c), key);
+                        if (SYM && x <= ct[c]) pivot_push(ep, pend, pcnt, c0 + c, (uint32_t)row, key);
                     }
+                    __syncwarp();
+                    if (*pcnt >= 32) pivot_flush(ep, pend, pcnt);
                     continue;
                 }
                 if constexpr (SYM) {
@@ -336,6 +377,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             }
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
+        if constexpr (PIVOT) {
+            __syncwarp();
+            pivot_flush(ep, pend, pcnt);
+        }
     }
     teardown(tmem_base);
 }
