@@ -307,7 +307,7 @@ def run_ours(args):
         rooflines.append((f_ms, tensor_roof("knn_fused_kernel (a-S5: a-S3 GEMM + a-S4 select in the epilogue)",
                                             "knn_fused_kernel", f_ms, f_n, R_local)))
     if g_n and plan_code in (3, 4):
-        S_samp = -(-(N // 8) // 256) * 256
+        S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
         gr = tensor_roof("dist_tc_kernel (pivot sample pass: rows x first N/8 columns)",
                          "dist_tc_kernel_sample", g_ms, g_n, R_local)
         avg = g_ms / g_n
@@ -332,7 +332,7 @@ def run_ours(args):
         rooflines.append((g_ms, gr))
     if s_n:
         sl = max(s_n // args.steps, 1)
-        ncols = -(-(N // 8) // 256) * 256 if plan_code in (3, 4) else N
+        ncols = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256 if plan_code in (3, 4) else N
         rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4%s)" % (
             ", pivot sample rows" if plan_code in (3, 4) else ""), "select_warp_kernel", s_ms, s_n,
             R_local / sl * (ncols * 4.0 + k * 8.0))))

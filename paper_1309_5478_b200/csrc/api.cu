@@ -35,6 +35,7 @@ struct knn_ctx {
     bool sym_ok = true;        // env KNN_SYM=0 disables the symmetric k-NNG GEMM
     bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
     int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
+    int32_t pivot_div = 8;     // sample = the first N / pivot_div corpus points
     int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;
     size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
@@ -186,7 +187,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     const bool fused = knn_fused_plan(ctx, k) == 1;
     // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = exact k-th
     // distance over a column sample, then the GEMM keeps only elements <= pivot.
-    const int64_t Ssamp = round_up(N / 8, 256);
+    const int64_t Ssamp = round_up(N / ctx->pivot_div, 256);
     const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
                        ctx->plan != KNN_PLAN_MATERIALISED && Ssamp - 1 >= k;
     const bool pivot_sym = pivot && same && self_shift == 0 && ctx->sym_ok;
@@ -394,6 +395,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     if (fz && strcmp(fz, "1") == 0) c->plan = KNN_PLAN_FUSED;
     const char* pv = getenv("KNN_PIVOT");
     if (pv && strcmp(pv, "0") == 0) c->pivot_ok = false;
+    const char* pd = getenv("KNN_PIVOT_DIV");
+    if (pd && atoi(pd) >= 2) c->pivot_div = atoi(pd);
     const char* pc = getenv("KNN_PIVOT_CAP");
     if (pc) c->pivot_cap = atoi(pc) > 32 ? atoi(pc) : 32;
     const char* sy = getenv("KNN_SYM");
