@@ -308,7 +308,7 @@ def run_ours(args):
                                             "knn_fused_kernel", f_ms, f_n, R_local)))
     if g_n and plan_code in (3, 4):
         S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
-        gr = tensor_roof("dist_tc_kernel (pivot sample pass: rows x first N/8 columns)",
+        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x first N/8 columns -> 32-column chunk minima)",
                          "dist_tc_kernel_sample", g_ms, g_n, R_local)
         avg = g_ms / g_n
         flop = 6.0 * R_local * S_samp * d_pad

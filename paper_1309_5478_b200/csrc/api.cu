@@ -185,11 +185,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     const bool same = (Q == X) && (M == N);
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
     const bool fused = knn_fused_plan(ctx, k) == 1;
-    // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = exact k-th
-    // distance over a column sample, then the GEMM keeps only elements <= pivot.
+    // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = k-th smallest of
+    // the minima of the 32-column chunks of a column sample (>= the row's k-th distance),
+    // then the GEMM keeps only elements <= pivot.
     const int64_t Ssamp = round_up(N / ctx->pivot_div, 256);
     const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
-                       ctx->plan != KNN_PLAN_MATERIALISED && Ssamp - 1 >= k;
+                       ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= k + 1;
     const bool pivot_sym = pivot && same && self_shift == 0 && ctx->sym_ok;
     const int32_t cap = ctx->pivot_cap;
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
@@ -205,13 +206,6 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                      (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
     if (sym) rows_blk = M;
     ctx->last_plan = fused ? 1 : pivot_sym ? 3 : pivot ? 4 : sym ? 2 : 0;
-    // pivot plan: the sample pass uses distance blocks of M' rows x Ssamp columns
-    const int64_t ldS = round_up(Ssamp, 4);
-    if (pivot) {
-        rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldS * sizeof(float)));
-        rows_blk = rows_blk < 128 ? 128 : (rows_blk / 128) * 128;
-        if (rows_blk > M) rows_blk = M;
-    }
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -223,7 +217,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         };
         prep(px, N);
         if (same) pq = px; else prep(pq, M);
-        D = c.take<float>((size_t)rows_blk * (pivot ? ldS : ldD));
+        D = c.take<float>(pivot ? (size_t)(Ssamp / 32) * M : (size_t)rows_blk * ldD);
     };
     Carve probe{nullptr};
     Prepared pq{}, px{};
@@ -236,7 +230,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     uint32_t *ckey = nullptr, *cidx = nullptr;
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
-        if ((fused && S > 1) || pivot) {
+        if (fused && S > 1) {
             part_i = c.take<int32_t>((size_t)S * M * k);
             part_d = c.take<float>((size_t)S * M * k);
         }
@@ -279,23 +273,18 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         return KNN_OK;
     }
     if (pivot) {
-        // 1. sample pass: exact k-NN of every query among the first Ssamp corpus points
-        for (int64_t r0 = 0; r0 < M; r0 += rows_blk) {
-            const int64_t R = (M - r0) < rows_blk ? (M - r0) : rows_blk;
-            const int64_t shift = self_shift == KNN_NO_SELF ? KNN_NO_SELF : self_shift + r0;
-            knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
-                               px.hi, px.lo, px.sqn, px.rs, Ssamp, d_pad};
+        // 1. sample pass: per-row minima of 32-column chunks over the first Ssamp corpus
+        //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
+        {
+            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, Ssamp, d_pad};
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc(op, metric, shift, D, ldS, ctx->num_sms, s));
+            KNN_CUDA(knn::launch_dist_tc_mins(op, metric, self_shift, D, ctx->num_sms, s));
             tg.done();
-            Timed ts(ctx, KNN_KERNEL_SELECT, s);
-            KNN_CUDA(knn::launch_select(D, R, Ssamp, ldS, k, 0, part_i + r0 * k, part_d + r0 * k, s));
-            ts.done();
+            Timed tp(ctx, KNN_KERNEL_PREP, s);
+            KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, k, metric, thr, cnt, s));
+            tp.done();
         }
-        // 2. pivots, 3. partition GEMM over the whole matrix, 4. exact select of candidates
-        Timed tp(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_pivot_prep(part_d, M, k, metric, thr, cnt, s));
-        tp.done();
+        // 3. partition GEMM over the whole matrix, 4. exact select of the candidates
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
         Timed tg(ctx, KNN_KERNEL_FUSED, s);
         KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,

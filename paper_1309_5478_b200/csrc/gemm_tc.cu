@@ -100,7 +100,11 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
     }
 }
 
-template <int METRIC, bool SYM, bool PIVOT, class Sched>
+// Epilogue modes: MODE_STORE writes D; MODE_PIVOT keeps the partition's candidates;
+// MODE_MINS writes, per row, the minimum distance of every 32-column chunk.
+enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2 };
+
+template <int METRIC, bool SYM, int MODE, class Sched>
 __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -108,6 +112,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                Sched sched, EpiArgs ep) {
     // SYM: upper-triangle pair blocks only, O1 everywhere (every element has i < j or is
     // mirrored from one), so the mainloop sees no self shift.
+    constexpr bool PIVOT = MODE == MODE_PIVOT;
+    constexpr bool MINS = MODE == MODE_MINS;
     const int64_t ml_shift = SYM ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
@@ -226,7 +232,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     for (int e = 0; e < 4; ++e) {
                         const int c = 4 * c4 + e;
                         const float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
-                        v[c] = PIVOT ? u : finalize_dist<METRIC>(u);
+                        v[c] = (PIVOT || MINS) ? u : finalize_dist<METRIC>(u);
                     }
                 }
                 const int64_t c0 = n0 + cb;
@@ -234,6 +240,32 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int c = 0; c < 32; ++c)
                         if (c0 + c == self_col) v[c] = __int_as_float(0x7F800000);
+                }
+                if constexpr (MINS) {
+                    // pivot sample pass: the chunk's minimum distance for this row (the self
+                    // pair was set to +inf above; a block straddling the diagonal comes in two
+                    // masked passes, the second folds into the first's value)
+                    if (tmask) {
+                        #pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            const bool lower = row + ep.self_shift > c0 + c;
+                            if (lower != (tmask == 2)) v[c] = __int_as_float(0x7F800000);
+                        }
+                    }
+                    float m[16];
+                    #pragma unroll
+                    for (int c = 0; c < 16; ++c) m[c] = fminf(v[c], v[c + 16]);
+                    #pragma unroll
+                    for (int wdt = 8; wdt > 0; wdt >>= 1)
+                        #pragma unroll
+                        for (int c = 0; c < wdt; ++c) m[c] = fminf(m[c], m[c + wdt]);
+                    if (row_ok && c0 < ep.N) {
+                        float* dst = ep.D + (c0 >> 5) * ep.ldD + row;  // mins[chunk][row]
+                        float mn = m[0] == __int_as_float(0x7F800000) ? m[0] : finalize_dist<METRIC>(m[0]);
+                        if (tmask == 2) mn = fminf(mn, *dst);
+                        *dst = mn;
+                    }
+                    continue;
                 }
                 if constexpr (PIVOT) {
                     // Partition (quickselect): keep the elements at or below the
@@ -459,7 +491,7 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int grid = (int)(pairs * CLUSTER);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD,
                nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-    auto kern = metric == 1 ? dist_tc_kernel<1, false, false, TileSched> : dist_tc_kernel<0, false, false, TileSched>;
+    auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_STORE, TileSched> : dist_tc_kernel<0, false, MODE_STORE, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     CUtensorMap md;
@@ -488,10 +520,35 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD,
                nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-    auto kern = metric == 1 ? dist_tc_kernel<1, true, false, SymSched> : dist_tc_kernel<0, true, false, SymSched>;
+    auto kern = metric == 1 ? dist_tc_kernel<1, true, MODE_STORE, SymSched> : dist_tc_kernel<0, true, MODE_STORE, SymSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 1, op.d_pad / BK,
+                                                                sched, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t self_shift, float* mins,
+                                int num_sms, cudaStream_t s) {
+    if (op.M == 0 || op.N == 0) return cudaSuccess;
+    if (op.N % 32 != 0) return cudaErrorInvalidValue;
+    CUtensorMap mqh, mql, mxh, mxl, md;
+    memset(&md, 0, sizeof md);
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
+        return cudaErrorInvalidValue;
+    // mins is [N/32][M]: ep.D / ep.ldD reused as its base / row stride
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+    const int64_t units = sched.n_mp * sched.n_nb;
+    const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+    auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
                                                                 sched, ep);
     return cudaGetLastError();
 }
@@ -515,7 +572,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         SymSched sched{ceil_div(op.N, BN)};
         const int64_t units = sched.n * (sched.n + 1) / 2;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric == 1 ? dist_tc_kernel<1, true, true, SymSched> : dist_tc_kernel<0, true, true, SymSched>;
+        auto kern = metric == 1 ? dist_tc_kernel<1, true, MODE_PIVOT, SymSched> : dist_tc_kernel<0, true, MODE_PIVOT, SymSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
@@ -524,7 +581,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
         const int64_t units = sched.n_mp * sched.n_nb;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric == 1 ? dist_tc_kernel<1, false, true, TileSched> : dist_tc_kernel<0, false, true, TileSched>;
+        auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_PIVOT, TileSched> : dist_tc_kernel<0, false, MODE_PIVOT, TileSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,

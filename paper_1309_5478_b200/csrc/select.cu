@@ -894,6 +894,34 @@ __global__ void pivot_prep_kernel(const float* __restrict__ kth, int64_t M, int 
     cnt[i] = 0;
 }
 
+// Pivot from chunk minima: the k-th smallest of the row's nchunk chunk minima (mins is
+// [nchunk][M]).  At least k elements of the row are <= it (one per chunk), so it bounds the
+// row's k-th distance from above: a quickselect pivot with L >= K.  Warp per row, folds of 32.
+__global__ void __launch_bounds__(256)
+pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int k, int metric,
+                       float* __restrict__ thr, int32_t* __restrict__ cnt) {
+    __shared__ uint32_t skey[8][32], sidx[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * 8 + w;
+    if (row >= M) return;
+    uint64_t L = ~0ull;
+    for (int64_t o = 0; o < nchunk; o += 32) {
+        const int64_t c = o + lane;
+        skey[w][lane] = c < nchunk ? ukey(mins[c * M + row]) : 0xFFFFFFFFu;
+        sidx[w][lane] = (uint32_t)c;
+        __syncwarp();
+        L = ws::warp_merge32<1>(L, skey[w], sidx[w], 32);
+        __syncwarp();
+    }
+    const uint32_t tk = (uint32_t)(__shfl_sync(FULL, L, k - 1) >> 32);
+    if (lane == 0) {
+        const float t = tk == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(tk);
+        const float t1 = nextafterf(t, __int_as_float(0x7F800000));
+        thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
+        cnt[row] = 0;
+    }
+}
+
 // Exact top-k (k <= 32) of each row's candidate list: warp per row, folds of 32.
 __global__ void __launch_bounds__(256)
 candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
@@ -1009,6 +1037,14 @@ cudaError_t launch_pivot_prep(const float* kth_dist, int64_t M, int32_t k, int32
                               int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     pivot_prep_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, s>>>(kth_dist, M, k, metric, thr, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
+                                   int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    if (k > 32 || nchunk < k) return cudaErrorInvalidValue;
+    pivot_from_mins_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
     return cudaGetLastError();
 }
 
