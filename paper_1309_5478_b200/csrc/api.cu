@@ -210,8 +210,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
         auto prep = [&](Prepared& p, int64_t n) {
-            p.sqn = c.take<float>(n);
-            p.rs = c.take<float>(n);
+            p.sqn = c.take<float>(round_up(n, knn::kColPad));
+            p.rs = c.take<float>(round_up(n, knn::kColPad));
             p.hi = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
             p.lo = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
         };
@@ -235,7 +235,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             part_d = c.take<float>((size_t)S * M * k);
         }
         if (pivot) {
-            thr = c.take<float>(M);
+            thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
             ckey = c.take<uint32_t>((size_t)M * cap);
             cidx = c.take<uint32_t>((size_t)M * cap);
@@ -569,8 +569,8 @@ knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, int32_t*& flag) {
         flag = c.take<int32_t>(4);
         auto prep = [&](Prepared& p, int64_t n) {
-            p.sqn = c.take<float>(n);
-            p.rs = c.take<float>(n);
+            p.sqn = c.take<float>(round_up(n, knn::kColPad));
+            p.rs = c.take<float>(round_up(n, knn::kColPad));
             p.hi = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
             p.lo = tc ? c.take<__half>((size_t)n * d_pad) : nullptr;
         };

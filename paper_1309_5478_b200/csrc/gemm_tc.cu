@@ -41,16 +41,21 @@ using namespace tc;
 
 constexpr int STAGES = 3;
 constexpr int EPI_WARPS = 8;     // 2 per TMEM lane quadrant, each owning BN/2 columns
-constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int COL_WARP = 2 + EPI_WARPS;  // column-data producer (one elected thread)
+constexpr int THREADS = 64 + 32 * EPI_WARPS + 32;
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 output chunk (TMA-store staging)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 1024 /*align*/ +
-                           1024 /*barriers*/;
+// Column data of a tile (||x_j||^2, 2^-sh_j and, SYM PIVOT, the column pivots), bulk-copied
+// by COL_WARP into an NCOL-deep ring so the epilogue warps never wait on each other.
+constexpr int NCOL = 4;
+constexpr int COL_BYTES = 3 * BN * 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + NCOL * COL_BYTES +
+                           1024 /*align*/ + 1024 /*barriers*/;
 // SYM (symmetric k-NNG): each warp's two staging buffers hold the direct and the transposed
 // chunk of the same 32x32 block.
 
 struct EpiArgs {
     const float* qn; const float* q_rs; int64_t M;
-    const float* xn; const float* x_rs; int64_t N;
+    const float* xn; const float* x_rs; int64_t N;  // column arrays padded to 256 entries
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
     // PIVOT (partition epilogue): per-row pivots in the squared domain, candidate lists
     const float* thr; int32_t* cnt; uint32_t* ckey; uint32_t* cidx; int32_t cap; int32_t* flag;
@@ -65,31 +70,7 @@ __device__ __forceinline__ float finalize_dist(float u) {
     return dd;
 }
 
-// Candidates found by a warp are first pushed to a warp-local shared list (row, col, key)
-// and flushed to the global per-row lists 32 at a time, so the returning global atomics
-// run in parallel across lanes instead of one survivor at a time.
-constexpr int PEND_CAP = 320;  // 12-byte entries in one 4 KB staging buffer
-struct PendEntry {
-    uint32_t row, col, key;
-};
-__device__ __forceinline__ void pivot_append(const struct EpiArgs& ep, int64_t r, uint32_t key, uint32_t col);
-__device__ __forceinline__ void pivot_push(const struct EpiArgs& ep, PendEntry* pend, int* pcnt, int64_t r,
-                                           uint32_t col, uint32_t key) {
-    const int pos = atomicAdd(pcnt, 1);
-    if (pos < PEND_CAP) pend[pos] = {(uint32_t)r, col, key};
-    else pivot_append(ep, r, key, col);  // list full (adversarial ties): direct
-}
-__device__ __forceinline__ void pivot_flush(const struct EpiArgs& ep, PendEntry* pend, int* pcnt) {
-    const int lane = threadIdx.x & 31;
-    int n = *pcnt;
-    n = n < PEND_CAP ? n : PEND_CAP;
-    for (int i = lane; i < n; i += 32) pivot_append(ep, pend[i].row, pend[i].key, pend[i].col);
-    __syncwarp();
-    if (lane == 0) *pcnt = 0;
-    __syncwarp();
-}
-
-// Append candidate (key, column) to row r's list; counts overflow.
+// Append candidate (key, column) to row r's global list; counts overflow.
 __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint32_t key, uint32_t col) {
     const int pos = atomicAdd(ep.cnt + r, 1);
     if (pos < ep.cap) {
@@ -98,6 +79,41 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
     } else {
         *ep.flag |= 2;  // overflow: the caller redoes the problem with the full matrix
     }
+}
+
+// Candidates found by a warp are first appended to a warp-private shared list (SoA: row,
+// col, key) and flushed to the global per-row lists in batches of up to PEND_CAP, four
+// returning atomics in flight per lane, so their latency is paid once per batch.
+constexpr int PEND_CAP = 320;  // 3 x 320 x 4 B in one 4 KB staging buffer
+__device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* prow, const uint32_t* pcol,
+                                            const uint32_t* pkey, int n) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    for (int i0 = 0; i0 < n; i0 += 128) {
+        int pos[4];
+        uint32_t r[4];
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + 32 * j + lane;
+            if (i < n) {
+                r[j] = prow[i];
+                pos[j] = atomicAdd(ep.cnt + r[j], 1);
+            }
+        }
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + 32 * j + lane;
+            if (i < n) {
+                if (pos[j] < ep.cap) {
+                    ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = pkey[i];
+                    ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = pcol[i];
+                } else {
+                    *ep.flag |= 2;
+                }
+            }
+        }
+    }
+    __syncwarp();
 }
 
 // Epilogue modes: MODE_STORE writes D; MODE_PIVOT keeps the partition's candidates;
@@ -114,21 +130,29 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     // mirrored from one), so the mainloop sees no self shift.
     constexpr bool PIVOT = MODE == MODE_PIVOT;
     constexpr bool MINS = MODE == MODE_MINS;
+    constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
     const int64_t ml_shift = SYM ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(16) float col_n[2][BN];  // ||x_j||^2 of the tile's columns
-    __shared__ __align__(16) float col_s[2][BN];  // 2^-sh_j of the tile's columns
-    __shared__ __align__(16) float col_t[PIVOT && SYM ? 2 : 1][BN];  // column pivots (SYM PIVOT)
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
     uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + EPI_WARPS * 2 * STG_BYTES);
+    float* col_base = reinterpret_cast<float*>(stg_base + EPI_WARPS * 2 * STG_BYTES);  // [NCOL][3][BN]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(col_base) + NCOL * COL_BYTES);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    const uint32_t colfull0 = smem_u32(bars + 2 * STAGES + 5);
+    const uint32_t colempty0 = colfull0 + 8 * NCOL;
     const Bars b{smem_u32(bars), smem_u32(bars + STAGES), smem_u32(bars + 2 * STAGES),
                  smem_u32(bars + 2 * STAGES + 2)};
     const uint32_t tfull0 = b.tfull0, tempty0 = b.tempty0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < NCOL; ++i) {
+            mbar_init(colfull0 + 8 * i, 1);
+            mbar_init(colempty0 + 8 * i, EPI_WARPS);
+        }
+    }
     const uint32_t tmem_base = setup(bars, STAGES, EPI_WARPS, tmem_slot, &map_qh, 1);
     const uint32_t crank = cluster_rank();
     const int64_t cid = blockIdx.x / CLUSTER, ncl = gridDim.x / CLUSTER;
@@ -141,58 +165,45 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     } else if (warp == 1) {
         if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
         __syncwarp();
+    } else if (warp == COL_WARP) {
+        // ------------------------------------------- column data of each work item --
+        if (lane == 0) {
+            int it = 0;
+            for (int64_t t = cid; t < sched.units(); t += ncl) {
+                const tc::Unit w = sched.get(t);
+                const int cls = tile_class(w.mp, w.nb0, ml_shift);
+                const int64_t n0 = w.nb0 * BN;
+                for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
+                    const int slot = it % NCOL;
+                    mbar_wait(colempty0 + 8 * slot, ((it / NCOL) & 1) ^ 1);
+                    const uint32_t fb = colfull0 + 8 * slot;
+                    const uint32_t dst = smem_u32(col_base + slot * 3 * BN);
+                    mbar_expect_tx(fb, NCOLARR * BN * 4);
+                    bulk_load(dst, ep.xn + n0, BN * 4, fb);
+                    bulk_load(dst + BN * 4, ep.x_rs + n0, BN * 4, fb);
+                    if (PIVOT && SYM) bulk_load(dst + 2 * BN * 4, ep.thr + n0, BN * 4, fb);
+                }
+            }
+        }
+        __syncwarp();
     } else {
         // ------------------------------------------------------ epilogue (8 warps) --
         const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
         const int half = (warp - 2) >> 2;           // which BN/2 columns it owns
-        const int etid = threadIdx.x - 64;          // 0..255
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
-        float pf_n = 0.0f, pf_s = 0.0f, pf_t = 0.0f;  // next tile's column data, prefetched
-        bool pf_ok = false;
         // PIVOT: the warp's pending-candidate list lives in its second staging buffer
-        PendEntry* pend = reinterpret_cast<PendEntry*>(stg_base + ((warp - 2) * 2 + 1) * STG_BYTES);
-        __shared__ int pend_cnt[EPI_WARPS];
-        int* pcnt = &pend_cnt[warp - 2];
-        if (PIVOT && lane == 0) *pcnt = 0;
-        __syncwarp();
-        for (int64_t t = cid; t < sched.units(); t += ncl)
-        for (int pass = 0, cls = tile_class(sched.get(t).mp, sched.get(t).nb0, ml_shift);
-             pass < tile_passes(cls); ++pass, ++it) {
+        uint32_t* prow = reinterpret_cast<uint32_t*>(stg_base + ((warp - 2) * 2 + 1) * STG_BYTES);
+        uint32_t* pcol = prow + PEND_CAP;
+        uint32_t* pkey = pcol + PEND_CAP;
+        int pend_n = 0;  // warp-uniform
+        for (int64_t t = cid; t < sched.units(); t += ncl) {
             const tc::Unit w = sched.get(t);
+            const int cls = tile_class(w.mp, w.nb0, ml_shift);
             const int64_t nb = w.nb0;
             const int64_t mb = 2 * w.mp + crank;
-            const int tmask = tile_mask(cls, pass);  // mixed block: keep one side only
-            const int buf = it & 1;
-            const uint32_t tphase = (it >> 1) & 1;
             const int64_t n0 = nb * BN;
-            // stage the tile's column norms and scales (double-buffered by `buf`); they
-            // were loaded into registers one tile ahead, and the next tile's are issued now
-            if (!pf_ok) {
-                const int64_t j = n0 + etid;
-                pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
-                pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
-                if (PIVOT && SYM) pf_t = j < ep.N ? __ldg(ep.thr + j) : 0.0f;
-            }
-            col_n[buf][etid] = pf_n;
-            col_s[buf][etid] = pf_s;
-            if constexpr (PIVOT && SYM) col_t[buf][etid] = pf_t;
-            pf_ok = false;
-            {
-                // next work item of this CTA (same unit's second pass, or the next unit)
-                int64_t tn = t;
-                bool again = pass + 1 < tile_passes(cls);
-                if (!again) tn = t + ncl;
-                if (tn < sched.units()) {
-                    const int64_t j = sched.get(tn).nb0 * BN + etid;
-                    pf_n = j < ep.N ? __ldg(ep.xn + j) : 0.0f;
-                    pf_s = j < ep.N ? __ldg(ep.x_rs + j) : 0.0f;
-                    if (PIVOT && SYM) pf_t = j < ep.N ? __ldg(ep.thr + j) : 0.0f;
-                    pf_ok = true;
-                }
-            }
-            named_bar(1, 32 * EPI_WARPS);
             const int64_t row0 = mb * BM + quad * 32;
             const int64_t row = row0 + lane;
             const bool row_ok = row < ep.M;
@@ -205,7 +216,15 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                               row0 + ep.self_shift < c_lo + BN / 2 && row0 + 31 + ep.self_shift >= c_lo;
             const int64_t self_col = row + ep.self_shift;
             float* drow = ep.D + row * ep.ldD;
-
+        for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
+            const int tmask = tile_mask(cls, pass);  // mixed block: keep one side only
+            const int buf = it & 1;
+            const uint32_t tphase = (it >> 1) & 1;
+            const int slot = it % NCOL;
+            const float* col_n = col_base + slot * 3 * BN;
+            const float* col_s = col_n + BN;
+            const float* col_t = col_n + 2 * BN;
+            mbar_wait(colfull0 + 8 * slot, (it / NCOL) & 1);
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + half * (BN / 2);
@@ -219,8 +238,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
                 }
                 const int cb = half * (BN / 2) + ch * 32;  // first column of the chunk in the tile
-                const float4* cn4 = reinterpret_cast<const float4*>(&col_n[buf][cb]);
-                const float4* cs4 = reinterpret_cast<const float4*>(&col_s[buf][cb]);
+                const float4* cn4 = reinterpret_cast<const float4*>(col_n + cb);
+                const float4* cs4 = reinterpret_cast<const float4*>(col_s + cb);
                 float v[32];
                 #pragma unroll
                 for (int c4 = 0; c4 < 8; ++c4) {
@@ -295,31 +314,78 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         for (int c = 0; c < 32; ++c)
                             if (c0 + c >= ep.N) v[c] = __int_as_float(0x7F800000);
                     }
-                    const float* ct = &col_t[PIVOT && SYM ? buf : 0][cb];
-                    uint32_t hm = 0;  // this row's survivors in the chunk (row side or column side)
+                    // this row's survivors in the chunk: row side (hr) and column side (hc)
+                    uint32_t hr = 0, hc = 0;
                     #pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        hm |= (uint32_t)((v[c] <= trow) | (SYM && v[c] <= ct[c])) << c;
+                    for (int c = 0; c < 32; ++c) hr |= (uint32_t)(v[c] <= trow) << c;
+                    if (SYM) {
+                        const float4* ct4 = reinterpret_cast<const float4*>(col_t + cb);
+                        #pragma unroll
+                        for (int c4 = 0; c4 < 8; ++c4) {
+                            const float4 tt = ct4[c4];
+                            hc |= (uint32_t)(v[4 * c4] <= tt.x) << (4 * c4);
+                            hc |= (uint32_t)(v[4 * c4 + 1] <= tt.y) << (4 * c4 + 1);
+                            hc |= (uint32_t)(v[4 * c4 + 2] <= tt.z) << (4 * c4 + 2);
+                            hc |= (uint32_t)(v[4 * c4 + 3] <= tt.w) << (4 * c4 + 3);
+                        }
+                    }
+                    const uint32_t hm = hr | hc;
                     if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
                     // stage the chunk's values (swizzled, conflict-free) so that each lane can
                     // walk its own survivors with dynamic indices
-                    const uint32_t sv = smem_u32(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    float* svp = reinterpret_cast<float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    const uint32_t sv = smem_u32(svp);
                     #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
                                v[4 * u + 2], v[4 * u + 3]);
-                    __syncwarp();
-                    const float* svp = reinterpret_cast<const float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
-                    while (hm) {
-                        const int c = __ffs(hm) - 1;
-                        hm &= hm - 1;
-                        const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
-                        const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
-                        if (x <= trow) pivot_push(ep, pend, pcnt, row, (uint32_t)(c0 + c), key);
-                        if (SYM && x <= ct[c]) pivot_push(ep, pend, pcnt, c0 + c, (uint32_t)row, key);
+                    // slots of this lane's entries in the warp's pending list (warp scan)
+                    const int mine = __popc(hr) + __popc(hc);
+                    int incl = mine;
+                    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    if (pend_n + total > PEND_CAP) {
+                        pivot_flush(ep, prow, pcol, pkey, pend_n);
+                        pend_n = 0;
                     }
                     __syncwarp();
-                    if (*pcnt >= 32) pivot_flush(ep, pend, pcnt);
+                    uint32_t h = hm;
+                    if (total <= PEND_CAP) {
+                        int pos = pend_n + incl - mine;
+                        while (h) {
+                            const int c = __ffs(h) - 1;
+                            h &= h - 1;
+                            const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
+                            const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
+                            if ((hr >> c) & 1) {
+                                prow[pos] = (uint32_t)row;
+                                pcol[pos] = (uint32_t)(c0 + c);
+                                pkey[pos] = key;
+                                ++pos;
+                            }
+                            if (SYM && ((hc >> c) & 1)) {
+                                prow[pos] = (uint32_t)(c0 + c);
+                                pcol[pos] = (uint32_t)row;
+                                pkey[pos] = key;
+                                ++pos;
+                            }
+                        }
+                        pend_n += total;
+                    } else {  // more survivors than the list holds (adversarial ties): direct
+                        while (h) {
+                            const int c = __ffs(h) - 1;
+                            h &= h - 1;
+                            const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
+                            const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
+                            if ((hr >> c) & 1) pivot_append(ep, row, key, (uint32_t)(c0 + c));
+                            if (SYM && ((hc >> c) & 1)) pivot_append(ep, c0 + c, key, (uint32_t)row);
+                        }
+                    }
+                    __syncwarp();
                     continue;
                 }
                 if constexpr (SYM) {
@@ -407,12 +473,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         if (c0 + c < ep.N) drow[c0 + c] = v[c];
                 }
             }
+            // this work item's column data fully read
+            __syncwarp();
+            if (lane == 0) mbar_arrive(colempty0 + 8 * slot);
+        }
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
-        if constexpr (PIVOT) {
-            __syncwarp();
-            pivot_flush(ep, pend, pcnt);
-        }
+        if constexpr (PIVOT) pivot_flush(ep, prow, pcol, pkey, pend_n);
     }
     teardown(tmem_base);
 }

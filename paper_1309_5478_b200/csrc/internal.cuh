@@ -28,6 +28,9 @@ __host__ __device__ constexpr int64_t round_up(int64_t a, int64_t b) { return ce
 
 // The K padding of the split operands: one 128-byte swizzle atom of fp16 = 64 elements.
 constexpr int kSplitKAlign = 64;
+// Per-point arrays read by the tensor-core GEMMs (norms, scales, pivots) are allocated and
+// zero-padded to a multiple of one column tile.
+constexpr int kColPad = 256;
 
 // ---------------------------------------------------------------- launchers --------
 // prep.cu: row norms (fp64 accumulate) + non-finite flag; optionally the scaled fp16
@@ -65,8 +68,6 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
 // select.cu: pivots = k-th smallest chunk minimum per row; exact select over candidates.
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s);
-cudaError_t launch_pivot_prep(const float* kth_dist, int64_t M, int32_t k, int32_t metric, float* thr,
-                              int32_t* cnt, cudaStream_t s);
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                     int32_t* out_idx, float* out_dist, cudaStream_t s);

@@ -32,7 +32,15 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
             __half* __restrict__ lo, int32_t* __restrict__ flag) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (row >= N) return;
+    if (row >= N) {
+        // tensor-core path: the column arrays are padded to a multiple of 256 entries (the
+        // GEMM bulk-copies whole tiles of them); the padding is zero
+        if (hi != nullptr && lane == 0 && row < round_up(N, (int64_t)kColPad)) {
+            sqn[row] = 0.0f;
+            rscale[row] = 0.0f;
+        }
+        return;
+    }
     const float* x = X + row * (int64_t)d;
 
     double s = 0.0;
@@ -83,7 +91,7 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
 cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
                         float* rscale, __half* hi, __half* lo, int32_t* flag, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
-    dim3 grid((unsigned)ceil_div(N, kWarpsPerBlock));
+    dim3 grid((unsigned)ceil_div(hi != nullptr ? round_up(N, (int64_t)kColPad) : N, kWarpsPerBlock));
     prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag);
     return cudaGetLastError();
 }

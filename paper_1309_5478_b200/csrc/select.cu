@@ -879,20 +879,6 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
                           out_idx + row * k, out_dist + row * k);
 }
 
-// ------------------------------------------------------------------ pivot plan --------
-// Row pivots from the exact k-th distance of a column sample (an upper bound of the row's
-// k-th distance: the quickselect pivot of PAPER.md:56 chosen so that L >= K), in the
-// squared domain of the GEMM's filter (L2: RU(next(t)^2), so no true neighbour is rejected).
-__global__ void pivot_prep_kernel(const float* __restrict__ kth, int64_t M, int k, int metric,
-                                  float* __restrict__ thr, int32_t* __restrict__ cnt) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    const float t = kth[i * k + k - 1];
-    // L2: every x with sqrt(x) rounding to <= t has sqrt(x) < next(t), so x <= RU(next(t)^2)
-    const float t1 = nextafterf(t, __int_as_float(0x7F800000));
-    thr[i] = metric == 1 ? __fmul_ru(t1, t1) : t;
-    cnt[i] = 0;
-}
 
 // Pivot from chunk minima: the k-th smallest of the row's nchunk chunk minima (mins is
 // [nchunk][M]).  At least k elements of the row are <= it (one per chunk), so it bounds the
@@ -903,7 +889,10 @@ pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M
     __shared__ uint32_t skey[8][32], sidx[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t row = (int64_t)blockIdx.x * 8 + w;
-    if (row >= M) return;
+    if (row >= M) {  // zero padding of thr (read as whole tiles by the symmetric partition)
+        if (lane == 0 && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
+        return;
+    }
     uint64_t L = ~0ull;
     for (int64_t o = 0; o < nchunk; o += 32) {
         const int64_t c = o + lane;
@@ -1033,18 +1022,11 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_pivot_prep(const float* kth_dist, int64_t M, int32_t k, int32_t metric, float* thr,
-                              int32_t* cnt, cudaStream_t s) {
-    if (M == 0) return cudaSuccess;
-    pivot_prep_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, s>>>(kth_dist, M, k, metric, thr, cnt);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 32 || nchunk < k) return cudaErrorInvalidValue;
-    pivot_from_mins_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
+    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), 8), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
     return cudaGetLastError();
 }
 

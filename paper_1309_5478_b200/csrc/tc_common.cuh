@@ -158,14 +158,17 @@ struct TileSched {
 struct SymSched {
     int64_t n;  // pair blocks per side
     __device__ __forceinline__ int64_t units() const { return n * (n + 1) / 2; }
+    // row m of the triangle starts at unit s(m) = m*n - m(m-1)/2: the largest m with
+    // s(m) <= u is the smaller root of m^2 - (2n+1) m + 2u = 0, rounded down and corrected
+    __device__ __forceinline__ int64_t start(int64_t m) const { return m * n - m * (m - 1) / 2; }
     __device__ __forceinline__ Unit get(int64_t u) const {
-        int64_t lo = 0, hi = n - 1;  // largest m with m*n - m(m-1)/2 <= u
-        while (lo < hi) {
-            const int64_t m = (lo + hi + 1) / 2;
-            if (m * n - m * (m - 1) / 2 <= u) lo = m; else hi = m - 1;
-        }
-        const int64_t nb = lo + (u - (lo * n - lo * (lo - 1) / 2));
-        return {lo, nb, nb + 1};
+        const double bq = 2.0 * (double)n + 1.0;
+        int64_t m = (int64_t)((bq - sqrt(bq * bq - 8.0 * (double)u)) * 0.5);
+        m = m < 0 ? 0 : m > n - 1 ? n - 1 : m;
+        while (m > 0 && start(m) > u) --m;
+        while (m < n - 1 && start(m + 1) <= u) ++m;
+        const int64_t nb = m + (u - start(m));
+        return {m, nb, nb + 1};
     }
 };
 
