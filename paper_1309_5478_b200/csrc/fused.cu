@@ -107,8 +107,8 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
             return METRIC == 1 ? __fmul_ru(t, t) : t;
         };
         int it = 0;
-        for (int64_t u = cid; u < sched.units(); u += ncl) {
-            const Unit w = sched.get(u);
+        for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+            const Unit w = sched.unit(cur);
             const int64_t row0 = (2 * w.mp + crank) * BM + quad * 32;  // warp's first row
             const int64_t row = row0 + lane;
             const bool row_ok = row < a.M;

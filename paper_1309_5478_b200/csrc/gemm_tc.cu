@@ -169,8 +169,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         // ------------------------------------------- column data of each work item --
         if (lane == 0) {
             int it = 0;
-            for (int64_t t = cid; t < sched.units(); t += ncl) {
-                const tc::Unit w = sched.get(t);
+            for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+                const tc::Unit w = sched.unit(cur);
                 const int cls = tile_class(w.mp, w.nb0, ml_shift);
                 const int64_t n0 = w.nb0 * BN;
                 for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
@@ -198,8 +198,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         uint32_t* pcol = prow + PEND_CAP;
         uint32_t* pkey = pcol + PEND_CAP;
         int pend_n = 0;  // warp-uniform
-        for (int64_t t = cid; t < sched.units(); t += ncl) {
-            const tc::Unit w = sched.get(t);
+        for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+            const tc::Unit w = sched.unit(cur);
             const int cls = tile_class(w.mp, w.nb0, ml_shift);
             const int64_t nb = w.nb0;
             const int64_t mb = 2 * w.mp + crank;

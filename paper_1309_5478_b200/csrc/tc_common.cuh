@@ -151,6 +151,33 @@ struct TileSched {
         const int64_t nb = r / gm;
         return {m0 + r % gm, nb, nb + 1};
     }
+    // Cursor: each CTA walks t = cid, cid + ncl, ... incrementally (no 64-bit divisions
+    // per work item): group g, offset r inside it.
+    struct Cur {
+        int64_t t, g, r;
+    };
+    __device__ __forceinline__ Cur first(int64_t t) const {
+        const int64_t g = t / ((int64_t)GROUP_M * n_nb);
+        return {t, g, t - g * GROUP_M * n_nb};
+    }
+    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
+    __device__ __forceinline__ void next(Cur& c, int64_t step) const {
+        c.t += step;
+        c.r += step;
+        while (c.g * GROUP_M < n_mp) {
+            const int64_t rem = n_mp - c.g * GROUP_M;
+            const int64_t pg = (rem < GROUP_M ? rem : GROUP_M) * n_nb;
+            if (c.r < pg) break;
+            c.r -= pg;
+            ++c.g;
+        }
+    }
+    __device__ __forceinline__ Unit unit(const Cur& c) const {
+        const int64_t m0 = c.g * GROUP_M;
+        const uint32_t gm = (uint32_t)((n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M);
+        const uint32_t nb = (uint32_t)c.r / gm;
+        return {m0 + ((uint32_t)c.r - nb * gm), (int64_t)nb, (int64_t)nb + 1};
+    }
 };
 
 // Symmetric k-NNG (queries = corpus): the upper triangle of 256x256 pair blocks, nb >= mp,
@@ -170,6 +197,24 @@ struct SymSched {
         const int64_t nb = m + (u - start(m));
         return {m, nb, nb + 1};
     }
+    // Cursor: row m of the triangle, offset o inside it (row m holds n - m units)
+    struct Cur {
+        int64_t t, m, o;
+    };
+    __device__ __forceinline__ Cur first(int64_t t) const {
+        const Unit w = get(t);
+        return {t, w.mp, w.nb0 - w.mp};
+    }
+    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
+    __device__ __forceinline__ void next(Cur& c, int64_t step) const {
+        c.t += step;
+        c.o += step;
+        while (c.m < n && c.o >= n - c.m) {
+            c.o -= n - c.m;
+            ++c.m;
+        }
+    }
+    __device__ __forceinline__ Unit unit(const Cur& c) const { return {c.m, c.m + c.o, c.m + c.o + 1}; }
 };
 
 // Fused GEMM+select: a unit is a row-block pair against one of S column splits; units of
@@ -183,6 +228,13 @@ struct SplitSched {
         const int64_t nb1 = nb0 + per < n_nb ? nb0 + per : n_nb;
         return {u % n_mp, nb0, nb1};
     }
+    struct Cur {
+        int64_t t;
+    };
+    __device__ __forceinline__ Cur first(int64_t t) const { return {t}; }
+    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
+    __device__ __forceinline__ void next(Cur& c, int64_t step) const { c.t += step; }
+    __device__ __forceinline__ Unit unit(const Cur& c) const { return get(c.t); }
 };
 
 // ------------------------------------------------------------------ orientation -------
@@ -226,8 +278,8 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const C
                                               int64_t shift) {
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t u = cid; u < sched.units(); u += ncl) {
-        const Unit w = sched.get(u);
+    for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+        const Unit w = sched.unit(cur);
         const int row_a = (int)((2 * w.mp + crank) * BM);
         for (int64_t nb = w.nb0; nb < w.nb1; ++nb)
         for (int pass = 0; pass < tile_passes(tile_class(w.mp, nb, shift)); ++pass) {
@@ -261,8 +313,8 @@ __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, con
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int64_t u = cid; u < sched.units(); u += ncl) {
-        const Unit w = sched.get(u);
+    for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+        const Unit w = sched.unit(cur);
         for (int64_t nb = w.nb0; nb < w.nb1; ++nb)
         for (int pass = 0, cls = tile_class(w.mp, nb, shift); pass < tile_passes(cls); ++pass, ++it) {
             const bool o2 = tile_orient(cls, pass) == TILE_BELOW;
