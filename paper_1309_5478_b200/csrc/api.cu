@@ -36,6 +36,7 @@ struct knn_ctx {
     bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
     int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
     int32_t pivot_div = 8;     // sample = the first N / pivot_div corpus points
+    float pivot_margin = __builtin_nanf("");  // KNN_PIVOT_MARGIN: override of the sample's error margin
     int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;
     size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
@@ -278,7 +279,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         {
             knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, Ssamp, d_pad};
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc_mins(op, metric, self_shift, D, ctx->num_sms, s));
+            KNN_CUDA(knn::launch_dist_tc_mins(op, metric, self_shift, D, ctx->pivot_margin, ctx->num_sms, s));
             tg.done();
             Timed tp(ctx, KNN_KERNEL_PREP, s);
             KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, k, metric, thr, cnt, s));
@@ -291,7 +292,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                                            flag, ctx->num_sms, s));
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
-        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, s));
+        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, flag, s));
         tc2.done();
         return KNN_OK;
     }
@@ -386,6 +387,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     if (pv && strcmp(pv, "0") == 0) c->pivot_ok = false;
     const char* pd = getenv("KNN_PIVOT_DIV");
     if (pd && atoi(pd) >= 2) c->pivot_div = atoi(pd);
+    const char* pm = getenv("KNN_PIVOT_MARGIN");
+    if (pm) c->pivot_margin = strtof(pm, nullptr);
     const char* pc = getenv("KNN_PIVOT_CAP");
     if (pc) c->pivot_cap = atoi(pc) > 32 ? atoi(pc) : 32;
     const char* sy = getenv("KNN_SYM");

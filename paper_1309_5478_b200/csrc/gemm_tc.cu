@@ -31,6 +31,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstring>
 #include <mutex>
 
@@ -59,6 +60,7 @@ struct EpiArgs {
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
     // PIVOT (partition epilogue): per-row pivots in the squared domain, candidate lists
     const float* thr; int32_t* cnt; uint32_t* ckey; uint32_t* cidx; int32_t cap; int32_t* flag;
+    float margin;  // MINS: error bound of the hi.hi value, relative to ||q||^2 + ||x||^2
 };
 
 // Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
@@ -131,7 +133,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     constexpr bool PIVOT = MODE == MODE_PIVOT;
     constexpr bool MINS = MODE == MODE_MINS;
     constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
-    const int64_t ml_shift = SYM ? INT64_MIN : ep.self_shift;
+    // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
+    constexpr int NSEG = MINS ? 1 : 3;
+    constexpr int KSTAGES = MINS ? 2 * STAGES : STAGES;
+    static_assert(KSTAGES * stage_bytes<NSEG>() == STAGES * STAGE_BYTES, "smem layout");
+    // the single product is orientation-free: no two-pass blocks on the diagonal
+    const int64_t ml_shift = SYM || MINS ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -139,11 +146,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
     float* col_base = reinterpret_cast<float*>(stg_base + EPI_WARPS * 2 * STG_BYTES);  // [NCOL][3][BN]
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(col_base) + NCOL * COL_BYTES);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-    const uint32_t colfull0 = smem_u32(bars + 2 * STAGES + 5);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * KSTAGES + 4);
+    const uint32_t colfull0 = smem_u32(bars + 2 * KSTAGES + 5);
     const uint32_t colempty0 = colfull0 + 8 * NCOL;
-    const Bars b{smem_u32(bars), smem_u32(bars + STAGES), smem_u32(bars + 2 * STAGES),
-                 smem_u32(bars + 2 * STAGES + 2)};
+    const Bars b{smem_u32(bars), smem_u32(bars + KSTAGES), smem_u32(bars + 2 * KSTAGES),
+                 smem_u32(bars + 2 * KSTAGES + 2)};
     const uint32_t tfull0 = b.tfull0, tempty0 = b.tempty0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -153,17 +160,18 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             mbar_init(colempty0 + 8 * i, EPI_WARPS);
         }
     }
-    const uint32_t tmem_base = setup(bars, STAGES, EPI_WARPS, tmem_slot, &map_qh, 1);
+    const uint32_t tmem_base = setup(bars, KSTAGES, EPI_WARPS, tmem_slot, &map_qh, 1);
     const uint32_t crank = cluster_rank();
     const int64_t cid = blockIdx.x / CLUSTER, ncl = gridDim.x / CLUSTER;
 
     if (warp == 0) {
         if (lane == 0)
-            producer_loop<STAGES>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched, num_kb,
-                                  crank, cid, ncl, ml_shift);
+            producer_loop<KSTAGES, Sched, NSEG>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched,
+                                                num_kb, crank, cid, ncl, ml_shift);
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<STAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
+        if (lane == 0)
+            mma_loop<KSTAGES, Sched, NSEG>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
         __syncwarp();
     } else if (warp == COL_WARP) {
         // ------------------------------------------- column data of each work item --
@@ -250,8 +258,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int c = 4 * c4 + e;
-                        const float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], qn + na[e]);
-                        v[c] = (PIVOT || MINS) ? u : finalize_dist<METRIC>(u);
+                        const float nsum = qn + na[e];
+                        const float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], nsum);
+                        // MINS: the hi.hi value plus a bound of its error, so that it is never
+                        // below the FP32-accurate u of the partition
+                        v[c] = MINS ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
                     }
                 }
                 const int64_t c0 = n0 + cb;
@@ -596,7 +607,7 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 }
 
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t self_shift, float* mins,
-                                int num_sms, cudaStream_t s) {
+                                float margin_override, int num_sms, cudaStream_t s) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     if (op.N % 32 != 0) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
@@ -606,9 +617,15 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
         !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
-    // mins is [N/32][M]: ep.D / ep.ldD reused as its base / row stride
+    // mins is [N/32][M]: ep.D / ep.ldD reused as its base / row stride.  Error of the single
+    // hi.hi product (prep.cu split, |lo| <= 2^-11 |x| per component): |2 q.x - 2 qh.xh| <=
+    // (2^-10 (1 + 2^-10) + d 2^-23) 2|q||x| (the d term bounds fp32 accumulation), and
+    // 2|q||x| <= ||q||^2 + ||x||^2; + 2^-20 covers the roundings of both u values.
+    float margin = (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
+                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
+    if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin};
     TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;

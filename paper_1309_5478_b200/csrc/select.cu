@@ -217,10 +217,6 @@ __device__ __forceinline__ float ld_stream1(const float* p) {
     return v;
 }
 
-__device__ __forceinline__ float f4get(const float4& v, int c) {
-    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-}
-
 // ------------------------------------------------------------------ select kernel ----
 // One CTA per row.  VEC: rows are 16-byte aligned (ldD % 4 == 0) -> 128-bit loads.
 // Element e = 4*j + c of a thread in the chunk at `base` sits at column
@@ -880,34 +876,87 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
 }
 
 
+// Bitonic sort of one 32-bit key per lane (ascending across the warp).
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    #pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t o = __shfl_xor_sync(FULL, v, stride);
+            const bool asc = (lane & size) == 0 || size == 32;
+            const bool lower = (lane & stride) == 0;
+            v = (lower == asc) ? min(v, o) : max(v, o);
+        }
+    }
+    return v;
+}
+
 // Pivot from chunk minima: the k-th smallest of the row's nchunk chunk minima (mins is
 // [nchunk][M]).  At least k elements of the row are <= it (one per chunk), so it bounds the
-// row's k-th distance from above: a quickselect pivot with L >= K.  Warp per row, folds of 32.
+// row's k-th distance from above: a quickselect pivot with L >= K.  A CTA takes 32 rows:
+// the minima are staged [chunk][row] through shared memory (coalesced reads), then each
+// warp keeps, per row, the sorted 32 smallest keys and inserts only the keys that beat the
+// current k-th (ballot), so most of the 32-key groups cost one compare.
+constexpr int PV_ROWS = 32, PV_SLAB = 256;
+__device__ __forceinline__ void pv_row(const uint32_t (*tile)[PV_ROWS + 1], int rl, int ns, bool first, int k,
+                                       uint32_t& S, uint32_t& Tk) {
+    const int lane = threadIdx.x & 31;
+    for (int g = 0; g < ns; g += 32) {
+        const uint32_t x = tile[g + lane][rl];
+        if (first && g == 0) {
+            S = warp_sort32(x);
+            Tk = __shfl_sync(FULL, S, k - 1);
+            continue;
+        }
+        uint32_t m = __ballot_sync(FULL, x < Tk);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t xv = __shfl_sync(FULL, x, src);
+            if (xv < Tk) {
+                const int pos = __popc(__ballot_sync(FULL, S <= xv));  // < k
+                const uint32_t up = __shfl_up_sync(FULL, S, 1);
+                S = lane > pos ? up : (lane == pos ? xv : S);
+                Tk = __shfl_sync(FULL, S, k - 1);
+            }
+        }
+    }
+}
 __global__ void __launch_bounds__(256)
 pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int k, int metric,
                        float* __restrict__ thr, int32_t* __restrict__ cnt) {
-    __shared__ uint32_t skey[8][32], sidx[8][32];
+    __shared__ uint32_t tile[PV_SLAB][PV_ROWS + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t row = (int64_t)blockIdx.x * 8 + w;
-    if (row >= M) {  // zero padding of thr (read as whole tiles by the symmetric partition)
-        if (lane == 0 && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
-        return;
+    const int64_t r0 = (int64_t)blockIdx.x * PV_ROWS;
+    if (threadIdx.x < PV_ROWS) {  // zero padding of thr (read as whole tiles by the SYM partition)
+        const int64_t row = r0 + threadIdx.x;
+        if (row >= M && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
     }
-    uint64_t L = ~0ull;
-    for (int64_t o = 0; o < nchunk; o += 32) {
-        const int64_t c = o + lane;
-        skey[w][lane] = c < nchunk ? ukey(mins[c * M + row]) : 0xFFFFFFFFu;
-        sidx[w][lane] = (uint32_t)c;
-        __syncwarp();
-        L = ws::warp_merge32<1>(L, skey[w], sidx[w], 32);
-        __syncwarp();
+    uint32_t S[4], Tk[4];  // the warp's 4 rows: sorted smallest keys (lane i = i-th), k-th key
+    for (int64_t s0 = 0; s0 < nchunk; s0 += PV_SLAB) {
+        const int ns = (int)(nchunk - s0 < PV_SLAB ? nchunk - s0 : PV_SLAB);
+        __syncthreads();
+        for (int i = w; i < PV_SLAB; i += 8) {
+            const int64_t row = r0 + lane;
+            tile[i][lane] = (i < ns && row < M) ? ukey(__ldg(mins + (s0 + i) * M + row)) : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        pv_row(tile, w * 4 + 0, ns, s0 == 0, k, S[0], Tk[0]);
+        pv_row(tile, w * 4 + 1, ns, s0 == 0, k, S[1], Tk[1]);
+        pv_row(tile, w * 4 + 2, ns, s0 == 0, k, S[2], Tk[2]);
+        pv_row(tile, w * 4 + 3, ns, s0 == 0, k, S[3], Tk[3]);
     }
-    const uint32_t tk = (uint32_t)(__shfl_sync(FULL, L, k - 1) >> 32);
-    if (lane == 0) {
-        const float t = tk == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(tk);
-        const float t1 = nextafterf(t, __int_as_float(0x7F800000));
-        thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
-        cnt[row] = 0;
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t row = r0 + w * 4 + j;
+        if (lane == 0 && row < M) {
+            const uint32_t tk = Tk[j];
+            const float t = tk == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(tk);
+            const float t1 = nextafterf(t, __int_as_float(0x7F800000));
+            thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
+            cnt[row] = 0;
+        }
     }
 }
 
@@ -916,19 +965,47 @@ __global__ void __launch_bounds__(256)
 candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
                         const uint32_t* __restrict__ cidx, int cap, int64_t M, int k,
                         int64_t idx_offset, int32_t* __restrict__ out_idx,
-                        float* __restrict__ out_dist) {
+                        float* __restrict__ out_dist, int32_t* __restrict__ flag) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (row >= M) return;
     int n = cnt[row];
+    // certificate of the partition: k elements at or below the pivot means every element of
+    // the true k nearest (ties included) is a candidate; otherwise redo (flag bit 2)
+    if (n < k && lane == 0) atomicOr(flag, 2);
     n = n < cap ? n : cap;
-    uint64_t L = ~0ull;
+    // sorted best-32 (key, idx) pairs (lane i = i-th); later groups of 32 candidates insert
+    // only the pairs that beat the current k-th (ballot), one shuffle-shift per insertion
     const uint32_t* rk = ckey + row * cap;
     const uint32_t* ri = cidx + row * cap;
-    for (int o = 0; o < n; o += 32) L = ws::warp_merge32<1>(L, rk + o, ri + o, n - o < 32 ? n - o : 32);
+    auto load = [&](int o) -> uint64_t {
+        const int i = o + lane;
+        return i < n ? ((uint64_t)__ldg(rk + i) << 32 | __ldg(ri + i)) : ~0ull;
+    };
+    uint64_t v[1] = {load(0)};
+    uint64_t nx = load(32);
+    ws::warp_bitonic<1>(v);
+    uint64_t S = v[0];
+    uint64_t Tk = __shfl_sync(FULL, S, k - 1);
+    for (int o = 32; o < n; o += 32) {
+        const uint64_t x = nx;
+        nx = load(o + 32);
+        uint32_t m = __ballot_sync(FULL, x < Tk);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const uint64_t xv = __shfl_sync(FULL, x, src);
+            if (xv < Tk) {
+                const int pos = __popc(__ballot_sync(FULL, S < xv));  // < k
+                const uint64_t up = __shfl_up_sync(FULL, S, 1);
+                S = lane > pos ? up : (lane == pos ? xv : S);
+                Tk = __shfl_sync(FULL, S, k - 1);
+            }
+        }
+    }
     if (lane < k) {
-        const uint32_t key = (uint32_t)(L >> 32);
-        out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)L + idx_offset);
+        const uint32_t key = (uint32_t)(S >> 32);
+        out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)S + idx_offset);
         out_dist[row * k + lane] = key == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(key);
     }
 }
@@ -1026,17 +1103,17 @@ cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 32 || nchunk < k) return cudaErrorInvalidValue;
-    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), 8), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
+    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), PV_ROWS), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
     return cudaGetLastError();
 }
 
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
-                                    int32_t* out_idx, float* out_dist, cudaStream_t s) {
+                                    int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
     candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, ckey, cidx, cap, M, k, idx_offset,
-                                                                    out_idx, out_dist);
+                                                                    out_idx, out_dist, flag);
     return cudaGetLastError();
 }
 

@@ -269,8 +269,11 @@ struct Bars {
 };
 
 // TMA producer (one elected thread): per K-block, the CTA's own qh/ql rows and its half of
-// the xh/xl rows multicast to both CTAs of the pair.
-template <int STAGES, class Sched>
+// the xh/xl rows multicast to both CTAs of the pair.  NSEG = 1 (the single hi.hi product of
+// the approximate pivot sample pass) loads only qh and xh: stage = [qh | xh].
+template <int NSEG>
+constexpr int stage_bytes() { return NSEG == 3 ? STAGE_BYTES : A_BYTES + B_BYTES; }
+template <int STAGES, class Sched, int NSEG = 3>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const CUtensorMap* map_ql,
                                               const CUtensorMap* map_xh, const CUtensorMap* map_xl,
                                               uint8_t* stage_base, const Bars& b, const Sched& sched,
@@ -287,13 +290,18 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const C
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(b.empty0 + 8 * stage, phase ^ 1);
                 const uint32_t fb = b.full0 + 8 * stage;
-                mbar_expect_tx(fb, STAGE_BYTES);
-                const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
+                mbar_expect_tx(fb, stage_bytes<NSEG>());
+                const uint32_t sb = smem_u32(stage_base + (size_t)stage * stage_bytes<NSEG>());
                 const uint32_t boff = crank * (B_BYTES / 2);
-                tma_load_2d(sb, map_qh, fb, kb * BK, row_a);
-                tma_load_2d(sb + A_BYTES, map_ql, fb, kb * BK, row_a);
-                tma_load_2d_mc(sb + 2 * A_BYTES + boff, map_xh, fb, kb * BK, row_b, 0x3);
-                tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + boff, map_xl, fb, kb * BK, row_b, 0x3);
+                if (NSEG == 3) {
+                    tma_load_2d(sb, map_qh, fb, kb * BK, row_a);
+                    tma_load_2d(sb + A_BYTES, map_ql, fb, kb * BK, row_a);
+                    tma_load_2d_mc(sb + 2 * A_BYTES + boff, map_xh, fb, kb * BK, row_b, 0x3);
+                    tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + boff, map_xl, fb, kb * BK, row_b, 0x3);
+                } else {
+                    tma_load_2d(sb, map_qh, fb, kb * BK, row_a);
+                    tma_load_2d_mc(sb + A_BYTES + boff, map_xh, fb, kb * BK, row_b, 0x3);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -306,7 +314,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const C
 // Single-thread MMA issuer: per tile, waits for a free TMEM accumulator, then per K-block
 // issues the three split segments (ql.xh, qh.xl, qh.xh; smallest first) and frees the
 // stage in both CTAs; finally signals the epilogue.
-template <int STAGES, class Sched>
+template <int STAGES, class Sched, int NSEG = 3>
 __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, const Sched& sched,
                                          int num_kb, uint32_t tmem_base, int64_t cid, int64_t ncl,
                                          int64_t shift) {
@@ -326,14 +334,15 @@ __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, con
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(b.full0 + 8 * stage, phase);
                 tc_fence_after();
-                const uint32_t sb = smem_u32(stage_base + (size_t)stage * STAGE_BYTES);
-                const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + 2 * A_BYTES,
+                const uint32_t sb = smem_u32(stage_base + (size_t)stage * stage_bytes<NSEG>());
+                const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + (NSEG == 3 ? 2 * A_BYTES : A_BYTES),
                                xl = sb + 2 * A_BYTES + B_BYTES;
-                // O1: ql.xh, qh.xl, qh.xh   O2: qh.xl, ql.xh, qh.xh  (smallest terms first)
-                const uint32_t sa[3] = {o2 ? qh : ql, o2 ? ql : qh, qh};
-                const uint32_t sbx[3] = {o2 ? xl : xh, o2 ? xh : xl, xh};
+                // O1: ql.xh, qh.xl, qh.xh   O2: qh.xl, ql.xh, qh.xh  (smallest terms first);
+                // NSEG = 1: qh.xh only
+                const uint32_t sa[3] = {NSEG == 1 ? qh : o2 ? qh : ql, o2 ? ql : qh, qh};
+                const uint32_t sbx[3] = {NSEG == 1 ? xh : o2 ? xl : xh, o2 ? xh : xl, xh};
                 #pragma unroll
-                for (int seg = 0; seg < 3; ++seg) {
+                for (int seg = 0; seg < NSEG; ++seg) {
                     #pragma unroll
                     for (int kk = 0; kk < BK / UMMA_K; ++kk) {
                         const uint32_t acc = (kb | seg | kk) != 0;

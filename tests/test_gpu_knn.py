@@ -5,6 +5,10 @@ Tolerances come from BASELINE.json's north star: distances within 1e-5 of
 and, on integer-grid data where every correct implementation is exact, bit-identical
 to the oracle (E2E-3).  Sizes span several GEMM tiles (128×256) with ragged tails; the
 BASELINE configs run at full size on sampled rows."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -233,7 +237,6 @@ def test_errors():
 
 def test_simt_cross_check_path():
     # The FFMA path (KNN_GEMM=simt) in a fresh process must pass the same tolerance.
-    import subprocess, sys, os
     code = (
         "import numpy as np, torch, oracle\n"
         "from oracle import checks\n"
@@ -394,3 +397,22 @@ def test_pivot_overflow_falls_back_exactly():
     ref = oracle.knn(X, X, 32, rows=rows, graph=True)
     assert np.array_equal(gi[rows], ref["idx32"])
     assert np.array_equal(gd[rows], ref["dist32"])
+
+
+def test_pivot_certificate_failure_falls_back_exactly():
+    # a sample margin far below the error bound gives pivots under the k-th distance for
+    # many rows; the candidate count certificate (cnt >= k) catches them and the call is
+    # redone on the full matrix: the result is the materialised plan's, bit for bit
+    #
+    code = (
+        "import torch\n"
+        "from paper_1309_5478_b200 import knn, datagen\n"
+        "X = torch.from_numpy(datagen.points(16384, 64, 'uniform', seed=54)).cuda()\n"
+        "gi, gd = knn.graph(X, 16)\n"
+        "assert knn.last_plan() != 3, knn.last_plan()\n"
+        "knn.set_plan(knn.PLAN_MATERIALISED)\n"
+        "ri, rd = knn.graph(X, 16)\n"
+        "assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))\n")
+    env = dict(os.environ, KNN_PIVOT_MARGIN="-0.02")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
