@@ -330,15 +330,21 @@ def run_ours(args):
             gr["frac"] = gr["achieved"] / gr["peak"]
             gr["kernel"] = "dist_tc_kernel<SYM> (a-S3, symmetric k-NNG: upper triangle, direct + transposed stores)"
         rooflines.append((g_ms, gr))
-    if s_n:
+    if s_n and plan_code in (3, 4):
+        S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
+        rooflines.append((s_ms, hbm_roof("pivot_from_mins_kernel (pivot = k-th smallest of the row's chunk minima)",
+                                         "pivot_from_mins_kernel", s_ms, s_n,
+                                         R_local * (S_samp // 32 * 4.0 + 8.0))))
+    elif s_n:
         sl = max(s_n // args.steps, 1)
-        ncols = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256 if plan_code in (3, 4) else N
-        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4%s)" % (
-            ", pivot sample rows" if plan_code in (3, 4) else ""), "select_warp_kernel", s_ms, s_n,
-            R_local / sl * (ncols * 4.0 + k * 8.0))))
+        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4)", "select_warp_kernel", s_ms, s_n,
+                                         R_local / sl * (N * 4.0 + k * 8.0))))
     if m_n and plan_code in (3, 4):
+        cands = knn.last_candidates()  # survivors of the partition (whole call)
         rooflines.append((m_ms, hbm_roof("candidate_select_kernel (exact select of the partition)",
-                                         "candidate_select_kernel", m_ms, m_n, R_local * (4.0 + k * 8.0))))
+                                         "candidate_select_kernel", m_ms, m_n,
+                                         cands * 8.0 + R_local * (4.0 + k * 8.0))))
+        rooflines[-1][1]["candidates_per_row"] = cands / max(R_local, 1)
     elif m_n:
         # partial lists per row merged (fused split-N, same rule as fused.cu's fused_splits)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count

@@ -162,13 +162,20 @@ int knn_fused_plan(knn_ctx_t ctx, int32_t k);
 /* Plan the last top-level call of this ctx executed: 0 = blocked distances + select,
  * 1 = fused GEMM+select, 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
  * each written directly and transposed) + select, 3 = pivot plan,
- * symmetric (k <= 32, N >= 16384: per-row pivot = exact k-th distance over the first
- * N/8 corpus points; the GEMM over the upper triangle keeps only elements <= pivot, for
- * rows and, transposed, columns; exact select of the candidates — the quick multi-select
- * partition of PAPER.md:56 applied at matrix scale), 4 = pivot plan, general block,
- * -1 = none yet.  All plans give bit-identical results; a pivot call whose candidate
- * buffer overflows (heavily tied data) is redone with the full matrix. */
+ * symmetric, 4 = pivot plan, general block, -1 = none yet.  The pivot plan (k <= 32,
+ * N >= 16384) is the quick multi-select partition of PAPER.md:56 applied at matrix scale:
+ * a sample pass over the first N/8 corpus points (one fp16 product plus a bound of its
+ * error) gives each row the minimum of every 32-column chunk; the row pivot is the k-th
+ * smallest of those minima (>= the row's k-th distance); the FP32-accurate GEMM keeps
+ * only elements <= pivot (for rows and, in the symmetric plan, transposed for columns);
+ * an exact select of the candidates follows.  Rows with fewer than k candidates (a
+ * failed certificate) or a candidate-buffer overflow make the call redo itself on the
+ * full matrix.  All plans give bit-identical results. */
 int knn_last_plan(knn_ctx_t ctx);
+/* Total candidates the last pivot-plan call kept (sum over rows of the partition's
+ * survivors; 0 for the other plans, -1 for a null ctx).  Diagnostic: the bench reports
+ * the candidate select's algorithmic bytes from it. */
+int64_t knn_last_candidates(knn_ctx_t ctx);
 
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by
  * CUDA events recorded on the launch stream.  knn_profile_enable(ctx, 1) also resets

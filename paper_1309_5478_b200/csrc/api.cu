@@ -23,7 +23,8 @@ struct knn_ctx {
     size_t ws_size = 0;
     void* io = nullptr;  // device copies for the host-buffer entry point
     size_t io_size = 0;
-    int32_t* flag_host = nullptr;  // pinned
+    int32_t* flag_host = nullptr;  // pinned copy of the workspace's flag slice (int32 x 4)
+    int64_t last_candidates = 0;   // pivot plans: candidates kept by the last call
     int64_t launches = 0;
     size_t d_budget = (size_t)4 << 30;  // bytes of distance-matrix block per launch pair
     // per-kernel event timing (knn_profile_*)
@@ -247,7 +248,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     Carve carve{static_cast<char*>(ctx->ws)};
     layout_all(carve);
 
-    KNN_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
         KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
@@ -281,7 +282,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
             KNN_CUDA(knn::launch_dist_tc_mins(op, metric, self_shift, D, ctx->pivot_margin, ctx->num_sms, s));
             tg.done();
-            Timed tp(ctx, KNN_KERNEL_PREP, s);
+            Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
             KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, k, metric, thr, cnt, s));
             tp.done();
         }
@@ -330,8 +331,10 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
 knn_status finish_blocking(knn_ctx* ctx, cudaStream_t s) {
     // The flag is the first slice of the workspace (see run_block's layout).
     int32_t* flag = static_cast<int32_t*>(ctx->ws);
-    KNN_CUDA(cudaMemcpyAsync(ctx->flag_host, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    // [0] = flags, [2..3] = int64 candidate count of the pivot plan
+    KNN_CUDA(cudaMemcpyAsync(ctx->flag_host, flag, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     KNN_CUDA(cudaStreamSynchronize(s));
+    memcpy(&ctx->last_candidates, ctx->flag_host + 2, sizeof(int64_t));
     if (*ctx->flag_host & 1)
         return fail(ctx, KNN_ERR_NONFINITE,
                     "input contains NaN/inf or a vector with ||x||^2 >= FLT_MAX/4");
@@ -395,7 +398,7 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     if (sy && strcmp(sy, "0") == 0) c->sym_ok = false;
     const char* b = getenv("KNN_D_BUDGET_MB");
     if (b) c->d_budget = (size_t)atoll(b) << 20;
-    if (cudaMallocHost(&c->flag_host, sizeof(int32_t)) != cudaSuccess) {
+    if (cudaMallocHost(&c->flag_host, 4 * sizeof(int32_t)) != cudaSuccess) {
         delete c;
         return KNN_ERR_CUDA;
     }
@@ -435,6 +438,8 @@ knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan) {
 }
 
 int knn_last_plan(knn_ctx_t ctx) { return ctx ? ctx->last_plan : -1; }
+
+int64_t knn_last_candidates(knn_ctx_t ctx) { return ctx ? ctx->last_candidates : -1; }
 
 int knn_gemm_path(knn_ctx_t ctx) {
     if (!ctx) return -1;

@@ -895,35 +895,39 @@ __device__ __forceinline__ uint32_t warp_sort32(uint32_t v) {
 // Pivot from chunk minima: the k-th smallest of the row's nchunk chunk minima (mins is
 // [nchunk][M]).  At least k elements of the row are <= it (one per chunk), so it bounds the
 // row's k-th distance from above: a quickselect pivot with L >= K.  A CTA takes 32 rows:
-// the minima are staged [chunk][row] through shared memory (coalesced reads), then each
-// warp keeps, per row, the sorted 32 smallest keys and inserts only the keys that beat the
-// current k-th (ballot), so most of the 32-key groups cost one compare.
-constexpr int PV_ROWS = 32, PV_SLAB = 256;
-__device__ __forceinline__ void pv_row(const uint32_t (*tile)[PV_ROWS + 1], int rl, int ns, bool first, int k,
-                                       uint32_t& S, uint32_t& Tk) {
-    const int lane = threadIdx.x & 31;
-    for (int g = 0; g < ns; g += 32) {
-        const uint32_t x = tile[g + lane][rl];
-        if (first && g == 0) {
-            S = warp_sort32(x);
-            Tk = __shfl_sync(FULL, S, k - 1);
-            continue;
-        }
-        uint32_t m = __ballot_sync(FULL, x < Tk);
-        while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const uint32_t xv = __shfl_sync(FULL, x, src);
-            if (xv < Tk) {
-                const int pos = __popc(__ballot_sync(FULL, S <= xv));  // < k
-                const uint32_t up = __shfl_up_sync(FULL, S, 1);
-                S = lane > pos ? up : (lane == pos ? xv : S);
-                Tk = __shfl_sync(FULL, S, k - 1);
-            }
-        }
-    }
+// the minima are staged [chunk][row] through shared memory (coalesced reads); lane l of a
+// row's warp keeps the sorted 8 smallest of the chunks l, l+32, ...; the k-th smallest is
+// then popped off the 32 lane heads with warp min-reductions.  (Beyond 256 chunks a lane
+// may drop a minimum; the result is then the k-th of a subset: still a valid pivot, as at
+// least k elements lie at or below it.)  The 4 rows of a warp run interleaved.
+constexpr int PV_ROWS = 32, PV_SLAB = 256, PV_PER = PV_SLAB / 32;
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
 }
-__global__ void __launch_bounds__(256)
+// sorted 8 smallest of a (sorted) and b (unsorted): sort b, then merge keeping 8
+__device__ __forceinline__ void pv_fold(uint32_t (&a)[PV_PER], uint32_t (&b)[PV_PER], bool first) {
+    // odd-even merge sort of 8 (19 compare-exchanges)
+    cswap(b[0], b[1]); cswap(b[2], b[3]); cswap(b[4], b[5]); cswap(b[6], b[7]);
+    cswap(b[0], b[2]); cswap(b[1], b[3]); cswap(b[4], b[6]); cswap(b[5], b[7]);
+    cswap(b[1], b[2]); cswap(b[5], b[6]);
+    cswap(b[0], b[4]); cswap(b[1], b[5]); cswap(b[2], b[6]); cswap(b[3], b[7]);
+    cswap(b[2], b[4]); cswap(b[3], b[5]);
+    cswap(b[1], b[2]); cswap(b[3], b[4]); cswap(b[5], b[6]);
+    if (first) {
+        #pragma unroll
+        for (int i = 0; i < PV_PER; ++i) a[i] = b[i];
+        return;
+    }
+    // the 8 smallest of two sorted 8-lists: min(a[i], b[7-i]) is a bitonic sequence
+    #pragma unroll
+    for (int i = 0; i < PV_PER; ++i) a[i] = min(a[i], b[PV_PER - 1 - i]);
+    cswap(a[0], a[4]); cswap(a[1], a[5]); cswap(a[2], a[6]); cswap(a[3], a[7]);
+    cswap(a[0], a[2]); cswap(a[1], a[3]); cswap(a[4], a[6]); cswap(a[5], a[7]);
+    cswap(a[0], a[1]); cswap(a[2], a[3]); cswap(a[4], a[5]); cswap(a[6], a[7]);
+}
+__global__ void __launch_bounds__(256, 2)
 pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int k, int metric,
                        float* __restrict__ thr, int32_t* __restrict__ cnt) {
     __shared__ uint32_t tile[PV_SLAB][PV_ROWS + 1];
@@ -933,25 +937,59 @@ pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M
         const int64_t row = r0 + threadIdx.x;
         if (row >= M && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
     }
-    uint32_t S[4], Tk[4];  // the warp's 4 rows: sorted smallest keys (lane i = i-th), k-th key
+    uint32_t a[4][PV_PER];  // per row of the warp: this lane's sorted 8 smallest
     for (int64_t s0 = 0; s0 < nchunk; s0 += PV_SLAB) {
         const int ns = (int)(nchunk - s0 < PV_SLAB ? nchunk - s0 : PV_SLAB);
         __syncthreads();
-        for (int i = w; i < PV_SLAB; i += 8) {
+        {
+            // all 32 loads of this warp in flight at once (the minima were just written by
+            // the sample GEMM and mostly hit L2)
             const int64_t row = r0 + lane;
-            tile[i][lane] = (i < ns && row < M) ? ukey(__ldg(mins + (s0 + i) * M + row)) : 0xFFFFFFFFu;
+            float x[PV_SLAB / 8];
+            #pragma unroll
+            for (int t = 0; t < PV_SLAB / 8; ++t) {
+                const int i = w + 8 * t;
+                x[t] = (i < ns && row < M) ? __ldg(mins + (s0 + i) * M + row) : __int_as_float(0x7FFFFFFF);
+            }
+            #pragma unroll
+            for (int t = 0; t < PV_SLAB / 8; ++t) {
+                const int i = w + 8 * t;
+                tile[i][lane] = (i < ns && row < M) ? ukey(x[t]) : 0xFFFFFFFFu;
+            }
         }
         __syncthreads();
-        pv_row(tile, w * 4 + 0, ns, s0 == 0, k, S[0], Tk[0]);
-        pv_row(tile, w * 4 + 1, ns, s0 == 0, k, S[1], Tk[1]);
-        pv_row(tile, w * 4 + 2, ns, s0 == 0, k, S[2], Tk[2]);
-        pv_row(tile, w * 4 + 3, ns, s0 == 0, k, S[3], Tk[3]);
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t b[PV_PER];
+            #pragma unroll
+            for (int i = 0; i < PV_PER; ++i) b[i] = tile[lane + 32 * i][w * 4 + j];
+            pv_fold(a[j], b, s0 == 0);
+        }
+    }
+    // pop the k smallest off the lane heads (equal heads pop together)
+    uint32_t T[4] = {0, 0, 0, 0};
+    int c[4] = {0, 0, 0, 0};
+    for (int it = 0; it < k; ++it) {
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (c[j] < k) {
+                const uint32_t mn = __reduce_min_sync(FULL, a[j][0]);
+                const bool mine = a[j][0] == mn;
+                c[j] += __popc(__ballot_sync(FULL, mine));
+                T[j] = mn;
+                if (mine) {
+                    #pragma unroll
+                    for (int i = 0; i < PV_PER - 1; ++i) a[j][i] = a[j][i + 1];
+                    a[j][PV_PER - 1] = 0xFFFFFFFFu;
+                }
+            }
+        }
     }
     #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int64_t row = r0 + w * 4 + j;
         if (lane == 0 && row < M) {
-            const uint32_t tk = Tk[j];
+            const uint32_t tk = T[j];
             const float t = tk == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(tk);
             const float t1 = nextafterf(t, __int_as_float(0x7F800000));
             thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
@@ -974,6 +1012,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
     // the true k nearest (ties included) is a candidate; otherwise redo (flag bit 2)
     if (n < k && lane == 0) atomicOr(flag, 2);
     n = n < cap ? n : cap;
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
     // sorted best-32 (key, idx) pairs (lane i = i-th); later groups of 32 candidates insert
     // only the pairs that beat the current k-th (ballot), one shuffle-shift per insertion
     const uint32_t* rk = ckey + row * cap;

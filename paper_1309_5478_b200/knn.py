@@ -27,7 +27,7 @@ STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_N
 SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
-           "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_profile_enable",
+           "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
            "knn_profile_read"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
@@ -79,6 +79,7 @@ def load_library():
             "knn_fused_plan": (ctypes.c_int, [p, i32]),
             "knn_set_plan": (st, [p, i32]),
             "knn_last_plan": (ctypes.c_int, [p]),
+            "knn_last_candidates": (ctypes.c_int64, [p]),
             "knn_profile_enable": (st, [p, i32]),
             "knn_profile_read": (st, [p, i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_int64)]),
@@ -276,8 +277,14 @@ def set_plan(plan, device=None):
 
 
 def last_plan(device=None):
-    """0 blocked distances+select, 1 fused, 2 symmetric k-NNG distances+select."""
+    """0 blocked distances+select, 1 fused, 2 symmetric k-NNG distances+select,
+    3 pivot plan (symmetric), 4 pivot plan (general block)."""
     return int(load_library().knn_last_plan(context(device)))
+
+
+def last_candidates(device=None):
+    """Candidates the last pivot-plan call kept (sum over rows)."""
+    return int(load_library().knn_last_candidates(context(device)))
 
 
 def fused_plan(k, device=None):

@@ -416,3 +416,20 @@ def test_pivot_certificate_failure_falls_back_exactly():
     env = dict(os.environ, KNN_PIVOT_MARGIN="-0.02")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
+
+
+def test_pivot_large_sample_multi_slab():
+    # a sample of N/2 points gives > 256 chunk minima per row: the pivot kernel's
+    # multi-slab path (per-lane best-8 folds across slabs) must still give a valid pivot
+    code = (
+        "import torch\n"
+        "from paper_1309_5478_b200 import knn, datagen\n"
+        "X = torch.from_numpy(datagen.points(20000, 40, 'clusters', seed=55)).cuda()\n"
+        "gi, gd = knn.graph(X, 24)\n"
+        "assert knn.last_plan() == 3, knn.last_plan()\n"
+        "knn.set_plan(knn.PLAN_MATERIALISED)\n"
+        "ri, rd = knn.graph(X, 24)\n"
+        "assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))\n")
+    env = dict(os.environ, KNN_PIVOT_DIV="2")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
