@@ -899,7 +899,7 @@ __device__ __forceinline__ uint32_t warp_sort32(uint32_t v) {
 // row's warp keeps the sorted 8 smallest of the chunks l, l+32, ...; the k-th smallest is
 // then popped off the 32 lane heads with warp min-reductions.  (Beyond 256 chunks a lane
 // may drop a minimum; the result is then the k-th of a subset: still a valid pivot, as at
-// least k elements lie at or below it.)  The 4 rows of a warp run interleaved.
+// least k elements lie at or below it.)  One warp per row, 32 warps per CTA.
 constexpr int PV_ROWS = 32, PV_SLAB = 256, PV_PER = PV_SLAB / 32;
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
@@ -927,85 +927,94 @@ __device__ __forceinline__ void pv_fold(uint32_t (&a)[PV_PER], uint32_t (&b)[PV_
     cswap(a[0], a[2]); cswap(a[1], a[3]); cswap(a[4], a[6]); cswap(a[5], a[7]);
     cswap(a[0], a[1]); cswap(a[2], a[3]); cswap(a[4], a[5]); cswap(a[6], a[7]);
 }
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(32 * PV_ROWS, 2)
 pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int k, int metric,
                        float* __restrict__ thr, int32_t* __restrict__ cnt) {
     __shared__ uint32_t tile[PV_SLAB][PV_ROWS + 1];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // warp w owns row r0 + w
     const int64_t r0 = (int64_t)blockIdx.x * PV_ROWS;
     if (threadIdx.x < PV_ROWS) {  // zero padding of thr (read as whole tiles by the SYM partition)
         const int64_t row = r0 + threadIdx.x;
         if (row >= M && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
     }
-    uint32_t a[4][PV_PER];  // per row of the warp: this lane's sorted 8 smallest
+    uint32_t a[PV_PER];  // this lane's sorted 8 smallest of the row's chunks lane, lane+32, ...
     for (int64_t s0 = 0; s0 < nchunk; s0 += PV_SLAB) {
         const int ns = (int)(nchunk - s0 < PV_SLAB ? nchunk - s0 : PV_SLAB);
         __syncthreads();
         {
-            // all 32 loads of this warp in flight at once (the minima were just written by
-            // the sample GEMM and mostly hit L2)
             const int64_t row = r0 + lane;
-            float x[PV_SLAB / 8];
+            float x[PV_SLAB / PV_ROWS];  // all loads of this warp in flight at once
             #pragma unroll
-            for (int t = 0; t < PV_SLAB / 8; ++t) {
-                const int i = w + 8 * t;
-                x[t] = (i < ns && row < M) ? __ldg(mins + (s0 + i) * M + row) : __int_as_float(0x7FFFFFFF);
+            for (int t = 0; t < PV_SLAB / PV_ROWS; ++t) {
+                const int i = w + PV_ROWS * t;
+                x[t] = (i < ns && row < M) ? __ldg(mins + (s0 + i) * M + row) : 0.0f;
             }
             #pragma unroll
-            for (int t = 0; t < PV_SLAB / 8; ++t) {
-                const int i = w + 8 * t;
+            for (int t = 0; t < PV_SLAB / PV_ROWS; ++t) {
+                const int i = w + PV_ROWS * t;
                 tile[i][lane] = (i < ns && row < M) ? ukey(x[t]) : 0xFFFFFFFFu;
             }
         }
         __syncthreads();
+        uint32_t b[PV_PER];
         #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            uint32_t b[PV_PER];
-            #pragma unroll
-            for (int i = 0; i < PV_PER; ++i) b[i] = tile[lane + 32 * i][w * 4 + j];
-            pv_fold(a[j], b, s0 == 0);
-        }
+        for (int i = 0; i < PV_PER; ++i) b[i] = tile[lane + 32 * i][w];
+        pv_fold(a, b, s0 == 0);
     }
     // pop the k smallest off the lane heads (equal heads pop together)
-    uint32_t T[4] = {0, 0, 0, 0};
-    int c[4] = {0, 0, 0, 0};
-    for (int it = 0; it < k; ++it) {
-        #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (c[j] < k) {
-                const uint32_t mn = __reduce_min_sync(FULL, a[j][0]);
-                const bool mine = a[j][0] == mn;
-                c[j] += __popc(__ballot_sync(FULL, mine));
-                T[j] = mn;
-                if (mine) {
-                    #pragma unroll
-                    for (int i = 0; i < PV_PER - 1; ++i) a[j][i] = a[j][i + 1];
-                    a[j][PV_PER - 1] = 0xFFFFFFFFu;
-                }
-            }
+    uint32_t T = 0;
+    for (int c = 0; c < k;) {
+        const uint32_t mn = __reduce_min_sync(FULL, a[0]);
+        const bool mine = a[0] == mn;
+        c += __popc(__ballot_sync(FULL, mine));
+        T = mn;
+        if (mine) {
+            #pragma unroll
+            for (int i = 0; i < PV_PER - 1; ++i) a[i] = a[i + 1];
+            a[PV_PER - 1] = 0xFFFFFFFFu;
         }
     }
-    #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int64_t row = r0 + w * 4 + j;
-        if (lane == 0 && row < M) {
-            const uint32_t tk = T[j];
-            const float t = tk == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(tk);
-            const float t1 = nextafterf(t, __int_as_float(0x7F800000));
-            thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
-            cnt[row] = 0;
-        }
+    const int64_t row = r0 + w;
+    if (lane == 0 && row < M) {
+        const float t = T == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(T);
+        const float t1 = nextafterf(t, __int_as_float(0x7F800000));
+        thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
+        cnt[row] = 0;
     }
 }
 
-// Exact top-k (k <= 32) of each row's candidate list: warp per row, folds of 32.
+// Exact top-k (k <= 32) of each row's candidate list, warp per row.  Up to 512
+// candidates: each lane sorts its <= 16 keys in registers and parks them in shared memory;
+// the k-th smallest key T is popped off the 32 lane heads with warp min-reductions; the
+// pairs with key < T, and those with key == T, are compacted and one 32-wide bitonic sort
+// orders them (ties at T beyond 32 pairs, or more than 512 candidates: the radix select of
+// warpsel.cuh over the list instead).
+constexpr int CS_PER = 16;
+__device__ __forceinline__ void sort16(uint32_t (&v)[CS_PER]) {
+    #pragma unroll
+    for (int size = 2; size <= CS_PER; size <<= 1)
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1)
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool asc = (i & size) == 0;
+                    const uint32_t lo = min(v[i], v[j]), hi = max(v[i], v[j]);
+                    v[i] = asc ? lo : hi;
+                    v[j] = asc ? hi : lo;
+                }
+            }
+}
 __global__ void __launch_bounds__(256)
 candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
                         const uint32_t* __restrict__ cidx, int cap, int64_t M, int k,
                         int64_t idx_offset, int32_t* __restrict__ out_idx,
                         float* __restrict__ out_dist, int32_t* __restrict__ flag) {
-    const int lane = threadIdx.x & 31;
-    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
+    __shared__ uint32_t hist[8][256], skey[8][32], sidx[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * 8 + w;
     if (row >= M) return;
     int n = cnt[row];
     // certificate of the partition: k elements at or below the pivot means every element of
@@ -1013,38 +1022,78 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
     if (n < k && lane == 0) atomicOr(flag, 2);
     n = n < cap ? n : cap;
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
-    // sorted best-32 (key, idx) pairs (lane i = i-th); later groups of 32 candidates insert
-    // only the pairs that beat the current k-th (ballot), one shuffle-shift per insertion
     const uint32_t* rk = ckey + row * cap;
     const uint32_t* ri = cidx + row * cap;
-    auto load = [&](int o) -> uint64_t {
-        const int i = o + lane;
-        return i < n ? ((uint64_t)__ldg(rk + i) << 32 | __ldg(ri + i)) : ~0ull;
-    };
-    uint64_t v[1] = {load(0)};
-    uint64_t nx = load(32);
-    ws::warp_bitonic<1>(v);
-    uint64_t S = v[0];
-    uint64_t Tk = __shfl_sync(FULL, S, k - 1);
-    for (int o = 32; o < n; o += 32) {
-        const uint64_t x = nx;
-        nx = load(o + 32);
-        uint32_t m = __ballot_sync(FULL, x < Tk);
-        while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const uint64_t xv = __shfl_sync(FULL, x, src);
-            if (xv < Tk) {
-                const int pos = __popc(__ballot_sync(FULL, S < xv));  // < k
-                const uint64_t up = __shfl_up_sync(FULL, S, 1);
-                S = lane > pos ? up : (lane == pos ? xv : S);
-                Tk = __shfl_sync(FULL, S, k - 1);
+    const uint32_t* fk = rk;
+    const uint32_t* fi = ri;
+    int m = n;
+    if (n > k) {
+        bool done = false;
+        if (n <= 32 * CS_PER) {
+            uint32_t uk[CS_PER], v[CS_PER];  // this lane's keys (list order), sorted copy
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) uk[i] = lane + 32 * i < n ? __ldg(rk + lane + 32 * i) : 0xFFFFFFFFu;
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) v[i] = uk[i];
+            sort16(v);
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) heads[w][i][lane] = v[i];
+            __syncwarp();
+            uint32_t h = v[0], T = 0;
+            int p = 0;
+            for (int c = 0; c < k;) {
+                const uint32_t mn = __reduce_min_sync(FULL, h);
+                const bool mine = h == mn;
+                c += __popc(__ballot_sync(FULL, mine));
+                T = mn;
+                if (mine) h = ++p < CS_PER ? heads[w][p][lane] : 0xFFFFFFFFu;
+            }
+            // compact the pairs with key < T (fewer than k), then those with key == T
+            int base = 0;
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) {
+                const bool p2 = uk[i] < T;
+                const uint32_t bm = __ballot_sync(FULL, p2);
+                if (p2) {
+                    const int pos = base + __popc(bm & ws::lanemask_lt());
+                    skey[w][pos] = uk[i];
+                    sidx[w][pos] = __ldg(ri + lane + 32 * i);
+                }
+                base += __popc(bm);
+            }
+            int eq = 0;
+            #pragma unroll
+            for (int i = 0; i < CS_PER; ++i) {
+                const bool p2 = uk[i] == T && lane + 32 * i < n;
+                const uint32_t bm = __ballot_sync(FULL, p2);
+                const int pos = base + eq + __popc(bm & ws::lanemask_lt());
+                if (p2 && pos < 32) {
+                    skey[w][pos] = T;
+                    sidx[w][pos] = __ldg(ri + lane + 32 * i);
+                }
+                eq += __popc(bm);
+            }
+            __syncwarp();
+            if (base + eq <= 32) {  // every tie at T kept: the k best are among them
+                fk = skey[w];
+                fi = sidx[w];
+                m = base + eq;
+                done = true;
             }
         }
+        if (!done) {
+            ws::warp_select_k<1>(rk, ri, n, k, skey[w], sidx[w], hist[w]);
+            fk = skey[w];
+            fi = sidx[w];
+            m = k;
+        }
     }
+    // sort the m <= 32 kept pairs; slots past m are empty (-1, +inf)
+    uint64_t v[1] = {lane < m ? ((uint64_t)fk[lane] << 32 | fi[lane]) : ~0ull};
+    ws::warp_bitonic<1>(v);
     if (lane < k) {
-        const uint32_t key = (uint32_t)(S >> 32);
-        out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)S + idx_offset);
+        const uint32_t key = (uint32_t)(v[0] >> 32);
+        out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)v[0] + idx_offset);
         out_dist[row * k + lane] = key == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(key);
     }
 }
@@ -1142,7 +1191,7 @@ cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 32 || nchunk < k) return cudaErrorInvalidValue;
-    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), PV_ROWS), 256, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
+    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), PV_ROWS), 32 * PV_ROWS, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
     return cudaGetLastError();
 }
 

@@ -354,12 +354,14 @@ def materialised_plan():
 
 
 @pytest.mark.parametrize("N,d,k,metric,dist", [(20000, 64, 32, 0, "uniform"), (17000, 128, 8, 1, "clusters"),
-                                               (16384, 3, 1, 0, "gauss")])
+                                               (16384, 3, 1, 0, "gauss"), (16384, 24, 32, 0, "grid")])
 def test_pivot_graph_equals_materialised(N, d, k, metric, dist):
+    # grid: integer coordinates, many tied distances at the k-th (the candidate select's
+    # tie handling) yet few enough candidates to stay on the pivot plan
     kn = knn()
     X = cuda(datagen.points(N, d, dist, seed=N + d + k))
     gi, gd = kn.graph(X, k, metric=metric)
-    assert kn.last_plan() == 3
+    assert kn.last_plan() == 3, kn.last_plan()
     kn.set_plan(kn.PLAN_MATERIALISED)
     try:
         ri, rd = kn.graph(X, k, metric=metric)
