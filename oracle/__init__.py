@@ -29,6 +29,8 @@ _lib = None
 
 L2SQ = 0
 L2 = 1
+COSINE = 2   # key 1 - x.y/(|x||y|) (reading R14); zero norm -> 3.0
+PEARSON = 3  # the cosine key of the mean-centred vectors
 
 
 def build(force: bool = False) -> str:

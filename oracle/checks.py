@@ -22,6 +22,10 @@ from __future__ import annotations
 import numpy as np
 
 REL_TOL = 1e-5  # BASELINE.json north_star: "within relative 1e-5 of (||q||^2 + ||c||^2)"
+# Cosine / Pearson keys (NEXT-2): 1 - cos = ||q^ - c^||^2 / 2 for the unit vectors, so the
+# north star's 1e-5 (||q^||^2 + ||c^||^2) = 2e-5 on the squared distance is 1e-5 on the key
+# (DESIGN.md §3 R19); absolute.
+COS_TOL = 1e-5
 _ULP = 2.0 ** -23
 
 
@@ -38,8 +42,10 @@ def check_rows(gpu_idx, gpu_dist, D64sq, qn, cn, rows, k, metric=0, graph=False)
     """Run E2E-1 and E2E-2 on sampled rows.
 
     gpu_idx/gpu_dist: R×k results of the CUDA path for the query rows ``rows``;
-    D64sq: R×N fp64 SQUARED distances from oracle.dist_rows(metric=L2SQ);
-    qn: fp64 ||q||^2 of the R query rows; cn: fp64 ||c||^2 of all N corpus rows.
+    D64sq: R×N fp64 SQUARED distances from oracle.dist_rows(metric=L2SQ), or the fp64
+    keys for metric 2 / 3 (cosine / Pearson, oracle.dist_rows(metric=2/3));
+    qn: fp64 ||q||^2 of the R query rows; cn: fp64 ||c||^2 of all N corpus rows (unused
+    for metric 2 / 3, whose tolerance is the absolute COS_TOL).
     Returns dict(n_rows, n_pinned, failures=[str]).
     """
     R, N = D64sq.shape
@@ -51,7 +57,7 @@ def check_rows(gpu_idx, gpu_dist, D64sq, qn, cn, rows, k, metric=0, graph=False)
         valid = np.ones(N, bool)
         if graph:
             valid[i] = False
-        tol = REL_TOL * (qn[r] + cn)
+        tol = np.full(N, COS_TOL) if metric in (2, 3) else REL_TOL * (qn[r] + cn)
         cand = np.nonzero(valid)[0]
         order = cand[np.lexsort((cand, D[cand]))]  # oracle order s: (D64, idx)
         kth = order[k - 1]
@@ -71,7 +77,7 @@ def check_rows(gpu_idx, gpu_dist, D64sq, qn, cn, rows, k, metric=0, graph=False)
             failures.append(f"{tag}: list not sorted by (distance, index)")
         S = D[gi]
         t = tol[gi]
-        if metric == 0:
+        if metric != 1:
             bad = np.abs(gd - S) > t
         else:
             lo = np.sqrt(np.maximum(0.0, S - t)) * (1 - _ULP)
@@ -100,9 +106,12 @@ def check_distances(D_gpu, D64sq, qn, cn, metric=0):
     """a-S3 parity: |D_gpu - D64| <= 1e-5 (||q_i||^2 + ||c_j||^2) elementwise.
 
     Returns (max ratio |err| / tol, number of violations)."""
-    tol = REL_TOL * (qn[:, None] + cn[None, :])
+    if metric in (2, 3):
+        tol = np.full((len(qn), len(cn)), COS_TOL)
+    else:
+        tol = REL_TOL * (qn[:, None] + cn[None, :])
     G = np.asarray(D_gpu, np.float64)
-    if metric == 0:
+    if metric != 1:
         err = np.abs(G - D64sq)
         ratio = err / np.maximum(tol, 1e-300)
         return float(ratio.max(initial=0.0)), int((err > tol).sum())

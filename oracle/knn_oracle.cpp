@@ -23,7 +23,8 @@
 // Readings: R1 tie-break by smaller index; R2 output sorted;
 // R3 graph mode excludes self by position; R5 squared distances >= 0
 // (the direct form never goes negative); R6 -0 == +0; NaN ordered after +inf
-// (knn_select rule); R15 norms accumulated in fp64.
+// (knn_select rule); R14 cosine / Pearson keys are 1 - similarity, zero norm -> 3.0;
+// R15 norms accumulated in fp64.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -64,8 +65,47 @@ inline double sqdist64(const float* q, const float* c, int32_t d) {
     return s;
 }
 
-// Metric 0 = squared Euclidean (the paper's d^2), 1 = Euclidean d_E = sqrt(d^2).
+// Cosine key (d_C(x,y) = x.y / (||x|| ||y||), a similarity; reading R14,
+// the selected key is 1 - d_C so that "k smallest" means nearest for every
+// metric; a zero-norm vector gets the sentinel key 3.0).  fp64, t ascending.
+inline double cosine64(const double* q, const double* c, int32_t d) {
+    double dot = 0.0, nq = 0.0, nc = 0.0;
+    for (int32_t t = 0; t < d; ++t) {
+        dot += q[t] * c[t];
+        nq += q[t] * q[t];
+        nc += c[t] * c[t];
+    }
+    if (nq == 0.0 || nc == 0.0) return 3.0;
+    return 1.0 - dot / (std::sqrt(nq) * std::sqrt(nc));
+}
+
+// x^ = x - mean(x) ("x^ = x - x_bar and x_bar is the mean of the entries
+// in x"), in fp64.
+inline void center64(const float* x, int32_t d, double* out) {
+    double s = 0.0;
+    for (int32_t t = 0; t < d; ++t) s += (double)x[t];
+    const double mean = s / (double)d;
+    for (int32_t t = 0; t < d; ++t) out[t] = (double)x[t] - mean;
+}
+
+// Metric 0 = squared Euclidean (the paper's d^2), 1 = Euclidean d_E = sqrt(d^2),
+// 2 = cosine key 1 - d_C, 3 = Pearson key: the cosine key of the centred
+// vectors ("the Pearson distance coefficient is essentially the Cosine
+// distance of the centered data sets").
 inline double metric64(const float* q, const float* c, int32_t d, int32_t metric) {
+    if (metric == 2 || metric == 3) {
+        std::vector<double> a(d), b(d);
+        if (metric == 3) {
+            center64(q, d, a.data());
+            center64(c, d, b.data());
+        } else {
+            for (int32_t t = 0; t < d; ++t) {
+                a[t] = q[t];
+                b[t] = c[t];
+            }
+        }
+        return cosine64(a.data(), b.data(), d);
+    }
     double s = sqdist64(q, c, d);
     return metric == 1 ? std::sqrt(s) : s;
 }
@@ -110,10 +150,11 @@ int oracle_sqnorms(const float* X, int64_t N, int32_t d, double* out) {
 }
 
 // Full distance rows for the queries Q[rows[r]], r < R, against all N corpus points:
-// out[r*N + j] = d(Q[rows[r]], X[j]) in fp64 (metric 0: d^2, metric 1: d_E).
+// out[r*N + j] = d(Q[rows[r]], X[j]) in fp64 (metric 0: d^2, 1: d_E, 2: cosine key,
+// 3: Pearson key).
 int oracle_dist_rows(const float* Q, const int64_t* rows, int64_t R, const float* X, int64_t N,
                      int32_t d, int32_t metric, int32_t threads, double* out) {
-    if (R < 0 || N < 1 || d < 1 || (metric != 0 && metric != 1)) return 1;
+    if (R < 0 || N < 1 || d < 1 || metric < 0 || metric > 3) return 1;
     parallel_rows(R, threads, [&](int64_t r) {
         const float* q = Q + rows[r] * (int64_t)d;
         double* o = out + r * N;
@@ -134,7 +175,7 @@ int oracle_dist_rows(const float* Q, const int64_t* rows, int64_t R, const float
 int oracle_knn(const float* Q, int64_t M, const float* X, int64_t N, int32_t d, int32_t k,
                int32_t metric, int32_t graph, const int64_t* rows, int64_t R, int32_t threads,
                int32_t* idx64, double* dist64, int32_t* idx32, float* dist32) {
-    if (M < 1 || N < 1 || d < 1 || k < 1 || (metric != 0 && metric != 1)) return 1;
+    if (M < 1 || N < 1 || d < 1 || k < 1 || metric < 0 || metric > 3) return 1;
     if (graph && (M != N || k > N - 1)) return 1;
     if (!graph && k > N) return 1;
     for (int64_t r = 0; r < R; ++r)

@@ -262,3 +262,93 @@ def test_pinned_flag_threshold():
         res = checks.check_rows(ref["idx64"], ref["dist64"], D64, n[:1], n, [0], k, graph=True)
         assert res["failures"] == []
         assert res["n_pinned"] == (1 if expect_pinned else 0)
+
+
+# ---------------------------------------------------------- cosine / Pearson (NEXT-2) --
+def test_golden_cosine_pearson():
+    g = golden("cosine_pearson.json")
+    for case in g["cases"]:
+        q = np.array([case["q"]], np.float32)
+        c = np.array([case["c"]], np.float32)
+        key = oracle.dist_rows(q, c, metric=case["metric"])[0, 0]
+        assert abs(key - case["key"]) <= case["abs"], case["what"]
+
+
+def test_cosine_key_of_known_angles():
+    # q, c on the unit circle at angles a, b: key = 1 - cos(a - b) (math library, not the
+    # oracle's dot/norm arithmetic); scaling either vector by a positive factor is a no-op
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        a, b = rng.uniform(-math.pi, math.pi, 2)
+        sq, sc = rng.uniform(0.01, 100.0, 2)
+        q = np.array([[sq * math.cos(a), sq * math.sin(a)]], np.float64)
+        c = np.array([[sc * math.cos(b), sc * math.sin(b)]], np.float64)
+        # the fp32 inputs are the rounded vectors: compare with their exact angle
+        qf, cf = q.astype(np.float32), c.astype(np.float32)
+        ang = math.atan2(float(qf[0, 1]), float(qf[0, 0])) - math.atan2(float(cf[0, 1]), float(cf[0, 0]))
+        key = oracle.dist_rows(qf, cf, metric=oracle.COSINE)[0, 0]
+        assert key == pytest.approx(1.0 - math.cos(ang), abs=1e-12)
+
+
+def test_cosine_equals_half_squared_distance_of_unit_vectors():
+    # ||q/|q| - c/|c| ||^2 = 2 (1 - cos): the cosine key against the (pinned) L2SQ oracle on
+    # vectors normalised in numpy; and the k-NN lists agree (no ties in random data)
+    Q = datagen.points(20, 33, "gauss", seed=11).astype(np.float64)
+    X = datagen.points(300, 33, "gauss", seed=12).astype(np.float64)
+    Qn = Q / np.linalg.norm(Q, axis=1, keepdims=True)
+    Xn = X / np.linalg.norm(X, axis=1, keepdims=True)
+    ref = ((Qn[:, None, :] - Xn[None, :, :]) ** 2).sum(-1) / 2
+    key = oracle.dist_rows(Q.astype(np.float32), X.astype(np.float32), metric=oracle.COSINE)
+    # the fp32 rounding of the inputs moves the key by ~1e-7
+    assert np.max(np.abs(key - ref)) < 1e-6
+    a = oracle.knn(Q.astype(np.float32), X.astype(np.float32), 10, metric=oracle.COSINE)["idx64"]
+    b = np.argsort(ref, axis=1, kind="stable")[:, :10]
+    assert np.array_equal(a, b)
+
+
+def test_pearson_is_cosine_of_centred_vectors():
+    # PAPER.md:71 "the Pearson distance coefficient is essentially the Cosine distance of
+    # the centered data sets": centre in numpy (fp64), then the cosine key; plus affine
+    # invariance y -> a*y + b (a > 0) and sign flip y -> -y giving 2 - key
+    Q = datagen.points(15, 21, "uniform", seed=13).astype(np.float64) * 5 + 2
+    X = datagen.points(200, 21, "uniform", seed=14).astype(np.float64) * 3 - 1
+    Qf, Xf = Q.astype(np.float32), X.astype(np.float32)
+    Qc = Qf.astype(np.float64) - Qf.astype(np.float64).mean(1, keepdims=True)
+    Xc = Xf.astype(np.float64) - Xf.astype(np.float64).mean(1, keepdims=True)
+    sim = (Qc @ Xc.T) / np.outer(np.linalg.norm(Qc, axis=1), np.linalg.norm(Xc, axis=1))
+    key = oracle.dist_rows(Qf, Xf, metric=oracle.PEARSON)
+    assert np.max(np.abs(key - (1 - sim))) < 1e-12
+    # affine invariance on exactly representable transforms (x2 and +8 are exact in fp32 here)
+    X2 = (Xf * 2 + 8).astype(np.float32)
+    key2 = oracle.dist_rows(Qf, X2, metric=oracle.PEARSON)
+    assert np.max(np.abs(key2 - key)) < 1e-6
+    key3 = oracle.dist_rows(Qf, -Xf, metric=oracle.PEARSON)
+    assert np.max(np.abs(key3 - (2 - key))) < 1e-12
+
+
+def test_cosine_graph_semantics():
+    # graph mode drops self by position; ties between parallel copies broken by index
+    X = np.array([[1, 0], [2, 0], [0, 1], [1, 1], [-1, 0]], np.float32)
+    r = oracle.knn(X, X, 3, metric=oracle.COSINE, graph=True)
+    # row 0: (1,0) -> 1 is parallel (key 0), 3 at 45 deg, 2 at 90 deg
+    assert r["idx64"][0].tolist() == [1, 3, 2]
+    assert r["dist64"][0, 0] == pytest.approx(0.0, abs=1e-15)
+    assert r["dist64"][0, 1] == pytest.approx(1 - math.sqrt(0.5), abs=1e-15)
+    # row 4: (-1,0): 2 and 3 at 90/135 deg, 0 and 1 antiparallel (key 2)
+    assert r["idx64"][4].tolist() == [2, 3, 0]
+
+
+def test_checks_cosine_tolerance():
+    X = datagen.points(150, 6, "gauss", seed=28)
+    rows = np.arange(0, 150, 11)
+    k = 4
+    for metric in (oracle.COSINE, oracle.PEARSON):
+        ref = oracle.knn(X, X, k, rows=rows, graph=True, metric=metric)
+        D64 = oracle.dist_rows(X, X, rows=rows, metric=metric)
+        n = oracle.sqnorms(X)
+        res = checks.check_rows(ref["idx64"], ref["dist64"], D64, n[rows], n, rows, k, metric=metric, graph=True)
+        assert res["failures"] == [] and res["n_pinned"] > 0
+        bad = ref["dist64"].copy()
+        bad[2, 1] += 2.5 * checks.COS_TOL
+        res = checks.check_rows(ref["idx64"], bad, D64, n[rows], n, rows, k, metric=metric, graph=True)
+        assert any("tolerance" in f for f in res["failures"])
