@@ -42,7 +42,12 @@ extern "C" {
 typedef struct knn_ctx* knn_ctx_t;
 
 /* Distance metrics.  L2SQ = d^2, L2 = d_E = sqrt(d^2)
- * (PAPER.md:61).  COSINE / PEARSON are NEXT work: KNN_ERR_UNSUPPORTED. */
+ * (PAPER.md:61).  COSINE: the key 1 - x.y / (||x|| ||y||) (PAPER.md:63-66 gives the
+ * similarity d_C; 1 - d_C makes "k smallest" mean nearest), in [0, 2];
+ * a zero-norm vector gets the key 3.0 against everything.  PEARSON: the
+ * cosine key of the mean-centred vectors (a constant vector has zero
+ * centred norm: 3.0).  COSINE / PEARSON need the tensor-core path (KNN_ERR_UNSUPPORTED
+ * under KNN_GEMM=simt).  Keys are within 1e-5 (absolute) of the fp64 definition. */
 typedef enum { KNN_L2SQ = 0, KNN_L2 = 1, KNN_COSINE = 2, KNN_PEARSON = 3 } knn_metric;
 
 typedef enum {
@@ -74,7 +79,7 @@ const char* knn_last_error(knn_ctx_t ctx);
  *
  * knn_graph: the k-NNG of X (N×d).  Row i lists the k nearest OTHER points of x_i:
  * self is excluded by position (reading R3), so 1 <= k <= min(N-1, 1024).
- * metric: KNN_L2SQ or KNN_L2.  out_idx/out_dist: N×k. */
+ * metric: any knn_metric.  out_idx/out_dist: N×k. */
 knn_status knn_graph(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
                      int32_t metric, int32_t* out_idx, float* out_dist, void* stream);
 
@@ -91,7 +96,7 @@ knn_status knn_search(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, 
  *     number fewer than k is padded with (+inf, excluded index) entries, which sort
  *     after every finite distance;
  *   - idx_offset added to every returned index (global index of X's first row).
- * 1 <= k <= min(N, 1024).  metric KNN_L2SQ / KNN_L2.  Blocking, like knn_graph. */
+ * 1 <= k <= min(N, 1024).  metric: any knn_metric.  Blocking, like knn_graph. */
 knn_status knn_search_block(knn_ctx_t ctx, const float* Q, int64_t M, const float* X,
                             int64_t N, int32_t d, int32_t k, int32_t metric,
                             int64_t self_shift, int64_t idx_offset,
@@ -119,6 +124,7 @@ knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, flo
 /* The distance matrix: for i < M, j < N
  *   D[i*ldD + j] = max(||q_i||^2 + ||x_j||^2 - 2 q_i.x_j, 0)   (metric KNN_L2SQ)
  *                 sqrt of that                                (metric KNN_L2)
+ *                 the cosine / Pearson key                     (KNN_COSINE / KNN_PEARSON)
  * with the dot products from the FP32-accurate split tensor-core GEMM
  * and +inf where j == i + self_shift.  ldD >= N.  D: M×ldD floats. */
 knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, int64_t N,

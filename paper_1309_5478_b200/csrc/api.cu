@@ -164,11 +164,14 @@ knn_status set_device(knn_ctx* ctx) {
 
 bool metric_ok(knn_ctx* ctx, int32_t metric, knn_status* st) {
     if (metric == KNN_L2SQ || metric == KNN_L2) return true;
-    if (metric == KNN_COSINE || metric == KNN_PEARSON)
-        *st = fail(ctx, KNN_ERR_UNSUPPORTED, "metric %d (cosine/pearson) is not implemented yet",
+    if (metric == KNN_COSINE || metric == KNN_PEARSON) {
+        // NEXT-2: the tensor-core GEMM only (the FFMA cross-check path is L2)
+        if (ctx->gemm_mode == 0 && ctx->tc_ok) return true;
+        *st = fail(ctx, KNN_ERR_UNSUPPORTED, "metric %d (cosine/pearson) needs the tensor-core path",
                    metric);
-    else
-        *st = fail(ctx, KNN_ERR_ARG, "unknown metric %d", metric);
+        return false;
+    }
+    *st = fail(ctx, KNN_ERR_ARG, "unknown metric %d", metric);
     return false;
 }
 
@@ -186,7 +189,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                      int32_t* out_idx, float* out_dist, cudaStream_t s, bool allow_pivot = true) {
     const bool same = (Q == X) && (M == N);
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
-    const bool fused = knn_fused_plan(ctx, k) == 1;
+    const bool fused = knn_fused_plan(ctx, k) == 1 && metric <= KNN_L2;  // fused.cu: L2 metrics
     // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = k-th smallest of
     // the minima of the 32-column chunks of a column sample (>= the row's k-th distance),
     // then the GEMM keeps only elements <= pivot.
@@ -251,12 +254,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
         t.done();
     }
     if (!same) {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, metric, s));
         t.done();
     }
     if (fused) {
@@ -553,7 +556,7 @@ knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, flo
     if (N == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
     Timed t(ctx, KNN_KERNEL_PREP, static_cast<cudaStream_t>(stream));
-    KNN_CUDA(knn::launch_prep(X, N, d, 0, out_sqn, nullptr, nullptr, nullptr, out_flag,
+    KNN_CUDA(knn::launch_prep(X, N, d, 0, out_sqn, nullptr, nullptr, nullptr, out_flag, 0,
                               static_cast<cudaStream_t>(stream)));
     t.done();
     return KNN_OK;
@@ -594,12 +597,12 @@ knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* 
     layout(carve, pq, px, flag);
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, s));
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
         t.done();
     }
     if (!same) {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, s));
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, metric, s));
         t.done();
     }
     Timed tg(ctx, KNN_KERNEL_GEMM, s);

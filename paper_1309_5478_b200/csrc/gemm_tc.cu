@@ -65,12 +65,18 @@ struct EpiArgs {
 
 // Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
 // materialised value max(u, 0) + 0 (+0 canonicalises -0), sqrt for L2.
+// METRIC 2 (cosine / Pearson): u = 1 - cos in [0, 2]; the zero-norm sentinel terms (5/2
+// per vector, prep.cu) clamp to 3.
 template <int METRIC>
 __device__ __forceinline__ float finalize_dist(float u) {
     float dd = fmaxf(u, 0.0f) + 0.0f;
     if (METRIC == 1) dd = sqrtf(dd);
+    if (METRIC == 2) dd = fminf(dd, 3.0f);
     return dd;
 }
+
+// kernel template argument of a metric: 0 squared L2, 1 L2 (sqrt), 2 cosine / Pearson
+inline int metric_kind(int32_t metric) { return metric == 1 ? 1 : metric >= 2 ? 2 : 0; }
 
 // Append candidate (key, column) to row r's global list; counts overflow.
 __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint32_t key, uint32_t col) {
@@ -259,7 +265,9 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     for (int e = 0; e < 4; ++e) {
                         const int c = 4 * c4 + e;
                         const float nsum = qn + na[e];
-                        const float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], nsum);
+                        float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], nsum);
+                        // cosine: the sentinel clamp before any comparison (key <= T => u <= T)
+                        if (METRIC == 2) u = fminf(u, 3.0f);
                         // MINS: the hi.hi value plus a bound of its error, so that it is never
                         // below the FP32-accurate u of the partition
                         v[c] = MINS ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
@@ -569,7 +577,7 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int grid = (int)(pairs * CLUSTER);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD,
                nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-    auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_STORE, TileSched> : dist_tc_kernel<0, false, MODE_STORE, TileSched>;
+    auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_STORE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_STORE, TileSched> : dist_tc_kernel<0, false, MODE_STORE, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     CUtensorMap md;
@@ -598,7 +606,7 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD,
                nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-    auto kern = metric == 1 ? dist_tc_kernel<1, true, MODE_STORE, SymSched> : dist_tc_kernel<0, true, MODE_STORE, SymSched>;
+    auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE_STORE, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, true, MODE_STORE, SymSched> : dist_tc_kernel<0, true, MODE_STORE, SymSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 1, op.d_pad / BK,
@@ -629,7 +637,7 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
     TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-    auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
+    auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
@@ -656,7 +664,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         SymSched sched{ceil_div(op.N, BN)};
         const int64_t units = sched.n * (sched.n + 1) / 2;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric == 1 ? dist_tc_kernel<1, true, MODE_PIVOT, SymSched> : dist_tc_kernel<0, true, MODE_PIVOT, SymSched>;
+        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE_PIVOT, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, true, MODE_PIVOT, SymSched> : dist_tc_kernel<0, true, MODE_PIVOT, SymSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
@@ -665,7 +673,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
         const int64_t units = sched.n_mp * sched.n_nb;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric == 1 ? dist_tc_kernel<1, false, MODE_PIVOT, TileSched> : dist_tc_kernel<0, false, MODE_PIVOT, TileSched>;
+        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_PIVOT, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_PIVOT, TileSched> : dist_tc_kernel<0, false, MODE_PIVOT, TileSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,

@@ -36,7 +36,8 @@ constexpr int kColPad = 256;
 // prep.cu: row norms (fp64 accumulate) + non-finite flag; optionally the scaled fp16
 // hi/lo split for the tensor-core GEMM (hi/lo may be null).
 cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
-                        float* rscale, __half* hi, __half* lo, int32_t* flag, cudaStream_t s);
+                        float* rscale, __half* hi, __half* lo, int32_t* flag, int32_t metric,
+                        cudaStream_t s);
 
 // gemm_simt.cu: FP32 FFMA distance GEMM with the fused epilogue.
 cudaError_t launch_dist_simt(const float* Q, const float* qn, int64_t M, const float* X,

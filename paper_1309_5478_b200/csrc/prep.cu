@@ -17,6 +17,13 @@
 //
 // Validation (reading R8): flag = 1 if any x is NaN/inf or
 // ||x||^2 >= FLT_MAX/4 (which bounds every distance below FLT_MAX).
+//
+// Cosine / Pearson (NEXT-2): the same GEMM computes 1 - cos.  Pearson
+// first centres the vector (fp64 mean, PAPER.md:69-71 / 85 "we center each vector"; the
+// centred value is rounded to fp32 once).  The per-vector terms become sqn = 1/2 (5/2 for
+// a zero-norm vector: the epilogue's clamp at 3 gives SPEC.md:143's sentinel) and
+// rscale = 2^-sh / (sqrt(2) ||x||), so the epilogue's fma(acc * (-2 rs_q), rs_x, 1/2 + 1/2)
+// is 1 - x.y / (||x|| ||y||).
 #include "internal.cuh"
 
 #include <cfloat>
@@ -29,7 +36,7 @@ constexpr int kWarpsPerBlock = 8;
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
             float* __restrict__ sqn, float* __restrict__ rscale, __half* __restrict__ hi,
-            __half* __restrict__ lo, int32_t* __restrict__ flag) {
+            __half* __restrict__ lo, int32_t* __restrict__ flag, int32_t metric) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (row >= N) {
@@ -42,15 +49,30 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
         return;
     }
     const float* x = X + row * (int64_t)d;
+    const bool angular = hi != nullptr && (metric == 2 || metric == 3);
 
+    // Pearson: the vector mean, fp64; the operands are x - mean
+    double mean = 0.0;
+    bool finite = true;
+    if (angular && metric == 3) {
+        double s1 = 0.0;
+        for (int t = lane; t < d; t += 32) {
+            const float v = __ldg(x + t);
+            finite &= isfinite(v);
+            s1 += (double)v;
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+        mean = s1 / (double)d;
+    }
     double s = 0.0;
     float amax = 0.0f;
-    bool finite = true;
     for (int t = lane; t < d; t += 32) {
         float v = __ldg(x + t);
         finite &= isfinite(v);
-        amax = fmaxf(amax, fabsf(v));
-        s += (double)v * (double)v;
+        const double c = (double)v - mean;
+        amax = fmaxf(amax, fabsf((float)c));
+        s += c * c;
     }
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -58,9 +80,11 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
         amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
     }
     finite = __all_sync(0xFFFFFFFFu, finite);
-    const float n2 = (float)s;
     if (lane == 0) {
-        sqn[row] = n2;
+        // L2: ||x||^2.  Cosine / Pearson: the GEMM epilogue's "norm" term is 1/2 per
+        // vector, so ||q||^2 + ||x||^2 = 1 and the epilogue yields 1 - cos; a zero-norm
+        // vector gets 5/2, which the cosine clamp turns into the sentinel 3
+        sqn[row] = angular ? (s > 0.0 ? 0.5f : 2.5f) : (float)s;
         if (flag && (!finite || !(s < (double)(FLT_MAX / 4)))) *flag = 1;
     }
     if (hi == nullptr) return;
@@ -75,11 +99,21 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
     // 2^sh may exceed the fp32 range for subnormal-only rows: apply it in two exact steps.
     const int sh1 = sh > 120 ? 120 : sh;
     const float s1 = ldexpf(1.0f, sh1), s2 = ldexpf(1.0f, sh - sh1);
-    if (lane == 0) rscale[row] = ldexpf(1.0f, -sh);
+    if (lane == 0) {
+        // L2: 2^-sh (the epilogue multiplies -2 rs_q rs_x).  Cosine / Pearson:
+        // 2^-sh / (sqrt(2) ||x||), so that -2 rs_q rs_x = -2^-(shq+shx) / (||q|| ||x||)
+        rscale[row] = !angular ? ldexpf(1.0f, -sh)
+                               : (s > 0.0 ? (float)(ldexp(1.0, -sh) / (sqrt(2.0) * sqrt(s))) : 0.0f);
+    }
     __half* h = hi + row * (int64_t)d_pad;
     __half* l = lo + row * (int64_t)d_pad;
     for (int t = lane; t < d_pad; t += 32) {
-        float v = (t < d && finite) ? __ldg(x + t) * s1 * s2 : 0.0f;
+        float v = 0.0f;
+        if (t < d && finite) {
+            // exact power-of-two scaling of x (or of the fp32-rounded centred value)
+            const float xv = metric == 3 && angular ? (float)((double)__ldg(x + t) - mean) : __ldg(x + t);
+            v = xv * s1 * s2;
+        }
         __half vh = __float2half_rn(v);
         h[t] = vh;
         l[t] = __float2half_rn(v - __half2float(vh));
@@ -89,10 +123,11 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
 }  // namespace
 
 cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
-                        float* rscale, __half* hi, __half* lo, int32_t* flag, cudaStream_t s) {
+                        float* rscale, __half* hi, __half* lo, int32_t* flag, int32_t metric,
+                        cudaStream_t s) {
     if (N == 0) return cudaSuccess;
     dim3 grid((unsigned)ceil_div(hi != nullptr ? round_up(N, (int64_t)kColPad) : N, kWarpsPerBlock));
-    prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag);
+    prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag, metric);
     return cudaGetLastError();
 }
 

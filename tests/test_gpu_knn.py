@@ -96,7 +96,8 @@ def run_graph(X, k, metric=0):
 
 
 def e2e_check(Q, X, gi, gd, k, rows, graph, metric=0, min_pinned=0.0):
-    D64 = oracle.dist_rows(Q, X, rows=rows)
+    # L2 is checked in the squared domain; cosine / Pearson on the keys themselves
+    D64 = oracle.dist_rows(Q, X, rows=rows, metric=metric if metric >= 2 else 0)
     res = checks.check_rows(gi[rows], gd[rows], D64, oracle.sqnorms(Q[rows]), oracle.sqnorms(X),
                             rows, k, metric=metric, graph=graph)
     assert res["failures"] == [], res["failures"][:5]
@@ -222,8 +223,8 @@ def test_errors():
         k.graph(X, 10)
     assert e.value.status == 1
     with pytest.raises(k.KnnError) as e:
-        k.graph(X, 3, metric=2)
-    assert e.value.status == 2
+        k.graph(X, 3, metric=7)
+    assert e.value.status == 1
     big = cuda(datagen.points(2000, 4, "uniform", seed=12))
     with pytest.raises(k.KnnError) as e:
         k.graph(big, 1025)
