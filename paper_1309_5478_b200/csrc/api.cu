@@ -233,8 +233,10 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     float* thr = nullptr;
     int32_t* cnt = nullptr;
     uint32_t *ckey = nullptr, *cidx = nullptr;
+    int32_t* redo = nullptr;
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
+        if (!fused && !pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
         if (fused && S > 1) {
             part_i = c.take<int32_t>((size_t)S * M * k);
             part_d = c.take<float>((size_t)S * M * k);
@@ -306,7 +308,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         KNN_CUDA(knn::launch_dist_tc_sym(op, metric, D, ldD, ctx->num_sms, s));
         tg.done();
         Timed ts(ctx, KNN_KERNEL_SELECT, s);
-        KNN_CUDA(knn::launch_select(D, M, N, ldD, k, idx_offset, out_idx, out_dist, s));
+        KNN_CUDA(knn::launch_select(D, M, N, ldD, k, idx_offset, out_idx, out_dist, redo, s));
         ts.done();
         return KNN_OK;
     }
@@ -325,7 +327,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         tg.done();
         Timed ts(ctx, KNN_KERNEL_SELECT, s);
         KNN_CUDA(knn::launch_select(D, R, N, ldD, k, idx_offset, out_idx + r0 * k,
-                                    out_dist + r0 * k, s));
+                                    out_dist + r0 * k, redo, s));
         ts.done();
     }
     return KNN_OK;
@@ -626,9 +628,11 @@ knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64
     if (M > 0 && (!D || !out_idx || !out_dist)) return fail(ctx, KNN_ERR_ARG, "null pointer");
     if (M == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
+    // workspace: the redo row list of the sampled-pivot select (M + 1 int32)
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, (size_t)(M + 1) * sizeof(int32_t) + 256));
     Timed t(ctx, KNN_KERNEL_SELECT, static_cast<cudaStream_t>(stream));
     KNN_CUDA(knn::launch_select(D, M, N, ldD, k, 0, out_idx, out_dist,
-                                static_cast<cudaStream_t>(stream)));
+                                static_cast<int32_t*>(ctx->ws), static_cast<cudaStream_t>(stream)));
     t.done();
     return KNN_OK;
 }

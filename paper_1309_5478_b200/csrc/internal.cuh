@@ -87,8 +87,11 @@ cudaError_t launch_knn_fused(const TcOperands& op, int32_t metric, int64_t self_
                              int num_sms, cudaStream_t s);
 
 // select.cu
+// redo: workspace of M + 1 int32 for the sampled-pivot plan of the CTA-per-row select (null:
+// plain running threshold).
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
-                          int64_t idx_offset, int32_t* out_idx, float* out_dist, cudaStream_t s);
+                          int64_t idx_offset, int32_t* out_idx, float* out_dist, int32_t* redo,
+                          cudaStream_t s);
 cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
                          int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                          float* out_dist, cudaStream_t s);

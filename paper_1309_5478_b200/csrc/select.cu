@@ -29,6 +29,9 @@
 #include "warpsel.cuh"
 
 #include <climits>
+#include <cmath>
+
+#define KNN_CUDA_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
 
 namespace knn {
 namespace {
@@ -179,7 +182,78 @@ __device__ void block_bitonic(uint32_t* key, uint32_t* idx, int KP) {
     }
 }
 
-// The finishing steps shared by select and merge: exact k, sort, write.
+// Register bitonic sort of KP = E * (KP / E threads) pairs by (key, idx), packed as
+// u64 = key << 32 | idx (pairs are distinct), fully unrolled for the compile-time KP.
+// Thread t holds positions t*E .. t*E+E-1: strides < E are exchanged in registers,
+// strides < 32E with __shfl_xor across lanes, larger (cross-warp) strides through shared
+// memory `tmp` (KP u64).  The first k positions are written to out_idx (idx + idx_offset)
+// and out_dist (the key's float).
+template <int THREADS, int KP>
+__device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k, uint64_t* tmp,
+                                 int64_t idx_offset, int32_t* out_idx, float* out_dist) {
+    constexpr int E = KP >= 4 * THREADS ? 4 : KP >= 2 * THREADS ? 2 : 1;
+    static_assert(KP <= E * THREADS, "KP too large for the block");
+    const int t = threadIdx.x;
+    const bool act = t * E < KP;
+    uint64_t v[E];
+    #pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = act ? ((uint64_t)key[t * E + e] << 32 | idx[t * E + e]) : ~0ull;
+    #pragma unroll
+    for (int size = 2; size <= KP; size <<= 1) {
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32 * E) {
+                csync<THREADS>();
+                if (act) {
+                    #pragma unroll
+                    for (int e = 0; e < E; ++e) tmp[t * E + e] = v[e];
+                }
+                csync<THREADS>();
+                if (act) {
+                    #pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int p = t * E + e;
+                        const uint64_t o = tmp[p ^ stride];
+                        const bool up = ((p & size) == 0) == ((p & stride) == 0);  // keep min
+                        v[e] = up ? min(v[e], o) : max(v[e], o);
+                    }
+                }
+            } else if (stride >= E) {
+                #pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int p = t * E + e;
+                    const uint64_t o = __shfl_xor_sync(FULL, v[e], stride / E);
+                    const bool up = ((p & size) == 0) == ((p & stride) == 0);
+                    v[e] = up ? min(v[e], o) : max(v[e], o);
+                }
+            } else {
+                #pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (e & stride) continue;
+                    const int f = e + stride;
+                    const bool asc = ((t * E + e) & size) == 0;
+                    const uint64_t lo = min(v[e], v[f]), hi = max(v[e], v[f]);
+                    v[e] = asc ? lo : hi;
+                    v[f] = asc ? hi : lo;
+                }
+            }
+        }
+    }
+    if (act) {
+        #pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int p = t * E + e;
+            if (p < k) {
+                out_idx[p] = (int32_t)((int64_t)(uint32_t)v[e] + idx_offset);
+                out_dist[p] = ukey_to_float((uint32_t)(v[e] >> 32));
+            }
+        }
+    }
+}
+
+// The finishing steps shared by select and merge: exact k, sort, write.  `tmp` needs KP
+// u64 of shared memory (the candidate buffer, free at this point, serves).
 template <int THREADS>
 __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int KP,
                              uint32_t* kkey, uint32_t* kidx, uint32_t* hist, Scal* sc,
@@ -198,10 +272,17 @@ __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int
         kidx[i] = 0xFFFFFFFFu;
     }
     csync<THREADS>();
-    block_bitonic<THREADS>(kkey, kidx, KP);
-    for (int r = threadIdx.x; r < k; r += THREADS) {
-        out_idx[r] = (int32_t)((int64_t)kidx[r] + idx_offset);
-        out_dist[r] = ukey_to_float(kkey[r]);
+    // ckey, cidx, kkey, kidx are contiguous (2 cap + 2 KP words, 8-byte aligned) and dead
+    // once the sort holds its pairs in registers: KP u64 of scratch
+    uint64_t* tmp = reinterpret_cast<uint64_t*>(ckey);
+    switch (KP) {
+#define KNN_SORT_CASE(P) \
+    case P: block_sort_write<THREADS, P>(kkey, kidx, k, tmp, idx_offset, out_idx, out_dist); break;
+        KNN_SORT_CASE(1) KNN_SORT_CASE(2) KNN_SORT_CASE(4) KNN_SORT_CASE(8) KNN_SORT_CASE(16)
+        KNN_SORT_CASE(32) KNN_SORT_CASE(64) KNN_SORT_CASE(128) KNN_SORT_CASE(256)
+        KNN_SORT_CASE(512) KNN_SORT_CASE(1024)
+#undef KNN_SORT_CASE
+        default: break;
     }
 }
 
@@ -453,18 +534,92 @@ __device__ __forceinline__ bool block_append(const float4 (&cur)[VPT], uint32_t 
     return over;
 }
 
+// Scan append for the ring select: each thread tests its EPT elements (held in registers)
+// into a bit mask; a warp-inclusive scan of the per-thread counts gives every survivor its
+// slot and one shared atomic per warp reserves the warp's range; survivors are re-read
+// from the ring slot `buf` (still owned by the consumers) by dynamic index, so the store
+// loop only visits set bits.  At low survival rates this costs ~2 instructions per element.
+// Returns true if the buffer grew past `limit` (warp-uniform); `*any_out` = some survivor
+// in the warp.
+template <int CTHREADS, int VPT>
+__device__ __forceinline__ bool ring_append(const float4 (&cur)[VPT], const float* buf, uint32_t T,
+                                            float tf, bool fast, bool full, int64_t N, int64_t base,
+                                            uint32_t* ckey, uint32_t* cidx, int* s_count, int limit) {
+    static_assert(VPT * 4 <= 32, "mask width");
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    uint32_t pm = 0;
+    if (full && fast) {  // steady state: float compares against the threshold's image
+        #pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            pm |= (uint32_t)(cur[j].x < tf) << (4 * j) | (uint32_t)(cur[j].y < tf) << (4 * j + 1) |
+                  (uint32_t)(cur[j].z < tf) << (4 * j + 2) | (uint32_t)(cur[j].w < tf) << (4 * j + 3);
+        }
+    } else if (full && T == kKeyMax) {  // no threshold yet: every key (NaN included) is < T
+        pm = VPT * 4 == 32 ? 0xFFFFFFFFu : (1u << (VPT * 4)) - 1u;
+    } else {
+        #pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const float c4[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+            #pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                bool ok = fast ? (c4[c] < tf) : (ukey(c4[c]) < T);
+                if (!full) ok = ok && base + 4 * (j * CTHREADS + tid) + c < N;
+                pm |= (uint32_t)ok << (4 * j + c);
+            }
+        }
+    }
+    if (!__any_sync(FULL, pm != 0)) return false;
+    const int my = __popc(pm);
+    int incl = my;
+    #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += n;
+    }
+    const int wtot = __shfl_sync(FULL, incl, 31);
+    int wbase = 0;
+    if (lane == 31) wbase = atomicAdd(s_count, wtot);
+    wbase = __shfl_sync(FULL, wbase, 31);
+    int off = wbase + incl - my;
+    while (pm) {
+        const int e = __ffs(pm) - 1;
+        pm &= pm - 1;
+        const int o = 4 * ((e >> 2) * CTHREADS + tid) + (e & 3);
+        ckey[off] = ukey(buf[o]);
+        cidx[off] = (uint32_t)(base + o);
+        ++off;
+    }
+    return wbase + wtot > limit;
+}
+
 // ------------------------------------------------------------------ ring select ------
 // Persistent CTAs, one row at a time: a producer warp streams the row in CHUNK-element
 // slices through a STAGES-deep shared-memory ring with 1-D bulk async copies (the TMA
 // engine; completion on mbarriers), prefetching across row boundaries, so the bytes in
 // flight do not depend on registers; CTHREADS consumer threads filter each slice with the
-// running threshold and compact survivors with ballot/popc exactly as above.
+// running threshold and compact survivors (warp scan + one shared atomic per warp).
 // Requires 16-byte aligned rows (ldD % 4 == 0, aligned D).
+//
+// Rows: list == nullptr -> rows 0..M-1; else rows list[1 .. list[0]] (the redo pass).
+//
+// Sampled pivot (r_pivot > 0; the quick multi-select of PAPER.md:56 with its pivot drawn
+// from a sample, reading R18): the first chunk is the sample; its r_pivot-th best pair
+// (key, idx) is the pivot and every later element must beat it.  r_pivot < k is chosen so
+// that ~1.4k elements of the row beat the pivot, which removes the repeated rebuilds of
+// the plain running threshold (the k-th of the first chunk is far above the row's k-th
+// when k/N is large).  Exactness: the candidates are then EXACTLY the elements that
+// precede the pivot in the order (key, idx) (later chunks have larger indices, so the
+// strict key test is the pair test), so the result is the true top k iff at least k
+// candidates remain at the end.  A row with fewer (a sample unlike the rest of the row,
+// e.g. a sorted row) is appended to redo[1..] (count redo[0]) and selected again by a
+// second launch without the pivot; a buffer overflow instead rebuilds to the exact k
+// best, after which the usual running-threshold invariant holds.
 template <int CTHREADS, int CHUNK, int STAGES>
-__global__ void __launch_bounds__(CTHREADS + 32, 1)
+__global__ void __launch_bounds__(CTHREADS + 32, 2)
 select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int cap,
                    int KP, int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
-                   float* __restrict__ out_dist) {
+                   float* __restrict__ out_dist, const int32_t* __restrict__ list, int r_pivot,
+                   int32_t* __restrict__ redo) {
     constexpr int VPT = CHUNK / CTHREADS / 4;  // float4 per consumer thread per slice
     static_assert(VPT * 4 * CTHREADS == CHUNK, "CHUNK must be a multiple of 4*CTHREADS");
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -481,6 +636,8 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
     const int64_t nchunk = ceil_div(N, CHUNK);
+    const int64_t nrows = list ? (int64_t)list[0] : M;
+    const bool use_pivot = r_pivot > 0 && r_pivot < k && N >= 2 * (int64_t)CHUNK;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full0 + 8 * s, 1);
@@ -496,7 +653,8 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             const uint64_t pol = policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+            for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
+                const int64_t row = list ? (int64_t)list[1 + i] : i;
                 const float* rp = D + row * ldD;
                 for (int64_t c = 0; c < nchunk; ++c) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
@@ -518,11 +676,13 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
     // ------------------------------------------------------------ consumers ----------
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+    for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
+        const int64_t row = list ? (int64_t)list[1 + i] : i;
         if (tid == 0) s_count = 0;
         uint32_t T = kKeyMax;
         float tf = 0.0f;
         bool fast = false;
+        bool piv = use_pivot;  // the sampled pivot still decides the candidate set
         csync<CTHREADS>();
         for (int64_t c = 0; c < nchunk; ++c) {
             const int64_t base = c * CHUNK;
@@ -531,40 +691,57 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             float4 cur[VPT];
             #pragma unroll
             for (int j = 0; j < VPT; ++j) cur[j] = buf[j * CTHREADS + tid];
+            const bool full = base + CHUNK <= N;
+            const bool over = ring_append<CTHREADS, VPT>(cur, reinterpret_cast<const float*>(buf), T, tf,
+                                                         fast, full, N, base, ckey, cidx, &s_count, limit);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);  // slot may be refilled
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
             }
-            const bool full = base + CHUNK <= N;
-            bool any = !(fast && full);
-            if (!any) {
-                #pragma unroll
-                for (int j = 0; j < VPT; ++j)
-                    any |= (cur[j].x < tf) | (cur[j].y < tf) | (cur[j].z < tf) | (cur[j].w < tf);
+            if (piv && c == 0) {
+                // the sample: keep exactly the r_pivot best of the first chunk; the
+                // r_pivot-th is the pivot (strict for the later, larger indices)
+                csync<CTHREADS>();
+                uint32_t tk, ti;
+                block_select_k<CTHREADS>(ckey, cidx, s_count, r_pivot, kkey, kidx, hist, &sc, false, tk, ti);
+                for (int q = tid; q < r_pivot; q += CTHREADS) {
+                    ckey[q] = kkey[q];
+                    cidx[q] = kidx[q];
+                }
+                if (tid == 0) s_count = r_pivot;
+                T = tk;
+                fast = T <= 0xFF800000u;
+                tf = ukey_to_float(T);
+                csync<CTHREADS>();
+                continue;
             }
-            bool over = false;
-            if (__any_sync(FULL, any))
-                over = block_append<VPT>(
-                    cur, T, tf, fast, full, N,
-                    [&](int e) -> int64_t { return base + 4 * ((e >> 2) * CTHREADS + tid) + (e & 3); },
-                    ckey, cidx, &s_count, limit);
             if (named_bar_or(1, CTHREADS, over)) {
                 uint32_t tk, ti;
                 block_select_k<CTHREADS>(ckey, cidx, s_count, k, kkey, kidx, hist, &sc, false, tk, ti);
-                for (int i = tid; i < k; i += CTHREADS) {
-                    ckey[i] = kkey[i];
-                    cidx[i] = kidx[i];
+                for (int q = tid; q < k; q += CTHREADS) {
+                    ckey[q] = kkey[q];
+                    cidx[q] = kidx[q];
                 }
                 if (tid == 0) s_count = k;
                 T = tk;
                 fast = T <= 0xFF800000u;
                 tf = ukey_to_float(T);
+                piv = false;  // k exact best kept: the running-threshold invariant holds
                 csync<CTHREADS>();
             }
         }
         csync<CTHREADS>();
+        if (piv && s_count < k) {
+            // fewer than k elements beat the sampled pivot: select this row again later
+            if (tid == 0) {
+                const int slot = atomicAdd(redo, 1);
+                redo[1 + slot] = (int32_t)row;
+            }
+            csync<CTHREADS>();
+            continue;
+        }
         block_finish<CTHREADS>(ckey, cidx, s_count, k, KP, kkey, kidx, hist, &sc, idx_offset,
                                out_idx + row * k, out_dist + row * k);
         csync<CTHREADS>();
@@ -1112,7 +1289,8 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
-                          int64_t idx_offset, int32_t* out_idx, float* out_dist, cudaStream_t s) {
+                          int64_t idx_offset, int32_t* out_idx, float* out_dist, int32_t* redo,
+                          cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     const int KP = next_pow2(k);
     const bool aligned = (ldD % 4 == 0) && ((reinterpret_cast<uintptr_t>(D) & 15) == 0);
@@ -1145,7 +1323,7 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         return pick(select_warp_kernel<4>);
     }
     if (aligned) {
-        constexpr int CT = 256, CHUNK = 4096, STAGES = 4;
+        constexpr int CT = 256, CHUNK = 4096;
         int cap, limit;
         if (N <= CHUNK) {
             cap = (int)round_up(N, 32);
@@ -1154,18 +1332,39 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
             limit = (int)round_up(k + 256 > 2 * k ? k + 256 : 2 * k, 32);
             cap = CHUNK + limit;
         }
-        const size_t smem = (size_t)STAGES * CHUNK * 4 + 2 * STAGES * 8 +
-                            (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
-        auto kern = select_ring_kernel<CT, CHUNK, STAGES>;
-        if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
-        int per_sm = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT + 32, smem)) != cudaSuccess)
-            return e;
-        int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-        if (grid > M) grid = M;
-        kern<<<(unsigned)grid, CT + 32, smem, s>>>(D, M, N, ldD, k, cap, KP, limit, idx_offset,
-                                                  out_idx, out_dist);
-        return cudaGetLastError();
+        // sampled pivot (see select_ring_kernel): r = the rank in the first chunk whose
+        // expected share of the row is ~k plus four standard deviations
+        int r_pivot = 0;
+        if (redo && N >= 2 * CHUNK) {
+            const double mean = (double)CHUNK * k / (double)N;
+            const double r = std::ceil(mean + 4.0 * std::sqrt(mean) + 2.0);
+            if (r < 0.75 * k) r_pivot = (int)r;
+        }
+        if (r_pivot) KNN_CUDA_TRY(cudaMemsetAsync(redo, 0, sizeof(int32_t), s));
+        auto run = [&](auto kern, int stages, const int32_t* list, int rp, int64_t grid_rows) -> cudaError_t {
+            const size_t smem = (size_t)stages * CHUNK * 4 + 2 * stages * 8 +
+                                (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
+            cudaError_t e2;
+            if ((e2 = set_smem(kern, smem)) != cudaSuccess) return e2;
+            int per_sm = 0;
+            if ((e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CT + 32, smem)) != cudaSuccess)
+                return e2;
+            int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+            if (grid > grid_rows) grid = grid_rows;
+            kern<<<(unsigned)grid, CT + 32, smem, s>>>(D, M, N, ldD, k, cap, KP, limit, idx_offset,
+                                                      out_idx, out_dist, list, rp, redo);
+            return cudaGetLastError();
+        };
+        // 4 ring stages when two CTAs still fit on an SM, else 3
+        const size_t base_smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
+        const bool four = base_smem + 4 * (size_t)CHUNK * 4 + 64 <= 112 * 1024;
+        auto k4 = select_ring_kernel<CT, CHUNK, 4>;
+        auto k3 = select_ring_kernel<CT, CHUNK, 3>;
+        e = four ? run(k4, 4, nullptr, r_pivot, M) : run(k3, 3, nullptr, r_pivot, M);
+        if (e != cudaSuccess || !r_pivot) return e;
+        // redo pass: rows whose sampled pivot kept fewer than k candidates (grid covers
+        // any count; CTAs beyond it exit at once)
+        return four ? run(k4, 4, redo, 0, M) : run(k3, 3, redo, 0, M);
     }
     constexpr int THREADS = 256, VPT = 4, CHUNK = THREADS * VPT * 4;
     int cap, limit;

@@ -174,3 +174,30 @@ def test_warp_select_special_values():
     D[::3, :5] = 1.0
     for k in (1, 17, 128):
         assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("N,k", [(8192, 1024), (20000, 200), (32768, 1024), (32768, 512),
+                                  (65536, 129), (100003, 777)])
+def test_select_sampled_pivot(N, k):
+    """CTA-per-row select with the pivot sampled from the first chunk (k > 128,
+    N >= 2 chunks): uniform rows take the pivot path, sorted rows the redo pass
+    (ascending: too few candidates) or the overflow rebuild (descending), mixed in one
+    call so the redo row list must map back to the right rows."""
+    D = datagen.keys(12, N, "uniform", seed=N + k)
+    D[3] = np.arange(N, dtype=np.float32)          # ascending: pivot too low -> redo
+    D[7] = np.arange(N, 0, -1, dtype=np.float32)   # descending: overflow -> rebuild
+    D[9, : N // 2] = np.float32(5.0)               # sample far above the rest of the row
+    D[10] = np.float32(0.25)                        # all equal: index order decides
+    D[11, 5::3] = np.inf
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+def test_select_sampled_pivot_few_finite():
+    """Rows with fewer finite keys than k on the sampled-pivot path."""
+    N, k = 16384, 600
+    D = np.full((4, N), np.inf, np.float32)
+    D[0, :100] = np.arange(100, dtype=np.float32)
+    D[1, -50:] = 1.0
+    D[2, ::40] = np.nan
+    D[3, 9000:9600] = -np.arange(600, dtype=np.float32)
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
