@@ -41,6 +41,7 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 struct Scal {
     uint32_t bin, before, neq;
     int kept;
+    uint32_t lo, hi;
 };
 
 // Barrier over the THREADS consumer threads 0..THREADS-1 of the CTA (named barrier 1), so
@@ -56,26 +57,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// One 8-bit radix-histogram pass over the candidates.  Counts digit `shift` of the key
-// (on_idx = false) or of the index among candidates whose key == key_eq (on_idx = true),
-// restricted to values v with (v & mask) == prefix; finds the bin holding the rank-th
-// (1-based) value.  Result in sc->{bin, before (count in lower bins), neq (count in bin)}.
-template <int THREADS>
-__device__ void radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt, bool on_idx,
-                           uint32_t key_eq, uint32_t prefix, uint32_t mask, int shift,
-                           uint32_t rank, uint32_t* hist, Scal* sc) {
-    const int tid = threadIdx.x;
-    for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
-    csync<THREADS>();
-    for (int i = tid; i < cnt; i += THREADS) {
-        uint32_t key = ckey[i];
-        uint32_t v = on_idx ? cidx[i] : key;
-        bool ok = on_idx ? (key == key_eq) : true;
-        if (ok && (v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
-    }
-    csync<THREADS>();
-    if (tid < 32) {
-        const int lane = tid;
+// Warp 0 (threads 0..31) scans a 256-bin histogram and records the bin holding the
+// rank-th (1-based) counted value in sc->{bin, before (count in lower bins), neq}.
+__device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t rank, Scal* sc) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         uint32_t c[8], sum = 0;
         #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -102,6 +88,61 @@ __device__ void radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt, 
             }
         }
     }
+}
+
+// Block-wide min and max of the keys ckey[0, cnt) (cnt >= 1), via sc->{lo, hi}.
+template <int THREADS>
+__device__ __forceinline__ void block_key_range(const uint32_t* ckey, int cnt, Scal* sc,
+                                                uint32_t& mn, uint32_t& mx) {
+    uint32_t a = 0xFFFFFFFFu, b = 0;
+    for (int i = threadIdx.x; i < cnt; i += THREADS) {
+        const uint32_t v = ckey[i];
+        a = min(a, v);
+        b = max(b, v);
+    }
+    a = __reduce_min_sync(FULL, a);
+    b = __reduce_max_sync(FULL, b);
+    if (threadIdx.x == 0) {
+        sc->lo = 0xFFFFFFFFu;
+        sc->hi = 0;
+    }
+    csync<THREADS>();
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&sc->lo, a);
+        atomicMax(&sc->hi, b);
+    }
+    csync<THREADS>();
+    mn = sc->lo;
+    mx = sc->hi;
+}
+
+// The shift of the first 8-bit digit that can separate keys in [mn, mx]: the digit just
+// below their common prefix (0 if they differ only in the low 8 bits or are equal).
+__device__ __forceinline__ int top_digit_shift(uint32_t mn, uint32_t mx) {
+    const uint32_t diff = mn ^ mx;
+    const int msb = diff ? 31 - __clz(diff) : 0;
+    return msb > 7 ? msb - 7 : 0;
+}
+
+// One 8-bit radix-histogram pass over the candidates.  Counts digit `shift` of the key
+// (on_idx = false) or of the index among candidates whose key == key_eq (on_idx = true),
+// restricted to values v with (v & mask) == prefix; finds the bin holding the rank-th
+// (1-based) value.  Result in sc->{bin, before (count in lower bins), neq (count in bin)}.
+template <int THREADS>
+__device__ void radix_pass(const uint32_t* ckey, const uint32_t* cidx, int cnt, bool on_idx,
+                           uint32_t key_eq, uint32_t prefix, uint32_t mask, int shift,
+                           uint32_t rank, uint32_t* hist, Scal* sc) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
+    csync<THREADS>();
+    for (int i = tid; i < cnt; i += THREADS) {
+        uint32_t key = ckey[i];
+        uint32_t v = on_idx ? cidx[i] : key;
+        bool ok = on_idx ? (key == key_eq) : true;
+        if (ok && (v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    csync<THREADS>();
+    hist_find(hist, rank, sc);
     csync<THREADS>();
 }
 
@@ -113,13 +154,20 @@ template <int THREADS>
 __device__ void block_select_k(const uint32_t* ckey, const uint32_t* cidx, int cnt, int k,
                                uint32_t* kkey, uint32_t* kidx, uint32_t* hist, Scal* sc,
                                bool exact_idx, uint32_t& Tkey, uint32_t& Tidx) {
-    uint32_t prefix = 0, mask = 0, rank = (uint32_t)k, neq = 0;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+    // digits start just below the common prefix of the candidates' key range; a digit
+    // may overlap bits already fixed by the prefix (their bins are then constant)
+    uint32_t mn, mx;
+    block_key_range<THREADS>(ckey, cnt, sc, mn, mx);
+    const int top = top_digit_shift(mn, mx);
+    uint32_t mask = top + 8 >= 32 ? 0u : ~((1u << (top + 8)) - 1u);
+    uint32_t prefix = mn & mask, rank = (uint32_t)k, neq = 0;
+    for (int shift = top;; shift = shift > 8 ? shift - 8 : 0) {
         radix_pass<THREADS>(ckey, cidx, cnt, false, 0, prefix, mask, shift, rank, hist, sc);
         rank -= sc->before;
-        prefix |= sc->bin << shift;
+        prefix = (prefix & ~(0xFFu << shift)) | (sc->bin << shift);
         mask |= 0xFFu << shift;
         neq = sc->neq;
+        if (shift == 0) break;
     }
     Tkey = prefix;
     Tidx = 0xFFFFFFFFu;
@@ -216,7 +264,7 @@ __device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k
                         const int p = t * E + e;
                         const uint64_t o = tmp[p ^ stride];
                         const bool up = ((p & size) == 0) == ((p & stride) == 0);  // keep min
-                        v[e] = up ? min(v[e], o) : max(v[e], o);
+                        v[e] = ((o < v[e]) == up) ? o : v[e];
                     }
                 }
             } else if (stride >= E) {
@@ -225,7 +273,7 @@ __device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k
                     const int p = t * E + e;
                     const uint64_t o = __shfl_xor_sync(FULL, v[e], stride / E);
                     const bool up = ((p & size) == 0) == ((p & stride) == 0);
-                    v[e] = up ? min(v[e], o) : max(v[e], o);
+                    v[e] = ((o < v[e]) == up) ? o : v[e];
                 }
             } else {
                 #pragma unroll
@@ -233,9 +281,10 @@ __device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k
                     if (e & stride) continue;
                     const int f = e + stride;
                     const bool asc = ((t * E + e) & size) == 0;
-                    const uint64_t lo = min(v[e], v[f]), hi = max(v[e], v[f]);
-                    v[e] = asc ? lo : hi;
-                    v[f] = asc ? hi : lo;
+                    const bool sw = (v[f] < v[e]) == asc;
+                    const uint64_t x = v[e];
+                    v[e] = sw ? v[f] : x;
+                    v[f] = sw ? x : v[f];
                 }
             }
         }
@@ -603,14 +652,13 @@ __device__ __forceinline__ bool ring_append(const float4 (&cur)[VPT], const floa
 // Rows: list == nullptr -> rows 0..M-1; else rows list[1 .. list[0]] (the redo pass).
 //
 // Sampled pivot (r_pivot > 0; the quick multi-select of PAPER.md:56 with its pivot drawn
-// from a sample, reading R18): the first chunk is the sample; its r_pivot-th best pair
-// (key, idx) is the pivot and every later element must beat it.  r_pivot < k is chosen so
-// that ~1.4k elements of the row beat the pivot, which removes the repeated rebuilds of
-// the plain running threshold (the k-th of the first chunk is far above the row's k-th
-// when k/N is large).  Exactness: the candidates are then EXACTLY the elements that
-// precede the pivot in the order (key, idx) (later chunks have larger indices, so the
-// strict key test is the pair test), so the result is the true top k iff at least k
-// candidates remain at the end.  A row with fewer (a sample unlike the rest of the row,
+// from a sample, reading R18): the first chunk is the sample; one histogram of its keys
+// gives a pivot key P with at least r_pivot sample keys below it, and the candidates are
+// all keys < P.  r_pivot < k is chosen so that ~1.4k elements of the row fall below P,
+// which removes the repeated rebuilds of the plain running threshold (the k-th of the
+// first chunk is far above the row's k-th when k/N is large).  Exactness: if at least k
+// keys of the row are < P, the k smallest keys (ties included) are all < P, so the
+// candidates hold the true top k; the count is checked at the end of the row.  A row with fewer (a sample unlike the rest of the row,
 // e.g. a sorted row) is appended to redo[1..] (count redo[0]) and selected again by a
 // second launch without the pivot; a buffer overflow instead rebuilds to the exact k
 // best, after which the usual running-threshold invariant holds.
@@ -678,7 +726,13 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
     uint32_t phase = 0;
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
         const int64_t row = list ? (int64_t)list[1 + i] : i;
-        if (tid == 0) s_count = 0;
+        if (tid == 0) {
+            s_count = 0;
+            sc.lo = 0xFFFFFFFFu;
+            sc.hi = 0;
+        }
+        if (use_pivot)
+            for (int q = tid; q < 256; q += CTHREADS) hist[q] = 0;
         uint32_t T = kKeyMax;
         float tf = 0.0f;
         bool fast = false;
@@ -692,6 +746,44 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             #pragma unroll
             for (int j = 0; j < VPT; ++j) cur[j] = buf[j * CTHREADS + tid];
             const bool full = base + CHUNK <= N;
+            if (piv && c == 0) {
+                // The sample (the first chunk, still in registers): one 8-bit histogram
+                // of its keys on the digit just below the common prefix of their range;
+                // the pivot P is the upper edge of the bin holding the r_pivot-th key, so
+                // at least r_pivot sample keys are < P.  Candidates: every key < P.
+                uint32_t a = 0xFFFFFFFFu, b = 0;
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    const uint32_t u0 = ukey(cur[j].x), u1 = ukey(cur[j].y), u2 = ukey(cur[j].z),
+                                   u3 = ukey(cur[j].w);
+                    a = min(a, min(min(u0, u1), min(u2, u3)));
+                    b = max(b, max(max(u0, u1), max(u2, u3)));
+                }
+                a = __reduce_min_sync(FULL, a);
+                b = __reduce_max_sync(FULL, b);
+                if (lane == 0) {
+                    atomicMin(&sc.lo, a);
+                    atomicMax(&sc.hi, b);
+                }
+                csync<CTHREADS>();
+                const uint32_t mn = sc.lo, mx = sc.hi;
+                const int sh = top_digit_shift(mn, mx);
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    atomicAdd(&hist[(ukey(cur[j].x) >> sh) & 255u], 1u);
+                    atomicAdd(&hist[(ukey(cur[j].y) >> sh) & 255u], 1u);
+                    atomicAdd(&hist[(ukey(cur[j].z) >> sh) & 255u], 1u);
+                    atomicAdd(&hist[(ukey(cur[j].w) >> sh) & 255u], 1u);
+                }
+                csync<CTHREADS>();
+                hist_find(hist, (uint32_t)r_pivot, &sc);
+                csync<CTHREADS>();
+                const uint64_t lowmask = (1ull << (sh + 8)) - 1ull;
+                const uint64_t P = ((uint64_t)mn & ~lowmask) + ((uint64_t)(sc.bin + 1) << sh);
+                T = P >= 0xFFFFFFFFull ? kKeyMax : (uint32_t)P;
+                fast = T <= 0xFF800000u;
+                tf = ukey_to_float(T);
+            }
             const bool over = ring_append<CTHREADS, VPT>(cur, reinterpret_cast<const float*>(buf), T, tf,
                                                          fast, full, N, base, ckey, cidx, &s_count, limit);
             __syncwarp();
@@ -699,23 +791,6 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
-            }
-            if (piv && c == 0) {
-                // the sample: keep exactly the r_pivot best of the first chunk; the
-                // r_pivot-th is the pivot (strict for the later, larger indices)
-                csync<CTHREADS>();
-                uint32_t tk, ti;
-                block_select_k<CTHREADS>(ckey, cidx, s_count, r_pivot, kkey, kidx, hist, &sc, false, tk, ti);
-                for (int q = tid; q < r_pivot; q += CTHREADS) {
-                    ckey[q] = kkey[q];
-                    cidx[q] = kidx[q];
-                }
-                if (tid == 0) s_count = r_pivot;
-                T = tk;
-                fast = T <= 0xFF800000u;
-                tf = ukey_to_float(T);
-                csync<CTHREADS>();
-                continue;
             }
             if (named_bar_or(1, CTHREADS, over)) {
                 uint32_t tk, ti;
