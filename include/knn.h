@@ -137,6 +137,23 @@ knn_status knn_distances(knn_ctx_t ctx, const float* Q, int64_t M, const float* 
  * ldD >= N.  Exact: bit-identical to sorting the row. */
 knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64_t ldD,
                       int32_t k, int32_t* out_idx, float* out_dist, void* stream);
+/* Which kernel the last knn_select-style launch of this process used (diagnostic):
+ * *kind = 0 warp per row (k <= 128, many rows), 1 CTA per row (persistent ring), 2 CTA per
+ * row on unaligned rows, 3 a thread-block cluster per row (few rows: one
+ * block per query cannot fill the GPU below ~#SM rows; NEXT-3), with *splits = the
+ * cluster size (row segments merged over distributed shared memory), else 1. */
+knn_status knn_last_select_kernel(int32_t* kind, int32_t* splits);
+
+/* ABLATION, not the product path: the paper's quick multi-select as written
+ * (PAPER.md:49-56): one warp per row, repeated ballot/popc partitions around a pivot into
+ * two global auxiliary arrays with two coalesced writes per 32 elements, recursion into
+ * the side holding the K-th element with a stack of references to the kept left sides,
+ * direct sort below 1024 elements.  Same contract and results as knn_select (pairs are
+ * (value, index) under the total order, so it is exact); used by scripts/select_sweep.py to
+ * measure the paper's algorithm on B200.  Workspace: 16 bytes per element of a row block
+ * (ctx-owned, rows processed in blocks of at most 4 GiB). */
+knn_status knn_select_paper(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64_t ldD,
+                            int32_t k, int32_t* out_idx, float* out_dist, void* stream);
 
 /* k-way merge of partial lists ("Batch execution will obviously require
  * merging of results"): part_dist / part_idx are G blocks laid out [G][M][k]; list g's

@@ -637,6 +637,36 @@ knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64
     return KNN_OK;
 }
 
+knn_status knn_last_select_kernel(int32_t* kind, int32_t* splits) {
+    if (!kind || !splits) return KNN_ERR_ARG;
+    *kind = knn::g_last_select_kind;
+    *splits = knn::g_last_select_splits;
+    return KNN_OK;
+}
+
+knn_status knn_select_paper(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64_t ldD,
+                            int32_t k, int32_t* out_idx, float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (M < 0 || N < 1 || ldD < N) return fail(ctx, KNN_ERR_ARG, "bad sizes");
+    if (N > INT32_MAX || M > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M and N must be < 2^31");
+    if (k < 1 || k > N) return fail(ctx, KNN_ERR_ARG, "k=%d outside [1, N]", k);
+    if (k > KNN_MAX_K) return fail(ctx, KNN_ERR_UNSUPPORTED, "k=%d > %d", k, KNN_MAX_K);
+    if (M > 0 && (!D || !out_idx || !out_dist)) return fail(ctx, KNN_ERR_ARG, "null pointer");
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    // aux arrays for a block of rows, at most 4 GiB (at least one row)
+    int64_t rows = (int64_t)(((size_t)4 << 30) / knn::select_paper_ws_bytes(1, N));
+    if (rows < 1) rows = 1;
+    if (rows > M) rows = M;
+    const size_t bytes = knn::select_paper_ws_bytes(rows, N);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, bytes + 256));
+    Timed t(ctx, KNN_KERNEL_SELECT, static_cast<cudaStream_t>(stream));
+    KNN_CUDA(knn::launch_select_paper(D, M, N, ldD, k, ctx->ws, bytes, out_idx, out_dist,
+                                      static_cast<cudaStream_t>(stream)));
+    t.done();
+    return KNN_OK;
+}
+
 knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_idx, int32_t G,
                      int64_t M, int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                      float* out_dist, void* stream) {

@@ -92,6 +92,13 @@ cudaError_t launch_knn_fused(const TcOperands& op, int32_t metric, int64_t self_
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
                           int64_t idx_offset, int32_t* out_idx, float* out_dist, int32_t* redo,
                           cudaStream_t s);
+// select_paper.cu: the paper's quick multi-select (ablation); ws of ws_bytes for the aux arrays.
+size_t select_paper_ws_bytes(int64_t rows, int64_t N);
+cudaError_t launch_select_paper(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
+                                void* ws, size_t ws_bytes, int32_t* out_idx, float* out_dist,
+                                cudaStream_t s);
+// The kernel of the last launch_select (knn_last_select_kernel).
+extern int g_last_select_kind, g_last_select_splits;
 cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
                          int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                          float* out_dist, cudaStream_t s);

@@ -29,6 +29,8 @@
 #include "warpsel.cuh"
 
 #include <climits>
+#include <cstdlib>
+#include <cooperative_groups.h>
 #include <cmath>
 
 #define KNN_CUDA_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
@@ -236,9 +238,8 @@ __device__ void block_bitonic(uint32_t* key, uint32_t* idx, int KP) {
 // strides < 32E with __shfl_xor across lanes, larger (cross-warp) strides through shared
 // memory `tmp` (KP u64).  The first k positions are written to out_idx (idx + idx_offset)
 // and out_dist (the key's float).
-template <int THREADS, int KP>
-__device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k, uint64_t* tmp,
-                                 int64_t idx_offset, int32_t* out_idx, float* out_dist) {
+template <int THREADS, int KP, class Out>
+__device__ void block_sort(const uint32_t* key, const uint32_t* idx, uint64_t* tmp, Out out) {
     constexpr int E = KP >= 4 * THREADS ? 4 : KP >= 2 * THREADS ? 2 : 1;
     static_assert(KP <= E * THREADS, "KP too large for the block");
     const int t = threadIdx.x;
@@ -291,13 +292,22 @@ __device__ void block_sort_write(const uint32_t* key, const uint32_t* idx, int k
     }
     if (act) {
         #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int p = t * E + e;
-            if (p < k) {
-                out_idx[p] = (int32_t)((int64_t)(uint32_t)v[e] + idx_offset);
-                out_dist[p] = ukey_to_float((uint32_t)(v[e] >> 32));
-            }
-        }
+        for (int e = 0; e < E; ++e) out(t * E + e, v[e]);
+    }
+}
+
+// block_sort of KP (a power of two <= 4 THREADS) pairs; out(p, key << 32 | idx) per position.
+template <int THREADS, class Out>
+__device__ __forceinline__ void block_sort_kp(const uint32_t* key, const uint32_t* idx, int KP,
+                                              uint64_t* tmp, Out out) {
+    switch (KP) {
+#define KNN_SORT_CASE(P) \
+    case P: block_sort<THREADS, P>(key, idx, tmp, out); break;
+        KNN_SORT_CASE(1) KNN_SORT_CASE(2) KNN_SORT_CASE(4) KNN_SORT_CASE(8) KNN_SORT_CASE(16)
+        KNN_SORT_CASE(32) KNN_SORT_CASE(64) KNN_SORT_CASE(128) KNN_SORT_CASE(256)
+        KNN_SORT_CASE(512) KNN_SORT_CASE(1024)
+#undef KNN_SORT_CASE
+        default: break;
     }
 }
 
@@ -324,15 +334,12 @@ __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int
     // ckey, cidx, kkey, kidx are contiguous (2 cap + 2 KP words, 8-byte aligned) and dead
     // once the sort holds its pairs in registers: KP u64 of scratch
     uint64_t* tmp = reinterpret_cast<uint64_t*>(ckey);
-    switch (KP) {
-#define KNN_SORT_CASE(P) \
-    case P: block_sort_write<THREADS, P>(kkey, kidx, k, tmp, idx_offset, out_idx, out_dist); break;
-        KNN_SORT_CASE(1) KNN_SORT_CASE(2) KNN_SORT_CASE(4) KNN_SORT_CASE(8) KNN_SORT_CASE(16)
-        KNN_SORT_CASE(32) KNN_SORT_CASE(64) KNN_SORT_CASE(128) KNN_SORT_CASE(256)
-        KNN_SORT_CASE(512) KNN_SORT_CASE(1024)
-#undef KNN_SORT_CASE
-        default: break;
-    }
+    block_sort_kp<THREADS>(kkey, kidx, KP, tmp, [&](int p, uint64_t v) {
+        if (p < k) {
+            out_idx[p] = (int32_t)((int64_t)(uint32_t)v + idx_offset);
+            out_dist[p] = ukey_to_float((uint32_t)(v >> 32));
+        }
+    });
 }
 
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
@@ -662,153 +669,186 @@ __device__ __forceinline__ bool ring_append(const float4 (&cur)[VPT], const floa
 // e.g. a sorted row) is appended to redo[1..] (count redo[0]) and selected again by a
 // second launch without the pivot; a buffer overflow instead rebuilds to the exact k
 // best, after which the usual running-threshold invariant holds.
+// Shared-memory state of one ring-select CTA.
+struct RingSmem {
+    float* ring;
+    uint32_t full0, empty0;  // mbarrier arrays (shared addresses)
+    uint32_t *ckey, *cidx, *kkey, *kidx, *hist;
+    Scal* sc;
+    int* s_count;
+};
+
+template <int CTHREADS, int CHUNK, int STAGES>
+__device__ __forceinline__ RingSmem ring_smem(uint8_t* smem_raw, int cap, int KP, Scal* sc, int* s_count) {
+    RingSmem r;
+    r.ring = reinterpret_cast<float*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(r.ring + (size_t)STAGES * CHUNK);  // full, empty
+    r.full0 = smem_u32(bars);
+    r.empty0 = smem_u32(bars + STAGES);
+    r.ckey = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
+    r.cidx = r.ckey + cap;
+    r.kkey = r.cidx + cap;
+    r.kidx = r.kkey + KP;
+    r.hist = r.kidx + KP;
+    r.sc = sc;
+    r.s_count = s_count;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < STAGES; ++q) {
+            mbar_init(r.full0 + 8 * q, 1);
+            mbar_init(r.empty0 + 8 * q, CTHREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    return r;
+}
+
+// Producer (one thread): stream the N-element row rp through the ring.
+template <int CHUNK, int STAGES>
+__device__ __forceinline__ void ring_produce_row(const RingSmem& r, const float* rp, int64_t N,
+                                                 uint64_t pol, int& stage, uint32_t& phase) {
+    const int64_t nchunk = ceil_div(N, CHUNK);
+    for (int64_t c = 0; c < nchunk; ++c) {
+        mbar_wait(r.empty0 + 8 * stage, phase ^ 1);
+        const int64_t elems = (N - c * CHUNK) < CHUNK ? (N - c * CHUNK) : CHUNK;
+        const uint32_t bytes = (uint32_t)round_up(elems * 4, 16);
+        mbar_expect_tx(r.full0 + 8 * stage, bytes);
+        bulk_load_evict_first(smem_u32(r.ring + (size_t)stage * CHUNK), rp + c * CHUNK, bytes,
+                              r.full0 + 8 * stage, pol);
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+}
+
+// Consumers (threads 0..CTHREADS-1): filter one N-element row arriving through the ring.
+// On return the candidates are ckey/cidx[0, *s_count) (indices local to the row) and the
+// result is the true top k of the row iff the function returned false; true means the
+// sampled pivot kept fewer than k candidates (select the row again without it).
+template <int CTHREADS, int CHUNK, int STAGES>
+__device__ __forceinline__ bool ring_consume_row(const RingSmem& r, int64_t N, int k, int limit,
+                                                 bool piv, int r_pivot, int& stage, uint32_t& phase) {
+    constexpr int VPT = CHUNK / CTHREADS / 4;  // float4 per consumer thread per slice
+    static_assert(VPT * 4 * CTHREADS == CHUNK, "CHUNK must be a multiple of 4*CTHREADS");
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    Scal& sc = *r.sc;
+    if (tid == 0) {
+        *r.s_count = 0;
+        sc.lo = 0xFFFFFFFFu;
+        sc.hi = 0;
+    }
+    if (piv)
+        for (int q = tid; q < 256; q += CTHREADS) r.hist[q] = 0;
+    uint32_t T = kKeyMax;
+    float tf = 0.0f;
+    bool fast = false;
+    csync<CTHREADS>();
+    const int64_t nchunk = ceil_div(N, CHUNK);
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t base = c * CHUNK;
+        mbar_wait(r.full0 + 8 * stage, phase);
+        const float4* buf = reinterpret_cast<const float4*>(r.ring + (size_t)stage * CHUNK);
+        float4 cur[VPT];
+        #pragma unroll
+        for (int j = 0; j < VPT; ++j) cur[j] = buf[j * CTHREADS + tid];
+        const bool full = base + CHUNK <= N;
+        if (piv && c == 0) {
+            // The sample (the first chunk, still in registers): one 8-bit histogram of its
+            // keys on the digit just below the common prefix of their range; the pivot P
+            // is the upper edge of the bin holding the r_pivot-th key, so at least r_pivot
+            // sample keys are < P.  Candidates: every key < P.
+            uint32_t a = 0xFFFFFFFFu, b = 0;
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const uint32_t u0 = ukey(cur[j].x), u1 = ukey(cur[j].y), u2 = ukey(cur[j].z),
+                               u3 = ukey(cur[j].w);
+                a = min(a, min(min(u0, u1), min(u2, u3)));
+                b = max(b, max(max(u0, u1), max(u2, u3)));
+            }
+            a = __reduce_min_sync(FULL, a);
+            b = __reduce_max_sync(FULL, b);
+            if (lane == 0) {
+                atomicMin(&sc.lo, a);
+                atomicMax(&sc.hi, b);
+            }
+            csync<CTHREADS>();
+            const uint32_t mn = sc.lo, mx = sc.hi;
+            const int sh = top_digit_shift(mn, mx);
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                atomicAdd(&r.hist[(ukey(cur[j].x) >> sh) & 255u], 1u);
+                atomicAdd(&r.hist[(ukey(cur[j].y) >> sh) & 255u], 1u);
+                atomicAdd(&r.hist[(ukey(cur[j].z) >> sh) & 255u], 1u);
+                atomicAdd(&r.hist[(ukey(cur[j].w) >> sh) & 255u], 1u);
+            }
+            csync<CTHREADS>();
+            hist_find(r.hist, (uint32_t)r_pivot, &sc);
+            csync<CTHREADS>();
+            const uint64_t lowmask = (1ull << (sh + 8)) - 1ull;
+            const uint64_t P = ((uint64_t)mn & ~lowmask) + ((uint64_t)(sc.bin + 1) << sh);
+            T = P >= 0xFFFFFFFFull ? kKeyMax : (uint32_t)P;
+            fast = T <= 0xFF800000u;
+            tf = ukey_to_float(T);
+        }
+        const bool over = ring_append<CTHREADS, VPT>(cur, reinterpret_cast<const float*>(buf), T, tf,
+                                                     fast, full, N, base, r.ckey, r.cidx, r.s_count,
+                                                     limit);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(r.empty0 + 8 * stage);  // slot may be refilled
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+        if (named_bar_or(1, CTHREADS, over)) {
+            uint32_t tk, ti;
+            block_select_k<CTHREADS>(r.ckey, r.cidx, *r.s_count, k, r.kkey, r.kidx, r.hist, &sc, false,
+                                     tk, ti);
+            for (int q = tid; q < k; q += CTHREADS) {
+                r.ckey[q] = r.kkey[q];
+                r.cidx[q] = r.kidx[q];
+            }
+            if (tid == 0) *r.s_count = k;
+            T = tk;
+            fast = T <= 0xFF800000u;
+            tf = ukey_to_float(T);
+            piv = false;  // k exact best kept: the running-threshold invariant holds
+            csync<CTHREADS>();
+        }
+    }
+    csync<CTHREADS>();
+    return piv && *r.s_count < k;
+}
+
 template <int CTHREADS, int CHUNK, int STAGES>
 __global__ void __launch_bounds__(CTHREADS + 32, 2)
 select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int cap,
                    int KP, int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
                    float* __restrict__ out_dist, const int32_t* __restrict__ list, int r_pivot,
                    int32_t* __restrict__ redo) {
-    constexpr int VPT = CHUNK / CTHREADS / 4;  // float4 per consumer thread per slice
-    static_assert(VPT * 4 * CTHREADS == CHUNK, "CHUNK must be a multiple of 4*CTHREADS");
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    float* ring = reinterpret_cast<float*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)STAGES * CHUNK);  // full, empty
-    uint32_t* ckey = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
-    uint32_t* cidx = ckey + cap;
-    uint32_t* kkey = cidx + cap;
-    uint32_t* kidx = kkey + KP;
-    uint32_t* hist = kidx + KP;
     __shared__ Scal sc;
     __shared__ int s_count;
-
+    const RingSmem r = ring_smem<CTHREADS, CHUNK, STAGES>(smem_raw, cap, KP, &sc, &s_count);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
-    const int64_t nchunk = ceil_div(N, CHUNK);
     const int64_t nrows = list ? (int64_t)list[0] : M;
     const bool use_pivot = r_pivot > 0 && r_pivot < k && N >= 2 * (int64_t)CHUNK;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, CTHREADS / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     __syncthreads();
-
+    int stage = 0;
+    uint32_t phase = 0;
     if (warp == CTHREADS / 32) {
-        // -------------------------------------------------------- producer warp ------
+        // producer warp: streams the rows ahead of the consumers, across row boundaries
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int stage = 0;
-            uint32_t phase = 0;
             for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
                 const int64_t row = list ? (int64_t)list[1 + i] : i;
-                const float* rp = D + row * ldD;
-                for (int64_t c = 0; c < nchunk; ++c) {
-                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
-                    const int64_t elems = (N - c * CHUNK) < CHUNK ? (N - c * CHUNK) : CHUNK;
-                    const uint32_t bytes = (uint32_t)round_up(elems * 4, 16);
-                    mbar_expect_tx(full0 + 8 * stage, bytes);
-                    bulk_load_evict_first(smem_u32(ring + (size_t)stage * CHUNK), rp + c * CHUNK,
-                                          bytes, full0 + 8 * stage, pol);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
+                ring_produce_row<CHUNK, STAGES>(r, D + row * ldD, N, pol, stage, phase);
             }
         }
         return;
     }
-
-    // ------------------------------------------------------------ consumers ----------
-    int stage = 0;
-    uint32_t phase = 0;
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
         const int64_t row = list ? (int64_t)list[1 + i] : i;
-        if (tid == 0) {
-            s_count = 0;
-            sc.lo = 0xFFFFFFFFu;
-            sc.hi = 0;
-        }
-        if (use_pivot)
-            for (int q = tid; q < 256; q += CTHREADS) hist[q] = 0;
-        uint32_t T = kKeyMax;
-        float tf = 0.0f;
-        bool fast = false;
-        bool piv = use_pivot;  // the sampled pivot still decides the candidate set
-        csync<CTHREADS>();
-        for (int64_t c = 0; c < nchunk; ++c) {
-            const int64_t base = c * CHUNK;
-            mbar_wait(full0 + 8 * stage, phase);
-            const float4* buf = reinterpret_cast<const float4*>(ring + (size_t)stage * CHUNK);
-            float4 cur[VPT];
-            #pragma unroll
-            for (int j = 0; j < VPT; ++j) cur[j] = buf[j * CTHREADS + tid];
-            const bool full = base + CHUNK <= N;
-            if (piv && c == 0) {
-                // The sample (the first chunk, still in registers): one 8-bit histogram
-                // of its keys on the digit just below the common prefix of their range;
-                // the pivot P is the upper edge of the bin holding the r_pivot-th key, so
-                // at least r_pivot sample keys are < P.  Candidates: every key < P.
-                uint32_t a = 0xFFFFFFFFu, b = 0;
-                #pragma unroll
-                for (int j = 0; j < VPT; ++j) {
-                    const uint32_t u0 = ukey(cur[j].x), u1 = ukey(cur[j].y), u2 = ukey(cur[j].z),
-                                   u3 = ukey(cur[j].w);
-                    a = min(a, min(min(u0, u1), min(u2, u3)));
-                    b = max(b, max(max(u0, u1), max(u2, u3)));
-                }
-                a = __reduce_min_sync(FULL, a);
-                b = __reduce_max_sync(FULL, b);
-                if (lane == 0) {
-                    atomicMin(&sc.lo, a);
-                    atomicMax(&sc.hi, b);
-                }
-                csync<CTHREADS>();
-                const uint32_t mn = sc.lo, mx = sc.hi;
-                const int sh = top_digit_shift(mn, mx);
-                #pragma unroll
-                for (int j = 0; j < VPT; ++j) {
-                    atomicAdd(&hist[(ukey(cur[j].x) >> sh) & 255u], 1u);
-                    atomicAdd(&hist[(ukey(cur[j].y) >> sh) & 255u], 1u);
-                    atomicAdd(&hist[(ukey(cur[j].z) >> sh) & 255u], 1u);
-                    atomicAdd(&hist[(ukey(cur[j].w) >> sh) & 255u], 1u);
-                }
-                csync<CTHREADS>();
-                hist_find(hist, (uint32_t)r_pivot, &sc);
-                csync<CTHREADS>();
-                const uint64_t lowmask = (1ull << (sh + 8)) - 1ull;
-                const uint64_t P = ((uint64_t)mn & ~lowmask) + ((uint64_t)(sc.bin + 1) << sh);
-                T = P >= 0xFFFFFFFFull ? kKeyMax : (uint32_t)P;
-                fast = T <= 0xFF800000u;
-                tf = ukey_to_float(T);
-            }
-            const bool over = ring_append<CTHREADS, VPT>(cur, reinterpret_cast<const float*>(buf), T, tf,
-                                                         fast, full, N, base, ckey, cidx, &s_count, limit);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * stage);  // slot may be refilled
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-            }
-            if (named_bar_or(1, CTHREADS, over)) {
-                uint32_t tk, ti;
-                block_select_k<CTHREADS>(ckey, cidx, s_count, k, kkey, kidx, hist, &sc, false, tk, ti);
-                for (int q = tid; q < k; q += CTHREADS) {
-                    ckey[q] = kkey[q];
-                    cidx[q] = kidx[q];
-                }
-                if (tid == 0) s_count = k;
-                T = tk;
-                fast = T <= 0xFF800000u;
-                tf = ukey_to_float(T);
-                piv = false;  // k exact best kept: the running-threshold invariant holds
-                csync<CTHREADS>();
-            }
-        }
-        csync<CTHREADS>();
-        if (piv && s_count < k) {
+        if (ring_consume_row<CTHREADS, CHUNK, STAGES>(r, N, k, limit, use_pivot, r_pivot, stage, phase)) {
             // fewer than k elements beat the sampled pivot: select this row again later
             if (tid == 0) {
                 const int slot = atomicAdd(redo, 1);
@@ -817,9 +857,111 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             csync<CTHREADS>();
             continue;
         }
-        block_finish<CTHREADS>(ckey, cidx, s_count, k, KP, kkey, kidx, hist, &sc, idx_offset,
+        block_finish<CTHREADS>(r.ckey, r.cidx, s_count, k, KP, r.kkey, r.kidx, r.hist, &sc, idx_offset,
                                out_idx + row * k, out_dist + row * k);
         csync<CTHREADS>();
+    }
+}
+
+// ------------------------------------------------------------------ cluster select ---
+// Few-row regime (NEXT-3; one block per query needs >= 128 queries to fill
+// the GPU): a thread-block cluster of S CTAs per row.  CTA s of the cluster runs the ring
+// select above on columns [s L, (s+1) L) (its own sampled pivot; a failed certificate
+// re-streams the segment without it, the producer waiting on the consumers' decision) and
+// leaves its sorted top-k as packed (key << 32 | column) in shared memory.  The S lists are
+// then merged in log2 S rounds over distributed shared memory: in round l, CTA s (s a
+// multiple of 2l) copies CTA s+l's list out of DSMEM and merges it with its own (each
+// element's output slot = its rank in its own list + its rank in the other, a merge path
+// without ties because the columns differ); CTA 0 writes the row.
+template <int CTHREADS, int CHUNK, int STAGES>
+__global__ void __launch_bounds__(CTHREADS + 32, 1)
+select_cluster_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k, int cap, int KP,
+                      int limit, int64_t L, int64_t idx_offset, int32_t* __restrict__ out_idx,
+                      float* __restrict__ out_dist, int r_pivot) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ Scal sc;
+    __shared__ int s_count;
+    __shared__ int s_redo;
+    const RingSmem r = ring_smem<CTHREADS, CHUNK, STAGES>(smem_raw, cap, KP, &sc, &s_count);
+    uint64_t* lst = reinterpret_cast<uint64_t*>(r.hist + 256);  // KP, 8-byte aligned
+    uint64_t* bbuf = lst + KP;
+    uint64_t* obuf = bbuf + KP;
+    const int S = (int)cluster.num_blocks();
+    const int seg = (int)cluster.block_rank();
+    const int64_t row = blockIdx.x / S;
+    const int64_t c0 = (int64_t)seg * L;
+    const int64_t Ns = N - c0 < L ? N - c0 : L;  // may be <= 0 for trailing segments
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const bool use_pivot = r_pivot > 0 && r_pivot < k && Ns >= 2 * (int64_t)CHUNK;
+    __syncthreads();
+    int stage = 0;
+    uint32_t phase = 0;
+    if (warp == CTHREADS / 32) {
+        const uint64_t pol = policy_evict_first();
+        if (lane == 0 && Ns > 0) ring_produce_row<CHUNK, STAGES>(r, D + row * ldD + c0, Ns, pol, stage, phase);
+        __syncwarp();
+        named_bar(2, CTHREADS + 32);  // the consumers' verdict on the sampled pivot
+        if (lane == 0 && s_redo) ring_produce_row<CHUNK, STAGES>(r, D + row * ldD + c0, Ns, pol, stage, phase);
+        __syncwarp();
+    } else {
+        bool redo = false;
+        if (Ns > 0) redo = ring_consume_row<CTHREADS, CHUNK, STAGES>(r, Ns, k, limit, use_pivot, r_pivot, stage, phase);
+        if (tid == 0) s_redo = redo;
+        named_bar(2, CTHREADS + 32);
+        if (redo) ring_consume_row<CTHREADS, CHUNK, STAGES>(r, Ns, k, limit, false, 0, stage, phase);
+        const int cnt = Ns > 0 ? s_count : 0;
+        // exact min(k, cnt) best, sorted, as packed pairs with the row's column index
+        if (cnt > k) {
+            uint32_t tk, ti;
+            block_select_k<CTHREADS>(r.ckey, r.cidx, cnt, k, r.kkey, r.kidx, r.hist, &sc, false, tk, ti);
+        } else {
+            for (int q = tid; q < cnt; q += CTHREADS) {
+                r.kkey[q] = r.ckey[q];
+                r.kidx[q] = r.cidx[q];
+            }
+        }
+        for (int q = (cnt < k ? cnt : k) + tid; q < KP; q += CTHREADS) {
+            r.kkey[q] = 0xFFFFFFFFu;
+            r.kidx[q] = 0xFFFFFFFFu;
+        }
+        csync<CTHREADS>();
+        block_sort_kp<CTHREADS>(r.kkey, r.kidx, KP, reinterpret_cast<uint64_t*>(r.ckey),
+                                [&](int q, uint64_t v) { lst[q] = v == ~0ull ? v : v + (uint64_t)c0; });
+    }
+    cluster.sync();
+    for (int l = 1; l < S; l <<= 1) {
+        if (seg % (2 * l) == 0) {
+            const uint64_t* remote = cluster.map_shared_rank(lst, seg + l);
+            for (int q = tid; q < KP; q += blockDim.x) bbuf[q] = remote[q];
+            __syncthreads();
+            for (int q = tid; q < KP; q += blockDim.x) {
+                const uint64_t a = lst[q], b = bbuf[q];
+                int lo = 0, hi = KP;  // #b' < a in bbuf
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (bbuf[mid] < a) lo = mid + 1; else hi = mid;
+                }
+                if (q + lo < KP) obuf[q + lo] = a;
+                int lo2 = 0, hi2 = KP;  // #a' <= b in lst
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (lst[mid] <= b) lo2 = mid + 1; else hi2 = mid;
+                }
+                if (q + lo2 < KP) obuf[q + lo2] = b;
+            }
+            __syncthreads();
+            for (int q = tid; q < KP; q += blockDim.x) lst[q] = obuf[q];
+        }
+        cluster.sync();  // lists of this round final before the next round reads them
+    }
+    if (seg == 0) {
+        for (int q = tid; q < k; q += blockDim.x) {
+            const uint64_t v = lst[q];
+            out_idx[row * k + q] = (int32_t)((int64_t)(uint32_t)v + idx_offset);
+            out_dist[row * k + q] = ukey_to_float((uint32_t)(v >> 32));
+        }
     }
 }
 
@@ -1356,12 +1498,19 @@ int next_pow2(int x) {
     return p;
 }
 
+bool getenv_flag(const char* name) {
+    const char* v = getenv(name);
+    return v && v[0] && v[0] != '0';
+}
+
 template <class K>
 cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 }  // namespace
+
+int g_last_select_kind = -1, g_last_select_splits = 1;
 
 cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int32_t k,
                           int64_t idx_offset, int32_t* out_idx, float* out_dist, int32_t* redo,
@@ -1393,9 +1542,61 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
                                                                out_idx, out_dist);
             return cudaGetLastError();
         };
+        g_last_select_kind = 0;
+        g_last_select_splits = 1;
         if (k <= 32) return pick(select_warp_kernel<1>);
         if (k <= 64) return pick(select_warp_kernel<2>);
         return pick(select_warp_kernel<4>);
+    }
+    if (aligned && M < sms && N >= 2 * 4096 && !getenv_flag("KNN_NO_CLUSTER_SELECT")) {
+        // few rows: a cluster of S CTAs per row (select_cluster_kernel)
+        constexpr int CT = 256, CHUNK = 4096, STAGES = 4;
+        int S = 1;
+        while (S < 16 && (int64_t)S * M < sms && (int64_t)(2 * S) * CHUNK <= N) S <<= 1;
+        if (S > 1) {
+            const int64_t L = round_up(ceil_div(N, S), CHUNK);
+            int cap, limit;
+            if (L <= CHUNK) {
+                cap = (int)round_up(L, 32);
+                limit = INT_MAX;
+            } else {
+                limit = (int)round_up(k + 256 > 2 * k ? k + 256 : 2 * k, 32);
+                cap = CHUNK + limit;
+            }
+            int r_pivot = 0;
+            if (L >= 2 * CHUNK) {
+                const double mean = (double)CHUNK * k / (double)L;
+                const double r = std::ceil(mean + 4.0 * std::sqrt(mean) + 2.0);
+                if (r < 0.75 * k) r_pivot = (int)r;
+            }
+            const size_t smem = (size_t)STAGES * CHUNK * 4 + 2 * STAGES * 8 +
+                                (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t) + 3 * (size_t)KP * 8;
+            auto kern = select_cluster_kernel<CT, CHUNK, STAGES>;
+            if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
+            if (S > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+                return e;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(M * S), 1, 1);
+            cfg.blockDim = dim3(CT + 32, 1, 1);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = S;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg) == cudaSuccess && nclusters > 0) {
+                g_last_select_kind = 3;
+                g_last_select_splits = S;
+                e = cudaLaunchKernelEx(&cfg, kern, D, N, ldD, k, cap, KP, limit, L, idx_offset, out_idx,
+                                       out_dist, r_pivot);
+                return e != cudaSuccess ? e : cudaGetLastError();
+            }
+            cudaGetLastError();  // cluster shape not schedulable: fall through to one CTA per row
+        }
     }
     if (aligned) {
         constexpr int CT = 256, CHUNK = 4096;
@@ -1430,6 +1631,8 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
                                                       out_idx, out_dist, list, rp, redo);
             return cudaGetLastError();
         };
+        g_last_select_kind = 1;
+        g_last_select_splits = 1;
         // 4 ring stages when two CTAs still fit on an SM, else 3
         const size_t base_smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
         const bool four = base_smem + 4 * (size_t)CHUNK * 4 + 64 <= 112 * 1024;
@@ -1455,6 +1658,8 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
     }
     const size_t smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
     auto kern = select_rows_kernel<THREADS, VPT, false>;
+    g_last_select_kind = 2;
+    g_last_select_splits = 1;
     if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
     kern<<<(unsigned)M, THREADS, smem, s>>>(D, N, ldD, k, cap, KP, limit, idx_offset, out_idx,
                                            out_dist);

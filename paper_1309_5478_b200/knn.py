@@ -28,7 +28,7 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
            "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
-           "knn_profile_read"]
+           "knn_profile_read", "knn_last_select_kernel", "knn_select_paper"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
@@ -74,6 +74,8 @@ def load_library():
             "knn_rownorms": (st, [p, p, i64, i32, p, p, p]),
             "knn_distances": (st, [p, p, i64, p, i64, i32, i32, i64, p, i64, p]),
             "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
+            "knn_select_paper": (st, [p, p, i64, i64, i64, i32, p, p, p]),
+            "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
             "knn_fused_plan": (ctypes.c_int, [p, i32]),
@@ -240,6 +242,36 @@ def select(D, k, N=None, stream=None):
                                    _stream(stream))
     _check(rc, ctx)
     return idx, dist
+
+
+def select_paper(D, k, N=None, stream=None):
+    """ABLATION: the paper's quick multi-select as written (knn_select_paper); same
+    contract and results as select()."""
+    import torch
+    M, ld = D.shape
+    N = ld if N is None else N
+    if not D.is_contiguous():
+        raise ValueError("D must be contiguous (use the N argument for a column prefix)")
+    ctx = context(D.device.index)
+    idx, dist = _outputs(M, k, D.device)
+    rc = load_library().knn_select_paper(ctx, _dev_ptr(D, torch.float32, "D"), M, N, ld, k,
+                                         ctypes.c_void_p(idx.data_ptr()),
+                                         ctypes.c_void_p(dist.data_ptr()), _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+SELECT_KERNELS = {0: "warp per row", 1: "CTA per row (ring)", 2: "CTA per row (unaligned)",
+                  3: "cluster per row"}
+
+
+def last_select_kernel():
+    """(kind name, splits) of the last select launch in this process."""
+    kind, splits = ctypes.c_int32(), ctypes.c_int32()
+    rc = load_library().knn_last_select_kernel(ctypes.byref(kind), ctypes.byref(splits))
+    if rc != 0:
+        raise KnnError(rc, "knn_last_select_kernel")
+    return SELECT_KERNELS.get(kind.value, str(kind.value)), splits.value
 
 
 def merge(part_dist, part_idx, offsets, stream=None):

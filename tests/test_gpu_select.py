@@ -201,3 +201,42 @@ def test_select_sampled_pivot_few_finite():
     D[2, ::40] = np.nan
     D[3, 9000:9600] = -np.arange(600, dtype=np.float32)
     assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("M", [1, 3, 17, 100])
+@pytest.mark.parametrize("N,k", [(8192, 1), (20000, 32), (65536, 100), (65536, 1024),
+                                  (1 << 20, 64), (1 << 20, 1024), (300001, 333)])
+def test_select_few_rows_cluster(M, N, k):
+    """Few rows (M < #SMs): a thread-block cluster per row, segments merged over DSMEM
+    (NEXT-3).  Adversarial rows exercise the in-kernel re-stream (ascending:
+    the segment pivots are too low) and the overflow rebuild (descending)."""
+    if M * N > 60_000_000:
+        N = 60_000_000 // M // 4 * 4
+    D = datagen.keys(M, N, "uniform", seed=M * 1000 + k)
+    if M >= 3:
+        D[1] = np.arange(N, dtype=np.float32)
+        D[2] = np.arange(N, 0, -1, dtype=np.float32)
+    if M >= 17:
+        D[5] = np.float32(0.5)
+        D[6, ::3] = np.inf
+        D[7, 1::5] = np.nan
+        D[8, N // 2:] = -1.0
+    assert_same(gpu_select(D, k), oracle.select_f32(D, k))
+
+
+def test_cluster_path_is_taken():
+    D = datagen.keys(4, 1 << 18, "uniform", seed=77)
+    assert_same(gpu_select(D, 64), oracle.select_f32(D, 64))
+    kind, splits = knn().last_select_kernel()
+    assert kind == "cluster per row" and splits >= 8
+
+
+@pytest.mark.parametrize("N,k", [(1000, 8), (5000, 1024), (70000, 64), (65536, 512)])
+@pytest.mark.parametrize("kind", ["uniform", "dup256", "descending", "equal"])
+def test_select_paper_ablation(N, k, kind):
+    """The paper's quick multi-select (ablation kernel) is exact too."""
+    D = datagen.keys(40, N, kind, seed=N + k)
+    ref = oracle.select_f32(D, k)
+    Dt = torch.from_numpy(D).cuda()
+    got = [t.cpu().numpy() for t in knn().select_paper(Dt, k)]
+    assert_same(got, ref)
