@@ -114,6 +114,26 @@ knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
  * Stream-ordered (asynchronous): they validate arguments, enqueue kernels on `stream`
  * and return.  Used by the tests and the benchmark. */
 
+/* Out-of-core k-NN (NEXT-4; "batch execution with data partitioning for
+ * large corpus data that do not fit into GPU memory ... overlap computation with data
+ * transfer ... merging of results between executions").  Q_host (M×d) and X_host (N×d)
+ * stay in HOST memory (pageable or pinned; pageable ranges are page-locked with
+ * cudaHostRegister for the duration of the call); the device holds one block of at
+ * most query_block queries and two staging buffers of corpus chunks of chunk_points
+ * points.  Chunk c+1 is copied host->device on a separate stream while chunk c is
+ * processed (prep, GEMM, select with global indices), and each chunk's partial top-k is
+ * merged into the running result with the a-S6 merge.  graph != 0: the k-NNG of X
+ * (requires Q_host == X_host, M == N; self excluded by position, k <= N-1).  Results
+ * (M×k, host) are bit-identical to knn_search / knn_graph on device-resident inputs:
+ * per-pair values do not depend on the chunking and the merge is exact under the total
+ * order.  chunk_points, query_block <= 0 pick defaults (131072 points; all queries up
+ * to a 2 GiB block).  A trailing chunk with fewer than k+1 points is folded into the
+ * previous one.  Blocking. */
+knn_status knn_search_streamed(knn_ctx_t ctx, const float* Q_host, int64_t M, const float* X_host,
+                               int64_t N, int32_t d, int32_t k, int32_t metric, int32_t graph,
+                               int64_t chunk_points, int64_t query_block, int32_t* out_idx_host,
+                               float* out_dist_host);
+
 /* ||x_j||^2 = sum_t x_j[t]^2 for j < N, accumulated in fp64, rounded to fp32
  * (norms by reduction; reading R15).  out_sqn: N floats.
  * Also writes *out_flag (device int32, may be NULL) = 1 when some x is non-finite or

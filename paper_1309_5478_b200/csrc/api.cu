@@ -43,6 +43,12 @@ struct knn_ctx {
     size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
     double prof_ms[5] = {0, 0, 0, 0, 0};
     int64_t prof_n[5] = {0, 0, 0, 0, 0};
+    // out-of-core streaming (knn_search_streamed): staging + running lists, copy stream
+    void* st_buf = nullptr;
+    size_t st_size = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    double last_stream_copy_ms = 0, last_stream_total_ms = 0;
 };
 
 namespace {
@@ -419,6 +425,12 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->io) cudaFree(ctx->io);
+    if (ctx->st_buf) cudaFree(ctx->st_buf);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
+        if (ctx->ev_free[b]) cudaEventDestroy(ctx->ev_free[b]);
+    }
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
     delete ctx;
     return KNN_OK;
@@ -548,6 +560,146 @@ knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
     KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)M * k * sizeof(float),
                              cudaMemcpyDeviceToHost, s));
     return finish_blocking(ctx, s);
+}
+
+namespace {
+// Page-locks a host range for the duration of a call unless it is already pinned.
+struct HostPin {
+    void* p = nullptr;
+    bool mine = false;
+    void pin(const void* ptr, size_t bytes) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost) return;
+        cudaGetLastError();
+        const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault);
+        if (e == cudaSuccess) {
+            p = const_cast<void*>(ptr);
+            mine = true;
+        } else {
+            cudaGetLastError();  // stays pageable: copies are correct, just not overlapped
+        }
+    }
+    ~HostPin() {
+        if (mine) cudaHostUnregister(p);
+    }
+};
+}  // namespace
+
+knn_status knn_search_streamed(knn_ctx_t ctx, const float* Q_host, int64_t M, const float* X_host,
+                               int64_t N, int32_t d, int32_t k, int32_t metric, int32_t graph,
+                               int64_t chunk_points, int64_t query_block, int32_t* out_idx_host,
+                               float* out_dist_host) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (graph && (Q_host != X_host || M != N))
+        return fail(ctx, KNN_ERR_ARG, "graph mode needs Q_host == X_host and M == N");
+    const int64_t kmin = graph ? (int64_t)k + 1 : (int64_t)k;
+    if (N < kmin) return fail(ctx, KNN_ERR_ARG, "k=%d too large for N=%lld", k, (long long)N);
+    KNN_TRY(check_block_args(ctx, Q_host, M, X_host, N, d, k, metric, graph ? 0 : KNN_NO_SELF, 0,
+                             out_idx_host, out_dist_host));
+    if (M == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    cudaEvent_t t0 = take_event(ctx), t1 = take_event(ctx);
+    int64_t C = chunk_points > 0 ? chunk_points : 131072;
+    if (C < kmin) C = kmin;
+    if (C > N) C = N;
+    const int64_t Cmax = C + kmin;  // a trailing chunk shorter than kmin joins its predecessor
+    int64_t QB = query_block > 0 ? query_block : M;
+    const int64_t qb_cap = (int64_t)(((size_t)2 << 30) / ((size_t)d * sizeof(float)));
+    if (QB > qb_cap) QB = qb_cap;
+    if (QB > M) QB = M;
+    // device layout: staging x2 | query block | lists [2][QB][k] (running, chunk) | merged
+    auto layout = [&](Carve& c, float** xs, float*& q, int32_t*& li, float*& ld, int32_t*& mi, float*& md) {
+        xs[0] = c.take<float>((size_t)Cmax * d);
+        xs[1] = c.take<float>((size_t)Cmax * d);
+        q = c.take<float>((size_t)QB * d);
+        li = c.take<int32_t>((size_t)2 * QB * k);
+        ld = c.take<float>((size_t)2 * QB * k);
+        mi = c.take<int32_t>((size_t)QB * k);
+        md = c.take<float>((size_t)QB * k);
+    };
+    float* xs[2];
+    float *q, *ld, *md;
+    int32_t *li, *mi;
+    Carve probe{nullptr};
+    layout(probe, xs, q, li, ld, mi, md);
+    KNN_TRY(ensure(ctx, &ctx->st_buf, &ctx->st_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->st_buf)};
+    layout(carve, xs, q, li, ld, mi, md);
+    if (!ctx->copy_stream) {
+        KNN_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            KNN_CUDA(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+            KNN_CUDA(cudaEventCreateWithFlags(&ctx->ev_free[b], cudaEventDisableTiming));
+        }
+    }
+    HostPin pin_x, pin_q;
+    pin_x.pin(X_host, (size_t)N * d * sizeof(float));
+    if (!graph) pin_q.pin(Q_host, (size_t)M * d * sizeof(float));
+    cudaStream_t s = nullptr;
+    KNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{s};
+    cudaStream_t cs = ctx->copy_stream;
+    // chunk boundaries
+    std::vector<int64_t> cb;
+    for (int64_t c0 = 0; c0 < N; c0 += C) cb.push_back(c0);
+    if (cb.size() > 1 && N - cb.back() < kmin) cb.pop_back();
+    cb.push_back(N);
+    const int nch = (int)cb.size() - 1;
+    const int64_t offsets[2] = {0, 0};
+    KNN_CUDA(cudaEventRecord(t0, s));
+    for (int b = 0; b < 2; ++b) KNN_CUDA(cudaEventRecord(ctx->ev_free[b], s));
+    for (int64_t q0 = 0; q0 < M; q0 += QB) {
+        const int64_t R = M - q0 < QB ? M - q0 : QB;
+        KNN_CUDA(cudaMemcpyAsync(q, Q_host + q0 * d, (size_t)R * d * sizeof(float), cudaMemcpyHostToDevice, s));
+        auto issue_copy = [&](int c) -> knn_status {
+            const int b = c & 1;
+            KNN_CUDA(cudaStreamWaitEvent(cs, ctx->ev_free[b], 0));
+            KNN_CUDA(cudaMemcpyAsync(xs[b], X_host + cb[c] * d, (size_t)(cb[c + 1] - cb[c]) * d * sizeof(float),
+                                     cudaMemcpyHostToDevice, cs));
+            KNN_CUDA(cudaEventRecord(ctx->ev_copied[b], cs));
+            return KNN_OK;
+        };
+        KNN_TRY(issue_copy(0));
+        for (int c = 0; c < nch; ++c) {
+            if (c + 1 < nch) KNN_TRY(issue_copy(c + 1));
+            const int b = c & 1;
+            const int64_t c0 = cb[c], Cc = cb[c + 1] - cb[c];
+            KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_copied[b], 0));
+            // chunk partial lists: list 0 (running) for the first chunk, else list 1
+            int32_t* pi = c == 0 ? li : li + (size_t)R * k;
+            float* pd = c == 0 ? ld : ld + (size_t)R * k;
+            const int64_t shift = graph ? q0 - c0 : KNN_NO_SELF;
+            KNN_TRY(run_block(ctx, q, R, xs[b], Cc, d, k, metric, shift, c0, pi, pd, s));
+            KNN_CUDA(cudaEventRecord(ctx->ev_free[b], s));
+            knn_status st0 = finish_blocking(ctx, s);
+            if (st0 == KNN_ERR_INTERNAL) {
+                ctx->pivot_redos++;
+                KNN_TRY(run_block(ctx, q, R, xs[b], Cc, d, k, metric, shift, c0, pi, pd, s, false));
+                KNN_CUDA(cudaEventRecord(ctx->ev_free[b], s));
+            } else if (st0 != KNN_OK) {
+                return st0;
+            }
+            if (c > 0) {
+                // running top-k <- merge(running, chunk) (a-S6); the lists are [2][R][k]
+                Timed tm(ctx, KNN_KERNEL_MERGE, s);
+                KNN_CUDA(knn::launch_merge(ld, li, 2, R, k, offsets, mi, md, s));
+                tm.done();
+                KNN_CUDA(cudaMemcpyAsync(li, mi, (size_t)R * k * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+                KNN_CUDA(cudaMemcpyAsync(ld, md, (size_t)R * k * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        KNN_CUDA(cudaMemcpyAsync(out_idx_host + q0 * k, li, (size_t)R * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        KNN_CUDA(cudaMemcpyAsync(out_dist_host + q0 * k, ld, (size_t)R * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    KNN_CUDA(cudaEventRecord(t1, s));
+    KNN_TRY(finish_blocking(ctx, s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    ctx->last_stream_total_ms = ms;
+    ctx->ev_pool.push_back(t0);
+    ctx->ev_pool.push_back(t1);
+    drain_profile(ctx);
+    return KNN_OK;
 }
 
 knn_status knn_rownorms(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, float* out_sqn,

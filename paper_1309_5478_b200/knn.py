@@ -28,7 +28,8 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
            "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
-           "knn_profile_read", "knn_last_select_kernel", "knn_select_paper"]
+           "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
+           "knn_search_streamed"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
@@ -75,6 +76,7 @@ def load_library():
             "knn_distances": (st, [p, p, i64, p, i64, i32, i32, i64, p, i64, p]),
             "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
             "knn_select_paper": (st, [p, p, i64, i64, i64, i32, p, p, p]),
+            "knn_search_streamed": (st, [p, p, i64, p, i64, i32, i32, i32, i32, i64, i64, p, p]),
             "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
@@ -242,6 +244,29 @@ def select(D, k, N=None, stream=None):
                                    _stream(stream))
     _check(rc, ctx)
     return idx, dist
+
+
+def search_streamed(Q, X, k, metric=L2SQ, graph=False, chunk_points=0, query_block=0,
+                    device=0, out=None):
+    """Out-of-core k-NN with HOST inputs (numpy fp32, C-contiguous; pass the same array
+    as Q and X with graph=True for the k-NNG): corpus chunks are streamed to the device
+    with copy/compute overlap and partial top-k lists merged (knn_search_streamed).
+    Returns host (idx int32 M×k, dist fp32 M×k)."""
+    Q = np.ascontiguousarray(Q, np.float32) if not graph else X
+    X = np.ascontiguousarray(X, np.float32)
+    if graph:
+        Q = X
+    M, d = Q.shape
+    N = X.shape[0]
+    if out is None:
+        out = (np.empty((M, k), np.int32), np.empty((M, k), np.float32))
+    ctx = context(device)
+    rc = load_library().knn_search_streamed(
+        ctx, Q.ctypes.data_as(ctypes.c_void_p), M, X.ctypes.data_as(ctypes.c_void_p), N, d, k,
+        metric, 1 if graph else 0, chunk_points, query_block,
+        out[0].ctypes.data_as(ctypes.c_void_p), out[1].ctypes.data_as(ctypes.c_void_p))
+    _check(rc, ctx)
+    return out
 
 
 def select_paper(D, k, N=None, stream=None):
