@@ -185,6 +185,27 @@ knn_status knn_merge(knn_ctx_t ctx, const float* part_dist, const int32_t* part_
                      int64_t M, int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                      float* out_dist, void* stream);
 
+/* The merge over a table of G list pointers (host arrays of G device pointers): list g
+ * of row row0 + r starts at dist_lists[g] + (row0 + r) * k (idx_lists likewise), its
+ * indices shifted by offsets_host[g]; output rows r < M.  The pointers may be local or
+ * mapped from a peer GPU's memory with knn_ipc_open: the corpus-sharded k-NNG (Par-2,
+ * PAPER.md:102) merges its own row block straight from its peers' partial lists over
+ * NVLink, with no all-to-all copy.  Same results as knn_merge.  1 <= G <= 64. */
+knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
+                           const int32_t* const* idx_lists, int32_t G, int64_t row0, int64_t M,
+                           int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                           float* out_dist, void* stream);
+
+/* CUDA IPC plumbing for knn_merge_lists across processes (one process per GPU):
+ * knn_ipc_export writes the 64-byte IPC handle of the allocation holding dev_ptr and the
+ * byte offset of dev_ptr inside it; a peer process passes both to knn_ipc_open, which maps
+ * the allocation (once per ctx; later opens of the same handle reuse the mapping) and
+ * returns the peer-visible pointer.  knn_ipc_close_all unmaps everything this ctx opened
+ * (also done by knn_ctx_destroy).  The exporter must keep the memory alive while mapped. */
+knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64], int64_t* offset);
+knn_status knn_ipc_open(knn_ctx_t ctx, const uint8_t handle[64], int64_t offset, void** dev_ptr);
+knn_status knn_ipc_close_all(knn_ctx_t ctx);
+
 /* ---------------------------------------------------------------- introspection ----
  * Number of kernel launches this ctx has issued so far (for benchmarks). */
 int64_t knn_launch_count(knn_ctx_t ctx);

@@ -5,6 +5,7 @@
 #include "../../include/knn.h"
 #include "internal.cuh"
 
+#include <cuda.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -49,6 +50,8 @@ struct knn_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     double last_stream_copy_ms = 0, last_stream_total_ms = 0;
+    // CUDA IPC mappings opened by knn_ipc_open: handle bytes -> mapped base
+    std::vector<std::pair<std::string, void*>> ipc_open;
 };
 
 namespace {
@@ -426,6 +429,7 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->io) cudaFree(ctx->io);
     if (ctx->st_buf) cudaFree(ctx->st_buf);
+    for (auto& m : ctx->ipc_open) cudaIpcCloseMemHandle(m.second);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (int b = 0; b < 2; ++b) {
         if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
@@ -816,6 +820,82 @@ knn_status knn_select_paper(knn_ctx_t ctx, const float* D, int64_t M, int64_t N,
     KNN_CUDA(knn::launch_select_paper(D, M, N, ldD, k, ctx->ws, bytes, out_idx, out_dist,
                                       static_cast<cudaStream_t>(stream)));
     t.done();
+    return KNN_OK;
+}
+
+knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
+                           const int32_t* const* idx_lists, int32_t G, int64_t row0, int64_t M,
+                           int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                           float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (G < 1 || G > 64 || M < 0 || row0 < 0) return fail(ctx, KNN_ERR_ARG, "bad G=%d, M or row0", G);
+    if (M > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "M must be < 2^31");
+    if (k < 1) return fail(ctx, KNN_ERR_ARG, "k=%d < 1", k);
+    if (k > KNN_MAX_K) return fail(ctx, KNN_ERR_UNSUPPORTED, "k=%d > %d", k, KNN_MAX_K);
+    if (M == 0) return KNN_OK;
+    if (!dist_lists || !idx_lists || !offsets_host || !out_idx || !out_dist)
+        return fail(ctx, KNN_ERR_ARG, "null pointer");
+    for (int g = 0; g < G; ++g) {
+        if (!dist_lists[g] || !idx_lists[g]) return fail(ctx, KNN_ERR_ARG, "null list %d", g);
+        if (offsets_host[g] < 0 || offsets_host[g] > INT32_MAX)
+            return fail(ctx, KNN_ERR_ARG, "offset %d out of range", g);
+    }
+    KNN_TRY(set_device(ctx));
+    Timed t(ctx, KNN_KERNEL_MERGE, static_cast<cudaStream_t>(stream));
+    KNN_CUDA(knn::launch_merge_lists(dist_lists, idx_lists, G, row0, M, k, offsets_host, out_idx,
+                                     out_dist, static_cast<cudaStream_t>(stream)));
+    t.done();
+    return KNN_OK;
+}
+
+knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64], int64_t* offset) {
+    if (!ctx || !dev_ptr || !handle || !offset) return KNN_ERR_ARG;
+    KNN_TRY(set_device(ctx));
+    // the IPC handle names a whole cudaMalloc allocation: find its base (driver API)
+    static CUresult (*get_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+    if (!get_range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(ctx, KNN_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        get_range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return fail(ctx, KNN_ERR_ARG, "pointer is not device memory");
+    cudaIpcMemHandle_t h;
+    KNN_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(handle, &h, 64);
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+    return KNN_OK;
+}
+
+knn_status knn_ipc_open(knn_ctx_t ctx, const uint8_t handle[64], int64_t offset, void** dev_ptr) {
+    if (!ctx || !handle || !dev_ptr || offset < 0) return KNN_ERR_ARG;
+    KNN_TRY(set_device(ctx));
+    const std::string key(reinterpret_cast<const char*>(handle), 64);
+    for (auto& m : ctx->ipc_open)
+        if (m.first == key) {
+            *dev_ptr = static_cast<char*>(m.second) + offset;
+            return KNN_OK;
+        }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    void* base = nullptr;
+    KNN_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->ipc_open.push_back({key, base});
+    *dev_ptr = static_cast<char*>(base) + offset;
+    return KNN_OK;
+}
+
+knn_status knn_ipc_close_all(knn_ctx_t ctx) {
+    if (!ctx) return KNN_ERR_ARG;
+    KNN_TRY(set_device(ctx));
+    for (auto& m : ctx->ipc_open) cudaIpcCloseMemHandle(m.second);
+    ctx->ipc_open.clear();
     return KNN_OK;
 }
 

@@ -99,6 +99,11 @@ cudaError_t launch_select_paper(const float* D, int64_t M, int64_t N, int64_t ld
                                 cudaStream_t s);
 // The kernel of the last launch_select (knn_last_select_kernel).
 extern int g_last_select_kind, g_last_select_splits;
+// Merge over a table of list pointers (local or peer-mapped): list g of row row0 + r at
+// dist_lists[g] + (row0 + r) * k; output rows r < M.
+cudaError_t launch_merge_lists(const float* const* dist_lists, const int32_t* const* idx_lists, int32_t G,
+                               int64_t row0, int64_t M, int32_t k, const int64_t* offsets_host,
+                               int32_t* out_idx, float* out_dist, cudaStream_t s);
 cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
                          int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                          float* out_dist, cudaStream_t s);

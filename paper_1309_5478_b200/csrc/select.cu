@@ -1190,12 +1190,18 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
 struct Offsets {
     int64_t v[64];
 };
+// The G partial lists of a merge: list g of row (row0 + r) starts at d[g] + (row0 + r) * k.
+// The pointers may be local or mapped from a peer GPU's memory (CUDA IPC over NVLink): the
+// fused exchange + merge of the corpus-sharded k-NNG reads its peers' lists directly.
+struct ListPtrs {
+    const float* d[64];
+    const int32_t* i[64];
+};
 
 template <int THREADS, int EPT>
 __global__ void __launch_bounds__(THREADS)
-merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ part_idx, int G,
-             int64_t M, int k, int cap, int KP, int limit, Offsets offs,
-             int32_t* __restrict__ out_idx, float* __restrict__ out_dist) {
+merge_kernel(const ListPtrs lists, int64_t row0, int G, int k, int cap, int KP, int limit,
+             Offsets offs, int32_t* __restrict__ out_idx, float* __restrict__ out_dist) {
     constexpr int CHUNK = THREADS * EPT;
     extern __shared__ uint32_t smem[];
     uint32_t* ckey = smem;
@@ -1221,9 +1227,9 @@ merge_kernel(const float* __restrict__ part_dist, const int32_t* __restrict__ pa
             bool ok = false;
             if (p < L) {
                 int g = (int)(p / k), r = (int)(p - (int64_t)g * k);
-                int64_t off = ((int64_t)g * M + row) * k + r;
-                u[e] = ukey(__ldg(part_dist + off));
-                id[e] = (uint32_t)((int64_t)__ldg(part_idx + off) + offs.v[g]);
+                int64_t off = (row0 + row) * k + r;
+                u[e] = ukey(__ldg(lists.d[g] + off));
+                id[e] = (uint32_t)((int64_t)__ldg(lists.i[g] + off) + offs.v[g]);
                 ok = u[e] < T || (u[e] == T && id[e] < Ti);
             }
             pm |= (uint32_t)ok << e;
@@ -1692,14 +1698,19 @@ cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, co
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
-                         int32_t k, const int64_t* offsets_host, int32_t* out_idx,
-                         float* out_dist, cudaStream_t s) {
+cudaError_t launch_merge_lists(const float* const* dist_lists, const int32_t* const* idx_lists, int32_t G,
+                               int64_t row0, int64_t M, int32_t k, const int64_t* offsets_host,
+                               int32_t* out_idx, float* out_dist, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (G < 1 || G > 64) return cudaErrorInvalidValue;
     constexpr int THREADS = 256, EPT = 4, CHUNK = THREADS * EPT;
     Offsets offs{};
-    for (int g = 0; g < G; ++g) offs.v[g] = offsets_host[g];
+    ListPtrs lists{};
+    for (int g = 0; g < G; ++g) {
+        offs.v[g] = offsets_host[g];
+        lists.d[g] = dist_lists[g];
+        lists.i[g] = idx_lists[g];
+    }
     const int KP = next_pow2(k);
     const int64_t L = (int64_t)G * k;
     int cap, limit;
@@ -1714,9 +1725,21 @@ cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_
     auto kern = merge_kernel<THREADS, EPT>;
     cudaError_t e;
     if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
-    kern<<<(unsigned)M, THREADS, smem, s>>>(part_dist, part_idx, G, M, k, cap, KP, limit, offs,
-                                           out_idx, out_dist);
+    kern<<<(unsigned)M, THREADS, smem, s>>>(lists, row0, G, k, cap, KP, limit, offs, out_idx, out_dist);
     return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_t G, int64_t M,
+                         int32_t k, const int64_t* offsets_host, int32_t* out_idx,
+                         float* out_dist, cudaStream_t s) {
+    if (G < 1 || G > 64) return cudaErrorInvalidValue;
+    const float* dl[64];
+    const int32_t* il[64];
+    for (int g = 0; g < G; ++g) {  // contiguous [G][M][k]
+        dl[g] = part_dist + (size_t)g * M * k;
+        il[g] = part_idx + (size_t)g * M * k;
+    }
+    return launch_merge_lists(dl, il, G, 0, M, k, offsets_host, out_idx, out_dist, s);
 }
 
 }  // namespace knn

@@ -29,7 +29,8 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
            "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
-           "knn_search_streamed"]
+           "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
+           "knn_ipc_close_all"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
@@ -77,6 +78,10 @@ def load_library():
             "knn_select": (st, [p, p, i64, i64, i64, i32, p, p, p]),
             "knn_select_paper": (st, [p, p, i64, i64, i64, i32, p, p, p]),
             "knn_search_streamed": (st, [p, p, i64, p, i64, i32, i32, i32, i32, i64, i64, p, p]),
+            "knn_merge_lists": (st, [p, p, p, i32, i64, i64, i32, p, p, p, p]),
+            "knn_ipc_export": (st, [p, p, p, ctypes.POINTER(ctypes.c_int64)]),
+            "knn_ipc_open": (st, [p, p, i64, ctypes.POINTER(ctypes.c_void_p)]),
+            "knn_ipc_close_all": (st, [p]),
             "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
@@ -267,6 +272,48 @@ def search_streamed(Q, X, k, metric=L2SQ, graph=False, chunk_points=0, query_blo
         out[0].ctypes.data_as(ctypes.c_void_p), out[1].ctypes.data_as(ctypes.c_void_p))
     _check(rc, ctx)
     return out
+
+
+def merge_lists(dist_ptrs, idx_ptrs, row0, M, k, offsets=None, device=None, stream=None):
+    """knn_merge_lists: merge G lists given as device pointers (ints; local or peer-mapped
+    with ipc_open); list g of row row0 + r at dist_ptrs[g] + (row0 + r) * k.  Returns
+    (idx M×k int32, dist M×k fp32) on `device`."""
+    import torch
+    G = len(dist_ptrs)
+    offs = np.zeros(G, np.int64) if offsets is None else np.ascontiguousarray(offsets, np.int64)
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = context(dev.index)
+    idx, dist = _outputs(M, k, dev)
+    dl = (ctypes.c_void_p * G)(*dist_ptrs)
+    il = (ctypes.c_void_p * G)(*idx_ptrs)
+    rc = load_library().knn_merge_lists(ctx, dl, il, G, row0, M, k, offs.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                        _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def ipc_export(t):
+    """(64-byte CUDA IPC handle, byte offset) of the allocation holding tensor t."""
+    ctx = context(t.device.index)
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_int64()
+    _check(load_library().knn_ipc_export(ctx, ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)), ctx)
+    return bytes(h), off.value
+
+
+def ipc_open(handle, offset, device=None):
+    """Map a peer process's allocation (from ipc_export); returns the device pointer (int)."""
+    ctx = context(device)
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = ctypes.c_void_p()
+    _check(load_library().knn_ipc_open(ctx, h, offset, ctypes.byref(ptr)), ctx)
+    return ptr.value
+
+
+def ipc_close_all(device=None):
+    ctx = context(device)
+    _check(load_library().knn_ipc_close_all(ctx), ctx)
 
 
 def select_paper(D, k, N=None, stream=None):

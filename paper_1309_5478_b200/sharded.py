@@ -109,10 +109,57 @@ def search_query_sharded(Q, X, k, group=None, compute=None, broadcast=True):
     return all_i[:M], all_d[:M]
 
 
-def graph_corpus_sharded(X, k, metric=0, group=None, compute=None, merge=None, broadcast=True):
+def _all_gather_rows(t, G, group):
+    """all_gather_into_tensor of equal row blocks; staged through host memory when the
+    backend cannot gather device tensors (gloo, used by the one-GPU tests)."""
+    out = torch.empty((G * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        host = torch.empty(out.shape, dtype=t.dtype)
+        dist.all_gather_into_tensor(host, t.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    return out
+
+
+def peer_merge(part_i, part_d, k, row0, rows, group=None):
+    """Fused exchange + merge of the corpus-sharded k-NNG (SURVEY §8(e) "better Par-2"):
+    every rank maps its peers' partial-list buffers (CUDA IPC; over NVLink between GPUs)
+    and the merge kernel reads the G lists of its own row block [row0, row0 + rows)
+    straight from peer memory — no all-to-all copy of the lists.  The partial lists must be
+    complete on every rank before any rank reads them (synchronize + barrier), and stay
+    alive until every rank has finished reading (second barrier)."""
+    from . import knn
+    G, r = _world(group)
+    hi, oi = knn.ipc_export(part_i)
+    hd, od = knn.ipc_export(part_d)
+    table = [None] * G
+    dist.all_gather_object(table, (hi, oi, hd, od), group=group)
+    dptrs, iptrs = [], []
+    for g, (h_i, o_i, h_d, o_d) in enumerate(table):
+        if g == r:
+            dptrs.append(part_d.data_ptr())
+            iptrs.append(part_i.data_ptr())
+        else:
+            dptrs.append(knn.ipc_open(h_d, o_d, part_d.device.index))
+            iptrs.append(knn.ipc_open(h_i, o_i, part_i.device.index))
+    torch.cuda.synchronize(part_i.device)
+    dist.barrier(group=group)
+    mi, md = knn.merge_lists(dptrs, iptrs, row0, rows, k, device=part_i.device.index)
+    torch.cuda.synchronize(part_i.device)
+    dist.barrier(group=group)
+    knn.ipc_close_all(part_i.device.index)
+    return mi, md
+
+
+def graph_corpus_sharded(X, k, metric=0, group=None, compute=None, merge=None, broadcast=True,
+                         exchange="all_to_all", peer_merge_fn=None):
     """k-NNG of X with the corpus columns sharded over the ranks (Par-2).
 
-    Needs k <= the smallest column block.  Returns the full graph on every rank."""
+    exchange="all_to_all": an all-to-all hands each rank the G partial lists of its row
+    block, merged with knn_merge.  exchange="peer": each rank merges its row block straight
+    from its peers' partial lists mapped over CUDA IPC (peer_merge).  Needs k <= the
+    smallest column block.  Returns the full graph on every rank."""
     compute = compute or _default_compute
     merge = merge or _default_merge
     G, r = _world(group)
@@ -131,15 +178,16 @@ def graph_corpus_sharded(X, k, metric=0, group=None, compute=None, merge=None, b
     part_d[:N] = d
     if G == 1:
         return merge(part_d[None, :N], part_i[None, :N], np.zeros(1, np.int64))
-    # all-to-all: rank g receives, from every rank, the partial lists of rows block g
-    recv_i = torch.empty_like(part_i)
-    recv_d = torch.empty_like(part_d)
-    dist.all_to_all_single(recv_i, part_i, group=group)
-    dist.all_to_all_single(recv_d, part_d, group=group)
-    # recv[s*per:(s+1)*per] = rank s's lists for this rank's rows -> [G][per][k]
-    mi, md = merge(recv_d.view(G, per, k), recv_i.view(G, per, k), np.zeros(G, np.int64))
-    all_i = torch.empty((G * per, k), dtype=torch.int32, device=X.device)
-    all_d = torch.empty((G * per, k), dtype=torch.float32, device=X.device)
-    dist.all_gather_into_tensor(all_i, mi.contiguous(), group=group)
-    dist.all_gather_into_tensor(all_d, md.contiguous(), group=group)
+    if exchange == "peer":
+        mi, md = (peer_merge_fn or peer_merge)(part_i, part_d, k, r * per, per, group)
+    else:
+        # all-to-all: rank g receives, from every rank, the partial lists of rows block g
+        recv_i = torch.empty_like(part_i)
+        recv_d = torch.empty_like(part_d)
+        dist.all_to_all_single(recv_i, part_i, group=group)
+        dist.all_to_all_single(recv_d, part_d, group=group)
+        # recv[s*per:(s+1)*per] = rank s's lists for this rank's rows -> [G][per][k]
+        mi, md = merge(recv_d.view(G, per, k), recv_i.view(G, per, k), np.zeros(G, np.int64))
+    all_i = _all_gather_rows(mi.contiguous(), G, group)
+    all_d = _all_gather_rows(md.contiguous(), G, group)
     return all_i[:N], all_d[:N]

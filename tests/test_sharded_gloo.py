@@ -42,6 +42,19 @@ def oracle_merge(part_dist, part_idx, offsets):
     return torch.from_numpy(idx), torch.from_numpy(dst)
 
 
+def oracle_peer_merge(part_i, part_d, k, row0, rows, group=None):
+    """Stand-in for sharded.peer_merge: every rank's partial lists are visible to every
+    rank (here through all_gather_object instead of CUDA IPC); the merge reads rows
+    [row0, row0 + rows) of each rank's lists."""
+    G = dist.get_world_size(group)
+    table = [None] * G
+    dist.all_gather_object(table, (part_i.numpy(), part_d.numpy()), group=group)
+    pd = np.stack([t[1][row0:row0 + rows] for t in table])
+    pi = np.stack([t[0][row0:row0 + rows] for t in table])
+    idx, dst = oracle.merge(pd, pi, np.zeros(G, np.int64))
+    return torch.from_numpy(idx), torch.from_numpy(dst)
+
+
 def _worker(rank, world, port, mode, N, d, k, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -53,6 +66,9 @@ def _worker(rank, world, port, mode, N, d, k, q):
             i, dd = sharded.graph_query_sharded(Xt, k, compute=oracle_compute)
         elif mode == "corpus":
             i, dd = sharded.graph_corpus_sharded(Xt, k, compute=oracle_compute, merge=oracle_merge)
+        elif mode == "corpus_peer":
+            i, dd = sharded.graph_corpus_sharded(Xt, k, compute=oracle_compute, merge=oracle_merge,
+                                                 exchange="peer", peer_merge_fn=oracle_peer_merge)
         else:
             Qt = torch.from_numpy(datagen.points(N + 3, d, "gauss", seed=78)) if rank == 0 \
                 else torch.zeros((N + 3, d), dtype=torch.float32)
@@ -63,7 +79,7 @@ def _worker(rank, world, port, mode, N, d, k, q):
 
 
 @pytest.mark.parametrize("mode,N", [("query", 301), ("corpus", 301), ("corpus", 64),
-                                    ("search", 200)])
+                                    ("corpus_peer", 301), ("corpus_peer", 64), ("search", 200)])
 def test_two_rank_sharding_equals_unsharded(mode, N):
     d, k = 9, 7
     ctx = mp.get_context("spawn")
