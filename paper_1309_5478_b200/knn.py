@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libknn.so")
+LIB_PATH = os.environ.get("KNN_LIB_PATH") or os.path.join(_HERE, "libknn.so")  # override: A/B builds
 
 L2SQ, L2, COSINE, PEARSON = 0, 1, 2, 3
 NO_SELF = -(2 ** 63)  # KNN_NO_SELF
