@@ -29,6 +29,7 @@
 #include "warpsel.cuh"
 
 #include <climits>
+#include <type_traits>
 #include <cstdlib>
 #include <cooperative_groups.h>
 #include <cmath>
@@ -819,8 +820,8 @@ __device__ __forceinline__ bool ring_consume_row(const RingSmem& r, int64_t N, i
     return piv && *r.s_count < k;
 }
 
-template <int CTHREADS, int CHUNK, int STAGES>
-__global__ void __launch_bounds__(CTHREADS + 32, 2)
+template <int CTHREADS, int CHUNK, int STAGES, int MINB = 2>
+__global__ void __launch_bounds__(CTHREADS + 32, MINB)
 select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int cap,
                    int KP, int limit, int64_t idx_offset, int32_t* __restrict__ out_idx,
                    float* __restrict__ out_dist, const int32_t* __restrict__ list, int r_pivot,
@@ -1613,7 +1614,12 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         }
     }
     if (aligned) {
-        constexpr int CT = 256, CHUNK = 4096;
+        static const int ring_chunk = [] {  // tuning knob (A/B): 4096 (default) or 2048
+            const char* v = getenv("KNN_RING_CHUNK");
+            return v && atoi(v) == 2048 ? 2048 : 4096;
+        }();
+        auto ring = [&](auto chunk_c, auto k4, auto k3) -> cudaError_t {
+        constexpr int CT = 256, CHUNK = decltype(chunk_c)::value;
         int cap, limit;
         if (N <= CHUNK) {
             cap = (int)round_up(N, 32);
@@ -1649,14 +1655,20 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         g_last_select_splits = 1;
         // 4 ring stages when two CTAs still fit on an SM, else 3
         const size_t base_smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
-        const bool four = base_smem + 4 * (size_t)CHUNK * 4 + 64 <= 112 * 1024;
-        auto k4 = select_ring_kernel<CT, CHUNK, 4>;
-        auto k3 = select_ring_kernel<CT, CHUNK, 3>;
-        e = four ? run(k4, 4, nullptr, r_pivot, M) : run(k3, 3, nullptr, r_pivot, M);
-        if (e != cudaSuccess || !r_pivot) return e;
+        const bool four = CHUNK < 4096 || base_smem + 4 * (size_t)CHUNK * 4 + 64 <= 112 * 1024;
+        cudaError_t e3 = four ? run(k4, 4, nullptr, r_pivot, M) : run(k3, 3, nullptr, r_pivot, M);
+        if (e3 != cudaSuccess || !r_pivot) return e3;
         // redo pass: rows whose sampled pivot kept fewer than k candidates (grid covers
         // any count; CTAs beyond it exit at once)
         return four ? run(k4, 4, redo, 0, M) : run(k3, 3, redo, 0, M);
+        };
+        // short rows: 2048-element slices, 3 CTAs per SM (n = 4096, k = 512: 1.85 -> 0.89 ms);
+        // longer rows keep 4096 (a better sample for the pivot, fewer slices per row)
+        if (ring_chunk == 2048 || N <= 8192)
+            return ring(std::integral_constant<int, 2048>{}, select_ring_kernel<256, 2048, 4, 3>,
+                        select_ring_kernel<256, 2048, 4, 3>);
+        return ring(std::integral_constant<int, 4096>{}, select_ring_kernel<256, 4096, 4>,
+                    select_ring_kernel<256, 4096, 3>);
     }
     constexpr int THREADS = 256, VPT = 4, CHUNK = THREADS * VPT * 4;
     int cap, limit;
