@@ -337,7 +337,10 @@ def run_ours(args):
                                          R_local * (S_samp // 32 * 4.0 + 8.0))))
     elif s_n:
         sl = max(s_n // args.steps, 1)
-        rooflines.append((s_ms, hbm_roof("select_warp_kernel (a-S4)", "select_warp_kernel", s_ms, s_n,
+        kind, splits = knn.last_select_kernel()
+        kname = {"warp per row": "select_warp_kernel", "cluster per row": "select_cluster_kernel"}.get(
+            kind, "select_ring_kernel")
+        rooflines.append((s_ms, hbm_roof(f"{kname} (a-S4, {kind})", kname, s_ms, s_n,
                                          R_local / sl * (N * 4.0 + k * 8.0))))
     if m_n and plan_code in (3, 4):
         cands = knn.last_candidates()  # survivors of the partition (whole call)

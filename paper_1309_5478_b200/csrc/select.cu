@@ -343,6 +343,167 @@ __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int
     });
 }
 
+// Bucket finish for large k (the ring select, KP >= 64): instead of an exact radix select
+// (3-4 histogram passes) plus a 55-stage bitonic sort, ONE BBINS-bucket histogram of the
+// candidates' values over [min, max] gives, after an
+// exclusive scan, every bucket's output offset (a counting sort: buckets are monotone in
+// the key) and the bucket b* holding the k-th candidate.  Buckets are linear in the value.  Candidates of buckets < b* are
+// scattered to their bucket's slots; b*'s few candidates are sorted by one warp and the
+// first k - before of them appended; finally odd-even transposition passes order each
+// bucket internally (pairs from different buckets are already in order, so plain passes
+// over the whole array are correct; max-bucket-size passes suffice).  Returns false —
+// before touching anything but `hist` and `sc` — when the buckets are too crowded (ties or
+// a very concentrated key range): the caller then runs block_finish.
+constexpr int BBITS = 10, BBINS = 1 << BBITS;
+constexpr int BSTAR_MAX = 64;   // candidates in b* one warp sorts (2 per lane)
+constexpr int BPASS_MAX = 12;   // odd-even passes (largest bucket below b*)
+template <int THREADS>
+__device__ bool block_finish_bucket(const uint32_t* ckey, const uint32_t* cidx, int cnt, int k,
+                                    uint32_t* kkey, uint32_t* kidx, uint32_t* hist, Scal* sc,
+                                    int64_t idx_offset, int32_t* out_idx, float* out_dist) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = THREADS / 32;
+    constexpr int BPT = BBINS / THREADS;  // bins per thread in the scan
+    static_assert(BPT * THREADS == BBINS, "bins per thread");
+    if (cnt <= k) return false;  // nothing to select: the plain finish is as cheap
+    uint32_t mn, mx;
+    block_key_range<THREADS>(ckey, cnt, sc, mn, mx);
+    // buckets linear in the VALUE over [min, max] (monotone: a rounded subtraction, a
+    // positive scale and floor are all monotone), so uniform keys and narrow distance
+    // bands both spread; non-finite or degenerate ranges take the radix path
+    const float fmn = ukey_to_float(mn), fmx = ukey_to_float(mx);
+    const float span = fmx - fmn;
+    const float scale = (float)BBINS / span;
+    if (!(isfinite(fmn) && isfinite(fmx) && span > 0.0f && isfinite(span) && isfinite(scale))) return false;
+    auto bucket = [&](uint32_t key) -> uint32_t {
+        const float b = (ukey_to_float(key) - fmn) * scale;
+        return min((uint32_t)b, (uint32_t)(BBINS - 1));
+    };
+    for (int i = tid; i < BBINS; i += THREADS) hist[i] = 0;
+    csync<THREADS>();
+    for (int i = tid; i < cnt; i += THREADS) atomicAdd(&hist[bucket(ckey[i])], 1u);
+    csync<THREADS>();
+    // exclusive scan of the bins; b* = bin holding rank k; largest bin below b*
+    uint32_t c[BPT], tsum = 0;
+    #pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+        c[j] = hist[tid * BPT + j];
+        tsum += c[j];
+    }
+    uint32_t incl = tsum;
+    #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t s_wsum[NW];
+    if (lane == 31) s_wsum[warp] = incl;
+    if (tid == 0) {
+        sc->bin = 0xFFFFFFFFu;
+        sc->kept = 0;
+    }
+    csync<THREADS>();
+    uint32_t wbase = 0;
+    #pragma unroll
+    for (int w = 0; w < NW; ++w) wbase += w < warp ? s_wsum[w] : 0u;
+    uint32_t run = wbase + incl - tsum;  // exclusive prefix of this thread's first bin
+    uint32_t mymax = 0;
+    #pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+        const int b = tid * BPT + j;
+        hist[b] = run;  // exclusive offset: the scatter's cursor
+        if (run < (uint32_t)k && (uint32_t)k <= run + c[j]) {
+            sc->bin = b;
+            sc->before = run;
+            sc->neq = c[j];
+        }
+        run += c[j];
+    }
+    csync<THREADS>();
+    const uint32_t bstar = sc->bin, before = sc->before, nstar = sc->neq;
+    #pragma unroll
+    for (int j = 0; j < BPT; ++j)
+        if ((uint32_t)(tid * BPT + j) < bstar) mymax = max(mymax, c[j]);
+    mymax = __reduce_max_sync(FULL, mymax);
+    if (lane == 0) atomicMax((uint32_t*)&sc->kept, mymax);
+    csync<THREADS>();
+    const uint32_t maxc = (uint32_t)sc->kept;
+    if (nstar > BSTAR_MAX || maxc > BPASS_MAX) return false;  // crowded: exact radix path
+    // scatter buckets < b* to their slots; b*'s candidates to a side list
+    __shared__ uint64_t s_star[BSTAR_MAX];
+    __shared__ int s_nstar;
+    if (tid == 0) s_nstar = 0;
+    csync<THREADS>();
+    for (int i = tid; i < cnt; i += THREADS) {
+        const uint32_t key = ckey[i];
+        const uint32_t b = bucket(key);
+        if (b < bstar) {
+            const uint32_t pos = atomicAdd(&hist[b], 1u);
+            kkey[pos] = key;
+            kidx[pos] = cidx[i];
+        } else if (b == bstar) {
+            const int q = atomicAdd(&s_nstar, 1);
+            s_star[q] = (uint64_t)key << 32 | cidx[i];
+        }
+    }
+    csync<THREADS>();
+    if (warp == 0) {
+        // sort b*'s candidates (<= 64, 2 per lane) by (key, idx); append the first k - before
+        uint64_t a0 = lane < (int)nstar ? s_star[lane] : ~0ull;
+        uint64_t a1 = lane + 32 < (int)nstar ? s_star[lane + 32] : ~0ull;
+        // bitonic over 64 = 2 x 32: element p = lane (a0) and 32 + lane (a1)
+        #pragma unroll
+        for (int size = 2; size <= 64; size <<= 1) {
+            #pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride == 32) {
+                    const bool sw = a1 < a0;  // size 64, ascending
+                    const uint64_t x = a0;
+                    a0 = sw ? a1 : a0;
+                    a1 = sw ? x : a1;
+                } else {
+                    #pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint64_t& v = h ? a1 : a0;
+                        const int p = lane + 32 * h;
+                        const uint64_t o = __shfl_xor_sync(FULL, v, stride);
+                        const bool up = ((p & size) == 0) == ((p & stride) == 0);
+                        v = ((o < v) == up) ? o : v;
+                    }
+                }
+            }
+        }
+        const uint32_t need = (uint32_t)k - before;
+        if ((uint32_t)lane < need) {
+            kkey[before + lane] = (uint32_t)(a0 >> 32);
+            kidx[before + lane] = (uint32_t)a0;
+        }
+        if ((uint32_t)lane + 32 < need) {
+            kkey[before + lane + 32] = (uint32_t)(a1 >> 32);
+            kidx[before + lane + 32] = (uint32_t)a1;
+        }
+    }
+    csync<THREADS>();
+    // odd-even transposition inside the buckets below b* (positions [0, before))
+    for (uint32_t pass = 0; pass < maxc; ++pass) {
+        for (uint32_t p = 2 * tid + (pass & 1); p + 1 < before; p += 2 * THREADS) {
+            const uint32_t k0 = kkey[p], k1 = kkey[p + 1], i0 = kidx[p], i1 = kidx[p + 1];
+            if (k1 < k0 || (k1 == k0 && i1 < i0)) {
+                kkey[p] = k1;
+                kkey[p + 1] = k0;
+                kidx[p] = i1;
+                kidx[p + 1] = i0;
+            }
+        }
+        csync<THREADS>();
+    }
+    for (int r = tid; r < k; r += THREADS) {
+        out_idx[r] = (int32_t)((int64_t)kidx[r] + idx_offset);
+        out_dist[r] = ukey_to_float(kkey[r]);
+    }
+    return true;
+}
+
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -690,7 +851,7 @@ __device__ __forceinline__ RingSmem ring_smem(uint8_t* smem_raw, int cap, int KP
     r.cidx = r.ckey + cap;
     r.kkey = r.cidx + cap;
     r.kidx = r.kkey + KP;
-    r.hist = r.kidx + KP;
+    r.hist = r.kidx + KP;  // BBINS words (the bucket finish's histogram)
     r.sc = sc;
     r.s_count = s_count;
     if (threadIdx.x == 0) {
@@ -858,8 +1019,10 @@ select_ring_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
             csync<CTHREADS>();
             continue;
         }
-        block_finish<CTHREADS>(r.ckey, r.cidx, s_count, k, KP, r.kkey, r.kidx, r.hist, &sc, idx_offset,
-                               out_idx + row * k, out_dist + row * k);
+        if (KP < 64 || !block_finish_bucket<CTHREADS>(r.ckey, r.cidx, s_count, k, r.kkey, r.kidx, r.hist,
+                                                        &sc, idx_offset, out_idx + row * k, out_dist + row * k))
+            block_finish<CTHREADS>(r.ckey, r.cidx, s_count, k, KP, r.kkey, r.kidx, r.hist, &sc, idx_offset,
+                                   out_idx + row * k, out_dist + row * k);
         csync<CTHREADS>();
     }
 }
@@ -1639,7 +1802,7 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         if (r_pivot) KNN_CUDA_TRY(cudaMemsetAsync(redo, 0, sizeof(int32_t), s));
         auto run = [&](auto kern, int stages, const int32_t* list, int rp, int64_t grid_rows) -> cudaError_t {
             const size_t smem = (size_t)stages * CHUNK * 4 + 2 * stages * 8 +
-                                (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
+                                (size_t)(2 * cap + 2 * KP + BBINS) * sizeof(uint32_t);
             cudaError_t e2;
             if ((e2 = set_smem(kern, smem)) != cudaSuccess) return e2;
             int per_sm = 0;
@@ -1654,7 +1817,7 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         g_last_select_kind = 1;
         g_last_select_splits = 1;
         // 4 ring stages when two CTAs still fit on an SM, else 3
-        const size_t base_smem = (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t);
+        const size_t base_smem = (size_t)(2 * cap + 2 * KP + BBINS) * sizeof(uint32_t);
         const bool four = CHUNK < 4096 || base_smem + 4 * (size_t)CHUNK * 4 + 64 <= 112 * 1024;
         cudaError_t e3 = four ? run(k4, 4, nullptr, r_pivot, M) : run(k3, 3, nullptr, r_pivot, M);
         if (e3 != cudaSuccess || !r_pivot) return e3;
