@@ -1697,10 +1697,10 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         const int x = v ? atoi(v) : WSEL_K;
         return x < 0 ? 0 : x > WSEL_K ? WSEL_K : x;
     }();
-    // warp per row for k <= 32, and for k <= 128 on short rows; longer rows with k > 32
-    // go to the CTA ring with its sampled pivot (measured: 65536-long rows, k = 64: 3.9 vs
-    // 6.5 ms; 8192-long rows: the warp path wins; scripts/select_mini.sh)
-    if (aligned && k <= warp_maxk && (k <= 32 || N < 24576) && M >= 4 * (int64_t)sms) {
+    // warp per row for k <= 32; k > 32 goes to the CTA ring (sampled pivot, bucket finish):
+    // measured 8192-long rows k = 64: 0.15 vs 0.30 ms, 65536-long rows k = 64: 3.6 vs
+    // 6.5 ms (scripts/select_short.sh, select_mini.sh)
+    if (aligned && k <= warp_maxk && k <= 32 && M >= 4 * (int64_t)sms) {
         // warp per row: enough rows to give every SM >= 4 warps
         // k <= 32 folds every 32 survivors into the sorted register list; larger k
         // rebuilds the buffer once it passes max(2k, k + 64)
