@@ -6,6 +6,7 @@
 #include "internal.cuh"
 
 #include <cuda.h>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -205,7 +206,20 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     const int64_t Ssamp = round_up(N / ctx->pivot_div, 256);
     const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
                        ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= k + 1;
-    const bool pivot_sym = pivot && same && self_shift == 0 && ctx->sym_ok;
+    // Quantile pivot for k > 32 (the same quickselect partition; the pivot is a bucketed
+    // order statistic of a single-product sample of Sq columns)
+    const int64_t Sq = round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
+    const bool pivotq = allow_pivot && !fused && tc && ctx->pivot_ok && k > 32 && N >= 16384 &&
+                        ctx->plan != KNN_PLAN_MATERIALISED && Sq <= N;
+    int32_t rq = 0;
+    if (pivotq) {
+        const double mu = (double)Sq * k / (double)N;
+        // five standard deviations: a row below its k-th (certificate failure) redoes the
+        // whole call, so the per-row failure rate must be ~1e-7
+        rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0);
+    }
+    const int32_t capq = (int32_t)round_up(3 * (int64_t)k > 2048 ? 3 * (int64_t)k : 2048, 256);
+    const bool pivot_sym = (pivot || pivotq) && same && self_shift == 0 && ctx->sym_ok;
     const int32_t cap = ctx->pivot_cap;
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
     const int64_t ldD = round_up(N, 4);
@@ -216,10 +230,10 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     if (fused) rows_blk = 0;  // no distance block
     // k-NNG with the transpose reuse of PAPER.md:83: only the upper triangle is multiplied
     // (bit-identical to the other plans thanks to the canonical orientation)
-    const bool sym = !fused && !pivot && tc && ctx->sym_ok && same && self_shift == 0 &&
+    const bool sym = !fused && !pivot && !pivotq && tc && ctx->sym_ok && same && self_shift == 0 &&
                      (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
     if (sym) rows_blk = M;
-    ctx->last_plan = fused ? 1 : pivot_sym ? 3 : pivot ? 4 : sym ? 2 : 0;
+    ctx->last_plan = fused ? 1 : pivot_sym ? 3 : (pivot || pivotq) ? 4 : sym ? 2 : 0;
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -231,7 +245,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         };
         prep(px, N);
         if (same) pq = px; else prep(pq, M);
-        D = c.take<float>(pivot ? (size_t)(Ssamp / 32) * M : (size_t)rows_blk * ldD);
+        D = c.take<float>(pivot ? (size_t)(Ssamp / 32) * M : pivotq ? (size_t)Sq * M : (size_t)rows_blk * ldD);
     };
     Carve probe{nullptr};
     Prepared pq{}, px{};
@@ -245,16 +259,17 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int32_t* redo = nullptr;
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
-        if (!fused && !pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
+        if (!fused && !pivot && !pivotq) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
         if (fused && S > 1) {
             part_i = c.take<int32_t>((size_t)S * M * k);
             part_d = c.take<float>((size_t)S * M * k);
         }
-        if (pivot) {
+        if (pivot || pivotq) {
+            const int32_t cp = pivot ? cap : capq;
             thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
-            ckey = c.take<uint32_t>((size_t)M * cap);
-            cidx = c.take<uint32_t>((size_t)M * cap);
+            ckey = c.take<uint32_t>((size_t)M * cp);
+            cidx = c.take<uint32_t>((size_t)M * cp);
         }
     };
     layout_all(probe);
@@ -308,6 +323,31 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, flag, s));
+        tc2.done();
+        return KNN_OK;
+    }
+    if (pivotq) {
+        // 1. sample: single-product upper bounds of the rows against the first Sq columns
+        //    (the self pair +inf), 2. pivots, 3. partition GEMM, 4. exact select (k > 32)
+        {
+            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, Sq, d_pad};
+            Timed tg(ctx, KNN_KERNEL_GEMM, s);
+            KNN_CUDA(knn::launch_dist_tc_sample(op, metric, self_shift, D, Sq, ctx->pivot_margin, ctx->num_sms, s));
+            tg.done();
+            KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
+            KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * sizeof(int32_t), s));
+            Timed tp(ctx, KNN_KERNEL_SELECT, s);
+            KNN_CUDA(knn::launch_pivot_from_sample(D, M, Sq, Sq, rq, thr, s));
+            tp.done();
+        }
+        knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        Timed tg(ctx, KNN_KERNEL_FUSED, s);
+        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, capq,
+                                           flag, ctx->num_sms, s));
+        tg.done();
+        Timed tc2(ctx, KNN_KERNEL_MERGE, s);
+        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, capq, M, k, idx_offset, out_idx, out_dist,
+                                                    flag, s));
         tc2.done();
         return KNN_OK;
     }

@@ -125,8 +125,10 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
 }
 
 // Epilogue modes: MODE_STORE writes D; MODE_PIVOT keeps the partition's candidates;
-// MODE_MINS writes, per row, the minimum distance of every 32-column chunk.
-enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2 };
+// MODE_MINS writes, per row, the minimum distance of every 32-column chunk; MODE_SAMPLE
+// writes the single-product upper bound v >= u of every element (the quantile pivot's
+// sample for k > 32), unclamped, in the u domain.
+enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3 };
 
 template <int METRIC, bool SYM, int MODE, class Sched>
 __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
@@ -138,13 +140,14 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     // mirrored from one), so the mainloop sees no self shift.
     constexpr bool PIVOT = MODE == MODE_PIVOT;
     constexpr bool MINS = MODE == MODE_MINS;
+    constexpr bool SAMPLE = MODE == MODE_SAMPLE;
     constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
     // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
-    constexpr int NSEG = MINS ? 1 : 3;
-    constexpr int KSTAGES = MINS ? 2 * STAGES : STAGES;
+    constexpr int NSEG = MINS || SAMPLE ? 1 : 3;
+    constexpr int KSTAGES = MINS || SAMPLE ? 2 * STAGES : STAGES;
     static_assert(KSTAGES * stage_bytes<NSEG>() == STAGES * STAGE_BYTES, "smem layout");
     // the single product is orientation-free: no two-pass blocks on the diagonal
-    const int64_t ml_shift = SYM || MINS ? INT64_MIN : ep.self_shift;
+    const int64_t ml_shift = SYM || MINS || SAMPLE ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -270,7 +273,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         if (METRIC == 2) u = fminf(u, 3.0f);
                         // MINS: the hi.hi value plus a bound of its error, so that it is never
                         // below the FP32-accurate u of the partition
-                        v[c] = MINS ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
+                        v[c] = MINS || SAMPLE ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
                     }
                 }
                 const int64_t c0 = n0 + cb;
@@ -641,6 +644,34 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+                                                                sched, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_sample(const TcOperands& op, int32_t metric, int64_t self_shift, float* Ds,
+                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s) {
+    if (op.M == 0 || op.N == 0) return cudaSuccess;
+    if (ldS % 4 != 0 || (reinterpret_cast<uintptr_t>(Ds) & 15) != 0) return cudaErrorInvalidValue;
+    CUtensorMap mqh, mql, mxh, mxl, md;
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2) ||
+        !tc_make_output_map(&md, Ds, op.M, op.N, ldS))
+        return cudaErrorInvalidValue;
+    // the same single-product error bound as the chunk-minimum sample (launch_dist_tc_mins)
+    float margin = (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
+                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
+    if (!std::isnan(margin_override)) margin = margin_override;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, Ds, ldS,
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin};
+    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+    const int64_t units = sched.n_mp * sched.n_nb;
+    const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+    auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_SAMPLE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_SAMPLE, TileSched> : dist_tc_kernel<0, false, MODE_SAMPLE, TileSched>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 1, op.d_pad / BK,
                                                                 sched, ep);
     return cudaGetLastError();
 }

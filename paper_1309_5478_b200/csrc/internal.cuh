@@ -66,12 +66,24 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
 // (N a multiple of 32; self pair excluded).
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t self_shift, float* mins,
                                 float margin_override, int num_sms, cudaStream_t s);
+// Quantile-pivot sample for k > 32: Ds[i][j] (ldS) = the single-product upper bound of u(i, j)
+// for corpus points j < op.N (self pair +inf), unclamped.
+cudaError_t launch_dist_tc_sample(const TcOperands& op, int32_t metric, int64_t self_shift, float* Ds,
+                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s);
 // select.cu: pivots = k-th smallest chunk minimum per row; exact select over candidates.
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s);
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                     int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
+// k > 32 pivot plan: per-row pivot with >= r of the S sampled upper bounds at or below it;
+// exact select over the partition's candidate lists (CTA per row; flag |= 2 on a failed
+// certificate or an overflowed list).
+cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int64_t ldS, int32_t r,
+                                     float* thr, cudaStream_t s);
+cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                          int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
+                                          int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
 // fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial

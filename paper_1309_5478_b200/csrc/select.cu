@@ -356,15 +356,15 @@ __device__ void block_finish(uint32_t* ckey, uint32_t* cidx, int cnt, int k, int
 // a very concentrated key range): the caller then runs block_finish.
 constexpr int BBITS = 10, BBINS = 1 << BBITS;
 constexpr int BSTAR_MAX = 64;   // candidates in b* one warp sorts (2 per lane)
-constexpr int BPASS_MAX = 12;   // odd-even passes (largest bucket below b*)
-template <int THREADS>
+constexpr int BPASS_MAX = 16;   // odd-even passes (largest bucket below b*)
+template <int THREADS, int NB = BBINS>
 __device__ bool block_finish_bucket(const uint32_t* ckey, const uint32_t* cidx, int cnt, int k,
                                     uint32_t* kkey, uint32_t* kidx, uint32_t* hist, Scal* sc,
                                     int64_t idx_offset, int32_t* out_idx, float* out_dist) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = THREADS / 32;
-    constexpr int BPT = BBINS / THREADS;  // bins per thread in the scan
-    static_assert(BPT * THREADS == BBINS, "bins per thread");
+    constexpr int BPT = NB / THREADS;  // bins per thread in the scan
+    static_assert(BPT * THREADS == NB, "bins per thread");
     if (cnt <= k) return false;  // nothing to select: the plain finish is as cheap
     uint32_t mn, mx;
     block_key_range<THREADS>(ckey, cnt, sc, mn, mx);
@@ -373,13 +373,13 @@ __device__ bool block_finish_bucket(const uint32_t* ckey, const uint32_t* cidx, 
     // bands both spread; non-finite or degenerate ranges take the radix path
     const float fmn = ukey_to_float(mn), fmx = ukey_to_float(mx);
     const float span = fmx - fmn;
-    const float scale = (float)BBINS / span;
+    const float scale = (float)NB / span;
     if (!(isfinite(fmn) && isfinite(fmx) && span > 0.0f && isfinite(span) && isfinite(scale))) return false;
     auto bucket = [&](uint32_t key) -> uint32_t {
         const float b = (ukey_to_float(key) - fmn) * scale;
-        return min((uint32_t)b, (uint32_t)(BBINS - 1));
+        return min((uint32_t)b, (uint32_t)(NB - 1));
     };
-    for (int i = tid; i < BBINS; i += THREADS) hist[i] = 0;
+    for (int i = tid; i < NB; i += THREADS) hist[i] = 0;
     csync<THREADS>();
     for (int i = tid; i < cnt; i += THREADS) atomicAdd(&hist[bucket(ckey[i])], 1u);
     csync<THREADS>();
@@ -1678,6 +1678,149 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// ------------------------------------------------------------ quantile pivot (k > 32) --
+// The pivot plan for k > 32: per row, a pivot P with at least r of the
+// row's S sampled upper bounds v <= P, from value-linear buckets: min/max of the finite
+// samples, one 1024-bucket histogram, the bucket b* holding the r-th sample, and P = the
+// largest sample in buckets <= b* (exact, so the r-th sample is <= P).  Fewer than r
+// finite samples: P = +inf (every element becomes a candidate; the list overflow then
+// sends the call to the materialised plan).  One CTA per row, rows re-read from L2.
+constexpr int QP_THREADS = 256;
+__global__ void __launch_bounds__(QP_THREADS)
+pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int64_t ldS, int r,
+                         float* __restrict__ thr) {
+    __shared__ uint32_t hist[BBINS];
+    __shared__ Scal sc;
+    __shared__ int s_nfin;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+        const float* rp = Ds + row * ldS;
+        if (tid == 0) {
+            sc.lo = 0xFFFFFFFFu;
+            sc.hi = 0;
+            sc.kept = 0;
+            sc.bin = BBINS - 1;
+            s_nfin = 0;
+        }
+        for (int i = tid; i < BBINS; i += QP_THREADS) hist[i] = 0;
+        __syncthreads();
+        float lo = __int_as_float(0x7F800000), hi = -__int_as_float(0x7F800000);
+        int nfin = 0;
+        for (int64_t j = tid; j < S; j += QP_THREADS) {
+            const float x = rp[j];
+            if (isfinite(x)) {
+                lo = fminf(lo, x);
+                hi = fmaxf(hi, x);
+                ++nfin;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+            nfin += __shfl_xor_sync(FULL, nfin, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&s_nfin, nfin);
+            atomicMin(&sc.lo, ukey(lo));  // float min / max through the order-preserving keys
+            atomicMax(&sc.hi, ukey(hi));
+        }
+        __syncthreads();
+        if (s_nfin < r) {  // not reached for finite inputs (S - 1 >= r finite samples)
+            if (tid == 0) thr[row] = s_nfin ? ukey_to_float(sc.hi) : -__int_as_float(0x7F800000);
+            __syncthreads();
+            continue;
+        }
+        const float fmn = ukey_to_float(sc.lo), fmx = ukey_to_float(sc.hi);
+        const float span = fmx - fmn;
+        const float scale = span > 0.0f && isfinite(span) && isfinite((float)BBINS / span) ? (float)BBINS / span : 0.0f;
+        auto bucket = [&](float x) -> uint32_t {
+            return min((uint32_t)((x - fmn) * scale), (uint32_t)(BBINS - 1));
+        };
+        for (int64_t j = tid; j < S; j += QP_THREADS) {
+            const float x = rp[j];
+            if (isfinite(x)) atomicAdd(&hist[bucket(x)], 1u);
+        }
+        __syncthreads();
+        // bucket holding the r-th finite sample (warp 0 scans 1024 bins, 32 per lane)
+        if (tid < 32) {
+            uint32_t c[32], sum = 0;
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                c[j] = hist[lane * 32 + j];
+                sum += c[j];
+            }
+            uint32_t incl = sum;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t run = incl - sum;
+            if (run < (uint32_t)r && (uint32_t)r <= incl) {
+                #pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (run + c[j] >= (uint32_t)r) {
+                        sc.bin = lane * 32 + j;
+                        break;
+                    }
+                    run += c[j];
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t bstar = sc.bin;
+        float p = -__int_as_float(0x7F800000);
+        for (int64_t j = tid; j < S; j += QP_THREADS) {
+            const float x = rp[j];
+            if (isfinite(x) && bucket(x) <= bstar) p = fmaxf(p, x);
+        }
+        for (int o = 16; o > 0; o >>= 1) p = fmaxf(p, __shfl_xor_sync(FULL, p, o));
+        if (lane == 0) atomicMax(reinterpret_cast<uint32_t*>(&sc.kept), ukey(p));
+        __syncthreads();
+        if (tid == 0) thr[row] = ukey_to_float((uint32_t)sc.kept);
+        __syncthreads();
+    }
+}
+
+// Exact select over the partition's candidate lists for k > 32: one CTA per row loads the
+// row's candidates (ukeys of the distances + column) into shared memory and runs the
+// bucket finish (or the exact radix + bitonic finish).  Certificate: fewer than k
+// candidates (or an overflowed list) sets flag bit 2, and the caller redoes the call.
+constexpr int CS_THREADS = 256;
+constexpr int CS_BINS = 4096;
+__global__ void __launch_bounds__(CS_THREADS, 4)
+candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
+                              const uint32_t* __restrict__ cidx_g, int32_t cap, int64_t M, int k,
+                              int KP, int64_t idx_offset, int32_t* __restrict__ out_idx,
+                              float* __restrict__ out_dist, int32_t* __restrict__ flag) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* ckey = smem;
+    uint32_t* cidx = ckey + cap;
+    uint32_t* kkey = cidx + cap;
+    uint32_t* kidx = kkey + KP;
+    uint32_t* hist = kidx + KP;  // CS_BINS
+    __shared__ Scal sc;
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+        const int n = cnt[row];
+        if (threadIdx.x == 0)  // diagnostic: candidates kept (knn_last_candidates)
+            atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
+        if (n > cap || n < k) {
+            if (threadIdx.x == 0) atomicOr(flag, 2);
+            continue;
+        }
+        for (int i = threadIdx.x; i < n; i += CS_THREADS) {
+            ckey[i] = ckey_g[row * cap + i];
+            cidx[i] = cidx_g[row * cap + i];
+        }
+        __syncthreads();
+        if (!block_finish_bucket<CS_THREADS, CS_BINS>(ckey, cidx, n, k, kkey, kidx, hist, &sc, idx_offset,
+                                                       out_idx + row * k, out_dist + row * k))
+            block_finish<CS_THREADS>(ckey, cidx, n, k, KP, kkey, kidx, hist, &sc, idx_offset,
+                                     out_idx + row * k, out_dist + row * k);
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 int g_last_select_kind = -1, g_last_select_splits = 1;
@@ -1915,6 +2058,37 @@ cudaError_t launch_merge(const float* part_dist, const int32_t* part_idx, int32_
         il[g] = part_idx + (size_t)g * M * k;
     }
     return launch_merge_lists(dl, il, G, 0, M, k, offsets_host, out_idx, out_dist, s);
+}
+
+cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int64_t ldS, int32_t r,
+                                     float* thr, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = (int64_t)sms * 8;
+    if (grid > M) grid = M;
+    pivot_from_sample_kernel<<<(unsigned)grid, QP_THREADS, 0, s>>>(Ds, M, S, ldS, r, thr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                          int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
+                                          int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    const int KP = next_pow2(k);
+    const size_t smem = (size_t)(2 * cap + 2 * KP + CS_BINS) * sizeof(uint32_t);
+    cudaError_t e;
+    if ((e = set_smem(candidate_select_large_kernel, smem)) != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, candidate_select_large_kernel, CS_THREADS, smem);
+    int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (grid > M) grid = M;
+    candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, ckey, cidx, cap, M, k, KP,
+                                                                          idx_offset, out_idx, out_dist, flag);
+    return cudaGetLastError();
 }
 
 }  // namespace knn

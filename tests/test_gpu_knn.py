@@ -436,3 +436,69 @@ def test_pivot_large_sample_multi_slab():
     env = dict(os.environ, KNN_PIVOT_DIV="2")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
+
+
+# ------------------------------------------------------- quantile pivot plan (k > 32) ---
+@pytest.mark.parametrize("N,d,k,metric,dist", [(20000, 48, 33, 0, "gauss"), (16384, 64, 128, 1, "uniform"),
+                                               (24000, 32, 512, 0, "clusters"), (32768, 40, 1024, 2, "gauss"),
+                                               (16500, 20, 100, 0, "grid")])
+def test_quantile_pivot_graph_equals_materialised(N, d, k, metric, dist):
+    """k > 32: the pivot is a bucketed order statistic of a single-product sample
+    (DESIGN.md §6.5); the candidate select is exact, so the graph equals the materialised
+    plan bit for bit (grid: massive ties; the lists may overflow and fall back)."""
+    kn = knn()
+    X = cuda(datagen.points(N, d, dist, seed=N + d + k))
+    gi, gd = kn.graph(X, k, metric=metric)
+    plan = kn.last_plan()
+    assert plan == 3 or dist == "grid", plan
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(X, k, metric=metric)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri)
+    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_quantile_pivot_search_and_shifted_blocks():
+    kn = knn()
+    X = cuda(datagen.points(40000, 48, "gauss", seed=61))
+    Q = cuda(datagen.points(3000, 48, "gauss", seed=62))
+    gi, gd = kn.search_block(Q, X, 200)
+    assert kn.last_plan() == 4
+    ai, ad = kn.search_block(X[5000:9000].contiguous(), X, 64, self_shift=5000, idx_offset=7)
+    assert kn.last_plan() == 4
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.search_block(Q, X, 200)
+        bi, bd = kn.search_block(X[5000:9000].contiguous(), X, 64, self_shift=5000, idx_offset=7)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri) and torch.equal(gd, rd)
+    assert torch.equal(ai, bi) and torch.equal(ad, bd)
+
+
+def test_quantile_pivot_e2e_vs_oracle():
+    X = datagen.points(20000, 64, "uniform", seed=63)
+    k = 300
+    gi, gd = run_graph(X, k)
+    rows = np.arange(0, 20000, 311)
+    D64 = oracle.dist_rows(X, X, rows=rows)
+    n = oracle.sqnorms(X)
+    res = checks.check_rows(gi[rows], gd[rows], D64, n[rows], n, rows, k, graph=True)
+    assert res["failures"] == [], res["failures"][:3]
+
+
+def test_quantile_pivot_certificate_failure_falls_back_exactly():
+    code = (
+        "import torch\n"
+        "from paper_1309_5478_b200 import knn, datagen\n"
+        "X = torch.from_numpy(datagen.points(16384, 64, 'uniform', seed=64)).cuda()\n"
+        "gi, gd = knn.graph(X, 100)\n"
+        "assert knn.last_plan() != 3, knn.last_plan()\n"
+        "knn.set_plan(knn.PLAN_MATERIALISED)\n"
+        "ri, rd = knn.graph(X, 100)\n"
+        "assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))\n")
+    env = dict(os.environ, KNN_PIVOT_MARGIN="-0.05")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=300)
