@@ -308,7 +308,11 @@ def run_ours(args):
                                             "knn_fused_kernel", f_ms, f_n, R_local)))
     if g_n and plan_code in (3, 4):
         S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
-        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x first N/8 columns -> 32-column chunk minima)",
+        if k > 32:  # quantile pivot: the sample is max(N/8, 4096) columns, stored
+            S_samp = -(-max(N // int(os.environ.get('KNN_PIVOT_DIV', '8')), 4096) // 256) * 256
+        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x first N/8 columns -> 32-column chunk minima)"
+                         if k <= 32 else
+                         f"dist_tc_kernel<SAMPLE> (quantile-pivot sample: single-product upper bounds, rows x first {S_samp} columns)",
                          "dist_tc_kernel_sample", g_ms, g_n, R_local)
         avg = g_ms / g_n
         flop = 2.0 * R_local * S_samp * d_pad  # one hi.hi product
@@ -332,9 +336,14 @@ def run_ours(args):
         rooflines.append((g_ms, gr))
     if s_n and plan_code in (3, 4):
         S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
-        rooflines.append((s_ms, hbm_roof("pivot_from_mins_kernel (pivot = k-th smallest of the row's chunk minima)",
-                                         "pivot_from_mins_kernel", s_ms, s_n,
-                                         R_local * (S_samp // 32 * 4.0 + 8.0))))
+        if k <= 32:
+            rooflines.append((s_ms, hbm_roof("pivot_from_mins_kernel (pivot = k-th smallest of the row's chunk minima)",
+                                             "pivot_from_mins_kernel", s_ms, s_n,
+                                             R_local * (S_samp // 32 * 4.0 + 8.0))))
+        else:
+            S_samp = -(-max(N // int(os.environ.get('KNN_PIVOT_DIV', '8')), 4096) // 256) * 256
+            rooflines.append((s_ms, hbm_roof("pivot_from_sample_kernel (pivot = bucketed order statistic of the sample)",
+                                             "pivot_from_sample_kernel", s_ms, s_n, R_local * (S_samp * 4.0 + 4.0))))
     elif s_n:
         sl = max(s_n // args.steps, 1)
         kind, splits = knn.last_select_kernel()
@@ -344,8 +353,9 @@ def run_ours(args):
                                          R_local / sl * (N * 4.0 + k * 8.0))))
     if m_n and plan_code in (3, 4):
         cands = knn.last_candidates()  # survivors of the partition (whole call)
-        rooflines.append((m_ms, hbm_roof("candidate_select_kernel (exact select of the partition)",
-                                         "candidate_select_kernel", m_ms, m_n,
+        cs_name = "candidate_select_kernel" if k <= 32 else "candidate_select_large_kernel"
+        rooflines.append((m_ms, hbm_roof(f"{cs_name} (exact select of the partition)",
+                                         cs_name, m_ms, m_n,
                                          cands * 8.0 + R_local * (4.0 + k * 8.0))))
         rooflines[-1][1]["candidates_per_row"] = cands / max(R_local, 1)
     elif m_n:

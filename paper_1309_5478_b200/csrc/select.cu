@@ -1686,6 +1686,9 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 // finite samples: P = +inf (every element becomes a candidate; the list overflow then
 // sends the call to the materialised plan).  One CTA per row, rows re-read from L2.
 constexpr int QP_THREADS = 256;
+// EPT > 0: the row (S <= EPT * QP_THREADS) is held in registers and read from memory once;
+// EPT == 0: three passes over the row (L2-resident after the first).
+template <int EPT>
 __global__ void __launch_bounds__(QP_THREADS)
 pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int64_t ldS, int r,
                          float* __restrict__ thr) {
@@ -1693,8 +1696,18 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
     __shared__ Scal sc;
     __shared__ int s_nfin;
     const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int NR = EPT > 0 ? EPT : 1;
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
         const float* rp = Ds + row * ldS;
+        float xr[NR];
+        auto elem = [&](int e, int64_t j) -> float { return EPT > 0 ? xr[e] : rp[j]; };
+        if (EPT > 0) {
+            #pragma unroll
+            for (int e = 0; e < NR; ++e) {
+                const int64_t j = (int64_t)e * QP_THREADS + tid;
+                xr[e] = j < S ? __ldg(rp + j) : __int_as_float(0x7F800000);
+            }
+        }
         if (tid == 0) {
             sc.lo = 0xFFFFFFFFu;
             sc.hi = 0;
@@ -1706,14 +1719,21 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
         __syncthreads();
         float lo = __int_as_float(0x7F800000), hi = -__int_as_float(0x7F800000);
         int nfin = 0;
-        for (int64_t j = tid; j < S; j += QP_THREADS) {
-            const float x = rp[j];
+        auto for_each = [&](auto f) {
+            if (EPT > 0) {
+                #pragma unroll
+                for (int e = 0; e < NR; ++e) f(elem(e, 0));
+            } else {
+                for (int64_t j = tid; j < S; j += QP_THREADS) f(elem(0, j));
+            }
+        };
+        for_each([&](float x) {
             if (isfinite(x)) {
                 lo = fminf(lo, x);
                 hi = fmaxf(hi, x);
                 ++nfin;
             }
-        }
+        });
         for (int o = 16; o > 0; o >>= 1) {
             lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
             hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
@@ -1736,10 +1756,9 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
         auto bucket = [&](float x) -> uint32_t {
             return min((uint32_t)((x - fmn) * scale), (uint32_t)(BBINS - 1));
         };
-        for (int64_t j = tid; j < S; j += QP_THREADS) {
-            const float x = rp[j];
+        for_each([&](float x) {
             if (isfinite(x)) atomicAdd(&hist[bucket(x)], 1u);
-        }
+        });
         __syncthreads();
         // bucket holding the r-th finite sample (warp 0 scans 1024 bins, 32 per lane)
         if (tid < 32) {
@@ -1770,10 +1789,9 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
         __syncthreads();
         const uint32_t bstar = sc.bin;
         float p = -__int_as_float(0x7F800000);
-        for (int64_t j = tid; j < S; j += QP_THREADS) {
-            const float x = rp[j];
+        for_each([&](float x) {
             if (isfinite(x) && bucket(x) <= bstar) p = fmaxf(p, x);
-        }
+        });
         for (int o = 16; o > 0; o >>= 1) p = fmaxf(p, __shfl_xor_sync(FULL, p, o));
         if (lane == 0) atomicMax(reinterpret_cast<uint32_t*>(&sc.kept), ukey(p));
         __syncthreads();
@@ -2068,7 +2086,12 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = (int64_t)sms * 8;
     if (grid > M) grid = M;
-    pivot_from_sample_kernel<<<(unsigned)grid, QP_THREADS, 0, s>>>(Ds, M, S, ldS, r, thr);
+    if (S <= 16 * QP_THREADS)
+        pivot_from_sample_kernel<16><<<(unsigned)grid, QP_THREADS, 0, s>>>(Ds, M, S, ldS, r, thr);
+    else if (S <= 32 * QP_THREADS)
+        pivot_from_sample_kernel<32><<<(unsigned)grid, QP_THREADS, 0, s>>>(Ds, M, S, ldS, r, thr);
+    else
+        pivot_from_sample_kernel<0><<<(unsigned)grid, QP_THREADS, 0, s>>>(Ds, M, S, ldS, r, thr);
     return cudaGetLastError();
 }
 
