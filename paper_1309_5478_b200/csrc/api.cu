@@ -204,19 +204,22 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     // the minima of the 32-column chunks of a column sample (>= the row's k-th distance),
     // then the GEMM keeps only elements <= pivot.
     const int64_t Ssamp = round_up(N / ctx->pivot_div, 256);
+    // the sample is a permuted column subset that may contain the row's own point: one
+    // more rank keeps k non-self elements at or below the pivot
+    const int32_t kk = self_shift != KNN_NO_SELF ? k + 1 : k;
     const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
-                       ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= k + 1;
+                       ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= kk + 1;
     // Quantile pivot for k > 32 (the same quickselect partition; the pivot is a bucketed
     // order statistic of a single-product sample of Sq columns)
     const int64_t Sq = round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
     const bool pivotq = allow_pivot && !fused && tc && ctx->pivot_ok && k > 32 && N >= 16384 &&
-                        ctx->plan != KNN_PLAN_MATERIALISED && Sq <= N;
+                        ctx->plan != KNN_PLAN_MATERIALISED && Sq <= (N / 256) * 256;
     int32_t rq = 0;
     if (pivotq) {
         const double mu = (double)Sq * k / (double)N;
         // five standard deviations: a row below its k-th (certificate failure) redoes the
         // whole call, so the per-row failure rate must be ~1e-7
-        rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0);
+        rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0) + (self_shift != KNN_NO_SELF ? 1 : 0);
     }
     const int32_t capq = (int32_t)round_up(3 * (int64_t)k > 2048 ? 3 * (int64_t)k : 2048, 256);
     const bool pivot_sym = (pivot || pivotq) && same && self_shift == 0 && ctx->sym_ok;
@@ -257,6 +260,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int32_t* cnt = nullptr;
     uint32_t *ckey = nullptr, *cidx = nullptr;
     int32_t* redo = nullptr;
+    Prepared smp{};  // the pivot plans' column sample (gathered points)
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
         if (!fused && !pivot && !pivotq) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
@@ -265,6 +269,11 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             part_d = c.take<float>((size_t)S * M * k);
         }
         if (pivot || pivotq) {
+            const int64_t Sx = pivot ? Ssamp : Sq;
+            smp.hi = c.take<__half>((size_t)Sx * d_pad);
+            smp.lo = c.take<__half>((size_t)Sx * d_pad);
+            smp.sqn = c.take<float>(round_up(Sx, knn::kColPad));
+            smp.rs = c.take<float>(round_up(Sx, knn::kColPad));
             const int32_t cp = pivot ? cap : capq;
             thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
@@ -307,12 +316,14 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         // 1. sample pass: per-row minima of 32-column chunks over the first Ssamp corpus
         //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
         {
-            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, Ssamp, d_pad};
+            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Ssamp, d_pad, smp.hi, smp.lo,
+                                               smp.sqn, smp.rs, s));
+            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc_mins(op, metric, self_shift, D, ctx->pivot_margin, ctx->num_sms, s));
+            KNN_CUDA(knn::launch_dist_tc_mins(op, Ssamp, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s));
             tg.done();
             Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
-            KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, k, metric, thr, cnt, s));
+            KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, kk, metric, thr, cnt, s));
             tp.done();
         }
         // 3. partition GEMM over the whole matrix, 4. exact select of the candidates
@@ -330,9 +341,11 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         // 1. sample: single-product upper bounds of the rows against the first Sq columns
         //    (the self pair +inf), 2. pivots, 3. partition GEMM, 4. exact select (k > 32)
         {
-            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, Sq, d_pad};
+            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Sq, d_pad, smp.hi, smp.lo,
+                                               smp.sqn, smp.rs, s));
+            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, smp.hi, smp.lo, smp.sqn, smp.rs, Sq, d_pad};
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc_sample(op, metric, self_shift, D, Sq, ctx->pivot_margin, ctx->num_sms, s));
+            KNN_CUDA(knn::launch_dist_tc_sample(op, Sq, metric, KNN_NO_SELF, D, Sq, ctx->pivot_margin, ctx->num_sms, s));
             tg.done();
             KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
             KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * sizeof(int32_t), s));

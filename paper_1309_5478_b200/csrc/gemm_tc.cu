@@ -61,6 +61,9 @@ struct EpiArgs {
     // PIVOT (partition epilogue): per-row pivots in the squared domain, candidate lists
     const float* thr; int32_t* cnt; uint32_t* ckey; uint32_t* cidx; int32_t cap; int32_t* flag;
     float margin;  // MINS: error bound of the hi.hi value, relative to ||q||^2 + ||x||^2
+    // MINS / SAMPLE with a strided column sample: matrix column block nb is output column
+    // block nb / nb_stride
+    int64_t nb_stride = 1;
 };
 
 // Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
@@ -221,6 +224,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const int64_t nb = w.nb0;
             const int64_t mb = 2 * w.mp + crank;
             const int64_t n0 = nb * BN;
+            const int64_t n0_out = (nb / ep.nb_stride) * BN;  // MINS / SAMPLE output column base
             const int64_t row0 = mb * BM + quad * 32;
             const int64_t row = row0 + lane;
             const bool row_ok = row < ep.M;
@@ -301,7 +305,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         #pragma unroll
                         for (int c = 0; c < wdt; ++c) m[c] = fminf(m[c], m[c + wdt]);
                     if (row_ok && c0 < ep.N) {
-                        float* dst = ep.D + (c0 >> 5) * ep.ldD + row;  // mins[chunk][row]
+                        float* dst = ep.D + ((n0_out + cb) >> 5) * ep.ldD + row;  // mins[chunk][row]
                         float mn = m[0] == __int_as_float(0x7F800000) ? m[0] : finalize_dist<METRIC>(m[0]);
                         if (tmask == 2) mn = fminf(mn, *dst);
                         *dst = mn;
@@ -478,7 +482,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&map_d, sbuf, (int)c0, (int)row0);
+                        tma_store_2d(&map_d, sbuf, (int)(SAMPLE ? n0_out + cb : c0), (int)row0);
                         bulk_commit();
                     }
                     sbsel ^= 1;
@@ -617,10 +621,12 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t self_shift, float* mins,
+cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
                                 float margin_override, int num_sms, cudaStream_t s) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
-    if (op.N % 32 != 0) return cudaErrorInvalidValue;
+    // S sampled columns = S/256 full column blocks spread evenly over the op.N columns
+    const int64_t ns = S / BN, nfull = op.N / BN;
+    if (S % BN != 0 || ns < 1 || ns > nfull) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
     memset(&md, 0, sizeof md);
     if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
@@ -628,7 +634,7 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
         !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
-    // mins is [N/32][M]: ep.D / ep.ldD reused as its base / row stride.  Error of the single
+    // mins is [S/32][M]: ep.D / ep.ldD reused as its base / row stride.  Error of the single
     // hi.hi product (prep.cu split, |lo| <= 2^-11 |x| per component): |2 q.x - 2 qh.xh| <=
     // (2^-10 (1 + 2^-10) + d 2^-23) 2|q||x| (the d term bounds fp32 accumulation), and
     // 2|q||x| <= ||q||^2 + ||x||^2; + 2^-20 covers the roundings of both u values.
@@ -636,8 +642,8 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
                            op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin};
-    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
+    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
@@ -648,24 +654,26 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t se
     return cudaGetLastError();
 }
 
-cudaError_t launch_dist_tc_sample(const TcOperands& op, int32_t metric, int64_t self_shift, float* Ds,
+cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,
                                   int64_t ldS, float margin_override, int num_sms, cudaStream_t s) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
+    const int64_t ns = S / BN, nfull = op.N / BN;
+    if (S % BN != 0 || ns < 1 || ns > nfull) return cudaErrorInvalidValue;
     if (ldS % 4 != 0 || (reinterpret_cast<uintptr_t>(Ds) & 15) != 0) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
     if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
         !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
         !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2) ||
-        !tc_make_output_map(&md, Ds, op.M, op.N, ldS))
+        !tc_make_output_map(&md, Ds, op.M, S, ldS))
         return cudaErrorInvalidValue;
     // the same single-product error bound as the chunk-minimum sample (launch_dist_tc_mins)
     float margin = (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
                            op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, Ds, ldS,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin};
-    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
+    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_SAMPLE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_SAMPLE, TileSched> : dist_tc_kernel<0, false, MODE_SAMPLE, TileSched>;

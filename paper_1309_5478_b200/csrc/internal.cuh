@@ -39,6 +39,13 @@ cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, flo
                         float* rscale, __half* hi, __half* lo, int32_t* flag, int32_t metric,
                         cudaStream_t s);
 
+// prep.cu: the pivot plans' column sample: S points perm(j) = (j * sample_stride(N)) mod N,
+// their split operands and epilogue terms copied contiguously (column arrays padded).
+int64_t sample_stride(int64_t N);
+cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float* sqn, const float* rs,
+                                 int64_t N, int64_t S, int32_t d_pad, __half* shi, __half* slo, float* ssqn,
+                                 float* srs, cudaStream_t s);
+
 // gemm_simt.cu: FP32 FFMA distance GEMM with the fused epilogue.
 cudaError_t launch_dist_simt(const float* Q, const float* qn, int64_t M, const float* X,
                              const float* xn, int64_t N, int32_t d, int32_t metric,
@@ -64,11 +71,14 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31
 // (N a multiple of 32; self pair excluded).
-cudaError_t launch_dist_tc_mins(const TcOperands& op, int32_t metric, int64_t self_shift, float* mins,
+// The sample is S columns (a multiple of 256): S/256 full column blocks of op's N columns,
+// spread evenly over them (block j * ((N/256) / (S/256))), so that ordered data (e.g. points
+// sorted by cluster) still gives every row a representative sample.
+cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
                                 float margin_override, int num_sms, cudaStream_t s);
 // Quantile-pivot sample for k > 32: Ds[i][j] (ldS) = the single-product upper bound of u(i, j)
 // for corpus points j < op.N (self pair +inf), unclamped.
-cudaError_t launch_dist_tc_sample(const TcOperands& op, int32_t metric, int64_t self_shift, float* Ds,
+cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,
                                   int64_t ldS, float margin_override, int num_sms, cudaStream_t s);
 // select.cu: pivots = k-th smallest chunk minimum per row; exact select over candidates.
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,

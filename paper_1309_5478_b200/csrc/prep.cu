@@ -131,4 +131,61 @@ cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, flo
     return cudaGetLastError();
 }
 
+// Column sample of the pivot plans: sample column j < S is point
+// perm(j) = (j * a) mod N (a coprime to N), a deterministic permutation that spreads the
+// sample over the whole index range one point at a time, so that ordered inputs (e.g.
+// points sorted along a coordinate or by cluster) still give every row a representative
+// sample.  Copies the split operands and the per-point epilogue terms of those points;
+// the column arrays are padded to kColPad with zeros.  One warp per sample column.
+namespace {
+__global__ void __launch_bounds__(256)
+gather_sample_kernel(const __half* __restrict__ hi, const __half* __restrict__ lo,
+                     const float* __restrict__ sqn, const float* __restrict__ rs, int64_t N,
+                     int64_t S, int64_t Spad, int64_t a, int32_t d_pad, __half* __restrict__ shi,
+                     __half* __restrict__ slo, float* __restrict__ ssqn, float* __restrict__ srs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (j >= Spad) return;
+    if (j >= S) {
+        if (lane == 0) {
+            ssqn[j] = 0.0f;
+            srs[j] = 0.0f;
+        }
+        return;
+    }
+    const int64_t src = (int64_t)(((uint64_t)j * (uint64_t)a) % (uint64_t)N);
+    const uint4* h4 = reinterpret_cast<const uint4*>(hi + src * d_pad);
+    const uint4* l4 = reinterpret_cast<const uint4*>(lo + src * d_pad);
+    uint4* sh4 = reinterpret_cast<uint4*>(shi + j * d_pad);
+    uint4* sl4 = reinterpret_cast<uint4*>(slo + j * d_pad);
+    for (int t = lane; t < d_pad / 8; t += 32) {
+        sh4[t] = h4[t];
+        sl4[t] = l4[t];
+    }
+    if (lane == 0) {
+        ssqn[j] = sqn[src];
+        srs[j] = rs[src];
+    }
+}
+}  // namespace
+
+int64_t sample_stride(int64_t N) {
+    // odd, coprime to N, near N * (sqrt(5) - 1) / 2
+    int64_t a = (int64_t)((double)N * 0.6180339887498949) | 1;
+    auto gcd = [](int64_t x, int64_t y) { while (y) { const int64_t t = x % y; x = y; y = t; } return x; };
+    while (a > 1 && gcd(a, N) != 1) a -= 2;
+    return a < 1 ? 1 : a;
+}
+
+cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float* sqn, const float* rs,
+                                 int64_t N, int64_t S, int32_t d_pad, __half* shi, __half* slo, float* ssqn,
+                                 float* srs, cudaStream_t s) {
+    if (S == 0) return cudaSuccess;
+    const int64_t Spad = round_up(S, kColPad);
+    gather_sample_kernel<<<(unsigned)ceil_div(Spad, 8), 256, 0, s>>>(hi, lo, sqn, rs, N, S, Spad,
+                                                                     sample_stride(N), d_pad, shi, slo,
+                                                                     ssqn, srs);
+    return cudaGetLastError();
+}
+
 }  // namespace knn

@@ -2019,7 +2019,7 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
-    if (k > 32 || nchunk < k) return cudaErrorInvalidValue;
+    if (k > 64 || nchunk < k) return cudaErrorInvalidValue;  // k: the pivot rank (<= 32 + self)
     pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), PV_ROWS), 32 * PV_ROWS, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
     return cudaGetLastError();
 }

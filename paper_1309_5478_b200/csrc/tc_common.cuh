@@ -141,6 +141,7 @@ struct Unit {
 // Materialised GEMM: one tile per unit, groups of GROUP_M pairs sweep all column blocks.
 struct TileSched {
     int64_t n_mp, n_nb;
+    int64_t nb_stride = 1;  // column block nb of the schedule is block nb * nb_stride of the matrix
     __device__ __forceinline__ int64_t units() const { return n_mp * n_nb; }
     __device__ __forceinline__ Unit get(int64_t t) const {
         const int64_t per_group = (int64_t)GROUP_M * n_nb;
@@ -148,7 +149,7 @@ struct TileSched {
         const int64_t r = t - g * per_group;
         const int64_t m0 = g * GROUP_M;
         const int64_t gm = (n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M;
-        const int64_t nb = r / gm;
+        const int64_t nb = (r / gm) * nb_stride;
         return {m0 + r % gm, nb, nb + 1};
     }
     // Cursor: each CTA walks t = cid, cid + ncl, ... incrementally (no 64-bit divisions
@@ -176,7 +177,8 @@ struct TileSched {
         const int64_t m0 = c.g * GROUP_M;
         const uint32_t gm = (uint32_t)((n_mp - m0) < GROUP_M ? (n_mp - m0) : GROUP_M);
         const uint32_t nb = (uint32_t)c.r / gm;
-        return {m0 + ((uint32_t)c.r - nb * gm), (int64_t)nb, (int64_t)nb + 1};
+        const int64_t nbg = (int64_t)nb * nb_stride;
+        return {m0 + ((uint32_t)c.r - nb * gm), nbg, nbg + 1};
     }
 };
 

@@ -502,3 +502,22 @@ def test_quantile_pivot_certificate_failure_falls_back_exactly():
     env = dict(os.environ, KNN_PIVOT_MARGIN="-0.05")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=300)
+
+
+@pytest.mark.parametrize("k", [16, 100])
+def test_pivot_plans_on_ordered_data(k):
+    """Points sorted along a coordinate (an ordered dataset): the pivot sample is a
+    permuted column subset (prep.cu gather_sample), so the plan does not fall back to the
+    full matrix, and the graph equals the materialised plan's."""
+    kn = knn()
+    X = datagen.points(32768, 32, "clusters", seed=71)
+    X = np.ascontiguousarray(X[np.argsort(X[:, 0] + 1000 * np.round(X[:, 1]))])
+    Xt = cuda(X)
+    gi, gd = kn.graph(Xt, k)
+    assert kn.last_plan() == 3, kn.last_plan()
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(Xt, k)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
