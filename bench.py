@@ -208,7 +208,13 @@ def run_ours(args):
     X = torch.from_numpy(X_host).to(dev) if rank == 0 else torch.empty((N, d), device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
+    # k-NNG on several GPUs: the ranks split the upper triangle (Par-3, the transpose reuse
+    # survives sharding); small problems shard query rows (Par-1)
+    sym_shard = world > 1 and N >= 16384 and os.environ.get("KNN_BENCH_PAR1", "0") != "1"
+
     def step():
+        if sym_shard:
+            return sharded.graph_sym_sharded(X, k, broadcast=True)
         return sharded.graph_query_sharded(X, k, broadcast=True)
 
     def barrier():
@@ -270,9 +276,10 @@ def run_ours(args):
         avg = ms / max(n, 1)
         pairs = rows_per_launch * N
         if plan_code in (2, 3) and kernel != "dist_tc_kernel_sample":
-            # symmetric: only the upper triangle of 256x256 blocks is multiplied
+            # symmetric: only the upper triangle of 256x256 blocks is multiplied (split over
+            # the ranks by Par-3)
             nblk = -(-N // 256)
-            pairs = nblk * (nblk + 1) / 2 * 256.0 * 256.0
+            pairs = nblk * (nblk + 1) / 2 * 256.0 * 256.0 / (world if sym_shard else 1)
         flop = 3 * 2.0 * pairs * d_pad  # 3 fp16 products per multiply-add
         useful = 2.0 * rows_per_launch * N * d  # the dot products the path delivers
         r = {"kernel": name, "bound": "tensor", "achieved": flop / (avg * 1e-3) / 1e12,
@@ -430,7 +437,10 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(cfg), "N": N, "d": d, "k": k,
-                       "sharding": "query rows (Par-1): bcast X, per-rank rows, all-gather",
+                       "sharding": ("upper triangle split over the ranks (Par-3): bcast X, pivots all-gathered, "
+                                    "partition GEMM on 1/G of the 256x256 blocks, select reading the ranks' "
+                                    "candidate lists over CUDA IPC, all-gather") if sym_shard else
+                                   "query rows (Par-1): bcast X, per-rank rows, all-gather",
                        "gemm": "tcgen05 3-pass split-fp16 (FP32-accurate), fp32 accumulate",
                        "l2": "flushed before every timed step (256 MiB write, untimed)"},
             "roofline": roofline,

@@ -196,6 +196,34 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
                            int32_t k, const int64_t* offsets_host, int32_t* out_idx,
                            float* out_dist, void* stream);
 
+/* Symmetric multi-GPU k-NNG (Par-3): the pivot plan's phases, so that the
+ * ranks of a job split the UPPER TRIANGLE of the distance matrix (the transpose reuse of
+ * PAPER.md:83 survives sharding) instead of splitting rows (which doubles the per-rank
+ * multiply work).  X is the full N×d point set on every rank (device).
+ *  1. knn_graph_pivots: pivots of rows [row0, row0+rows) (the sample pass of §6.5) into
+ *     thr[row0 .. row0+rows).  The caller all-gathers thr over the ranks; thr must hold
+ *     roundup(N, 256) floats, NaN past N.  Asynchronous.
+ *  2. knn_graph_partition: the partition GEMM over the triangle units [unit_lo, unit_hi)
+ *     (knn_graph_units(N) in total), appending candidates of ANY row to the caller's lists
+ *     cnt[N] (zeroed here), ckey/cidx[N][cap].  Asynchronous.
+ *  3. knn_graph_gather_select: for rows [row0, row0+rows), concatenates the G ranks' lists
+ *     (host arrays of G device pointers; peers' lists mapped with knn_ipc_open, read over
+ *     NVLink inside the kernel) and runs the exact candidate select into out (rows×k).
+ *     Blocking; returns KNN_ERR_INTERNAL when a list overflowed or a row's certificate
+ *     failed (fewer than k candidates): the caller then falls back to another plan.
+ * k <= N-1; N >= 16384 and 1 <= k <= 1024 (else KNN_ERR_UNSUPPORTED); tensor-core path. */
+int64_t knn_graph_units(int64_t N);
+int32_t knn_graph_list_cap(int32_t k);
+knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric,
+                            int64_t row0, int64_t rows, float* thr, void* stream);
+knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
+                               int32_t metric, const float* thr, int64_t unit_lo, int64_t unit_hi,
+                               int32_t* cnt, uint32_t* ckey, uint32_t* cidx, int32_t cap, void* stream);
+knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* const* cnts,
+                                   const uint32_t* const* ckeys, const uint32_t* const* cidxs,
+                                   int32_t cap, int64_t N, int32_t k, int64_t row0, int64_t rows,
+                                   int32_t* out_idx, float* out_dist, void* stream);
+
 /* CUDA IPC plumbing for knn_merge_lists across processes (one process per GPU):
  * knn_ipc_export writes the 64-byte IPC handle of the allocation holding dev_ptr and the
  * byte offset of dev_ptr inside it; a peer process passes both to knn_ipc_open, which maps

@@ -901,6 +901,166 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
     return KNN_OK;
 }
 
+int64_t knn_graph_units(int64_t N) {
+    const int64_t n = knn::ceil_div(N, 256);
+    return n * (n + 1) / 2;
+}
+
+int32_t knn_graph_list_cap(int32_t k) {
+    return k <= 32 ? 2048 : (int32_t)round_up(3 * (int64_t)k > 2048 ? 3 * (int64_t)k : 2048, 256);
+}
+
+namespace {
+knn_status graph_shard_check(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric) {
+    if (!ctx || !X) return KNN_ERR_ARG;
+    if (N < 2 || d < 1 || k < 1 || k > N - 1) return fail(ctx, KNN_ERR_ARG, "bad N, d or k");
+    if (N > INT32_MAX) return fail(ctx, KNN_ERR_ARG, "N must be < 2^31");
+    if (k > KNN_MAX_K || N < 16384) return fail(ctx, KNN_ERR_UNSUPPORTED, "needs N >= 16384, k <= 1024");
+    if (!(ctx->gemm_mode == 0 && ctx->tc_ok)) return fail(ctx, KNN_ERR_UNSUPPORTED, "needs the tensor-core path");
+    knn_status st;
+    if (!metric_ok(ctx, metric, &st)) return st;
+    return KNN_OK;
+}
+}  // namespace
+
+knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric,
+                            int64_t row0, int64_t rows, float* thr, void* stream) {
+    KNN_TRY(graph_shard_check(ctx, X, N, d, k, metric));
+    if (row0 < 0 || rows < 0 || row0 + rows > N || !thr) return fail(ctx, KNN_ERR_ARG, "bad row range");
+    if (rows == 0) return KNN_OK;
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    const int32_t kk = k + 1;  // the sample may hold the row's own point
+    const bool small = k <= 32;
+    const int64_t S = small ? round_up(N / ctx->pivot_div, 256)
+                            : round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
+    if (small && S / 32 < kk + 1) return fail(ctx, KNN_ERR_UNSUPPORTED, "sample too small for k");
+    Prepared px{}, smp{};
+    float* D = nullptr;
+    int32_t *flag = nullptr, *cnt = nullptr;
+    auto layout = [&](Carve& c) {
+        flag = c.take<int32_t>(4);
+        px.sqn = c.take<float>(round_up(N, knn::kColPad));
+        px.rs = c.take<float>(round_up(N, knn::kColPad));
+        px.hi = c.take<__half>((size_t)N * d_pad);
+        px.lo = c.take<__half>((size_t)N * d_pad);
+        smp.sqn = c.take<float>(round_up(S, knn::kColPad));
+        smp.rs = c.take<float>(round_up(S, knn::kColPad));
+        smp.hi = c.take<__half>((size_t)S * d_pad);
+        smp.lo = c.take<__half>((size_t)S * d_pad);
+        D = c.take<float>(small ? (size_t)(S / 32) * rows : (size_t)S * rows);
+        cnt = c.take<int32_t>(rows);
+    };
+    Carve probe{nullptr};
+    layout(probe);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve);
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
+        t.done();
+    }
+    KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo, smp.sqn,
+                                       smp.rs, s));
+    knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, px.sqn + row0, px.rs + row0, rows,
+                       smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
+    Timed tg(ctx, KNN_KERNEL_GEMM, s);
+    if (small)
+        KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s));
+    else
+        KNN_CUDA(knn::launch_dist_tc_sample(op, S, metric, KNN_NO_SELF, D, S, ctx->pivot_margin, ctx->num_sms, s));
+    tg.done();
+    Timed tp(ctx, KNN_KERNEL_SELECT, s);
+    if (small) {
+        KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, rows, kk, metric, thr + row0, cnt, s));
+    } else {
+        const double mu = (double)S * k / (double)N;
+        const int32_t rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0) + 1;
+        KNN_CUDA(knn::launch_pivot_from_sample(D, rows, S, S, rq, thr + row0, s));
+    }
+    tp.done();
+    return KNN_OK;
+}
+
+knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
+                               int32_t metric, const float* thr, int64_t unit_lo, int64_t unit_hi,
+                               int32_t* cnt, uint32_t* ckey, uint32_t* cidx, int32_t cap, void* stream) {
+    KNN_TRY(graph_shard_check(ctx, X, N, d, k, metric));
+    if (!thr || !cnt || !ckey || !cidx || cap < k) return fail(ctx, KNN_ERR_ARG, "bad lists");
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    Prepared px{};
+    int32_t* flag = nullptr;
+    auto layout = [&](Carve& c) {
+        flag = c.take<int32_t>(4);
+        px.sqn = c.take<float>(round_up(N, knn::kColPad));
+        px.rs = c.take<float>(round_up(N, knn::kColPad));
+        px.hi = c.take<__half>((size_t)N * d_pad);
+        px.lo = c.take<__half>((size_t)N * d_pad);
+    };
+    Carve probe{nullptr};
+    layout(probe);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve);
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)N * sizeof(int32_t), s));
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
+        t.done();
+    }
+    knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+    Timed tg(ctx, KNN_KERNEL_FUSED, s);
+    KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, 0, true, thr, cnt, ckey, cidx, cap, flag, ctx->num_sms, s,
+                                       unit_lo, unit_hi));
+    tg.done();
+    ctx->last_plan = 3;
+    return KNN_OK;
+}
+
+knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* const* cnts,
+                                   const uint32_t* const* ckeys, const uint32_t* const* cidxs,
+                                   int32_t cap, int64_t N, int32_t k, int64_t row0, int64_t rows,
+                                   int32_t* out_idx, float* out_dist, void* stream) {
+    if (!ctx) return KNN_ERR_ARG;
+    if (G < 1 || G > 64 || !cnts || !ckeys || !cidxs || cap < k || k < 1 || k > KNN_MAX_K)
+        return fail(ctx, KNN_ERR_ARG, "bad G, lists or k");
+    if (row0 < 0 || rows < 0 || row0 + rows > N) return fail(ctx, KNN_ERR_ARG, "bad row range");
+    if (rows == 0) return KNN_OK;
+    if (!out_idx || !out_dist) return fail(ctx, KNN_ERR_ARG, "null output");
+    KNN_TRY(set_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t *flag = nullptr, *cnt = nullptr;
+    uint32_t *ckey = nullptr, *cidx = nullptr;
+    auto layout = [&](Carve& c) {
+        flag = c.take<int32_t>(4);
+        cnt = c.take<int32_t>(rows);
+        ckey = c.take<uint32_t>((size_t)rows * cap);
+        cidx = c.take<uint32_t>((size_t)rows * cap);
+    };
+    Carve probe{nullptr};
+    layout(probe);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve);
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    Timed tm(ctx, KNN_KERNEL_MERGE, s);
+    KNN_CUDA(knn::launch_gather_lists(cnts, ckeys, cidxs, G, cap, row0, rows, cap, cnt, ckey, cidx, flag, s));
+    if (k <= 32)
+        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, s));
+    else
+        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, s));
+    tm.done();
+    knn_status st = finish_blocking(ctx, s);
+    drain_profile(ctx);
+    return st;
+}
+
 knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64], int64_t* offset) {
     if (!ctx || !dev_ptr || !handle || !offset) return KNN_ERR_ARG;
     KNN_TRY(set_device(ctx));

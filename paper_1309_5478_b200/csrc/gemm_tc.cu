@@ -686,7 +686,8 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
 
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
-                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s) {
+                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
+                                 int64_t unit_lo, int64_t unit_hi) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     if (sym && op.M != op.N) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
@@ -701,7 +702,11 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
     cudaError_t e;
     if (sym) {
         SymSched sched{ceil_div(op.N, BN)};
-        const int64_t units = sched.n * (sched.n + 1) / 2;
+        const int64_t all = sched.n * (sched.n + 1) / 2;
+        sched.u_lo = unit_lo < 0 ? 0 : unit_lo;
+        sched.u_hi = unit_hi < 0 || unit_hi > all ? all : unit_hi;
+        if (sched.u_hi <= sched.u_lo) return cudaSuccess;
+        const int64_t units = sched.u_hi - sched.u_lo;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
         auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE_PIVOT, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, true, MODE_PIVOT, SymSched> : dist_tc_kernel<0, true, MODE_PIVOT, SymSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)

@@ -66,9 +66,11 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 // Pivot (partition) plan: the GEMM keeps, per row, the elements at or below thr[row]
 // (squared domain) as candidates ckey/cidx[row*cap + i], i < cnt[row]; SYM also records
 // the transposed element for the column's row.  flag |= 2 on candidate overflow.
+// unit_lo / unit_hi (sym only): the triangle's units [unit_lo, unit_hi); -1 = all.
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
-                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
+                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
+                                 int64_t unit_lo = -1, int64_t unit_hi = -1);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31
 // (N a multiple of 32; self pair excluded).
 // The sample is S columns (a multiple of 256): S/256 full column blocks of op's N columns,
@@ -94,6 +96,11 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                           int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
+// Multi-GPU symmetric k-NNG: concatenate G (possibly peer-mapped) candidate lists per row.
+cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* const* keys, const uint32_t* const* idxs,
+                                int32_t G, int32_t cap_src, int64_t row0, int64_t rows, int32_t cap_dst,
+                                int32_t* cnt_dst, uint32_t* key_dst, uint32_t* idx_dst, int32_t* flag,
+                                cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
 // fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial

@@ -1839,6 +1839,50 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
     }
 }
 
+// ------------------------------------------------------------ multi-GPU gather -------
+// Symmetric multi-GPU k-NNG: the G ranks' partial candidate lists of rows [row0, row0+rows)
+// (list g may live in a peer GPU's memory, mapped with CUDA IPC: the reads cross NVLink)
+// are concatenated into one local list per row.  Warp per row.  A source list that
+// overflowed (cnt > cap_src) or a row whose concatenation exceeds cap_dst sets flag bit 2.
+struct SrcLists {
+    const int32_t* cnt[64];
+    const uint32_t* key[64];
+    const uint32_t* idx[64];
+};
+__global__ void __launch_bounds__(256)
+gather_lists_kernel(const SrcLists src, int G, int cap_src, int64_t row0, int64_t rows, int cap_dst,
+                    int32_t* __restrict__ cnt_dst, uint32_t* __restrict__ key_dst,
+                    uint32_t* __restrict__ idx_dst, int32_t* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const int64_t row = row0 + r;
+    int total = 0;
+    bool bad = false;
+    for (int g = 0; g < G; ++g) {
+        int n = src.cnt[g][row];
+        if (n > cap_src) {
+            bad = true;
+            n = cap_src;
+        }
+        const uint32_t* sk = src.key[g] + row * cap_src;
+        const uint32_t* si = src.idx[g] + row * cap_src;
+        for (int i = lane; i < n; i += 32) {
+            const int o = total + i;
+            if (o < cap_dst) {
+                key_dst[r * cap_dst + o] = sk[i];
+                idx_dst[r * cap_dst + o] = si[i];
+            }
+        }
+        total += n;
+    }
+    if (total > cap_dst) bad = true;
+    if (lane == 0) {
+        cnt_dst[r] = total < cap_dst ? total : cap_dst;
+        if (bad) atomicOr(flag, 2);
+    }
+}
+
 }  // namespace
 
 int g_last_select_kind = -1, g_last_select_splits = 1;
@@ -2111,6 +2155,23 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ck
     if (grid > M) grid = M;
     candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, ckey, cidx, cap, M, k, KP,
                                                                           idx_offset, out_idx, out_dist, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* const* keys, const uint32_t* const* idxs,
+                                int32_t G, int32_t cap_src, int64_t row0, int64_t rows, int32_t cap_dst,
+                                int32_t* cnt_dst, uint32_t* key_dst, uint32_t* idx_dst, int32_t* flag,
+                                cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    if (G < 1 || G > 64) return cudaErrorInvalidValue;
+    SrcLists src{};
+    for (int g = 0; g < G; ++g) {
+        src.cnt[g] = cnts[g];
+        src.key[g] = keys[g];
+        src.idx[g] = idxs[g];
+    }
+    gather_lists_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(src, G, cap_src, row0, rows, cap_dst, cnt_dst,
+                                                                    key_dst, idx_dst, flag);
     return cudaGetLastError();
 }
 

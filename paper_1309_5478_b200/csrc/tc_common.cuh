@@ -186,7 +186,10 @@ struct TileSched {
 // row by row (consecutive units share the A panel); each block is also written transposed.
 struct SymSched {
     int64_t n;  // pair blocks per side
+    // units [u_lo, u_hi) of the triangle only (the multi-GPU symmetric k-NNG splits it)
+    int64_t u_lo = 0, u_hi = INT64_MAX;
     __device__ __forceinline__ int64_t units() const { return n * (n + 1) / 2; }
+    __device__ __forceinline__ int64_t end() const { return u_hi < units() ? u_hi : units(); }
     // row m of the triangle starts at unit s(m) = m*n - m(m-1)/2: the largest m with
     // s(m) <= u is the smaller root of m^2 - (2n+1) m + 2u = 0, rounded down and corrected
     __device__ __forceinline__ int64_t start(int64_t m) const { return m * n - m * (m - 1) / 2; }
@@ -204,10 +207,12 @@ struct SymSched {
         int64_t t, m, o;
     };
     __device__ __forceinline__ Cur first(int64_t t) const {
+        t += u_lo;
+        if (t >= end()) return {t, n, 0};
         const Unit w = get(t);
         return {t, w.mp, w.nb0 - w.mp};
     }
-    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
+    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < end(); }
     __device__ __forceinline__ void next(Cur& c, int64_t step) const {
         c.t += step;
         c.o += step;

@@ -30,7 +30,8 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
            "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
-           "knn_ipc_close_all"]
+           "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_graph_pivots",
+           "knn_graph_partition", "knn_graph_gather_select"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
@@ -82,6 +83,11 @@ def load_library():
             "knn_ipc_export": (st, [p, p, p, ctypes.POINTER(ctypes.c_int64)]),
             "knn_ipc_open": (st, [p, p, i64, ctypes.POINTER(ctypes.c_void_p)]),
             "knn_ipc_close_all": (st, [p]),
+            "knn_graph_units": (i64, [i64]),
+            "knn_graph_list_cap": (i32, [i32]),
+            "knn_graph_pivots": (st, [p, p, i64, i32, i32, i32, i64, i64, p, p]),
+            "knn_graph_partition": (st, [p, p, i64, i32, i32, i32, p, i64, i64, p, p, p, i32, p]),
+            "knn_graph_gather_select": (st, [p, i32, p, p, p, i32, i64, i32, i64, i64, p, p, p]),
             "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
@@ -289,6 +295,55 @@ def merge_lists(dist_ptrs, idx_ptrs, row0, M, k, offsets=None, device=None, stre
     rc = load_library().knn_merge_lists(ctx, dl, il, G, row0, M, k, offs.ctypes.data_as(ctypes.c_void_p),
                                         ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
                                         _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def graph_units(N):
+    """Units (256x256 pair blocks) of the upper triangle of the k-NNG of N points."""
+    return int(load_library().knn_graph_units(N))
+
+
+def graph_list_cap(k):
+    return int(load_library().knn_graph_list_cap(k))
+
+
+def graph_pivots(X, k, row0, rows, thr, metric=L2SQ, stream=None):
+    """knn_graph_pivots: pivots of rows [row0, row0+rows) into thr (roundup(N,256) floats)."""
+    import torch
+    N, d = X.shape
+    ctx = context(X.device.index)
+    rc = load_library().knn_graph_pivots(ctx, _dev_ptr(X, torch.float32, "X"), N, d, k, metric, row0, rows,
+                                         _dev_ptr(thr, torch.float32, "thr"), _stream(stream))
+    _check(rc, ctx)
+
+
+def graph_partition(X, k, thr, unit_lo, unit_hi, cnt, ckey, cidx, metric=L2SQ, stream=None):
+    """knn_graph_partition: candidates of the triangle units [unit_lo, unit_hi) into the lists."""
+    import torch
+    N, d = X.shape
+    cap = ckey.shape[1]
+    ctx = context(X.device.index)
+    rc = load_library().knn_graph_partition(
+        ctx, _dev_ptr(X, torch.float32, "X"), N, d, k, metric, _dev_ptr(thr, torch.float32, "thr"),
+        unit_lo, unit_hi, _dev_ptr(cnt, torch.int32, "cnt"), ctypes.c_void_p(ckey.data_ptr()),
+        ctypes.c_void_p(cidx.data_ptr()), cap, _stream(stream))
+    _check(rc, ctx)
+
+
+def graph_gather_select(cnt_ptrs, key_ptrs, idx_ptrs, cap, N, k, row0, rows, device=None, stream=None):
+    """knn_graph_gather_select over G list sources (device pointers, local or peer-mapped).
+    Returns (idx rows×k, dist rows×k); raises KnnError(KNN_ERR_INTERNAL) on a failed
+    certificate / overflow (the caller falls back)."""
+    import torch
+    G = len(cnt_ptrs)
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = context(dev.index)
+    idx, dist = _outputs(rows, k, dev)
+    P = ctypes.c_void_p * G
+    rc = load_library().knn_graph_gather_select(ctx, G, P(*cnt_ptrs), P(*key_ptrs), P(*idx_ptrs), cap, N, k,
+                                                row0, rows, ctypes.c_void_p(idx.data_ptr()),
+                                                ctypes.c_void_p(dist.data_ptr()), _stream(stream))
     _check(rc, ctx)
     return idx, dist
 

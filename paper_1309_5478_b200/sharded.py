@@ -9,6 +9,14 @@ PAPER.md:102):
   select) on its contiguous block of ceil(N/G) query rows against all N points, and the
   M×k results are all-gathered.  The only exchanges are the input broadcast and the
   output gather; there is no collective inside the hot path.
+* ``graph_sym_sharded`` (Par-3, the default k-NNG path for N >= 16384): the ranks split
+  the UPPER TRIANGLE of the distance matrix (the transpose reuse of PAPER.md:83 survives
+  sharding; a row split would double each rank's multiply work): every rank computes the
+  pivots of its row block (the pivot plan's sample pass), the pivots are all-gathered,
+  every rank runs the partition GEMM over 1/G of the triangle's 256x256 blocks appending
+  candidates of ANY row to its own lists, and each rank's select kernel reads the G ranks'
+  lists of its row block straight from their memory (CUDA IPC over NVLink) before the
+  results are all-gathered.  Bit-identical to one GPU.
 * ``graph_corpus_sharded`` (Par-2): corpus columns are split in G contiguous blocks;
   every rank computes partial top-k lists of ALL rows against its block (global self
   exclusion and global indices via knn_search_block's self_shift / idx_offset), an
@@ -150,6 +158,114 @@ def peer_merge(part_i, part_d, k, row0, rows, group=None):
     dist.barrier(group=group)
     knn.ipc_close_all(part_i.device.index)
     return mi, md
+
+
+class _SymLists:
+    """Per-process candidate lists of the symmetric sharded k-NNG, kept across calls so
+    that their CUDA IPC mappings are exported / opened once."""
+    cache = {}
+
+    @classmethod
+    def get(cls, N, cap, device, group):
+        key = (N, cap, device.index, id(group))
+        ent = cls.cache.get(key)
+        if ent is None:
+            cnt = torch.zeros(N, dtype=torch.int32, device=device)
+            ckey = torch.empty((N, cap), dtype=torch.int32, device=device)
+            cidx = torch.empty((N, cap), dtype=torch.int32, device=device)
+            ent = {"cnt": cnt, "ckey": ckey, "cidx": cidx, "ptrs": None}
+            cls.cache[key] = ent
+        return ent
+
+
+def _peer_pointers(ent, group):
+    """Device pointers of every rank's (cnt, ckey, cidx): own ones local, peers' mapped
+    with CUDA IPC (exchanged once with all_gather_object)."""
+    from . import knn
+    if ent["ptrs"] is not None:
+        return ent["ptrs"]
+    G, r = _world(group)
+    mine = tuple(knn.ipc_export(ent[n]) for n in ("cnt", "ckey", "cidx"))
+    table = [None] * G
+    dist.all_gather_object(table, mine, group=group)
+    dev = ent["cnt"].device.index
+    ptrs = ([], [], [])
+    for g in range(G):
+        for j, name in enumerate(("cnt", "ckey", "cidx")):
+            if g == r:
+                ptrs[j].append(ent[name].data_ptr())
+            else:
+                h, off = table[g][j]
+                ptrs[j].append(knn.ipc_open(h, off, dev))
+    ent["ptrs"] = ptrs
+    return ptrs
+
+
+def graph_sym_sharded(X, k, metric=0, group=None, broadcast=True):
+    """k-NNG of X with the upper triangle of the distance matrix split over the ranks
+    (Par-3).  X: N x d fp32 on this rank's device, valid on rank 0 (broadcast here unless
+    broadcast=False).  Returns the full (idx N x k, dist N x k) on every rank.  Falls back
+    to the query-row sharding (Par-1, materialised plan) if any rank's certificate fails."""
+    from . import knn
+    G, r = _world(group)
+    N, d = X.shape
+    if broadcast and G > 1:
+        broadcast_points(X, group)
+    per = -(-N // G)
+    lo, hi = block_range(N, G, r)
+    npad = -(-N // 256) * 256
+    thr = torch.full((max(npad, G * per),), float("nan"), dtype=torch.float32, device=X.device)
+    if hi > lo:
+        knn.graph_pivots(X, k, lo, hi - lo, thr, metric=metric)
+    if G > 1:
+        blk = thr[r * per:(r + 1) * per].clone()
+        gathered = torch.empty(G * per, dtype=torch.float32, device=X.device)
+        if X.is_cuda and dist.get_backend(group) != "nccl":
+            host = torch.empty(G * per, dtype=torch.float32)
+            dist.all_gather_into_tensor(host, blk.cpu(), group=group)
+            gathered.copy_(host)
+        else:
+            dist.all_gather_into_tensor(gathered, blk, group=group)
+        thr[:G * per] = gathered
+        thr[N:] = float("nan")
+    units = knn.graph_units(N)
+    u_lo, u_hi = block_range(units, G, r)
+    cap = knn.graph_list_cap(k)
+    ent = _SymLists.get(N, cap, X.device, group)
+    knn.graph_partition(X, k, thr, u_lo, u_hi, ent["cnt"], ent["ckey"], ent["cidx"], metric=metric)
+    if G > 1:
+        ptrs = _peer_pointers(ent, group)
+        torch.cuda.synchronize(X.device)
+        dist.barrier(group=group)
+    else:
+        ptrs = ([ent["cnt"].data_ptr()], [ent["ckey"].data_ptr()], [ent["cidx"].data_ptr()])
+    ok = True
+    out_i = torch.zeros((per, k), dtype=torch.int32, device=X.device)
+    out_d = torch.full((per, k), float("inf"), dtype=torch.float32, device=X.device)
+    if hi > lo:
+        try:
+            i, dd = knn.graph_gather_select(ptrs[0], ptrs[1], ptrs[2], cap, N, k, lo, hi - lo,
+                                            device=X.device.index)
+            out_i[: hi - lo] = i
+            out_d[: hi - lo] = dd
+        except knn.KnnError as e:
+            if e.status != 7:  # KNN_ERR_INTERNAL: certificate / overflow
+                raise
+            ok = False
+    if G == 1:
+        if not ok:
+            return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
+        return out_i[:N], out_d[:N]
+    torch.cuda.synchronize(X.device)
+    nccl = dist.get_backend(group) == "nccl"
+    flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=X.device if nccl else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)  # any rank's certificate failed?
+    dist.barrier(group=group)  # peers done reading this rank's lists
+    if int(flag.item()):
+        return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
+    all_i = _all_gather_rows(out_i, G, group)
+    all_d = _all_gather_rows(out_d, G, group)
+    return all_i[:N], all_d[:N]
 
 
 def graph_corpus_sharded(X, k, metric=0, group=None, compute=None, merge=None, broadcast=True,
