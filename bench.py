@@ -196,10 +196,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # KNN_BENCH_SHARE_GPU=1 (testing the multi-rank flow on a one-GPU box): every rank on
+    # cuda:0, gloo for the host-side collectives; never used for a reported number
+    share = os.environ.get("KNN_BENCH_SHARE_GPU", "0") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = get_config(args.config)
     if cfg.mode != "graph":
         raise SystemExit("bench.py times the k-NNG workloads (H, C1, C2, C4, C5)")
