@@ -497,6 +497,7 @@ __device__ bool block_finish_bucket(const uint32_t* ckey, const uint32_t* cidx, 
         }
         csync<THREADS>();
     }
+    if (out_idx == nullptr) return true;  // caller takes the sorted k from kkey / kidx
     for (int r = tid; r < k; r += THREADS) {
         out_idx[r] = (int32_t)((int64_t)kidx[r] + idx_offset);
         out_dist[r] = ukey_to_float(kkey[r]);
@@ -1049,7 +1050,7 @@ select_cluster_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k
     __shared__ int s_count;
     __shared__ int s_redo;
     const RingSmem r = ring_smem<CTHREADS, CHUNK, STAGES>(smem_raw, cap, KP, &sc, &s_count);
-    uint64_t* lst = reinterpret_cast<uint64_t*>(r.hist + 256);  // KP, 8-byte aligned
+    uint64_t* lst = reinterpret_cast<uint64_t*>(r.hist + BBINS);  // KP, 8-byte aligned
     uint64_t* bbuf = lst + KP;
     uint64_t* obuf = bbuf + KP;
     const int S = (int)cluster.num_blocks();
@@ -1077,6 +1078,11 @@ select_cluster_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k
         if (redo) ring_consume_row<CTHREADS, CHUNK, STAGES>(r, Ns, k, limit, false, 0, stage, phase);
         const int cnt = Ns > 0 ? s_count : 0;
         // exact min(k, cnt) best, sorted, as packed pairs with the row's column index
+        if (cnt > k && KP >= 64 &&
+            block_finish_bucket<CTHREADS>(r.ckey, r.cidx, cnt, k, r.kkey, r.kidx, r.hist, &sc, 0, nullptr, nullptr)) {
+            for (int q = tid; q < KP; q += CTHREADS)
+                lst[q] = q < k ? ((uint64_t)r.kkey[q] << 32 | r.kidx[q]) + (uint64_t)c0 : ~0ull;
+        } else {
         if (cnt > k) {
             uint32_t tk, ti;
             block_select_k<CTHREADS>(r.ckey, r.cidx, cnt, k, r.kkey, r.kidx, r.hist, &sc, false, tk, ti);
@@ -1093,6 +1099,7 @@ select_cluster_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k
         csync<CTHREADS>();
         block_sort_kp<CTHREADS>(r.kkey, r.kidx, KP, reinterpret_cast<uint64_t*>(r.ckey),
                                 [&](int q, uint64_t v) { lst[q] = v == ~0ull ? v : v + (uint64_t)c0; });
+        }
     }
     cluster.sync();
     for (int l = 1; l < S; l <<= 1) {
@@ -1953,7 +1960,7 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
                 if (r < 0.75 * k) r_pivot = (int)r;
             }
             const size_t smem = (size_t)STAGES * CHUNK * 4 + 2 * STAGES * 8 +
-                                (size_t)(2 * cap + 2 * KP + 256) * sizeof(uint32_t) + 3 * (size_t)KP * 8;
+                                (size_t)(2 * cap + 2 * KP + BBINS) * sizeof(uint32_t) + 3 * (size_t)KP * 8;
             auto kern = select_cluster_kernel<CT, CHUNK, STAGES>;
             if ((e = set_smem(kern, smem)) != cudaSuccess) return e;
             if (S > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
