@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -514,6 +515,19 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
 
+// Rows per group of the symmetric schedule (SymSched::gm): group-major once the split
+// operands (hi + lo, 4 bytes per coordinate) outgrow ~2/3 of the 126 MB L2, row-major below
+// (measured: N = 65536, d = 256 (64 MB): row-major 2.70 vs 2.77 ms; C4 (128 MB): 2.67 ->
+// 2.42 ms with 16 rows; C5 (128 MB): 11.6 -> 11.1 ms).  Env KNN_SYM_GROUP overrides.
+int64_t sym_group_rows(int64_t N, int32_t d_pad) {
+    static const int64_t env = [] {
+        const char* v = getenv("KNN_SYM_GROUP");
+        return v ? (int64_t)atoi(v) : (int64_t)-1;
+    }();
+    if (env >= 0) return env;
+    return (double)N * d_pad * 4.0 > 80e6 ? 16 : 0;
+}
+
 void init_encode() {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -609,6 +623,7 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
         !tc_make_output_map(&md, D, op.N, op.N, ldD))
         return cudaErrorInvalidValue;
     SymSched sched{ceil_div(op.N, BN)};
+    sched.gm = sym_group_rows(op.N, op.d_pad);
     const int64_t units = sched.n * (sched.n + 1) / 2;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD,
@@ -702,6 +717,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
     cudaError_t e;
     if (sym) {
         SymSched sched{ceil_div(op.N, BN)};
+        sched.gm = sym_group_rows(op.N, op.d_pad);
         const int64_t all = sched.n * (sched.n + 1) / 2;
         sched.u_lo = unit_lo < 0 ? 0 : unit_lo;
         sched.u_hi = unit_hi < 0 || unit_hi > all ? all : unit_hi;

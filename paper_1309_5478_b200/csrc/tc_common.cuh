@@ -182,12 +182,17 @@ struct TileSched {
     }
 };
 
-// Symmetric k-NNG (queries = corpus): the upper triangle of 256x256 pair blocks, nb >= mp,
-// row by row (consecutive units share the A panel); each block is also written transposed.
+// Symmetric k-NNG (queries = corpus): the upper triangle of 256x256 pair blocks, nb >= mp;
+// each block is also written transposed.  Unit order: gm == 0, row by row (consecutive
+// units share the A panel); gm > 0, GROUP-MAJOR: groups of gm triangle rows [m0, m0+gm)
+// sweep the column blocks nb >= m0, the rows of the group that reach nb taking column nb in
+// turn, so every B block is used by up to gm row blocks while it is L2-resident (operand
+// sets larger than L2: C4 / C5 re-read B from HBM for every triangle row otherwise).
 struct SymSched {
     int64_t n;  // pair blocks per side
     // units [u_lo, u_hi) of the triangle only (the multi-GPU symmetric k-NNG splits it)
     int64_t u_lo = 0, u_hi = INT64_MAX;
+    int64_t gm = 0;  // rows per group (0: row-major)
     __device__ __forceinline__ int64_t units() const { return n * (n + 1) / 2; }
     __device__ __forceinline__ int64_t end() const { return u_hi < units() ? u_hi : units(); }
     // row m of the triangle starts at unit s(m) = m*n - m(m-1)/2: the largest m with
@@ -202,26 +207,65 @@ struct SymSched {
         const int64_t nb = m + (u - start(m));
         return {m, nb, nb + 1};
     }
-    // Cursor: row m of the triangle, offset o inside it (row m holds n - m units)
+    // group g: rows [g gm, min(n, g gm + gm)); its units: the triangle part (columns below
+    // the group's last row) then gr units per column
+    __device__ __forceinline__ int64_t gsize(int64_t g) const {
+        const int64_t m0 = g * gm, gr = (n - m0) < gm ? (n - m0) : gm;
+        return gr * (gr - 1) / 2 + (n - (m0 + gr - 1)) * gr;
+    }
+    // Cursor: row-major (m, o) or group-major (g, o = unit index inside the group, sz)
     struct Cur {
-        int64_t t, m, o;
+        int64_t t, m, o, sz;
     };
     __device__ __forceinline__ Cur first(int64_t t) const {
         t += u_lo;
-        if (t >= end()) return {t, n, 0};
+        if (t >= end()) return {t, n, 0, 0};
+        if (gm > 0) {
+            int64_t g = 0, o = t, sz = gsize(0);
+            while (o >= sz) {
+                o -= sz;
+                sz = gsize(++g);
+            }
+            return {t, g, o, sz};
+        }
         const Unit w = get(t);
-        return {t, w.mp, w.nb0 - w.mp};
+        return {t, w.mp, w.nb0 - w.mp, 0};
     }
     __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < end(); }
     __device__ __forceinline__ void next(Cur& c, int64_t step) const {
         c.t += step;
         c.o += step;
+        if (gm > 0) {
+            while (c.t < end() && c.o >= c.sz) {
+                c.o -= c.sz;
+                c.sz = gsize(++c.m);
+            }
+            return;
+        }
         while (c.m < n && c.o >= n - c.m) {
             c.o -= n - c.m;
             ++c.m;
         }
     }
-    __device__ __forceinline__ Unit unit(const Cur& c) const { return {c.m, c.m + c.o, c.m + c.o + 1}; }
+    __device__ __forceinline__ Unit unit(const Cur& c) const {
+        if (gm > 0) {
+            const int64_t m0 = c.m * gm, gr = (n - m0) < gm ? (n - m0) : gm;
+            const int64_t tri = gr * (gr - 1) / 2;
+            int64_t nb, m;
+            if (c.o < tri) {  // column m0 + a holds rows m0 .. m0 + a
+                int64_t a = 0;
+                while ((a + 1) * (a + 2) / 2 <= c.o) ++a;
+                nb = m0 + a;
+                m = m0 + (c.o - a * (a + 1) / 2);
+            } else {
+                const int64_t v = c.o - tri;
+                nb = m0 + gr - 1 + v / gr;
+                m = m0 + v % gr;
+            }
+            return {m, nb, nb + 1};
+        }
+        return {c.m, c.m + c.o, c.m + c.o + 1};
+    }
 };
 
 // Fused GEMM+select: a unit is a row-block pair against one of S column splits; units of
