@@ -1833,9 +1833,25 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
             if (threadIdx.x == 0) atomicOr(flag, 2);
             continue;
         }
-        for (int i = threadIdx.x; i < n; i += CS_THREADS) {
-            ckey[i] = ckey_g[row * cap + i];
-            cidx[i] = cidx_g[row * cap + i];
+        // all of this thread's loads in flight before the shared-memory stores
+        const uint32_t* gk = ckey_g + row * cap;
+        const uint32_t* gi = cidx_g + row * cap;
+        for (int i0 = 0; i0 < n; i0 += 8 * CS_THREADS) {
+            uint32_t kv[8], iv[8];
+            #pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * CS_THREADS + threadIdx.x;
+                kv[u] = i < n ? __ldcs(gk + i) : 0u;
+                iv[u] = i < n ? __ldcs(gi + i) : 0u;
+            }
+            #pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * CS_THREADS + threadIdx.x;
+                if (i < n) {
+                    ckey[i] = kv[u];
+                    cidx[i] = iv[u];
+                }
+            }
         }
         __syncthreads();
         if (!block_finish_bucket<CS_THREADS, CS_BINS>(ckey, cidx, n, k, kkey, kidx, hist, &sc, idx_offset,
