@@ -30,7 +30,7 @@ METRIC = "k-NNG points/sec at N=65536,d=256,k=32 (1/2/4/8 B200); select GB/s; GE
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=150)  # ~0.5 s timed: enough nvidia-smi clock samples
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="H", help="H (headline) or C1..C5")
