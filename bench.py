@@ -122,21 +122,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle ------
-def oracle_rows_per_s(X, k, graph, target_s, threads):
-    """Time the oracle (as it stands) on a bounded sample of query rows."""
+def oracle_rows_per_s(X, k, graph, target_s, threads, Q=None):
+    """Time the oracle (as it stands) on a bounded sample of query rows (of Q, default X)."""
     import numpy as np
     import oracle
-    N = X.shape[0]
+    Q = X if Q is None else Q
+    N = Q.shape[0]
     g = np.random.Generator(np.random.Philox(4242))
     rows = g.choice(N, size=min(N, threads), replace=False)
     t0 = time.perf_counter()
-    oracle.knn(X, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
+    oracle.knn(Q, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
     t1 = time.perf_counter() - t0
     R = int(min(N, max(len(rows), len(rows) * target_s / max(t1, 1e-3))))
     R = max(threads, (R // threads) * threads)
     rows = g.choice(N, size=min(N, R), replace=False)
     t0 = time.perf_counter()
-    oracle.knn(X, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
+    oracle.knn(Q, X, k, rows=rows, graph=graph, threads=threads, want_r32=False)
     dt = time.perf_counter() - t0
     return len(rows) / dt, len(rows), dt
 
@@ -209,18 +210,22 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=dev)
     cfg = get_config(args.config)
-    if cfg.mode != "graph":
-        raise SystemExit("bench.py times the k-NNG workloads (H, C1, C2, C4, C5)")
+    search = cfg.mode != "graph"  # C3: k-NN search of M queries against N corpus points
     N, d, k = cfg.N, cfg.d, cfg.k
+    M = cfg.M if search else N  # rows (queries) of the job
     X_host = datagen.points(N, d, cfg.dist, cfg.seed) if rank == 0 else None
     X = torch.from_numpy(X_host).to(dev) if rank == 0 else torch.empty((N, d), device=dev)
+    Q_host = (datagen.points(M, d, cfg.dist, cfg.seed + 1000) if rank == 0 else None) if search else X_host
+    Q = (torch.from_numpy(Q_host).to(dev) if rank == 0 else torch.empty((M, d), device=dev)) if search else X
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
     # k-NNG on several GPUs: the ranks split the upper triangle (Par-3, the transpose reuse
     # survives sharding); small problems shard query rows (Par-1)
-    sym_shard = world > 1 and N >= 16384 and os.environ.get("KNN_BENCH_PAR1", "0") != "1"
+    sym_shard = not search and world > 1 and N >= 16384 and os.environ.get("KNN_BENCH_PAR1", "0") != "1"
 
     def step():
+        if search:
+            return sharded.search_query_sharded(Q, X, k, broadcast=True)
         if sym_shard:
             return sharded.graph_sym_sharded(X, k, broadcast=True)
         return sharded.graph_query_sharded(X, k, broadcast=True)
@@ -265,11 +270,11 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = N / (ms_per_step / 1e3)
+    value = M / (ms_per_step / 1e3)  # points (query rows) per second, whole job
 
     # ---- roofline of the dominant kernel (per-launch averages over the timed region)
     peaks = load_peaks()
-    lo_r, hi_r = sharded.block_range(N, world, rank)
+    lo_r, hi_r = sharded.block_range(M, world, rank)
     R_local = hi_r - lo_r
     d_pad = -(-d // 64) * 64
     try:
@@ -401,7 +406,7 @@ def run_ours(args):
     # ---- e2e: the public host-buffer API, H2D of the inputs and D2H of the results inside
     e2e = None
     if not args.no_e2e:
-        lo, hi = sharded.block_range(N, world, rank)
+        lo, hi = sharded.block_range(M, world, rank)
         Xh = torch.empty((N, d), dtype=torch.float32, pin_memory=True)
         if rank == 0:
             Xh.copy_(torch.from_numpy(X_host))
@@ -410,10 +415,15 @@ def run_ours(args):
         Xn = Xh.numpy()
         oi = torch.empty((hi - lo, k), dtype=torch.int32, pin_memory=True).numpy()
         od = torch.empty((hi - lo, k), dtype=torch.float32, pin_memory=True).numpy()
-        Qn = Xn[lo:hi]
+        if search:
+            Qh = torch.empty((hi - lo, d), dtype=torch.float32, pin_memory=True)
+            Qh.copy_(torch.from_numpy(Q_host[lo:hi]) if rank == 0 else Q[lo:hi].cpu())
+            Qn = Qh.numpy()
+        else:
+            Qn = Xn[lo:hi]
 
         def e2e_step():
-            knn.search_block_host(Qn, Xn, k, self_shift=lo, out=(oi, od))
+            knn.search_block_host(Qn, Xn, k, self_shift=knn.NO_SELF if search else lo, out=(oi, od))
 
         for _ in range(2):
             e2e_step()
@@ -430,17 +440,19 @@ def run_ours(args):
         te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": N / (float(te.item()) / 1e3), "unit": "points/s",
-               "h2d_bytes_per_step": int(N * d * 4), "d2h_bytes_per_step": int((hi - lo) * k * 8),
+        e2e = {"value": M / (float(te.item()) / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": int((N + (hi - lo if search else 0)) * d * 4),
+               "d2h_bytes_per_step": int((hi - lo) * k * 8),
                "api": "knn_search_block_host (pinned host buffers)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         threads = oracle.default_threads()
-        rps, R, dt = oracle_rows_per_s(X_host, k, True, args.cpu_seconds, threads)
+        rps, R, dt = oracle_rows_per_s(X_host, k, not search, args.cpu_seconds, threads,
+                                       Q=Q_host if search else None)
         cpu = {"value": rps, "unit": "points/s", "cores": threads, "kind": "oracle",
-               "sample": f"{R} seeded query rows of the N={N} k-NNG ({dt:.1f} s; fp64 direct "
+               "sample": f"{R} seeded query rows of the {workload_name(cfg)} ({dt:.1f} s; fp64 direct "
                          f"distances + full std::sort per row)"}
 
     if rank == 0:
@@ -449,7 +461,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "N": N, "d": d, "k": k,
+            "config": {"workload": workload_name(cfg), "N": N, "M": M, "d": d, "k": k,
                        "sharding": ("upper triangle split over the ranks (Par-3): bcast X, pivots all-gathered, "
                                     "partition GEMM on 1/G of the 256x256 blocks, select reading the ranks' "
                                     "candidate lists over CUDA IPC, all-gather") if sym_shard else
