@@ -1,7 +1,7 @@
 # Build libknn.so (sm_100a) and the CPU oracle.  `make` or __graft_entry__.build().
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall \
+NVFLAGS   := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall $(NVFLAGS_EXTRA) \
              -Xptxas -v --expt-relaxed-constexpr
 SRC_DIR   := paper_1309_5478_b200/csrc
 BUILD     := build

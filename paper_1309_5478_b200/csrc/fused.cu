@@ -78,7 +78,11 @@ knn_fused_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_consta
                                    crank, cid, ncl, a.self_shift);
         __syncwarp();
     } else if (warp == 1) {
+#ifdef KNN_MMA_CONVERGED
+        mma_loop<FSTAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, a.self_shift);
+#else
         if (lane == 0) mma_loop<FSTAGES>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, a.self_shift);
+#endif
         __syncwarp();
     } else {
         // -------------------------------------------------------- epilogue -----------

@@ -183,8 +183,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                                                 num_kb, crank, cid, ncl, ml_shift);
         __syncwarp();
     } else if (warp == 1) {
+#ifdef KNN_MMA_CONVERGED
+        mma_loop<KSTAGES, Sched, NSEG>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
+#else
         if (lane == 0)
             mma_loop<KSTAGES, Sched, NSEG>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
+#endif
         __syncwarp();
     } else if (warp == COL_WARP) {
         // ------------------------------------------- column data of each work item --

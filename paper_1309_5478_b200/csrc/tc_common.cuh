@@ -53,10 +53,18 @@ __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* 
 }
 // Commit this CTA's prior MMAs to the mbarrier at `bar` in every CTA of ctaMask.
 __device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+#ifdef KNN_MMA_CONVERGED
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(bar), "h"(mask)
+        : "memory");
+#else
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(bar), "h"(mask)
         : "memory");
+#endif
 }
 // TMA store of a box with an L2 eviction-priority hint (evict-first for the streamed
 // distance matrix, so it does not push the reused operands out of L2).
@@ -88,9 +96,29 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     return r;
 }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
+#ifdef KNN_MMA_CONVERGED
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+                 : "memory");
+#else
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
+#endif
 }
+// KNN_MMA_CONVERGED: the whole MMA warp runs the issue loop (warp-uniform descriptors, which
+// the compiler can keep in uniform registers) and one lane, picked by elect.sync inside the
+// instruction sequence, issues each tcgen05 instruction.
+#ifdef KNN_MMA_CONVERGED
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+#else
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                        uint32_t accumulate) {
     asm volatile(
@@ -99,6 +127,7 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
+#endif
 // Shared-memory matrix descriptor, K-major, SWZ-byte swizzle (PTX ISA "Matrix
 // descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
 // [32,46) SBO>>4 = 8 rows * SWZ bytes between 8-row core-matrix groups; [46,48)
