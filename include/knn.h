@@ -234,6 +234,13 @@ knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64]
 knn_status knn_ipc_open(knn_ctx_t ctx, const uint8_t handle[64], int64_t offset, void** dev_ptr);
 knn_status knn_ipc_close_all(knn_ctx_t ctx);
 
+/* DIAGNOSTIC (not the hot path): the distance GEMM of X against itself (sym != 0: the
+ * symmetric upper-triangle schedule) with an epilogue that only drains the TMEM
+ * accumulators — the tensor-core mainloop's own rate.  Runs `reps` timed launches after one
+ * warm-up and returns the mean launch time in *ms.  Blocking. */
+knn_status knn_diag_mainloop(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t sym,
+                             int32_t reps, double* ms);
+
 /* ---------------------------------------------------------------- introspection ----
  * Number of kernel launches this ctx has issued so far (for benchmarks). */
 int64_t knn_launch_count(knn_ctx_t ctx);

@@ -1061,6 +1061,44 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     return st;
 }
 
+knn_status knn_diag_mainloop(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t sym,
+                             int32_t reps, double* ms) {
+    if (!ctx || !X || !ms || N < 1 || d < 1 || reps < 1) return KNN_ERR_ARG;
+    if (!(ctx->gemm_mode == 0 && ctx->tc_ok)) return fail(ctx, KNN_ERR_UNSUPPORTED, "needs the tensor-core path");
+    KNN_TRY(set_device(ctx));
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    Prepared px{};
+    int32_t* flag = nullptr;
+    auto layout = [&](Carve& c) {
+        flag = c.take<int32_t>(4);
+        px.sqn = c.take<float>(round_up(N, knn::kColPad));
+        px.rs = c.take<float>(round_up(N, knn::kColPad));
+        px.hi = c.take<__half>((size_t)N * d_pad);
+        px.lo = c.take<__half>((size_t)N * d_pad);
+    };
+    Carve probe{nullptr};
+    layout(probe);
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
+    Carve carve{static_cast<char*>(ctx->ws)};
+    layout(carve);
+    cudaStream_t s = nullptr;
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, 0, s));
+    knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+    KNN_CUDA(knn::launch_dist_tc_null(op, sym != 0, ctx->num_sms, s));
+    cudaEvent_t a = take_event(ctx), b = take_event(ctx);
+    KNN_CUDA(cudaEventRecord(a, s));
+    for (int i = 0; i < reps; ++i) KNN_CUDA(knn::launch_dist_tc_null(op, sym != 0, ctx->num_sms, s));
+    KNN_CUDA(cudaEventRecord(b, s));
+    KNN_CUDA(cudaEventSynchronize(b));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    ctx->ev_pool.push_back(a);
+    ctx->ev_pool.push_back(b);
+    *ms = t / reps;
+    return KNN_OK;
+}
+
 knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64], int64_t* offset) {
     if (!ctx || !dev_ptr || !handle || !offset) return KNN_ERR_ARG;
     KNN_TRY(set_device(ctx));

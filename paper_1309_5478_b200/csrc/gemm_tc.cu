@@ -65,6 +65,7 @@ struct EpiArgs {
     // MINS / SAMPLE with a strided column sample: matrix column block nb is output column
     // block nb / nb_stride
     int64_t nb_stride = 1;
+    int32_t dbg = 0;  // DIAGNOSTIC (env KNN_DBG_EPI, wrong results): 1 skip column test, 2 skip appends, 4 skip both tests
 };
 
 // Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
@@ -132,7 +133,9 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
 // MODE_MINS writes, per row, the minimum distance of every 32-column chunk; MODE_SAMPLE
 // writes the single-product upper bound v >= u of every element (the quantile pivot's
 // sample for k > 32), unclamped, in the u domain.
-enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3 };
+enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL = 4 };
+// MODE_NULL (diagnostic, knn_diag_mainloop): the epilogue only drains TMEM (tcgen05.ld) and
+// frees the accumulator, so the kernel runs at the mainloop's own rate.
 
 template <int METRIC, bool SYM, int MODE, class Sched>
 __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
@@ -263,6 +266,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
                 }
+                if constexpr (MODE == MODE_NULL) {
+                    asm volatile("" ::"r"(r[0]), "r"(r[31]));  // keep the TMEM load
+                    continue;
+                }
                 const int cb = half * (BN / 2) + ch * 32;  // first column of the chunk in the tile
                 const float4* cn4 = reinterpret_cast<const float4*>(col_n + cb);
                 const float4* cs4 = reinterpret_cast<const float4*>(col_s + cb);
@@ -347,9 +354,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     }
                     // this row's survivors in the chunk: row side (hr) and column side (hc)
                     uint32_t hr = 0, hc = 0;
+                    if (ep.dbg & 4) {
+                        asm volatile("" ::"f"(v[0]), "f"(v[31]));
+                        continue;
+                    }
                     #pragma unroll
                     for (int c = 0; c < 32; ++c) hr |= (uint32_t)(v[c] <= trow) << c;
-                    if (SYM) {
+                    if (SYM && !(ep.dbg & 1)) {
                         const float4* ct4 = reinterpret_cast<const float4*>(col_t + cb);
                         #pragma unroll
                         for (int c4 = 0; c4 < 8; ++c4) {
@@ -361,6 +372,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         }
                     }
                     const uint32_t hm = hr | hc;
+                    if (ep.dbg & 2) {
+                        asm volatile("" ::"r"(hm));
+                        continue;
+                    }
                     if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
                     // stage the chunk's values (swizzled, conflict-free) so that each lane can
                     // walk its own survivors with dynamic indices
@@ -380,7 +395,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     }
                     const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
                     if (pend_n + total > PEND_CAP) {
-                        pivot_flush(ep, prow, pcol, pkey, pend_n);
+                        if (!(ep.dbg & 8)) pivot_flush(ep, prow, pcol, pkey, pend_n);
                         pend_n = 0;
                     }
                     __syncwarp();
@@ -718,6 +733,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         return cudaErrorInvalidValue;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, sym ? 0 : self_shift, nullptr, 0,
                thr, cnt, ckey, cidx, cap, flag};
+    if (const char* dv = getenv("KNN_DBG_EPI")) ep.dbg = atoi(dv);
     cudaError_t e;
     if (sym) {
         SymSched sched{ceil_div(op.N, BN)};
@@ -738,6 +754,41 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         const int64_t units = sched.n_mp * sched.n_nb;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
         auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_PIVOT, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_PIVOT, TileSched> : dist_tc_kernel<0, false, MODE_PIVOT, TileSched>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+            return e;
+        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+                                                                    sched, ep);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s) {
+    if (op.M == 0 || op.N == 0) return cudaSuccess;
+    CUtensorMap mqh, mql, mxh, mxl, md;
+    memset(&md, 0, sizeof md);
+    if (!tc_make_operand_map(&mqh, op.q_hi, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mql, op.q_lo, op.M, op.d_pad, BM) ||
+        !tc_make_operand_map(&mxh, op.x_hi, op.N, op.d_pad, BN / 2) ||
+        !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
+        return cudaErrorInvalidValue;
+    EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, 0, INT64_MIN, nullptr, 0,
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+    cudaError_t e;
+    if (sym) {
+        SymSched sched{ceil_div(op.N, BN)};
+        sched.gm = sym_group_rows(op.N, op.d_pad);
+        const int64_t units = sched.n * (sched.n + 1) / 2;
+        const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+        auto kern = dist_tc_kernel<0, true, MODE_NULL, SymSched>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+            return e;
+        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+                                                                    sched, ep);
+    } else {
+        TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
+        const int64_t units = sched.n_mp * sched.n_nb;
+        const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
+        auto kern = dist_tc_kernel<0, false, MODE_NULL, TileSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,

@@ -71,6 +71,8 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
                                  int64_t unit_lo = -1, int64_t unit_hi = -1);
+// Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
+cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31
 // (N a multiple of 32; self pair excluded).
 // The sample is S columns (a multiple of 256): S/256 full column blocks of op's N columns,

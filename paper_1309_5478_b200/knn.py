@@ -31,7 +31,7 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
            "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
            "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_graph_pivots",
-           "knn_graph_partition", "knn_graph_gather_select"]
+           "knn_graph_partition", "knn_graph_gather_select", "knn_diag_mainloop"]
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
 
@@ -84,6 +84,7 @@ def load_library():
             "knn_ipc_open": (st, [p, p, i64, ctypes.POINTER(ctypes.c_void_p)]),
             "knn_ipc_close_all": (st, [p]),
             "knn_graph_units": (i64, [i64]),
+            "knn_diag_mainloop": (st, [p, p, i64, i32, i32, i32, ctypes.POINTER(ctypes.c_double)]),
             "knn_graph_list_cap": (i32, [i32]),
             "knn_graph_pivots": (st, [p, p, i64, i32, i32, i32, i64, i64, p, p]),
             "knn_graph_partition": (st, [p, p, i64, i32, i32, i32, p, i64, i64, p, p, p, i32, p]),
@@ -346,6 +347,17 @@ def graph_gather_select(cnt_ptrs, key_ptrs, idx_ptrs, cap, N, k, row0, rows, dev
                                                 ctypes.c_void_p(dist.data_ptr()), _stream(stream))
     _check(rc, ctx)
     return idx, dist
+
+
+def diag_mainloop(X, sym=True, reps=10):
+    """DIAGNOSTIC: mean ms of the 3-product GEMM of X with a TMEM-draining null epilogue."""
+    import torch
+    N, d = X.shape
+    ctx = context(X.device.index)
+    ms = ctypes.c_double()
+    _check(load_library().knn_diag_mainloop(ctx, _dev_ptr(X, torch.float32, "X"), N, d, 1 if sym else 0, reps,
+                                            ctypes.byref(ms)), ctx)
+    return ms.value
 
 
 def ipc_export(t):
