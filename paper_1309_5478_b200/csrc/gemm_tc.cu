@@ -65,7 +65,8 @@ struct EpiArgs {
     // MINS / SAMPLE with a strided column sample: matrix column block nb is output column
     // block nb / nb_stride
     int64_t nb_stride = 1;
-    int32_t dbg = 0;  // DIAGNOSTIC (env KNN_DBG_EPI, wrong results): 1 skip column test, 2 skip appends, 4 skip both tests
+    int32_t dbg = 0;  // DIAGNOSTIC (env KNN_DBG_EPI, wrong results): 1 skip column test, 2 skip appends,
+                      // 4 skip both tests, 8 skip global flushes, 16 staging without appends
 };
 
 // Distance from the unclamped value u = ||q||^2 + ||x||^2 - 2 q.x (one rounding): the
@@ -385,6 +386,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     for (int u = 0; u < 8; ++u)
                         sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
                                v[4 * u + 2], v[4 * u + 3]);
+                    if (ep.dbg & 16) {  // DIAGNOSTIC: staging only
+                        __syncwarp();
+                        continue;
+                    }
                     // slots of this lane's entries in the warp's pending list (warp scan)
                     const int mine = __popc(hr) + __popc(hc);
                     int incl = mine;
