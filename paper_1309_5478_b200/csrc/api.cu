@@ -237,6 +237,11 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                      (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
     if (sym) rows_blk = M;
     ctx->last_plan = fused ? 1 : pivot_sym ? 3 : (pivot || pivotq) ? 4 : sym ? 2 : 0;
+    // the pivot plans' sample storage is processed in row blocks of at most d_budget bytes
+    const int64_t samp_row_bytes = pivot ? (Ssamp / 32) * 4 : pivotq ? Sq * 4 : 1;
+    int64_t samp_blk = (int64_t)(ctx->d_budget / (size_t)samp_row_bytes);
+    samp_blk = samp_blk < 256 ? 256 : (samp_blk / 256) * 256;
+    if (samp_blk > M) samp_blk = M;
 
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
         flag = c.take<int32_t>(4);
@@ -248,7 +253,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         };
         prep(px, N);
         if (same) pq = px; else prep(pq, M);
-        D = c.take<float>(pivot ? (size_t)(Ssamp / 32) * M : pivotq ? (size_t)Sq * M : (size_t)rows_blk * ldD);
+        D = c.take<float>(pivot ? (size_t)(Ssamp / 32) * samp_blk : pivotq ? (size_t)Sq * samp_blk
+                                                                        : (size_t)rows_blk * ldD);
     };
     Carve probe{nullptr};
     Prepared pq{}, px{};
@@ -318,13 +324,18 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         {
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Ssamp, d_pad, smp.hi, smp.lo,
                                                smp.sqn, smp.rs, s));
-            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
-            Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc_mins(op, Ssamp, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s));
-            tg.done();
-            Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
-            KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, M, kk, metric, thr, cnt, s));
-            tp.done();
+            for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
+                const int64_t R = M - r0 < samp_blk ? M - r0 : samp_blk;
+                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
+                                   smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
+                Timed tg(ctx, KNN_KERNEL_GEMM, s);
+                KNN_CUDA(knn::launch_dist_tc_mins(op, Ssamp, metric, KNN_NO_SELF, D, ctx->pivot_margin,
+                                                  ctx->num_sms, s));
+                tg.done();
+                Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
+                KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, kk, metric, thr + r0, cnt + r0, s));
+                tp.done();
+            }
         }
         // 3. partition GEMM over the whole matrix, 4. exact select of the candidates
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
@@ -343,15 +354,20 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         {
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Sq, d_pad, smp.hi, smp.lo,
                                                smp.sqn, smp.rs, s));
-            knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, smp.hi, smp.lo, smp.sqn, smp.rs, Sq, d_pad};
-            Timed tg(ctx, KNN_KERNEL_GEMM, s);
-            KNN_CUDA(knn::launch_dist_tc_sample(op, Sq, metric, KNN_NO_SELF, D, Sq, ctx->pivot_margin, ctx->num_sms, s));
-            tg.done();
             KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
             KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * sizeof(int32_t), s));
-            Timed tp(ctx, KNN_KERNEL_SELECT, s);
-            KNN_CUDA(knn::launch_pivot_from_sample(D, M, Sq, Sq, rq, thr, s));
-            tp.done();
+            for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
+                const int64_t R = M - r0 < samp_blk ? M - r0 : samp_blk;
+                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
+                                   smp.hi, smp.lo, smp.sqn, smp.rs, Sq, d_pad};
+                Timed tg(ctx, KNN_KERNEL_GEMM, s);
+                KNN_CUDA(knn::launch_dist_tc_sample(op, Sq, metric, KNN_NO_SELF, D, Sq, ctx->pivot_margin,
+                                                    ctx->num_sms, s));
+                tg.done();
+                Timed tp(ctx, KNN_KERNEL_SELECT, s);
+                KNN_CUDA(knn::launch_pivot_from_sample(D, R, Sq, Sq, rq, thr + r0, s));
+                tp.done();
+            }
         }
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
         Timed tg(ctx, KNN_KERNEL_FUSED, s);

@@ -521,3 +521,24 @@ def test_pivot_plans_on_ordered_data(k):
     finally:
         kn.set_plan(kn.PLAN_AUTO)
     assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+@pytest.mark.parametrize("k", [16, 80])
+def test_pivot_sample_row_blocks(k):
+    """The pivot plans' sample pass in several row blocks (a tiny KNN_D_BUDGET, as at very
+    large N) gives the same graph as one block."""
+    code = (
+        "import torch\n"
+        "from paper_1309_5478_b200 import knn, datagen\n"
+        f"X = torch.from_numpy(datagen.points(20000, 32, 'gauss', seed=81)).cuda()\n"
+        f"gi, gd = knn.graph(X, {k})\n"
+        "assert knn.last_plan() == 3, knn.last_plan()\n"
+        "torch.save((gi.cpu(), gd.cpu()), 'gpurun_out/_blk.pt')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, timeout=300,
+                   env=dict(os.environ, KNN_D_BUDGET_MB="1"))  # 1 MiB: many sample row blocks
+    bi, bd = torch.load(os.path.join(root, "gpurun_out", "_blk.pt"))
+    X = cuda(datagen.points(20000, 32, "gauss", seed=81))
+    gi, gd = knn().graph(X, k)
+    assert torch.equal(gi.cpu(), bi) and torch.equal(gd.cpu().view(torch.int32), bd.view(torch.int32))
