@@ -267,6 +267,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     uint32_t *ckey = nullptr, *cidx = nullptr;
     int32_t* redo = nullptr;
     Prepared smp{};  // the pivot plans' column sample (gathered points)
+    float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
         if (!fused && !pivot && !pivotq) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
@@ -276,6 +277,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         }
         if (pivot || pivotq) {
             const int64_t Sx = pivot ? Ssamp : Sq;
+            smax = c.take<float>(1);
             smp.hi = c.take<__half>((size_t)Sx * d_pad);
             smp.lo = c.take<__half>((size_t)Sx * d_pad);
             smp.sqn = c.take<float>(round_up(Sx, knn::kColPad));
@@ -323,14 +325,14 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
         {
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Ssamp, d_pad, smp.hi, smp.lo,
-                                               smp.sqn, smp.rs, s));
+                                               smp.sqn, smp.rs, smax, s));
             for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
                 const int64_t R = M - r0 < samp_blk ? M - r0 : samp_blk;
                 knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
                                    smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
                 Timed tg(ctx, KNN_KERNEL_GEMM, s);
                 KNN_CUDA(knn::launch_dist_tc_mins(op, Ssamp, metric, KNN_NO_SELF, D, ctx->pivot_margin,
-                                                  ctx->num_sms, s));
+                                                  ctx->num_sms, s, smax));
                 tg.done();
                 Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
                 KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, kk, metric, thr + r0, cnt + r0, s));
@@ -353,7 +355,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         //    (the self pair +inf), 2. pivots, 3. partition GEMM, 4. exact select (k > 32)
         {
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Sq, d_pad, smp.hi, smp.lo,
-                                               smp.sqn, smp.rs, s));
+                                               smp.sqn, smp.rs, nullptr, s));
             KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
             KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * sizeof(int32_t), s));
             for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
@@ -953,7 +955,7 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
                             : round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
     if (small && S / 32 < kk + 1) return fail(ctx, KNN_ERR_UNSUPPORTED, "sample too small for k");
     Prepared px{}, smp{};
-    float* D = nullptr;
+    float *D = nullptr, *smax = nullptr;
     int32_t *flag = nullptr, *cnt = nullptr;
     auto layout = [&](Carve& c) {
         flag = c.take<int32_t>(4);
@@ -967,6 +969,7 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
         smp.lo = c.take<__half>((size_t)S * d_pad);
         D = c.take<float>(small ? (size_t)(S / 32) * rows : (size_t)S * rows);
         cnt = c.take<int32_t>(rows);
+        smax = c.take<float>(1);
     };
     Carve probe{nullptr};
     layout(probe);
@@ -980,12 +983,12 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
         t.done();
     }
     KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo, smp.sqn,
-                                       smp.rs, s));
+                                       smp.rs, small ? smax : nullptr, s));
     knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, px.sqn + row0, px.rs + row0, rows,
                        smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
     Timed tg(ctx, KNN_KERNEL_GEMM, s);
     if (small)
-        KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s));
+        KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s, smax));
     else
         KNN_CUDA(knn::launch_dist_tc_sample(op, S, metric, KNN_NO_SELF, D, S, ctx->pivot_margin, ctx->num_sms, s));
     tg.done();

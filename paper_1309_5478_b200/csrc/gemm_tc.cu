@@ -65,6 +65,7 @@ struct EpiArgs {
     // MINS / SAMPLE with a strided column sample: matrix column block nb is output column
     // block nb / nb_stride
     int64_t nb_stride = 1;
+    const float* xmax = nullptr;  // MINS: upper bound of every column's sqn term (device scalar)
     int32_t dbg = 0;  // DIAGNOSTIC (env KNN_DBG_EPI, wrong results): 1 skip column test, 2 skip appends,
                       // 4 skip both tests, 8 skip global flushes, 16 staging without appends
 };
@@ -240,6 +241,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
             const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
             const float trow = PIVOT && row_ok ? __ldg(ep.thr + row) : -1.0f;  // row pivot
+            // MINS: qn (1 + m) + m XMAX, and the cosine sentinel cap 3 + m (qn + XMAX)
+            const float xmx = MINS ? __ldg(ep.xmax) : 0.0f;
+            const float mins_row_term = MINS ? fmaf(ep.margin, qn + xmx, qn) * (1.0f + 0x1p-22f) : 0.0f;
+            const float mins_cos_cap = MINS ? fmaf(ep.margin, qn + xmx, 3.0f) : 0.0f;
             const int64_t c_lo = n0 + half * (BN / 2);
             // does this warp's 32x(BN/2) block touch the excluded self pairs?
             const bool diag = ep.self_shift != INT64_MIN &&
@@ -274,6 +279,39 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 const int cb = half * (BN / 2) + ch * 32;  // first column of the chunk in the tile
                 const float4* cn4 = reinterpret_cast<const float4*>(col_n + cb);
                 const float4* cs4 = reinterpret_cast<const float4*>(col_s + cb);
+                if constexpr (MINS) {
+                    // pivot sample pass: an upper bound of the chunk's minimum distance for
+                    // this row in three operations per element.  With a_j = acc_j 2^-sh_j and
+                    // w_j = cq a_j + xn_j (cq = -2^(1-sh_q): the single-product u_j - qn),
+                    // value = min_j w_j + qn (1 + m) + m XMAX >= u_j* + m (qn + xn_j*) for the
+                    // minimising j*, i.e. >= the hi.hi value of element j* plus its error bound,
+                    // so at least one element of the chunk has an FP32-accurate u at or below
+                    // it (XMAX >= every xn_j).  No self pair: the sample is a
+                    // gathered column subset.
+                    float m[8];
+                    #pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 nn = cn4[c4];
+                        const float4 ss = cs4[c4];
+                        const float w0 = fmaf(cq, __uint_as_float(r[4 * c4]) * ss.x, nn.x);
+                        const float w1 = fmaf(cq, __uint_as_float(r[4 * c4 + 1]) * ss.y, nn.y);
+                        const float w2 = fmaf(cq, __uint_as_float(r[4 * c4 + 2]) * ss.z, nn.z);
+                        const float w3 = fmaf(cq, __uint_as_float(r[4 * c4 + 3]) * ss.w, nn.w);
+                        m[c4] = fminf(fminf(w0, w1), fminf(w2, w3));
+                    }
+                    #pragma unroll
+                    for (int wdt = 4; wdt > 0; wdt >>= 1)
+                        #pragma unroll
+                        for (int c = 0; c < wdt; ++c) m[c] = fminf(m[c], m[c + wdt]);
+                    const int64_t c0m = n0 + cb;
+                    if (row_ok && c0m < ep.N) {
+                        float val = m[0] + mins_row_term;
+                        if (METRIC == 2) val = fminf(val, mins_cos_cap);
+                        float* dst = ep.D + ((n0_out + cb) >> 5) * ep.ldD + row;  // mins[chunk][row]
+                        *dst = finalize_dist<METRIC>(val);
+                    }
+                    continue;
+                }
                 float v[32];
                 #pragma unroll
                 for (int c4 = 0; c4 < 8; ++c4) {
@@ -661,7 +699,8 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 }
 
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
-                                float margin_override, int num_sms, cudaStream_t s) {
+                                float margin_override, int num_sms, cudaStream_t s, const float* xmax) {
+    if (!xmax || self_shift != INT64_MIN) return cudaErrorInvalidValue;  // gathered samples only
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     // S sampled columns = S/256 full column blocks spread evenly over the op.N columns
     const int64_t ns = S / BN, nfull = op.N / BN;
@@ -681,7 +720,7 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
                            op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
+               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns, xmax};
     TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;

@@ -42,9 +42,10 @@ cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, flo
 // prep.cu: the pivot plans' column sample: S points perm(j) = (j * sample_stride(N)) mod N,
 // their split operands and epilogue terms copied contiguously (column arrays padded).
 int64_t sample_stride(int64_t N);
+// smax (device float, may be null): the max of the sample's sqn terms.
 cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float* sqn, const float* rs,
                                  int64_t N, int64_t S, int32_t d_pad, __half* shi, __half* slo, float* ssqn,
-                                 float* srs, cudaStream_t s);
+                                 float* srs, float* smax, cudaStream_t s);
 
 // gemm_simt.cu: FP32 FFMA distance GEMM with the fused epilogue.
 cudaError_t launch_dist_simt(const float* Q, const float* qn, int64_t M, const float* X,
@@ -78,8 +79,9 @@ cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cud
 // The sample is S columns (a multiple of 256): S/256 full column blocks of op's N columns,
 // spread evenly over them (block j * ((N/256) / (S/256))), so that ordered data (e.g. points
 // sorted by cluster) still gives every row a representative sample.
+// xmax: device pointer to an upper bound of the columns' sqn terms (the sample's max).
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
-                                float margin_override, int num_sms, cudaStream_t s);
+                                float margin_override, int num_sms, cudaStream_t s, const float* xmax);
 // Quantile-pivot sample for k > 32: Ds[i][j] (ldS) = the single-product upper bound of u(i, j)
 // for corpus points j < op.N (self pair +inf), unclamped.
 cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,

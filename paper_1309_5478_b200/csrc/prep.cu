@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(256)
 gather_sample_kernel(const __half* __restrict__ hi, const __half* __restrict__ lo,
                      const float* __restrict__ sqn, const float* __restrict__ rs, int64_t N,
                      int64_t S, int64_t Spad, int64_t a, int32_t d_pad, __half* __restrict__ shi,
-                     __half* __restrict__ slo, float* __restrict__ ssqn, float* __restrict__ srs) {
+                     __half* __restrict__ slo, float* __restrict__ ssqn, float* __restrict__ srs,
+                     float* __restrict__ smax) {
     const int lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (j >= Spad) return;
@@ -165,6 +166,9 @@ gather_sample_kernel(const __half* __restrict__ hi, const __half* __restrict__ l
     if (lane == 0) {
         ssqn[j] = sqn[src];
         srs[j] = rs[src];
+        // max of the sample's epilogue terms (>= 0: ordered as ints), for the sample pass's
+        // per-chunk error bound
+        if (smax) atomicMax(reinterpret_cast<int*>(smax), __float_as_int(fmaxf(sqn[src], 0.0f)));
     }
 }
 }  // namespace
@@ -179,12 +183,16 @@ int64_t sample_stride(int64_t N) {
 
 cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float* sqn, const float* rs,
                                  int64_t N, int64_t S, int32_t d_pad, __half* shi, __half* slo, float* ssqn,
-                                 float* srs, cudaStream_t s) {
+                                 float* srs, float* smax, cudaStream_t s) {
     if (S == 0) return cudaSuccess;
     const int64_t Spad = round_up(S, kColPad);
+    if (smax) {
+        const cudaError_t e = cudaMemsetAsync(smax, 0, sizeof(float), s);
+        if (e != cudaSuccess) return e;
+    }
     gather_sample_kernel<<<(unsigned)ceil_div(Spad, 8), 256, 0, s>>>(hi, lo, sqn, rs, N, S, Spad,
                                                                      sample_stride(N), d_pad, shi, slo,
-                                                                     ssqn, srs);
+                                                                     ssqn, srs, smax);
     return cudaGetLastError();
 }
 
