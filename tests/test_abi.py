@@ -76,3 +76,15 @@ def test_product_package_does_not_import_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "knn_oracle" not in src, f
+
+
+def test_header_is_plain_c_and_example_links(lib, tmp_path):
+    """include/knn.h compiles as C11 and examples/knn_demo.c links against libknn.so (the
+    boundary needs no C++, Python or torch types)."""
+    exe = tmp_path / "knn_demo"
+    cuda_inc = "/usr/local/cuda/include"
+    cuda_lib = "/usr/local/cuda/lib64"
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           "-I", cuda_inc, os.path.join(ROOT, "examples", "knn_demo.c"),
+                           "-L", os.path.dirname(LIB), "-lknn", "-L", cuda_lib, "-lcudart", "-o", str(exe)])
+    assert exe.exists()

@@ -542,3 +542,17 @@ def test_pivot_sample_row_blocks(k):
     X = cuda(datagen.points(20000, 32, "gauss", seed=81))
     gi, gd = knn().graph(X, k)
     assert torch.equal(gi.cpu(), bi) and torch.equal(gd.cpu().view(torch.int32), bd.view(torch.int32))
+
+
+def test_c_example_runs(tmp_path):
+    """The plain-C example (examples/knn_demo.c) runs the k-NNG through the C ABI."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "knn_demo"
+    libdir = os.path.join(root, "paper_1309_5478_b200")
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                           os.path.join(root, "examples", "knn_demo.c"), "-L", libdir, "-lknn",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart", "-o", str(exe)])
+    out = subprocess.run([str(exe), "20000", "32", "8"], capture_output=True, text=True, timeout=120,
+                         env=dict(os.environ, LD_LIBRARY_PATH=libdir + ":" + os.environ.get("LD_LIBRARY_PATH", "")))
+    assert out.returncode == 0, out.stderr
+    assert "point 0:" in out.stdout and "host-buffer API" in out.stdout
