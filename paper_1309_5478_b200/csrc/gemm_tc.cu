@@ -228,6 +228,9 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         uint32_t* pcol = prow + PEND_CAP;
         uint32_t* pkey = pcol + PEND_CAP;
         int pend_n = 0;  // warp-uniform
+        __shared__ int s_pend[EPI_WARPS];  // PIVOT: each warp's pending-list length (slot allocator)
+        if (PIVOT && lane == 0) s_pend[warp - 2] = 0;
+        __syncwarp();
         for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
             const tc::Unit w = sched.unit(cur);
             const int cls = tile_class(w.mp, w.nb0, ml_shift);
@@ -428,23 +431,20 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         __syncwarp();
                         continue;
                     }
-                    // slots of this lane's entries in the warp's pending list (warp scan)
+                    // slots of this lane's entries in the warp's pending list: the warp total
+                    // by one reduction, each lane's base by a shared atomic on the warp's
+                    // running count (order inside the list is irrelevant)
                     const int mine = __popc(hr) + __popc(hc);
-                    int incl = mine;
-                    #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    const int total = __reduce_add_sync(0xFFFFFFFFu, mine);
                     if (pend_n + total > PEND_CAP) {
                         if (!(ep.dbg & 8)) pivot_flush(ep, prow, pcol, pkey, pend_n);
                         pend_n = 0;
+                        if (lane == 0) s_pend[warp - 2] = 0;
                     }
                     __syncwarp();
                     uint32_t h = hm;
                     if (total <= PEND_CAP) {
-                        int pos = pend_n + incl - mine;
+                        int pos = mine ? atomicAdd(&s_pend[warp - 2], mine) : 0;
                         while (h) {
                             const int c = __ffs(h) - 1;
                             h &= h - 1;
