@@ -445,10 +445,14 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     uint32_t h = hm;
                     if (total <= PEND_CAP) {
                         int pos = mine ? atomicAdd(&s_pend[warp - 2], mine) : 0;
+                        // staged element c of this lane's row: 16-byte unit (c >> 2) ^ (lane & 7)
+                        // of the row, i.e. index lane * 32 + (c ^ ((lane & 7) << 2))
+                        const float* srow = svp + lane * 32;
+                        const int sx = (lane & 7) << 2;
                         while (h) {
                             const int c = __ffs(h) - 1;
                             h &= h - 1;
-                            const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
+                            const float x = srow[c ^ sx];
                             const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
                             if ((hr >> c) & 1) {
                                 prow[pos] = (uint32_t)row;
