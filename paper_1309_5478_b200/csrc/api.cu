@@ -207,12 +207,14 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     // the sample is a permuted column subset that may contain the row's own point: one
     // more rank keeps k non-self elements at or below the pivot
     const int32_t kk = self_shift != KNN_NO_SELF ? k + 1 : k;
-    const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 &&
+    // (fewer than 256 query rows fill less than one 2-CTA row-block pair: the sample pass
+    // then costs as much as it saves; measured M = 8 vs N = 2^20: 0.66 vs 0.82 ms)
+    const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 && M >= 256 &&
                        ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= kk + 1;
     // Quantile pivot for k > 32 (the same quickselect partition; the pivot is a bucketed
     // order statistic of a single-product sample of Sq columns)
     const int64_t Sq = round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
-    const bool pivotq = allow_pivot && !fused && tc && ctx->pivot_ok && k > 32 && N >= 16384 &&
+    const bool pivotq = allow_pivot && !fused && tc && ctx->pivot_ok && k > 32 && N >= 16384 && M >= 256 &&
                         ctx->plan != KNN_PLAN_MATERIALISED && Sq <= (N / 256) * 256;
     int32_t rq = 0;
     if (pivotq) {
