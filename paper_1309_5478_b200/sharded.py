@@ -31,6 +31,8 @@ the CUDA library (there is no CPU fallback in the product path).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -178,25 +180,48 @@ class _SymLists:
         return ent
 
 
+def _agree(ok, device, group):
+    """True on every rank iff `ok` holds on every rank (one MAX all-reduce)."""
+    nccl = dist.get_backend(group) == "nccl"
+    f = torch.tensor([0 if ok else 1], dtype=torch.int32, device=device if nccl else "cpu")
+    dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+    return int(f.item()) == 0
+
+
 def _peer_pointers(ent, group):
     """Device pointers of every rank's (cnt, ckey, cidx): own ones local, peers' mapped
-    with CUDA IPC (exchanged once with all_gather_object)."""
+    with CUDA IPC (exchanged once with all_gather_object).  None on every rank if any rank
+    could not export or map (e.g. an allocator without IPC support): the caller falls back
+    to a path without peer mappings."""
     from . import knn
     if ent["ptrs"] is not None:
-        return ent["ptrs"]
+        return ent["ptrs"] if ent["ptrs"] != "none" else None
     G, r = _world(group)
-    mine = tuple(knn.ipc_export(ent[n]) for n in ("cnt", "ckey", "cidx"))
+    try:
+        if os.environ.get("KNN_SHARD_NO_IPC", "0") == "1":  # tests: force the fallback
+            raise RuntimeError("CUDA IPC disabled")
+        mine = tuple(knn.ipc_export(ent[n]) for n in ("cnt", "ckey", "cidx"))
+    except Exception:
+        mine = None
     table = [None] * G
     dist.all_gather_object(table, mine, group=group)
     dev = ent["cnt"].device.index
     ptrs = ([], [], [])
-    for g in range(G):
-        for j, name in enumerate(("cnt", "ckey", "cidx")):
-            if g == r:
-                ptrs[j].append(ent[name].data_ptr())
-            else:
-                h, off = table[g][j]
-                ptrs[j].append(knn.ipc_open(h, off, dev))
+    ok = all(t is not None for t in table)
+    if ok:
+        try:
+            for g in range(G):
+                for j, name in enumerate(("cnt", "ckey", "cidx")):
+                    if g == r:
+                        ptrs[j].append(ent[name].data_ptr())
+                    else:
+                        h, off = table[g][j]
+                        ptrs[j].append(knn.ipc_open(h, off, dev))
+        except Exception:
+            ok = False
+    if not _agree(ok, ent["cnt"].device, group):
+        ent["ptrs"] = "none"
+        return None
     ent["ptrs"] = ptrs
     return ptrs
 
@@ -235,6 +260,8 @@ def graph_sym_sharded(X, k, metric=0, group=None, broadcast=True):
     knn.graph_partition(X, k, thr, u_lo, u_hi, ent["cnt"], ent["ckey"], ent["cidx"], metric=metric)
     if G > 1:
         ptrs = _peer_pointers(ent, group)
+        if ptrs is None:  # no CUDA IPC between these ranks: shard query rows instead
+            return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
         torch.cuda.synchronize(X.device)
         dist.barrier(group=group)
     else:
@@ -257,11 +284,9 @@ def graph_sym_sharded(X, k, metric=0, group=None, broadcast=True):
             return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
         return out_i[:N], out_d[:N]
     torch.cuda.synchronize(X.device)
-    nccl = dist.get_backend(group) == "nccl"
-    flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=X.device if nccl else "cpu")
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)  # any rank's certificate failed?
+    all_ok = _agree(ok, X.device, group)  # any rank's certificate failed?
     dist.barrier(group=group)  # peers done reading this rank's lists
-    if int(flag.item()):
+    if not all_ok:
         return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
     all_i = _all_gather_rows(out_i, G, group)
     all_d = _all_gather_rows(out_d, G, group)

@@ -79,9 +79,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, N, d, k, q):
+def _worker(rank, world, port, N, d, k, q, no_ipc=False):
     import torch.distributed as dist
     from paper_1309_5478_b200 import sharded
+    if no_ipc:
+        os.environ["KNN_SHARD_NO_IPC"] = "1"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -98,13 +100,15 @@ def _worker(rank, world, port, N, d, k, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("N,k", [(16384, 16), (20000, 64)])
-def test_two_processes_one_gpu(N, k):
+@pytest.mark.parametrize("N,k,no_ipc", [(16384, 16, False), (20000, 64, False), (16384, 16, True)])
+def test_two_processes_one_gpu(N, k, no_ipc):
+    """no_ipc: the ranks cannot map each other's lists; they agree on it and fall back to
+    the query-row sharding, still bit-identical."""
     d = 24
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, N, d, k, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, N, d, k, q, no_ipc)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
