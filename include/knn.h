@@ -205,7 +205,9 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
  *     roundup(N, 256) floats, NaN past N.  Asynchronous.
  *  2. knn_graph_partition: the partition GEMM over the triangle units [unit_lo, unit_hi)
  *     (knn_graph_units(N) in total), appending candidates of ANY row to the caller's lists
- *     cnt[N] (zeroed here), ckey/cidx[N][cap].  Asynchronous.
+ *     cnt[N] (zeroed here), ckey/cidx[N][cap].  Asynchronous.  Directly after
+ *     knn_graph_pivots on the same ctx, points, metric and stream it reuses the operands
+ *     that call prepared (no second pass over X).
  *  3. knn_graph_gather_select: for rows [row0, row0+rows), concatenates the G ranks' lists
  *     (host arrays of G device pointers; peers' lists mapped with knn_ipc_open, read over
  *     NVLink inside the kernel) and runs the exact candidate select into out (rows×k).

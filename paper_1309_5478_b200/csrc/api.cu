@@ -51,6 +51,11 @@ struct knn_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     double last_stream_copy_ms = 0, last_stream_total_ms = 0;
+    // knn_graph_pivots leaves the prepared operands of X at the start of ws (after the flag);
+    // knn_graph_partition on the same (X, N, d, metric) reuses them while ws is untouched
+    const float* prep_X = nullptr;
+    int64_t prep_N = 0;
+    int32_t prep_d = 0, prep_metric = -1;
     // CUDA IPC mappings opened by knn_ipc_open: handle bytes -> mapped base
     std::vector<std::pair<std::string, void*>> ipc_open;
 };
@@ -86,6 +91,7 @@ knn_status fail(knn_ctx* c, knn_status st, const char* fmt, ...) {
     } while (0)
 
 knn_status ensure(knn_ctx* ctx, void** buf, size_t* size, size_t need) {
+    if (buf == &ctx->ws) ctx->prep_X = nullptr;  // any new use of ws invalidates the kept operands
     if (need <= *size) return KNN_OK;
     if (*buf) {
         cudaError_t e = cudaDeviceSynchronize();
@@ -984,6 +990,10 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
         KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
         t.done();
     }
+    ctx->prep_X = X;  // knn_graph_partition may reuse px (same carve offsets, ws untouched)
+    ctx->prep_N = N;
+    ctx->prep_d = d;
+    ctx->prep_metric = metric;
     KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo, smp.sqn,
                                        smp.rs, small ? smax : nullptr, s));
     knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, px.sqn + row0, px.rs + row0, rows,
@@ -1025,12 +1035,17 @@ knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t
     };
     Carve probe{nullptr};
     layout(probe);
+    // the operands knn_graph_pivots prepared are still at the same offsets of ws if the
+    // last ws user was that call on the same points (ensure() does not reallocate: this
+    // call needs less workspace)
+    const bool reuse = ctx->prep_X == X && ctx->prep_N == N && ctx->prep_d == d && ctx->prep_metric == metric &&
+                       probe.off + 256 <= ctx->ws_size;
     KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve);
-    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
     KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)N * sizeof(int32_t), s));
-    {
+    if (!reuse) {
+        KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
         Timed t(ctx, KNN_KERNEL_PREP, s);
         KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
         t.done();
