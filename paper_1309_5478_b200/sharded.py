@@ -262,8 +262,14 @@ def graph_sym_sharded(X, k, metric=0, group=None, broadcast=True):
         ptrs = _peer_pointers(ent, group)
         if ptrs is None:  # no CUDA IPC between these ranks: shard query rows instead
             return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
-        torch.cuda.synchronize(X.device)
-        dist.barrier(group=group)
+        # every rank's partition must be complete before any rank reads its lists: with NCCL a
+        # stream-ordered all-reduce is that barrier on the device (no host synchronisation);
+        # host-side backends synchronise explicitly
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(torch.zeros(1, dtype=torch.int32, device=X.device), group=group)
+        else:
+            torch.cuda.synchronize(X.device)
+            dist.barrier(group=group)
     else:
         ptrs = ([ent["cnt"].data_ptr()], [ent["ckey"].data_ptr()], [ent["cidx"].data_ptr()])
     ok = True
@@ -283,9 +289,11 @@ def graph_sym_sharded(X, k, metric=0, group=None, broadcast=True):
         if not ok:
             return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
         return out_i[:N], out_d[:N]
-    torch.cuda.synchronize(X.device)
-    all_ok = _agree(ok, X.device, group)  # any rank's certificate failed?
-    dist.barrier(group=group)  # peers done reading this rank's lists
+    # any rank's certificate failed?  (every rank calls this after its select returned, so
+    # when it completes no rank still reads another's lists)
+    all_ok = _agree(ok, X.device, group)
+    if dist.get_backend(group) != "nccl":
+        dist.barrier(group=group)
     if not all_ok:
         return graph_query_sharded(X, k, metric=metric, group=group, broadcast=False)
     all_i = _all_gather_rows(out_i, G, group)
