@@ -1807,6 +1807,90 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
     }
 }
 
+// Warp-per-row form of the same pivot (no CTA barriers; rows re-read from L2): pass 1 the
+// row's finite min / max, pass 2 a warp-private 1024-bucket histogram, a warp scan for the
+// bucket b* holding the r-th sample, pass 3 the largest sample in buckets <= b*.
+constexpr int QPW_WARPS = 8;
+__global__ void __launch_bounds__(32 * QPW_WARPS)
+pivot_from_sample_warp_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int64_t ldS, int r,
+                              float* __restrict__ thr) {
+    __shared__ uint32_t hist_all[QPW_WARPS][BBINS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* hist = hist_all[w];
+    const int64_t gw = (int64_t)blockIdx.x * QPW_WARPS + w, nw = (int64_t)gridDim.x * QPW_WARPS;
+    const bool vec = (S % 4 == 0) && (ldS % 4 == 0) && ((reinterpret_cast<uintptr_t>(Ds) & 15) == 0);
+    for (int64_t row = gw; row < M; row += nw) {
+        const float* rp = Ds + row * ldS;
+        auto for_each = [&](auto f) {
+            if (vec) {
+                const float4* r4 = reinterpret_cast<const float4*>(rp);
+                for (int64_t j = lane; j < S / 4; j += 32) {
+                    const float4 x = __ldg(r4 + j);
+                    f(x.x); f(x.y); f(x.z); f(x.w);
+                }
+            } else {
+                for (int64_t j = lane; j < S; j += 32) f(__ldg(rp + j));
+            }
+        };
+        for (int i = lane; i < BBINS; i += 32) hist[i] = 0;
+        float lo = __int_as_float(0x7F800000), hi = -__int_as_float(0x7F800000);
+        int nfin = 0;
+        for_each([&](float x) {
+            if (isfinite(x)) {
+                lo = fminf(lo, x);
+                hi = fmaxf(hi, x);
+                ++nfin;
+            }
+        });
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+            nfin += __shfl_xor_sync(FULL, nfin, o);
+        }
+        if (nfin < r) {  // not reached for finite inputs (S - 1 >= r finite samples)
+            if (lane == 0) thr[row] = nfin ? hi : -__int_as_float(0x7F800000);
+            __syncwarp();
+            continue;
+        }
+        const float span = hi - lo;
+        const float scale = span > 0.0f && isfinite(span) && isfinite((float)BBINS / span) ? (float)BBINS / span : 0.0f;
+        auto bucket = [&](float x) -> uint32_t { return min((uint32_t)((x - lo) * scale), (uint32_t)(BBINS - 1)); };
+        __syncwarp();
+        for_each([&](float x) {
+            if (isfinite(x)) atomicAdd(&hist[bucket(x)], 1u);
+        });
+        __syncwarp();
+        uint32_t c[BBINS / 32], sum = 0;
+        #pragma unroll
+        for (int j = 0; j < BBINS / 32; ++j) {
+            c[j] = hist[lane * (BBINS / 32) + j];
+            sum += c[j];
+        }
+        uint32_t incl = sum;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - sum, mybin = 0xFFFFFFFFu;
+        if (run < (uint32_t)r && (uint32_t)r <= incl) {
+            #pragma unroll
+            for (int j = 0; j < BBINS / 32; ++j) {
+                if (mybin == 0xFFFFFFFFu && run + c[j] >= (uint32_t)r) mybin = lane * (BBINS / 32) + j;
+                run += c[j];
+            }
+        }
+        const uint32_t bstar = __reduce_min_sync(FULL, mybin);
+        float p = -__int_as_float(0x7F800000);
+        for_each([&](float x) {
+            if (isfinite(x) && bucket(x) <= bstar) p = fmaxf(p, x);
+        });
+        for (int o = 16; o > 0; o >>= 1) p = fmaxf(p, __shfl_xor_sync(FULL, p, o));
+        if (lane == 0) thr[row] = p;
+        __syncwarp();
+    }
+}
+
 // Exact select over the partition's candidate lists for k > 32: one CTA per row loads the
 // row's candidates (ukeys of the distances + column) into shared memory and runs the
 // bucket finish (or the exact radix + bitonic finish).  Certificate: fewer than k
@@ -2151,6 +2235,14 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!getenv_flag("KNN_PIVOT_CTA")) {  // warp per row (default); env: the CTA-per-row form
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pivot_from_sample_warp_kernel, 32 * QPW_WARPS, 0);
+        int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+        if (g > ceil_div(M, QPW_WARPS)) g = ceil_div(M, QPW_WARPS);
+        pivot_from_sample_warp_kernel<<<(unsigned)g, 32 * QPW_WARPS, 0, s>>>(Ds, M, S, ldS, r, thr);
+        return cudaGetLastError();
+    }
     int64_t grid = (int64_t)sms * 8;
     if (grid > M) grid = M;
     if (S <= 16 * QP_THREADS)
