@@ -278,7 +278,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
-        if (!fused && !pivot && !pivotq) redo = c.take<int32_t>((size_t)(rows_blk > 0 ? rows_blk : M) + 1);
+        if (!fused && !pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 && !pivotq ? rows_blk : M) + 1);
         if (fused && S > 1) {
             part_i = c.take<int32_t>((size_t)S * M * k);
             part_d = c.take<float>((size_t)S * M * k);
@@ -386,7 +386,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, capq, M, k, idx_offset, out_idx, out_dist,
-                                                    flag, s));
+                                                    flag, redo, s));
         tc2.done();
         return KNN_OK;
     }
@@ -1073,8 +1073,10 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t *flag = nullptr, *cnt = nullptr;
     uint32_t *ckey = nullptr, *cidx = nullptr;
+    int32_t* redo = nullptr;
     auto layout = [&](Carve& c) {
         flag = c.take<int32_t>(4);
+        redo = c.take<int32_t>(rows + 1);
         cnt = c.take<int32_t>(rows);
         ckey = c.take<uint32_t>((size_t)rows * cap);
         cidx = c.take<uint32_t>((size_t)rows * cap);
@@ -1090,7 +1092,8 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     if (k <= 32)
         KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, s));
     else
-        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, s));
+        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, redo,
+                                                          s));
     tm.done();
     knn_status st = finish_blocking(ctx, s);
     drain_profile(ctx);

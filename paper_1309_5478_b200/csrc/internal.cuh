@@ -97,9 +97,11 @@ cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, co
 // certificate or an overflowed list).
 cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int64_t ldS, int32_t r,
                                      float* thr, cudaStream_t s);
+// redo: M + 1 int32 of workspace for the warp-per-row form (null: CTA per row only).
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
-                                          int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
+                                          int32_t* out_idx, float* out_dist, int32_t* flag, int32_t* redo,
+                                          cudaStream_t s);
 // Multi-GPU symmetric k-NNG: concatenate G (possibly peer-mapped) candidate lists per row.
 cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* const* keys, const uint32_t* const* idxs,
                                 int32_t G, int32_t cap_src, int64_t row0, int64_t rows, int32_t cap_dst,

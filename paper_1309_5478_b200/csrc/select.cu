@@ -30,6 +30,7 @@
 
 #include <climits>
 #include <type_traits>
+#include <cstdio>
 #include <cstdlib>
 #include <cooperative_groups.h>
 #include <cmath>
@@ -1901,7 +1902,8 @@ __global__ void __launch_bounds__(CS_THREADS, 4)
 candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
                               const uint32_t* __restrict__ cidx_g, int32_t cap, int64_t M, int k,
                               int KP, int64_t idx_offset, int32_t* __restrict__ out_idx,
-                              float* __restrict__ out_dist, int32_t* __restrict__ flag) {
+                              float* __restrict__ out_dist, int32_t* __restrict__ flag,
+                              const int32_t* __restrict__ list) {
     extern __shared__ uint32_t smem[];
     uint32_t* ckey = smem;
     uint32_t* cidx = ckey + cap;
@@ -1909,9 +1911,11 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
     uint32_t* kidx = kkey + KP;
     uint32_t* hist = kidx + KP;  // CS_BINS
     __shared__ Scal sc;
-    for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+    const int64_t nrows = list ? (int64_t)list[0] : M;
+    for (int64_t i_row = blockIdx.x; i_row < nrows; i_row += gridDim.x) {
+        const int64_t row = list ? (int64_t)list[1 + i_row] : i_row;
         const int n = cnt[row];
-        if (threadIdx.x == 0)  // diagnostic: candidates kept (knn_last_candidates)
+        if (threadIdx.x == 0 && !list)  // diagnostic: candidates kept (knn_last_candidates)
             atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
         if (n > cap || n < k) {
             if (threadIdx.x == 0) atomicOr(flag, 2);
@@ -1943,6 +1947,215 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
             block_finish<CS_THREADS>(ckey, cidx, n, k, KP, kkey, kidx, hist, &sc, idx_offset,
                                      out_idx + row * k, out_dist + row * k);
         __syncthreads();
+    }
+}
+
+// Warp-per-row form (the default for k > 32): the bucket finish of block_finish_bucket done
+// by one warp with warp-private buckets and output, the candidates re-read from global
+// memory (L2) in three passes (key range; 1024-bucket histogram; scatter), no CTA
+// barriers.  Rows whose buckets are crowded, or whose keys are non-finite, are appended
+// to redo[1..] for the CTA kernel above.
+constexpr int CSW_WARPS = 8;
+constexpr int CSW_BINS = 1024;
+constexpr int CSW_STAR = 64;
+constexpr int CSW_PASS = 16;
+constexpr int CSW_EPT = 8;
+__host__ __device__ constexpr size_t csw_slab_bytes(int KP) {
+    return (size_t)CSW_BINS * 4 + (size_t)KP * 8 + (size_t)CSW_STAR * 8 + 16;
+}
+__global__ void __launch_bounds__(32 * CSW_WARPS)
+candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
+                             const uint32_t* __restrict__ cidx_g, int32_t cap, int64_t M, int k, int KP,
+                             int64_t idx_offset, int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
+                             int32_t* __restrict__ flag, int32_t* __restrict__ redo) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint8_t* slab = smem_raw + csw_slab_bytes(KP) * w;
+    uint64_t* star = reinterpret_cast<uint64_t*>(slab);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(star + CSW_STAR);
+    uint32_t* okey = hist + CSW_BINS;
+    uint32_t* oidx = okey + KP;
+    int* nst = reinterpret_cast<int*>(oidx + KP);
+    const int64_t gw = (int64_t)blockIdx.x * CSW_WARPS + w, nw = (int64_t)gridDim.x * CSW_WARPS;
+    for (int64_t row = gw; row < M; row += nw) {
+        const int n = cnt[row];
+        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
+        if (n > cap || n < k) {  // overflow or failed certificate: the caller redoes the call
+            if (lane == 0) atomicOr(flag, 2);
+            continue;
+        }
+        const uint32_t* gk = ckey_g + row * cap;
+        const uint32_t* gi = cidx_g + row * cap;
+        auto to_redo = [&]() {
+            if (lane == 0) {
+                const int slot = atomicAdd(redo, 1);
+                redo[1 + slot] = (int32_t)row;
+            }
+            __syncwarp();
+        };
+        // pass 1: key range
+        // (every pass loads CSW_EPT elements per lane before using them: the loads are
+        // L2 latency bound, one outstanding load per lane would stall each iteration)
+        uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
+        for (int base = 0; base < n; base += 32 * CSW_EPT) {
+            uint32_t kv[CSW_EPT];
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j) {
+                const int i = base + 32 * j + lane;
+                kv[j] = i < n ? __ldcg(gk + i) : 0xFFFFFFFFu;
+            }
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j) {
+                kmin = min(kmin, kv[j]);
+                if (base + 32 * j + lane < n) kmax = max(kmax, kv[j]);
+            }
+        }
+        kmin = __reduce_min_sync(FULL, kmin);
+        kmax = __reduce_max_sync(FULL, kmax);
+        const float fmn = ukey_to_float(kmin), fmx = ukey_to_float(kmax);
+        const float span = fmx - fmn;
+        const float scale = (float)CSW_BINS / span;
+        if (!(isfinite(fmn) && isfinite(fmx) && span > 0.0f && isfinite(span) && isfinite(scale))) {
+            to_redo();
+            continue;
+        }
+        auto bucket = [&](uint32_t key) -> uint32_t {
+            return min((uint32_t)((ukey_to_float(key) - fmn) * scale), (uint32_t)(CSW_BINS - 1));
+        };
+        for (int i = lane; i < CSW_BINS; i += 32) hist[i] = 0;
+        if (lane == 0) *nst = 0;
+        __syncwarp();
+        // pass 2: histogram
+        for (int base = 0; base < n; base += 32 * CSW_EPT) {
+            uint32_t kv[CSW_EPT];
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j) {
+                const int i = base + 32 * j + lane;
+                kv[j] = i < n ? __ldcg(gk + i) : 0u;
+            }
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j)
+                if (base + 32 * j + lane < n) atomicAdd(&hist[bucket(kv[j])], 1u);
+        }
+        __syncwarp();
+        // exclusive offsets; b* = bucket of rank k; the largest bucket below b*
+        constexpr int BPL = CSW_BINS / 32;
+        uint32_t c[BPL], sum = 0;
+        #pragma unroll
+        for (int j = 0; j < BPL; ++j) {
+            c[j] = hist[lane * BPL + j];
+            sum += c[j];
+        }
+        uint32_t incl = sum;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - sum, mybin = 0xFFFFFFFFu, mybefore = 0, myn = 0;
+        #pragma unroll
+        for (int j = 0; j < BPL; ++j) {
+            hist[lane * BPL + j] = run;
+            if (mybin == 0xFFFFFFFFu && run < (uint32_t)k && (uint32_t)k <= run + c[j]) {
+                mybin = lane * BPL + j;
+                mybefore = run;
+                myn = c[j];
+            }
+            run += c[j];
+        }
+        const uint32_t bstar = __reduce_min_sync(FULL, mybin);
+        const int owner = (int)(bstar / BPL);
+        const uint32_t before = __shfl_sync(FULL, mybefore, owner);
+        const uint32_t nstar = __shfl_sync(FULL, myn, owner);
+        uint32_t mymax = 0;
+        #pragma unroll
+        for (int j = 0; j < BPL; ++j)
+            if ((uint32_t)(lane * BPL + j) < bstar) mymax = max(mymax, c[j]);
+        const uint32_t maxc = __reduce_max_sync(FULL, mymax);
+        if (nstar > CSW_STAR || maxc > CSW_PASS) {
+            to_redo();
+            continue;
+        }
+        __syncwarp();
+        // pass 3: scatter below b*, collect b*
+        for (int base = 0; base < n; base += 32 * CSW_EPT) {
+            uint32_t kv[CSW_EPT], iv[CSW_EPT];
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j) {
+                const int i = base + 32 * j + lane;
+                kv[j] = i < n ? __ldcs(gk + i) : 0xFFFFFFFFu;
+                iv[j] = i < n ? __ldcs(gi + i) : 0u;
+            }
+            #pragma unroll
+            for (int j = 0; j < CSW_EPT; ++j) {
+                if (base + 32 * j + lane >= n) continue;
+                const uint32_t b = bucket(kv[j]);
+                if (b < bstar) {
+                    const uint32_t pos = atomicAdd(&hist[b], 1u);
+                    okey[pos] = kv[j];
+                    oidx[pos] = iv[j];
+                } else if (b == bstar) {
+                    const int q = atomicAdd(nst, 1);
+                    star[q] = (uint64_t)kv[j] << 32 | iv[j];
+                }
+            }
+        }
+        __syncwarp();
+        {   // b*'s candidates sorted (<= 64, two per lane); the first k - before appended
+            uint64_t a0 = lane < (int)nstar ? star[lane] : ~0ull;
+            uint64_t a1 = lane + 32 < (int)nstar ? star[lane + 32] : ~0ull;
+            #pragma unroll
+            for (int size = 2; size <= 64; size <<= 1) {
+                #pragma unroll
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    if (stride == 32) {
+                        const bool sw = a1 < a0;
+                        const uint64_t x = a0;
+                        a0 = sw ? a1 : a0;
+                        a1 = sw ? x : a1;
+                    } else {
+                        #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint64_t& v = h ? a1 : a0;
+                            const int p = lane + 32 * h;
+                            const uint64_t o = __shfl_xor_sync(FULL, v, stride);
+                            const bool up = ((p & size) == 0) == ((p & stride) == 0);
+                            v = ((o < v) == up) ? o : v;
+                        }
+                    }
+                }
+            }
+            const uint32_t need = (uint32_t)k - before;
+            if ((uint32_t)lane < need) {
+                okey[before + lane] = (uint32_t)(a0 >> 32);
+                oidx[before + lane] = (uint32_t)a0;
+            }
+            if ((uint32_t)lane + 32 < need) {
+                okey[before + lane + 32] = (uint32_t)(a1 >> 32);
+                oidx[before + lane + 32] = (uint32_t)a1;
+            }
+        }
+        __syncwarp();
+        // odd-even transposition inside the buckets below b* (maxc passes); a lane per
+        // bucket (insertion sort) measured slower: the counts are skewed toward b*, so the
+        // few lanes holding the dense buckets serialise the warp
+        for (uint32_t pass = 0; pass < maxc; ++pass) {
+            for (uint32_t p = 2 * lane + (pass & 1); p + 1 < before; p += 64) {
+                const uint32_t k0 = okey[p], k1 = okey[p + 1], i0 = oidx[p], i1 = oidx[p + 1];
+                if (k1 < k0 || (k1 == k0 && i1 < i0)) {
+                    okey[p] = k1;
+                    okey[p + 1] = k0;
+                    oidx[p] = i1;
+                    oidx[p + 1] = i0;
+                }
+            }
+            __syncwarp();
+        }
+        for (int q = lane; q < k; q += 32) {
+            out_idx[row * k + q] = (int32_t)((int64_t)oidx[q] + idx_offset);
+            out_dist[row * k + q] = ukey_to_float(okey[q]);
+        }
+        __syncwarp();
     }
 }
 
@@ -2256,20 +2469,42 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
 
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
-                                          int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s) {
+                                          int32_t* out_idx, float* out_dist, int32_t* flag, int32_t* redo,
+                                          cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     const int KP = next_pow2(k);
-    const size_t smem = (size_t)(2 * cap + 2 * KP + CS_BINS) * sizeof(uint32_t);
     cudaError_t e;
-    if ((e = set_smem(candidate_select_large_kernel, smem)) != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool warp = redo != nullptr && !getenv_flag("KNN_CANDSEL_CTA");
+    if (warp) {
+        if ((e = cudaMemsetAsync(redo, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
+        const size_t wsm = csw_slab_bytes(KP) * CSW_WARPS;
+        if ((e = set_smem(candidate_select_warp_kernel, wsm)) != cudaSuccess) return e;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, candidate_select_warp_kernel, 32 * CSW_WARPS, wsm);
+        int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+        if (g > ceil_div(M, CSW_WARPS)) g = ceil_div(M, CSW_WARPS);
+        candidate_select_warp_kernel<<<(unsigned)g, 32 * CSW_WARPS, wsm, s>>>(cnt, ckey, cidx, cap, M, k, KP,
+                                                                            idx_offset, out_idx, out_dist, flag,
+                                                                            redo);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (getenv_flag("KNN_CANDSEL_STATS")) {  // diagnostic: rows handed to the CTA kernel
+            int32_t nr = 0;
+            cudaMemcpyAsync(&nr, redo, sizeof(nr), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "candidate_select_warp: %d of %lld rows redone\n", nr, (long long)M);
+        }
+    }
+    // CTA per row: every row, or (after the warp kernel) the rows it could not bucket
+    const size_t smem = (size_t)(2 * cap + 2 * KP + CS_BINS) * sizeof(uint32_t);
+    if ((e = set_smem(candidate_select_large_kernel, smem)) != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, candidate_select_large_kernel, CS_THREADS, smem);
     int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > M) grid = M;
     candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, ckey, cidx, cap, M, k, KP,
-                                                                          idx_offset, out_idx, out_dist, flag);
+                                                                          idx_offset, out_idx, out_dist, flag,
+                                                                          warp ? redo : nullptr);
     return cudaGetLastError();
 }
 

@@ -460,6 +460,46 @@ def test_quantile_pivot_graph_equals_materialised(N, d, k, metric, dist):
     assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
 
 
+@pytest.mark.parametrize("dup", [1, 40, 90])
+def test_quantile_candidate_select_warp_and_cta_forms(dup):
+    """k > 32 candidate select: the warp-per-row bucket finish hands crowded rows (many
+    equal keys: every point repeated `dup` times) to the CTA kernel through a row list;
+    both forms and the materialised plan agree bit for bit."""
+    base = datagen.points(20000 // dup, 32, "gauss", seed=65 + dup)
+    X = np.ascontiguousarray(np.repeat(base, dup, axis=0)[:20000])
+    X = X[np.random.Generator(np.random.Philox(dup)).permutation(len(X))]
+    code = (
+        "import sys, numpy as np, torch\n"
+        "from paper_1309_5478_b200 import knn\n"
+        "X = torch.from_numpy(np.load(sys.argv[1])).cuda()\n"
+        "gi, gd = knn.graph(X, 120)\n"
+        "np.save(sys.argv[2], np.stack([gi.cpu().numpy(), gd.view(torch.int32).cpu().numpy()]))\n"
+        "print(knn.last_plan())\n")
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as tmp:
+        xin = os.path.join(tmp, "x.npy")
+        np.save(xin, X)
+        outs, plans = [], []
+        for env_extra in ({}, {"KNN_CANDSEL_CTA": "1"}):
+            out = os.path.join(tmp, "o%d.npy" % len(outs))
+            r = subprocess.run([sys.executable, "-c", code, xin, out], check=True, cwd=root, timeout=300,
+                               env=dict(os.environ, **env_extra), capture_output=True, text=True)
+            plans.append(int(r.stdout.split()[-1]))
+            outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+    kn = knn()
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(cuda(X), 120)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert np.array_equal(outs[0][0], ri.cpu().numpy())
+    assert np.array_equal(outs[0][1], rd.view(torch.int32).cpu().numpy())
+    if dup == 1:
+        assert plans == [3, 3], plans
+
+
 def test_quantile_pivot_search_and_shifted_blocks():
     kn = knn()
     X = cuda(datagen.points(40000, 48, "gauss", seed=61))
