@@ -39,6 +39,7 @@ struct knn_ctx {
     bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
     int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
     int32_t pivot_div = 8;     // sample = the first N / pivot_div corpus points
+    bool pivot1 = false;       // k <= 32, L2: single-product partition + re-evaluation (env KNN_PIVOT1=1)
     float pivot_margin = __builtin_nanf("");  // KNN_PIVOT_MARGIN: override of the sample's error margin
     int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;
@@ -275,6 +276,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     uint32_t *ckey = nullptr, *cidx = nullptr;
     int32_t* redo = nullptr;
     Prepared smp{};  // the pivot plans' column sample (gathered points)
+    float *nsc_x = nullptr, *nsc_q = nullptr;  // single-product partition: scaled norms
     float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
@@ -291,6 +293,10 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             smp.sqn = c.take<float>(round_up(Sx, knn::kColPad));
             smp.rs = c.take<float>(round_up(Sx, knn::kColPad));
             const int32_t cp = pivot ? cap : capq;
+            if (pivot) {
+                nsc_x = c.take<float>(round_up(N, knn::kColPad));
+                nsc_q = c.take<float>(round_up(M, knn::kColPad));
+            }
             thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
             ckey = c.take<uint32_t>((size_t)M * cp);
@@ -349,12 +355,32 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         }
         // 3. partition GEMM over the whole matrix, 4. exact select of the candidates
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+        // L2 metrics: the partition from the single hi.hi product with its error bound (a
+        // third of the MMA work) and the survivors near the k-th re-evaluated exactly
+        const bool one = ctx->pivot1 && metric <= KNN_L2;
+        if (one) {  // the lower bound u_hh - F n_qx as the u of norms scaled by 1 - F
+            const float f = 1.0f - knn::pivot1_margin(d_pad);
+            KNN_CUDA(knn::launch_scale_norms(px.sqn, nsc_x, round_up(N, knn::kColPad), f, s));
+            if (!same) KNN_CUDA(knn::launch_scale_norms(pq.sqn, nsc_q, round_up(M, knn::kColPad), f, s));
+            op.qn = same ? nsc_x : nsc_q;
+            op.xn = nsc_x;
+        }
         Timed tg(ctx, KNN_KERNEL_FUSED, s);
-        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
-                                           flag, ctx->num_sms, s));
+        if (one)
+            KNN_CUDA(knn::launch_dist_tc_pivot1(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
+                                                flag, ctx->num_sms, s));
+        else
+            KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
+                                               flag, ctx->num_sms, s));
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
-        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, flag, s));
+        if (one)
+            KNN_CUDA(knn::launch_candidate_recompute(cnt, ckey, cidx, cap, M, k, idx_offset, Q, X, d, pq.sqn,
+                                                     px.sqn, thr, knn::pivot1_margin(d_pad), metric, out_idx,
+                                                     out_dist, flag, s));
+        else
+            KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, flag,
+                                                  s));
         tc2.done();
         return KNN_OK;
     }
@@ -483,6 +509,8 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     if (pv && strcmp(pv, "0") == 0) c->pivot_ok = false;
     const char* pd = getenv("KNN_PIVOT_DIV");
     if (pd && atoi(pd) >= 2) c->pivot_div = atoi(pd);
+    const char* p1 = getenv("KNN_PIVOT1");
+    if (p1 && p1[0] && strcmp(p1, "0") != 0) c->pivot1 = true;
     const char* pm = getenv("KNN_PIVOT_MARGIN");
     if (pm) c->pivot_margin = strtof(pm, nullptr);
     const char* pc = getenv("KNN_PIVOT_CAP");

@@ -135,7 +135,11 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
 // MODE_MINS writes, per row, the minimum distance of every 32-column chunk; MODE_SAMPLE
 // writes the single-product upper bound v >= u of every element (the quantile pivot's
 // sample for k > 32), unclamped, in the u domain.
-enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL = 4 };
+enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL = 4, MODE_PIVOT1 = 5 };
+// MODE_PIVOT1: the partition from the single hi.hi product; the kept key is the lower bound
+// u_hh - F (||q||^2 + ||x||^2) <= the exact distance (computed as the u of norms scaled by
+// 1 - F, launch_scale_norms), so every element at or below the pivot is kept; the
+// candidate select re-evaluates the survivors exactly (select.cu).
 // MODE_NULL (diagnostic, knn_diag_mainloop): the epilogue only drains TMEM (tcgen05.ld) and
 // frees the accumulator, so the kernel runs at the mainloop's own rate.
 
@@ -147,16 +151,17 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                Sched sched, EpiArgs ep) {
     // SYM: upper-triangle pair blocks only, O1 everywhere (every element has i < j or is
     // mirrored from one), so the mainloop sees no self shift.
-    constexpr bool PIVOT = MODE == MODE_PIVOT;
+    constexpr bool PIVOT1 = MODE == MODE_PIVOT1;
+    constexpr bool PIVOT = MODE == MODE_PIVOT || PIVOT1;
     constexpr bool MINS = MODE == MODE_MINS;
     constexpr bool SAMPLE = MODE == MODE_SAMPLE;
     constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
     // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
-    constexpr int NSEG = MINS || SAMPLE ? 1 : 3;
-    constexpr int KSTAGES = MINS || SAMPLE ? 2 * STAGES : STAGES;
+    constexpr int NSEG = MINS || SAMPLE || PIVOT1 ? 1 : 3;
+    constexpr int KSTAGES = NSEG == 1 ? 2 * STAGES : STAGES;
     static_assert(KSTAGES * stage_bytes<NSEG>() == STAGES * STAGE_BYTES, "smem layout");
     // the single product is orientation-free: no two-pass blocks on the diagonal
-    const int64_t ml_shift = SYM || MINS || SAMPLE ? INT64_MIN : ep.self_shift;
+    const int64_t ml_shift = SYM || NSEG == 1 ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -331,6 +336,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         if (METRIC == 2) u = fminf(u, 3.0f);
                         // MINS: the hi.hi value plus a bound of its error, so that it is never
                         // below the FP32-accurate u of the partition
+                        // (PIVOT1: qn, xn arrive scaled by 1 - F, so u is already the lower bound)
                         v[c] = MINS || SAMPLE ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
                     }
                 }
@@ -400,6 +406,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         asm volatile("" ::"f"(v[0]), "f"(v[31]));
                         continue;
                     }
+                    // (one combined test against max(row pivot, column pivot), with the
+                    // survivors split after staging, measured slower: 2.92 vs 2.84 ms)
                     #pragma unroll
                     for (int c = 0; c < 32; ++c) hr |= (uint32_t)(v[c] <= trow) << c;
                     if (SYM && !(ep.dbg & 1)) {
@@ -431,6 +439,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         __syncwarp();
                         continue;
                     }
+                    // staged element c of this lane's row: 16-byte unit (c >> 2) ^ (lane & 7)
+                    // of the row, i.e. index lane * 32 + (c ^ ((lane & 7) << 2))
+                    const float* srow = svp + lane * 32;
+                    const int sx = (lane & 7) << 2;
                     // slots of this lane's entries in the warp's pending list: the warp total
                     // by one reduction, each lane's base by a shared atomic on the warp's
                     // running count (order inside the list is irrelevant)
@@ -445,15 +457,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     uint32_t h = hm;
                     if (total <= PEND_CAP) {
                         int pos = mine ? atomicAdd(&s_pend[warp - 2], mine) : 0;
-                        // staged element c of this lane's row: 16-byte unit (c >> 2) ^ (lane & 7)
-                        // of the row, i.e. index lane * 32 + (c ^ ((lane & 7) << 2))
-                        const float* srow = svp + lane * 32;
-                        const int sx = (lane & 7) << 2;
                         while (h) {
                             const int c = __ffs(h) - 1;
                             h &= h - 1;
                             const float x = srow[c ^ sx];
-                            const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
+                            const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
                             if ((hr >> c) & 1) {
                                 prow[pos] = (uint32_t)row;
                                 pcol[pos] = (uint32_t)(c0 + c);
@@ -473,7 +481,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             const int c = __ffs(h) - 1;
                             h &= h - 1;
                             const float x = svp[lane * 32 + (((c >> 2) ^ (lane & 7)) << 2) + (c & 3)];
-                            const uint32_t key = __float_as_uint(finalize_dist<METRIC>(x)) | 0x80000000u;
+                            const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
                             if ((hr >> c) & 1) pivot_append(ep, row, key, (uint32_t)(c0 + c));
                             if (SYM && ((hc >> c) & 1)) pivot_append(ep, c0 + c, key, (uint32_t)row);
                         }
@@ -766,10 +774,11 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
     return cudaGetLastError();
 }
 
-cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
-                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                                 int64_t unit_lo, int64_t unit_hi) {
+template <int MODE>
+cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                              const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                              int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
+                              int64_t unit_lo, int64_t unit_hi, float margin) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     if (sym && op.M != op.N) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
@@ -780,7 +789,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, sym ? 0 : self_shift, nullptr, 0,
-               thr, cnt, ckey, cidx, cap, flag};
+               thr, cnt, ckey, cidx, cap, flag, margin};
     if (const char* dv = getenv("KNN_DBG_EPI")) ep.dbg = atoi(dv);
     cudaError_t e;
     if (sym) {
@@ -792,7 +801,7 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         if (sched.u_hi <= sched.u_lo) return cudaSuccess;
         const int64_t units = sched.u_hi - sched.u_lo;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE_PIVOT, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, true, MODE_PIVOT, SymSched> : dist_tc_kernel<0, true, MODE_PIVOT, SymSched>;
+        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<MODE == MODE_PIVOT ? 2 : 0, true, MODE, SymSched> : dist_tc_kernel<0, true, MODE, SymSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
@@ -801,13 +810,37 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
         TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
         const int64_t units = sched.n_mp * sched.n_nb;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
-        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_PIVOT, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_PIVOT, TileSched> : dist_tc_kernel<0, false, MODE_PIVOT, TileSched>;
+        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<MODE == MODE_PIVOT ? 2 : 0, false, MODE, TileSched> : dist_tc_kernel<0, false, MODE, TileSched>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
             return e;
         kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
                                                                     sched, ep);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                 int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
+                                 int64_t unit_lo, int64_t unit_hi) {
+    return launch_pivot_impl<MODE_PIVOT>(op, metric, self_shift, sym, thr, cnt, ckey, cidx, cap, flag, num_sms,
+                                         s, unit_lo, unit_hi, 0.0f);
+}
+
+float pivot1_margin(int32_t d_pad) {
+    // |u_hh - D| <= F (||q||^2 + ||x||^2) for the exact distance D of the fp32 inputs: the
+    // sample pass's bound (launch_dist_tc_mins) with one more d_pad 2^-23 for the fp32
+    // rounding of the two norms and of u, and 2^-20 for the lower bound's own roundings
+    return (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) + 2.0 * d_pad * std::ldexp(1.0, -23) +
+                   std::ldexp(1.0, -19));
+}
+
+cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s) {
+    if (metric_kind(metric) == 2) return cudaErrorInvalidValue;  // L2 metrics only
+    return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, ckey, cidx, cap, flag,
+                                          num_sms, s, -1, -1, pivot1_margin(op.d_pad));
 }
 
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s) {

@@ -72,6 +72,15 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
                                  int64_t unit_lo = -1, int64_t unit_hi = -1);
+// The same partition from the single hi.hi product (L2 metrics): kept iff the lower bound
+// L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); ckey holds L.
+// F = pivot1_margin(d_pad) bounds |u_hh - D| / (||q||^2 + ||x||^2) for the exact D.
+// op.qn / op.xn must be the prep norms scaled by 1 - F (launch_scale_norms).
+cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s);
+float pivot1_margin(int32_t d_pad);
+cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
+                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
 // Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31
@@ -97,6 +106,15 @@ cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, co
 // certificate or an overflowed list).
 cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int64_t ldS, int32_t r,
                                      float* thr, cudaStream_t s);
+// Exact top-k (k <= 32, L2 metrics) of the single-product partition's lists (lower bounds):
+// re-evaluates the few candidates whose bounds reach the k-th upper bound in fp64 from the
+// fp32 inputs Q [M][d] / X [N][d]; qn / xn the prep norms, margin = pivot1_margin.
+// flag |= 2 when the partition is not certified exact for some row (the caller redoes).
+cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                       int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
+                                       const float* X, int32_t d, const float* qn, const float* xn,
+                                       const float* thr, float margin, int32_t metric, int32_t* out_idx,
+                                       float* out_dist, int32_t* flag, cudaStream_t s);
 // redo: M + 1 int32 of workspace for the warp-per-row form (null: CTA per row only).
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,

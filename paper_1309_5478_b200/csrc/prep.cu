@@ -196,4 +196,19 @@ cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float
     return cudaGetLastError();
 }
 
+namespace {
+__global__ void scale_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n, float f) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] * f;
+}
+}  // namespace
+
+// dst = f * src (the single-product partition's scaled norms; n includes the zero padding)
+cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int64_t blocks = ceil_div(n, (int64_t)256);
+    scale_kernel<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(src, dst, n, f);
+    return cudaGetLastError();
+}
+
 }  // namespace knn

@@ -1670,6 +1670,216 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
     }
 }
 
+// Exact top-k (k <= 32) of the single-product partition (gemm_tc.cu MODE_PIVOT1, L2
+// metrics), warp per row.  The list holds lower bounds L = u_hh - F n_qx <= D (n_qx =
+// ||q||^2 + ||x||^2), so U = L + 2F n_qx >= D:
+//  1. T = the k-th smallest U over the first <= 512 candidates: k candidates have D <= T,
+//     so the row's k nearest candidates (and their fp32 ties) all have L <= T;
+//  2. R = {L <= T (1 + 4 e) + slack} (e = the re-evaluation's error bound): typically k
+//     plus the few whose bounds straddle T (51 per row at the headline);
+//  3. D of every member of R from the fp32 inputs as the sum of squared differences, in
+//     fp32 (relative error <= e = (d/32 + 8) 2^-24: ~1e-6 at d = 256, 1e-7 typical, vs
+//     ~1e-5 for the split-fp16 GEMM value), 8 candidates per step so that their L2
+//     loads overlap; the k smallest (value, index) pairs kept by a warp merge;
+//  4. certificate: the k-th D (1 + 2 e + 2^-20) <= the pivot, i.e. every element that can
+//     rank among the k, had L <= pivot and is a candidate; else flag bit 2 and the caller
+//     redoes the call on the full matrix.
+constexpr int CR_PER = 16;
+constexpr int CR_RCAP = 256;
+constexpr int CR_G = 8;
+__global__ void __launch_bounds__(256)
+candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
+                           const uint32_t* __restrict__ cidx, int cap, int64_t M, int k, int64_t idx_offset,
+                           const float* __restrict__ Q, const float* __restrict__ X, int d,
+                           const float* __restrict__ qn, const float* __restrict__ xn,
+                           const float* __restrict__ thr, float margin, float rerr, int metric, int vec,
+                           int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
+                           int32_t* __restrict__ flag) {
+    __shared__ uint32_t heads[8][CS_PER][33];
+    __shared__ uint32_t rlist[8][CR_RCAP];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * 8 + w;
+    if (row >= M) return;
+    int n = cnt[row];
+    if (n < k) {  // fewer than k lower bounds at or below the pivot: the partition is not exact
+        if (lane == 0) atomicOr(flag, 2);
+        return;
+    }
+    n = n < cap ? n : cap;
+    if (lane == 0 && !(vec & 2)) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
+    const uint32_t* rk = ckey + row * cap;
+    const uint32_t* ri = cidx + row * cap;
+    const float qnr = __ldg(qn + row), f2 = 2.0f * margin;
+    // 1. T
+    const int n1 = n < 32 * CR_PER ? n : 32 * CR_PER;
+    uint32_t v[CR_PER], lk[CR_PER], li[CR_PER];
+    #pragma unroll
+    for (int i = 0; i < CR_PER; ++i) {
+        const int pos = lane + 32 * i;
+        lk[i] = pos < n1 ? __ldg(rk + pos) : 0xFFFFFFFFu;
+        li[i] = pos < n1 ? __ldg(ri + pos) : 0u;
+    }
+    #pragma unroll
+    for (int i = 0; i < CR_PER; ++i) {
+        const float xj = lane + 32 * i < n1 ? __ldg(xn + li[i]) : 0.0f;
+        v[i] = lk[i] == 0xFFFFFFFFu ? 0xFFFFFFFFu : ukey(fmaf(f2, qnr + xj, ukey_to_float(lk[i])));
+    }
+    sort16(v);
+    #pragma unroll
+    for (int i = 0; i < CS_PER; ++i) heads[w][i][lane] = v[i];
+    __syncwarp();
+    uint32_t h = v[0], Tk = 0;
+    int p = 0;
+    for (int c = 0; c < k;) {
+        const uint32_t mn = __reduce_min_sync(FULL, h);
+        const bool mine = h == mn;
+        c += __popc(__ballot_sync(FULL, mine));
+        Tk = mn;
+        if (mine) h = ++p < CS_PER ? heads[w][p][lane] : 0xFFFFFFFFu;
+    }
+    const float T = ukey_to_float(Tk);
+    // every candidate whose re-evaluated value can reach the k-th re-evaluated value
+    const uint32_t Tf = ukey(T + (4.0f * rerr + 0x1p-20f) * (fabsf(T) + qnr));
+    // 2. R (the first 512 from registers)
+    int nr = 0;
+    #pragma unroll
+    for (int i = 0; i < CR_PER; ++i) {
+        const bool keep = lk[i] <= Tf;  // padding is 0xFFFFFFFF
+        const uint32_t bm = __ballot_sync(FULL, keep);
+        const int slot = nr + __popc(bm & ws::lanemask_lt());
+        if (keep && slot < CR_RCAP) rlist[w][slot] = li[i];
+        nr += __popc(bm);
+    }
+    for (int base = n1; base < n; base += 32) {
+        const int pos = base + lane;
+        const bool keep = pos < n && __ldg(rk + pos) <= Tf;
+        const uint32_t bm = __ballot_sync(FULL, keep);
+        const int slot = nr + __popc(bm & ws::lanemask_lt());
+        if (keep && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + pos);
+        nr += __popc(bm);
+    }
+    if (lane == 0 && (vec & 2))  // diagnostic (KNN_RECOMP_STATS): count |R| instead
+        atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)nr);
+    if (nr > CR_RCAP) {  // pathological ties: redo the call on the full matrix
+        if (lane == 0) atomicOr(flag, 2);
+        return;
+    }
+    __syncwarp();
+    // 3. exact values, k smallest (CR_G candidates per step, all their loads in flight)
+    const float* q = Q + row * (int64_t)d;
+    uint64_t best = ~0ull;  // this lane's entry of the sorted best-32 (key << 32 | idx)
+    for (int g = 0; g < nr; g += 32) {
+        uint64_t mine = ~0ull;
+        for (int t0 = 0; t0 < 32 && g + t0 < nr; t0 += CR_G) {
+            const float* xr[CR_G];
+            uint32_t id[CR_G];
+            #pragma unroll
+            for (int u = 0; u < CR_G; ++u) {
+                const int c = g + t0 + u;
+                id[u] = rlist[w][c < nr ? c : g + t0];
+                xr[u] = X + (int64_t)id[u] * d;
+            }
+            float acc[CR_G];
+            #pragma unroll
+            for (int u = 0; u < CR_G; ++u) acc[u] = 0.0f;
+            if (vec & 1) {
+                for (int t = 4 * lane; t < d; t += 256) {
+                    const bool two = t + 128 < d;
+                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + t));
+                    const float4 qv2 = two ? __ldg(reinterpret_cast<const float4*>(q + t + 128)) : qv;
+                    float4 xv[CR_G], xv2[CR_G];
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) {
+                        xv[u] = __ldg(reinterpret_cast<const float4*>(xr[u] + t));
+                        xv2[u] = two ? __ldg(reinterpret_cast<const float4*>(xr[u] + t + 128)) : qv2;
+                    }
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) {
+                        const float e0 = qv.x - xv[u].x, e1 = qv.y - xv[u].y;
+                        const float e2 = qv.z - xv[u].z, e3 = qv.w - xv[u].w;
+                        const float f0 = qv2.x - xv2[u].x, f1 = qv2.y - xv2[u].y;
+                        const float f2_ = qv2.z - xv2[u].z, f3 = qv2.w - xv2[u].w;
+                        acc[u] = fmaf(e0, e0, acc[u]);
+                        acc[u] = fmaf(e1, e1, acc[u]);
+                        acc[u] = fmaf(e2, e2, acc[u]);
+                        acc[u] = fmaf(e3, e3, acc[u]);
+                        acc[u] = fmaf(f0, f0, acc[u]);
+                        acc[u] = fmaf(f1, f1, acc[u]);
+                        acc[u] = fmaf(f2_, f2_, acc[u]);
+                        acc[u] = fmaf(f3, f3, acc[u]);
+                    }
+                }
+            } else {
+                for (int t = lane; t < d; t += 32) {
+                    const float qv = __ldg(q + t);
+                    float xv[CR_G];
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) xv[u] = __ldg(xr[u] + t);
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) {
+                        const float e = qv - xv[u];
+                        acc[u] = fmaf(e, e, acc[u]);
+                    }
+                }
+            }
+            // butterfly reduce-scatter of the 8 sums (9 shuffles): lanes 4u..4u+3 end with
+            // candidate u's total
+            static_assert(CR_G == 8, "reduce-scatter is written for 8 candidates");
+            float a4[4], a2[2];
+            {
+                const bool b = lane & 16;
+                #pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float send = b ? acc[i] : acc[i + 4], keep = b ? acc[i + 4] : acc[i];
+                    a4[i] = keep + __shfl_xor_sync(FULL, send, 16);
+                }
+            }
+            {
+                const bool b = lane & 8;
+                #pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float send = b ? a4[i] : a4[i + 2], keep = b ? a4[i + 2] : a4[i];
+                    a2[i] = keep + __shfl_xor_sync(FULL, send, 8);
+                }
+            }
+            float tot;
+            {
+                const bool b = lane & 4;
+                const float send = b ? a2[0] : a2[1], keep = b ? a2[1] : a2[0];
+                tot = keep + __shfl_xor_sync(FULL, send, 4);
+            }
+            tot += __shfl_xor_sync(FULL, tot, 2);
+            tot += __shfl_xor_sync(FULL, tot, 1);
+            const float su = __shfl_sync(FULL, tot, ((lane - t0) & 7) * 4);
+            if (lane >= t0 && lane < t0 + CR_G && g + lane < nr) {
+                const float val = metric == 1 ? sqrtf(su) : su;
+                mine = (uint64_t)ukey(val) << 32 | rlist[w][g + lane];
+            }
+        }
+        uint64_t b[1] = {mine};
+        ws::warp_bitonic<1>(b);
+        const uint64_t br = __shfl_sync(FULL, b[0], 31 - lane);
+        uint64_t c = best < br ? best : br;
+        #pragma unroll
+        for (int stride = 16; stride > 0; stride >>= 1) {
+            const uint64_t o = __shfl_xor_sync(FULL, c, stride);
+            c = (lane & stride) ? (o > c ? o : c) : (o < c ? o : c);
+        }
+        best = c;
+    }
+    // 4. certificate, output
+    const float vk = ukey_to_float((uint32_t)(__shfl_sync(FULL, best, k - 1) >> 32));
+    const double dk = metric == 1 ? (double)vk * vk : (double)vk;
+    if (!(dk * (1.0 + 2.0 * rerr + 0x1p-20) <= (double)__ldg(thr + row))) {
+        if (lane == 0) atomicOr(flag, 2);
+        return;
+    }
+    if (lane < k) {
+        out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)best + idx_offset);
+        out_dist[row * k + lane] = ukey_to_float((uint32_t)(best >> 32));
+    }
+}
+
 int next_pow2(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -2505,6 +2715,24 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ck
     candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, ckey, cidx, cap, M, k, KP,
                                                                           idx_offset, out_idx, out_dist, flag,
                                                                           warp ? redo : nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+                                       int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
+                                       const float* X, int32_t d, const float* qn, const float* xn,
+                                       const float* thr, float margin, int32_t metric, int32_t* out_idx,
+                                       float* out_dist, int32_t* flag, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    if (k < 1 || k > 32 || metric < 0 || metric > 1) return cudaErrorInvalidValue;
+    // relative error bound of the fp32 re-evaluation: d/32 sequential fmas per lane, a
+    // 5-level shuffle tree, the difference and (L2) the sqrt, each 2^-24 relative
+    const float rerr = (float)(((d + 31) / 32 + 8) * std::ldexp(1.0, -24));
+    const int vec = ((d % 4 == 0) && ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(X)) & 15) == 0) |
+                    (getenv_flag("KNN_RECOMP_STATS") ? 2 : 0);
+    candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, ckey, cidx, cap, M, k, idx_offset, Q,
+                                                                       X, d, qn, xn, thr, margin, rerr, metric, vec,
+                                                                       out_idx, out_dist, flag);
     return cudaGetLastError();
 }
 

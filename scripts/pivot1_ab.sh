@@ -1,0 +1,4 @@
+for cfg in "65536 256 32 0" "65536 256 32 1" "20000 48 10 0 gauss" "32768 64 16 1 clusters"; do
+  timeout 300 python scripts/pivot1_check.py $cfg 2>&1 | tail -2
+  KNN_PIVOT_EXACT3=1 timeout 300 python scripts/pivot1_check.py $cfg 2>&1 | tail -2
+done

@@ -596,3 +596,53 @@ def test_c_example_runs(tmp_path):
                          env=dict(os.environ, LD_LIBRARY_PATH=libdir + ":" + os.environ.get("LD_LIBRARY_PATH", "")))
     assert out.returncode == 0, out.stderr
     assert "point 0:" in out.stdout and "host-buffer API" in out.stdout
+
+
+# ------------------------- single-product partition + re-evaluation (opt-in, KNN_PIVOT1) ---
+_PIVOT1_CODE = """
+import sys, numpy as np, torch
+from paper_1309_5478_b200 import knn, datagen
+N, d, k, metric, dist, nq = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5], int(sys.argv[6])
+X = torch.from_numpy(datagen.points(N, d, dist, seed=N + d)).cuda()
+if nq:
+    Q = torch.from_numpy(datagen.points(nq, d, dist, seed=N + d + 1)).cuda()
+    gi, gd = knn.search_block(Q, X, k, metric=metric)
+else:
+    gi, gd = knn.graph(X, k, metric=metric)
+np.save(sys.argv[7], np.stack([gi.cpu().numpy().astype(np.float64), gd.cpu().numpy().astype(np.float64)]))
+print(knn.last_plan(), knn.last_candidates())
+"""
+
+
+@pytest.mark.parametrize("N,d,k,metric,dist,nq", [(65536, 256, 32, 0, "uniform", 0), (20000, 48, 10, 0, "gauss", 0),
+                                                  (32768, 64, 16, 1, "uniform", 0), (40000, 36, 20, 1, "gauss", 3000),
+                                                  (24576, 30, 7, 0, "clusters", 0)])
+def test_pivot1_single_product_partition_vs_oracle(N, d, k, metric, dist, nq, tmp_path):
+    """KNN_PIVOT1=1: the partition from the single hi.hi product keeps every
+    element whose lower bound reaches the pivot; the survivors near the k-th are re-evaluated
+    in fp32 from the inputs.  Checked against the oracle on sampled rows, and the values
+    against the oracle's fp64 distances of the returned pairs (relative error <= (d/32 + 8)
+    2^-24, tighter than the split GEMM's)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "r.npy")
+    r = subprocess.run([sys.executable, "-c", _PIVOT1_CODE, str(N), str(d), str(k), str(metric), dist, str(nq), out],
+                       check=True, cwd=root, timeout=600, env=dict(os.environ, KNN_PIVOT1="1"),
+                       capture_output=True, text=True)
+    plan = int(r.stdout.split()[0])
+    assert plan in (3, 4) or dist == "clusters", plan  # clusters: wide bounds may fall back
+    res = np.load(out)
+    gi, gd = res[0].astype(np.int64), res[1].astype(np.float32)
+    X = datagen.points(N, d, dist, seed=N + d)
+    Q = datagen.points(nq, d, dist, seed=N + d + 1) if nq else X
+    M = len(Q)
+    rows = np.arange(0, M, max(1, M // 61))
+    D64 = oracle.dist_rows(Q, X, rows=rows)
+    res_chk = checks.check_rows(gi[rows], gd[rows], D64, oracle.sqnorms(Q)[rows], oracle.sqnorms(X), rows, k,
+                                metric=metric, graph=not nq)
+    assert res_chk["failures"] == [], res_chk["failures"][:3]
+    ex = np.take_along_axis(D64, gi[rows], axis=1)
+    if metric == 1:
+        ex = np.sqrt(ex)
+    if plan in (3, 4):
+        bound = ((d + 31) // 32 + 8) * 2.0 ** -24 * (0.5 if metric == 1 else 1.0) + 2.0 ** -24
+        assert np.all(np.abs(gd[rows] - ex) <= bound * ex + 1e-30)
