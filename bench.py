@@ -290,7 +290,11 @@ def run_ours(args):
     def tkey(kernel):
         return kernel + "_c4" if args.config == "C4" and kernel.startswith("dist_tc_kernel") else kernel
 
-    def tensor_roof(name, kernel, ms, n, rows_per_launch):
+    # KNN_PIVOT1=1 (opt-in): the k <= 32 partition runs on the single hi.hi product and the
+    # candidate select re-evaluates the survivors
+    pivot1 = os.environ.get("KNN_PIVOT1", "0") not in ("", "0") and k <= 32 and plan_code in (3, 4)
+
+    def tensor_roof(name, kernel, ms, n, rows_per_launch, products=3):
         avg = ms / max(n, 1)
         pairs = rows_per_launch * N
         if plan_code in (2, 3) and kernel != "dist_tc_kernel_sample":
@@ -298,7 +302,7 @@ def run_ours(args):
             # the ranks by Par-3)
             nblk = -(-N // 256)
             pairs = nblk * (nblk + 1) / 2 * 256.0 * 256.0 / (world if sym_shard else 1)
-        flop = 3 * 2.0 * pairs * d_pad  # 3 fp16 products per multiply-add
+        flop = products * 2.0 * pairs * d_pad  # fp16 products per multiply-add (3: split)
         useful = 2.0 * rows_per_launch * N * d  # the dot products the path delivers
         r = {"kernel": name, "bound": "tensor", "achieved": flop / (avg * 1e-3) / 1e12,
              "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
@@ -326,8 +330,10 @@ def run_ours(args):
     p_ms, p_n = prof["prep"]
     if f_n and plan_code in (3, 4):
         rooflines.append((f_ms, tensor_roof(
-            "dist_tc_kernel<PIVOT%s> (a-S5: GEMM with the quickselect partition in its epilogue)"
-            % (",SYM" if plan_code == 3 else ""), "dist_tc_kernel", f_ms, f_n, R_local)))
+            "dist_tc_kernel<PIVOT%s%s> (a-S5: GEMM with the quickselect partition in its epilogue%s)"
+            % ("1" if pivot1 else "", ",SYM" if plan_code == 3 else "",
+               ", single hi.hi product" if pivot1 else ""), "dist_tc_kernel", f_ms, f_n, R_local,
+            products=1 if pivot1 else 3)))
     elif f_n:
         rooflines.append((f_ms, tensor_roof("knn_fused_kernel (a-S5: a-S3 GEMM + a-S4 select in the epilogue)",
                                             "knn_fused_kernel", f_ms, f_n, R_local)))
@@ -378,7 +384,8 @@ def run_ours(args):
                                          R_local / sl * (N * 4.0 + k * 8.0))))
     if m_n and plan_code in (3, 4):
         cands = knn.last_candidates()  # survivors of the partition (whole call)
-        cs_name = "candidate_select_kernel" if k <= 32 else "candidate_select_large_kernel"
+        cs_name = ("candidate_recompute_kernel" if pivot1 else "candidate_select_kernel") if k <= 32 \
+            else "candidate_select_warp_kernel"
         rooflines.append((m_ms, hbm_roof(f"{cs_name} (exact select of the partition)",
                                          cs_name, m_ms, m_n,
                                          cands * 8.0 + R_local * (4.0 + k * 8.0))))

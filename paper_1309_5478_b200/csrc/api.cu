@@ -338,6 +338,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         // 1. sample pass: per-row minima of 32-column chunks over the first Ssamp corpus
         //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
         {
+            ctx->launches++;  // (not timed separately)
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Ssamp, d_pad, smp.hi, smp.lo,
                                                smp.sqn, smp.rs, smax, s));
             for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
@@ -362,6 +363,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             const float f = 1.0f - knn::pivot1_margin(d_pad);
             KNN_CUDA(knn::launch_scale_norms(px.sqn, nsc_x, round_up(N, knn::kColPad), f, s));
             if (!same) KNN_CUDA(knn::launch_scale_norms(pq.sqn, nsc_q, round_up(M, knn::kColPad), f, s));
+            ctx->launches += same ? 1 : 2;
             op.qn = same ? nsc_x : nsc_q;
             op.xn = nsc_x;
         }
@@ -388,6 +390,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         // 1. sample: single-product upper bounds of the rows against the first Sq columns
         //    (the self pair +inf), 2. pivots, 3. partition GEMM, 4. exact select (k > 32)
         {
+            ctx->launches++;  // (not timed separately)
             KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Sq, d_pad, smp.hi, smp.lo,
                                                smp.sqn, smp.rs, nullptr, s));
             KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
@@ -411,6 +414,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                                            flag, ctx->num_sms, s));
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
+        ctx->launches++;  // warp-per-row select + the CTA kernel for its redo rows
         KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, capq, M, k, idx_offset, out_idx, out_dist,
                                                     flag, redo, s));
         tc2.done();
@@ -1022,6 +1026,7 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     ctx->prep_N = N;
     ctx->prep_d = d;
     ctx->prep_metric = metric;
+    ctx->launches++;
     KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo, smp.sqn,
                                        smp.rs, small ? smax : nullptr, s));
     knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, px.sqn + row0, px.rs + row0, rows,

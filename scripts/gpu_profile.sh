@@ -21,7 +21,7 @@ cap candsel "candidate_select"
 cap prep "prep_kernel"
 # C4 (k = 1024): the quantile-pivot plan's own kernels
 B="python bench.py --config C4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
-cap c4_candsel "candidate_select_large"
+cap c4_candsel "candidate_select_warp"
 cap c4_pivot "pivot_from_sample"
 cap c4_sample "\(int\)3, knn::tc::TileSched"
 cap c4_partition "SymSched"

@@ -19,7 +19,7 @@ P = os.path.join(ROOT, "profiles")
 KEYS = {"partition": "dist_tc_kernel", "sample": "dist_tc_kernel_sample", "pivot": "pivot_from_mins_kernel",
         "candsel": "candidate_select_kernel", "prep": "prep_kernel",
         # C4 (k = 1024, quantile pivot): keys distinct from the headline's
-        "c4_candsel": "candidate_select_large_kernel", "c4_pivot": "pivot_from_sample_kernel",
+        "c4_candsel": "candidate_select_warp_kernel", "c4_pivot": "pivot_from_sample_kernel",
         "c4_sample": "dist_tc_kernel_sample_c4", "c4_partition": "dist_tc_kernel_c4"}
 summ, traffic = [], {}
 for rep, key in KEYS.items():
