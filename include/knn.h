@@ -251,11 +251,22 @@ int64_t knn_launch_count(knn_ctx_t ctx);
  * (gemm_tc.cu), 1 = SIMT FP32 FFMA (gemm_simt.cu; selected by env KNN_GEMM=simt at
  * ctx creation, or when the device is not sm_100). */
 int knn_gemm_path(knn_ctx_t ctx);
-/* Plan of the top-level calls: KNN_PLAN_AUTO (default; currently the materialised
- * distances + select plan, which measures faster on B200), KNN_PLAN_FUSED (fused.cu:
- * GEMM with the select in its epilogue, the distance matrix never reaches HBM; used for
- * k <= 32 on the tensor-core path), KNN_PLAN_MATERIALISED.  Env KNN_FUSED=1 / 0 at ctx
- * creation selects FUSED / MATERIALISED.  All plans give bit-identical results. */
+/* Plan of the top-level calls (PAPER.md:56 quick multi-select):
+ * KNN_PLAN_AUTO (default): for N >= 16384 and M >= 256 on the tensor-core path the pivot
+ * (partition) plan — a sampled per-row pivot, the GEMM epilogue keeping only elements below
+ * it, an exact select of the candidates, the call redone on the full matrix if a row's
+ * certificate fails; otherwise the materialised distances (symmetric upper-triangle GEMM
+ * for the k-NNG) + select.  KNN_PLAN_FUSED (fused.cu: per-row lists in the GEMM epilogue,
+ * k <= 32, opt-in), KNN_PLAN_MATERIALISED (never the pivot plan).  All plans give
+ * bit-identical results.
+ * Environment, read at ctx creation: KNN_FUSED=1 / 0 (FUSED / MATERIALISED), KNN_PIVOT=0
+ * (no pivot plan), KNN_SYM=0 (no symmetric GEMM), KNN_PIVOT_DIV=n (sample N/n columns,
+ * default 8), KNN_PIVOT_CAP (candidate list capacity), KNN_D_BUDGET_MB (distance block
+ * budget), KNN_GEMM=simt (FFMA cross-check GEMM), KNN_PIVOT_MARGIN (tests: override the
+ * sample's error margin), KNN_PIVOT1=1 (k <= 32, L2: partition from the single hi.hi
+ * product with an error bound and the survivors near the k-th re-evaluated in fp32 from
+ * the inputs — faster and more accurate, but its values are not bit-identical to the
+ * other plans'; off by default). */
 typedef enum { KNN_PLAN_AUTO = 0, KNN_PLAN_FUSED = 1, KNN_PLAN_MATERIALISED = 2 } knn_plan;
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
 /* 1 if the top-level calls run the fused plan for this k under the current setting. */
