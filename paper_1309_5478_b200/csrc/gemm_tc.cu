@@ -100,6 +100,25 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
 // col, key) and flushed to the global per-row lists in batches of up to PEND_CAP, four
 // returning atomics in flight per lane, so their latency is paid once per batch.
 constexpr int PEND_CAP = 320;  // 3 x 320 x 4 B in one 4 KB staging buffer
+
+// Per-mode epilogue shape.  The partition (PIVOT) epilogue is latency-bound (2 warps per
+// SM sub-partition issue ~45% of cycles), so it runs 12 warps — 3 per TMEM lane quadrant,
+// owning 3/3/2 of the tile's eight 32-column chunks — with a smaller pending list and a
+// 3-deep column ring to fit the shared memory; the other modes keep 8 warps (BN/2 each).
+template <int MODE>
+struct EpiCfg {
+    static constexpr bool PV = MODE == 1 || MODE == 5;  // MODE_PIVOT, MODE_PIVOT1
+    static constexpr int WARPS = PV ? 12 : EPI_WARPS;
+    static constexpr int PARTS = WARPS / 4;
+    static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
+    static constexpr int PEND = PV ? 160 : PEND_CAP;
+    static constexpr int SLAB = PV ? STG_BYTES + 3 * PEND * 4 : 2 * STG_BYTES;  // per warp
+    static constexpr int NCOLS = PV ? 3 : NCOL;
+    static constexpr int THREADS = 64 + 32 * WARPS + 32;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
+    static_assert(SMEM <= 232448, "shared memory");
+    static_assert(SLAB % 16 == 0, "slab alignment");
+};
 __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* prow, const uint32_t* pcol,
                                             const uint32_t* pkey, int n) {
     const int lane = threadIdx.x & 31;
@@ -144,7 +163,7 @@ enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL
 // frees the accumulator, so the kernel runs at the mainloop's own rate.
 
 template <int METRIC, bool SYM, int MODE, class Sched>
-__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(EpiCfg<MODE>::THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                const __grid_constant__ CUtensorMap map_d, int use_tma_store, int num_kb,
@@ -156,6 +175,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     constexpr bool MINS = MODE == MODE_MINS;
     constexpr bool SAMPLE = MODE == MODE_SAMPLE;
     constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
+    using E = EpiCfg<MODE>;
+    constexpr int NCOL = E::NCOLS;
+    constexpr int EPI_WARPS = E::WARPS;
+    constexpr int COL_WARP = 2 + EPI_WARPS;
+    constexpr int PEND_CAP = E::PEND;
     // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
     constexpr int NSEG = MINS || SAMPLE || PIVOT1 ? 1 : 3;
     constexpr int KSTAGES = NSEG == 1 ? 2 * STAGES : STAGES;
@@ -166,8 +190,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
-    uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][2] output chunks
-    float* col_base = reinterpret_cast<float*>(stg_base + EPI_WARPS * 2 * STG_BYTES);  // [NCOL][3][BN]
+    uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS] slabs of E::SLAB bytes
+    float* col_base = reinterpret_cast<float*>(stg_base + EPI_WARPS * E::SLAB);  // [NCOL][3][BN]
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(col_base) + NCOL * COL_BYTES);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * KSTAGES + 4);
     const uint32_t colfull0 = smem_u32(bars + 2 * KSTAGES + 5);
@@ -222,14 +246,17 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------ epilogue (8 warps) --
+        // -------------------------------------------- epilogue (EPI_WARPS warps) --
         const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;           // which BN/2 columns it owns
+        const int part = (warp - 2) >> 2;           // which chunks of 32 columns it owns
+        const int ch0 = part * E::CPW;
+        const int nch = (BN / 32 - ch0) < E::CPW ? (BN / 32 - ch0) : E::CPW;
+        uint8_t* slab = stg_base + (warp - 2) * E::SLAB;
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
         // PIVOT: the warp's pending-candidate list lives in its second staging buffer
-        uint32_t* prow = reinterpret_cast<uint32_t*>(stg_base + ((warp - 2) * 2 + 1) * STG_BYTES);
+        uint32_t* prow = reinterpret_cast<uint32_t*>(slab + STG_BYTES);
         uint32_t* pcol = prow + PEND_CAP;
         uint32_t* pkey = pcol + PEND_CAP;
         int pend_n = 0;  // warp-uniform
@@ -253,10 +280,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const float xmx = MINS ? __ldg(ep.xmax) : 0.0f;
             const float mins_row_term = MINS ? fmaf(ep.margin, qn + xmx, qn) * (1.0f + 0x1p-22f) : 0.0f;
             const float mins_cos_cap = MINS ? fmaf(ep.margin, qn + xmx, 3.0f) : 0.0f;
-            const int64_t c_lo = n0 + half * (BN / 2);
-            // does this warp's 32x(BN/2) block touch the excluded self pairs?
+            const int64_t c_lo = n0 + ch0 * 32;
+            // does this warp's 32 x (32 nch) block touch the excluded self pairs?
             const bool diag = ep.self_shift != INT64_MIN &&
-                              row0 + ep.self_shift < c_lo + BN / 2 && row0 + 31 + ep.self_shift >= c_lo;
+                              row0 + ep.self_shift < c_lo + 32 * nch && row0 + 31 + ep.self_shift >= c_lo;
             const int64_t self_col = row + ep.self_shift;
             float* drow = ep.D + row * ep.ldD;
         for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
@@ -270,12 +297,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             mbar_wait(colfull0 + 8 * slot, (it / NCOL) & 1);
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + half * (BN / 2);
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + ch0 * 32;
             #pragma unroll 1
-            for (int ch = 0; ch < BN / 64; ++ch) {
+            for (int ch = 0; ch < nch; ++ch) {
                 uint32_t r[32];
                 tmem_ld32(taddr + ch * 32, r);
-                if (ch == BN / 64 - 1) {
+                if (ch == nch - 1) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
@@ -284,7 +311,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     asm volatile("" ::"r"(r[0]), "r"(r[31]));  // keep the TMEM load
                     continue;
                 }
-                const int cb = half * (BN / 2) + ch * 32;  // first column of the chunk in the tile
+                const int cb = (ch0 + ch) * 32;  // first column of the chunk in the tile
                 const float4* cn4 = reinterpret_cast<const float4*>(col_n + cb);
                 const float4* cs4 = reinterpret_cast<const float4*>(col_s + cb);
                 if constexpr (MINS) {
@@ -433,7 +460,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
                     // stage the chunk's values (swizzled, conflict-free) so that each lane can
                     // walk its own survivors with dynamic indices
-                    float* svp = reinterpret_cast<float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    float* svp = reinterpret_cast<float*>(slab);
                     const uint32_t sv = smem_u32(svp);
                     #pragma unroll
                     for (int u = 0; u < 8; ++u)
@@ -498,7 +525,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     // diagonal: produced by the mirror chunk.  Above: stored directly and
                     // transposed.  On it: lower triangle mirrored from the upper in smem.
                     if (c0 < row0) continue;
-                    const uint32_t sd = smem_u32(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                    const uint32_t sd = smem_u32(slab);
                     const uint32_t st = sd + STG_BYTES;
                     if (lane == 0) bulk_wait_read<0>();  // both buffers' previous stores read
                     __syncwarp();
@@ -508,7 +535,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                                v[4 * u + 2], v[4 * u + 3]);
                     if (c0 == row0) {
                         __syncwarp();
-                        float* sp = reinterpret_cast<float*>(stg_base + ((warp - 2) * 2) * STG_BYTES);
+                        float* sp = reinterpret_cast<float*>(slab);
                         for (int j = 0; j < lane; ++j)  // (lane, j) <- (j, lane)
                             sp[lane * 32 + (((j >> 2) ^ (lane & 7)) << 2) + (j & 3)] =
                                 sp[j * 32 + (((lane >> 2) ^ (j & 7)) << 2) + (lane & 3)];
@@ -553,7 +580,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     // rows >= M / columns >= N are clipped by the TMA unit.
                     if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store read
                     __syncwarp();
-                    const uint32_t sbuf = smem_u32(stg_base + ((warp - 2) * 2 + sbsel) * STG_BYTES);
+                    const uint32_t sbuf = smem_u32(slab + sbsel * STG_BYTES);
                     #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         sts128(sbuf + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
@@ -806,19 +833,21 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
         const int64_t units = sched.u_hi - sched.u_lo;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
         auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<MODE == MODE_PIVOT ? 2 : 0, true, MODE, SymSched> : dist_tc_kernel<0, true, MODE, SymSched>;
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EpiCfg<MODE>::SMEM)) !=
+            cudaSuccess)
             return e;
-        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
-                                                                    sched, ep);
+        kern<<<(unsigned)(pairs * CLUSTER), EpiCfg<MODE>::THREADS, EpiCfg<MODE>::SMEM, s>>>(
+            mqh, mql, mxh, mxl, md, 0, op.d_pad / BK, sched, ep);
     } else {
         TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ceil_div(op.N, BN)};
         const int64_t units = sched.n_mp * sched.n_nb;
         const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
         auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<MODE == MODE_PIVOT ? 2 : 0, false, MODE, TileSched> : dist_tc_kernel<0, false, MODE, TileSched>;
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EpiCfg<MODE>::SMEM)) !=
+            cudaSuccess)
             return e;
-        kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
-                                                                    sched, ep);
+        kern<<<(unsigned)(pairs * CLUSTER), EpiCfg<MODE>::THREADS, EpiCfg<MODE>::SMEM, s>>>(
+            mqh, mql, mxh, mxl, md, 0, op.d_pad / BK, sched, ep);
     }
     return cudaGetLastError();
 }
