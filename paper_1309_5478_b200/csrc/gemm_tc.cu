@@ -249,8 +249,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         // -------------------------------------------- epilogue (EPI_WARPS warps) --
         const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
         const int part = (warp - 2) >> 2;           // which chunks of 32 columns it owns
-        const int ch0 = part * E::CPW;
-        const int nch = (BN / 32 - ch0) < E::CPW ? (BN / 32 - ch0) : E::CPW;
+        int wi = 0;  // work items seen: rotates the short share of chunks among the warps
         uint8_t* slab = stg_base + (warp - 2) * E::SLAB;
         const bool vec_ok = (ep.ldD % 4) == 0 && ((reinterpret_cast<uintptr_t>(ep.D) & 15) == 0);
         int sbsel = 0;  // which of the warp's two staging buffers
@@ -263,9 +262,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         __shared__ int s_pend[EPI_WARPS];  // PIVOT: each warp's pending-list length (slot allocator)
         if (PIVOT && lane == 0) s_pend[warp - 2] = 0;
         __syncwarp();
-        for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+        for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++wi) {
             const tc::Unit w = sched.unit(cur);
             const int cls = tile_class(w.mp, w.nb0, ml_shift);
+            // this warp's chunks of the tile (3 warps per quadrant: 3/3/2, the short share
+            // rotating per work item so that a warp can run ahead into the other accumulator)
+            const int ch0 = ((E::PV ? part + wi : part) % E::PARTS) * E::CPW;
+            const int nch = (BN / 32 - ch0) < E::CPW ? (BN / 32 - ch0) : E::CPW;
             const int64_t nb = w.nb0;
             const int64_t mb = 2 * w.mp + crank;
             const int64_t n0 = nb * BN;
