@@ -101,6 +101,50 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
 // returning atomics in flight per lane, so their latency is paid once per batch.
 constexpr int PEND_CAP = 320;  // 3 x 320 x 4 B in one 4 KB staging buffer
 
+// Deferred flush (PIVOT modes): the pending list is moved into registers (J entries per
+// lane) and its slots reserved with returning atomics, but the entries are written only at
+// the next flush, when those atomics have long returned — the warp never waits for them.
+template <int J>
+struct DeferredFlush {
+    uint32_t r[J], c[J], k[J];
+    int pos[J];
+    __device__ __forceinline__ void init() {
+        #pragma unroll
+        for (int j = 0; j < J; ++j) pos[j] = -1;
+    }
+    __device__ __forceinline__ void complete(const EpiArgs& ep) {
+        #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            if (pos[j] >= 0) {
+                if (pos[j] < ep.cap) {
+                    ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = k[j];
+                    ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = c[j];
+                } else {
+                    *ep.flag |= 2;
+                }
+            }
+            pos[j] = -1;
+        }
+    }
+    __device__ __forceinline__ void flush(const EpiArgs& ep, const uint32_t* prow, const uint32_t* pcol,
+                                          const uint32_t* pkey, int n) {
+        const int lane = threadIdx.x & 31;
+        complete(ep);
+        __syncwarp();
+        #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int i = 32 * j + lane;
+            if (i < n) {
+                r[j] = prow[i];
+                c[j] = pcol[i];
+                k[j] = pkey[i];
+                pos[j] = atomicAdd(ep.cnt + r[j], 1);
+            }
+        }
+        __syncwarp();
+    }
+};
+
 // Per-mode epilogue shape.  The partition (PIVOT) epilogue is latency-bound (2 warps per
 // SM sub-partition issue ~45% of cycles), so it runs 12 warps — 3 per TMEM lane quadrant,
 // owning 3/3/2 of the tile's eight 32-column chunks — with a smaller pending list and a
@@ -259,6 +303,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         uint32_t* pcol = prow + PEND_CAP;
         uint32_t* pkey = pcol + PEND_CAP;
         int pend_n = 0;  // warp-uniform
+        DeferredFlush<(E::PEND + 31) / 32> dfl;  // PIVOT: the previous flush's entries
+        dfl.init();
         __shared__ int s_pend[EPI_WARPS];  // PIVOT: each warp's pending-list length (slot allocator)
         if (PIVOT && lane == 0) s_pend[warp - 2] = 0;
         __syncwarp();
@@ -483,7 +529,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     const int mine = __popc(hr) + __popc(hc);
                     const int total = __reduce_add_sync(0xFFFFFFFFu, mine);
                     if (pend_n + total > PEND_CAP) {
-                        if (!(ep.dbg & 8)) pivot_flush(ep, prow, pcol, pkey, pend_n);
+                        if (!(ep.dbg & 8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
                         pend_n = 0;
                         if (lane == 0) s_pend[warp - 2] = 0;
                     }
@@ -614,7 +660,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         }
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
-        if constexpr (PIVOT) pivot_flush(ep, prow, pcol, pkey, pend_n);
+        if constexpr (PIVOT) {
+            dfl.complete(ep);
+            pivot_flush(ep, prow, pcol, pkey, pend_n);
+        }
     }
     teardown(tmem_base);
 }
