@@ -2165,13 +2165,13 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
 // memory (L2) in three passes (key range; 1024-bucket histogram; scatter), no CTA
 // barriers.  Rows whose buckets are crowded, or whose keys are non-finite, are appended
 // to redo[1..] for the CTA kernel above.
-constexpr int CSW_WARPS = 8;
-constexpr int CSW_BINS = 1024;
+constexpr int CSW_WARPS = 4;  // 4-warp CTAs, 5 per SM (20 warps) with the 10.8 KB slabs
+constexpr int CSW_BINS = 1024;  // 16-bit counters, two per word (n <= cap < 2^16)
 constexpr int CSW_STAR = 64;
 constexpr int CSW_PASS = 16;
 constexpr int CSW_EPT = 8;
 __host__ __device__ constexpr size_t csw_slab_bytes(int KP) {
-    return (size_t)CSW_BINS * 4 + (size_t)KP * 8 + (size_t)CSW_STAR * 8 + 16;
+    return (size_t)CSW_BINS * 2 + (size_t)KP * 8 + (size_t)CSW_STAR * 8 + 16;
 }
 __global__ void __launch_bounds__(32 * CSW_WARPS)
 candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
@@ -2183,7 +2183,7 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
     uint8_t* slab = smem_raw + csw_slab_bytes(KP) * w;
     uint64_t* star = reinterpret_cast<uint64_t*>(slab);
     uint32_t* hist = reinterpret_cast<uint32_t*>(star + CSW_STAR);
-    uint32_t* okey = hist + CSW_BINS;
+    uint32_t* okey = hist + CSW_BINS / 2;
     uint32_t* oidx = okey + KP;
     int* nst = reinterpret_cast<int*>(oidx + KP);
     const int64_t gw = (int64_t)blockIdx.x * CSW_WARPS + w, nw = (int64_t)gridDim.x * CSW_WARPS;
@@ -2232,7 +2232,7 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
         auto bucket = [&](uint32_t key) -> uint32_t {
             return min((uint32_t)((ukey_to_float(key) - fmn) * scale), (uint32_t)(CSW_BINS - 1));
         };
-        for (int i = lane; i < CSW_BINS; i += 32) hist[i] = 0;
+        for (int i = lane; i < CSW_BINS / 2; i += 32) hist[i] = 0;
         if (lane == 0) *nst = 0;
         __syncwarp();
         // pass 2: histogram
@@ -2245,16 +2245,21 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
             }
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j)
-                if (base + 32 * j + lane < n) atomicAdd(&hist[bucket(kv[j])], 1u);
+                if (base + 32 * j + lane < n) {
+                    const uint32_t b = bucket(kv[j]);
+                    atomicAdd(&hist[b >> 1], 1u << ((b & 1) * 16));
+                }
         }
         __syncwarp();
         // exclusive offsets; b* = bucket of rank k; the largest bucket below b*
         constexpr int BPL = CSW_BINS / 32;
         uint32_t c[BPL], sum = 0;
         #pragma unroll
-        for (int j = 0; j < BPL; ++j) {
-            c[j] = hist[lane * BPL + j];
-            sum += c[j];
+        for (int j = 0; j < BPL; j += 2) {
+            const uint32_t wd = hist[(lane * BPL + j) >> 1];
+            c[j] = wd & 0xFFFFu;
+            c[j + 1] = wd >> 16;
+            sum += c[j] + c[j + 1];
         }
         uint32_t incl = sum;
         #pragma unroll
@@ -2265,7 +2270,7 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
         uint32_t run = incl - sum, mybin = 0xFFFFFFFFu, mybefore = 0, myn = 0;
         #pragma unroll
         for (int j = 0; j < BPL; ++j) {
-            hist[lane * BPL + j] = run;
+            if (j & 1) hist[(lane * BPL + j) >> 1] = (run << 16) | (run - c[j - 1]);
             if (mybin == 0xFFFFFFFFu && run < (uint32_t)k && (uint32_t)k <= run + c[j]) {
                 mybin = lane * BPL + j;
                 mybefore = run;
@@ -2301,7 +2306,8 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
                 if (base + 32 * j + lane >= n) continue;
                 const uint32_t b = bucket(kv[j]);
                 if (b < bstar) {
-                    const uint32_t pos = atomicAdd(&hist[b], 1u);
+                    const uint32_t sh = (b & 1) * 16;
+                    const uint32_t pos = (atomicAdd(&hist[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
                     okey[pos] = kv[j];
                     oidx[pos] = iv[j];
                 } else if (b == bstar) {
@@ -2687,7 +2693,9 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ck
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const bool warp = redo != nullptr && !getenv_flag("KNN_CANDSEL_CTA");
+    // warp per row while its slab fits and the 16-bit counters hold the list (always for
+    // the API's k <= 1024)
+    const bool warp = redo != nullptr && KP <= 2048 && cap < 65536 && !getenv_flag("KNN_CANDSEL_CTA");
     if (warp) {
         if ((e = cudaMemsetAsync(redo, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
         const size_t wsm = csw_slab_bytes(KP) * CSW_WARPS;
