@@ -482,8 +482,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         asm volatile("" ::"f"(v[0]), "f"(v[31]));
                         continue;
                     }
-                    // Kept iff u < pivot (strict; the pivots are strict upper bounds, see
-                    // DESIGN.md §6.5).  fl(u - t) is negative iff u < t (exact sign of a
+                    // Kept iff u < thr, i.e. u <= pivot: the pivot kernels store nextup(pivot)
+                    // in thr (select.cu).  fl(u - t) is negative iff u < t (exact sign of a
                     // rounded difference; inf - inf is the canonical, positive NaN), so each
                     // test is an FADD and a funnel shift of its sign bit into the mask, c
                     // descending so that bit c ends at position c.  (One combined test

@@ -1550,7 +1550,8 @@ pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M
     if (lane == 0 && row < M) {
         const float t = T == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(T);
         const float t1 = nextafterf(t, __int_as_float(0x7F800000));
-        thr[row] = metric == 1 ? __fmul_ru(t1, t1) : t;
+        // stored as nextup(pivot): the partition keeps u < thr, i.e. u <= pivot
+        thr[row] = nextafterf(metric == 1 ? __fmul_ru(t1, t1) : t, __int_as_float(0x7F800000));
         cnt[row] = 0;
     }
 }
@@ -1964,7 +1965,7 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
         }
         __syncthreads();
         if (s_nfin < r) {  // not reached for finite inputs (S - 1 >= r finite samples)
-            if (tid == 0) thr[row] = s_nfin ? ukey_to_float(sc.hi) : -__int_as_float(0x7F800000);
+            if (tid == 0) thr[row] = nextafterf(s_nfin ? ukey_to_float(sc.hi) : -__int_as_float(0x7F800000), __int_as_float(0x7F800000));
             __syncthreads();
             continue;
         }
@@ -2013,7 +2014,7 @@ pivot_from_sample_kernel(const float* __restrict__ Ds, int64_t M, int64_t S, int
         for (int o = 16; o > 0; o >>= 1) p = fmaxf(p, __shfl_xor_sync(FULL, p, o));
         if (lane == 0) atomicMax(reinterpret_cast<uint32_t*>(&sc.kept), ukey(p));
         __syncthreads();
-        if (tid == 0) thr[row] = ukey_to_float((uint32_t)sc.kept);
+        if (tid == 0) thr[row] = nextafterf(ukey_to_float((uint32_t)sc.kept), __int_as_float(0x7F800000));
         __syncthreads();
     }
 }
@@ -2059,7 +2060,7 @@ pivot_from_sample_warp_kernel(const float* __restrict__ Ds, int64_t M, int64_t S
             nfin += __shfl_xor_sync(FULL, nfin, o);
         }
         if (nfin < r) {  // not reached for finite inputs (S - 1 >= r finite samples)
-            if (lane == 0) thr[row] = nfin ? hi : -__int_as_float(0x7F800000);
+            if (lane == 0) thr[row] = nextafterf(nfin ? hi : -__int_as_float(0x7F800000), __int_as_float(0x7F800000));
             __syncwarp();
             continue;
         }
@@ -2097,7 +2098,7 @@ pivot_from_sample_warp_kernel(const float* __restrict__ Ds, int64_t M, int64_t S
             if (isfinite(x) && bucket(x) <= bstar) p = fmaxf(p, x);
         });
         for (int o = 16; o > 0; o >>= 1) p = fmaxf(p, __shfl_xor_sync(FULL, p, o));
-        if (lane == 0) thr[row] = p;
+        if (lane == 0) thr[row] = nextafterf(p, __int_as_float(0x7F800000));  // nextup: u < thr <=> u <= P
         __syncwarp();
     }
 }
