@@ -646,3 +646,23 @@ def test_pivot1_single_product_partition_vs_oracle(N, d, k, metric, dist, nq, tm
     if plan in (3, 4):
         bound = ((d + 31) // 32 + 8) * 2.0 ** -24 * (0.5 if metric == 1 else 1.0) + 2.0 ** -24
         assert np.all(np.abs(gd[rows] - ex) <= bound * ex + 1e-30)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_pivot_plan_zero_vectors_and_duplicates(metric):
+    """Zero-norm points (the single-product error bound vanishes, pivot = an exact value) and
+    exact duplicates: the partition keeps u <= pivot (thr = nextup(pivot), strict test), so
+    the pivot plan matches the materialised plan bit for bit."""
+    kn = knn()
+    X = datagen.points(20000, 24, "gauss", seed=91)
+    X[::3] = 0.0
+    X[1::7] = X[2::7][: len(X[1::7])] if len(X[2::7]) >= len(X[1::7]) else X[1::7]
+    Xt = cuda(np.ascontiguousarray(X))
+    gi, gd = kn.graph(Xt, 16, metric=metric)
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(Xt, 16, metric=metric)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri)
+    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
