@@ -1761,14 +1761,28 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
     }
     if (lane == 0 && (vec & 2))  // diagnostic (KNN_RECOMP_STATS): count |R| instead
         atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)nr);
-    if (nr > CR_RCAP) {  // pathological ties: redo the call on the full matrix
-        if (lane == 0) atomicOr(flag, 2);
-        return;
-    }
+    const int nr_total = nr;
     __syncwarp();
-    // 3. exact values, k smallest (CR_G candidates per step, all their loads in flight)
+    // 3. exact values, k smallest (CR_G candidates per step, all their loads in flight);
+    //    more than CR_RCAP members (wide bounds: data far from the origin) are processed in
+    //    windows of CR_RCAP, each re-collected by a scan of the list
     const float* q = Q + row * (int64_t)d;
     uint64_t best = ~0ull;  // this lane's entry of the sorted best-32 (key << 32 | idx)
+    for (int win = 0; win * CR_RCAP < nr_total; ++win) {
+    if (win > 0) {
+        __syncwarp();
+        int ridx = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int pos = base + lane;
+            const bool keep = pos < n && __ldg(rk + pos) <= Tf;
+            const uint32_t bm = __ballot_sync(FULL, keep);
+            const int slot = ridx + __popc(bm & ws::lanemask_lt()) - win * CR_RCAP;
+            if (keep && slot >= 0 && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + pos);
+            ridx += __popc(bm);
+        }
+        __syncwarp();
+    }
+    const int nr = nr_total - win * CR_RCAP < CR_RCAP ? nr_total - win * CR_RCAP : CR_RCAP;
     for (int g = 0; g < nr; g += 32) {
         uint64_t mine = ~0ull;
         for (int t0 = 0; t0 < 32 && g + t0 < nr; t0 += CR_G) {
@@ -1867,6 +1881,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
             c = (lane & stride) ? (o > c ? o : c) : (o < c ? o : c);
         }
         best = c;
+    }
     }
     // 4. certificate, output
     const float vk = ukey_to_float((uint32_t)(__shfl_sync(FULL, best, k - 1) >> 32));
