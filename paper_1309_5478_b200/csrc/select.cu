@@ -1688,7 +1688,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
 constexpr int CR_PER = 16;
 constexpr int CR_RCAP = 256;
 constexpr int CR_G = 8;
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
                            const uint32_t* __restrict__ cidx, int cap, int64_t M, int k, int64_t idx_offset,
                            const float* __restrict__ Q, const float* __restrict__ X, int d,
