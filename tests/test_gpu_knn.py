@@ -666,3 +666,31 @@ def test_pivot_plan_zero_vectors_and_duplicates(metric):
         kn.set_plan(kn.PLAN_AUTO)
     assert torch.equal(gi, ri)
     assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+_PIVOT1_BLOCK_CODE = """
+import sys, numpy as np, torch
+from paper_1309_5478_b200 import knn, datagen
+X = torch.from_numpy(datagen.points(20000, 40, "gauss", seed=95)).cuda()
+gi, gd = knn.search_block(X[5000:9000].contiguous(), X, 16, metric=int(sys.argv[2]), self_shift=5000, idx_offset=7)
+assert knn.last_plan() == 4, knn.last_plan()
+np.save(sys.argv[1], np.stack([gi.cpu().numpy().astype(np.float64), gd.cpu().numpy().astype(np.float64)]))
+"""
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_pivot1_shifted_block_vs_oracle(metric, tmp_path):
+    """KNN_PIVOT1=1 on a row block of the k-NNG (self pair j = i + 5000 excluded, indices
+    offset by 7): the re-evaluated lists are the oracle's nearest neighbours."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "b.npy")
+    subprocess.run([sys.executable, "-c", _PIVOT1_BLOCK_CODE, out, str(metric)], check=True, cwd=root, timeout=600,
+                   env=dict(os.environ, KNN_PIVOT1="1"))
+    res = np.load(out)
+    gi, gd = res[0].astype(np.int64) - 7, res[1].astype(np.float32)
+    X = datagen.points(20000, 40, "gauss", seed=95)
+    rows = np.arange(5000, 9000, 97)
+    D64 = oracle.dist_rows(X, X, rows=rows)
+    n = oracle.sqnorms(X)
+    chk = checks.check_rows(gi[rows - 5000], gd[rows - 5000], D64, n[rows], n, rows, 16, metric=metric, graph=True)
+    assert chk["failures"] == [], chk["failures"][:3]
