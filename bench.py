@@ -34,7 +34,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="H", help="H (headline) or C1..C5")
-    ap.add_argument("--plan", default="auto", choices=["auto", "fused", "materialised"])
+    ap.add_argument("--plan", default="auto", choices=["auto", "materialised"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -235,7 +235,7 @@ def run_ours(args):
             dist.barrier()
 
     assert knn.gemm_path() == 0 or os.environ.get("KNN_GEMM") == "simt", "tensor-core path expected"
-    knn.set_plan({"auto": knn.PLAN_AUTO, "fused": knn.PLAN_FUSED,
+    knn.set_plan({"auto": knn.PLAN_AUTO,
                   "materialised": knn.PLAN_MATERIALISED}[args.plan])
     for _ in range(args.warmup):
         step()

@@ -256,10 +256,11 @@ int knn_gemm_path(knn_ctx_t ctx);
  * (partition) plan — a sampled per-row pivot, the GEMM epilogue keeping only elements below
  * it, an exact select of the candidates, the call redone on the full matrix if a row's
  * certificate fails; otherwise the materialised distances (symmetric upper-triangle GEMM
- * for the k-NNG) + select.  KNN_PLAN_FUSED (fused.cu: per-row lists in the GEMM epilogue,
- * k <= 32, opt-in), KNN_PLAN_MATERIALISED (never the pivot plan).  All plans give
- * bit-identical results.
- * Environment, read at ctx creation: KNN_FUSED=1 / 0 (FUSED / MATERIALISED), KNN_PIVOT=0
+ * for the k-NNG) + select.  KNN_PLAN_MATERIALISED: never the pivot plan.  KNN_PLAN_FUSED
+ * is reserved: round 1's per-row-list fused kernel was retired (4.5x slower than the pivot
+ * plan, which is the fused GEMM+select); setting it returns KNN_ERR_UNSUPPORTED.  All
+ * plans give bit-identical results.
+ * Environment, read at ctx creation: KNN_FUSED=0 (MATERIALISED), KNN_PIVOT=0
  * (no pivot plan), KNN_SYM=0 (no symmetric GEMM), KNN_PIVOT_DIV=n (sample N/n columns,
  * default 8), KNN_PIVOT_CAP (candidate list capacity), KNN_D_BUDGET_MB (distance block
  * budget), KNN_GEMM=simt (FFMA cross-check GEMM), KNN_PIVOT_MARGIN (tests: override the
@@ -269,10 +270,8 @@ int knn_gemm_path(knn_ctx_t ctx);
  * other plans'; off by default). */
 typedef enum { KNN_PLAN_AUTO = 0, KNN_PLAN_FUSED = 1, KNN_PLAN_MATERIALISED = 2 } knn_plan;
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
-/* 1 if the top-level calls run the fused plan for this k under the current setting. */
-int knn_fused_plan(knn_ctx_t ctx, int32_t k);
 /* Plan the last top-level call of this ctx executed: 0 = blocked distances + select,
- * 1 = fused GEMM+select, 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
+ * 1 = (retired fused plan, never reported), 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
  * each written directly and transposed) + select, 3 = pivot plan,
  * symmetric, 4 = pivot plan, general block, -1 = none yet.  The pivot plan (k <= 32,
  * N >= 16384) is the quick multi-select partition of PAPER.md:56 applied at matrix scale:

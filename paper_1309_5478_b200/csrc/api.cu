@@ -57,6 +57,10 @@ struct knn_ctx {
     const float* prep_X = nullptr;
     int64_t prep_N = 0;
     int32_t prep_d = 0, prep_metric = -1;
+    // Par-3 phases: the input-validation flag of the prep passes run by knn_graph_pivots /
+    // knn_graph_partition (a dedicated slice: the workspace flag is reset by every call),
+    // reported by knn_graph_gather_select as KNN_ERR_NONFINITE
+    int32_t* pv_flag = nullptr;
     // CUDA IPC mappings opened by knn_ipc_open: handle bytes -> mapped base
     std::vector<std::pair<std::string, void*>> ipc_open;
 };
@@ -206,7 +210,6 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                      int32_t* out_idx, float* out_dist, cudaStream_t s, bool allow_pivot = true) {
     const bool same = (Q == X) && (M == N);
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
-    const bool fused = knn_fused_plan(ctx, k) == 1 && metric <= KNN_L2;  // fused.cu: L2 metrics
     // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = k-th smallest of
     // the minima of the 32-column chunks of a column sample (>= the row's k-th distance),
     // then the GEMM keeps only elements <= pivot.
@@ -216,12 +219,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     const int32_t kk = self_shift != KNN_NO_SELF ? k + 1 : k;
     // (fewer than 256 query rows fill less than one 2-CTA row-block pair: the sample pass
     // then costs as much as it saves; measured M = 8 vs N = 2^20: 0.66 vs 0.82 ms)
-    const bool pivot = allow_pivot && !fused && tc && ctx->pivot_ok && k <= 32 && N >= 16384 && M >= 256 &&
+    const bool pivot = allow_pivot && tc && ctx->pivot_ok && k <= 32 && N >= 16384 && M >= 256 &&
                        ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= kk + 1;
     // Quantile pivot for k > 32 (the same quickselect partition; the pivot is a bucketed
     // order statistic of a single-product sample of Sq columns)
     const int64_t Sq = round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
-    const bool pivotq = allow_pivot && !fused && tc && ctx->pivot_ok && k > 32 && N >= 16384 && M >= 256 &&
+    const bool pivotq = allow_pivot && tc && ctx->pivot_ok && k > 32 && N >= 16384 && M >= 256 &&
                         ctx->plan != KNN_PLAN_MATERIALISED && Sq <= (N / 256) * 256;
     int32_t rq = 0;
     if (pivotq) {
@@ -238,14 +241,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int64_t rows_blk = (int64_t)(ctx->d_budget / ((size_t)ldD * sizeof(float)));
     rows_blk = rows_blk < 128 ? 128 : (rows_blk / 128) * 128;
     if (rows_blk > M) rows_blk = M;
-    const int S = fused ? (int)knn::fused_actual_splits(N, knn::fused_splits(M, N, ctx->num_sms)) : 1;
-    if (fused) rows_blk = 0;  // no distance block
     // k-NNG with the transpose reuse of PAPER.md:83: only the upper triangle is multiplied
     // (bit-identical to the other plans thanks to the canonical orientation)
-    const bool sym = !fused && !pivot && !pivotq && tc && ctx->sym_ok && same && self_shift == 0 &&
+    const bool sym = !pivot && !pivotq && tc && ctx->sym_ok && same && self_shift == 0 &&
                      (size_t)N * ldD * sizeof(float) <= ctx->sym_budget;
     if (sym) rows_blk = M;
-    ctx->last_plan = fused ? 1 : pivot_sym ? 3 : (pivot || pivotq) ? 4 : sym ? 2 : 0;
+    ctx->last_plan = pivot_sym ? 3 : (pivot || pivotq) ? 4 : sym ? 2 : 0;
     // the pivot plans' sample storage is processed in row blocks of at most d_budget bytes
     const int64_t samp_row_bytes = pivot ? (Ssamp / 32) * 4 : pivotq ? Sq * 4 : 1;
     int64_t samp_blk = (int64_t)(ctx->d_budget / (size_t)samp_row_bytes);
@@ -269,8 +270,6 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     Prepared pq{}, px{};
     float* D = nullptr;
     int32_t* flag = nullptr;
-    int32_t* part_i = nullptr;
-    float* part_d = nullptr;
     float* thr = nullptr;
     int32_t* cnt = nullptr;
     uint32_t *ckey = nullptr, *cidx = nullptr;
@@ -280,11 +279,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
-        if (!fused && !pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 && !pivotq ? rows_blk : M) + 1);
-        if (fused && S > 1) {
-            part_i = c.take<int32_t>((size_t)S * M * k);
-            part_d = c.take<float>((size_t)S * M * k);
-        }
+        if (!pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 && !pivotq ? rows_blk : M) + 1);
         if (pivot || pivotq) {
             const int64_t Sx = pivot ? Ssamp : Sq;
             smax = c.take<float>(1);
@@ -319,21 +314,6 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, metric, s));
         t.done();
     }
-    if (fused) {
-        knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
-        Timed tf(ctx, KNN_KERNEL_FUSED, s);
-        KNN_CUDA(knn::launch_knn_fused(op, metric, self_shift, k, idx_offset, S,
-                                       S > 1 ? part_i : out_idx, S > 1 ? part_d : out_dist,
-                                       ctx->num_sms, s));
-        tf.done();
-        if (S > 1) {
-            int64_t zeros[64] = {0};
-            Timed tm(ctx, KNN_KERNEL_MERGE, s);
-            KNN_CUDA(knn::launch_merge(part_d, part_i, S, M, k, zeros, out_idx, out_dist, s));
-            tm.done();
-        }
-        return KNN_OK;
-    }
     if (pivot) {
         // 1. sample pass: per-row minima of 32-column chunks over the first Ssamp corpus
         //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
@@ -350,7 +330,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                                                   ctx->num_sms, s, smax));
                 tg.done();
                 Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
-                KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, kk, metric, thr + r0, cnt + r0, s));
+                KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, round_up(r0 + R, knn::kColPad) - r0, kk, metric,
+                                                         thr + r0, cnt + r0, s));
                 tp.done();
             }
         }
@@ -508,7 +489,6 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     if (g && strcmp(g, "simt") == 0) c->gemm_mode = 1;
     const char* fz = getenv("KNN_FUSED");
     if (fz && strcmp(fz, "0") == 0) c->plan = KNN_PLAN_MATERIALISED;
-    if (fz && strcmp(fz, "1") == 0) c->plan = KNN_PLAN_FUSED;
     const char* pv = getenv("KNN_PIVOT");
     if (pv && strcmp(pv, "0") == 0) c->pivot_ok = false;
     const char* pd = getenv("KNN_PIVOT_DIV");
@@ -547,6 +527,7 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
         if (ctx->ev_free[b]) cudaEventDestroy(ctx->ev_free[b]);
     }
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
+    if (ctx->pv_flag) cudaFree(ctx->pv_flag);
     delete ctx;
     return KNN_OK;
 }
@@ -555,16 +536,12 @@ const char* knn_last_error(knn_ctx_t ctx) { return ctx ? ctx->err.c_str() : "nul
 
 int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
-int knn_fused_plan(knn_ctx_t ctx, int32_t k) {
-    if (!ctx) return -1;
-    return (ctx->gemm_mode == 0 && ctx->tc_ok && ctx->plan == KNN_PLAN_FUSED && k >= 1 &&
-            k <= knn::fused_max_k()) ? 1 : 0;
-}
-
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan) {
     if (!ctx) return KNN_ERR_ARG;
     if (plan < KNN_PLAN_AUTO || plan > KNN_PLAN_MATERIALISED)
         return fail(ctx, KNN_ERR_ARG, "unknown plan %d", plan);
+    if (plan == KNN_PLAN_FUSED)  // the per-row-list fused kernel was retired
+        return fail(ctx, KNN_ERR_UNSUPPORTED, "KNN_PLAN_FUSED was retired; the pivot plan is the fused path");
     ctx->plan = plan;
     return KNN_OK;
 }
@@ -752,8 +729,17 @@ knn_status knn_search_streamed(knn_ctx_t ctx, const float* Q_host, int64_t M, co
     if (!graph) pin_q.pin(Q_host, (size_t)M * d * sizeof(float));
     cudaStream_t s = nullptr;
     KNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{s};
     cudaStream_t cs = ctx->copy_stream;
+    // on every exit (errors included) both streams drain before the host pins (declared
+    // above, destroyed after this guard) are released and st_buf can be reused
+    struct StreamGuard {
+        cudaStream_t s, cs;
+        ~StreamGuard() {
+            cudaStreamSynchronize(cs);
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } sg{s, cs};
     // chunk boundaries
     std::vector<int64_t> cb;
     for (int64_t c0 = 0; c0 < N; c0 += C) cb.push_back(c0);
@@ -969,6 +955,16 @@ int32_t knn_graph_list_cap(int32_t k) {
 }
 
 namespace {
+knn_status ensure_pv_flag(knn_ctx* ctx) {
+    if (ctx->pv_flag) return KNN_OK;
+    if (cudaMalloc(&ctx->pv_flag, 4 * sizeof(int32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->pv_flag = nullptr;
+        return fail(ctx, KNN_ERR_OOM, "cannot allocate the Par-3 flag");
+    }
+    return KNN_OK;
+}
+
 knn_status graph_shard_check(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric) {
     if (!ctx || !X) return KNN_ERR_ARG;
     if (N < 2 || d < 1 || k < 1 || k > N - 1) return fail(ctx, KNN_ERR_ARG, "bad N, d or k");
@@ -1017,9 +1013,11 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve);
     KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_TRY(ensure_pv_flag(ctx));
+    KNN_CUDA(cudaMemsetAsync(ctx->pv_flag, 0, 4 * sizeof(int32_t), s));
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, ctx->pv_flag, metric, s));
         t.done();
     }
     ctx->prep_X = X;  // knn_graph_partition may reuse px (same carve offsets, ws untouched)
@@ -1039,7 +1037,10 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     tg.done();
     Timed tp(ctx, KNN_KERNEL_SELECT, s);
     if (small) {
-        KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, rows, kk, metric, thr + row0, cnt, s));
+        KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, rows,
+                                                     // pad only to the absolute 256-row boundary
+                                                     round_up(row0 + rows, knn::kColPad) - row0, kk,
+                                                     metric, thr + row0, cnt, s));
     } else {
         const double mu = (double)S * k / (double)N;
         const int32_t rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0) + 1;
@@ -1079,8 +1080,9 @@ knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t
     KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)N * sizeof(int32_t), s));
     if (!reuse) {
         KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+        KNN_TRY(ensure_pv_flag(ctx));
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, ctx->pv_flag, metric, s));
         t.done();
     }
     knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
@@ -1130,6 +1132,12 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     tm.done();
     knn_status st = finish_blocking(ctx, s);
     drain_profile(ctx);
+    if (st == KNN_OK && ctx->pv_flag) {  // the prep flag of this rank's pivots / partition
+        int32_t f = 0;
+        KNN_CUDA(cudaMemcpy(&f, ctx->pv_flag, sizeof f, cudaMemcpyDeviceToHost));
+        if (f & 1)
+            return fail(ctx, KNN_ERR_NONFINITE, "input contains NaN/inf or a vector with ||x||^2 >= FLT_MAX/4");
+    }
     return st;
 }
 

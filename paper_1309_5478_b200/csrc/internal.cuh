@@ -96,7 +96,9 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
 cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,
                                   int64_t ldS, float margin_override, int num_sms, cudaStream_t s);
 // select.cu: pivots = k-th smallest chunk minimum per row; exact select over candidates.
-cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
+// thr[M .. pad_end) (relative to thr) is zero-filled: the SYM partition reads whole 256-row
+// tiles of pivots; pad_end must not pass the caller's allocation (absolute limit).
+cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int64_t pad_end, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s);
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
@@ -127,17 +129,6 @@ cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* cons
                                 cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
-// fused.cu: GEMM + per-row select in the epilogue (k <= fused_max_k()); writes S partial
-// lists [S][M][k] (final lists when S == 1).
-int fused_max_k();
-int fused_splits(int64_t M, int64_t N, int num_sms);  // requested S
-inline int64_t fused_actual_splits(int64_t N, int S) {
-    const int64_t n_nb = ceil_div(N, 256);
-    return ceil_div(n_nb, ceil_div(n_nb, S));
-}
-cudaError_t launch_knn_fused(const TcOperands& op, int32_t metric, int64_t self_shift, int32_t k,
-                             int64_t idx_offset, int S, int32_t* out_idx, float* out_dist,
-                             int num_sms, cudaStream_t s);
 
 // select.cu
 // redo: workspace of M + 1 int32 for the sampled-pivot plan of the CTA-per-row select (null:

@@ -1500,14 +1500,14 @@ __device__ __forceinline__ void pv_fold(uint32_t (&a)[PV_PER], uint32_t (&b)[PV_
     cswap(a[0], a[1]); cswap(a[2], a[3]); cswap(a[4], a[5]); cswap(a[6], a[7]);
 }
 __global__ void __launch_bounds__(32 * PV_ROWS, 2)
-pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int k, int metric,
-                       float* __restrict__ thr, int32_t* __restrict__ cnt) {
+pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int64_t pad_end, int k,
+                       int metric, float* __restrict__ thr, int32_t* __restrict__ cnt) {
     __shared__ uint32_t tile[PV_SLAB][PV_ROWS + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // warp w owns row r0 + w
     const int64_t r0 = (int64_t)blockIdx.x * PV_ROWS;
     if (threadIdx.x < PV_ROWS) {  // zero padding of thr (read as whole tiles by the SYM partition)
         const int64_t row = r0 + threadIdx.x;
-        if (row >= M && row < round_up(M, (int64_t)kColPad)) thr[row] = 0.0f;
+        if (row >= M && row < pad_end) thr[row] = 0.0f;
     }
     uint32_t a[PV_PER];  // this lane's sorted 8 smallest of the row's chunks lane, lane+32, ...
     for (int64_t s0 = 0; s0 < nchunk; s0 += PV_SLAB) {
@@ -2612,11 +2612,13 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int32_t k,
+cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int64_t pad_end, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 64 || nchunk < k) return cudaErrorInvalidValue;  // k: the pivot rank (<= 32 + self)
-    pivot_from_mins_kernel<<<(unsigned)ceil_div(round_up(M, kColPad), PV_ROWS), 32 * PV_ROWS, 0, s>>>(mins, nchunk, M, k, metric, thr, cnt);
+    if (pad_end < M) pad_end = M;
+    pivot_from_mins_kernel<<<(unsigned)ceil_div(pad_end, PV_ROWS), 32 * PV_ROWS, 0, s>>>(mins, nchunk, M, pad_end,
+                                                                                        k, metric, thr, cnt);
     return cudaGetLastError();
 }
 

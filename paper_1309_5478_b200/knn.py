@@ -27,7 +27,7 @@ STATUS = {0: "KNN_OK", 1: "KNN_ERR_ARG", 2: "KNN_ERR_UNSUPPORTED", 3: "KNN_ERR_N
 SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_error",
            "knn_graph", "knn_search", "knn_search_block", "knn_search_block_host",
            "knn_rownorms", "knn_distances", "knn_select", "knn_merge", "knn_launch_count",
-           "knn_gemm_path", "knn_set_plan", "knn_fused_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
+           "knn_gemm_path", "knn_set_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
            "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
            "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_graph_pivots",
@@ -92,7 +92,6 @@ def load_library():
             "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
-            "knn_fused_plan": (ctypes.c_int, [p, i32]),
             "knn_set_plan": (st, [p, i32]),
             "knn_last_plan": (ctypes.c_int, [p]),
             "knn_last_candidates": (ctypes.c_int64, [p]),
@@ -441,14 +440,14 @@ def gemm_path(device=None):
 
 
 def set_plan(plan, device=None):
-    """PLAN_AUTO (default), PLAN_FUSED (GEMM with the select in its epilogue, k <= 32) or
-    PLAN_MATERIALISED; all give bit-identical results."""
+    """PLAN_AUTO (default) or PLAN_MATERIALISED; both give bit-identical results
+    (PLAN_FUSED is reserved: the per-row-list fused kernel was retired)."""
     ctx = context(device)
     _check(load_library().knn_set_plan(ctx, int(plan)), ctx)
 
 
 def last_plan(device=None):
-    """0 blocked distances+select, 1 fused, 2 symmetric k-NNG distances+select,
+    """0 blocked distances+select, 2 symmetric k-NNG distances+select,
     3 pivot plan (symmetric), 4 pivot plan (general block)."""
     return int(load_library().knn_last_plan(context(device)))
 
@@ -456,11 +455,6 @@ def last_plan(device=None):
 def last_candidates(device=None):
     """Candidates the last pivot-plan call kept (sum over rows)."""
     return int(load_library().knn_last_candidates(context(device)))
-
-
-def fused_plan(k, device=None):
-    """1 if the top-level calls run the fused GEMM+select plan for this k."""
-    return int(load_library().knn_fused_plan(context(device), k))
 
 
 def profile_enable(on=True, device=None):

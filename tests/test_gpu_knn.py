@@ -95,11 +95,20 @@ def run_graph(X, k, metric=0):
     return i.cpu().numpy(), d.cpu().numpy()
 
 
-def e2e_check(Q, X, gi, gd, k, rows, graph, metric=0, min_pinned=0.0):
-    # L2 is checked in the squared domain; cosine / Pearson on the keys themselves
-    D64 = oracle.dist_rows(Q, X, rows=rows, metric=metric if metric >= 2 else 0)
-    res = checks.check_rows(gi[rows], gd[rows], D64, oracle.sqnorms(Q[rows]), oracle.sqnorms(X),
-                            rows, k, metric=metric, graph=graph)
+def e2e_check(Q, X, gi, gd, k, rows, graph, metric=0, min_pinned=0.0, chunk=128):
+    # L2 is checked in the squared domain; cosine / Pearson on the keys themselves.  Rows
+    # are checked in chunks so that the fp64 oracle rows stay small at full size.
+    rows = np.asarray(rows)
+    cn = oracle.sqnorms(X)
+    res = {"n_rows": 0, "n_pinned": 0, "failures": []}
+    for c0 in range(0, len(rows), chunk):
+        rr = rows[c0:c0 + chunk]
+        D64 = oracle.dist_rows(Q, X, rows=rr, metric=metric if metric >= 2 else 0)
+        r = checks.check_rows(gi[rr], gd[rr], D64, oracle.sqnorms(Q[rr]), cn, rr, k, metric=metric,
+                              graph=graph)
+        for key in ("n_rows", "n_pinned"):
+            res[key] += r[key]
+        res["failures"] += r["failures"]
     assert res["failures"] == [], res["failures"][:5]
     assert res["n_pinned"] >= min_pinned * len(rows)
     return res
@@ -136,6 +145,17 @@ def _sample_rows(M, n, seed):
     return rows
 
 
+def _block_rows(M, n_random, seed):
+    """Full-size oracle sample: the first and last row of every 256-row block
+    (the partition GEMM's 256x256 tiles: every row's diagonal block straddles the
+    diagonal), the 128-row CTA boundary rows of every 8th block, plus seeded random rows."""
+    b0 = np.arange(0, M, 256)
+    edges = [b0, np.minimum(b0 + 255, M - 1), np.minimum(b0[::8] + 127, M - 1),
+             np.minimum(b0[::8] + 128, M - 1)]
+    g = np.random.Generator(np.random.Philox(seed))
+    return np.unique(np.concatenate(edges + [[M - 1], g.integers(0, M, n_random)]))
+
+
 def test_c2_graph_full_size():
     cfg = datagen.CONFIGS["C2"]
     X, _ = datagen.config_inputs(cfg)
@@ -147,15 +167,18 @@ def test_c3_search_full_size():
     cfg = datagen.CONFIGS["C3"]
     Q, X = datagen.config_inputs(cfg)
     i, d = knn().search(cuda(Q), cuda(X), cfg.k)
-    e2e_check(Q, X, i.cpu().numpy(), d.cpu().numpy(), cfg.k, _sample_rows(cfg.M, 40, 2), False,
-              min_pinned=0.5)
+    rows = _block_rows(cfg.M, 480, 2)
+    assert len(rows) >= 1024
+    e2e_check(Q, X, i.cpu().numpy(), d.cpu().numpy(), cfg.k, rows, False, min_pinned=0.5)
 
 
 def test_headline_graph_full_size():
     cfg = datagen.HEADLINE
     X, _ = datagen.config_inputs(cfg)
     gi, gd = run_graph(X, cfg.k)
-    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 40, 3), True, min_pinned=0.5)
+    rows = _block_rows(cfg.N, 480, 3)
+    assert len(rows) >= 1024
+    e2e_check(X, X, gi, gd, cfg.k, rows, True, min_pinned=0.5)
 
 
 def test_c4_graph_large_k_full_size():
@@ -169,7 +192,9 @@ def test_c5_graph_single_gpu_full_size():
     cfg = datagen.CONFIGS["C5"]
     X, _ = datagen.config_inputs(cfg)
     gi, gd = run_graph(X, cfg.k)
-    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 12, 5), True)
+    rows = _block_rows(cfg.N, 100, 5)
+    assert len(rows) >= 1024
+    e2e_check(X, X, gi, gd, cfg.k, rows, True)
 
 
 def test_corpus_shards_plus_merge_equal_graph():
@@ -249,68 +274,6 @@ def test_simt_cross_check_path():
     env = dict(os.environ, KNN_GEMM="simt")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
-
-
-# ------------------------------------------------------------------ a-S5 fused -------
-@pytest.fixture
-def fused_plan():
-    kn = knn()
-    kn.set_plan(kn.PLAN_FUSED)
-    yield kn
-    kn.set_plan(kn.PLAN_AUTO)
-
-
-# The fused GEMM+select (k <= 32) must equal knn_distances + knn_select (the
-# materialised building blocks) bit-for-bit: same distance expression, exact select.
-@pytest.mark.parametrize("M,N,d,k", [(300, 300, 3, 1), (1000, 1000, 64, 8), (2500, 2500, 33, 32),
-                                     (5000, 5000, 200, 31), (777, 4099, 128, 16)])
-@pytest.mark.parametrize("metric", [0, 1])
-def test_fused_equals_materialised(M, N, d, k, metric, fused_plan):
-    kn = fused_plan
-    X = datagen.points(N, d, "clusters", seed=N + d)
-    Xt = cuda(X)
-    if M == N:
-        assert kn.fused_plan(k) == 1
-        gi, gd = kn.graph(Xt, k, metric=metric)
-        D = kn.distances(Xt, Xt, metric=metric, self_shift=0)
-    else:
-        Q = cuda(datagen.points(M, d, "gauss", seed=M))
-        gi, gd = kn.search_block(Q, Xt, k, metric=metric)
-        D = kn.distances(Q, Xt, metric=metric)
-    ri, rd = kn.select(D.contiguous(), k)
-    assert torch.equal(gi, ri)
-    assert torch.equal(gd.view(torch.int32), rd.view(torch.int32))
-
-
-def test_fused_many_splits_long_rows(fused_plan):
-    # few query rows against a long corpus: the fused plan splits columns and merges
-    kn = fused_plan
-    Q = cuda(datagen.points(2000, 256, "uniform", seed=31))
-    X = cuda(datagen.points(65536, 256, "uniform", seed=32))
-    gi, gd = kn.search_block(Q, X, 32)
-    ri, rd = kn.select(kn.distances(Q, X).contiguous(), 32)
-    assert torch.equal(gi, ri) and torch.equal(gd, rd)
-
-
-def test_fused_self_shift_and_offsets(fused_plan):
-    kn = fused_plan
-    assert kn.fused_plan(20) == 1
-    X = datagen.points(3000, 24, "gauss", seed=33)
-    Xt = cuda(X)
-    ref_i, ref_d = kn.graph(Xt, 20)
-    parts = [kn.search_block(Xt, Xt[a:b].contiguous(), 20, self_shift=-a, idx_offset=a)
-             for a, b in ((0, 1000), (1000, 2000), (2000, 3000))]
-    i, d = kn.merge(torch.stack([p[1] for p in parts]), torch.stack([p[0] for p in parts]),
-                    np.zeros(3, np.int64))
-    assert torch.equal(i, ref_i) and torch.equal(d, ref_d)
-
-
-@pytest.mark.parametrize("cfg_name", ["C1", "C2"])
-def test_fused_plan_e2e(cfg_name, fused_plan):
-    cfg = datagen.CONFIGS[cfg_name]
-    X, _ = datagen.config_inputs(cfg)
-    gi, gd = run_graph(X, cfg.k)
-    e2e_check(X, X, gi, gd, cfg.k, _sample_rows(cfg.N, 100, 9), True)
 
 
 # ------------------------------------------------------------------ canonical orientation

@@ -352,3 +352,64 @@ def test_checks_cosine_tolerance():
         bad[2, 1] += 2.5 * checks.COS_TOL
         res = checks.check_rows(ref["idx64"], bad, D64, n[rows], n, rows, k, metric=metric, graph=True)
         assert any("tolerance" in f for f in res["failures"])
+
+
+# ---------------------------------------------------------------- check_distances ----
+# oracle.checks.check_distances is the a-S3 parity gate (|D - D64| <= 1e-5 (||q||^2 +
+# ||c||^2), BASELINE.json north_star).  Pinned here against hand arithmetic and
+# independently computed tolerances: it must accept the exact values and values inside
+# the band, and flag a single element pushed to 2x the tolerance, in every branch
+# (L2SQ absolute error, the L2 sqrt band, the absolute cosine key tolerance).
+def test_check_distances_hand_example():
+    # q = (3, 4), c = (0, 0) and (3, 0): d^2 = 25 and 16, ||q||^2 = 25, ||c||^2 = 0 and 9
+    # (SPEC.md:133's 3-4-5 example), so tol = 2.5e-4 and 3.4e-4.
+    D64 = np.array([[25.0, 16.0]])
+    qn, cn = np.array([25.0]), np.array([0.0, 9.0])
+    assert checks.check_distances(D64, D64, qn, cn) == (0.0, 0)
+    ratio, nbad = checks.check_distances(np.array([[25.0 + 5e-4, 16.0]]), D64, qn, cn)
+    assert nbad == 1 and ratio == pytest.approx(2.0)
+    ratio, nbad = checks.check_distances(np.array([[25.0 - 1.2e-4, 16.0 + 1.7e-4]]), D64, qn, cn)
+    assert nbad == 0 and ratio == pytest.approx(0.5)
+    # L2: d_E = 5 and 4; the band is sqrt(d^2 -+ tol) widened by one ulp
+    E = np.array([[5.0, 4.0]])
+    assert checks.check_distances(E, D64, qn, cn, metric=1)[1] == 0
+    assert checks.check_distances(np.array([[math.sqrt(25 + 5e-4), 4.0]]), D64, qn, cn, metric=1)[1] == 1
+    assert checks.check_distances(np.array([[5.0, math.sqrt(16 - 6.8e-4)]]), D64, qn, cn, metric=1)[1] == 1
+    assert checks.check_distances(np.array([[math.sqrt(25 + 1e-4), math.sqrt(16 - 1e-4)]]),
+                                  D64, qn, cn, metric=1)[1] == 0
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_check_distances_accepts_oracle_flags_perturbation(metric):
+    X = datagen.points(70, 48, "gauss", seed=21)
+    Q = datagen.points(30, 48, "uniform", seed=22)
+    if metric == 2:
+        D64 = oracle.dist_rows(Q, X, metric=2)
+        tol = np.full(D64.shape, 1e-5)
+        qn = np.ones(30)
+        cn = np.ones(70)
+    else:
+        D64 = oracle.dist_rows(Q, X, metric=oracle.L2SQ)
+        # norms by math.fsum of the fp64 squares (not the oracle's own norm routine)
+        qn = np.array([math.fsum(float(v) ** 2 for v in row) for row in Q])
+        cn = np.array([math.fsum(float(v) ** 2 for v in row) for row in X])
+        tol = 1e-5 * (qn[:, None] + cn[None, :])
+    base = np.sqrt(D64) if metric == 1 else D64.copy()
+    assert checks.check_distances(base, D64, qn, cn, metric=metric)[1] == 0
+    # whole matrix inside half the band (alternating signs): accepted
+    sign = np.where((np.arange(D64.size).reshape(D64.shape) % 2) == 0, 1.0, -1.0)
+    inside = np.maximum(D64 + 0.5 * tol * sign, 0.0)
+    G = np.sqrt(inside) if metric == 1 else inside
+    assert checks.check_distances(G, D64, qn, cn, metric=metric)[1] == 0
+    # one element at +2 tol, one at -2 tol (where D64 > 2 tol): exactly two violations
+    rng = np.random.default_rng(5)
+    a = (int(rng.integers(30)), int(rng.integers(70)))
+    b = (int(rng.integers(30)), int(rng.integers(70)))
+    while b == a or D64[b] <= 2 * tol[b]:
+        b = (int(rng.integers(30)), int(rng.integers(70)))
+    P = D64.copy()
+    P[a] += 2 * tol[a]
+    P[b] -= 2 * tol[b]
+    G = np.sqrt(P) if metric == 1 else P
+    ratio, nbad = checks.check_distances(G, D64, qn, cn, metric=metric)
+    assert nbad == 2 and ratio == pytest.approx(2.0, rel=1e-3)
