@@ -57,7 +57,7 @@ typedef enum {
     KNN_ERR_NONFINITE = 3,    /* input holds NaN/inf, or a squared norm >= FLT_MAX/4 (R8) */
     KNN_ERR_OOM = 4,          /* device workspace allocation failed */
     KNN_ERR_CUDA = 5,         /* a CUDA runtime/driver call failed */
-    KNN_ERR_NCCL = 6,         /* reserved for collective failures */
+    KNN_ERR_NCCL = 6,         /* a collective failed (NCCL or the host transport), or NCCL missing */
     KNN_ERR_INTERNAL = 7
 } knn_status;
 
@@ -235,6 +235,81 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
 knn_status knn_ipc_export(knn_ctx_t ctx, const void* dev_ptr, uint8_t handle[64], int64_t* offset);
 knn_status knn_ipc_open(knn_ctx_t ctx, const uint8_t handle[64], int64_t offset, void** dev_ptr);
 knn_status knn_ipc_close_all(knn_ctx_t ctx);
+
+/* ---------------------------------------------------------------- multi-GPU ---------
+ * One process per GPU, each with its own ctx (PAPER.md:102:
+ * "batch execution with data partitioning ... merging of results"; the
+ * queries are independent, coarse-grained parallelism).  The caller creates the
+ * communicator once per ctx, then every rank makes the SAME sharded call with the same
+ * arguments (collective semantics: a rank that does not call blocks the others).
+ *
+ * knn_comm_unique_id: an NCCL unique id (128 bytes) made on ONE rank; the caller ships it
+ *   to the others (e.g. torch.distributed.broadcast_object_list).  NCCL is loaded at run
+ *   time (dlopen "libnccl.so.2", else the build-time path, else env KNN_NCCL_LIB);
+ *   KNN_ERR_NCCL if it cannot be loaded.
+ * knn_comm_init: joins the communicator of `nranks` ranks as `rank` on the ctx's device
+ *   (blocking, collective).  Collectives then run on the caller's stream over NVLink /
+ *   NVSwitch.  Re-initialising replaces the previous communicator.
+ * knn_comm_init_ops: the same with a caller-supplied HOST transport instead of NCCL (for
+ *   process groups NCCL cannot serve, e.g. several ranks sharing one GPU in tests): the
+ *   library synchronises the stream, stages the data through pinned host memory and calls
+ *   the callbacks, which must perform the collective over all ranks and return 0 (nonzero:
+ *   the call fails with KNN_ERR_NCCL).  All pointers passed to the callbacks are HOST
+ *   pointers; `bytes` counts are per rank.  The ops struct is copied; `user` is passed back.
+ * knn_comm_destroy: releases the communicator (also done by knn_ctx_destroy).
+ * knn_comm_info: *backend = 0 none, 1 NCCL, 2 host callbacks; *rank, *nranks. */
+typedef struct knn_comm_ops {
+    int (*allgather)(void* user, const void* send, void* recv, int64_t bytes);  /* recv: nranks*bytes */
+    int (*broadcast)(void* user, void* buf, int64_t bytes, int root);
+    int (*alltoall)(void* user, const void* send, void* recv, int64_t bytes);   /* block g -> rank g */
+    int (*allreduce_max_i32)(void* user, int32_t* buf, int64_t count);
+    void* user;
+} knn_comm_ops;
+knn_status knn_comm_unique_id(uint8_t id[128]);
+knn_status knn_comm_init(knn_ctx_t ctx, int32_t rank, int32_t nranks, const uint8_t id[128]);
+knn_status knn_comm_init_ops(knn_ctx_t ctx, int32_t rank, int32_t nranks, const knn_comm_ops* ops);
+knn_status knn_comm_destroy(knn_ctx_t ctx);
+knn_status knn_comm_info(knn_ctx_t ctx, int32_t* backend, int32_t* rank, int32_t* nranks);
+
+/* Contiguous block r of ceil(n/parts)-sized blocks of [0, n): [*lo, *hi) (possibly empty).
+ * The split every sharded call uses for rows, columns and triangle units.  Host only. */
+void knn_shard_range(int64_t n, int32_t parts, int32_t r, int64_t* lo, int64_t* hi);
+
+/* Sharded calls.  shard_mode:
+ *   KNN_SHARD_QUERY  (Par-1): query rows split in contiguous blocks; each rank runs the
+ *                    whole single-GPU hot path (knn_search_block) on its rows against all
+ *                    N points; results all-gathered.
+ *   KNN_SHARD_CORPUS (Par-2): corpus columns split; each rank computes partial top-k lists
+ *                    of EVERY query row against its columns (global self exclusion and
+ *                    indices), an all-to-all hands each rank the nranks partial lists of its
+ *                    own rows, the k-way merge kernel (a-S6) reduces them, results
+ *                    all-gathered.  Needs k <= the smallest column block.
+ *   KNN_SHARD_SYM    (Par-3, knn_graph_sharded only; N >= 16384 on the tensor-core path):
+ *                    the ranks split the UPPER TRIANGLE of the k-NNG's distance matrix (the
+ *                    transpose reuse of PAPER.md:83 survives sharding): pivots of own rows
+ *                    (all-gathered), the partition GEMM over 1/nranks of the triangle's
+ *                    256x256 blocks appending candidates of any row to rank-local lists,
+ *                    then each rank's select reads the lists of its rows from every rank
+ *                    directly in peer memory (CUDA IPC mappings, exchanged once over the
+ *                    communicator; NVLink loads inside the kernel); results all-gathered.
+ *                    Falls back to KNN_SHARD_QUERY (on every rank alike) when peer mappings
+ *                    are unavailable, N < 16384, or a certificate fails.
+ * Inputs: X (N×d) and Q (M×d) are device buffers on every rank; their contents on rank 0
+ * are broadcast into them on the other ranks inside the call (so they must be writable).
+ * Outputs: the full M×k (N×k) lists on EVERY rank, bit-identical to the single-GPU calls
+ * for every mode and rank count.  Blocking.  Without a communicator they run as one rank.
+ * Argument rules as knn_search_block / knn_graph.  knn_search_sharded: squared L2,
+ * modes QUERY / CORPUS.  Collective failures return KNN_ERR_NCCL; a rank whose local
+ * computation fails makes every rank return an error (statuses agreed by an all-reduce). */
+#define KNN_SHARD_QUERY 0
+#define KNN_SHARD_CORPUS 1
+#define KNN_SHARD_SYM 2
+knn_status knn_graph_sharded(knn_ctx_t ctx, int32_t shard_mode, float* X, int64_t N, int32_t d, int32_t k,
+                             int32_t metric, int32_t* out_idx, float* out_dist, void* stream);
+knn_status knn_search_sharded(knn_ctx_t ctx, int32_t shard_mode, float* Q, int64_t M, float* X, int64_t N,
+                              int32_t d, int32_t k, int32_t* out_idx, float* out_dist, void* stream);
+/* Mode the last sharded call of this ctx actually ran (after fallbacks), -1 none. */
+int knn_last_shard_mode(knn_ctx_t ctx);
 
 /* DIAGNOSTIC (not the hot path): the distance GEMM of X against itself (sym != 0: the
  * symmetric upper-triangle schedule) with an epilogue that only drains the TMEM
