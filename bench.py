@@ -35,6 +35,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="H", help="H (headline) or C1..C5")
     ap.add_argument("--plan", default="auto", choices=["auto", "materialised"])
+    ap.add_argument("--shard", default="auto", choices=["auto", "sym", "query", "corpus"],
+                    help="multi-GPU sharding (knn_graph_sharded / knn_search_sharded); auto: sym for "
+                         "the k-NNG (corpus for C5, BASELINE configs[4]), query rows for search")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -205,10 +208,14 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        # host-side plumbing (id exchange, barriers, max over ranks) on gloo; the data path's
+        # collectives are the library's: NCCL over NVLink (its init log on, so the ranks'
+        # communicator is visible), or the host transport when the ranks share one GPU
+        if not share:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("gloo")
+        sharded.init(transport="host" if share else "nccl")
     cfg = get_config(args.config)
     search = cfg.mode != "graph"  # C3: k-NN search of M queries against N corpus points
     N, d, k = cfg.N, cfg.d, cfg.k
@@ -219,16 +226,21 @@ def run_ours(args):
     Q = (torch.from_numpy(Q_host).to(dev) if rank == 0 else torch.empty((M, d), device=dev)) if search else X
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
-    # k-NNG on several GPUs: the ranks split the upper triangle (Par-3, the transpose reuse
-    # survives sharding); small problems shard query rows (Par-1)
-    sym_shard = not search and world > 1 and N >= 16384 and os.environ.get("KNN_BENCH_PAR1", "0") != "1"
+    # sharding: k-NNG -> the ranks split the upper triangle (Par-3, the transpose reuse
+    # survives sharding), C5 -> corpus columns + all-to-all + k-way merge (BASELINE
+    # configs[4]); search -> query rows (Par-1).  One GPU runs the same call as one rank.
+    shard = args.shard
+    if shard == "auto":
+        shard = "query" if search else ("corpus" if cfg.sharding == "corpus" else "sym")
+    if search and shard == "sym":
+        raise SystemExit("--shard sym is a k-NNG mode")
+    out_i = torch.empty((M, k), dtype=torch.int32, device=dev)
+    out_d = torch.empty((M, k), dtype=torch.float32, device=dev)
 
     def step():
         if search:
-            return sharded.search_query_sharded(Q, X, k, broadcast=True)
-        if sym_shard:
-            return sharded.graph_sym_sharded(X, k, broadcast=True)
-        return sharded.graph_query_sharded(X, k, broadcast=True)
+            return sharded.search(Q, X, k, mode=shard, out=(out_i, out_d))
+        return sharded.graph(X, k, mode=shard, out=(out_i, out_d))
 
     def barrier():
         if world > 1:
@@ -261,7 +273,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
     launches = knn.launch_count() - launches0
-    prof = {kname: knn.profile_read(kname) for kname in ("prep", "gemm", "select", "merge", "fused")}
+    shard_ran = {0: "query", 1: "corpus", 2: "sym"}.get(knn.last_shard_mode(), "none")
+    sym_shard = shard_ran == "sym" and world > 1
+    prof = {kname: knn.profile_read(kname) for kname in knn.KERNELS}
     knn.profile_enable(False)
     clocks = sampler.stop()
 
@@ -276,6 +290,13 @@ def run_ours(args):
     peaks = load_peaks()
     lo_r, hi_r = sharded.block_range(M, world, rank)
     R_local = hi_r - lo_r
+    # this rank's share of the work: query rows x all N points, or (corpus sharding) all M
+    # rows x its column block; the symmetric plans multiply the upper triangle only
+    if shard_ran == "corpus":
+        c_lo, c_hi = sharded.block_range(N, world, rank)
+        rows_w, cols_w = M, c_hi - c_lo
+    else:
+        rows_w, cols_w = R_local, N
     d_pad = -(-d // 64) * 64
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -284,6 +305,8 @@ def run_ours(args):
         traffic = {}
 
     plan_code = knn.last_plan()
+    div = int(os.environ.get("KNN_PIVOT_DIV", "8"))
+    S_samp = -(-(cols_w // div) // 256) * 256 if k <= 32 else -(-max(cols_w // div, 4096) // 256) * 256
 
     # committed ncu captures: the headline's kernels under their names, C4's GEMMs with a
     # "_c4" suffix (profiles/traffic.json)
@@ -294,23 +317,31 @@ def run_ours(args):
     # candidate select re-evaluates the survivors
     pivot1 = os.environ.get("KNN_PIVOT1", "0") not in ("", "0") and k <= 32 and plan_code in (3, 4)
 
-    def tensor_roof(name, kernel, ms, n, rows_per_launch, products=3):
-        avg = ms / max(n, 1)
-        pairs = rows_per_launch * N
-        if plan_code in (2, 3) and kernel != "dist_tc_kernel_sample":
-            # symmetric: only the upper triangle of 256x256 blocks is multiplied (split over
-            # the ranks by Par-3)
+    def pairs_of(kernel):
+        if kernel == "dist_tc_kernel_sample":
+            return rows_w * S_samp
+        if plan_code in (2, 3):
+            # symmetric: the upper triangle of 256x256 blocks (split over the ranks by Par-3)
             nblk = -(-N // 256)
-            pairs = nblk * (nblk + 1) / 2 * 256.0 * 256.0 / (world if sym_shard else 1)
-        flop = products * 2.0 * pairs * d_pad  # fp16 products per multiply-add (3: split)
-        useful = 2.0 * rows_per_launch * N * d  # the dot products the path delivers
+            return nblk * (nblk + 1) / 2 * 256.0 * 256.0 / (world if sym_shard else 1)
+        return rows_w * cols_w
+
+    # Peak: the measured BURST bf16 (= fp16) dense rate — the timed region is well under a
+    # second, so the sustained (power-capped, 4 s) figure would flatter the kernel; the
+    # sustained fraction is reported beside it.
+    def tensor_roof(name, kernel, ms, n, products=3):
+        avg = ms / max(n, 1)
+        pairs = pairs_of(kernel)
+        flop = products * 2.0 * pairs * d_pad  # executed fp16 tensor flop (3 products: split)
+        useful = 2.0 * pairs * d  # the dot products the method needs (triangle for the k-NNG)
         r = {"kernel": name, "bound": "tensor", "achieved": flop / (avg * 1e-3) / 1e12,
-             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-             "peak_kind": f"fp16 dense = bf16 {peaks['source']} sustained",
+             "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+             "peak_kind": f"fp16 dense = bf16 {peaks['source']} burst",
              "useful_tflops": useful / (avg * 1e-3) / 1e12, "avg_launch_ms": avg,
-             "launches": n, "traffic": traffic.get(tkey(kernel)),
+             "launches": n, "flop_per_launch": flop, "traffic": traffic.get(tkey(kernel)),
              "traffic_source": traffic.get("_source")}
         r["frac"] = r["achieved"] / r["peak"]
+        r["frac_sustained"] = r["achieved"] / peaks["bf16_tflops_sustained"]
         return r
 
     def hbm_roof(name, kernel, ms, n, bytes_per_launch):
@@ -328,36 +359,30 @@ def run_ours(args):
     s_ms, s_n = prof["select"]
     m_ms, m_n = prof["merge"]
     p_ms, p_n = prof["prep"]
+    x_ms, x_n = prof["xmerge"]
     if f_n and plan_code in (3, 4):
         rooflines.append((f_ms, tensor_roof(
             "dist_tc_kernel<PIVOT%s%s> (a-S5: GEMM with the quickselect partition in its epilogue%s)"
             % ("1" if pivot1 else "", ",SYM" if plan_code == 3 else "",
-               ", single hi.hi product" if pivot1 else ""), "dist_tc_kernel", f_ms, f_n, R_local,
+               ", single hi.hi product" if pivot1 else ""), "dist_tc_kernel", f_ms, f_n,
             products=1 if pivot1 else 3)))
-    elif f_n:
-        rooflines.append((f_ms, tensor_roof("knn_fused_kernel (a-S5: a-S3 GEMM + a-S4 select in the epilogue)",
-                                            "knn_fused_kernel", f_ms, f_n, R_local)))
     if g_n and plan_code in (3, 4):
-        S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
-        if k > 32:  # quantile pivot: the sample is max(N/8, 4096) columns, stored
-            S_samp = -(-max(N // int(os.environ.get('KNN_PIVOT_DIV', '8')), 4096) // 256) * 256
-        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x first N/8 columns -> 32-column chunk minima)"
+        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x N/8 sampled columns -> 32-column chunk minima)"
                          if k <= 32 else
-                         f"dist_tc_kernel<SAMPLE> (quantile-pivot sample: single-product upper bounds, rows x first {S_samp} columns)",
-                         "dist_tc_kernel_sample", g_ms, g_n, R_local)
-        avg = g_ms / g_n
-        flop = 2.0 * R_local * S_samp * d_pad  # one hi.hi product
-        gr.update({"achieved": flop / (avg * 1e-3) / 1e12, "useful_tflops": 2.0 * R_local * S_samp * d / (avg * 1e-3) / 1e12})
-        gr["frac"] = gr["achieved"] / gr["peak"]
+                         f"dist_tc_kernel<SAMPLE> (quantile-pivot sample: single-product upper bounds, rows x {S_samp} columns)",
+                         "dist_tc_kernel_sample", g_ms, g_n, products=1)
         rooflines.append((g_ms, gr))
     elif g_n:
-        gl = max(g_n // args.steps, 1)
-        gr = tensor_roof("dist_tc_kernel (a-S3)", "dist_tc_kernel", g_ms, g_n, R_local / gl)
+        gr = tensor_roof("dist_tc_kernel (a-S3)", "dist_tc_kernel", g_ms, g_n)
+        if plan_code == 0:  # blocked: the launches split the rows
+            gl = max(g_n // args.steps, 1)
+            for key in ("achieved", "useful_tflops", "flop_per_launch", "frac", "frac_sustained"):
+                gr[key] /= gl
         if plan_code == 2:
             # the symmetric GEMM does half the MMA work and writes the whole matrix: its
             # binding roofline is the HBM write of D (+ operand reads)
             avg = g_ms / g_n
-            dbytes = R_local * (-(-N // 4) * 4) * 4.0 + 2 * N * d_pad * 4.0
+            dbytes = rows_w * (-(-N // 4) * 4) * 4.0 + 2 * N * d_pad * 4.0
             gr["tensor_frac"] = gr["frac"]
             gr.update({"bound": "hbm", "achieved": dbytes / (avg * 1e-3) / 1e9,
                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "algorithmic_bytes": dbytes,
@@ -365,46 +390,45 @@ def run_ours(args):
             gr["frac"] = gr["achieved"] / gr["peak"]
             gr["kernel"] = "dist_tc_kernel<SYM> (a-S3, symmetric k-NNG: upper triangle, direct + transposed stores)"
         rooflines.append((g_ms, gr))
+    piv_rows = R_local if sym_shard else rows_w
     if s_n and plan_code in (3, 4):
-        S_samp = -(-(N // int(os.environ.get('KNN_PIVOT_DIV', '8'))) // 256) * 256
         if k <= 32:
             rooflines.append((s_ms, hbm_roof("pivot_from_mins_kernel (pivot = k-th smallest of the row's chunk minima)",
                                              "pivot_from_mins_kernel", s_ms, s_n,
-                                             R_local * (S_samp // 32 * 4.0 + 8.0))))
+                                             piv_rows * (S_samp // 32 * 4.0 + 8.0))))
         else:
-            S_samp = -(-max(N // int(os.environ.get('KNN_PIVOT_DIV', '8')), 4096) // 256) * 256
             rooflines.append((s_ms, hbm_roof("pivot_from_sample_kernel (pivot = bucketed order statistic of the sample)",
-                                             "pivot_from_sample_kernel", s_ms, s_n, R_local * (S_samp * 4.0 + 4.0))))
+                                             "pivot_from_sample_kernel", s_ms, s_n, piv_rows * (S_samp * 4.0 + 4.0))))
     elif s_n:
         sl = max(s_n // args.steps, 1)
         kind, splits = knn.last_select_kernel()
         kname = {"warp per row": "select_warp_kernel", "cluster per row": "select_cluster_kernel"}.get(
             kind, "select_ring_kernel")
         rooflines.append((s_ms, hbm_roof(f"{kname} (a-S4, {kind})", kname, s_ms, s_n,
-                                         R_local / sl * (N * 4.0 + k * 8.0))))
+                                         rows_w / sl * (cols_w * 4.0 + k * 8.0))))
     if m_n and plan_code in (3, 4):
         cands = knn.last_candidates()  # survivors of the partition (whole call)
+        sel_rows = R_local if sym_shard else rows_w
         cs_name = ("candidate_recompute_kernel" if pivot1 else "candidate_select_kernel") if k <= 32 \
             else "candidate_select_warp_kernel"
         rooflines.append((m_ms, hbm_roof(f"{cs_name} (exact select of the partition)",
                                          cs_name, m_ms, m_n,
-                                         cands * 8.0 + R_local * (4.0 + k * 8.0))))
-        rooflines[-1][1]["candidates_per_row"] = cands / max(R_local, 1)
-    elif m_n:
-        # partial lists per row merged (fused split-N, same rule as fused.cu's fused_splits)
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        n_mp, n_nb, ncl = -(-(-(-R_local // 128)) // 2), -(-N // 256), sms // 2
-        best = min(range(1, min(8, n_nb) + 1), key=lambda S: (-(-n_mp * S // ncl)) * (-(-n_nb // S)) * 100 + S)
-        S = -(-n_nb // (-(-n_nb // best)))
-        rooflines.append((m_ms, hbm_roof("merge_kernel (a-S6)", "merge_kernel", m_ms, m_n,
-                                         R_local * k * 8.0 * (S + 1))))
+                                         cands * 8.0 + sel_rows * (4.0 + k * 8.0))))
+        rooflines[-1][1]["candidates_per_row"] = cands / max(sel_rows, 1)
+    if x_n:  # Par-2: the k-way merge of the ranks' partial lists of this rank's rows
+        rooflines.append((x_ms, hbm_roof("merge_lists_kernel (a-S6, corpus-sharded k-way merge)",
+                                         "merge_lists_kernel", x_ms, x_n, R_local * k * 8.0 * (world + 1))))
     rooflines.sort(key=lambda x: -x[0])
     roofline = dict(rooflines[0][1])
     roofline["others"] = [r for _, r in rooflines[1:]]
-    roofline["step_share"] = {"fused": f_ms / total_ms, "gemm": g_ms / total_ms,
-                              "select": s_ms / total_ms, "merge": m_ms / total_ms,
-                              "prep": p_ms / total_ms}
-    roofline["plan"] = {0: "blocked distances + select", 1: "fused GEMM+select",
+    roofline["step_share"] = {"partition": f_ms / total_ms, "gemm": g_ms / total_ms,
+                              "select": s_ms / total_ms, "candidate_select": m_ms / total_ms,
+                              "prep": p_ms / total_ms, "shard_merge": x_ms / total_ms}
+    if roofline["bound"] == "tensor":
+        # the step against the dominant kernel's own floor (its flop at the burst peak)
+        roofline["step_floor_frac"] = roofline["flop_per_launch"] * (roofline["launches"] / args.steps) / \
+            (roofline["peak"] * 1e12) / (ms_per_step * 1e-3)
+    roofline["plan"] = {0: "blocked distances + select",
                         2: "symmetric k-NNG distances (PAPER.md:83 transpose reuse) + select",
                         3: "pivot (quickselect partition, PAPER.md:56) over the symmetric GEMM",
                         4: "pivot (quickselect partition, PAPER.md:56) over the GEMM"}.get(
@@ -469,10 +493,16 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(cfg), "N": N, "M": M, "d": d, "k": k,
-                       "sharding": ("upper triangle split over the ranks (Par-3): bcast X, pivots all-gathered, "
-                                    "partition GEMM on 1/G of the 256x256 blocks, select reading the ranks' "
-                                    "candidate lists over CUDA IPC, all-gather") if sym_shard else
-                                   "query rows (Par-1): bcast X, per-rank rows, all-gather",
+                       "sharding": {"sym": "upper triangle split over the ranks (Par-3): bcast X, pivots "
+                                            "all-gathered, partition GEMM on 1/G of the 256x256 blocks, select "
+                                            "reading the ranks' candidate lists in peer memory, all-gather",
+                                    "corpus": "corpus columns (Par-2): bcast X, per-rank partial top-k of all rows, "
+                                              "all-to-all of row blocks, k-way merge kernel, all-gather",
+                                    "query": "query rows (Par-1): bcast X, per-rank rows, all-gather"}[shard_ran]
+                                   if world > 1 else f"one GPU ({shard_ran} call as one rank)",
+                       "collectives": ("NCCL inside libknn (knn_comm_init)" if not share else
+                                       "host transport (ranks share one GPU; not a reported number)")
+                                      if world > 1 else "none",
                        "gemm": "tcgen05 3-pass split-fp16 (FP32-accurate), fp32 accumulate",
                        "l2": "flushed before every timed step (256 MiB write, untimed)"},
             "roofline": roofline,
@@ -488,8 +518,23 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def self_launch(args):
+    """--gpus N > 1 without a launcher: start N ranks (one per GPU) with torch.distributed.run
+    on 127.0.0.1 and relay their output (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

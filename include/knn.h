@@ -297,7 +297,9 @@ void knn_shard_range(int64_t n, int32_t parts, int32_t r, int64_t* lo, int64_t* 
  * Inputs: X (N×d) and Q (M×d) are device buffers on every rank; their contents on rank 0
  * are broadcast into them on the other ranks inside the call (so they must be writable).
  * Outputs: the full M×k (N×k) lists on EVERY rank, bit-identical to the single-GPU calls
- * for every mode and rank count.  Blocking.  Without a communicator they run as one rank.
+ * for every mode and rank count.  Blocking.  Without a communicator they run as one rank;
+ * one rank runs the single-GPU call directly (env KNN_SHARD_G1_PHASES=1: the sharded
+ * phases anyway, for tests).
  * Argument rules as knn_search_block / knn_graph.  knn_search_sharded: squared L2,
  * modes QUERY / CORPUS.  Collective failures return KNN_ERR_NCCL; a rank whose local
  * computation fails makes every rank return an error (statuses agreed by an all-reduce). */
@@ -366,9 +368,13 @@ int64_t knn_last_candidates(knn_ctx_t ctx);
 /* Per-kernel device timing for benchmarks: when enabled, every launch is bracketed by
  * CUDA events recorded on the launch stream.  knn_profile_enable(ctx, 1) also resets
  * the counters.  knn_profile_read waits for the recorded events and returns the summed
- * duration (ms) and the launch count of one kernel class. */
+ * duration (ms) and the launch count of one kernel class.  Classes: PREP (a-S2), GEMM
+ * (materialised distance GEMM, or the pivot plans' sample pass), SELECT (a-S4 select, or
+ * the pivot select), MERGE (the pivot plans' candidate select; the streamed merge),
+ * FUSED (the partition GEMM of the pivot plans), SHARD_MERGE (the k-way merge of the
+ * corpus-sharded calls). */
 typedef enum { KNN_KERNEL_PREP = 0, KNN_KERNEL_GEMM = 1, KNN_KERNEL_SELECT = 2,
-               KNN_KERNEL_MERGE = 3, KNN_KERNEL_FUSED = 4 } knn_kernel;
+               KNN_KERNEL_MERGE = 3, KNN_KERNEL_FUSED = 4, KNN_KERNEL_SHARD_MERGE = 5 } knn_kernel;
 knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on);
 knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches);
 

@@ -455,7 +455,7 @@ knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on) {
     if (!ctx) return KNN_ERR_ARG;
     cudaSetDevice(ctx->device);
     drain_profile(ctx);
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < 6; ++i) {
         ctx->prof_ms[i] = 0;
         ctx->prof_n[i] = 0;
     }
@@ -464,7 +464,7 @@ knn_status knn_profile_enable(knn_ctx_t ctx, int32_t on) {
 }
 
 knn_status knn_profile_read(knn_ctx_t ctx, int32_t kernel, double* total_ms, int64_t* launches) {
-    if (!ctx || kernel < 0 || kernel > 4 || !total_ms || !launches) return KNN_ERR_ARG;
+    if (!ctx || kernel < 0 || kernel > 5 || !total_ms || !launches) return KNN_ERR_ARG;
     cudaSetDevice(ctx->device);
     drain_profile(ctx);
     *total_ms = ctx->prof_ms[kernel];

@@ -42,8 +42,8 @@ struct knn_ctx {
     int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;
     size_t sym_budget = (size_t)96 << 30;  // largest full N x N matrix for the symmetric plan
-    double prof_ms[5] = {0, 0, 0, 0, 0};
-    int64_t prof_n[5] = {0, 0, 0, 0, 0};
+    double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t prof_n[6] = {0, 0, 0, 0, 0, 0};
     // out-of-core streaming (knn_search_streamed): staging + running lists, copy stream
     void* st_buf = nullptr;
     size_t st_size = 0;

@@ -375,7 +375,7 @@ knn_status run_corpus_sharded(knn_ctx* ctx, const float* Q, int64_t M, const flo
             dl[g] = recv_d + (size_t)g * per * k;
             il[g] = recv_i + (size_t)g * per * k;
         }
-        Timed tm(ctx, KNN_KERNEL_MERGE, s);
+        Timed tm(ctx, KNN_KERNEL_SHARD_MERGE, s);
         KNN_CUDA(knn::launch_merge_lists(dl.data(), il.data(), G, 0, rr.hi - rr.lo, k, zeros.data(), own_i, own_d,
                                          s));
         tm.done();
@@ -542,6 +542,13 @@ knn_status run_sym_sharded(knn_ctx* ctx, const float* X, int64_t N, int32_t d, i
     return gather_rows(ctx, own_i, own_d, stage_i, stage_d, per, N, k, out_idx, out_dist, s);
 }
 
+// One rank runs the single-GPU call directly (the decompositions only add exchanges);
+// env KNN_SHARD_G1_PHASES=1 (tests) runs the sharded phases anyway.
+bool g1_phases() {
+    const char* v = getenv("KNN_SHARD_G1_PHASES");
+    return v && strcmp(v, "1") == 0;
+}
+
 // One-rank communicator used when the caller never initialised one.
 Comm* comm_or_single(knn_ctx* ctx) {
     if (!ctx->comm) {
@@ -665,6 +672,10 @@ knn_status knn_graph_sharded(knn_ctx_t ctx, int32_t shard_mode, float* X, int64_
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Comm* c = comm_or_single(ctx);
+    if (c->nranks == 1 && !g1_phases()) {  // one rank: every mode is the single-GPU k-NNG
+        c->last_mode = shard_mode;
+        return knn_search_block(ctx, X, N, X, N, d, k, metric, 0, 0, out_idx, out_dist, stream);
+    }
     KNN_TRY(c_bcast(ctx, X, (size_t)N * d * sizeof(float), s));
     if (shard_mode == KNN_SHARD_SYM) {
         const bool able = N >= 16384 && k <= KNN_MAX_K && ctx->gemm_mode == 0 && ctx->tc_ok;
@@ -690,7 +701,11 @@ knn_status knn_search_sharded(knn_ctx_t ctx, int32_t shard_mode, float* Q, int64
     if (M == 0) return KNN_OK;
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    comm_or_single(ctx);
+    Comm* c = comm_or_single(ctx);
+    if (c->nranks == 1 && !g1_phases()) {
+        c->last_mode = shard_mode;
+        return knn_search_block(ctx, Q, M, X, N, d, k, KNN_L2SQ, KNN_NO_SELF, 0, out_idx, out_dist, stream);
+    }
     KNN_TRY(c_bcast(ctx, X, (size_t)N * d * sizeof(float), s));
     if (Q != X) KNN_TRY(c_bcast(ctx, Q, (size_t)M * d * sizeof(float), s));
     if (shard_mode == KNN_SHARD_CORPUS)

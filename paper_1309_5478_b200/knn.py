@@ -31,9 +31,25 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
            "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
            "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_graph_pivots",
-           "knn_graph_partition", "knn_graph_gather_select", "knn_diag_mainloop"]
+           "knn_graph_partition", "knn_graph_gather_select", "knn_diag_mainloop",
+           "knn_comm_unique_id", "knn_comm_init", "knn_comm_init_ops", "knn_comm_destroy", "knn_comm_info",
+           "knn_shard_range", "knn_graph_sharded", "knn_search_sharded", "knn_last_shard_mode"]
+SHARD_QUERY, SHARD_CORPUS, SHARD_SYM = 0, 1, 2
+SHARD_MODES = {"query": SHARD_QUERY, "corpus": SHARD_CORPUS, "sym": SHARD_SYM}
 PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
-KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4}
+KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4, "xmerge": 5}
+
+
+# knn_comm_ops: the host-callback transport (include/knn.h "multi-GPU")
+_AG = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_BC = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int)
+_A2A = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_ARM = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
+class CommOps(ctypes.Structure):
+    _fields_ = [("allgather", _AG), ("broadcast", _BC), ("alltoall", _A2A),
+                ("allreduce_max_i32", _ARM), ("user", ctypes.c_void_p)]
 
 
 class KnnError(RuntimeError):
@@ -96,6 +112,17 @@ def load_library():
             "knn_last_plan": (ctypes.c_int, [p]),
             "knn_last_candidates": (ctypes.c_int64, [p]),
             "knn_profile_enable": (st, [p, i32]),
+            "knn_comm_unique_id": (st, [p]),
+            "knn_comm_init": (st, [p, i32, i32, p]),
+            "knn_comm_init_ops": (st, [p, i32, i32, ctypes.POINTER(CommOps)]),
+            "knn_comm_destroy": (st, [p]),
+            "knn_comm_info": (st, [p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32)]),
+            "knn_shard_range": (None, [i64, i32, i32, ctypes.POINTER(ctypes.c_int64),
+                                       ctypes.POINTER(ctypes.c_int64)]),
+            "knn_graph_sharded": (st, [p, i32, p, i64, i32, i32, i32, p, p, p]),
+            "knn_search_sharded": (st, [p, i32, p, i64, p, i64, i32, i32, p, p, p]),
+            "knn_last_shard_mode": (ctypes.c_int, [p]),
             "knn_profile_read": (st, [p, i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_int64)]),
         }
@@ -469,3 +496,110 @@ def profile_read(kernel, device=None):
     _check(load_library().knn_profile_read(ctx, KERNELS[kernel], ctypes.byref(ms),
                                            ctypes.byref(n)), ctx)
     return ms.value, n.value
+
+
+# ------------------------------------------------------------------ multi-GPU --------
+def shard_range(n, parts, r):
+    """knn_shard_range: [lo, hi) of block r of ceil(n/parts)-sized blocks (host only)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    load_library().knn_shard_range(int(n), int(parts), int(r), ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (make it on one rank, ship it to the others)."""
+    buf = (ctypes.c_uint8 * 128)()
+    rc = load_library().knn_comm_unique_id(buf)
+    if rc != 0:
+        raise KnnError(rc, "knn_comm_unique_id (is libnccl.so.2 loadable?)")
+    return bytes(buf)
+
+
+def comm_init(rank, nranks, uid, device=None):
+    """knn_comm_init: join the NCCL communicator (collective, blocking)."""
+    ctx = context(device)
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(load_library().knn_comm_init(ctx, int(rank), int(nranks), buf), ctx)
+
+
+_ops_keep = {}
+
+
+def comm_init_ops(rank, nranks, transport, device=None):
+    """knn_comm_init_ops: a host transport object with methods
+    allgather(send u8[n], recv u8[G*n]), broadcast(buf u8[n], root), alltoall(send u8[G*n],
+    recv u8[G*n]) and allreduce_max(buf int32[c]) operating on numpy views of the library's
+    pinned staging buffers (marshalling only: the collective is the transport's)."""
+    def u8(ptr, n):
+        return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(int(n),))
+
+    def wrap(fn):
+        def call(*a):
+            try:
+                fn(*a)
+                return 0
+            except Exception as e:  # reported as KNN_ERR_NCCL by the library
+                import sys
+                print(f"knn comm transport error: {e!r}", file=sys.stderr)
+                return 1
+        return call
+
+    G = int(nranks)
+    ops = CommOps(
+        _AG(wrap(lambda u, s_, r_, n: transport.allgather(u8(s_, n), u8(r_, G * n)))),
+        _BC(wrap(lambda u, b, n, root: transport.broadcast(u8(b, n), root))),
+        _A2A(wrap(lambda u, s_, r_, n: transport.alltoall(u8(s_, G * n), u8(r_, G * n)))),
+        _ARM(wrap(lambda u, b, c: transport.allreduce_max(np.ctypeslib.as_array(
+            ctypes.cast(b, ctypes.POINTER(ctypes.c_int32)), shape=(int(c),))))),
+        None)
+    ctx = context(device)
+    _check(load_library().knn_comm_init_ops(ctx, int(rank), G, ctypes.byref(ops)), ctx)
+    _ops_keep[ctx.value] = ops  # the library keeps the function pointers
+
+
+def comm_destroy(device=None):
+    ctx = context(device)
+    _check(load_library().knn_comm_destroy(ctx), ctx)
+    _ops_keep.pop(ctx.value, None)
+
+
+def comm_info(device=None):
+    """(backend 0 none / 1 NCCL / 2 host callbacks, rank, nranks)."""
+    ctx = context(device)
+    b, r, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(load_library().knn_comm_info(ctx, ctypes.byref(b), ctypes.byref(r), ctypes.byref(n)), ctx)
+    return b.value, r.value, n.value
+
+
+def graph_sharded(X, k, mode="sym", metric=L2SQ, out=None, stream=None):
+    """knn_graph_sharded (collective): X (N×d CUDA tensor) valid on rank 0, broadcast into X
+    on the other ranks; returns the full (idx N×k, dist N×k) on every rank."""
+    import torch
+    N, d = X.shape
+    ctx = context(X.device.index)
+    idx, dist = out if out is not None else _outputs(N, k, X.device)
+    rc = load_library().knn_graph_sharded(ctx, SHARD_MODES.get(mode, mode), _dev_ptr(X, torch.float32, "X"), N, d,
+                                          k, metric, _dev_ptr(idx, torch.int32, "out_idx"),
+                                          _dev_ptr(dist, torch.float32, "out_dist"), _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def search_sharded(Q, X, k, mode="query", out=None, stream=None):
+    """knn_search_sharded (collective): Q (M×d) and X (N×d) valid on rank 0."""
+    import torch
+    M, d = Q.shape
+    N = X.shape[0]
+    ctx = context(X.device.index)
+    idx, dist = out if out is not None else _outputs(M, k, X.device)
+    rc = load_library().knn_search_sharded(ctx, SHARD_MODES.get(mode, mode), _dev_ptr(Q, torch.float32, "Q"), M,
+                                           _dev_ptr(X, torch.float32, "X"), N, d, k,
+                                           _dev_ptr(idx, torch.int32, "out_idx"),
+                                           _dev_ptr(dist, torch.float32, "out_dist"), _stream(stream))
+    _check(rc, ctx)
+    return idx, dist
+
+
+def last_shard_mode(device=None):
+    """Mode the last sharded call ran (after fallbacks): 0 query, 1 corpus, 2 sym, -1 none."""
+    return int(load_library().knn_last_shard_mode(context(device)))

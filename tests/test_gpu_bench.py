@@ -44,3 +44,20 @@ def test_bench_reference_arm_is_the_oracle():
     assert b["impl"] == "reference" and b["value"] > 0
     assert b["cpu_baseline"]["kind"] == "oracle"
     assert b["e2e"]["h2d_bytes_per_step"] == 0 and b["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.parametrize("shard", ["sym", "corpus"])
+def test_bench_self_launches_ranks(shard):
+    # --gpus 2 without a launcher: bench.py starts the ranks itself; on this one-GPU box they
+    # share cuda:0 through the library's host transport (KNN_BENCH_SHARE_GPU=1)
+    env = dict(os.environ, KNN_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--shard", shard,
+                        "--no-cpu-baseline", "--no-e2e"], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    b = json.loads(lines[0])
+    assert b["n_gpus"] == 2 and b["value"] > 0
+    assert b["config"]["sharding"].startswith({"sym": "upper triangle", "corpus": "corpus columns"}[shard])
