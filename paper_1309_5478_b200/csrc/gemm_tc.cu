@@ -325,6 +325,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
             const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
             const float trow = PIVOT && row_ok ? __ldg(ep.thr + row) : -1.0f;  // row pivot
+            const uint64_t cq2 = f2_pack(cq, cq), qn2 = f2_pack(qn, qn), trow2 = f2_pack(trow, trow);
             // MINS: qn (1 + m) + m XMAX, and the cosine sentinel cap 3 + m (qn + XMAX)
             const float xmx = MINS ? __ldg(ep.xmax) : 0.0f;
             const float mins_row_term = MINS ? fmaf(ep.margin, qn + xmx, qn) * (1.0f + 0x1p-22f) : 0.0f;
@@ -397,23 +398,48 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     continue;
                 }
                 float v[32];
-                #pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    const float4 nn = cn4[c4];
-                    const float4 ss = cs4[c4];
-                    const float na[4] = {nn.x, nn.y, nn.z, nn.w};
-                    const float sa4[4] = {ss.x, ss.y, ss.z, ss.w};
+                if constexpr (SAMPLE) {
                     #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int c = 4 * c4 + e;
-                        const float nsum = qn + na[e];
-                        float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], nsum);
-                        // cosine: the sentinel clamp before any comparison (key <= T => u <= T)
-                        if (METRIC == 2) u = fminf(u, 3.0f);
-                        // MINS: the hi.hi value plus a bound of its error, so that it is never
-                        // below the FP32-accurate u of the partition
-                        // (PIVOT1: qn, xn arrive scaled by 1 - F, so u is already the lower bound)
-                        v[c] = MINS || SAMPLE ? fmaf(nsum, ep.margin, u) : PIVOT ? u : finalize_dist<METRIC>(u);
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 nn = cn4[c4];
+                        const float4 ss = cs4[c4];
+                        const float na[4] = {nn.x, nn.y, nn.z, nn.w};
+                        const float sa4[4] = {ss.x, ss.y, ss.z, ss.w};
+                        #pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int c = 4 * c4 + e;
+                            const float nsum = qn + na[e];
+                            float u = fmaf(__uint_as_float(r[c]) * cq, sa4[e], nsum);
+                            if (METRIC == 2) u = fminf(u, 3.0f);
+                            // the hi.hi value plus a bound of its error, so that it is never
+                            // below the FP32-accurate u of the partition
+                            v[c] = fmaf(nsum, ep.margin, u);
+                        }
+                    }
+                } else {
+                    // u = fl(fl(acc cq) s_j + fl(qn + xn_j)), two columns per FMUL2 / FADD2 /
+                    // FFMA2 (each half rounds as the scalar op: the same bits as before)
+                    // (PIVOT1: qn, xn arrive scaled by 1 - F, so u is already the lower bound)
+                    #pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 nn = cn4[c4];
+                        const float4 ss = cs4[c4];
+                        #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c = 4 * c4 + 2 * h;
+                            const uint64_t p = f2_mul(f2_pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), cq2);
+                            const uint64_t ns = f2_add(qn2, h ? f2_pack(nn.z, nn.w) : f2_pack(nn.x, nn.y));
+                            const uint64_t u2 = f2_fma(p, h ? f2_pack(ss.z, ss.w) : f2_pack(ss.x, ss.y), ns);
+                            float u0, u1;
+                            f2_unpack(u2, u0, u1);
+                            // cosine: the sentinel clamp before any comparison (key <= T => u <= T)
+                            if (METRIC == 2) {
+                                u0 = fminf(u0, 3.0f);
+                                u1 = fminf(u1, 3.0f);
+                            }
+                            v[c] = PIVOT ? u0 : finalize_dist<METRIC>(u0);
+                            v[c + 1] = PIVOT ? u1 : finalize_dist<METRIC>(u1);
+                        }
                     }
                 }
                 const int64_t c0 = n0 + cb;
@@ -488,17 +514,26 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     // test is an FADD and a funnel shift of its sign bit into the mask, c
                     // descending so that bit c ends at position c.  (One combined test
                     // against max(row pivot, column pivot) measured slower: 2.92 vs 2.84 ms.)
+                    // (the differences two at a time: FADD2)
                     #pragma unroll
-                    for (int c = 31; c >= 0; --c) hr = __funnelshift_l(__float_as_uint(v[c] - trow), hr, 1);
+                    for (int c = 30; c >= 0; c -= 2) {
+                        float d0, d1;
+                        f2_unpack(f2_sub(f2_pack(v[c], v[c + 1]), trow2), d0, d1);
+                        hr = __funnelshift_l(__float_as_uint(d1), hr, 1);
+                        hr = __funnelshift_l(__float_as_uint(d0), hr, 1);
+                    }
                     if (SYM && !(ep.dbg & 1)) {
                         const float4* ct4 = reinterpret_cast<const float4*>(col_t + cb);
                         #pragma unroll
                         for (int c4 = 7; c4 >= 0; --c4) {
                             const float4 tt = ct4[c4];
-                            hc = __funnelshift_l(__float_as_uint(v[4 * c4 + 3] - tt.w), hc, 1);
-                            hc = __funnelshift_l(__float_as_uint(v[4 * c4 + 2] - tt.z), hc, 1);
-                            hc = __funnelshift_l(__float_as_uint(v[4 * c4 + 1] - tt.y), hc, 1);
-                            hc = __funnelshift_l(__float_as_uint(v[4 * c4] - tt.x), hc, 1);
+                            float d0, d1, d2, d3;
+                            f2_unpack(f2_sub(f2_pack(v[4 * c4 + 2], v[4 * c4 + 3]), f2_pack(tt.z, tt.w)), d2, d3);
+                            f2_unpack(f2_sub(f2_pack(v[4 * c4], v[4 * c4 + 1]), f2_pack(tt.x, tt.y)), d0, d1);
+                            hc = __funnelshift_l(__float_as_uint(d3), hc, 1);
+                            hc = __funnelshift_l(__float_as_uint(d2), hc, 1);
+                            hc = __funnelshift_l(__float_as_uint(d1), hc, 1);
+                            hc = __funnelshift_l(__float_as_uint(d0), hc, 1);
                         }
                     }
                     const uint32_t hm = hr | hc;
