@@ -117,8 +117,12 @@ struct DeferredFlush {
         for (int j = 0; j < J; ++j) {
             if (pos[j] >= 0) {
                 if (pos[j] < ep.cap) {
-                    ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = k[j];
-                    ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = c[j];
+                    if (ep.dbg & 32) {  // DIAGNOSTIC: one interleaved 8-byte store per entry (wrong lists)
+                        reinterpret_cast<uint2*>(ep.ckey)[(int64_t)r[j] * ep.cap + pos[j]] = make_uint2(k[j], c[j]);
+                    } else {
+                        ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = k[j];
+                        ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = c[j];
+                    }
                 } else {
                     *ep.flag |= 2;
                 }

@@ -130,8 +130,10 @@ __device__ __noinline__ uint32_t warp_select_k(const uint32_t* ckey, const uint3
         const uint32_t m = __ballot_sync(FULL, p);
         if (p) {
             const int pos = base + __popc(m & lanemask_lt());
-            okey[pos] = kk;
-            oidx[pos] = ii;
+            if (pos < k) {  // (only repeated (key, idx) pairs, never produced, could pass k)
+                okey[pos] = kk;
+                oidx[pos] = ii;
+            }
         }
         base += __popc(m);
     }
