@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define KNN_ABI_VERSION 1
+#define KNN_ABI_VERSION 2
 
 typedef struct knn_ctx* knn_ctx_t;
 
@@ -205,7 +205,9 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
  *     roundup(N, 256) floats, NaN past N.  Asynchronous.
  *  2. knn_graph_partition: the partition GEMM over the triangle units [unit_lo, unit_hi)
  *     (knn_graph_units(N) in total), appending candidates of ANY row to the caller's lists
- *     cnt[N] (zeroed here), ckey/cidx[N][cap].  Asynchronous.  Directly after
+ *     cnt[N] (zeroed here) and cent[N][cap] (cap = knn_graph_list_cap(k)): 64-bit entries
+ *     (key << 32 | column), key = the order-preserving bits of the distance (IEEE bits
+ *     with the sign bit set, for values >= +0).  Asynchronous.  Directly after
  *     knn_graph_pivots on the same ctx, points, metric and stream it reuses the operands
  *     that call prepared (no second pass over X).
  *  3. knn_graph_gather_select: for rows [row0, row0+rows), concatenates the G ranks' lists
@@ -220,11 +222,10 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
                             int64_t row0, int64_t rows, float* thr, void* stream);
 knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
                                int32_t metric, const float* thr, int64_t unit_lo, int64_t unit_hi,
-                               int32_t* cnt, uint32_t* ckey, uint32_t* cidx, int32_t cap, void* stream);
+                               int32_t* cnt, uint64_t* cent, int32_t cap, void* stream);
 knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* const* cnts,
-                                   const uint32_t* const* ckeys, const uint32_t* const* cidxs,
-                                   int32_t cap, int64_t N, int32_t k, int64_t row0, int64_t rows,
-                                   int32_t* out_idx, float* out_dist, void* stream);
+                                   const uint64_t* const* cents, int32_t cap, int64_t N, int32_t k,
+                                   int64_t row0, int64_t rows, int32_t* out_idx, float* out_dist, void* stream);
 
 /* CUDA IPC plumbing for knn_merge_lists across processes (one process per GPU):
  * knn_ipc_export writes the 64-byte IPC handle of the allocation holding dev_ptr and the

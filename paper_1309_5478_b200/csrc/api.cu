@@ -165,7 +165,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int32_t* flag = nullptr;
     float* thr = nullptr;
     int32_t* cnt = nullptr;
-    uint32_t *ckey = nullptr, *cidx = nullptr;
+    uint64_t* cent = nullptr;  // per-row candidate lists (ukey << 32 | col)
     int32_t* redo = nullptr;
     Prepared smp{};  // the pivot plans' column sample (gathered points)
     float *nsc_x = nullptr, *nsc_q = nullptr;  // single-product partition: scaled norms
@@ -187,8 +187,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             }
             thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
-            ckey = c.take<uint32_t>((size_t)M * cp);
-            cidx = c.take<uint32_t>((size_t)M * cp);
+            cent = c.take<uint64_t>((size_t)M * cp);
         }
     };
     layout_all(probe);
@@ -243,19 +242,19 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         }
         Timed tg(ctx, KNN_KERNEL_FUSED, s);
         if (one)
-            KNN_CUDA(knn::launch_dist_tc_pivot1(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
+            KNN_CUDA(knn::launch_dist_tc_pivot1(op, metric, self_shift, pivot_sym, thr, cnt, cent, cap,
                                                 flag, ctx->num_sms, s));
         else
-            KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, cap,
+            KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, cent, cap,
                                                flag, ctx->num_sms, s));
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         if (one)
-            KNN_CUDA(knn::launch_candidate_recompute(cnt, ckey, cidx, cap, M, k, idx_offset, Q, X, d, pq.sqn,
+            KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, M, k, idx_offset, Q, X, d, pq.sqn,
                                                      px.sqn, thr, knn::pivot1_margin(d_pad), metric, out_idx,
                                                      out_dist, flag, s));
         else
-            KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, M, k, idx_offset, out_idx, out_dist, flag,
+            KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, M, k, idx_offset, out_idx, out_dist, flag,
                                                   s));
         tc2.done();
         return KNN_OK;
@@ -284,12 +283,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         }
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
         Timed tg(ctx, KNN_KERNEL_FUSED, s);
-        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, ckey, cidx, capq,
+        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, cent, capq,
                                            flag, ctx->num_sms, s));
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         ctx->launches++;  // warp-per-row select + the CTA kernel for its redo rows
-        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, capq, M, k, idx_offset, out_idx, out_dist,
+        KNN_CUDA(knn::launch_candidate_select_large(cnt, cent, capq, M, k, idx_offset, out_idx, out_dist,
                                                     flag, redo, s));
         tc2.done();
         return KNN_OK;
@@ -948,9 +947,9 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
 
 knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,
                                int32_t metric, const float* thr, int64_t unit_lo, int64_t unit_hi,
-                               int32_t* cnt, uint32_t* ckey, uint32_t* cidx, int32_t cap, void* stream) {
+                               int32_t* cnt, uint64_t* cent, int32_t cap, void* stream) {
     KNN_TRY(graph_shard_check(ctx, X, N, d, k, metric));
-    if (!thr || !cnt || !ckey || !cidx || cap < k) return fail(ctx, KNN_ERR_ARG, "bad lists");
+    if (!thr || !cnt || !cent || cap < k) return fail(ctx, KNN_ERR_ARG, "bad lists");
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
@@ -983,7 +982,7 @@ knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t
     }
     knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
     Timed tg(ctx, KNN_KERNEL_FUSED, s);
-    KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, 0, true, thr, cnt, ckey, cidx, cap, flag, ctx->num_sms, s,
+    KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
                                        unit_lo, unit_hi));
     tg.done();
     ctx->last_plan = 3;
@@ -991,11 +990,10 @@ knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t
 }
 
 knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* const* cnts,
-                                   const uint32_t* const* ckeys, const uint32_t* const* cidxs,
-                                   int32_t cap, int64_t N, int32_t k, int64_t row0, int64_t rows,
-                                   int32_t* out_idx, float* out_dist, void* stream) {
+                                   const uint64_t* const* cents, int32_t cap, int64_t N, int32_t k,
+                                   int64_t row0, int64_t rows, int32_t* out_idx, float* out_dist, void* stream) {
     if (!ctx) return KNN_ERR_ARG;
-    if (G < 1 || G > 64 || !cnts || !ckeys || !cidxs || cap < k || k < 1 || k > KNN_MAX_K)
+    if (G < 1 || G > 64 || !cnts || !cents || cap < k || k < 1 || k > KNN_MAX_K)
         return fail(ctx, KNN_ERR_ARG, "bad G, lists or k");
     if (row0 < 0 || rows < 0 || row0 + rows > N) return fail(ctx, KNN_ERR_ARG, "bad row range");
     if (rows == 0) return KNN_OK;
@@ -1003,14 +1001,13 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t *flag = nullptr, *cnt = nullptr;
-    uint32_t *ckey = nullptr, *cidx = nullptr;
+    uint64_t* cent = nullptr;
     int32_t* redo = nullptr;
     auto layout = [&](Carve& c) {
         flag = c.take<int32_t>(4);
         redo = c.take<int32_t>(rows + 1);
         cnt = c.take<int32_t>(rows);
-        ckey = c.take<uint32_t>((size_t)rows * cap);
-        cidx = c.take<uint32_t>((size_t)rows * cap);
+        cent = c.take<uint64_t>((size_t)rows * cap);
     };
     Carve probe{nullptr};
     layout(probe);
@@ -1019,12 +1016,11 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     layout(carve);
     KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
     Timed tm(ctx, KNN_KERNEL_MERGE, s);
-    KNN_CUDA(knn::launch_gather_lists(cnts, ckeys, cidxs, G, cap, row0, rows, cap, cnt, ckey, cidx, flag, s));
+    KNN_CUDA(knn::launch_gather_lists(cnts, cents, G, cap, row0, rows, cap, cnt, cent, flag, s));
     if (k <= 32)
-        KNN_CUDA(knn::launch_candidate_select(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, s));
+        KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, rows, k, 0, out_idx, out_dist, flag, s));
     else
-        KNN_CUDA(knn::launch_candidate_select_large(cnt, ckey, cidx, cap, rows, k, 0, out_idx, out_dist, flag, redo,
-                                                          s));
+        KNN_CUDA(knn::launch_candidate_select_large(cnt, cent, cap, rows, k, 0, out_idx, out_dist, flag, redo, s));
     tm.done();
     knn_status st = finish_blocking(ctx, s);
     drain_profile(ctx);

@@ -59,8 +59,9 @@ struct EpiArgs {
     const float* qn; const float* q_rs; int64_t M;
     const float* xn; const float* x_rs; int64_t N;  // column arrays padded to 256 entries
     int32_t metric; int64_t self_shift; float* D; int64_t ldD;
-    // PIVOT (partition epilogue): per-row pivots in the squared domain, candidate lists
-    const float* thr; int32_t* cnt; uint32_t* ckey; uint32_t* cidx; int32_t cap; int32_t* flag;
+    // PIVOT (partition epilogue): per-row pivots in the squared domain; per-row candidate
+    // lists cent[row * cap + i], i < cnt[row], entries (ukey << 32 | col)
+    const float* thr; int32_t* cnt; uint64_t* cent; int32_t cap; int32_t* flag;
     float margin;  // MINS: error bound of the hi.hi value, relative to ||q||^2 + ||x||^2
     // MINS / SAMPLE with a strided column sample: matrix column block nb is output column
     // block nb / nb_stride
@@ -89,8 +90,7 @@ inline int metric_kind(int32_t metric) { return metric == 1 ? 1 : metric >= 2 ? 
 __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint32_t key, uint32_t col) {
     const int pos = atomicAdd(ep.cnt + r, 1);
     if (pos < ep.cap) {
-        ep.ckey[r * ep.cap + pos] = key;
-        ep.cidx[r * ep.cap + pos] = col;
+        ep.cent[r * ep.cap + pos] = (uint64_t)key << 32 | col;
     } else {
         *ep.flag |= 2;  // overflow: the caller redoes the problem with the full matrix
     }
@@ -117,12 +117,10 @@ struct DeferredFlush {
         for (int j = 0; j < J; ++j) {
             if (pos[j] >= 0) {
                 if (pos[j] < ep.cap) {
-                    if (ep.dbg & 32) {  // DIAGNOSTIC: one interleaved 8-byte store per entry (wrong lists)
-                        reinterpret_cast<uint2*>(ep.ckey)[(int64_t)r[j] * ep.cap + pos[j]] = make_uint2(k[j], c[j]);
-                    } else {
-                        ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = k[j];
-                        ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = c[j];
-                    }
+                    // one 8-byte store per entry (two 4-byte lists cost twice the scattered
+                    // L2 transactions and left twice the partially written sectors, which
+                    // HBM3 fills by read-modify-write: profiles/r02_partition_traffic.txt)
+                    ep.cent[(int64_t)r[j] * ep.cap + pos[j]] = (uint64_t)k[j] << 32 | c[j];
                 } else {
                     *ep.flag |= 2;
                 }
@@ -187,8 +185,7 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
             const int i = i0 + 32 * j + lane;
             if (i < n) {
                 if (pos[j] < ep.cap) {
-                    ep.ckey[(int64_t)r[j] * ep.cap + pos[j]] = pkey[i];
-                    ep.cidx[(int64_t)r[j] * ep.cap + pos[j]] = pcol[i];
+                    ep.cent[(int64_t)r[j] * ep.cap + pos[j]] = (uint64_t)pkey[i] << 32 | pcol[i];
                 } else {
                     *ep.flag |= 2;
                 }
@@ -793,7 +790,7 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
     const int64_t pairs = num_tiles < num_sms / CLUSTER ? num_tiles : num_sms / CLUSTER;
     const int grid = (int)(pairs * CLUSTER);
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, D, ldD,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+               nullptr, nullptr, nullptr, 0, nullptr};
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_STORE, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_STORE, TileSched> : dist_tc_kernel<0, false, MODE_STORE, TileSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
@@ -823,7 +820,7 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
     const int64_t units = sched.n * (sched.n + 1) / 2;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, 0, D, ldD,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+               nullptr, nullptr, nullptr, 0, nullptr};
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, true, MODE_STORE, SymSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, true, MODE_STORE, SymSched> : dist_tc_kernel<0, true, MODE_STORE, SymSched>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
@@ -854,7 +851,7 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
                            op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns, xmax};
+               nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns, xmax};
     TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
@@ -884,7 +881,7 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
                            op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, Ds, ldS,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
+               nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
     TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
@@ -898,7 +895,7 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
 
 template <int MODE>
 cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                              const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                              const float* thr, int32_t* cnt, uint64_t* cent,
                               int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
                               int64_t unit_lo, int64_t unit_hi, float margin) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
@@ -911,7 +908,7 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, sym ? 0 : self_shift, nullptr, 0,
-               thr, cnt, ckey, cidx, cap, flag, margin};
+               thr, cnt, cent, cap, flag, margin};
     if (const char* dv = getenv("KNN_DBG_EPI")) ep.dbg = atoi(dv);
     cudaError_t e;
     if (sym) {
@@ -944,10 +941,10 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
 }
 
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                 const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
                                  int64_t unit_lo, int64_t unit_hi) {
-    return launch_pivot_impl<MODE_PIVOT>(op, metric, self_shift, sym, thr, cnt, ckey, cidx, cap, flag, num_sms,
+    return launch_pivot_impl<MODE_PIVOT>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag, num_sms,
                                          s, unit_lo, unit_hi, 0.0f);
 }
 
@@ -960,10 +957,10 @@ float pivot1_margin(int32_t d_pad) {
 }
 
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                   int32_t cap, int32_t* flag, int num_sms, cudaStream_t s) {
     if (metric_kind(metric) == 2) return cudaErrorInvalidValue;  // L2 metrics only
-    return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, ckey, cidx, cap, flag,
+    return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag,
                                           num_sms, s, -1, -1, pivot1_margin(op.d_pad));
 }
 
@@ -977,7 +974,7 @@ cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cud
         !tc_make_operand_map(&mxl, op.x_lo, op.N, op.d_pad, BN / 2))
         return cudaErrorInvalidValue;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, 0, INT64_MIN, nullptr, 0,
-               nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+               nullptr, nullptr, nullptr, 0, nullptr};
     cudaError_t e;
     if (sym) {
         SymSched sched{ceil_div(op.N, BN)};

@@ -65,21 +65,22 @@ cudaError_t launch_dist_tc(const TcOperands& op, int32_t metric, int64_t self_sh
 cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, int64_t ldD,
                                int num_sms, cudaStream_t s);
 // Pivot (partition) plan: the GEMM keeps, per row, the elements at or below thr[row]
-// (squared domain) as candidates ckey/cidx[row*cap + i], i < cnt[row]; SYM also records
-// the transposed element for the column's row.  flag |= 2 on candidate overflow.
+// (squared domain) as candidates cent[row*cap + i], i < cnt[row], entries (ukey << 32 | col)
+// (the ukey of the distance: order-preserving bits); SYM also records the transposed
+// element for the column's row.  flag |= 2 on candidate overflow.
 // unit_lo / unit_hi (sym only): the triangle's units [unit_lo, unit_hi); -1 = all.
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                                 const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                 const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
                                  int64_t unit_lo = -1, int64_t unit_hi = -1);
 // The same partition from the single hi.hi product (L2 metrics): kept iff the lower bound
-// L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); ckey holds L.
+// L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); the key is L.
 // F = pivot1_margin(d_pad) bounds |u_hh - D| / (||q||^2 + ||x||^2) for the exact D.
 // op.qn / op.xn must be the prep norms scaled by 1 - F (launch_scale_norms).
 cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s);
 float pivot1_margin(int32_t d_pad);
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
-                                  const float* thr, int32_t* cnt, uint32_t* ckey, uint32_t* cidx,
+                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                   int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
 // Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s);
@@ -100,7 +101,7 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
 // tiles of pivots; pad_end must not pass the caller's allocation (absolute limit).
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int64_t pad_end, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s);
-cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_select(const int32_t* cnt, const uint64_t* cent,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                     int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
 // k > 32 pivot plan: per-row pivot with >= r of the S sampled upper bounds at or below it;
@@ -112,21 +113,20 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
 // re-evaluates the few candidates whose bounds reach the k-th upper bound in fp64 from the
 // fp32 inputs Q [M][d] / X [N][d]; qn / xn the prep norms, margin = pivot1_margin.
 // flag |= 2 when the partition is not certified exact for some row (the caller redoes).
-cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
                                        const float* X, int32_t d, const float* qn, const float* xn,
                                        const float* thr, float margin, int32_t metric, int32_t* out_idx,
                                        float* out_dist, int32_t* flag, cudaStream_t s);
 // redo: M + 1 int32 of workspace for the warp-per-row form (null: CTA per row only).
-cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint64_t* cent,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                           int32_t* out_idx, float* out_dist, int32_t* flag, int32_t* redo,
                                           cudaStream_t s);
 // Multi-GPU symmetric k-NNG: concatenate G (possibly peer-mapped) candidate lists per row.
-cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* const* keys, const uint32_t* const* idxs,
+cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint64_t* const* ents,
                                 int32_t G, int32_t cap_src, int64_t row0, int64_t rows, int32_t cap_dst,
-                                int32_t* cnt_dst, uint32_t* key_dst, uint32_t* idx_dst, int32_t* flag,
-                                cudaStream_t s);
+                                int32_t* cnt_dst, uint64_t* ent_dst, int32_t* flag, cudaStream_t s);
 bool tc_supported();  // device is sm_100 and the driver entry point for TMA maps exists
 
 

@@ -1580,8 +1580,8 @@ __device__ __forceinline__ void sort16(uint32_t (&v)[CS_PER]) {
             }
 }
 __global__ void __launch_bounds__(256)
-candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
-                        const uint32_t* __restrict__ cidx, int cap, int64_t M, int k,
+candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                        int cap, int64_t M, int k,
                         int64_t idx_offset, int32_t* __restrict__ out_idx,
                         float* __restrict__ out_dist, int32_t* __restrict__ flag) {
     __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
@@ -1595,8 +1595,9 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
     if (n < k && lane == 0) atomicOr(flag, 2);
     n = n < cap ? n : cap;
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
-    const uint32_t* rk = ckey + row * cap;
-    const uint32_t* ri = cidx + row * cap;
+    // the row's entries (ukey << 32 | col): keys are the odd words, columns the even ones
+    const uint32_t* ri = reinterpret_cast<const uint32_t*>(cent + row * cap);
+    const uint32_t* rk = ri + 1;
     const uint32_t* fk = rk;
     const uint32_t* fi = ri;
     int m = n;
@@ -1605,7 +1606,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
         if (n <= 32 * CS_PER) {
             uint32_t uk[CS_PER], v[CS_PER];  // this lane's keys (list order), sorted copy
             #pragma unroll
-            for (int i = 0; i < CS_PER; ++i) uk[i] = lane + 32 * i < n ? __ldg(rk + lane + 32 * i) : 0xFFFFFFFFu;
+            for (int i = 0; i < CS_PER; ++i) uk[i] = lane + 32 * i < n ? __ldg(rk + 2 * (lane + 32 * i)) : 0xFFFFFFFFu;
             #pragma unroll
             for (int i = 0; i < CS_PER; ++i) v[i] = uk[i];
             sort16(v);
@@ -1630,7 +1631,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
                 if (p2) {
                     const int pos = base + __popc(bm & ws::lanemask_lt());
                     skey[w][pos] = uk[i];
-                    sidx[w][pos] = __ldg(ri + lane + 32 * i);
+                    sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
                 }
                 base += __popc(bm);
             }
@@ -1642,7 +1643,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
                 const int pos = base + eq + __popc(bm & ws::lanemask_lt());
                 if (p2 && pos < 32) {
                     skey[w][pos] = T;
-                    sidx[w][pos] = __ldg(ri + lane + 32 * i);
+                    sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
                 }
                 eq += __popc(bm);
             }
@@ -1655,7 +1656,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restr
             }
         }
         if (!done) {
-            ws::warp_select_k<1>(rk, ri, n, k, skey[w], sidx[w], hist[w]);
+            ws::warp_select_k<2>(rk, ri, n, k, skey[w], sidx[w], hist[w]);
             fk = skey[w];
             fi = sidx[w];
             m = k;
@@ -1689,8 +1690,8 @@ constexpr int CR_PER = 16;
 constexpr int CR_RCAP = 256;
 constexpr int CR_G = 8;
 __global__ void __launch_bounds__(256, 4)
-candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey,
-                           const uint32_t* __restrict__ cidx, int cap, int64_t M, int k, int64_t idx_offset,
+candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                           int cap, int64_t M, int k, int64_t idx_offset,
                            const float* __restrict__ Q, const float* __restrict__ X, int d,
                            const float* __restrict__ qn, const float* __restrict__ xn,
                            const float* __restrict__ thr, float margin, float rerr, int metric, int vec,
@@ -1708,8 +1709,8 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
     }
     n = n < cap ? n : cap;
     if (lane == 0 && !(vec & 2)) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
-    const uint32_t* rk = ckey + row * cap;
-    const uint32_t* ri = cidx + row * cap;
+    const uint32_t* ri = reinterpret_cast<const uint32_t*>(cent + row * cap);  // (key << 32 | col)
+    const uint32_t* rk = ri + 1;
     const float qnr = __ldg(qn + row), f2 = 2.0f * margin;
     // 1. T
     const int n1 = n < 32 * CR_PER ? n : 32 * CR_PER;
@@ -1717,8 +1718,8 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
     #pragma unroll
     for (int i = 0; i < CR_PER; ++i) {
         const int pos = lane + 32 * i;
-        lk[i] = pos < n1 ? __ldg(rk + pos) : 0xFFFFFFFFu;
-        li[i] = pos < n1 ? __ldg(ri + pos) : 0u;
+        lk[i] = pos < n1 ? __ldg(rk + 2 * pos) : 0xFFFFFFFFu;
+        li[i] = pos < n1 ? __ldg(ri + 2 * pos) : 0u;
     }
     #pragma unroll
     for (int i = 0; i < CR_PER; ++i) {
@@ -1753,10 +1754,10 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
     }
     for (int base = n1; base < n; base += 32) {
         const int pos = base + lane;
-        const bool keep = pos < n && __ldg(rk + pos) <= Tf;
+        const bool keep = pos < n && __ldg(rk + 2 * pos) <= Tf;
         const uint32_t bm = __ballot_sync(FULL, keep);
         const int slot = nr + __popc(bm & ws::lanemask_lt());
-        if (keep && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + pos);
+        if (keep && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + 2 * pos);
         nr += __popc(bm);
     }
     if (lane == 0 && (vec & 2))  // diagnostic (KNN_RECOMP_STATS): count |R| instead
@@ -1774,10 +1775,10 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint32_t* __re
         int ridx = 0;
         for (int base = 0; base < n; base += 32) {
             const int pos = base + lane;
-            const bool keep = pos < n && __ldg(rk + pos) <= Tf;
+            const bool keep = pos < n && __ldg(rk + 2 * pos) <= Tf;
             const uint32_t bm = __ballot_sync(FULL, keep);
             const int slot = ridx + __popc(bm & ws::lanemask_lt()) - win * CR_RCAP;
-            if (keep && slot >= 0 && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + pos);
+            if (keep && slot >= 0 && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + 2 * pos);
             ridx += __popc(bm);
         }
         __syncwarp();
@@ -2125,8 +2126,8 @@ pivot_from_sample_warp_kernel(const float* __restrict__ Ds, int64_t M, int64_t S
 constexpr int CS_THREADS = 256;
 constexpr int CS_BINS = 4096;
 __global__ void __launch_bounds__(CS_THREADS, 4)
-candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
-                              const uint32_t* __restrict__ cidx_g, int32_t cap, int64_t M, int k,
+candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                              int32_t cap, int64_t M, int k,
                               int KP, int64_t idx_offset, int32_t* __restrict__ out_idx,
                               float* __restrict__ out_dist, int32_t* __restrict__ flag,
                               const int32_t* __restrict__ list) {
@@ -2148,22 +2149,20 @@ candidate_select_large_kernel(const int32_t* __restrict__ cnt, const uint32_t* _
             continue;
         }
         // all of this thread's loads in flight before the shared-memory stores
-        const uint32_t* gk = ckey_g + row * cap;
-        const uint32_t* gi = cidx_g + row * cap;
+        const unsigned long long* ge = reinterpret_cast<const unsigned long long*>(cent + row * cap);
         for (int i0 = 0; i0 < n; i0 += 8 * CS_THREADS) {
-            uint32_t kv[8], iv[8];
+            uint64_t ev[8];
             #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i = i0 + u * CS_THREADS + threadIdx.x;
-                kv[u] = i < n ? __ldcs(gk + i) : 0u;
-                iv[u] = i < n ? __ldcs(gi + i) : 0u;
+                ev[u] = i < n ? __ldcs(ge + i) : 0ull;
             }
             #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i = i0 + u * CS_THREADS + threadIdx.x;
                 if (i < n) {
-                    ckey[i] = kv[u];
-                    cidx[i] = iv[u];
+                    ckey[i] = (uint32_t)(ev[u] >> 32);
+                    cidx[i] = (uint32_t)ev[u];
                 }
             }
         }
@@ -2190,8 +2189,8 @@ __host__ __device__ constexpr size_t csw_slab_bytes(int KP) {
     return (size_t)CSW_BINS * 2 + (size_t)KP * 8 + (size_t)CSW_STAR * 8 + 16;
 }
 __global__ void __launch_bounds__(32 * CSW_WARPS)
-candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ckey_g,
-                             const uint32_t* __restrict__ cidx_g, int32_t cap, int64_t M, int k, int KP,
+candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                             int32_t cap, int64_t M, int k, int KP,
                              int64_t idx_offset, int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
                              int32_t* __restrict__ flag, int32_t* __restrict__ redo) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -2210,8 +2209,9 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
             if (lane == 0) atomicOr(flag, 2);
             continue;
         }
-        const uint32_t* gk = ckey_g + row * cap;
-        const uint32_t* gi = cidx_g + row * cap;
+        // the row's entries (ukey << 32 | col): keys are the odd words, columns the even ones
+        const uint32_t* gi = reinterpret_cast<const uint32_t*>(cent + row * cap);
+        const uint32_t* gk = gi + 1;
         auto to_redo = [&]() {
             if (lane == 0) {
                 const int slot = atomicAdd(redo, 1);
@@ -2228,7 +2228,7 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j) {
                 const int i = base + 32 * j + lane;
-                kv[j] = i < n ? __ldcg(gk + i) : 0xFFFFFFFFu;
+                kv[j] = i < n ? __ldcg(gk + 2 * i) : 0xFFFFFFFFu;
             }
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j) {
@@ -2257,7 +2257,7 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j) {
                 const int i = base + 32 * j + lane;
-                kv[j] = i < n ? __ldcg(gk + i) : 0u;
+                kv[j] = i < n ? __ldcg(gk + 2 * i) : 0u;
             }
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j)
@@ -2314,8 +2314,8 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j) {
                 const int i = base + 32 * j + lane;
-                kv[j] = i < n ? __ldcs(gk + i) : 0xFFFFFFFFu;
-                iv[j] = i < n ? __ldcs(gi + i) : 0u;
+                kv[j] = i < n ? __ldcs(gk + 2 * i) : 0xFFFFFFFFu;
+                iv[j] = i < n ? __ldcs(gi + 2 * i) : 0u;
             }
             #pragma unroll
             for (int j = 0; j < CSW_EPT; ++j) {
@@ -2398,13 +2398,11 @@ candidate_select_warp_kernel(const int32_t* __restrict__ cnt, const uint32_t* __
 // overflowed (cnt > cap_src) or a row whose concatenation exceeds cap_dst sets flag bit 2.
 struct SrcLists {
     const int32_t* cnt[64];
-    const uint32_t* key[64];
-    const uint32_t* idx[64];
+    const uint64_t* ent[64];
 };
 __global__ void __launch_bounds__(256)
 gather_lists_kernel(const SrcLists src, int G, int cap_src, int64_t row0, int64_t rows, int cap_dst,
-                    int32_t* __restrict__ cnt_dst, uint32_t* __restrict__ key_dst,
-                    uint32_t* __restrict__ idx_dst, int32_t* __restrict__ flag) {
+                    int32_t* __restrict__ cnt_dst, uint64_t* __restrict__ ent_dst, int32_t* __restrict__ flag) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= rows) return;
@@ -2417,14 +2415,10 @@ gather_lists_kernel(const SrcLists src, int G, int cap_src, int64_t row0, int64_
             bad = true;
             n = cap_src;
         }
-        const uint32_t* sk = src.key[g] + row * cap_src;
-        const uint32_t* si = src.idx[g] + row * cap_src;
+        const uint64_t* se = src.ent[g] + row * cap_src;
         for (int i = lane; i < n; i += 32) {
             const int o = total + i;
-            if (o < cap_dst) {
-                key_dst[r * cap_dst + o] = sk[i];
-                idx_dst[r * cap_dst + o] = si[i];
-            }
+            if (o < cap_dst) ent_dst[r * cap_dst + o] = se[i];
         }
         total += n;
     }
@@ -2622,12 +2616,12 @@ cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M,
     return cudaGetLastError();
 }
 
-cudaError_t launch_candidate_select(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_select(const int32_t* cnt, const uint64_t* cent,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                     int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s) {
     if (M == 0) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
-    candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, ckey, cidx, cap, M, k, idx_offset,
+    candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset,
                                                                     out_idx, out_dist, flag);
     return cudaGetLastError();
 }
@@ -2701,7 +2695,7 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
     return cudaGetLastError();
 }
 
-cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint64_t* cent,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
                                           int32_t* out_idx, float* out_dist, int32_t* flag, int32_t* redo,
                                           cudaStream_t s) {
@@ -2721,7 +2715,7 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ck
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, candidate_select_warp_kernel, 32 * CSW_WARPS, wsm);
         int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
         if (g > ceil_div(M, CSW_WARPS)) g = ceil_div(M, CSW_WARPS);
-        candidate_select_warp_kernel<<<(unsigned)g, 32 * CSW_WARPS, wsm, s>>>(cnt, ckey, cidx, cap, M, k, KP,
+        candidate_select_warp_kernel<<<(unsigned)g, 32 * CSW_WARPS, wsm, s>>>(cnt, cent, cap, M, k, KP,
                                                                             idx_offset, out_idx, out_dist, flag,
                                                                             redo);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -2738,13 +2732,13 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint32_t* ck
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, candidate_select_large_kernel, CS_THREADS, smem);
     int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > M) grid = M;
-    candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, ckey, cidx, cap, M, k, KP,
+    candidate_select_large_kernel<<<(unsigned)grid, CS_THREADS, smem, s>>>(cnt, cent, cap, M, k, KP,
                                                                           idx_offset, out_idx, out_dist, flag,
                                                                           warp ? redo : nullptr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint32_t* ckey, const uint32_t* cidx,
+cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
                                        const float* X, int32_t d, const float* qn, const float* xn,
                                        const float* thr, float margin, int32_t metric, int32_t* out_idx,
@@ -2756,26 +2750,24 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint32_t* ckey,
     const float rerr = (float)(((d + 31) / 32 + 8) * std::ldexp(1.0, -24));
     const int vec = ((d % 4 == 0) && ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(X)) & 15) == 0) |
                     (getenv_flag("KNN_RECOMP_STATS") ? 2 : 0);
-    candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, ckey, cidx, cap, M, k, idx_offset, Q,
+    candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset, Q,
                                                                        X, d, qn, xn, thr, margin, rerr, metric, vec,
                                                                        out_idx, out_dist, flag);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint32_t* const* keys, const uint32_t* const* idxs,
+cudaError_t launch_gather_lists(const int32_t* const* cnts, const uint64_t* const* ents,
                                 int32_t G, int32_t cap_src, int64_t row0, int64_t rows, int32_t cap_dst,
-                                int32_t* cnt_dst, uint32_t* key_dst, uint32_t* idx_dst, int32_t* flag,
-                                cudaStream_t s) {
+                                int32_t* cnt_dst, uint64_t* ent_dst, int32_t* flag, cudaStream_t s) {
     if (rows == 0) return cudaSuccess;
     if (G < 1 || G > 64) return cudaErrorInvalidValue;
     SrcLists src{};
     for (int g = 0; g < G; ++g) {
         src.cnt[g] = cnts[g];
-        src.key[g] = keys[g];
-        src.idx[g] = idxs[g];
+        src.ent[g] = ents[g];
     }
     gather_lists_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(src, G, cap_src, row0, rows, cap_dst, cnt_dst,
-                                                                    key_dst, idx_dst, flag);
+                                                                    ent_dst, flag);
     return cudaGetLastError();
 }
 

@@ -91,8 +91,8 @@ struct Comm {
     int32_t* dflag = nullptr;  // device int32 x 4: agreement / barrier all-reduces
     void* hbuf = nullptr;      // pinned host staging of the callback transport
     size_t hbuf_size = 0;
-    // Par-3 candidate lists: one cudaMalloc (cnt | ckey | cidx) so that one IPC handle maps
-    // it; peers' lists mapped once per allocation
+    // Par-3 candidate lists: one cudaMalloc (cnt | cent) so that one IPC handle maps it;
+    // peers' lists mapped once per allocation
     void* lists = nullptr;
     int64_t lists_N = 0;
     int32_t lists_cap = 0;
@@ -389,7 +389,7 @@ knn_status ensure_lists(knn_ctx* ctx, Comm* c, int64_t N, int32_t cap) {
     if (c->lists && c->lists_N == N && c->lists_cap == cap) return KNN_OK;
     KNN_CUDA(cudaDeviceSynchronize());
     release_lists(ctx, c);
-    const size_t bytes = (size_t)round_up(N, knn::kColPad) * 4 + 2 * (size_t)N * cap * 4;
+    const size_t bytes = (size_t)round_up(N, knn::kColPad) * 4 + (size_t)N * cap * 8;
     if (cudaMalloc(&c->lists, bytes) != cudaSuccess) {
         cudaGetLastError();
         c->lists = nullptr;
@@ -510,26 +510,24 @@ knn_status run_sym_sharded(knn_ctx* ctx, const float* X, int64_t N, int32_t d, i
     KNN_CUDA(cudaMemsetAsync(thr + N, 0xFF, (size_t)(T - N) * sizeof(float), s));
     // 2. partition GEMM over this rank's units of the triangle -> own lists (any row)
     int32_t* cnt = static_cast<int32_t*>(c->lists);
-    uint32_t* ckey = reinterpret_cast<uint32_t*>(static_cast<char*>(c->lists) + npad * 4);
-    uint32_t* cidx = ckey + (size_t)N * cap;
+    uint64_t* cent = reinterpret_cast<uint64_t*>(static_cast<char*>(c->lists) + npad * 4);
     const Range ur = shard_range(knn_graph_units(N), G, r);
-    st = knn_graph_partition(ctx, X, N, d, k, metric, thr, ur.lo, ur.hi, cnt, ckey, cidx, cap, s);
+    st = knn_graph_partition(ctx, X, N, d, k, metric, thr, ur.lo, ur.hi, cnt, cent, cap, s);
     KNN_TRY(agree_status(ctx, st, 0, &agreed, s));  // also: every rank's partition was queued
     // every rank's partition must be complete before any rank reads its lists
     KNN_TRY(c_stream_barrier(ctx, s));
     // 3. exact select of this rank's rows from the G ranks' lists (peer memory over NVLink)
     std::vector<const int32_t*> cnts(G);
-    std::vector<const uint32_t*> ckeys(G), cidxs(G);
+    std::vector<const uint64_t*> cents(G);
     for (int g = 0; g < G; ++g) {
         char* base = static_cast<char*>(G > 1 ? c->peer[g] : c->lists);
         cnts[g] = reinterpret_cast<const int32_t*>(base);
-        ckeys[g] = reinterpret_cast<const uint32_t*>(base + npad * 4);
-        cidxs[g] = ckeys[g] + (size_t)N * cap;
+        cents[g] = reinterpret_cast<const uint64_t*>(base + npad * 4);
     }
     st = KNN_OK;
     if (rr.hi > rr.lo)
-        st = knn_graph_gather_select(ctx, G, cnts.data(), ckeys.data(), cidxs.data(), cap, N, k, rr.lo,
-                                     rr.hi - rr.lo, own_i, own_d, s);
+        st = knn_graph_gather_select(ctx, G, cnts.data(), cents.data(), cap, N, k, rr.lo, rr.hi - rr.lo, own_i,
+                                     own_d, s);
     const bool cert_failed = st == KNN_ERR_INTERNAL;
     // after this agreement no rank reads another's lists any more (each contributes after
     // its blocking select), so the next call may overwrite them

@@ -103,8 +103,8 @@ def load_library():
             "knn_diag_mainloop": (st, [p, p, i64, i32, i32, i32, ctypes.POINTER(ctypes.c_double)]),
             "knn_graph_list_cap": (i32, [i32]),
             "knn_graph_pivots": (st, [p, p, i64, i32, i32, i32, i64, i64, p, p]),
-            "knn_graph_partition": (st, [p, p, i64, i32, i32, i32, p, i64, i64, p, p, p, i32, p]),
-            "knn_graph_gather_select": (st, [p, i32, p, p, p, i32, i64, i32, i64, i64, p, p, p]),
+            "knn_graph_partition": (st, [p, p, i64, i32, i32, i32, p, i64, i64, p, p, i32, p]),
+            "knn_graph_gather_select": (st, [p, i32, p, p, i32, i64, i32, i64, i64, p, p, p]),
             "knn_last_select_kernel": (st, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
             "knn_merge": (st, [p, p, p, i32, i64, i32, p, p, p, p]),
             "knn_gemm_path": (ctypes.c_int, [p]),
@@ -127,6 +127,8 @@ def load_library():
                                       ctypes.POINTER(ctypes.c_int64)]),
         }
         for name, (res, args) in sig.items():
+            if "KNN_LIB_PATH" in os.environ and not hasattr(lib, name):
+                continue  # an older build under A/B test: only the symbols it has
             f = getattr(lib, name)
             f.restype, f.argtypes = res, args
         _lib = lib
@@ -345,20 +347,21 @@ def graph_pivots(X, k, row0, rows, thr, metric=L2SQ, stream=None):
     _check(rc, ctx)
 
 
-def graph_partition(X, k, thr, unit_lo, unit_hi, cnt, ckey, cidx, metric=L2SQ, stream=None):
-    """knn_graph_partition: candidates of the triangle units [unit_lo, unit_hi) into the lists."""
+def graph_partition(X, k, thr, unit_lo, unit_hi, cnt, cent, metric=L2SQ, stream=None):
+    """knn_graph_partition: candidates of the triangle units [unit_lo, unit_hi) into the lists
+    (cnt int32[N], cent int64[N, cap]: entries key << 32 | column)."""
     import torch
     N, d = X.shape
-    cap = ckey.shape[1]
+    cap = cent.shape[1]
     ctx = context(X.device.index)
     rc = load_library().knn_graph_partition(
         ctx, _dev_ptr(X, torch.float32, "X"), N, d, k, metric, _dev_ptr(thr, torch.float32, "thr"),
-        unit_lo, unit_hi, _dev_ptr(cnt, torch.int32, "cnt"), ctypes.c_void_p(ckey.data_ptr()),
-        ctypes.c_void_p(cidx.data_ptr()), cap, _stream(stream))
+        unit_lo, unit_hi, _dev_ptr(cnt, torch.int32, "cnt"), _dev_ptr(cent, torch.int64, "cent"), cap,
+        _stream(stream))
     _check(rc, ctx)
 
 
-def graph_gather_select(cnt_ptrs, key_ptrs, idx_ptrs, cap, N, k, row0, rows, device=None, stream=None):
+def graph_gather_select(cnt_ptrs, ent_ptrs, cap, N, k, row0, rows, device=None, stream=None):
     """knn_graph_gather_select over G list sources (device pointers, local or peer-mapped).
     Returns (idx rows×k, dist rows×k); raises KnnError(KNN_ERR_INTERNAL) on a failed
     certificate / overflow (the caller falls back)."""
@@ -368,9 +371,9 @@ def graph_gather_select(cnt_ptrs, key_ptrs, idx_ptrs, cap, N, k, row0, rows, dev
     ctx = context(dev.index)
     idx, dist = _outputs(rows, k, dev)
     P = ctypes.c_void_p * G
-    rc = load_library().knn_graph_gather_select(ctx, G, P(*cnt_ptrs), P(*key_ptrs), P(*idx_ptrs), cap, N, k,
-                                                row0, rows, ctypes.c_void_p(idx.data_ptr()),
-                                                ctypes.c_void_p(dist.data_ptr()), _stream(stream))
+    rc = load_library().knn_graph_gather_select(ctx, G, P(*cnt_ptrs), P(*ent_ptrs), cap, N, k, row0, rows,
+                                                ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                                _stream(stream))
     _check(rc, ctx)
     return idx, dist
 

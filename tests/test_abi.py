@@ -47,7 +47,7 @@ def test_binding_covers_the_header():
 
 def test_abi_version_and_no_device(lib):
     lib.knn_abi_version.restype = ctypes.c_int
-    assert lib.knn_abi_version() == 1
+    assert lib.knn_abi_version() == 2
     try:
         import torch
         if torch.cuda.is_available():

@@ -99,16 +99,15 @@ def test_emulated_ranks_equal_graph(G, k, metric):
     for g in range(G):
         ulo, uhi = units * g // G, units * (g + 1) // G
         cnt = torch.zeros(N, dtype=torch.int32, device="cuda")
-        ck = torch.empty((N, cap), dtype=torch.int32, device="cuda")
-        ci = torch.empty((N, cap), dtype=torch.int32, device="cuda")
-        kn.graph_partition(X, k, thr, ulo, uhi, cnt, ck, ci, metric=metric)
-        lists.append((cnt, ck, ci))
+        ce = torch.empty((N, cap), dtype=torch.int64, device="cuda")
+        kn.graph_partition(X, k, thr, ulo, uhi, cnt, ce, metric=metric)
+        lists.append((cnt, ce))
     torch.cuda.synchronize()
-    ptrs = [[l[j].data_ptr() for l in lists] for j in range(3)]
     parts_i, parts_d = [], []
     for g in range(G):
         lo, hi = g * per, min(N, (g + 1) * per)
-        i, dd = kn.graph_gather_select(ptrs[0], ptrs[1], ptrs[2], cap, N, k, lo, hi - lo)
+        i, dd = kn.graph_gather_select([l[0].data_ptr() for l in lists], [l[1].data_ptr() for l in lists], cap, N,
+                                       k, lo, hi - lo)
         parts_i.append(i)
         parts_d.append(dd)
     gi, gd = torch.cat(parts_i), torch.cat(parts_d)
