@@ -53,6 +53,21 @@ int main(int argc, char** argv) {
     /* the same graph through the host-buffer entry point (copies inside the call) */
     CHECK(knn_search_block_host(ctx, X, N, X, N, d, k, KNN_L2SQ, 0, 0, idx, dist, NULL));
     printf("host-buffer API, point 0 nearest: %d (%.4f)\n", idx[0], dist[0]);
+    /* the multi-GPU boundary from C: an NCCL communicator (one rank here; with one process
+       per GPU, rank 0 makes the id and the caller ships it to the others) and the sharded
+       k-NNG (the triangle split over the ranks; every rank gets the full graph) */
+    uint8_t uid[128];
+    if (knn_comm_unique_id(uid) == KNN_OK) {
+        CHECK(knn_comm_init(ctx, 0, 1, uid));
+        CHECK(knn_graph_sharded(ctx, KNN_SHARD_SYM, dX, N, d, k, KNN_L2SQ, dI, dD, NULL));
+        cudaMemcpy(idx, dI, (size_t)k * sizeof(int32_t), cudaMemcpyDeviceToHost);
+        int32_t backend = 0, rank = 0, nranks = 0;
+        knn_comm_info(ctx, &backend, &rank, &nranks);
+        printf("sharded (backend %d, %d rank): point 0 nearest: %d\n", backend, nranks, idx[0]);
+        CHECK(knn_comm_destroy(ctx));
+    } else {
+        printf("NCCL not loadable: sharded call skipped\n");
+    }
     cudaFree(dX);
     cudaFree(dI);
     cudaFree(dD);

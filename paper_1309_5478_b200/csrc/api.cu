@@ -420,6 +420,7 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
         if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
         if (ctx->ev_free[b]) cudaEventDestroy(ctx->ev_free[b]);
     }
+    for (auto e : ctx->ev_chunk) cudaEventDestroy(e);
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
     if (ctx->pv_flag) cudaFree(ctx->pv_flag);
     comm_release(ctx);
@@ -505,6 +506,180 @@ knn_status knn_search(knn_ctx_t ctx, const float* Q, int64_t M, const float* X, 
                             stream);
 }
 
+namespace {
+// Page-locks a host range for the duration of a call unless it is already pinned.
+struct HostPin {
+    void* p = nullptr;
+    bool mine = false;
+    void pin(const void* ptr, size_t bytes) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost) return;
+        cudaGetLastError();
+        const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault);
+        if (e == cudaSuccess) {
+            p = const_cast<void*>(ptr);
+            mine = true;
+        } else {
+            cudaGetLastError();  // stays pageable: copies are correct, just not overlapped
+        }
+    }
+    ~HostPin() {
+        if (mine) cudaHostUnregister(p);
+    }
+};
+}  // namespace
+
+// End-to-end k-NNG from HOST points with the host->device copy overlapped by the hot path
+// ("overlap computation with data transfer").  The pivot
+// plan over the symmetric GEMM, reorganised by arrival: the copy stream sends a sample of
+// every 8th point (one strided 2-D copy) and then the points in chunks; the compute stream
+// prepares the sample, and per chunk: its rows' split operands, their sample pass and
+// pivots, and the partition of the triangle's units whose column block lies in the chunk
+// (column-major unit order: those units only touch rows and columns that have arrived).
+// After the last chunk: the candidate select and the device->host copy of the lists.
+// Results are those of the device-resident call: the pivots (sample) differ, but every
+// plan's result is the exact select of the same per-pair values (certificates redo).
+// Returns KNN_ERR_UNSUPPORTED (nothing queued) when the shape does not fit the scheme.
+knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, int32_t d, int32_t k,
+                                int32_t metric, int32_t* out_idx_host, float* out_dist_host, cudaStream_t s) {
+    const char* env = getenv("KNN_HOST_PIPE");
+    const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
+    if ((env && strcmp(env, "0") == 0) || !tc || !ctx->pivot_ok || !ctx->sym_ok ||
+        ctx->plan == KNN_PLAN_MATERIALISED || ctx->pivot1 || k > 32 || N < 16384 || N % 2048 != 0 ||
+        ctx->pivot_div != 8)
+        return KNN_ERR_UNSUPPORTED;
+    const int64_t S = N / 8;                    // sample: points 8j, j < S (a multiple of 256)
+    const int64_t CH = N / 8 >= 8192 ? N / 8 : 8192;  // chunk rows (a multiple of 256)
+    const int nch = (int)ceil_div(N, CH);
+    const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
+    const int32_t cap = ctx->pivot_cap;
+    const int32_t kk = k + 1;  // the sample may hold the row's own point
+    if (S / 32 < kk + 1) return KNN_ERR_UNSUPPORTED;
+    // device buffers: io = points | sample staging | outputs; ws = operands, sample, lists
+    float *x, *xs, *od;
+    int32_t* oi;
+    auto io_layout = [&](Carve& c) {
+        x = c.take<float>((size_t)N * d);
+        xs = c.take<float>((size_t)S * d);
+        oi = c.take<int32_t>((size_t)N * k);
+        od = c.take<float>((size_t)N * k);
+    };
+    Prepared px{}, smp{};
+    float *D, *smax, *thr;
+    int32_t *flag, *cnt;
+    uint64_t* cent;
+    auto ws_layout = [&](Carve& c) {
+        flag = c.take<int32_t>(4);
+        px.sqn = c.take<float>(N);
+        px.rs = c.take<float>(N);
+        px.hi = c.take<__half>((size_t)N * d_pad);
+        px.lo = c.take<__half>((size_t)N * d_pad);
+        smp.sqn = c.take<float>(S);
+        smp.rs = c.take<float>(S);
+        smp.hi = c.take<__half>((size_t)S * d_pad);
+        smp.lo = c.take<__half>((size_t)S * d_pad);
+        smax = c.take<float>(1);
+        D = c.take<float>((size_t)(S / 32) * CH);
+        thr = c.take<float>(N);
+        cnt = c.take<int32_t>(N);
+        cent = c.take<uint64_t>((size_t)N * cap);
+    };
+    Carve p1{nullptr}, p2{nullptr};
+    io_layout(p1);
+    ws_layout(p2);
+    KNN_TRY(ensure(ctx, &ctx->io, &ctx->io_size, p1.off + 256));
+    KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, p2.off + 256));
+    Carve c1{static_cast<char*>(ctx->io)}, c2{static_cast<char*>(ctx->ws)};
+    io_layout(c1);
+    ws_layout(c2);
+    if (!ctx->copy_stream) {
+        KNN_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            KNN_CUDA(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+            KNN_CUDA(cudaEventCreateWithFlags(&ctx->ev_free[b], cudaEventDisableTiming));
+        }
+    }
+    while ((int)ctx->ev_chunk.size() < nch + 2) {
+        cudaEvent_t e = nullptr;
+        KNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ev_chunk.push_back(e);
+    }
+    cudaStream_t cs = ctx->copy_stream;
+    HostPin pin;
+    pin.pin(X_host, (size_t)N * d * sizeof(float));
+    // the copies overwrite x / xs only after the work queued before this call on s
+    KNN_CUDA(cudaEventRecord(ctx->ev_chunk[nch + 1], s));
+    KNN_CUDA(cudaStreamWaitEvent(cs, ctx->ev_chunk[nch + 1], 0));
+    KNN_CUDA(cudaMemcpy2DAsync(xs, (size_t)d * sizeof(float), X_host, (size_t)8 * d * sizeof(float),
+                               (size_t)d * sizeof(float), (size_t)S, cudaMemcpyHostToDevice, cs));
+    KNN_CUDA(cudaEventRecord(ctx->ev_chunk[nch], cs));
+    for (int c = 0; c < nch; ++c) {
+        const int64_t c0 = c * CH, R = N - c0 < CH ? N - c0 : CH;
+        KNN_CUDA(cudaMemcpyAsync(x + c0 * d, X_host + c0 * d, (size_t)R * d * sizeof(float), cudaMemcpyHostToDevice,
+                                 cs));
+        KNN_CUDA(cudaEventRecord(ctx->ev_chunk[c], cs));
+    }
+    struct CopyGuard {  // errors below: the copies drain before the pin is released
+        cudaStream_t cs;
+        ~CopyGuard() { cudaStreamSynchronize(cs); }
+    } cg{cs};
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_chunk[nch], 0));
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(xs, S, d, d_pad, smp.sqn, smp.rs, smp.hi, smp.lo, flag, metric, s));
+        t.done();
+    }
+    KNN_CUDA(knn::launch_max_nonneg(smp.sqn, S, smax, s));
+    ctx->launches++;
+    knn::TcOperands full{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+    for (int c = 0; c < nch; ++c) {
+        const int64_t c0 = c * CH, R = N - c0 < CH ? N - c0 : CH;
+        KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_chunk[c], 0));
+        {
+            Timed t(ctx, KNN_KERNEL_PREP, s);
+            KNN_CUDA(knn::launch_prep(x + c0 * d, R, d, d_pad, px.sqn + c0, px.rs + c0, px.hi + c0 * d_pad,
+                                      px.lo + c0 * d_pad, flag, metric, s));
+            t.done();
+        }
+        knn::TcOperands op{px.hi + c0 * d_pad, px.lo + c0 * d_pad, px.sqn + c0, px.rs + c0, R,
+                           smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
+        {
+            Timed tg(ctx, KNN_KERNEL_GEMM, s);
+            KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s,
+                                              smax));
+            tg.done();
+        }
+        {
+            Timed tp(ctx, KNN_KERNEL_SELECT, s);
+            KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, R, R, kk, metric, thr + c0, cnt + c0, s));
+            tp.done();
+        }
+        // the triangle's units whose column block lies in this chunk (rows and columns < c0 + R)
+        const int64_t b0 = c0 / knn::kColPad, b1 = (c0 + R) / knn::kColPad;  // 256-column blocks
+        Timed tf(ctx, KNN_KERNEL_FUSED, s);
+        KNN_CUDA(knn::launch_dist_tc_pivot(full, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
+                                           b0 * (b0 + 1) / 2, b1 * (b1 + 1) / 2, true));
+        tf.done();
+    }
+    {
+        Timed tc2(ctx, KNN_KERNEL_MERGE, s);
+        KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, N, k, 0, oi, od, flag, s));
+        tc2.done();
+    }
+    ctx->last_plan = 3;
+    knn_status st = finish_blocking(ctx, s);
+    if (st == KNN_ERR_INTERNAL) {  // a certificate failed / a list overflowed: the full matrix
+        ctx->pivot_redos++;
+        KNN_TRY(run_block(ctx, x, N, x, N, d, k, metric, 0, 0, oi, od, s, false));
+        st = finish_blocking(ctx, s);
+    }
+    if (st != KNN_OK) return st;
+    KNN_CUDA(cudaMemcpyAsync(out_idx_host, oi, (size_t)N * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)N * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+    return finish_blocking(ctx, s);
+}
+
 knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
                                  const float* X_host, int64_t N, int32_t d, int32_t k,
                                  int32_t metric, int64_t self_shift, int64_t idx_offset,
@@ -516,6 +691,10 @@ knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool same = Q_host == X_host && M == N;
+    if (same && self_shift == 0 && idx_offset == 0) {
+        const knn_status sp = host_graph_pipelined(ctx, X_host, N, d, k, metric, out_idx_host, out_dist_host, s);
+        if (sp != KNN_ERR_UNSUPPORTED) return sp;
+    }
     auto layout = [&](Carve& c, float*& q, float*& x, int32_t*& oi, float*& od) {
         x = c.take<float>((size_t)N * d);
         q = same ? x : c.take<float>((size_t)M * d);
@@ -549,28 +728,6 @@ knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
     return finish_blocking(ctx, s);
 }
 
-namespace {
-// Page-locks a host range for the duration of a call unless it is already pinned.
-struct HostPin {
-    void* p = nullptr;
-    bool mine = false;
-    void pin(const void* ptr, size_t bytes) {
-        cudaPointerAttributes a{};
-        if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost) return;
-        cudaGetLastError();
-        const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault);
-        if (e == cudaSuccess) {
-            p = const_cast<void*>(ptr);
-            mine = true;
-        } else {
-            cudaGetLastError();  // stays pageable: copies are correct, just not overlapped
-        }
-    }
-    ~HostPin() {
-        if (mine) cudaHostUnregister(p);
-    }
-};
-}  // namespace
 
 knn_status knn_search_streamed(knn_ctx_t ctx, const float* Q_host, int64_t M, const float* X_host,
                                int64_t N, int32_t d, int32_t k, int32_t metric, int32_t graph,

@@ -280,6 +280,9 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
                     const int slot = it % NCOL;
                     mbar_wait(colempty0 + 8 * slot, ((it / NCOL) & 1) ^ 1);
+                    // the epilogue's generic-proxy reads of this slot (ordered by the
+                    // mbarrier) before the async-proxy writes of the refill
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     const uint32_t fb = colfull0 + 8 * slot;
                     const uint32_t dst = smem_u32(col_base + slot * 3 * BN);
                     mbar_expect_tx(fb, NCOLARR * BN * 4);
@@ -897,7 +900,7 @@ template <int MODE>
 cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                               const float* thr, int32_t* cnt, uint64_t* cent,
                               int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                              int64_t unit_lo, int64_t unit_hi, float margin) {
+                              int64_t unit_lo, int64_t unit_hi, float margin, bool col_major = false) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     if (sym && op.M != op.N) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
@@ -913,7 +916,7 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
     cudaError_t e;
     if (sym) {
         SymSched sched{ceil_div(op.N, BN)};
-        sched.gm = sym_group_rows(op.N, op.d_pad);
+        sched.gm = col_major ? -1 : sym_group_rows(op.N, op.d_pad);
         const int64_t all = sched.n * (sched.n + 1) / 2;
         sched.u_lo = unit_lo < 0 ? 0 : unit_lo;
         sched.u_hi = unit_hi < 0 || unit_hi > all ? all : unit_hi;
@@ -943,9 +946,9 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                                 int64_t unit_lo, int64_t unit_hi) {
+                                 int64_t unit_lo, int64_t unit_hi, bool col_major) {
     return launch_pivot_impl<MODE_PIVOT>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag, num_sms,
-                                         s, unit_lo, unit_hi, 0.0f);
+                                         s, unit_lo, unit_hi, 0.0f, col_major);
 }
 
 float pivot1_margin(int32_t d_pad) {

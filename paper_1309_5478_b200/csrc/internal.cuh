@@ -47,6 +47,9 @@ cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float
                                  int64_t N, int64_t S, int32_t d_pad, __half* shi, __half* slo, float* ssqn,
                                  float* srs, float* smax, cudaStream_t s);
 
+// *out = max(0, v[0..n)) (the sample pass's XMAX for a sample prepared in place).
+cudaError_t launch_max_nonneg(const float* v, int64_t n, float* out, cudaStream_t s);
+
 // gemm_simt.cu: FP32 FFMA distance GEMM with the fused epilogue.
 cudaError_t launch_dist_simt(const float* Q, const float* qn, int64_t M, const float* X,
                              const float* xn, int64_t N, int32_t d, int32_t metric,
@@ -69,10 +72,12 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 // (the ukey of the distance: order-preserving bits); SYM also records the transposed
 // element for the column's row.  flag |= 2 on candidate overflow.
 // unit_lo / unit_hi (sym only): the triangle's units [unit_lo, unit_hi); -1 = all.
+// col_major (sym only): units in column-major order (the units of column blocks [0, J) are
+// [0, J (J + 1) / 2)): the host-pipelined k-NNG partitions the triangle as chunks arrive.
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                                 int64_t unit_lo = -1, int64_t unit_hi = -1);
+                                 int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false);
 // The same partition from the single hi.hi product (L2 metrics): kept iff the lower bound
 // L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); the key is L.
 // F = pivot1_margin(d_pad) bounds |u_hh - D| / (||q||^2 + ||x||^2) for the exact D.

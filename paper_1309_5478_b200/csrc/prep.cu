@@ -197,6 +197,27 @@ cudaError_t launch_gather_sample(const __half* hi, const __half* lo, const float
 }
 
 namespace {
+__global__ void max_nonneg_kernel(const float* __restrict__ v, int64_t n, float* __restrict__ out) {
+    float m = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, v[i]);
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(m));  // >= 0: int order
+}
+}  // namespace
+
+// *out = max(0, v[0..n)) (the sample pass's bound of the columns' sqn terms for a sample
+// that was prepared in place rather than gathered)
+cudaError_t launch_max_nonneg(const float* v, int64_t n, float* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), s);
+    if (e != cudaSuccess || n == 0) return e;
+    const int64_t blocks = ceil_div(n, (int64_t)256);
+    max_nonneg_kernel<<<(unsigned)(blocks < 592 ? blocks : 592), 256, 0, s>>>(v, n, out);
+    return cudaGetLastError();
+}
+
+namespace {
 __global__ void scale_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n, float f) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i] * f;

@@ -67,8 +67,10 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+// (barrier.sync without .aligned: a warp may arrive from divergent code, e.g. after one
+// lane ran a producer loop — compute-sanitizer synccheck flagged bar.sync there)
 __device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 // Named-barrier OR-reduction over `n` threads: true iff any participant passed true.
 __device__ __forceinline__ bool named_bar_or(int id, int n, bool pred) {
@@ -76,7 +78,7 @@ __device__ __forceinline__ bool named_bar_or(int id, int n, bool pred) {
     asm volatile(
         "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.u32 p, %3, 0;\n\t"
-        "bar.red.or.pred q, %1, %2, p;\n\t"
+        "barrier.red.or.pred q, %1, %2, p;\n\t"
         "selp.u32 %0, 1, 0, q;\n\t}"
         : "=r"(r) : "r"(id), "r"(n), "r"((uint32_t)pred) : "memory");
     return r != 0;

@@ -49,6 +49,7 @@ struct knn_ctx {
     size_t st_size = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_chunk;  // the host-pipelined k-NNG's chunk arrivals
     double last_stream_copy_ms = 0, last_stream_total_ms = 0;
     // knn_graph_pivots leaves the prepared operands of X at the start of ws (after the flag);
     // knn_graph_partition on the same (X, N, d, metric) reuses them while ws is untouched

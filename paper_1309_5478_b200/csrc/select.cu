@@ -1147,9 +1147,18 @@ select_cluster_kernel(const float* __restrict__ D, int64_t N, int64_t ldD, int k
 // bulk async copies (TMA engine) that lane 0 keeps WS stages ahead, across row
 // boundaries, so one row's rebuild/sort tail overlaps the other warps' streaming.
 constexpr int WSEL_K = 128;      // largest k of the warp path
-constexpr int WSEL_C = 1024;     // floats per ring stage (4 KB)
-constexpr int WSEL_S = 3;        // ring stages per warp
-constexpr int WSEL_WARPS = 4;    // warps (rows in flight) per CTA
+#ifndef KNN_WSEL_C
+#define KNN_WSEL_C 1024
+#endif
+#ifndef KNN_WSEL_S
+#define KNN_WSEL_S 3
+#endif
+#ifndef KNN_WSEL_WARPS
+#define KNN_WSEL_WARPS 4
+#endif
+constexpr int WSEL_C = KNN_WSEL_C;        // floats per ring stage (4 KB)
+constexpr int WSEL_S = KNN_WSEL_S;        // ring stages per warp
+constexpr int WSEL_WARPS = KNN_WSEL_WARPS;  // warps (rows in flight) per CTA
 constexpr int WSEL_SUB = 256;    // elements appended between buffer checks
 
 __host__ __device__ constexpr int64_t wsel_slab_bytes(int cap) {
@@ -1165,6 +1174,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // lane), 32 at a time.  Out of line to keep the streaming loop small in the I-cache.
 __device__ __noinline__ uint64_t warp_fold32(uint64_t L, const uint32_t* ckey, const uint32_t* cidx,
                                              int count) {
+    __syncwarp();  // the lanes' appends are visible to every lane (racecheck)
     for (int o = 0; o < count; o += 32)
         L = ws::warp_merge32<1>(L, ckey + o, cidx + o, count - o < 32 ? count - o : 32);
     __syncwarp();
@@ -1175,6 +1185,7 @@ __device__ __noinline__ uint64_t warp_fold32(uint64_t L, const uint32_t* ckey, c
 // k-th best key (the new strict threshold).  Out of line: it runs a few times per row.
 __device__ __noinline__ uint32_t warp_rebuild(uint32_t* ckey, uint32_t* cidx, int count, int k,
                                               uint32_t* kkey, uint32_t* kidx, uint32_t* hist) {
+    __syncwarp();  // the lanes' appends are visible to every lane
     const int lane = threadIdx.x & 31;
     const uint32_t t = ws::warp_select_k<1>(ckey, cidx, count, k, kkey, kidx, hist);
     for (int i = lane; i < k; i += 32) {
@@ -1503,6 +1514,7 @@ __global__ void __launch_bounds__(32 * PV_ROWS, 2)
 pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M, int64_t pad_end, int k,
                        int metric, float* __restrict__ thr, int32_t* __restrict__ cnt) {
     __shared__ uint32_t tile[PV_SLAB][PV_ROWS + 1];
+    __shared__ uint32_t phist[PV_ROWS][32], pbuf[PV_ROWS][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // warp w owns row r0 + w
     const int64_t r0 = (int64_t)blockIdx.x * PV_ROWS;
     if (threadIdx.x < PV_ROWS) {  // zero padding of thr (read as whole tiles by the SYM partition)
@@ -1533,9 +1545,60 @@ pivot_from_mins_kernel(const float* __restrict__ mins, int64_t nchunk, int64_t M
         for (int i = 0; i < PV_PER; ++i) b[i] = tile[lane + 32 * i][w];
         pv_fold(a, b, s0 == 0);
     }
-    // pop the k smallest off the lane heads (equal heads pop together)
+    // k-th smallest of the 32 lanes' kept minima.  Common case: 32 value-linear buckets over
+    // [min, max] of the keys; the bucket b* holding the k-th and the keys in it (usually a
+    // handful) are sorted by one warp — ~4x fewer instructions than popping k heads.
     uint32_t T = 0;
-    for (int c = 0; c < k;) {
+    bool got = false;
+    {
+        uint32_t kmx = 0;
+        #pragma unroll
+        for (int i = 0; i < PV_PER; ++i)
+            if (a[i] != 0xFFFFFFFFu) kmx = max(kmx, a[i]);
+        const uint32_t gmn = __reduce_min_sync(FULL, a[0]);
+        const uint32_t gmx = __reduce_max_sync(FULL, kmx);
+        const float fmn = ukey_to_float(gmn), fmx = ukey_to_float(gmx);
+        const float scale = 32.0f / (fmx - fmn);
+        if (gmn != 0xFFFFFFFFu && fmn >= 0.0f && fmx > fmn && isfinite(fmx) && isfinite(scale)) {
+            phist[w][lane] = 0;
+            __syncwarp();
+            auto bucket = [&](uint32_t u) -> uint32_t {
+                return min((uint32_t)((ukey_to_float(u) - fmn) * scale), 31u);
+            };
+            #pragma unroll
+            for (int i = 0; i < PV_PER; ++i)
+                if (a[i] != 0xFFFFFFFFu) atomicAdd(&phist[w][bucket(a[i])], 1u);
+            __syncwarp();
+            const uint32_t c = phist[w][lane];
+            uint32_t incl = c;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t hit = __ballot_sync(FULL, incl >= (uint32_t)k);
+            if (hit) {  // (else fewer than k finite keys: the pop path below)
+                const int bs = __ffs(hit) - 1;
+                const uint32_t before = __shfl_sync(FULL, incl - c, bs), nstar = __shfl_sync(FULL, c, bs);
+                if (nstar <= 32) {
+                    int base = 0;
+                    #pragma unroll
+                    for (int i = 0; i < PV_PER; ++i) {
+                        const bool p2 = a[i] != 0xFFFFFFFFu && bucket(a[i]) == (uint32_t)bs;
+                        const uint32_t bm = __ballot_sync(FULL, p2);
+                        if (p2) pbuf[w][base + __popc(bm & ws::lanemask_lt())] = a[i];
+                        base += __popc(bm);
+                    }
+                    __syncwarp();
+                    const uint32_t v = warp_sort32(lane < base ? pbuf[w][lane] : 0xFFFFFFFFu);
+                    T = __shfl_sync(FULL, v, k - 1 - (int)before);
+                    got = true;
+                }
+            }
+        }
+    }
+    // pop the k smallest off the lane heads (equal heads pop together)
+    for (int c = 0; c < k && !got;) {
         const uint32_t mn = __reduce_min_sync(FULL, a[0]);
         const bool mine = a[0] == mn;
         c += __popc(__ballot_sync(FULL, mine));
@@ -1585,7 +1648,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                         int64_t idx_offset, int32_t* __restrict__ out_idx,
                         float* __restrict__ out_dist, int32_t* __restrict__ flag) {
     __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
-    __shared__ uint32_t hist[8][256], skey[8][32], sidx[8][32];
+    __shared__ uint32_t hist[8][256], skey[8][64], sidx[8][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t row = (int64_t)blockIdx.x * 8 + w;
     if (row >= M) return;
@@ -1607,6 +1670,72 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
             uint32_t uk[CS_PER], v[CS_PER];  // this lane's keys (list order), sorted copy
             #pragma unroll
             for (int i = 0; i < CS_PER; ++i) uk[i] = lane + 32 * i < n ? __ldg(rk + 2 * (lane + 32 * i)) : 0xFFFFFFFFu;
+            // Bucket select (the common case): 32 value-linear buckets over [min, max] of the
+            // keys (the candidates of a row are spread over [0, pivot]); the bucket b* holding
+            // the k-th key and every bucket below it hold every key of the k nearest, ties at
+            // the k-th included (the bucket map is monotone in the value).  When those are at
+            // most 64 they are compacted and sorted once (64-wide bitonic); crowded buckets
+            // take the exact path below.  ~4x fewer instructions than sorting and popping.
+            {
+                uint32_t kmn = 0xFFFFFFFFu, kmx = 0;
+                #pragma unroll
+                for (int i = 0; i < CS_PER; ++i)
+                    if (lane + 32 * i < n) {
+                        kmn = min(kmn, uk[i]);
+                        kmx = max(kmx, uk[i]);
+                    }
+                kmn = __reduce_min_sync(FULL, kmn);
+                kmx = __reduce_max_sync(FULL, kmx);
+                const float fmn = ukey_to_float(kmn), fmx = ukey_to_float(kmx);
+                const float scale = 32.0f / (fmx - fmn);
+                if (fmn >= 0.0f && fmx > fmn && isfinite(fmx) && isfinite(scale)) {
+                    hist[w][lane] = 0;
+                    __syncwarp();
+                    auto bucket = [&](uint32_t u) -> uint32_t {
+                        return min((uint32_t)((ukey_to_float(u) - fmn) * scale), 31u);
+                    };
+                    #pragma unroll
+                    for (int i = 0; i < CS_PER; ++i)
+                        if (lane + 32 * i < n) atomicAdd(&hist[w][bucket(uk[i])], 1u);
+                    __syncwarp();
+                    const uint32_t c = hist[w][lane];
+                    uint32_t incl = c;
+                    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int bs = __ffs(__ballot_sync(FULL, incl >= (uint32_t)k)) - 1;  // b*
+                    const uint32_t upto = __shfl_sync(FULL, incl, bs);  // keys in buckets <= b*
+                    if (upto <= 64) {
+                        int base = 0;
+                        #pragma unroll
+                        for (int i = 0; i < CS_PER; ++i) {
+                            const bool p2 = lane + 32 * i < n && bucket(uk[i]) <= (uint32_t)bs;
+                            const uint32_t bm = __ballot_sync(FULL, p2);
+                            if (p2) {
+                                const int pos = base + __popc(bm & ws::lanemask_lt());
+                                skey[w][pos] = uk[i];
+                                sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
+                            }
+                            base += __popc(bm);
+                        }
+                        __syncwarp();
+                        uint64_t b2[2];
+                        #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int e = h * 32 + lane;
+                            b2[h] = e < base ? ((uint64_t)skey[w][e] << 32 | sidx[w][e]) : ~0ull;
+                        }
+                        ws::warp_bitonic<2>(b2);
+                        if (lane < k) {
+                            out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)b2[0] + idx_offset);
+                            out_dist[row * k + lane] = ukey_to_float((uint32_t)(b2[0] >> 32));
+                        }
+                        return;
+                    }
+                }
+            }
             #pragma unroll
             for (int i = 0; i < CS_PER; ++i) v[i] = uk[i];
             sort16(v);

@@ -221,7 +221,9 @@ struct SymSched {
     int64_t n;  // pair blocks per side
     // units [u_lo, u_hi) of the triangle only (the multi-GPU symmetric k-NNG splits it)
     int64_t u_lo = 0, u_hi = INT64_MAX;
-    int64_t gm = 0;  // rows per group (0: row-major)
+    int64_t gm = 0;  // rows per group (0: row-major; -1: COLUMN-major, unit u of column j =
+                     // row block u - j(j+1)/2: the units of columns [0, J) are a prefix, so a
+                     // caller can partition the triangle as the columns' points arrive)
     __device__ __forceinline__ int64_t units() const { return n * (n + 1) / 2; }
     __device__ __forceinline__ int64_t end() const { return u_hi < units() ? u_hi : units(); }
     // row m of the triangle starts at unit s(m) = m*n - m(m-1)/2: the largest m with
@@ -249,6 +251,12 @@ struct SymSched {
     __device__ __forceinline__ Cur first(int64_t t) const {
         t += u_lo;
         if (t >= end()) return {t, n, 0, 0};
+        if (gm < 0) {  // column j: the largest j with j (j + 1) / 2 <= t
+            int64_t j = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while (j > 0 && j * (j + 1) / 2 > t) --j;
+            while ((j + 1) * (j + 2) / 2 <= t) ++j;
+            return {t, j, t - j * (j + 1) / 2, 0};
+        }
         if (gm > 0) {
             int64_t g = 0, o = t, sz = gsize(0);
             while (o >= sz) {
@@ -264,6 +272,13 @@ struct SymSched {
     __device__ __forceinline__ void next(Cur& c, int64_t step) const {
         c.t += step;
         c.o += step;
+        if (gm < 0) {
+            while (c.t < end() && c.o > c.m) {
+                c.o -= c.m + 1;
+                ++c.m;
+            }
+            return;
+        }
         if (gm > 0) {
             while (c.t < end() && c.o >= c.sz) {
                 c.o -= c.sz;
@@ -277,6 +292,7 @@ struct SymSched {
         }
     }
     __device__ __forceinline__ Unit unit(const Cur& c) const {
+        if (gm < 0) return {c.o, c.m, c.m + 1};  // (row block o, column block m), o <= m
         if (gm > 0) {
             const int64_t m0 = c.m * gm, gr = (n - m0) < gm ? (n - m0) : gm;
             const int64_t tri = gr * (gr - 1) / 2;

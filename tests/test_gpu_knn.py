@@ -234,6 +234,20 @@ def test_host_entry_point_equals_device():
     assert np.array_equal(hi, ref_i) and np.array_equal(hd, ref_d)
 
 
+@pytest.mark.parametrize("N,d,k,metric,dist", [(16384, 48, 16, 0, "uniform"), (32768, 100, 32, 1, "clusters"),
+                                                (18432, 64, 8, 2, "gauss"), (20000, 32, 16, 0, "uniform")])
+def test_host_pipelined_graph_equals_device(N, d, k, metric, dist):
+    # knn_search_block_host's k-NNG overlaps the host->device copy with the hot path (chunks
+    # of points, sample of every 8th point, column-major partition launches) when N is a
+    # multiple of 2048 (20000 is not: the plain path); the lists equal the device call's
+    X = datagen.points(N, d, dist, seed=N + d)
+    ref_i, ref_d = run_graph(X, k, metric)
+    pinned_x = torch.from_numpy(X).pin_memory().numpy()
+    hi, hd = knn().search_block_host(pinned_x, pinned_x, k, metric=metric, self_shift=0)
+    assert knn().last_plan() == 3
+    assert np.array_equal(hi, ref_i) and np.array_equal(hd.view(np.uint32), ref_d.view(np.uint32))
+
+
 def test_deterministic_and_small_row_blocks(monkeypatch):
     X = datagen.points(4000, 64, "uniform", seed=10)
     a = run_graph(X, 16)
@@ -559,6 +573,8 @@ def test_c_example_runs(tmp_path):
                          env=dict(os.environ, LD_LIBRARY_PATH=libdir + ":" + os.environ.get("LD_LIBRARY_PATH", "")))
     assert out.returncode == 0, out.stderr
     assert "point 0:" in out.stdout and "host-buffer API" in out.stdout
+    # the sharded k-NNG through a one-rank NCCL communicator, from C (NCCL dlopen'ed)
+    assert "sharded (backend 1, 1 rank)" in out.stdout, out.stdout
 
 
 # ------------------------- single-product partition + re-evaluation (opt-in, KNN_PIVOT1) ---
