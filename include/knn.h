@@ -161,7 +161,9 @@ knn_status knn_select(knn_ctx_t ctx, const float* D, int64_t M, int64_t N, int64
  * *kind = 0 warp per row (k <= 128, many rows), 1 CTA per row (persistent ring), 2 CTA per
  * row on unaligned rows, 3 a thread-block cluster per row (few rows: one
  * block per query cannot fill the GPU below ~#SM rows; NEXT-3), with *splits = the
- * cluster size (row segments merged over distributed shared memory), else 1. */
+ * cluster size (row segments merged over distributed shared memory), else 1; 4 two-pass
+ * warp per row (k <= 32, 1024 <= N <= 131072: pivot = the k-th smallest group minimum,
+ * PAPER.md:56). */
 knn_status knn_last_select_kernel(int32_t* kind, int32_t* splits);
 
 /* ABLATION, not the product path: the paper's quick multi-select as written

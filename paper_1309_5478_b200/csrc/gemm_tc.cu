@@ -546,14 +546,19 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         continue;
                     }
                     if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
-                    // stage the chunk's values (swizzled, conflict-free) so that each lane can
-                    // walk its own survivors with dynamic indices
+                    // stage the chunk's values (swizzled) so that each lane can walk its own
+                    // survivors with dynamic indices.  Only lanes with survivors store (a lane
+                    // reads back only its own row): ~5 of 32 lanes, so each store is about one
+                    // shared-memory wavefront instead of four — the tensor core's operand reads
+                    // already take most of the shared-memory bandwidth.
                     float* svp = reinterpret_cast<float*>(slab);
                     const uint32_t sv = smem_u32(svp);
-                    #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
-                               v[4 * u + 2], v[4 * u + 3]);
+                    if (hm) {
+                        #pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
+                                   v[4 * u + 2], v[4 * u + 3]);
+                    }
                     if (ep.dbg & 16) {  // DIAGNOSTIC: staging only
                         __syncwarp();
                         continue;

@@ -1369,6 +1369,262 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
     }
 }
 
+// ------------------------------------------------------------------ two-pass warp select --
+// k <= 32, 32k <= N <= WS2_MAXN (materialised rows, warp per row).  The running-threshold
+// select above admits ~k ln(N/1024) survivors per row (the threshold only tightens as the
+// row streams by), and each survivor costs a ballot-compaction append and a share of a
+// 32-wide bitonic fold: ~80 warp-instructions per survivor, most of the kernel's issue at
+// N = 65536 and nearly all of it for short rows (ncu: 5.8 k warp-instructions per
+// 4096-long row, 21.7 k per 65536-long row; latency-bound at 12 warps per SM).
+// Here the paper's quick multi-select (partition around a pivot, keep the side
+// holding the K-th) takes its pivot from the row itself, in two passes:
+//   pass 1 (streamed from HBM through the warp's bulk-copy ring): every lane reduces its 32
+//          elements of each 1024-element chunk to their minimum — a group minimum G_g, the
+//          key of an actual element of group g — stores it, and keeps its 4 smallest;
+//   pivot:  P = the k-th smallest group minimum (k pops off the 32 lanes' sorted heads;
+//          a lane that runs out of heads only makes P larger).  At least k elements (one per
+//          popped group) have key <= P, so every element of the row's true k nearest (ties
+//          included) has key <= P: the partition is exact, no certificate needed;
+//   pass 2: only the groups with G_g <= P (~k of N/32) are re-read — 8 float4 each, from
+//          L2 — their elements with key <= P are compacted (warp scan + per-lane re-reads by
+//          dynamic index, L1) and folded into the sorted best-32 register list.
+// ~2.5 k warp-instructions per 65536-long row, ~1 k per 4096-long row.
+constexpr int WS2_MAXN = 131072;
+constexpr int WS2_CAP = 256;    // candidate buffer entries per warp
+constexpr int WS2_MAXS = 16;    // ring stages per warp (runtime S <= this)
+// slab: ring | S full barriers | 16-bit group minima [nchunk][32] | group list | cand key, idx
+__host__ __device__ constexpr int64_t ws2_slab_bytes(int64_t N, int S) {
+    return round_up((int64_t)S * WSEL_C * 4 + S * 8 + ceil_div(N, WSEL_C) * 32 * 2 + WS2_CAP * 4 +
+                        2 * WS2_CAP * 4,
+                    128);
+}
+
+// Fold `count` buffered candidates into the sorted best-32 list L (warp_fold32, inlined).
+__device__ __forceinline__ uint64_t ws2_fold(uint64_t L, const uint32_t* ckey, const uint32_t* cidx, int count) {
+    __syncwarp();  // the lanes' appends are visible to every lane
+    for (int o = 0; o < count; o += 32)
+        L = ws::warp_merge32<1>(L, ckey + o, cidx + o, count - o < 32 ? count - o : 32);
+    __syncwarp();
+    return L;
+}
+
+// Bitonic sort of 64 keys, 2 per lane (element e = r * 32 + lane), ascending.
+__device__ __forceinline__ void warp_bitonic64_u32(uint32_t (&v)[2]) {
+    const int lane = threadIdx.x & 31;
+    #pragma unroll
+    for (int size = 2; size <= 64; size <<= 1) {
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride == 32) {
+                const bool asc = (lane & size) == 0;  // e & 64 == 0 for both halves
+                const uint32_t lo = min(v[0], v[1]), hi = max(v[0], v[1]);
+                v[0] = asc ? lo : hi;
+                v[1] = asc ? hi : lo;
+            } else {
+                #pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int e = r * 32 + lane;
+                    const uint32_t o = __shfl_xor_sync(FULL, v[r], stride);
+                    const bool asc = (e & size) == 0;
+                    const bool lower = (lane & stride) == 0;
+                    v[r] = (lower == asc) ? min(o, v[r]) : max(o, v[r]);
+                }
+            }
+        }
+    }
+}
+
+// One warp per CTA (occupancy in whole warps), S ring stages of WSEL_C floats per warp.
+__global__ void __launch_bounds__(32)
+select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int S,
+                     int64_t idx_offset, int32_t* __restrict__ out_idx, float* __restrict__ out_dist) {
+    constexpr int VPT = WSEL_C / 128;  // float4 per lane per chunk (8)
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunk = ceil_div(N, WSEL_C);
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * WSEL_C);
+    uint16_t* gmin = reinterpret_cast<uint16_t*>(bars + S);
+    uint32_t* glist = reinterpret_cast<uint32_t*>(smem_raw + round_up((int64_t)S * WSEL_C * 4 + S * 8 + nchunk * 64, 16));
+    uint32_t* ckey = glist + WS2_CAP;
+    uint32_t* cidx = ckey + WS2_CAP;
+    const uint32_t full0 = smem_u32(bars);
+    const uint32_t ring0 = smem_u32(ring);
+
+    const int64_t gw = blockIdx.x;
+    const int64_t nw = gridDim.x;
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(full0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // producer state (lane 0): the next chunk, prefetching across row boundaries
+    int64_t prow = gw, pc = 0;
+    const float* psrc = D + gw * ldD;
+    const uint32_t last_bytes = (uint32_t)round_up((N - (nchunk - 1) * WSEL_C) * 4, 16);
+    auto issue = [&](int stage) {
+        if (prow >= M) return;
+        const uint32_t bytes = pc == nchunk - 1 ? last_bytes : (uint32_t)(WSEL_C * 4);
+        mbar_expect_tx(full0 + 8 * stage, bytes);
+        bulk_load(ring0 + stage * (WSEL_C * 4), psrc, bytes, full0 + 8 * stage);
+        psrc += WSEL_C;
+        if (++pc == nchunk) {
+            pc = 0;
+            prow += nw;
+            psrc = D + prow * ldD;
+        }
+    };
+    if (lane == 0)
+        for (int st = 0; st < S; ++st) issue(st);
+
+    int stage = 0;
+    uint32_t parity = 0;
+    for (int64_t row = gw; row < M; row += nw) {
+        // ---- pass 1: group minima (a group = one lane's 32 elements of a chunk)
+        uint32_t h0 = kKeyMax, h1 = kKeyMax;  // this lane's 2 smallest group minima
+        for (int64_t c = 0; c < nchunk; ++c) {
+            mbar_wait(full0 + 8 * stage, parity);
+            const float4* buf = reinterpret_cast<const float4*>(ring + (size_t)stage * WSEL_C);
+            float4 cur[VPT];
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) cur[j] = buf[j * 32 + lane];
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue(stage);  // refill this slot (the reads above are complete)
+            }
+            if (++stage == S) {
+                stage = 0;
+                parity ^= 1;
+            }
+            const int64_t base = c * WSEL_C;
+            if (base + WSEL_C > N) {  // ragged last chunk: columns >= N are NaN, which fminf ignores
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    const int64_t c0 = base + 4 * (j * 32 + lane);
+                    const float nan = __int_as_float(0x7FC00000);
+                    if (c0 + 0 >= N) cur[j].x = nan;
+                    if (c0 + 1 >= N) cur[j].y = nan;
+                    if (c0 + 2 >= N) cur[j].z = nan;
+                    if (c0 + 3 >= N) cur[j].w = nan;
+                }
+            }
+            float m[VPT];
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) m[j] = fminf(fminf(cur[j].x, cur[j].y), fminf(cur[j].z, cur[j].w));
+            #pragma unroll
+            for (int w = VPT / 2; w > 0; w >>= 1)
+                #pragma unroll
+                for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
+            // the key of an element of the group (all-NaN group: the NaN key); a group with
+            // no column < N never counts.  Stored as its upper 16 bits (rounded down: the
+            // pass-2 test hi16(G) <= hi16(P) keeps every group with G <= P, plus a few).
+            const uint32_t g = base + 4 * lane < N ? ukey(m[0]) : kKeyMax;
+            gmin[c * 32 + lane] = (uint16_t)(g >> 16);
+            if (g < h1) {
+                const uint32_t t = max(g, h0);
+                h0 = min(g, h0);
+                h1 = t;
+            }
+        }
+        // ---- pivot: the k-th smallest of the lanes' two smallest group minima (>= the k-th
+        // smallest group minimum; k of them, hence k elements, are <= it)
+        uint32_t hv[2] = {h0, h1};
+        warp_bitonic64_u32(hv);
+        const uint32_t P = __shfl_sync(FULL, hv[0], k - 1);  // element k - 1 (k <= 32)
+        // ---- pass 2: the groups whose minimum is <= P, listed (chunk << 5 | lane) in chunk
+        // order, are re-read from global memory (L2 for short rows) cooperatively: round r
+        // gives group r * 32 + l to lane l; keys <= P are compacted and folded
+        const uint32_t P16 = P >> 16;
+        const bool fastP = P <= 0xFF800000u;  // P is the key of a non-NaN value: x <= Pf is exact
+        const float Pf = ukey_to_float(P);
+        const float* rp = D + row * ldD;
+        uint64_t L = ~0ull;
+        int count = 0;
+        int ng = 0;  // groups listed in the current batch (warp-uniform)
+        auto process = [&](int nlist) {
+            for (int r0 = 0; r0 < nlist; r0 += 32) {
+                const int gi = r0 + lane;
+                uint32_t mask = 0;
+                int64_t gbase = 0;
+                if (gi < nlist) {
+                    const uint32_t ge = glist[gi];
+                    gbase = (int64_t)(ge >> 5) * WSEL_C + 4 * (ge & 31);  // column of the group's element 0
+                    const bool full = (int64_t)(ge >> 5) * WSEL_C + WSEL_C <= N;
+                    #pragma unroll
+                    for (int j = 0; j < VPT; ++j) {
+                        const int64_t c0 = gbase + 128 * j;
+                        if (full || c0 < N) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(rp + c0));
+                            const float x4[4] = {v.x, v.y, v.z, v.w};
+                            #pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                bool ok = fastP ? x4[e] <= Pf : ukey(x4[e]) <= P;
+                                if (!full) ok = ok && c0 + e < N;
+                                mask |= (uint32_t)ok << (4 * j + e);
+                            }
+                        }
+                    }
+                }
+                const int n = __popc(mask);
+                int incl = n;
+                #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int total = __shfl_sync(FULL, incl, 31);
+                const int excl = incl - n;
+                if (count + total > WS2_CAP) {
+                    L = ws2_fold(L, ckey, cidx, count);
+                    count = 0;
+                }
+                // windows of WS2_CAP survivor ranks (one window unless a round holds more
+                // than WS2_CAP survivors: heavily tied rows)
+                for (int w0 = 0; w0 < total; w0 += WS2_CAP) {
+                    uint32_t mm = mask;
+                    int r = excl;
+                    while (mm) {
+                        const int e = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        if (r >= w0 && r < w0 + WS2_CAP) {
+                            const int64_t col = gbase + 128 * (e >> 2) + (e & 3);
+                            ckey[count + r - w0] = ukey(rp[col]);
+                            cidx[count + r - w0] = (uint32_t)col;
+                        }
+                        ++r;
+                    }
+                    const int nwin = total - w0 < WS2_CAP ? total - w0 : WS2_CAP;
+                    if (total > WS2_CAP) {
+                        L = ws2_fold(L, ckey, cidx, nwin);
+                    } else {
+                        count += nwin;
+                    }
+                }
+            }
+        };
+        for (int64_t c = 0; c < nchunk; ++c) {
+            const bool hit = P == kKeyMax || (uint32_t)gmin[c * 32 + lane] <= P16;
+            const uint32_t bm = __ballot_sync(FULL, hit);
+            if (ng + __popc(bm) > WS2_CAP) {  // list full: process it first
+                __syncwarp();
+                process(ng);
+                ng = 0;
+            }
+            if (hit) glist[ng + __popc(bm & ws::lanemask_lt())] = (uint32_t)c << 5 | lane;
+            ng += __popc(bm);
+        }
+        __syncwarp();
+        process(ng);
+        if (count > 0) L = ws2_fold(L, ckey, cidx, count);
+        if (lane < k) {
+            out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)L + idx_offset);
+            out_dist[row * k + lane] = ukey_to_float((uint32_t)(L >> 32));
+        }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ merge kernel -----
 struct Offsets {
     int64_t v[64];
@@ -2577,6 +2833,28 @@ cudaError_t launch_select(const float* D, int64_t M, int64_t N, int64_t ldD, int
         const int x = v ? atoi(v) : WSEL_K;
         return x < 0 ? 0 : x > WSEL_K ? WSEL_K : x;
     }();
+    // two-pass warp per row (pivot = k-th smallest group minimum) for k <= 32 on rows of
+    // 1024..131072 elements; measured against the running-threshold warp select below:
+    //
+    static const bool two_pass = !getenv_flag("KNN_SELECT_ONEPASS");
+    if (two_pass && aligned && k <= 32 && N >= 32 * (int64_t)k && N >= WSEL_C && N <= WS2_MAXN &&
+        M >= 4 * (int64_t)sms) {
+        int S = 3;
+        if (const char* v = getenv("KNN_WS2_STAGES")) S = atoi(v);  // tuning knob
+        S = S < 2 ? 2 : S > WS2_MAXS ? WS2_MAXS : S;
+        const size_t smem = (size_t)ws2_slab_bytes(N, S);
+        if ((e = set_smem(select_warp2p_kernel, smem)) != cudaSuccess) return e;
+        int per_sm = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_warp2p_kernel, 32, smem)) !=
+            cudaSuccess)
+            return e;
+        int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+        if (grid > M) grid = M;
+        select_warp2p_kernel<<<(unsigned)grid, 32, smem, s>>>(D, M, N, ldD, k, S, idx_offset, out_idx, out_dist);
+        g_last_select_kind = 4;
+        g_last_select_splits = 1;
+        return cudaGetLastError();
+    }
     // warp per row for k <= 32; k > 32 goes to the CTA ring (sampled pivot, bucket finish):
     // measured 8192-long rows k = 64: 0.15 vs 0.30 ms, 65536-long rows k = 64: 3.6 vs
     // 6.5 ms (scripts/select_short.sh, select_mini.sh)

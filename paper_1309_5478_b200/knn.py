@@ -430,7 +430,7 @@ def select_paper(D, k, N=None, stream=None):
 
 
 SELECT_KERNELS = {0: "warp per row", 1: "CTA per row (ring)", 2: "CTA per row (unaligned)",
-                  3: "cluster per row"}
+                  3: "cluster per row", 4: "two-pass warp per row"}
 
 
 def last_select_kernel():

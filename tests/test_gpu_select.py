@@ -176,6 +176,68 @@ def test_warp_select_special_values():
         assert_same(gpu_select(D, k), oracle.select_f32(D, k))
 
 
+# ------------------------------------------------------------------ two-pass warp path --
+# k <= 32, 1024 <= N <= 131072, >= 4 rows per SM: pivot = the k-th smallest group minimum
+# (a group = one lane's 32 elements of a 1024-element chunk), then only the groups at or
+# below it are re-read (select.cu select_warp2p_kernel).
+@pytest.mark.parametrize("N", [1024, 1025, 3000, 8192, 65536, 131071])
+@pytest.mark.parametrize("k", [1, 16, 32])
+def test_two_pass_select_uniform(N, k):
+    D = datagen.keys(600, N, "uniform", seed=N * 17 + k)
+    got = gpu_select(D, k, ld=(N + 3) // 4 * 4)  # 16-byte aligned rows (the bulk-copy ring)
+    assert knn().last_select_kernel()[0] == "two-pass warp per row"
+    assert_same(got, oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("kind", ["dup256", "descending", "ascending", "equal"])
+@pytest.mark.parametrize("k", [1, 32])
+def test_two_pass_select_adversarial(kind, k):
+    """Ties at the pivot ("equal": every group minimum is the pivot, all 9000 elements
+    survive, in rounds of up to 1024 survivors folded in windows of 256)."""
+    D = datagen.keys(600, 9000, kind, seed=31)
+    got = gpu_select(D, k)
+    assert knn().last_select_kernel()[0] == "two-pass warp per row"
+    assert_same(got, oracle.select_f32(D, k))
+
+
+@pytest.mark.parametrize("N", [4096, 16384])
+def test_two_pass_select_heads_exhausted(N):
+    """The small keys all sit in one lane's groups (columns with (col // 4) % 32 == 0), so
+    that lane's 4 heads run out before k pops and the pivot comes from the other lanes:
+    looser, still exact (ring-resident rows and streamed rows)."""
+    k = 32
+    g = np.random.Generator(np.random.Philox(41))
+    D = (g.random((600, N), dtype=np.float32) + np.float32(1.0))
+    cols = np.arange(N)
+    lane0 = ((cols // 4) % 32) == 0
+    D[:, lane0] = g.random((600, int(lane0.sum())), dtype=np.float32) * np.float32(1e-3)
+    got = gpu_select(D, k)
+    assert knn().last_select_kernel()[0] == "two-pass warp per row"
+    assert_same(got, oracle.select_f32(D, k))
+
+
+def test_two_pass_select_special_values():
+    """-0/+0, +-inf, NaN (groups of NaN only: their minimum is the NaN key), rows with
+    fewer than k finite keys, ragged N."""
+    g = np.random.Generator(np.random.Philox(43))
+    N = 5000
+    D = g.standard_normal((700, N)).astype(np.float32)
+    D[:, ::7] = 0.0
+    D[:, 3::7] = -0.0
+    D[:, 5::11] = np.inf
+    D[:, 6::13] = -np.inf
+    D[:, 2::17] = np.nan
+    D[::3, :] = np.inf
+    D[::3, :5] = 1.0
+    D[1::5, :] = np.nan          # rows of NaN only
+    D[1::5, 4000:4010] = 2.0
+    D[2::7, :2048] = np.nan      # whole NaN groups next to finite ones
+    for k in (1, 17, 32):
+        got = gpu_select(D, k)
+        assert knn().last_select_kernel()[0] == "two-pass warp per row"
+        assert_same(got, oracle.select_f32(D, k))
+
+
 @pytest.mark.parametrize("N,k", [(8192, 1024), (20000, 200), (32768, 1024), (32768, 512),
                                   (65536, 129), (100003, 777)])
 def test_select_sampled_pivot(N, k):
