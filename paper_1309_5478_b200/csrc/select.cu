@@ -1392,11 +1392,17 @@ select_warp_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ld
 constexpr int WS2_MAXN = 131072;
 constexpr int WS2_CAP = 256;    // candidate buffer entries per warp
 constexpr int WS2_MAXS = 16;    // ring stages per warp (runtime S <= this)
-// slab: ring | S full barriers | 16-bit group minima [nchunk][32] | group list | cand key, idx
+#ifndef KNN_WS2_PRE
+#define KNN_WS2_PRE 1
+#endif
+constexpr int WS2_PRE = KNN_WS2_PRE;  // listed groups per lane loaded one row ahead (1 or 2)
+// slab: ring | S full barriers | 16-bit group minima [nchunk][32] | 16-bit group list
+// [nchunk * 32] | candidates key, idx [WS2_CAP]
+__host__ __device__ constexpr int64_t ws2_cand_offset(int64_t N, int S) {
+    return round_up((int64_t)S * WSEL_C * 4 + S * 8 + ceil_div(N, WSEL_C) * 32 * 2 * 2, 16);
+}
 __host__ __device__ constexpr int64_t ws2_slab_bytes(int64_t N, int S) {
-    return round_up((int64_t)S * WSEL_C * 4 + S * 8 + ceil_div(N, WSEL_C) * 32 * 2 + WS2_CAP * 4 +
-                        2 * WS2_CAP * 4,
-                    128);
+    return round_up(ws2_cand_offset(N, S) + 2 * WS2_CAP * 4, 128);
 }
 
 // Fold `count` buffered candidates into the sorted best-32 list L (warp_fold32, inlined).
@@ -1434,7 +1440,32 @@ __device__ __forceinline__ void warp_bitonic64_u32(uint32_t (&v)[2]) {
     }
 }
 
+// Group loads of pass 2, issued one row ahead: volatile so that the compiler keeps them
+// where they are (before the next row's pass 1) instead of sinking them to their use.
+__device__ __forceinline__ float4 ld_group4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+// Element e (0..31) of a group held in registers (predicated selects, no local memory).
+__device__ __forceinline__ float group_elem(const float4 (&v)[8], int e) {
+    float x = 0.0f;
+    #pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        x = e == 4 * j + 0 ? v[j].x : x;
+        x = e == 4 * j + 1 ? v[j].y : x;
+        x = e == 4 * j + 2 ? v[j].z : x;
+        x = e == 4 * j + 3 ? v[j].w : x;
+    }
+    return x;
+}
+
 // One warp per CTA (occupancy in whole warps), S ring stages of WSEL_C floats per warp.
+// Software-pipelined over rows: the first 64 listed groups of row r are loaded into
+// registers (two per lane) right after its pivot, and consumed only after pass 1 of the
+// warp's next row, so their L2 / HBM round trip overlaps that streaming.
 __global__ void __launch_bounds__(32)
 select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t ldD, int k, int S,
                      int64_t idx_offset, int32_t* __restrict__ out_idx, float* __restrict__ out_dist) {
@@ -1444,9 +1475,9 @@ select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t 
     const int64_t nchunk = ceil_div(N, WSEL_C);
     float* ring = reinterpret_cast<float*>(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * WSEL_C);
-    uint16_t* gmin = reinterpret_cast<uint16_t*>(bars + S);
-    uint32_t* glist = reinterpret_cast<uint32_t*>(smem_raw + round_up((int64_t)S * WSEL_C * 4 + S * 8 + nchunk * 64, 16));
-    uint32_t* ckey = glist + WS2_CAP;
+    uint16_t* gmin = reinterpret_cast<uint16_t*>(bars + S);   // [nchunk][32] upper key halves
+    uint16_t* glist = gmin + nchunk * 32;                      // [nchunk * 32] chunk << 5 | lane
+    uint32_t* ckey = reinterpret_cast<uint32_t*>(smem_raw + ws2_cand_offset(N, S));
     uint32_t* cidx = ckey + WS2_CAP;
     const uint32_t full0 = smem_u32(bars);
     const uint32_t ring0 = smem_u32(ring);
@@ -1476,18 +1507,26 @@ select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t 
     };
     if (lane == 0)
         for (int st = 0; st < S; ++st) issue(st);
-
     int stage = 0;
     uint32_t parity = 0;
-    for (int64_t row = gw; row < M; row += nw) {
-        // ---- pass 1: group minima (a group = one lane's 32 elements of a chunk)
-        uint32_t h0 = kKeyMax, h1 = kKeyMax;  // this lane's 2 smallest group minima
+
+    // ---- pass 1 of the next row of the FIFO: group minima (a group = one lane's 32
+    // elements of a chunk), stored as their upper 16 key bits (the pass-2 test
+    // hi16(G) <= hi16(P) keeps every group with G <= P, plus a few); the lane's two smallest
+    // full keys in h0 <= h1
+    auto pass1 = [&](uint32_t& h0, uint32_t& h1) {
+        h0 = kKeyMax;
+        h1 = kKeyMax;
         for (int64_t c = 0; c < nchunk; ++c) {
             mbar_wait(full0 + 8 * stage, parity);
             const float4* buf = reinterpret_cast<const float4*>(ring + (size_t)stage * WSEL_C);
+            // the lane's group = its 32 CONTIGUOUS elements [32 lane, 32 lane + 32) of the chunk
+            // (one 128-byte line to re-read in pass 2); float4 jj of the group is read as
+            // cur[(jj - lane) & 7], a rotation that keeps the 16-byte accesses of the warp
+            // conflict-free (4 wavefronts per load, the minimum)
             float4 cur[VPT];
             #pragma unroll
-            for (int j = 0; j < VPT; ++j) cur[j] = buf[j * 32 + lane];
+            for (int j = 0; j < VPT; ++j) cur[j] = buf[lane * VPT + ((j + lane) & (VPT - 1))];
             __syncwarp();
             if (lane == 0) {
                 fence_proxy_async_smem();
@@ -1501,7 +1540,7 @@ select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t 
             if (base + WSEL_C > N) {  // ragged last chunk: columns >= N are NaN, which fminf ignores
                 #pragma unroll
                 for (int j = 0; j < VPT; ++j) {
-                    const int64_t c0 = base + 4 * (j * 32 + lane);
+                    const int64_t c0 = base + 32 * lane + 4 * ((j + lane) & (VPT - 1));
                     const float nan = __int_as_float(0x7FC00000);
                     if (c0 + 0 >= N) cur[j].x = nan;
                     if (c0 + 1 >= N) cur[j].y = nan;
@@ -1517,9 +1556,8 @@ select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t 
                 #pragma unroll
                 for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
             // the key of an element of the group (all-NaN group: the NaN key); a group with
-            // no column < N never counts.  Stored as its upper 16 bits (rounded down: the
-            // pass-2 test hi16(G) <= hi16(P) keeps every group with G <= P, plus a few).
-            const uint32_t g = base + 4 * lane < N ? ukey(m[0]) : kKeyMax;
+            // no column < N never counts
+            const uint32_t g = base + 32 * lane < N ? ukey(m[0]) : kKeyMax;
             gmin[c * 32 + lane] = (uint16_t)(g >> 16);
             if (g < h1) {
                 const uint32_t t = max(g, h0);
@@ -1527,101 +1565,209 @@ select_warp2p_kernel(const float* __restrict__ D, int64_t M, int64_t N, int64_t 
                 h1 = t;
             }
         }
-        // ---- pivot: the k-th smallest of the lanes' two smallest group minima (>= the k-th
-        // smallest group minimum; k of them, hence k elements, are <= it)
+    };
+
+    // per-row pass-2 state, carried one row ahead
+    uint32_t P = 0;
+    float Pf = 0.0f;
+    bool fastP = true;
+    int ng = 0;                // groups listed
+    float4 va[VPT], vb[VPT];   // this lane's listed groups lane and lane + 32 (when < ng)
+    int64_t ga = 0, gb = 0;    // their element-0 columns
+    // pivot, group list and the first round's loads of row r (after its pass 1)
+    auto pivot_and_issue = [&](int64_t r, uint32_t h0, uint32_t h1) {
+        // P = the k-th smallest of the lanes' two smallest group minima (>= the k-th
+        // smallest group minimum; k of them, hence k elements of the row, are <= it)
         uint32_t hv[2] = {h0, h1};
         warp_bitonic64_u32(hv);
-        const uint32_t P = __shfl_sync(FULL, hv[0], k - 1);  // element k - 1 (k <= 32)
-        // ---- pass 2: the groups whose minimum is <= P, listed (chunk << 5 | lane) in chunk
-        // order, are re-read from global memory (L2 for short rows) cooperatively: round r
-        // gives group r * 32 + l to lane l; keys <= P are compacted and folded
+        P = __shfl_sync(FULL, hv[0], k - 1);  // element k - 1 (k <= 32)
+        fastP = P <= 0xFF800000u;  // P is the key of a non-NaN value: x <= Pf is exact
+        Pf = ukey_to_float(P);
         const uint32_t P16 = P >> 16;
-        const bool fastP = P <= 0xFF800000u;  // P is the key of a non-NaN value: x <= Pf is exact
-        const float Pf = ukey_to_float(P);
-        const float* rp = D + row * ldD;
-        uint64_t L = ~0ull;
-        int count = 0;
-        int ng = 0;  // groups listed in the current batch (warp-uniform)
-        auto process = [&](int nlist) {
-            for (int r0 = 0; r0 < nlist; r0 += 32) {
-                const int gi = r0 + lane;
-                uint32_t mask = 0;
-                int64_t gbase = 0;
-                if (gi < nlist) {
-                    const uint32_t ge = glist[gi];
-                    gbase = (int64_t)(ge >> 5) * WSEL_C + 4 * (ge & 31);  // column of the group's element 0
-                    const bool full = (int64_t)(ge >> 5) * WSEL_C + WSEL_C <= N;
-                    #pragma unroll
-                    for (int j = 0; j < VPT; ++j) {
-                        const int64_t c0 = gbase + 128 * j;
-                        if (full || c0 < N) {
-                            const float4 v = __ldg(reinterpret_cast<const float4*>(rp + c0));
-                            const float x4[4] = {v.x, v.y, v.z, v.w};
-                            #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                bool ok = fastP ? x4[e] <= Pf : ukey(x4[e]) <= P;
-                                if (!full) ok = ok && c0 + e < N;
-                                mask |= (uint32_t)ok << (4 * j + e);
-                            }
-                        }
-                    }
-                }
-                const int n = __popc(mask);
-                int incl = n;
-                #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(FULL, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int total = __shfl_sync(FULL, incl, 31);
-                const int excl = incl - n;
-                if (count + total > WS2_CAP) {
-                    L = ws2_fold(L, ckey, cidx, count);
-                    count = 0;
-                }
-                // windows of WS2_CAP survivor ranks (one window unless a round holds more
-                // than WS2_CAP survivors: heavily tied rows)
-                for (int w0 = 0; w0 < total; w0 += WS2_CAP) {
-                    uint32_t mm = mask;
-                    int r = excl;
-                    while (mm) {
-                        const int e = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        if (r >= w0 && r < w0 + WS2_CAP) {
-                            const int64_t col = gbase + 128 * (e >> 2) + (e & 3);
-                            ckey[count + r - w0] = ukey(rp[col]);
-                            cidx[count + r - w0] = (uint32_t)col;
-                        }
-                        ++r;
-                    }
-                    const int nwin = total - w0 < WS2_CAP ? total - w0 : WS2_CAP;
-                    if (total > WS2_CAP) {
-                        L = ws2_fold(L, ckey, cidx, nwin);
-                    } else {
-                        count += nwin;
-                    }
-                }
-            }
-        };
+        ng = 0;
         for (int64_t c = 0; c < nchunk; ++c) {
-            const bool hit = P == kKeyMax || (uint32_t)gmin[c * 32 + lane] <= P16;
+            const bool hit = (uint32_t)gmin[c * 32 + lane] <= P16;
             const uint32_t bm = __ballot_sync(FULL, hit);
-            if (ng + __popc(bm) > WS2_CAP) {  // list full: process it first
-                __syncwarp();
-                process(ng);
-                ng = 0;
-            }
-            if (hit) glist[ng + __popc(bm & ws::lanemask_lt())] = (uint32_t)c << 5 | lane;
+            if (hit) glist[ng + __popc(bm & ws::lanemask_lt())] = (uint16_t)((uint32_t)c << 5 | lane);
             ng += __popc(bm);
         }
         __syncwarp();
-        process(ng);
-        if (count > 0) L = ws2_fold(L, ckey, cidx, count);
-        if (lane < k) {
-            out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)L + idx_offset);
-            out_dist[row * k + lane] = ukey_to_float((uint32_t)(L >> 32));
+        const float* rp = D + r * ldD;
+        #pragma unroll
+        for (int h = 0; h < WS2_PRE; ++h) {
+            const int gi = lane + 32 * h;
+            int64_t gbase = 0;
+            float4* v = h ? vb : va;
+            if (gi < ng) {
+                const uint32_t ge = glist[gi];
+                gbase = (int64_t)(ge >> 5) * WSEL_C + 32 * (ge & 31);
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j)
+                    v[j] = gbase + 4 * j < N ? ld_group4(rp + gbase + 4 * j)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (h) gb = gbase; else ga = gbase;
         }
-        __syncwarp();
+    };
+    // survivors of one group held in registers: the keys <= P of columns < N.  Full chunk
+    // and P non-NaN (the common case): one test per float4 on its minimum, element tests
+    // only inside float4s holding a survivor.
+    auto group_mask = [&](const float4 (&v)[VPT], int64_t gbase) -> uint32_t {
+        uint32_t mask = 0;
+        const bool full = (gbase / WSEL_C) * WSEL_C + WSEL_C <= N;  // the group's whole chunk is < N
+        if (full && fastP) {
+            #pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                if (fminf(fminf(v[j].x, v[j].y), fminf(v[j].z, v[j].w)) <= Pf) {
+                    mask |= (uint32_t)(v[j].x <= Pf) << (4 * j);
+                    mask |= (uint32_t)(v[j].y <= Pf) << (4 * j + 1);
+                    mask |= (uint32_t)(v[j].z <= Pf) << (4 * j + 2);
+                    mask |= (uint32_t)(v[j].w <= Pf) << (4 * j + 3);
+                }
+            }
+            return mask;
+        }
+        #pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const float x4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            #pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const bool ok = (fastP ? x4[e] <= Pf : ukey(x4[e]) <= P) && gbase + 4 * j + e < N;
+                mask |= (uint32_t)ok << (4 * j + e);
+            }
+        }
+        return mask;
+    };
+    // write a group's survivors (register values, static indices) at ckey/cidx[pos...]
+    auto put_group = [&](const float4 (&v)[VPT], int64_t gbase, uint32_t mask, int pos) {
+        #pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            if ((mask >> (4 * j)) & 15u) {
+                const float x4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+                #pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if ((mask >> (4 * j + e)) & 1u) {
+                        ckey[pos] = ukey(x4[e]);
+                        cidx[pos] = (uint32_t)(gbase + 4 * j + e);
+                        ++pos;
+                    }
+                }
+            }
+        }
+    };
+    uint64_t L = ~0ull;
+    int count = 0;
+    // compact one round's survivors (mask per lane; element values re-read by dynamic index
+    // from registers) into the buffer, folding as it fills; windows of WS2_CAP survivor
+    // ranks when a round alone holds more (heavily tied rows)
+    auto append = [&](uint32_t mask, const float4 (&v)[VPT], int64_t gbase) {
+        const int n = __popc(mask);
+        int incl = n;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        const int excl = incl - n;
+        if (count + total > WS2_CAP) {
+            L = ws2_fold(L, ckey, cidx, count);
+            count = 0;
+        }
+        if (total <= WS2_CAP) {
+            put_group(v, gbase, mask, count + excl);
+            count += total;
+            return;
+        }
+        for (int w0 = 0; w0 < total; w0 += WS2_CAP) {
+            uint32_t mm = mask;
+            int r = excl;
+            while (mm) {
+                const int e = __ffs(mm) - 1;
+                mm &= mm - 1;
+                if (r >= w0 && r < w0 + WS2_CAP) {
+                    ckey[r - w0] = ukey(group_elem(v, e));
+                    cidx[r - w0] = (uint32_t)(gbase + e);
+                }
+                ++r;
+            }
+            L = ws2_fold(L, ckey, cidx, total - w0 < WS2_CAP ? total - w0 : WS2_CAP);
+        }
+    };
+    // pass 2 of row r: the preloaded first 64 groups, then any further listed groups.  The
+    // common case (<= 64 candidates in all) ends with one 64-wide sort instead of folds.
+    auto complete = [&](int64_t r) {
+        const float* rp = D + r * ldD;
+        L = ~0ull;
+        count = 0;
+        {
+            const uint32_t ma = lane < ng ? group_mask(va, ga) : 0u;
+            const uint32_t mb = WS2_PRE > 1 && lane + 32 < ng ? group_mask(vb, gb) : 0u;
+            const int n = __popc(ma) + __popc(mb);
+            int incl = n;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(FULL, incl, 31);
+            if (total <= WS2_CAP) {
+                put_group(va, ga, ma, incl - n);
+                put_group(vb, gb, mb, incl - n + __popc(ma));
+                count = total;
+            } else {
+                append(ma, va, ga);
+                append(mb, vb, gb);
+            }
+        }
+        for (int r0 = 32 * WS2_PRE; r0 < ng; r0 += 32) {  // (ties / loose pivots) synchronous rounds
+            const int gi = r0 + lane;
+            float4 v[VPT];
+            int64_t gbase = 0;
+            uint32_t mask = 0;
+            if (gi < ng) {
+                const uint32_t ge = glist[gi];
+                gbase = (int64_t)(ge >> 5) * WSEL_C + 32 * (ge & 31);
+                #pragma unroll
+                for (int j = 0; j < VPT; ++j)
+                    v[j] = gbase + 4 * j < N ? __ldg(reinterpret_cast<const float4*>(rp + gbase + 4 * j))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                mask = group_mask(v, gbase);
+            }
+            append(mask, v, gbase);
+        }
+        if (__all_sync(FULL, L == ~0ull) && count <= 64) {  // (no fold happened)
+            // one sort of the (<= 64) candidates; the first k are the row's result
+            __syncwarp();
+            uint64_t sv[2];
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 32 * h + lane;
+                sv[h] = i < count ? ((uint64_t)ckey[i] << 32 | cidx[i]) : ~0ull;
+            }
+            ws::warp_bitonic<2>(sv);
+            L = sv[0];
+        } else if (count > 0) {
+            L = ws2_fold(L, ckey, cidx, count);
+        }
+        if (lane < k) {
+            out_idx[r * k + lane] = (int32_t)((int64_t)(uint32_t)L + idx_offset);
+            out_dist[r * k + lane] = ukey_to_float((uint32_t)(L >> 32));
+        }
+        __syncwarp();  // glist / buffer reads done before the next row's list
+    };
+
+    if (gw < M) {
+        uint32_t h0, h1;
+        pass1(h0, h1);
+        pivot_and_issue(gw, h0, h1);
+    }
+    for (int64_t row = gw; row < M; row += nw) {
+        const int64_t next = row + nw;
+        uint32_t h0 = kKeyMax, h1 = kKeyMax;
+        if (next < M) pass1(h0, h1);  // (gmin is free: row's list is built)
+        complete(row);
+        if (next < M) pivot_and_issue(next, h0, h1);
     }
 }
 
