@@ -97,6 +97,37 @@ bool metric_ok(knn_ctx* ctx, int32_t metric, knn_status* st) {
     return false;
 }
 
+// Rank of the chunk-minimum pivot.  Rank kk (the k-th smallest non-self
+// element guaranteed at or below the pivot: kk distinct chunk minima are) certifies the
+// partition by construction, at ~kk N/S candidates per row.  A smaller rank r keeps ~r N/S
+// and fails — fewer than k candidates, which the candidate select detects (the call is then
+// redone on the full matrix) — only if r or more of the S sampled columns fall among the
+// row's kk - 1 nearest points: probability <= P(Bin(kk - 1, S/N) >= r) per row (the r-th
+// chunk minimum is >= the r-th smallest sampled value; the sample's error margin only raises
+// the pivot).  r = the smallest rank with that tail below 1e-3 / M: a call is redone with
+// probability < 1e-3 on data the column sample represents (headline: 18 instead of 33,
+// ~150 instead of ~330 candidates per row).  KNN_PIVOT_RANK: 0 = certified, r > 0 = fixed.
+int32_t pivot_rank(int32_t kk, int64_t S, int64_t N, int64_t M) {
+    static const int env = [] {
+        const char* v = getenv("KNN_PIVOT_RANK");
+        return v ? atoi(v) : -1;
+    }();
+    if (env == 0) return kk;
+    if (env > 0) return env < kk ? env : kk;
+    const double p = (double)S / (double)N, eps = 1e-3 / (double)(M > 1 ? M : 1);
+    const int n = kk - 1;
+    if (n < 1 || p >= 1.0) return kk;
+    double tail = 0.0;  // P(Bin(n, p) >= r), accumulated from r = n down
+    int best = kk;
+    for (int r = n; r >= 1; --r) {
+        tail += std::exp(std::lgamma(n + 1.0) - std::lgamma(r + 1.0) - std::lgamma(n - r + 1.0) +
+                         r * std::log(p) + (n - r) * std::log1p(-p));
+        if (tail > eps) break;
+        best = r;
+    }
+    return best;
+}
+
 // Queue the whole hot path for one block problem; asynchronous on `s`.
 knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
                      int32_t d, int32_t k, int32_t metric, int64_t self_shift, int64_t idx_offset,
@@ -222,7 +253,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                                                   ctx->num_sms, s, smax));
                 tg.done();
                 Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
-                KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, round_up(r0 + R, knn::kColPad) - r0, kk, metric,
+                KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, round_up(r0 + R, knn::kColPad) - r0,
+                                                     pivot_rank(kk, Ssamp, N, M), metric,
                                                          thr + r0, cnt + r0, s));
                 tp.done();
             }
@@ -652,7 +684,8 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         }
         {
             Timed tp(ctx, KNN_KERNEL_SELECT, s);
-            KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, R, R, kk, metric, thr + c0, cnt + c0, s));
+            KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, R, R, knn_rt::pivot_rank(kk, S, N, N), metric,
+                                                 thr + c0, cnt + c0, s));
             tp.done();
         }
         // the triangle's units whose column block lies in this chunk (rows and columns < c0 + R)
@@ -1091,8 +1124,8 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     if (small) {
         KNN_CUDA(knn::launch_pivot_from_mins(D, S / 32, rows,
                                                      // pad only to the absolute 256-row boundary
-                                                     round_up(row0 + rows, knn::kColPad) - row0, kk,
-                                                     metric, thr + row0, cnt, s));
+                                                     round_up(row0 + rows, knn::kColPad) - row0,
+                                                     knn_rt::pivot_rank(kk, S, N, N), metric, thr + row0, cnt, s));
     } else {
         const double mu = (double)S * k / (double)N;
         const int32_t rq = (int32_t)std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0) + 1;
