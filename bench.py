@@ -313,14 +313,17 @@ def run_ours(args):
     def tkey(kernel):
         return kernel + "_c4" if args.config == "C4" and kernel.startswith("dist_tc_kernel") else kernel
 
-    # KNN_PIVOT1=1 (opt-in): the k <= 32 partition runs on the single hi.hi product and the
-    # candidate select re-evaluates the survivors
-    pivot1 = os.environ.get("KNN_PIVOT1", "0") not in ("", "0") and k <= 32 and plan_code in (3, 4)
+    # plans 5 / 6: the k <= 32 partition ran on the single hi.hi product (chosen on the
+    # device, or KNN_PIVOT1=1) and the candidate select re-evaluated the survivors in fp32
+    # (DESIGN.md §6.5); 3 / 4: the FP32-accurate 3-product partition
+    pivot1 = plan_code in (5, 6)
+    sym_plan = plan_code in (2, 3, 5)
+    pivot_plan = plan_code in (3, 4, 5, 6)
 
     def pairs_of(kernel):
         if kernel == "dist_tc_kernel_sample":
             return rows_w * S_samp
-        if plan_code in (2, 3):
+        if sym_plan:
             # symmetric: the upper triangle of 256x256 blocks (split over the ranks by Par-3)
             nblk = -(-N // 256)
             return nblk * (nblk + 1) / 2 * 256.0 * 256.0 / (world if sym_shard else 1)
@@ -360,13 +363,13 @@ def run_ours(args):
     m_ms, m_n = prof["merge"]
     p_ms, p_n = prof["prep"]
     x_ms, x_n = prof["xmerge"]
-    if f_n and plan_code in (3, 4):
+    if f_n and pivot_plan:
         rooflines.append((f_ms, tensor_roof(
             "dist_tc_kernel<PIVOT%s%s> (a-S5: GEMM with the quickselect partition in its epilogue%s)"
-            % ("1" if pivot1 else "", ",SYM" if plan_code == 3 else "",
+            % ("1" if pivot1 else "", ",SYM" if plan_code in (3, 5) else "",
                ", single hi.hi product" if pivot1 else ""), "dist_tc_kernel", f_ms, f_n,
             products=1 if pivot1 else 3)))
-    if g_n and plan_code in (3, 4):
+    if g_n and pivot_plan:
         gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x N/8 sampled columns -> 32-column chunk minima)"
                          if k <= 32 else
                          f"dist_tc_kernel<SAMPLE> (quantile-pivot sample: single-product upper bounds, rows x {S_samp} columns)",
@@ -391,7 +394,7 @@ def run_ours(args):
             gr["kernel"] = "dist_tc_kernel<SYM> (a-S3, symmetric k-NNG: upper triangle, direct + transposed stores)"
         rooflines.append((g_ms, gr))
     piv_rows = R_local if sym_shard else rows_w
-    if s_n and plan_code in (3, 4):
+    if s_n and pivot_plan:
         if k <= 32:
             rooflines.append((s_ms, hbm_roof("pivot_from_mins_kernel (pivot = k-th smallest of the row's chunk minima)",
                                              "pivot_from_mins_kernel", s_ms, s_n,
@@ -406,7 +409,7 @@ def run_ours(args):
             kind, "select_ring_kernel")
         rooflines.append((s_ms, hbm_roof(f"{kname} (a-S4, {kind})", kname, s_ms, s_n,
                                          rows_w / sl * (cols_w * 4.0 + k * 8.0))))
-    if m_n and plan_code in (3, 4):
+    if m_n and pivot_plan:
         cands = knn.last_candidates()  # survivors of the partition (whole call)
         sel_rows = R_local if sym_shard else rows_w
         cs_name = ("candidate_recompute_kernel" if pivot1 else "candidate_select_kernel") if k <= 32 \
@@ -431,7 +434,11 @@ def run_ours(args):
     roofline["plan"] = {0: "blocked distances + select",
                         2: "symmetric k-NNG distances (PAPER.md:83 transpose reuse) + select",
                         3: "pivot (quickselect partition, PAPER.md:56) over the symmetric GEMM",
-                        4: "pivot (quickselect partition, PAPER.md:56) over the GEMM"}.get(
+                        4: "pivot (quickselect partition, PAPER.md:56) over the GEMM",
+                        5: "pivot (quickselect partition, PAPER.md:56) over the symmetric single-product GEMM, "
+                           "survivors re-evaluated in fp32",
+                        6: "pivot (quickselect partition, PAPER.md:56) over the single-product GEMM, "
+                           "survivors re-evaluated in fp32"}.get(
                             plan_code, "unknown")
 
     # ---- e2e: the public host-buffer API, H2D of the inputs and D2H of the results inside

@@ -338,22 +338,35 @@ int knn_gemm_path(knn_ctx_t ctx);
  * certificate fails; otherwise the materialised distances (symmetric upper-triangle GEMM
  * for the k-NNG) + select.  KNN_PLAN_MATERIALISED: never the pivot plan.  KNN_PLAN_FUSED
  * is reserved: round 1's per-row-list fused kernel was retired (4.5x slower than the pivot
- * plan, which is the fused GEMM+select); setting it returns KNN_ERR_UNSUPPORTED.  All
- * plans give bit-identical results.
+ * plan, which is the fused GEMM+select); setting it returns KNN_ERR_UNSUPPORTED.
+ * For k <= 32 and the L2 metrics the AUTO pivot plan may partition on the single hi.hi
+ * product with its error bound and re-evaluate the survivors near the k-th from the fp32
+ * inputs (chosen on the device per call when that bound is narrow against
+ * the pivots): its distances are then the direct fp32 sum of squared differences (more
+ * accurate than the split-fp16 contraction, within the same tolerance of the exact value,
+ * but not the same bits).  KNN_PLAN_PIVOT_EXACT: the pivot plan with the FP32-accurate
+ * 3-product partition only; it, MATERIALISED and the symmetric plan give bit-identical
+ * results.
  * Environment, read at ctx creation: KNN_FUSED=0 (MATERIALISED), KNN_PIVOT=0
  * (no pivot plan), KNN_SYM=0 (no symmetric GEMM), KNN_PIVOT_DIV=n (sample N/n columns,
  * default 8), KNN_PIVOT_CAP (candidate list capacity), KNN_D_BUDGET_MB (distance block
  * budget), KNN_GEMM=simt (FFMA cross-check GEMM), KNN_PIVOT_MARGIN (tests: override the
- * sample's error margin), KNN_PIVOT1=1 (k <= 32, L2: partition from the single hi.hi
- * product with an error bound and the survivors near the k-th re-evaluated in fp32 from
- * the inputs — faster and more accurate, but its values are not bit-identical to the
- * other plans'; off by default). */
-typedef enum { KNN_PLAN_AUTO = 0, KNN_PLAN_FUSED = 1, KNN_PLAN_MATERIALISED = 2 } knn_plan;
+ * sample's error margin), KNN_PIVOT1=1 / 0 (k <= 32, L2: always / never the single-product
+ * partition; unset: chosen on the device), KNN_PIVOT1_RATIO (the choice's largest bound
+ * width relative to the mean pivot, default 0.02), KNN_PIVOT_RANK (0: the certified pivot
+ * rank k+1; r: rank r). */
+typedef enum {
+    KNN_PLAN_AUTO = 0,
+    KNN_PLAN_FUSED = 1,
+    KNN_PLAN_MATERIALISED = 2,
+    KNN_PLAN_PIVOT_EXACT = 3
+} knn_plan;
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
 /* Plan the last top-level call of this ctx executed: 0 = blocked distances + select,
  * 1 = (retired fused plan, never reported), 2 = symmetric k-NNG distances (upper triangle of 256x256 blocks,
  * each written directly and transposed) + select, 3 = pivot plan,
- * symmetric, 4 = pivot plan, general block, -1 = none yet.  The pivot plan (k <= 32,
+ * symmetric, 4 = pivot plan, general block, 5 / 6 = the same with the single-product
+ * partition and the fp32 re-evaluation (L2 metrics, k <= 32), -1 = none yet.  The pivot plan (k <= 32,
  * N >= 16384) is the quick multi-select partition of PAPER.md:56 applied at matrix scale:
  * a sample pass over the first N/8 corpus points (one fp16 product plus a bound of its
  * error) gives each row the minimum of every 32-column chunk; the row pivot is the k-th
@@ -361,7 +374,7 @@ knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan);
  * only elements <= pivot (for rows and, in the symmetric plan, transposed for columns);
  * an exact select of the candidates follows.  Rows with fewer than k candidates (a
  * failed certificate) or a candidate-buffer overflow make the call redo itself on the
- * full matrix.  All plans give bit-identical results. */
+ * full matrix. */
 int knn_last_plan(knn_ctx_t ctx);
 /* Total candidates the last pivot-plan call kept (sum over rows of the partition's
  * survivors; 0 for the other plans, -1 for a null ctx).  Diagnostic: the bench reports

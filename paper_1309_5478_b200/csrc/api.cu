@@ -262,32 +262,47 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         // 3. partition GEMM over the whole matrix, 4. exact select of the candidates
         knn::TcOperands op{pq.hi, pq.lo, pq.sqn, pq.rs, M, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
         // L2 metrics: the partition from the single hi.hi product with its error bound (a
-        // third of the MMA work) and the survivors near the k-th re-evaluated exactly
-        const bool one = ctx->pivot1 && metric <= KNN_L2;
-        if (one) {  // the lower bound u_hh - F n_qx as the u of norms scaled by 1 - F
-            const float f = 1.0f - knn::pivot1_margin(d_pad);
-            KNN_CUDA(knn::launch_scale_norms(px.sqn, nsc_x, round_up(N, knn::kColPad), f, s));
-            if (!same) KNN_CUDA(knn::launch_scale_norms(pq.sqn, nsc_q, round_up(M, knn::kColPad), f, s));
+        // third of the MMA work) and the survivors near the k-th re-evaluated exactly from the
+        // fp32 inputs.  Chosen on the device (pivot1_decide: the bound must be narrow against
+        // the pivots — data far from the origin widens it), forced by KNN_PIVOT1=1, never
+        // with KNN_PIVOT1=0 or KNN_PLAN_PIVOT_EXACT (the FP32-accurate 3-product partition,
+        // bit-identical to the materialised plan).
+        const bool p1_ok = metric <= KNN_L2 && ctx->plan != KNN_PLAN_PIVOT_EXACT && ctx->pivot1 != 0;
+        const bool p1_auto = p1_ok && ctx->pivot1 < 0;
+        const bool one = p1_ok && ctx->pivot1 > 0;
+        knn::TcOperands op1 = op;
+        const float F = knn::pivot1_margin(d_pad);
+        if (p1_ok) {  // the lower bound u_hh - F n_qx as the u of norms scaled by 1 - F
+            KNN_CUDA(knn::launch_scale_norms(px.sqn, nsc_x, round_up(N, knn::kColPad), 1.0f - F, s));
+            if (!same) KNN_CUDA(knn::launch_scale_norms(pq.sqn, nsc_q, round_up(M, knn::kColPad), 1.0f - F, s));
             ctx->launches += same ? 1 : 2;
-            op.qn = same ? nsc_x : nsc_q;
-            op.xn = nsc_x;
+            op1.qn = same ? nsc_x : nsc_q;
+            op1.xn = nsc_x;
         }
+        if (p1_auto) {
+            KNN_CUDA(knn::launch_pivot1_decide(thr, pq.sqn, M, px.sqn, N, F, ctx->pivot1_ratio, flag, s));
+            ctx->launches++;
+        }
+        ctx->last_plan_auto1 = p1_auto;
+        if (one) ctx->last_plan += 2;  // 5 / 6: the single-product partition
         Timed tg(ctx, KNN_KERNEL_FUSED, s);
-        if (one)
-            KNN_CUDA(knn::launch_dist_tc_pivot1(op, metric, self_shift, pivot_sym, thr, cnt, cent, cap,
-                                                flag, ctx->num_sms, s));
-        else
+        if (one || p1_auto)
+            KNN_CUDA(knn::launch_dist_tc_pivot1(op1, metric, self_shift, pivot_sym, thr, cnt, cent, cap,
+                                                flag, ctx->num_sms, s, p1_auto ? 1 : -1));
+        if (!one)
             KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, self_shift, pivot_sym, thr, cnt, cent, cap,
-                                               flag, ctx->num_sms, s));
+                                               flag, ctx->num_sms, s, -1, -1, false, p1_auto ? 0 : -1));
+        ctx->launches += p1_auto ? 1 : 0;
         tg.done();
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
-        if (one)
+        if (one || p1_auto)
             KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, M, k, idx_offset, Q, X, d, pq.sqn,
-                                                     px.sqn, thr, knn::pivot1_margin(d_pad), metric, out_idx,
-                                                     out_dist, flag, s));
-        else
+                                                     px.sqn, thr, F, metric, out_idx, out_dist, flag, s,
+                                                     p1_auto ? 1 : -1));
+        if (!one)
             KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, M, k, idx_offset, out_idx, out_dist, flag,
-                                                  s));
+                                                  s, p1_auto ? 0 : -1));
+        ctx->launches += p1_auto ? 1 : 0;
         tc2.done();
         return KNN_OK;
     }
@@ -363,6 +378,10 @@ knn_status finish_blocking(knn_ctx* ctx, cudaStream_t s) {
     KNN_CUDA(cudaMemcpyAsync(ctx->flag_host, flag, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     KNN_CUDA(cudaStreamSynchronize(s));
     memcpy(&ctx->last_candidates, ctx->flag_host + 2, sizeof(int64_t));
+    // the device chose the single-product partition: plans 3 / 4 -> 5 / 6
+    if (ctx->last_plan_auto1 && ctx->flag_host[1] == 1 && (ctx->last_plan == 3 || ctx->last_plan == 4))
+        ctx->last_plan += 2;
+    ctx->last_plan_auto1 = false;
     if (*ctx->flag_host & 1)
         return fail(ctx, KNN_ERR_NONFINITE,
                     "input contains NaN/inf or a vector with ||x||^2 >= FLT_MAX/4");
@@ -420,7 +439,9 @@ knn_status knn_ctx_create(int device, knn_ctx_t* out) {
     const char* pd = getenv("KNN_PIVOT_DIV");
     if (pd && atoi(pd) >= 2) c->pivot_div = atoi(pd);
     const char* p1 = getenv("KNN_PIVOT1");
-    if (p1 && p1[0] && strcmp(p1, "0") != 0) c->pivot1 = true;
+    if (p1 && p1[0]) c->pivot1 = strcmp(p1, "0") != 0 ? 1 : 0;
+    const char* pr = getenv("KNN_PIVOT1_RATIO");
+    if (pr) c->pivot1_ratio = strtof(pr, nullptr);
     const char* pm = getenv("KNN_PIVOT_MARGIN");
     if (pm) c->pivot_margin = strtof(pm, nullptr);
     const char* pc = getenv("KNN_PIVOT_CAP");
@@ -466,7 +487,7 @@ int64_t knn_launch_count(knn_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
 knn_status knn_set_plan(knn_ctx_t ctx, int32_t plan) {
     if (!ctx) return KNN_ERR_ARG;
-    if (plan < KNN_PLAN_AUTO || plan > KNN_PLAN_MATERIALISED)
+    if (plan < KNN_PLAN_AUTO || plan > KNN_PLAN_PIVOT_EXACT)
         return fail(ctx, KNN_ERR_ARG, "unknown plan %d", plan);
     if (plan == KNN_PLAN_FUSED)  // the per-row-list fused kernel was retired
         return fail(ctx, KNN_ERR_UNSUPPORTED, "KNN_PLAN_FUSED was retired; the pivot plan is the fused path");
@@ -577,7 +598,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     const char* env = getenv("KNN_HOST_PIPE");
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
     if ((env && strcmp(env, "0") == 0) || !tc || !ctx->pivot_ok || !ctx->sym_ok ||
-        ctx->plan == KNN_PLAN_MATERIALISED || ctx->pivot1 || k > 32 || N < 16384 || N % 2048 != 0 ||
+        ctx->plan == KNN_PLAN_MATERIALISED || ctx->pivot1 > 0 || k > 32 || N < 16384 || N % 2048 != 0 ||
         ctx->pivot_div != 8)
         return KNN_ERR_UNSUPPORTED;
     const int64_t S = N / 8;                    // sample: points 8j, j < S (a multiple of 256)

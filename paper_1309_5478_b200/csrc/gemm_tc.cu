@@ -50,7 +50,7 @@ constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 output chunk (TMA-stor
 // by COL_WARP into an NCOL-deep ring so the epilogue warps never wait on each other.
 constexpr int NCOL = 4;
 constexpr int COL_BYTES = 3 * BN * 4;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + NCOL * COL_BYTES +
+constexpr int SMEM_BYTES = RING_BYTES + EPI_WARPS * 2 * STG_BYTES + NCOL * COL_BYTES +
                            1024 /*align*/ + 1024 /*barriers*/;
 // SYM (symmetric k-NNG): each warp's two staging buffers hold the direct and the transposed
 // chunk of the same 32x32 block.
@@ -67,6 +67,7 @@ struct EpiArgs {
     // block nb / nb_stride
     int64_t nb_stride = 1;
     const float* xmax = nullptr;  // MINS: upper bound of every column's sqn term (device scalar)
+    int32_t gate = -1;  // PIVOT modes: run only if flag[1] == gate (device plan choice), -1 always
     int32_t dbg = 0;  // DIAGNOSTIC (env KNN_DBG_EPI, wrong results): 1 skip column test, 2 skip appends,
                       // 4 skip both tests, 8 skip global flushes, 16 staging without appends
 };
@@ -99,7 +100,11 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
 // Candidates found by a warp are first appended to a warp-private shared list (SoA: row,
 // col, key) and flushed to the global per-row lists in batches of up to PEND_CAP, four
 // returning atomics in flight per lane, so their latency is paid once per batch.
-constexpr int PEND_CAP = 320;  // 3 x 320 x 4 B in one 4 KB staging buffer
+constexpr int PEND_CAP = 320;
+#ifndef KNN_EPI_REG
+#define KNN_EPI_REG 1  // survivor slots by warp scan, padded staging rows (1), or round 1's path (0)
+#endif
+constexpr int SROW = 36;  // staged floats per lane row (KNN_EPI_REG): 144-byte rows  // 3 x 320 x 4 B in one 4 KB staging buffer
 
 // Deferred flush (PIVOT modes): the pending list is moved into registers (J entries per
 // lane) and its slots reserved with returning atomics, but the entries are written only at
@@ -151,17 +156,25 @@ struct DeferredFlush {
 // SM sub-partition issue ~45% of cycles), so it runs 12 warps — 3 per TMEM lane quadrant,
 // owning 3/3/2 of the tile's eight 32-column chunks — with a smaller pending list and a
 // 3-deep column ring to fit the shared memory; the other modes keep 8 warps (BN/2 each).
-template <int MODE>
+// ARES (A-panel-resident sample pass, PanelSched): the operand region holds two A panels
+// (d_pad <= 256) and a 5-stage B ring, using the staging slabs the MINS epilogue does not
+// need (it stores its chunk minima directly).
+constexpr int ARES_KB = CTA2 ? 10 : 5;      // B ring stages
+constexpr int ARES_PANEL = 8 * A_BYTES;     // one A panel: BM x 256 fp16
+template <int MODE, bool ARES = false>
 struct EpiCfg {
     static constexpr bool PV = MODE == 1 || MODE == 5;  // MODE_PIVOT, MODE_PIVOT1
     static constexpr int WARPS = PV ? 12 : EPI_WARPS;
     static constexpr int PARTS = WARPS / 4;
     static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
-    static constexpr int PEND = PV ? 160 : PEND_CAP;
-    static constexpr int SLAB = PV ? STG_BYTES + 3 * PEND * 4 : 2 * STG_BYTES;  // per warp
+    // PV staging: 32 rows of SROW floats (KNN_EPI_REG) or a swizzled 32x32 chunk
+    static constexpr int STG_PV = KNN_EPI_REG ? 32 * SROW * 4 : STG_BYTES;
+    static constexpr int PEND = PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 128) : 160) : PEND_CAP;
+    static constexpr int SLAB = PV ? STG_PV + 3 * PEND * 4 : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
     static constexpr int NCOLS = PV ? 3 : NCOL;
     static constexpr int THREADS = 64 + 32 * WARPS + 32;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
+    static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : RING_BYTES;
+    static constexpr int SMEM = RING + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
     static_assert(SMEM <= 232448, "shared memory");
     static_assert(SLAB % 16 == 0, "slab alignment");
 };
@@ -208,7 +221,7 @@ enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL
 // frees the accumulator, so the kernel runs at the mainloop's own rate.
 
 template <int METRIC, bool SYM, int MODE, class Sched>
-__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(EpiCfg<MODE>::THREADS, 1)
+__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(EpiCfg<MODE, Sched::kResidentA>::THREADS, 1)
 dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant__ CUtensorMap map_ql,
                const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                const __grid_constant__ CUtensorMap map_d, int use_tma_store, int num_kb,
@@ -220,61 +233,87 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     constexpr bool MINS = MODE == MODE_MINS;
     constexpr bool SAMPLE = MODE == MODE_SAMPLE;
     constexpr int NCOLARR = PIVOT && SYM ? 3 : 2;  // column arrays per tile
-    using E = EpiCfg<MODE>;
+    constexpr bool ARES = Sched::kResidentA;
+    using E = EpiCfg<MODE, ARES>;
     constexpr int NCOL = E::NCOLS;
     constexpr int EPI_WARPS = E::WARPS;
     constexpr int COL_WARP = 2 + EPI_WARPS;
     constexpr int PEND_CAP = E::PEND;
     // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
     constexpr int NSEG = MINS || SAMPLE || PIVOT1 ? 1 : 3;
-    constexpr int KSTAGES = NSEG == 1 ? 2 * STAGES : STAGES;
-    static_assert(KSTAGES * stage_bytes<NSEG>() == STAGES * STAGE_BYTES, "smem layout");
+    constexpr int KSTAGES = ARES ? ARES_KB : ring_stages<NSEG>();
+    static_assert(ARES || KSTAGES * stage_bytes<NSEG>() <= RING_BYTES, "smem layout");
+    static_assert(!ARES || (MODE == MODE_MINS && !SYM), "A-resident mainloop: sample pass only");
     // the single product is orientation-free: no two-pass blocks on the diagonal
     const int64_t ml_shift = SYM || NSEG == 1 ? INT64_MIN : ep.self_shift;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align by pointer arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
-    uint8_t* stg_base = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS] slabs of E::SLAB bytes
+    uint8_t* stg_base = smem + E::RING;  // [EPI_WARPS] slabs of E::SLAB bytes
     float* col_base = reinterpret_cast<float*>(stg_base + EPI_WARPS * E::SLAB);  // [NCOL][3][BN]
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(col_base) + NCOL * COL_BYTES);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * KSTAGES + 4);
     const uint32_t colfull0 = smem_u32(bars + 2 * KSTAGES + 5);
     const uint32_t colempty0 = colfull0 + 8 * NCOL;
+    const uint32_t afull0 = colempty0 + 8 * NCOL, aempty0 = afull0 + 16;  // ARES panel buffers
     const Bars b{smem_u32(bars), smem_u32(bars + KSTAGES), smem_u32(bars + 2 * KSTAGES),
                  smem_u32(bars + 2 * KSTAGES + 2)};
     const uint32_t tfull0 = b.tfull0, tempty0 = b.tempty0;
 
+    // the other partition was chosen on the device: every CTA of the pair leaves before any
+    // barrier, TMEM allocation or cluster synchronisation
+    if (PIVOT && ep.gate >= 0 && ep.flag[1] != ep.gate) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < NCOL; ++i) {
             mbar_init(colfull0 + 8 * i, 1);
             mbar_init(colempty0 + 8 * i, EPI_WARPS);
         }
+        if (ARES)
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(afull0 + 8 * i, 1);
+                mbar_init(aempty0 + 8 * i, 1);
+            }
     }
     const uint32_t tmem_base = setup(bars, KSTAGES, EPI_WARPS, tmem_slot, &map_qh, 1);
     const uint32_t crank = cluster_rank();
     const int64_t cid = blockIdx.x / CLUSTER, ncl = gridDim.x / CLUSTER;
 
     if (warp == 0) {
-        if (lane == 0)
-            producer_loop<KSTAGES, Sched, NSEG>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched,
-                                                num_kb, crank, cid, ncl, ml_shift);
+        if (lane == 0) {
+            if constexpr (ARES)
+                producer_loop_ares<KSTAGES>(&map_qh, &map_xh, stage_base, stage_base + 2 * ARES_PANEL, b, afull0,
+                                            aempty0, sched, num_kb, crank, cid, ncl);
+            else
+                producer_loop<KSTAGES, Sched, NSEG>(&map_qh, &map_ql, &map_xh, &map_xl, stage_base, b, sched,
+                                                    num_kb, crank, cid, ncl, ml_shift);
+        }
         __syncwarp();
     } else if (warp == 1) {
+        if (CTA2 && crank != 0) {
+            // the pair's MMAs are issued by the leader CTA only
+        } else if constexpr (ARES) {
+            if (lane == 0)
+                mma_loop_ares<KSTAGES>(stage_base, stage_base + 2 * ARES_PANEL, b, afull0, aempty0, sched, num_kb,
+                                       tmem_base, cid, ncl);
+        } else {
 #ifdef KNN_MMA_CONVERGED
         mma_loop<KSTAGES, Sched, NSEG>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
 #else
         if (lane == 0)
             mma_loop<KSTAGES, Sched, NSEG>(stage_base, b, sched, num_kb, tmem_base, cid, ncl, ml_shift);
 #endif
+        }
         __syncwarp();
     } else if (warp == COL_WARP) {
         // ------------------------------------------- column data of each work item --
         if (lane == 0) {
             int it = 0;
             for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
-                const tc::Unit w = sched.unit(cur);
+                const tc::Unit wu = sched.unit(cur);
+                for (int64_t nbu = wu.nb0; nbu < wu.nb1; ++nbu) {  // (one tile per unit but PanelSched)
+                const tc::Unit w{wu.mp, nbu, nbu + 1};
                 const int cls = tile_class(w.mp, w.nb0, ml_shift);
                 const int64_t n0 = w.nb0 * BN;
                 for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
@@ -290,6 +329,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     bulk_load(dst + BN * 4, ep.x_rs + n0, BN * 4, fb);
                     if (PIVOT && SYM) bulk_load(dst + 2 * BN * 4, ep.thr + n0, BN * 4, fb);
                 }
+                }
             }
         }
         __syncwarp();
@@ -303,7 +343,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
         // PIVOT: the warp's pending-candidate list lives in its second staging buffer
-        uint32_t* prow = reinterpret_cast<uint32_t*>(slab + STG_BYTES);
+        uint32_t* prow = reinterpret_cast<uint32_t*>(slab + E::STG_PV);
         uint32_t* pcol = prow + PEND_CAP;
         uint32_t* pkey = pcol + PEND_CAP;
         int pend_n = 0;  // warp-uniform
@@ -313,7 +353,9 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         if (PIVOT && lane == 0) s_pend[warp - 2] = 0;
         __syncwarp();
         for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++wi) {
-            const tc::Unit w = sched.unit(cur);
+            const tc::Unit wu = sched.unit(cur);
+            for (int64_t nbu = wu.nb0; nbu < wu.nb1; ++nbu) {  // (one tile per unit but PanelSched)
+            const tc::Unit w{wu.mp, nbu, nbu + 1};
             const int cls = tile_class(w.mp, w.nb0, ml_shift);
             // this warp's chunks of the tile (3 warps per quadrant: 3/3/2, the short share
             // rotating per work item so that a warp can run ahead into the other accumulator)
@@ -359,7 +401,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 if (ch == nch - 1) {
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                    if (lane == 0) {
+                        if constexpr (CTA2)
+                            mbar_arrive_leader(tempty0 + 8 * buf);  // the leader's MMA waits for both CTAs
+                        else
+                            mbar_arrive(tempty0 + 8 * buf);
+                    }
                 }
                 if constexpr (MODE == MODE_NULL) {
                     asm volatile("" ::"r"(r[0]), "r"(r[31]));  // keep the TMEM load
@@ -546,6 +593,70 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         continue;
                     }
                     if (!__any_sync(0xFFFFFFFFu, hm != 0)) continue;
+#if KNN_EPI_REG
+                    // each lane's slots in the warp's pending list from a warp prefix sum of
+                    // the lanes' counts (no shared atomic on one counter, which serialises
+                    // the ~10 lanes holding survivors); survivor values staged by the lanes that
+                    // have some, rows padded to 36 floats (conflict-free 16-byte stores at
+                    // immediate offsets, no swizzle arithmetic), then read back by index
+                    const int mine = __popc(hr) + __popc(hc);
+                    int incl = mine;
+                    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    float* srow = reinterpret_cast<float*>(slab) + lane * SROW;
+                    if (hm) {
+                        #pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            *reinterpret_cast<float4*>(srow + 4 * u) =
+                                make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                    }
+                    if (ep.dbg & 16) {  // DIAGNOSTIC: tests, slot scan and staging only
+                        __syncwarp();
+                        continue;
+                    }
+                    if (pend_n + total > PEND_CAP) {
+                        if (!(ep.dbg & 8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
+                        pend_n = 0;
+                    }
+                    uint32_t h = hm;
+                    if (total <= PEND_CAP) {
+                        int pos = pend_n + incl - mine;
+                        while (h) {
+                            const int c = __ffs(h) - 1;
+                            h &= h - 1;
+                            const float x = srow[c];
+                            const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
+                            if ((hr >> c) & 1) {
+                                prow[pos] = (uint32_t)row;
+                                pcol[pos] = (uint32_t)(c0 + c);
+                                pkey[pos] = key;
+                                ++pos;
+                            }
+                            if (SYM && ((hc >> c) & 1)) {
+                                prow[pos] = (uint32_t)(c0 + c);
+                                pcol[pos] = (uint32_t)row;
+                                pkey[pos] = key;
+                                ++pos;
+                            }
+                        }
+                        pend_n += total;
+                    } else {  // more survivors than the list holds (adversarial ties): direct
+                        while (h) {
+                            const int c = __ffs(h) - 1;
+                            h &= h - 1;
+                            const float x = srow[c];
+                            const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
+                            if ((hr >> c) & 1) pivot_append(ep, row, key, (uint32_t)(c0 + c));
+                            if (SYM && ((hc >> c) & 1)) pivot_append(ep, c0 + c, key, (uint32_t)row);
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+#else
                     // stage the chunk's values (swizzled) so that each lane can walk its own
                     // survivors with dynamic indices.  Only lanes with survivors store (a lane
                     // reads back only its own row): ~5 of 32 lanes, so each store is about one
@@ -612,6 +723,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     }
                     __syncwarp();
                     continue;
+#endif
                 }
                 if constexpr (SYM) {
                     // chunk rows [row0, +32) x cols [c0, +32), both global.  Below the
@@ -701,6 +813,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             // this work item's column data fully read
             __syncwarp();
             if (lane == 0) mbar_arrive(colempty0 + 8 * slot);
+        }
         }
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
@@ -860,7 +973,31 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
     if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
                nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns, xmax};
-    TileSched sched{ceil_div(ceil_div(op.M, BM), 2), ns, nfull / ns};
+    const int64_t n_mp = ceil_div(ceil_div(op.M, BM), 2);
+    static const bool ares_env = [] {
+        const char* v = getenv("KNN_MINS_RESIDENT");  // 0: stream A with every tile (round 1)
+        return !(v && atoi(v) == 0);
+    }();
+    if (ares_env && nfull == ns && op.d_pad <= 256) {
+        // A-panel-resident: units of `run` column blocks per row-block pair, run chosen so
+        // that the units spread evenly over the clusters (>= 8 units per cluster)
+        const int64_t ncl = num_sms / CLUSTER;
+        int64_t run = ns;
+        while (run > 2 && n_mp * ceil_div(ns, run) < 8 * ncl) run = ceil_div(run, 2);
+        PanelSched sched{n_mp, ns, run};
+        const int64_t units = n_mp * ceil_div(ns, run);
+        const int64_t pairs = units < ncl ? units : ncl;
+        auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_MINS, PanelSched>
+                    : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_MINS, PanelSched>
+                                               : dist_tc_kernel<0, false, MODE_MINS, PanelSched>;
+        constexpr int smem = EpiCfg<MODE_MINS, true>::SMEM;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)(pairs * CLUSTER), THREADS, smem, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK, sched,
+                                                               ep);
+        return cudaGetLastError();
+    }
+    TileSched sched{n_mp, ns, nfull / ns};
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
@@ -905,7 +1042,8 @@ template <int MODE>
 cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                               const float* thr, int32_t* cnt, uint64_t* cent,
                               int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                              int64_t unit_lo, int64_t unit_hi, float margin, bool col_major = false) {
+                              int64_t unit_lo, int64_t unit_hi, float margin, bool col_major = false,
+                              int32_t gate = -1) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     if (sym && op.M != op.N) return cudaErrorInvalidValue;
     CUtensorMap mqh, mql, mxh, mxl, md;
@@ -917,6 +1055,7 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
         return cudaErrorInvalidValue;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, sym ? 0 : self_shift, nullptr, 0,
                thr, cnt, cent, cap, flag, margin};
+    ep.gate = gate;
     if (const char* dv = getenv("KNN_DBG_EPI")) ep.dbg = atoi(dv);
     cudaError_t e;
     if (sym) {
@@ -951,9 +1090,9 @@ cudaError_t launch_pivot_impl(const TcOperands& op, int32_t metric, int64_t self
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                                 int64_t unit_lo, int64_t unit_hi, bool col_major) {
+                                 int64_t unit_lo, int64_t unit_hi, bool col_major, int32_t gate) {
     return launch_pivot_impl<MODE_PIVOT>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag, num_sms,
-                                         s, unit_lo, unit_hi, 0.0f, col_major);
+                                         s, unit_lo, unit_hi, 0.0f, col_major, gate);
 }
 
 float pivot1_margin(int32_t d_pad) {
@@ -966,10 +1105,10 @@ float pivot1_margin(int32_t d_pad) {
 
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
-                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s) {
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate) {
     if (metric_kind(metric) == 2) return cudaErrorInvalidValue;  // L2 metrics only
     return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag,
-                                          num_sms, s, -1, -1, pivot1_margin(op.d_pad));
+                                          num_sms, s, -1, -1, pivot1_margin(op.d_pad), false, gate);
 }
 
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s) {

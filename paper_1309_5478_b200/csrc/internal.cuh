@@ -77,7 +77,8 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                  const float* thr, int32_t* cnt, uint64_t* cent,
                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s,
-                                 int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false);
+                                 int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false,
+                                 int32_t gate = -1);
 // The same partition from the single hi.hi product (L2 metrics): kept iff the lower bound
 // L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); the key is L.
 // F = pivot1_margin(d_pad) bounds |u_hh - D| / (||q||^2 + ||x||^2) for the exact D.
@@ -86,7 +87,12 @@ cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f,
 float pivot1_margin(int32_t d_pad);
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
-                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s);
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate = -1);
+// Device-side choice of the pivot plan's partition: flag[1] = 1 (single
+// product + re-evaluation) iff the single-product bound is narrow against the pivots,
+// 2 F (mean ||q||^2 + mean ||x||^2) <= ratio * mean(finite pivots), else 0 (3 products).
+cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, const float* xn, int64_t N,
+                                 float F, float ratio, int32_t* flag, cudaStream_t s);
 // Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31
@@ -106,9 +112,12 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
 // tiles of pivots; pad_end must not pass the caller's allocation (absolute limit).
 cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M, int64_t pad_end, int32_t k,
                                    int32_t metric, float* thr, int32_t* cnt, cudaStream_t s);
+// gate >= 0: the kernel runs only if flag[1] == gate (the device-side plan choice of
+// launch_pivot1_decide; both partitions and both candidate selects are queued, one runs).
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint64_t* cent,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
-                                    int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s);
+                                    int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s,
+                                    int32_t gate = -1);
 // k > 32 pivot plan: per-row pivot with >= r of the S sampled upper bounds at or below it;
 // exact select over the partition's candidate lists (CTA per row; flag |= 2 on a failed
 // certificate or an overflowed list).
@@ -122,7 +131,7 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
                                        const float* X, int32_t d, const float* qn, const float* xn,
                                        const float* thr, float margin, int32_t metric, int32_t* out_idx,
-                                       float* out_dist, int32_t* flag, cudaStream_t s);
+                                       float* out_dist, int32_t* flag, cudaStream_t s, int32_t gate = -1);
 // redo: M + 1 int32 of workspace for the warp-per-row form (null: CTA per row only).
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint64_t* cent,
                                           int32_t cap, int64_t M, int32_t k, int64_t idx_offset,

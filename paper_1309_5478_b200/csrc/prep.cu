@@ -224,6 +224,58 @@ __global__ void scale_kernel(const float* __restrict__ src, float* __restrict__ 
 }
 }  // namespace
 
+namespace {
+// One CTA: sums of the row norms, the column norms and the finite pivots (double), then the
+// decision.  (~65 k rows: a few microseconds.)
+__global__ void __launch_bounds__(1024) pivot1_decide_kernel(const float* __restrict__ thr,
+                                                            const float* __restrict__ qn, int64_t M,
+                                                            const float* __restrict__ xn, int64_t N, float F,
+                                                            float ratio, int32_t* __restrict__ flag) {
+    __shared__ double red[3][32];
+    double sq = 0.0, sx = 0.0, st = 0.0;
+    int64_t nt = 0;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+        sq += qn[i];
+        const float t = thr[i];
+        if (isfinite(t)) {
+            st += t;
+            ++nt;
+        }
+    }
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) sx += xn[j];
+    double v[3] = {sq, sx, st + (double)nt * 1e-300};
+    #pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(0xFFFFFFFFu, v[a], o);
+        if ((threadIdx.x & 31) == 0) red[a][threadIdx.x >> 5] = v[a];
+    }
+    // finite-pivot count through the same reduction (as a double)
+    __shared__ double rcnt[32];
+    double c = (double)nt;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0) rcnt[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0, t = 0, n = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += red[0][w];
+            b += red[1][w];
+            t += red[2][w];
+            n += rcnt[w];
+        }
+        const double width = 2.0 * (double)F * (a / (double)M + b / (double)N);
+        flag[1] = (n > 0 && width <= (double)ratio * (t / n)) ? 1 : 0;
+    }
+}
+}  // namespace
+
+cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, const float* xn, int64_t N,
+                                 float F, float ratio, int32_t* flag, cudaStream_t s) {
+    if (M == 0 || N == 0) return cudaSuccess;
+    pivot1_decide_kernel<<<1, 1024, 0, s>>>(thr, qn, M, xn, N, F, ratio, flag);
+    return cudaGetLastError();
+}
+
 // dst = f * src (the single-product partition's scaled norms; n includes the zero padding)
 cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

@@ -37,7 +37,11 @@ struct knn_ctx {
     bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
     int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
     int32_t pivot_div = 8;     // sample = the first N / pivot_div corpus points
-    bool pivot1 = false;       // k <= 32, L2: single-product partition + re-evaluation (env KNN_PIVOT1=1)
+    // k <= 32, L2 metrics: single-product partition + re-evaluation: -1 chosen
+    // on the device per call (default), 1 always (env KNN_PIVOT1=1), 0 never (KNN_PIVOT1=0)
+    int pivot1 = -1;
+    bool last_plan_auto1 = false;
+    float pivot1_ratio = 0.02f;  // pivot1_decide: largest bound width / mean pivot (env KNN_PIVOT1_RATIO)  // the last pivot-plan call let the device choose (finish_blocking reads it)
     float pivot_margin = __builtin_nanf("");  // KNN_PIVOT_MARGIN: override of the sample's error margin
     int64_t pivot_redos = 0;   // calls redone with the full matrix after an overflow
     int last_plan = -1;

@@ -2048,7 +2048,8 @@ __global__ void __launch_bounds__(256)
 candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
                         int cap, int64_t M, int k,
                         int64_t idx_offset, int32_t* __restrict__ out_idx,
-                        float* __restrict__ out_dist, int32_t* __restrict__ flag) {
+                        float* __restrict__ out_dist, int32_t* __restrict__ flag, int gate) {
+    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
     __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
     __shared__ uint32_t hist[8][256], skey[8][64], sidx[8][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2227,7 +2228,8 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
                            const float* __restrict__ qn, const float* __restrict__ xn,
                            const float* __restrict__ thr, float margin, float rerr, int metric, int vec,
                            int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
-                           int32_t* __restrict__ flag) {
+                           int32_t* __restrict__ flag, int gate) {
+    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
     __shared__ uint32_t heads[8][CS_PER][33];
     __shared__ uint32_t rlist[8][CR_RCAP];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -3171,11 +3173,12 @@ cudaError_t launch_pivot_from_mins(const float* mins, int64_t nchunk, int64_t M,
 
 cudaError_t launch_candidate_select(const int32_t* cnt, const uint64_t* cent,
                                     int32_t cap, int64_t M, int32_t k, int64_t idx_offset,
-                                    int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s) {
+                                    int32_t* out_idx, float* out_dist, int32_t* flag, cudaStream_t s,
+                                    int32_t gate) {
     if (M == 0) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
     candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset,
-                                                                    out_idx, out_dist, flag);
+                                                                    out_idx, out_dist, flag, gate);
     return cudaGetLastError();
 }
 
@@ -3295,7 +3298,7 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
                                        const float* X, int32_t d, const float* qn, const float* xn,
                                        const float* thr, float margin, int32_t metric, int32_t* out_idx,
-                                       float* out_dist, int32_t* flag, cudaStream_t s) {
+                                       float* out_dist, int32_t* flag, cudaStream_t s, int32_t gate) {
     if (M == 0) return cudaSuccess;
     if (k < 1 || k > 32 || metric < 0 || metric > 1) return cudaErrorInvalidValue;
     // relative error bound of the fp32 re-evaluation: d/32 sequential fmas per lane, a
@@ -3305,7 +3308,7 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                     (getenv_flag("KNN_RECOMP_STATS") ? 2 : 0);
     candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset, Q,
                                                                        X, d, qn, xn, thr, margin, rerr, metric, vec,
-                                                                       out_idx, out_dist, flag);
+                                                                       out_idx, out_dist, flag, gate);
     return cudaGetLastError();
 }
 

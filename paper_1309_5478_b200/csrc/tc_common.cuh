@@ -10,6 +10,15 @@
 namespace knn {
 namespace tc {
 
+// KNN_CTA2 (default): the CTA pair runs ONE tcgen05.mma.cta_group::2 of M = 256 (each CTA
+// holds its 128 rows of A and its 128-column half of B, issued by the pair's leader CTA)
+// instead of one M = 128 MMA per CTA over a B operand multicast to both.  Per CTA the tensor
+// core then reads 8 KB of shared memory per 128-cycle MMA instead of 12 KB and the TMA writes
+// a third less — the operand traffic was above the 128 B/clk shared-memory port.
+#ifndef KNN_CTA2
+#define KNN_CTA2 0
+#endif
+constexpr bool CTA2 = KNN_CTA2 != 0;
 constexpr int BM = 128;          // rows per tile (TMEM lanes)
 constexpr int BN = 256;          // columns per tile (TMEM columns per accumulator)
 constexpr int BK = 32;           // fp16 K elements per stage = one 64-byte swizzle row
@@ -17,7 +26,10 @@ constexpr int SWZ = BK * 2;      // swizzle span in bytes (64)
 constexpr int UMMA_K = 16;
 constexpr int A_BYTES = BM * BK * 2;  // one fp16 A tile (8 KB)
 constexpr int B_BYTES = BN * BK * 2;  // one fp16 B tile (16 KB)
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi+lo of both operands (48 KB)
+constexpr int B_TILE = CTA2 ? B_BYTES / 2 : B_BYTES;  // per-CTA bytes of one B tile
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_TILE;  // hi+lo of both operands (32 / 48 KB)
+// the operand region: 3 stages of 48 KB (1-CTA) or 4 of 32 KB (CTA2)
+constexpr int RING_BYTES = CTA2 ? 4 * STAGE_BYTES : 3 * (2 * A_BYTES + 2 * B_BYTES);
 constexpr int TMEM_COLS = 512;   // 2 accumulators x BN fp32 columns
 constexpr int CLUSTER = 2;       // CTA pair along M: the B operand is TMA-multicast to both
 constexpr int GROUP_M = 8;       // tile order: 8 row-block pairs share a column sweep
@@ -25,7 +37,7 @@ constexpr int GROUP_M = 8;       // tile order: 8 row-block pairs share a column
 // Instruction descriptor (PTX ISA, tcgen05 "Instruction descriptor", kind::f16):
 // [4,6) D format = F32 (1); [7,10) A = F16 (0); [10,13) B = F16 (0); bit 15/16 = 0:
 // both K-major; [17,23) N>>3; [24,29) M>>4.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((CTA2 ? 2 * BM : BM) >> 4) << 24);
 
 // Operand tiles are re-read by many tiles: keep them in L2 (evict-last).
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -128,6 +140,37 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
         "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 #endif
+// shared::cluster address of the same shared-memory offset in the pair's leader CTA (rank 0):
+// a CTA's own shared window address carries its rank in bit 24
+__device__ __forceinline__ uint32_t leader_addr(uint32_t a) { return a & 0xFEFFFFFFu; }
+// TMA load into this CTA's shared memory whose completion is counted on the LEADER's
+// mbarrier (cta_group::2: the leader's MMA consumes both CTAs' halves)
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar_leader,
+                                                int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader), "l"(policy_evict_last())
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+// commit the pair's prior cta_group::2 MMAs to the mbarrier at `bar` in both CTAs
+__device__ __forceinline__ void tc_commit2_mc(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(bar), "h"((uint16_t)0x3) : "memory");
+}
+// arrive on the leader CTA's copy of a barrier (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar)) : "memory");
+}
+
 // Shared-memory matrix descriptor, K-major, SWZ-byte swizzle (PTX ISA "Matrix
 // descriptor"): [0,14) start>>4; [16,30) LBO>>4 (unused for swizzled K-major: 1);
 // [32,46) SBO>>4 = 8 rows * SWZ bytes between 8-row core-matrix groups; [46,48)
@@ -169,6 +212,7 @@ struct Unit {
 
 // Materialised GEMM: one tile per unit, groups of GROUP_M pairs sweep all column blocks.
 struct TileSched {
+    static constexpr bool kResidentA = false;
     int64_t n_mp, n_nb;
     int64_t nb_stride = 1;  // column block nb of the schedule is block nb * nb_stride of the matrix
     __device__ __forceinline__ int64_t units() const { return n_mp * n_nb; }
@@ -218,6 +262,7 @@ struct TileSched {
 // turn, so every B block is used by up to gm row blocks while it is L2-resident (operand
 // sets larger than L2: C4 / C5 re-read B from HBM for every triangle row otherwise).
 struct SymSched {
+    static constexpr bool kResidentA = false;
     int64_t n;  // pair blocks per side
     // units [u_lo, u_hi) of the triangle only (the multi-GPU symmetric k-NNG splits it)
     int64_t u_lo = 0, u_hi = INT64_MAX;
@@ -316,6 +361,7 @@ struct SymSched {
 // Fused GEMM+select: a unit is a row-block pair against one of S column splits; units of
 // the same split are consecutive so concurrent clusters sweep the same B panel.
 struct SplitSched {
+    static constexpr bool kResidentA = false;
     int64_t n_mp, n_nb, S, per;  // per = column blocks per split
     __device__ __forceinline__ int64_t units() const { return n_mp * S; }
     __device__ __forceinline__ Unit get(int64_t u) const {
@@ -331,6 +377,30 @@ struct SplitSched {
     __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
     __device__ __forceinline__ void next(Cur& c, int64_t step) const { c.t += step; }
     __device__ __forceinline__ Unit unit(const Cur& c) const { return get(c.t); }
+};
+
+// A-panel-resident GEMM (the single-product sample pass, d_pad <= 256): a unit is a row-block
+// pair against a RUN of `run` consecutive column blocks; each CTA loads its 128-row A panel
+// (all of K) once per unit into one of two panel buffers and streams only the B tiles, so
+// the operand traffic from L2 per tile halves (A was re-read for every tile).  Units are
+// mp-major: consecutive units (concurrent clusters) cover a few row-block pairs and every run.
+struct PanelSched {
+    static constexpr bool kResidentA = true;
+    int64_t n_mp, n_nb, run;  // (column blocks are matrix blocks: no sampling stride)
+    __device__ __forceinline__ int64_t nruns() const { return (n_nb + run - 1) / run; }
+    __device__ __forceinline__ int64_t units() const { return n_mp * nruns(); }
+    struct Cur {
+        int64_t t;
+    };
+    __device__ __forceinline__ Cur first(int64_t t) const { return {t}; }
+    __device__ __forceinline__ bool valid(const Cur& c) const { return c.t < units(); }
+    __device__ __forceinline__ void next(Cur& c, int64_t step) const { c.t += step; }
+    __device__ __forceinline__ Unit unit(const Cur& c) const {
+        const int64_t nr = nruns();
+        const int64_t mp = c.t / nr, r = c.t - mp * nr;
+        const int64_t nb0 = r * run, nb1 = nb0 + run < n_nb ? nb0 + run : n_nb;
+        return {mp, nb0, nb1};
+    }
 };
 
 // ------------------------------------------------------------------ orientation -------
@@ -368,7 +438,9 @@ struct Bars {
 // the xh/xl rows multicast to both CTAs of the pair.  NSEG = 1 (the single hi.hi product of
 // the approximate pivot sample pass) loads only qh and xh: stage = [qh | xh].
 template <int NSEG>
-constexpr int stage_bytes() { return NSEG == 3 ? STAGE_BYTES : A_BYTES + B_BYTES; }
+constexpr int stage_bytes() { return NSEG == 3 ? STAGE_BYTES : A_BYTES + B_TILE; }
+template <int NSEG>
+constexpr int ring_stages() { return RING_BYTES / stage_bytes<NSEG>(); }
 template <int STAGES, class Sched, int NSEG = 3>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const CUtensorMap* map_ql,
                                               const CUtensorMap* map_xh, const CUtensorMap* map_xl,
@@ -386,8 +458,28 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* map_qh, const C
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(b.empty0 + 8 * stage, phase ^ 1);
                 const uint32_t fb = b.full0 + 8 * stage;
-                mbar_expect_tx(fb, stage_bytes<NSEG>());
                 const uint32_t sb = smem_u32(stage_base + (size_t)stage * stage_bytes<NSEG>());
+                if constexpr (CTA2) {
+                    // own A rows and own B half into own shared memory, completion counted on
+                    // the leader's barrier (the leader expects both CTAs' bytes)
+                    if (crank == 0) mbar_expect_tx(fb, 2 * stage_bytes<NSEG>());
+                    const uint32_t fl = leader_addr(fb);
+                    if (NSEG == 3) {
+                        tma_load_2d_2sm(sb, map_qh, fl, kb * BK, row_a);
+                        tma_load_2d_2sm(sb + A_BYTES, map_ql, fl, kb * BK, row_a);
+                        tma_load_2d_2sm(sb + 2 * A_BYTES, map_xh, fl, kb * BK, row_b);
+                        tma_load_2d_2sm(sb + 2 * A_BYTES + B_TILE, map_xl, fl, kb * BK, row_b);
+                    } else {
+                        tma_load_2d_2sm(sb, map_qh, fl, kb * BK, row_a);
+                        tma_load_2d_2sm(sb + A_BYTES, map_xh, fl, kb * BK, row_b);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+                }
+                mbar_expect_tx(fb, stage_bytes<NSEG>());
                 const uint32_t boff = crank * (B_BYTES / 2);
                 if (NSEG == 3) {
                     tma_load_2d(sb, map_qh, fb, kb * BK, row_a);
@@ -432,7 +524,7 @@ __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, con
                 tc_fence_after();
                 const uint32_t sb = smem_u32(stage_base + (size_t)stage * stage_bytes<NSEG>());
                 const uint32_t qh = sb, ql = sb + A_BYTES, xh = sb + (NSEG == 3 ? 2 * A_BYTES : A_BYTES),
-                               xl = sb + 2 * A_BYTES + B_BYTES;
+                               xl = sb + 2 * A_BYTES + B_TILE;
                 // O1: ql.xh, qh.xl, qh.xh   O2: qh.xl, ql.xh, qh.xh  (smallest terms first);
                 // NSEG = 1: qh.xh only
                 const uint32_t sa[3] = {NSEG == 1 ? qh : o2 ? qh : ql, o2 ? ql : qh, qh};
@@ -442,18 +534,126 @@ __device__ __forceinline__ void mma_loop(uint8_t* stage_base, const Bars& b, con
                     #pragma unroll
                     for (int kk = 0; kk < BK / UMMA_K; ++kk) {
                         const uint32_t acc = (kb | seg | kk) != 0;
-                        tc_mma(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2), sdesc(sbx[seg] + kk * UMMA_K * 2),
-                               acc);
+                        if constexpr (CTA2)
+                            tc_mma2(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2), sdesc(sbx[seg] + kk * UMMA_K * 2), acc);
+                        else
+                            tc_mma(tmem_d, sdesc(sa[seg] + kk * UMMA_K * 2), sdesc(sbx[seg] + kk * UMMA_K * 2),
+                                   acc);
                     }
                 }
-                tc_commit_mc(b.empty0 + 8 * stage, 0x3);  // stage free in both CTAs
+                if constexpr (CTA2)
+                    tc_commit2_mc(b.empty0 + 8 * stage);  // stage free in both CTAs
+                else
+                    tc_commit_mc(b.empty0 + 8 * stage, 0x3);  // stage free in both CTAs
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            tc_commit(b.tfull0 + 8 * buf);  // accumulator ready for the epilogue
+            if constexpr (CTA2)
+                tc_commit2_mc(b.tfull0 + 8 * buf);  // both CTAs' accumulators ready
+            else
+                tc_commit(b.tfull0 + 8 * buf);  // accumulator ready for the epilogue
         }
+    }
+}
+
+// A-resident mainloop (PanelSched, single product qh.xh): per unit the CTA's A panel
+// (num_kb tiles of BM x BK) lands in panel buffer (unit & 1) on afull[buf]; B tiles stream
+// through a KB-stage ring (the B halves multicast to both CTAs, as above).  The MMA warp
+// releases a panel buffer by committing aempty[buf] after the unit's last MMA.
+template <int KB, class Sched>
+__device__ __forceinline__ void producer_loop_ares(const CUtensorMap* map_qh, const CUtensorMap* map_xh,
+                                                   uint8_t* abase, uint8_t* bbase, const Bars& b,
+                                                   uint32_t afull0, uint32_t aempty0, const Sched& sched,
+                                                   int num_kb, uint32_t crank, int64_t cid, int64_t ncl) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int ui = 0;
+    for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++ui) {
+        const Unit w = sched.unit(cur);
+        const int row_a = (int)((2 * w.mp + crank) * BM);
+        const int ab = ui & 1;
+        mbar_wait(aempty0 + 8 * ab, ((ui >> 1) & 1) ^ 1);
+        const uint32_t pa = smem_u32(abase + (size_t)ab * num_kb * A_BYTES);
+        if constexpr (CTA2) {
+            if (crank == 0) mbar_expect_tx(afull0 + 8 * ab, (uint32_t)(2 * num_kb * A_BYTES));
+            for (int kb = 0; kb < num_kb; ++kb)
+                tma_load_2d_2sm(pa + kb * A_BYTES, map_qh, leader_addr(afull0 + 8 * ab), kb * BK, row_a);
+        } else {
+            mbar_expect_tx(afull0 + 8 * ab, (uint32_t)(num_kb * A_BYTES));
+            for (int kb = 0; kb < num_kb; ++kb)
+                tma_load_2d(pa + kb * A_BYTES, map_qh, afull0 + 8 * ab, kb * BK, row_a);
+        }
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb) {
+            const int row_b = (int)(nb * BN + crank * (BN / 2));
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(b.empty0 + 8 * stage, phase ^ 1);
+                const uint32_t fb = b.full0 + 8 * stage;
+                if constexpr (CTA2) {
+                    if (crank == 0) mbar_expect_tx(fb, 2 * B_TILE);
+                    tma_load_2d_2sm(smem_u32(bbase + (size_t)stage * B_TILE), map_xh, leader_addr(fb), kb * BK, row_b);
+                } else {
+                    mbar_expect_tx(fb, B_BYTES);
+                    tma_load_2d_mc(smem_u32(bbase + (size_t)stage * B_BYTES) + crank * (B_BYTES / 2), map_xh, fb,
+                                   kb * BK, row_b, 0x3);
+                }
+                if (++stage == KB) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+}
+template <int KB, class Sched>
+__device__ __forceinline__ void mma_loop_ares(uint8_t* abase, uint8_t* bbase, const Bars& b, uint32_t afull0,
+                                              uint32_t aempty0, const Sched& sched, int num_kb, uint32_t tmem_base,
+                                              int64_t cid, int64_t ncl) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, ui = 0;
+    for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++ui) {
+        const Unit w = sched.unit(cur);
+        const int ab = ui & 1;
+        mbar_wait(afull0 + 8 * ab, (ui >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(abase + (size_t)ab * num_kb * A_BYTES);
+        for (int64_t nb = w.nb0; nb < w.nb1; ++nb, ++it) {
+            const int buf = it & 1;
+            mbar_wait(b.tempty0 + 8 * buf, ((it >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + buf * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(b.full0 + 8 * stage, phase);
+                tc_fence_after();
+                const uint32_t sa = pa + kb * A_BYTES;
+                const uint32_t sb = smem_u32(bbase + (size_t)stage * B_TILE);
+                #pragma unroll
+                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                    if constexpr (CTA2)
+                        tc_mma2(tmem_d, sdesc(sa + kk * UMMA_K * 2), sdesc(sb + kk * UMMA_K * 2), (kb | kk) != 0);
+                    else
+                        tc_mma(tmem_d, sdesc(sa + kk * UMMA_K * 2), sdesc(sb + kk * UMMA_K * 2), (kb | kk) != 0);
+                }
+                if constexpr (CTA2)
+                    tc_commit2_mc(b.empty0 + 8 * stage);
+                else
+                    tc_commit_mc(b.empty0 + 8 * stage, 0x3);  // stage free in both CTAs
+                if (++stage == KB) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if constexpr (CTA2)
+                tc_commit2_mc(b.tfull0 + 8 * buf);
+            else
+                tc_commit(b.tfull0 + 8 * buf);  // accumulator ready for the epilogue
+        }
+        if constexpr (CTA2)
+            tc_commit2_mc(aempty0 + 8 * ab);  // the unit's MMAs done: both panel buffers free
+        else
+            tc_commit(aempty0 + 8 * ab);  // the unit's MMAs done: panel buffer free
     }
 }
 
@@ -466,21 +666,31 @@ __device__ __forceinline__ uint32_t setup(uint64_t* bars, int stages, int epi_wa
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, CLUSTER);  // both CTAs' MMAs must release a stage
+            // CTA2: the leader's MMA commit releases the stage in both CTAs; else both CTAs'
+            // own MMAs must release it (the B halves are multicast)
+            mbar_init(empty0 + 8 * s, CTA2 ? 1 : CLUSTER);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, epi_warps);  // one arrive per epilogue warp
+            // one arrive per epilogue warp (CTA2: of both CTAs, on the leader's barrier)
+            mbar_init(tempty0 + 8 * b, CTA2 ? 2 * epi_warps : epi_warps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < nmaps; ++i)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps + i)));
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CTA2) {  // the same columns in both CTAs (warp 1 of each)
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     cluster_sync_all();  // barriers of both CTAs initialised before any multicast
@@ -493,8 +703,12 @@ __device__ __forceinline__ void teardown(uint32_t tmem_base) {
     cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
     if ((threadIdx.x >> 5) == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(TMEM_COLS));
+        if constexpr (CTA2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS));
     }
 }
 

@@ -36,7 +36,7 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_shard_range", "knn_graph_sharded", "knn_search_sharded", "knn_last_shard_mode"]
 SHARD_QUERY, SHARD_CORPUS, SHARD_SYM = 0, 1, 2
 SHARD_MODES = {"query": SHARD_QUERY, "corpus": SHARD_CORPUS, "sym": SHARD_SYM}
-PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED = 0, 1, 2
+PLAN_AUTO, PLAN_FUSED, PLAN_MATERIALISED, PLAN_PIVOT_EXACT = 0, 1, 2, 3
 KERNELS = {"prep": 0, "gemm": 1, "select": 2, "merge": 3, "fused": 4, "xmerge": 5}
 
 
@@ -478,7 +478,8 @@ def set_plan(plan, device=None):
 
 def last_plan(device=None):
     """0 blocked distances+select, 2 symmetric k-NNG distances+select,
-    3 pivot plan (symmetric), 4 pivot plan (general block)."""
+    3 pivot plan (symmetric), 4 pivot plan (general block), 5 / 6 the pivot plan with the
+    single-product partition and the fp32 re-evaluation (symmetric / general block)."""
     return int(load_library().knn_last_plan(context(device)))
 
 

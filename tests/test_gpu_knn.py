@@ -95,6 +95,19 @@ def run_graph(X, k, metric=0):
     return i.cpu().numpy(), d.cpu().numpy()
 
 
+class exact_plan:
+    """Pivot plan with the FP32-accurate 3-product partition (PLAN_PIVOT_EXACT): bit-identical
+    to the materialised plan and to the sharded / pipelined decompositions.  The automatic
+    plan may instead partition on the single product and re-evaluate the survivors in fp32
+    (DESIGN.md §6.5); it is checked against the oracle."""
+
+    def __enter__(self):
+        knn().set_plan(knn().PLAN_PIVOT_EXACT)
+
+    def __exit__(self, *a):
+        knn().set_plan(knn().PLAN_AUTO)
+
+
 def e2e_check(Q, X, gi, gd, k, rows, graph, metric=0, min_pinned=0.0, chunk=128):
     # L2 is checked in the squared domain; cosine / Pearson on the keys themselves.  Rows
     # are checked in chunks so that the fp64 oracle rows stay small at full size.
@@ -241,10 +254,11 @@ def test_host_pipelined_graph_equals_device(N, d, k, metric, dist):
     # of points, sample of every 8th point, column-major partition launches) when N is a
     # multiple of 2048 (20000 is not: the plain path); the lists equal the device call's
     X = datagen.points(N, d, dist, seed=N + d)
-    ref_i, ref_d = run_graph(X, k, metric)
     pinned_x = torch.from_numpy(X).pin_memory().numpy()
-    hi, hd = knn().search_block_host(pinned_x, pinned_x, k, metric=metric, self_shift=0)
-    assert knn().last_plan() == 3
+    with exact_plan():  # (the pipelined scheme runs the 3-product partition)
+        ref_i, ref_d = run_graph(X, k, metric)
+        hi, hd = knn().search_block_host(pinned_x, pinned_x, k, metric=metric, self_shift=0)
+        assert knn().last_plan() == 3
     assert np.array_equal(hi, ref_i) and np.array_equal(hd.view(np.uint32), ref_d.view(np.uint32))
 
 
@@ -338,8 +352,9 @@ def test_pivot_graph_equals_materialised(N, d, k, metric, dist):
     # tie handling) yet few enough candidates to stay on the pivot plan
     kn = knn()
     X = cuda(datagen.points(N, d, dist, seed=N + d + k))
-    gi, gd = kn.graph(X, k, metric=metric)
-    assert kn.last_plan() == 3, kn.last_plan()
+    with exact_plan():
+        gi, gd = kn.graph(X, k, metric=metric)
+        assert kn.last_plan() == 3, kn.last_plan()
     kn.set_plan(kn.PLAN_MATERIALISED)
     try:
         ri, rd = kn.graph(X, k, metric=metric)
@@ -354,10 +369,11 @@ def test_pivot_search_blocks_equal_materialised():
     kn = knn()
     X = cuda(datagen.points(20000, 48, "gauss", seed=51))
     Q = cuda(datagen.points(3000, 48, "gauss", seed=52))
-    gi, gd = kn.search_block(Q, X, 20)
-    assert kn.last_plan() == 4
-    ai, ad = kn.search_block(X[5000:9000].contiguous(), X, 16, self_shift=5000)
-    assert kn.last_plan() == 4
+    with exact_plan():
+        gi, gd = kn.search_block(Q, X, 20)
+        assert kn.last_plan() == 4
+        ai, ad = kn.search_block(X[5000:9000].contiguous(), X, 16, self_shift=5000)
+        assert kn.last_plan() == 4
     kn.set_plan(kn.PLAN_MATERIALISED)
     try:
         ri, rd = kn.search_block(Q, X, 20)
@@ -410,7 +426,7 @@ def test_pivot_large_sample_multi_slab():
         "knn.set_plan(knn.PLAN_MATERIALISED)\n"
         "ri, rd = knn.graph(X, 24)\n"
         "assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))\n")
-    env = dict(os.environ, KNN_PIVOT_DIV="2")
+    env = dict(os.environ, KNN_PIVOT_DIV="2", KNN_PIVOT1="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.check_call([sys.executable, "-c", code], env=env, cwd=root)
 
@@ -530,8 +546,9 @@ def test_pivot_plans_on_ordered_data(k):
     X = datagen.points(32768, 32, "clusters", seed=71)
     X = np.ascontiguousarray(X[np.argsort(X[:, 0] + 1000 * np.round(X[:, 1]))])
     Xt = cuda(X)
-    gi, gd = kn.graph(Xt, k)
-    assert kn.last_plan() == 3, kn.last_plan()
+    with exact_plan():
+        gi, gd = kn.graph(Xt, k)
+        assert kn.last_plan() == 3, kn.last_plan()
     kn.set_plan(kn.PLAN_MATERIALISED)
     try:
         ri, rd = kn.graph(Xt, k)
@@ -554,10 +571,11 @@ def test_pivot_sample_row_blocks(k):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, timeout=300,
-                   env=dict(os.environ, KNN_D_BUDGET_MB="1"))  # 1 MiB: many sample row blocks
+                   env=dict(os.environ, KNN_D_BUDGET_MB="1", KNN_PIVOT1="0"))  # 1 MiB: many sample row blocks
     bi, bd = torch.load(os.path.join(root, "gpurun_out", "_blk.pt"))
     X = cuda(datagen.points(20000, 32, "gauss", seed=81))
-    gi, gd = knn().graph(X, k)
+    with exact_plan():
+        gi, gd = knn().graph(X, k)
     assert torch.equal(gi.cpu(), bi) and torch.equal(gd.cpu().view(torch.int32), bd.view(torch.int32))
 
 
@@ -608,7 +626,7 @@ def test_pivot1_single_product_partition_vs_oracle(N, d, k, metric, dist, nq, tm
                        check=True, cwd=root, timeout=600, env=dict(os.environ, KNN_PIVOT1="1"),
                        capture_output=True, text=True)
     plan = int(r.stdout.split()[0])
-    assert plan in (3, 4), plan  # clusters (wide bounds): windowed re-evaluation, no fallback
+    assert plan in (5, 6), plan  # clusters (wide bounds): windowed re-evaluation, no fallback
     res = np.load(out)
     gi, gd = res[0].astype(np.int64), res[1].astype(np.float32)
     X = datagen.points(N, d, dist, seed=N + d)
@@ -637,7 +655,8 @@ def test_pivot_plan_zero_vectors_and_duplicates(metric):
     X[::3] = 0.0
     X[1::7] = X[2::7][: len(X[1::7])] if len(X[2::7]) >= len(X[1::7]) else X[1::7]
     Xt = cuda(np.ascontiguousarray(X))
-    gi, gd = kn.graph(Xt, 16, metric=metric)
+    with exact_plan():
+        gi, gd = kn.graph(Xt, 16, metric=metric)
     kn.set_plan(kn.PLAN_MATERIALISED)
     try:
         ri, rd = kn.graph(Xt, 16, metric=metric)
@@ -652,7 +671,7 @@ import sys, numpy as np, torch
 from paper_1309_5478_b200 import knn, datagen
 X = torch.from_numpy(datagen.points(20000, 40, "gauss", seed=95)).cuda()
 gi, gd = knn.search_block(X[5000:9000].contiguous(), X, 16, metric=int(sys.argv[2]), self_shift=5000, idx_offset=7)
-assert knn.last_plan() == 4, knn.last_plan()
+assert knn.last_plan() == 6, knn.last_plan()
 np.save(sys.argv[1], np.stack([gi.cpu().numpy().astype(np.float64), gd.cpu().numpy().astype(np.float64)]))
 """
 
@@ -673,3 +692,57 @@ def test_pivot1_shifted_block_vs_oracle(metric, tmp_path):
     n = oracle.sqnorms(X)
     chk = checks.check_rows(gi[rows - 5000], gd[rows - 5000], D64, n[rows], n, rows, 16, metric=metric, graph=True)
     assert chk["failures"] == [], chk["failures"][:3]
+
+
+# ----------------------------------------------- automatic single-product partition ----
+@pytest.mark.parametrize("N,d,k,metric,dist", [(20000, 64, 32, 0, "uniform"), (18000, 100, 16, 1, "gauss"),
+                                               (16384, 256, 1, 0, "uniform"), (24576, 32, 32, 0, "gauss")])
+def test_auto_plan_single_product_vs_oracle(N, d, k, metric, dist):
+    """The automatic plan on data near the origin: the device chooses the single-product
+    partition (plan 5) and the re-evaluated lists pass the oracle's E2E checks on >= 300
+    rows, including every 256-row block's first and last row."""
+    kn = knn()
+    X = datagen.points(N, d, dist, seed=N + 3 * d + k)
+    gi, gd = kn.graph(cuda(X), k, metric=metric)
+    assert kn.last_plan() == 5, kn.last_plan()
+    e2e_check(X, X, gi.cpu().numpy(), gd.cpu().numpy(), k, _block_rows(N, 100, N + k), True, metric=metric)
+
+
+def test_auto_plan_search_single_product_vs_oracle():
+    kn = knn()
+    X = datagen.points(20000, 48, "uniform", seed=61)
+    Q = datagen.points(2000, 48, "uniform", seed=62)
+    gi, gd = kn.search_block(cuda(Q), cuda(X), 24)
+    assert kn.last_plan() == 6, kn.last_plan()
+    e2e_check(Q, X, gi.cpu().numpy(), gd.cpu().numpy(), 24, np.arange(0, 2000, 7), False)
+
+
+def test_auto_plan_far_from_origin_keeps_exact_partition():
+    """C2 (Gaussian clusters away from the origin): the single-product bound scales with the
+    norms, so the device keeps the FP32-accurate 3-product partition (plan 3), bit-identical
+    to the materialised plan."""
+    kn = knn()
+    cfg = datagen.CONFIGS["C2"]
+    X, _ = datagen.config_inputs(cfg)
+    Xt = cuda(X)
+    gi, gd = kn.graph(Xt, cfg.k)
+    assert kn.last_plan() == 3, kn.last_plan()
+    kn.set_plan(kn.PLAN_MATERIALISED)
+    try:
+        ri, rd = kn.graph(Xt, cfg.k)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_auto_plan_ties_and_zero_vectors_vs_oracle():
+    """Duplicates and zero vectors under the automatic plan (the bound vanishes at zero norm;
+    ties at the k-th are resolved by index in the re-evaluated values)."""
+    kn = knn()
+    X = datagen.points(20000, 24, "gauss", seed=64)
+    X[::97] = 0.0                      # 207 zero vectors: 206 ties at distance 0 each
+    X[1::7] = X[2::7][: len(X[1::7])]  # exact duplicates
+    X = np.ascontiguousarray(X)
+    gi, gd = kn.graph(cuda(X), 16)
+    assert kn.last_plan() == 5, kn.last_plan()
+    e2e_check(X, X, gi.cpu().numpy(), gd.cpu().numpy(), 16, np.arange(0, 20000, 97), True)

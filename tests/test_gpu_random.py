@@ -1,7 +1,9 @@
 """Seeded random sweep over shapes and parameters around the plans' thresholds (pivot
 plans from N = 16384 and M = 256, k = 32 | 33, d around the 64-wide K padding, ragged
-tiles), every metric: the automatic plan must equal the materialised plan bit for bit and
-pass the oracle's E2E checks on sampled rows."""
+tiles), every metric: the pivot plan with the FP32-accurate partition (PLAN_PIVOT_EXACT) must
+equal the materialised plan bit for bit, and the automatic plan (which may partition on the
+single product and re-evaluate the survivors in fp32) and the exact plan
+must both pass the oracle's E2E checks on sampled rows."""
 import numpy as np
 import pytest
 
@@ -46,21 +48,27 @@ def test_random_case(i, graph, M, N, d, k, metric, dist):
             return kn.graph(Xt, k, metric=metric)
         return kn.search_block(Qt, Xt, k, metric=metric)
 
-    gi, gd = run()
-    kn.set_plan(kn.PLAN_MATERIALISED)
+    ai, ad = run()  # automatic plan
     try:
+        kn.set_plan(kn.PLAN_PIVOT_EXACT)
+        gi, gd = run()
+        kn.set_plan(kn.PLAN_MATERIALISED)
         ri, rd = run()
     finally:
         kn.set_plan(kn.PLAN_AUTO)
     assert torch.equal(gi, ri), "plans differ (indices)"
     assert torch.equal(gd.view(torch.int32), rd.view(torch.int32)), "plans differ (distances)"
     rows = np.unique(np.linspace(0, M - 1, 24).astype(np.int64))
-    gi_np, gd_np = gi.cpu().numpy(), gd.cpu().numpy()
     if metric >= 2:
         D64 = oracle.dist_rows(Q, X, rows=rows, metric=metric)
-        res = checks.check_rows(gi_np[rows], gd_np[rows], D64, None, None, rows, k, metric=metric, graph=graph)
     else:
         D64 = oracle.dist_rows(Q, X, rows=rows)  # squared; check_rows maps L2 through sqrt
-        res = checks.check_rows(gi_np[rows], gd_np[rows], D64, oracle.sqnorms(Q)[rows], oracle.sqnorms(X),
-                                rows, k, metric=metric, graph=graph)
-    assert res["failures"] == [], res["failures"][:3]
+    for ii, dd in ((gi, gd), (ai, ad)):
+        gi_np, gd_np = ii.cpu().numpy(), dd.cpu().numpy()
+        if metric >= 2:
+            res = checks.check_rows(gi_np[rows], gd_np[rows], D64, None, None, rows, k, metric=metric,
+                                    graph=graph)
+        else:
+            res = checks.check_rows(gi_np[rows], gd_np[rows], D64, oracle.sqnorms(Q)[rows], oracle.sqnorms(X),
+                                    rows, k, metric=metric, graph=graph)
+        assert res["failures"] == [], res["failures"][:3]

@@ -19,6 +19,16 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _exact_plan():
+    """These tests compare decompositions bit for bit: the one-GPU reference runs the pivot
+    plan with the FP32-accurate partition (the sharded / streamed phases always do)."""
+    from paper_1309_5478_b200 import knn as k
+    k.set_plan(k.PLAN_PIVOT_EXACT)
+    yield
+    k.set_plan(k.PLAN_AUTO)
+
+
 def knn():
     from paper_1309_5478_b200 import knn as k
     return k
@@ -136,6 +146,7 @@ def _worker(rank, world, port, case, q):
     try:
         sharded.init()  # gloo group: the library's host-callback transport
         kn = knn()
+        kn.set_plan(kn.PLAN_PIVOT_EXACT)  # (the Par-1 fallback's blocks: as the reference)
         assert kn.comm_info() == (2, rank, world)
         X = torch.from_numpy(datagen.points(N, d, "gauss", seed=93)).cuda()
         if rank != 0:

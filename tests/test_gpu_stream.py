@@ -16,6 +16,16 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _exact_plan():
+    """These tests compare decompositions bit for bit: the one-GPU reference runs the pivot
+    plan with the FP32-accurate partition (the sharded / streamed phases always do)."""
+    from paper_1309_5478_b200 import knn as k
+    k.set_plan(k.PLAN_PIVOT_EXACT)
+    yield
+    k.set_plan(k.PLAN_AUTO)
+
+
 def knn():
     from paper_1309_5478_b200 import knn as k
     return k
