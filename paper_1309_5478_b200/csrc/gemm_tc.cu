@@ -162,18 +162,24 @@ struct DeferredFlush {
 constexpr int ARES_KB = CTA2 ? 10 : 5;      // B ring stages
 constexpr int ARES_PANEL = 8 * A_BYTES;     // one A panel: BM x 256 fp16
 template <int MODE, bool ARES = false>
+#ifndef KNN_PV1_WARPS
+#define KNN_PV1_WARPS 16  // epilogue warps of the single-product partition (12 or 16)
+#endif
 struct EpiCfg {
     static constexpr bool PV = MODE == 1 || MODE == 5;  // MODE_PIVOT, MODE_PIVOT1
-    static constexpr int WARPS = PV ? 12 : EPI_WARPS;
+    // the single-product partition is bound by its epilogue's latency: 16 warps (4 per TMEM
+    // lane quadrant, 2 chunks each) over a 4-stage operand ring (the MMA is not its limit)
+    static constexpr bool PV16 = MODE == 5 && KNN_PV1_WARPS == 16;
+    static constexpr int WARPS = PV16 ? 16 : PV ? 12 : EPI_WARPS;
     static constexpr int PARTS = WARPS / 4;
     static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
     // PV staging: 32 rows of SROW floats (KNN_EPI_REG) or a swizzled 32x32 chunk
     static constexpr int STG_PV = KNN_EPI_REG ? 32 * SROW * 4 : STG_BYTES;
-    static constexpr int PEND = PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 128) : 160) : PEND_CAP;
+    static constexpr int PEND = PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 128) : 160) : PEND_CAP;
     static constexpr int SLAB = PV ? STG_PV + 3 * PEND * 4 : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
     static constexpr int NCOLS = PV ? 3 : NCOL;
     static constexpr int THREADS = 64 + 32 * WARPS + 32;
-    static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : RING_BYTES;
+    static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : PV16 ? 4 * (A_BYTES + B_TILE) : RING_BYTES;
     static constexpr int SMEM = RING + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
     static_assert(SMEM <= 232448, "shared memory");
     static_assert(SLAB % 16 == 0, "slab alignment");
@@ -241,8 +247,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     constexpr int PEND_CAP = E::PEND;
     // MINS (approximate pivot sample): one hi.hi product per K-block, twice the stages
     constexpr int NSEG = MINS || SAMPLE || PIVOT1 ? 1 : 3;
-    constexpr int KSTAGES = ARES ? ARES_KB : ring_stages<NSEG>();
-    static_assert(ARES || KSTAGES * stage_bytes<NSEG>() <= RING_BYTES, "smem layout");
+    constexpr int KSTAGES = ARES ? ARES_KB : E::RING / stage_bytes<NSEG>();
+    static_assert(ARES || KSTAGES * stage_bytes<NSEG>() <= E::RING, "smem layout");
     static_assert(!ARES || (MODE == MODE_MINS && !SYM), "A-resident mainloop: sample pass only");
     // the single product is orientation-free: no two-pass blocks on the diagonal
     const int64_t ml_shift = SYM || NSEG == 1 ? INT64_MIN : ep.self_shift;
