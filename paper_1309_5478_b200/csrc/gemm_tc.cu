@@ -101,6 +101,13 @@ __device__ __forceinline__ void pivot_append(const EpiArgs& ep, int64_t r, uint3
 // col, key) and flushed to the global per-row lists in batches of up to PEND_CAP, four
 // returning atomics in flight per lane, so their latency is paid once per batch.
 constexpr int PEND_CAP = 320;
+// KNN_DIAG_EPI builds (scripts/epi_cost.py) honour env KNN_DBG_EPI; product builds compile
+// the diagnostic switches out of the epilogue
+#ifdef KNN_DIAG_EPI
+#define EPI_DBG(bit) (ep.dbg & (bit))
+#else
+#define EPI_DBG(bit) 0
+#endif
 #ifndef KNN_EPI_REG
 #define KNN_EPI_REG 1  // survivor slots by warp scan, padded staging rows (1), or round 1's path (0)
 #endif
@@ -162,6 +169,9 @@ struct DeferredFlush {
 constexpr int ARES_KB = CTA2 ? 10 : 5;      // B ring stages
 constexpr int ARES_PANEL = 8 * A_BYTES;     // one A panel: BM x 256 fp16
 template <int MODE, bool ARES = false>
+#ifndef KNN_MINS_WARPS
+#define KNN_MINS_WARPS 8  // epilogue warps of the chunk-minimum sample pass (8 or 16)
+#endif
 #ifndef KNN_PV1_WARPS
 #define KNN_PV1_WARPS 16  // epilogue warps of the single-product partition (12 or 16)
 #endif
@@ -170,14 +180,14 @@ struct EpiCfg {
     // the single-product partition is bound by its epilogue's latency: 16 warps (4 per TMEM
     // lane quadrant, 2 chunks each) over a 4-stage operand ring (the MMA is not its limit)
     static constexpr bool PV16 = MODE == 5 && KNN_PV1_WARPS == 16;
-    static constexpr int WARPS = PV16 ? 16 : PV ? 12 : EPI_WARPS;
+    static constexpr int WARPS = PV16 || (MODE == 2 && KNN_MINS_WARPS == 16) ? 16 : PV ? 12 : EPI_WARPS;
     static constexpr int PARTS = WARPS / 4;
     static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
     // PV staging: 32 rows of SROW floats (KNN_EPI_REG) or a swizzled 32x32 chunk
     static constexpr int STG_PV = KNN_EPI_REG ? 32 * SROW * 4 : STG_BYTES;
     static constexpr int PEND = PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 128) : 160) : PEND_CAP;
     static constexpr int SLAB = PV ? STG_PV + 3 * PEND * 4 : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
-    static constexpr int NCOLS = PV ? 3 : NCOL;
+    static constexpr int NCOLS = PV16 ? 6 : PV ? 3 : NCOL;  // column-data ring slots
     static constexpr int THREADS = 64 + 32 * WARPS + 32;
     static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : PV16 ? 4 * (A_BYTES + B_TILE) : RING_BYTES;
     static constexpr int SMEM = RING + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
@@ -358,6 +368,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         __shared__ int s_pend[EPI_WARPS];  // PIVOT: each warp's pending-list length (slot allocator)
         if (PIVOT && lane == 0) s_pend[warp - 2] = 0;
         __syncwarp();
+        // the row terms of the last work item: consecutive items of a CTA often share the row
+        // block (row-major triangle schedule), so the three loads are skipped then
+        int64_t row_c = -1;
+        float qn_c = 0.0f, cq_c = 0.0f, trow_c = -1.0f;
         for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++wi) {
             const tc::Unit wu = sched.unit(cur);
             for (int64_t nbu = wu.nb0; nbu < wu.nb1; ++nbu) {  // (one tile per unit but PanelSched)
@@ -374,9 +388,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const int64_t row0 = mb * BM + quad * 32;
             const int64_t row = row0 + lane;
             const bool row_ok = row < ep.M;
-            const float qn = row_ok ? __ldg(ep.qn + row) : 0.0f;
-            const float cq = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
-            const float trow = PIVOT && row_ok ? __ldg(ep.thr + row) : -1.0f;  // row pivot
+            if (row != row_c) {
+                row_c = row;
+                qn_c = row_ok ? __ldg(ep.qn + row) : 0.0f;
+                cq_c = row_ok ? -2.0f * __ldg(ep.q_rs + row) : 0.0f;
+                trow_c = PIVOT && row_ok ? __ldg(ep.thr + row) : -1.0f;  // row pivot
+            }
+            const float qn = qn_c, cq = cq_c, trow = trow_c;
             const uint64_t cq2 = f2_pack(cq, cq), qn2 = f2_pack(qn, qn), trow2 = f2_pack(trow, trow);
             // MINS: qn (1 + m) + m XMAX, and the cosine sentinel cap 3 + m (qn + XMAX)
             const float xmx = MINS ? __ldg(ep.xmax) : 0.0f;
@@ -561,7 +579,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     }
                     // this row's survivors in the chunk: row side (hr) and column side (hc)
                     uint32_t hr = 0, hc = 0;
-                    if (ep.dbg & 4) {
+                    if (EPI_DBG(4)) {
                         asm volatile("" ::"f"(v[0]), "f"(v[31]));
                         continue;
                     }
@@ -579,7 +597,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         hr = __funnelshift_l(__float_as_uint(d1), hr, 1);
                         hr = __funnelshift_l(__float_as_uint(d0), hr, 1);
                     }
-                    if (SYM && !(ep.dbg & 1)) {
+                    if (SYM && !EPI_DBG(1)) {
                         const float4* ct4 = reinterpret_cast<const float4*>(col_t + cb);
                         #pragma unroll
                         for (int c4 = 7; c4 >= 0; --c4) {
@@ -594,7 +612,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         }
                     }
                     const uint32_t hm = hr | hc;
-                    if (ep.dbg & 2) {
+                    if (EPI_DBG(2)) {
                         asm volatile("" ::"r"(hm));
                         continue;
                     }
@@ -620,12 +638,12 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             *reinterpret_cast<float4*>(srow + 4 * u) =
                                 make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
                     }
-                    if (ep.dbg & 16) {  // DIAGNOSTIC: tests, slot scan and staging only
+                    if (EPI_DBG(16)) {  // DIAGNOSTIC: tests, slot scan and staging only
                         __syncwarp();
                         continue;
                     }
                     if (pend_n + total > PEND_CAP) {
-                        if (!(ep.dbg & 8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
+                        if (!EPI_DBG(8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
                         pend_n = 0;
                     }
                     uint32_t h = hm;
@@ -676,7 +694,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             sts128(sv + lane * 128 + ((u ^ (lane & 7)) << 4), v[4 * u], v[4 * u + 1],
                                    v[4 * u + 2], v[4 * u + 3]);
                     }
-                    if (ep.dbg & 16) {  // DIAGNOSTIC: staging only
+                    if (EPI_DBG(16)) {  // DIAGNOSTIC: staging only
                         __syncwarp();
                         continue;
                     }
@@ -690,7 +708,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     const int mine = __popc(hr) + __popc(hc);
                     const int total = __reduce_add_sync(0xFFFFFFFFu, mine);
                     if (pend_n + total > PEND_CAP) {
-                        if (!(ep.dbg & 8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
+                        if (!EPI_DBG(8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
                         pend_n = 0;
                         if (lane == 0) s_pend[warp - 2] = 0;
                     }
@@ -999,7 +1017,7 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
         constexpr int smem = EpiCfg<MODE_MINS, true>::SMEM;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        kern<<<(unsigned)(pairs * CLUSTER), THREADS, smem, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK, sched,
+        kern<<<(unsigned)(pairs * CLUSTER), EpiCfg<MODE_MINS, true>::THREADS, smem, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK, sched,
                                                                ep);
         return cudaGetLastError();
     }
@@ -1007,9 +1025,10 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
     const int64_t units = sched.n_mp * sched.n_nb;
     const int64_t pairs = units < num_sms / CLUSTER ? units : num_sms / CLUSTER;
     auto kern = metric_kind(metric) == 1 ? dist_tc_kernel<1, false, MODE_MINS, TileSched> : metric_kind(metric) == 2 ? dist_tc_kernel<2, false, MODE_MINS, TileSched> : dist_tc_kernel<0, false, MODE_MINS, TileSched>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         EpiCfg<MODE_MINS>::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)(pairs * CLUSTER), THREADS, SMEM_BYTES, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
+    kern<<<(unsigned)(pairs * CLUSTER), EpiCfg<MODE_MINS>::THREADS, EpiCfg<MODE_MINS>::SMEM, s>>>(mqh, mql, mxh, mxl, md, 0, op.d_pad / BK,
                                                                 sched, ep);
     return cudaGetLastError();
 }

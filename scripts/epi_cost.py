@@ -1,5 +1,7 @@
 """DIAGNOSTIC: partition GEMM time with parts of its epilogue disabled (KNN_DBG_EPI, set by
-the caller; results are wrong and the call falls back, only the partition launch is read)."""
+the caller, honoured only by a -DKNN_DIAG_EPI build: make BUILD=build_diag LIB=ablibs/diag.so
+NVFLAGS_EXTRA=-DKNN_DIAG_EPI ablibs/diag.so, then KNN_LIB_PATH=ablibs/diag.so); results are
+wrong and the call falls back, only the partition launch is read)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -11,12 +11,13 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
-R = sys.argv[1] if len(sys.argv) > 1 else "r01"
+R = sys.argv[1] if len(sys.argv) > 1 else "r02"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 # report -> the key bench.py looks up
 KEYS = {"partition": "dist_tc_kernel", "sample": "dist_tc_kernel_sample", "pivot": "pivot_from_mins_kernel",
+        "recompute": "candidate_recompute_kernel", "partition3": "dist_tc_kernel_exact",
         "candsel": "candidate_select_kernel", "prep": "prep_kernel",
         # C4 (k = 1024, quantile pivot): keys distinct from the headline's
         "c4_candsel": "candidate_select_warp_kernel", "c4_pivot": "pivot_from_sample_kernel",
@@ -31,7 +32,8 @@ for rep, key in KEYS.items():
     if t:
         traffic[key] = list(t.values())[0]
 traffic["_source"] = (f"ncu --set full --clock-control none, one launch each, headline bench command, "
-                      f"pivot plan (profiles/{R}_ncu_full_summary.txt)")
+                      f"default plan (single-product pivot partition; dist_tc_kernel_exact = the 3-product "
+                      f"partition under KNN_PIVOT1=0) (profiles/{R}_ncu_full_summary.txt)")
 with open(os.path.join(P, f"{R}_ncu_full_summary.txt"), "w") as f:
     f.write("\n".join(summ) + "\n")
 with open(os.path.join(P, "traffic.json"), "w") as f:
