@@ -598,7 +598,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     const char* env = getenv("KNN_HOST_PIPE");
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
     if ((env && strcmp(env, "0") == 0) || !tc || !ctx->pivot_ok || !ctx->sym_ok ||
-        ctx->plan == KNN_PLAN_MATERIALISED || ctx->pivot1 > 0 || k > 32 || N < 16384 || N % 2048 != 0 ||
+        ctx->plan == KNN_PLAN_MATERIALISED || k > 32 || N < 16384 || N % 2048 != 0 ||
         ctx->pivot_div != 8)
         return KNN_ERR_UNSUPPORTED;
     const int64_t S = N / 8;                    // sample: points 8j, j < S (a multiple of 256)
@@ -617,12 +617,19 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         oi = c.take<int32_t>((size_t)N * k);
         od = c.take<float>((size_t)N * k);
     };
+    // the single-product partition (chosen on the device after the first chunk's pivots, or
+    // forced by KNN_PIVOT1=1; L2 metrics, not under KNN_PLAN_PIVOT_EXACT), as in run_block
+    const bool p1_ok = metric <= KNN_L2 && ctx->plan != KNN_PLAN_PIVOT_EXACT && ctx->pivot1 != 0;
+    const bool p1_auto = p1_ok && ctx->pivot1 < 0;
+    const bool one = p1_ok && ctx->pivot1 > 0;
+    const float F = knn::pivot1_margin(d_pad);
     Prepared px{}, smp{};
-    float *D, *smax, *thr;
+    float *D, *smax, *thr, *nsc = nullptr;
     int32_t *flag, *cnt;
     uint64_t* cent;
     auto ws_layout = [&](Carve& c) {
         flag = c.take<int32_t>(4);
+        if (p1_ok) nsc = c.take<float>(round_up(N, knn::kColPad));
         px.sqn = c.take<float>(N);
         px.rs = c.take<float>(N);
         px.hi = c.take<__half>((size_t)N * d_pad);
@@ -686,6 +693,9 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     KNN_CUDA(knn::launch_max_nonneg(smp.sqn, S, smax, s));
     ctx->launches++;
     knn::TcOperands full{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+    knn::TcOperands full1 = full;  // the single-product partition: norms scaled by 1 - F
+    full1.qn = nsc;
+    full1.xn = nsc;
     for (int c = 0; c < nch; ++c) {
         const int64_t c0 = c * CH, R = N - c0 < CH ? N - c0 : CH;
         KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_chunk[c], 0));
@@ -694,6 +704,10 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
             KNN_CUDA(knn::launch_prep(x + c0 * d, R, d, d_pad, px.sqn + c0, px.rs + c0, px.hi + c0 * d_pad,
                                       px.lo + c0 * d_pad, flag, metric, s));
             t.done();
+        }
+        if (p1_ok) {
+            KNN_CUDA(knn::launch_scale_norms(px.sqn + c0, nsc + c0, R, 1.0f - F, s));
+            ctx->launches++;
         }
         knn::TcOperands op{px.hi + c0 * d_pad, px.lo + c0 * d_pad, px.sqn + c0, px.rs + c0, R,
                            smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
@@ -709,19 +723,34 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
                                                  thr + c0, cnt + c0, s));
             tp.done();
         }
+        if (c == 0 && p1_auto) {  // the device's choice, from the first chunk's rows and the sample
+            KNN_CUDA(knn::launch_pivot1_decide(thr, px.sqn, R, smp.sqn, S, F, ctx->pivot1_ratio, flag, s));
+            ctx->launches++;
+        }
         // the triangle's units whose column block lies in this chunk (rows and columns < c0 + R)
         const int64_t b0 = c0 / knn::kColPad, b1 = (c0 + R) / knn::kColPad;  // 256-column blocks
         Timed tf(ctx, KNN_KERNEL_FUSED, s);
-        KNN_CUDA(knn::launch_dist_tc_pivot(full, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
-                                           b0 * (b0 + 1) / 2, b1 * (b1 + 1) / 2, true));
+        if (one || p1_auto)
+            KNN_CUDA(knn::launch_dist_tc_pivot1(full1, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
+                                                p1_auto ? 1 : -1, b0 * (b0 + 1) / 2, b1 * (b1 + 1) / 2, true));
+        if (!one)
+            KNN_CUDA(knn::launch_dist_tc_pivot(full, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
+                                               b0 * (b0 + 1) / 2, b1 * (b1 + 1) / 2, true, p1_auto ? 0 : -1));
+        ctx->launches += p1_auto ? 1 : 0;
         tf.done();
     }
     {
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
-        KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, N, k, 0, oi, od, flag, s));
+        if (one || p1_auto)
+            KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, N, k, 0, x, x, d, px.sqn, px.sqn, thr, F, metric,
+                                                     oi, od, flag, s, p1_auto ? 1 : -1));
+        if (!one)
+            KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, N, k, 0, oi, od, flag, s, p1_auto ? 0 : -1));
+        ctx->launches += p1_auto ? 1 : 0;
         tc2.done();
     }
-    ctx->last_plan = 3;
+    ctx->last_plan = one ? 5 : 3;
+    ctx->last_plan_auto1 = p1_auto;
     knn_status st = finish_blocking(ctx, s);
     if (st == KNN_ERR_INTERNAL) {  // a certificate failed / a list overflowed: the full matrix
         ctx->pivot_redos++;

@@ -1130,10 +1130,11 @@ float pivot1_margin(int32_t d_pad) {
 
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
-                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate) {
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate,
+                                  int64_t unit_lo, int64_t unit_hi, bool col_major) {
     if (metric_kind(metric) == 2) return cudaErrorInvalidValue;  // L2 metrics only
     return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag,
-                                          num_sms, s, -1, -1, pivot1_margin(op.d_pad), false, gate);
+                                          num_sms, s, unit_lo, unit_hi, pivot1_margin(op.d_pad), col_major, gate);
 }
 
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s) {

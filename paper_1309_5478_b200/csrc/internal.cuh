@@ -87,7 +87,8 @@ cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f,
 float pivot1_margin(int32_t d_pad);
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
-                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate = -1);
+                                  int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate = -1,
+                                  int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false);
 // Device-side choice of the pivot plan's partition: flag[1] = 1 (single
 // product + re-evaluation) iff the single-product bound is narrow against the pivots,
 // 2 F (mean ||q||^2 + mean ||x||^2) <= ratio * mean(finite pivots), else 0 (3 products).

@@ -232,18 +232,40 @@ __global__ void __launch_bounds__(1024) pivot1_decide_kernel(const float* __rest
                                                             const float* __restrict__ xn, int64_t N, float F,
                                                             float ratio, int32_t* __restrict__ flag) {
     __shared__ double red[3][32];
-    double sq = 0.0, sx = 0.0, st = 0.0;
-    int64_t nt = 0;
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    // float4 loads with several in flight (the arrays are 16-byte aligned device carves);
+    // fp32 partial sums per thread (<= M / 4096 terms each), then fp64
+    float sq = 0.0f, sx = 0.0f, st = 0.0f;
+    int nt = 0;
+    const int64_t M4 = M / 4, N4 = N / 4;
+    const float4* qn4 = reinterpret_cast<const float4*>(qn);
+    const float4* th4 = reinterpret_cast<const float4*>(thr);
+    const float4* xn4 = reinterpret_cast<const float4*>(xn);
+    #pragma unroll 4
+    for (int64_t i = threadIdx.x; i < M4; i += blockDim.x) {
+        const float4 a = qn4[i], t = th4[i];
+        sq += (a.x + a.y) + (a.z + a.w);
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+        #pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (isfinite(tv[e])) {
+                st += tv[e];
+                ++nt;
+            }
+    }
+    #pragma unroll 4
+    for (int64_t j = threadIdx.x; j < N4; j += blockDim.x) {
+        const float4 b = xn4[j];
+        sx += (b.x + b.y) + (b.z + b.w);
+    }
+    for (int64_t i = 4 * M4 + threadIdx.x; i < M; i += blockDim.x) {
         sq += qn[i];
-        const float t = thr[i];
-        if (isfinite(t)) {
-            st += t;
+        if (isfinite(thr[i])) {
+            st += thr[i];
             ++nt;
         }
     }
-    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) sx += xn[j];
-    double v[3] = {sq, sx, st + (double)nt * 1e-300};
+    for (int64_t j = 4 * N4 + threadIdx.x; j < N; j += blockDim.x) sx += xn[j];
+    double v[3] = {(double)sq, (double)sx, (double)st};
     #pragma unroll
     for (int a = 0; a < 3; ++a) {
         for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(0xFFFFFFFFu, v[a], o);

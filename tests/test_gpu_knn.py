@@ -746,3 +746,19 @@ def test_auto_plan_ties_and_zero_vectors_vs_oracle():
     gi, gd = kn.graph(cuda(X), 16)
     assert kn.last_plan() == 5, kn.last_plan()
     e2e_check(X, X, gi.cpu().numpy(), gd.cpu().numpy(), 16, np.arange(0, 20000, 97), True)
+
+
+@pytest.mark.parametrize("N,d,k,metric", [(16384, 48, 16, 0), (32768, 100, 32, 1)])
+def test_host_pipelined_auto_plan_equals_device(N, d, k, metric):
+    """knn_search_block_host's pipelined k-NNG under the automatic plan: the device picks the
+    single-product partition from the first chunk's pivots; the re-evaluated values are the
+    same fp32 sums as the device call's, so the lists are identical, and they pass the
+    oracle's E2E checks."""
+    X = datagen.points(N, d, "uniform", seed=N + 7 * d)
+    ref_i, ref_d = run_graph(X, k, metric)
+    assert knn().last_plan() == 5, knn().last_plan()
+    pinned_x = torch.from_numpy(X).pin_memory().numpy()
+    hi, hd = knn().search_block_host(pinned_x, pinned_x, k, metric=metric, self_shift=0)
+    assert knn().last_plan() == 5, knn().last_plan()
+    assert np.array_equal(hi, ref_i) and np.array_equal(hd.view(np.uint32), ref_d.view(np.uint32))
+    e2e_check(X, X, hi, hd, k, np.arange(0, N, 131), True, metric=metric)
