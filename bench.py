@@ -405,8 +405,8 @@ def run_ours(args):
     elif s_n:
         sl = max(s_n // args.steps, 1)
         kind, splits = knn.last_select_kernel()
-        kname = {"warp per row": "select_warp_kernel", "cluster per row": "select_cluster_kernel"}.get(
-            kind, "select_ring_kernel")
+        kname = {"warp per row": "select_warp_kernel", "cluster per row": "select_cluster_kernel",
+                 "two-pass warp per row": "select_warp2p_kernel"}.get(kind, "select_ring_kernel")
         rooflines.append((s_ms, hbm_roof(f"{kname} (a-S4, {kind})", kname, s_ms, s_n,
                                          rows_w / sl * (cols_w * 4.0 + k * 8.0))))
     if m_n and pivot_plan:

@@ -2221,7 +2221,13 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
 constexpr int CR_PER = 16;
 constexpr int CR_RCAP = 256;
 constexpr int CR_G = 8;
-__global__ void __launch_bounds__(256, 4)
+#ifndef KNN_CR_ONEHALF
+#define KNN_CR_ONEHALF 1  // one 128-float slice of the candidates at a time (no spills)
+#endif
+#ifndef KNN_CR_MINB
+#define KNN_CR_MINB 4  // CTAs per SM of the re-evaluation (4: 64 registers)
+#endif
+__global__ void __launch_bounds__(256, KNN_CR_MINB)
 candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
                            int cap, int64_t M, int k, int64_t idx_offset,
                            const float* __restrict__ Q, const float* __restrict__ X, int d,
@@ -2332,6 +2338,26 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
             #pragma unroll
             for (int u = 0; u < CR_G; ++u) acc[u] = 0.0f;
             if (vec & 1) {
+#if KNN_CR_ONEHALF
+                // one 128-float slice at a time: CR_G float4 loads in flight per lane (32
+                // registers), no spills at 64 registers; the other warps supply the MLP
+                #pragma unroll 1
+                for (int t = 4 * lane; t < d; t += 128) {
+                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + t));
+                    float4 xv[CR_G];
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) xv[u] = __ldg(reinterpret_cast<const float4*>(xr[u] + t));
+                    #pragma unroll
+                    for (int u = 0; u < CR_G; ++u) {
+                        const float e0 = qv.x - xv[u].x, e1 = qv.y - xv[u].y;
+                        const float e2 = qv.z - xv[u].z, e3 = qv.w - xv[u].w;
+                        acc[u] = fmaf(e0, e0, acc[u]);
+                        acc[u] = fmaf(e1, e1, acc[u]);
+                        acc[u] = fmaf(e2, e2, acc[u]);
+                        acc[u] = fmaf(e3, e3, acc[u]);
+                    }
+                }
+#else
                 for (int t = 4 * lane; t < d; t += 256) {
                     const bool two = t + 128 < d;
                     const float4 qv = __ldg(reinterpret_cast<const float4*>(q + t));
@@ -2358,6 +2384,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
                         acc[u] = fmaf(f3, f3, acc[u]);
                     }
                 }
+#endif
             } else {
                 for (int t = lane; t < d; t += 32) {
                     const float qv = __ldg(q + t);
