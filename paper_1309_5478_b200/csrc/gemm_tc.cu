@@ -273,6 +273,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     const uint32_t colfull0 = smem_u32(bars + 2 * KSTAGES + 5);
     const uint32_t colempty0 = colfull0 + 8 * NCOL;
     const uint32_t afull0 = colempty0 + 8 * NCOL, aempty0 = afull0 + 16;  // ARES panel buffers
+    // per column slot, the work item it belongs to (written by COL_WARP before the slot's
+    // expect_tx, read by the epilogue after the slot's full barrier): {mp, nb, cls | pass << 8,
+    // unit index}; mp = -1 ends the stream.  The epilogue warps then never run the scheduler.
+    int4* col_hdr = reinterpret_cast<int4*>(bars + 2 * KSTAGES + 5 + 2 * NCOL + 4 + 1);
     const Bars b{smem_u32(bars), smem_u32(bars + KSTAGES), smem_u32(bars + 2 * KSTAGES),
                  smem_u32(bars + 2 * KSTAGES + 2)};
     const uint32_t tfull0 = b.tfull0, tempty0 = b.tempty0;
@@ -325,8 +329,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
     } else if (warp == COL_WARP) {
         // ------------------------------------------- column data of each work item --
         if (lane == 0) {
-            int it = 0;
-            for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl)) {
+            int it = 0, ui = 0;
+            for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++ui) {
                 const tc::Unit wu = sched.unit(cur);
                 for (int64_t nbu = wu.nb0; nbu < wu.nb1; ++nbu) {  // (one tile per unit but PanelSched)
                 const tc::Unit w{wu.mp, nbu, nbu + 1};
@@ -340,6 +344,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     const uint32_t fb = colfull0 + 8 * slot;
                     const uint32_t dst = smem_u32(col_base + slot * 3 * BN);
+                    col_hdr[slot] = make_int4((int)w.mp, (int)w.nb0, cls | pass << 8, ui);
                     mbar_expect_tx(fb, NCOLARR * BN * 4);
                     bulk_load(dst, ep.xn + n0, BN * 4, fb);
                     bulk_load(dst + BN * 4, ep.x_rs + n0, BN * 4, fb);
@@ -347,6 +352,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                 }
                 }
             }
+            // end of the stream: a header-only item
+            const int slot = it % NCOL;
+            mbar_wait(colempty0 + 8 * slot, ((it / NCOL) & 1) ^ 1);
+            col_hdr[slot] = make_int4(-1, 0, 0, 0);
+            mbar_arrive(colfull0 + 8 * slot);
         }
         __syncwarp();
     } else {
@@ -372,11 +382,15 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         // block (row-major triangle schedule), so the three loads are skipped then
         int64_t row_c = -1;
         float qn_c = 0.0f, cq_c = 0.0f, trow_c = -1.0f;
-        for (auto cur = sched.first(cid); sched.valid(cur); sched.next(cur, ncl), ++wi) {
-            const tc::Unit wu = sched.unit(cur);
-            for (int64_t nbu = wu.nb0; nbu < wu.nb1; ++nbu) {  // (one tile per unit but PanelSched)
-            const tc::Unit w{wu.mp, nbu, nbu + 1};
-            const int cls = tile_class(w.mp, w.nb0, ml_shift);
+        for (;; ++it) {
+            const int slot = it % NCOL;
+            mbar_wait(colfull0 + 8 * slot, (it / NCOL) & 1);
+            const int4 hdr = col_hdr[slot];
+            if (hdr.x < 0) break;  // end of the work items
+            wi = hdr.w;
+            const tc::Unit w{hdr.x, hdr.y, hdr.y + 1};
+            const int cls = hdr.z & 0xFF;
+            const int pass = hdr.z >> 8;
             // this warp's chunks of the tile (3 warps per quadrant: 3/3/2, the short share
             // rotating per work item so that a warp can run ahead into the other accumulator)
             const int ch0 = ((E::PV ? part + wi : part) % E::PARTS) * E::CPW;
@@ -406,15 +420,13 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                               row0 + ep.self_shift < c_lo + 32 * nch && row0 + 31 + ep.self_shift >= c_lo;
             const int64_t self_col = row + ep.self_shift;
             float* drow = ep.D + row * ep.ldD;
-        for (int pass = 0; pass < tile_passes(cls); ++pass, ++it) {
+        {
             const int tmask = tile_mask(cls, pass);  // mixed block: keep one side only
             const int buf = it & 1;
             const uint32_t tphase = (it >> 1) & 1;
-            const int slot = it % NCOL;
             const float* col_n = col_base + slot * 3 * BN;
             const float* col_s = col_n + BN;
             const float* col_t = col_n + 2 * BN;
-            mbar_wait(colfull0 + 8 * slot, (it / NCOL) & 1);
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + ch0 * 32;
@@ -837,7 +849,6 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             // this work item's column data fully read
             __syncwarp();
             if (lane == 0) mbar_arrive(colempty0 + 8 * slot);
-        }
         }
         }
         if (use_tma_store && lane == 0) bulk_wait_all();
