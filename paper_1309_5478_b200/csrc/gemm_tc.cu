@@ -140,8 +140,7 @@ struct DeferredFlush {
             pos[j] = -1;
         }
     }
-    __device__ __forceinline__ void flush(const EpiArgs& ep, const uint32_t* prow, const uint32_t* pcol,
-                                          const uint32_t* pkey, int n) {
+    __device__ __forceinline__ void flush(const EpiArgs& ep, const uint4* pent, int n) {
         const int lane = threadIdx.x & 31;
         complete(ep);
         __syncwarp();
@@ -149,9 +148,10 @@ struct DeferredFlush {
         for (int j = 0; j < J; ++j) {
             const int i = 32 * j + lane;
             if (i < n) {
-                r[j] = prow[i];
-                c[j] = pcol[i];
-                k[j] = pkey[i];
+                const uint4 e = pent[i];  // {row, col, key, -}: one 16-byte load per entry
+                r[j] = e.x;
+                c[j] = e.y;
+                k[j] = e.z;
                 pos[j] = atomicAdd(ep.cnt + r[j], 1);
             }
         }
@@ -185,8 +185,8 @@ struct EpiCfg {
     static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
     // PV staging: 32 rows of SROW floats (KNN_EPI_REG) or a swizzled 32x32 chunk
     static constexpr int STG_PV = KNN_EPI_REG ? 32 * SROW * 4 : STG_BYTES;
-    static constexpr int PEND = PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 128) : 160) : PEND_CAP;
-    static constexpr int SLAB = PV ? STG_PV + 3 * PEND * 4 : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
+    static constexpr int PEND = PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 96) : 128) : PEND_CAP;
+    static constexpr int SLAB = PV ? STG_PV + 16 * PEND : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
     static constexpr int NCOLS = PV16 ? 6 : PV ? 3 : NCOL;  // column-data ring slots
     static constexpr int THREADS = 64 + 32 * WARPS + 32;
     static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : PV16 ? 4 * (A_BYTES + B_TILE) : RING_BYTES;
@@ -194,8 +194,7 @@ struct EpiCfg {
     static_assert(SMEM <= 232448, "shared memory");
     static_assert(SLAB % 16 == 0, "slab alignment");
 };
-__device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* prow, const uint32_t* pcol,
-                                            const uint32_t* pkey, int n) {
+__device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint4* pent, int n) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
     for (int i0 = 0; i0 < n; i0 += 128) {
@@ -205,7 +204,7 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
         for (int j = 0; j < 4; ++j) {
             const int i = i0 + 32 * j + lane;
             if (i < n) {
-                r[j] = prow[i];
+                r[j] = pent[i].x;
                 pos[j] = atomicAdd(ep.cnt + r[j], 1);
             }
         }
@@ -214,7 +213,7 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint32_t* p
             const int i = i0 + 32 * j + lane;
             if (i < n) {
                 if (pos[j] < ep.cap) {
-                    ep.cent[(int64_t)r[j] * ep.cap + pos[j]] = (uint64_t)pkey[i] << 32 | pcol[i];
+                    ep.cent[(int64_t)r[j] * ep.cap + pos[j]] = (uint64_t)pent[i].z << 32 | pent[i].y;
                 } else {
                     *ep.flag |= 2;
                 }
@@ -369,9 +368,8 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         int sbsel = 0;  // which of the warp's two staging buffers
         int it = 0;
         // PIVOT: the warp's pending-candidate list lives in its second staging buffer
-        uint32_t* prow = reinterpret_cast<uint32_t*>(slab + E::STG_PV);
-        uint32_t* pcol = prow + PEND_CAP;
-        uint32_t* pkey = pcol + PEND_CAP;
+        // pending entries {row, col, key, -}, one 16-byte store / load each
+        uint4* pent = reinterpret_cast<uint4*>(slab + E::STG_PV);
         int pend_n = 0;  // warp-uniform
         DeferredFlush<(E::PEND + 31) / 32> dfl;  // PIVOT: the previous flush's entries
         dfl.init();
@@ -570,8 +568,9 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         for (int c = 0; c < 32; ++c) v[c] = __int_as_float(0x7F800000);
                     }
                     if (SYM) {
-                        if (c0 < row0) continue;  // lower chunks: produced by their mirror
-                        if (c0 == row0) {        // diagonal chunk: keep col > row only
+                        // (32-bit compares: indices are < 2^31, include/knn.h)
+                        if ((int32_t)c0 < (int32_t)row0) continue;  // lower chunks: produced by their mirror
+                        if ((int32_t)c0 == (int32_t)row0) {        // diagonal chunk: keep col > row only
                             #pragma unroll
                             for (int c = 0; c < 32; ++c)
                                 if (c <= lane) v[c] = __int_as_float(0x7F800000);
@@ -584,10 +583,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                                 v[c] = __int_as_float(0x7F800000);
                         }
                     }
-                    if (c0 + 32 > ep.N) {
+                    if ((uint32_t)c0 + 32u > (uint32_t)ep.N) {
                         #pragma unroll
                         for (int c = 0; c < 32; ++c)
-                            if (c0 + c >= ep.N) v[c] = __int_as_float(0x7F800000);
+                            if ((int32_t)c0 + c >= (int32_t)ep.N) v[c] = __int_as_float(0x7F800000);
                     }
                     // this row's survivors in the chunk: row side (hr) and column side (hc)
                     uint32_t hr = 0, hc = 0;
@@ -655,7 +654,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         continue;
                     }
                     if (pend_n + total > PEND_CAP) {
-                        if (!EPI_DBG(8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
+                        if (!EPI_DBG(8)) dfl.flush(ep, pent, pend_n);
                         pend_n = 0;
                     }
                     uint32_t h = hm;
@@ -667,15 +666,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             const float x = srow[c];
                             const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
                             if ((hr >> c) & 1) {
-                                prow[pos] = (uint32_t)row;
-                                pcol[pos] = (uint32_t)(c0 + c);
-                                pkey[pos] = key;
+                                pent[pos] = make_uint4((uint32_t)row, (uint32_t)(c0 + c), key, 0u);
                                 ++pos;
                             }
                             if (SYM && ((hc >> c) & 1)) {
-                                prow[pos] = (uint32_t)(c0 + c);
-                                pcol[pos] = (uint32_t)row;
-                                pkey[pos] = key;
+                                pent[pos] = make_uint4((uint32_t)(c0 + c), (uint32_t)row, key, 0u);
                                 ++pos;
                             }
                         }
@@ -720,7 +715,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                     const int mine = __popc(hr) + __popc(hc);
                     const int total = __reduce_add_sync(0xFFFFFFFFu, mine);
                     if (pend_n + total > PEND_CAP) {
-                        if (!EPI_DBG(8)) dfl.flush(ep, prow, pcol, pkey, pend_n);
+                        if (!EPI_DBG(8)) dfl.flush(ep, pent, pend_n);
                         pend_n = 0;
                         if (lane == 0) s_pend[warp - 2] = 0;
                     }
@@ -734,15 +729,11 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                             const float x = srow[c ^ sx];
                             const uint32_t key = __float_as_uint(PIVOT1 ? fmaxf(x, 0.0f) : finalize_dist<METRIC>(x)) | 0x80000000u;
                             if ((hr >> c) & 1) {
-                                prow[pos] = (uint32_t)row;
-                                pcol[pos] = (uint32_t)(c0 + c);
-                                pkey[pos] = key;
+                                pent[pos] = make_uint4((uint32_t)row, (uint32_t)(c0 + c), key, 0u);
                                 ++pos;
                             }
                             if (SYM && ((hc >> c) & 1)) {
-                                prow[pos] = (uint32_t)(c0 + c);
-                                pcol[pos] = (uint32_t)row;
-                                pkey[pos] = key;
+                                pent[pos] = make_uint4((uint32_t)(c0 + c), (uint32_t)row, key, 0u);
                                 ++pos;
                             }
                         }
@@ -854,7 +845,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
         if (use_tma_store && lane == 0) bulk_wait_all();
         if constexpr (PIVOT) {
             dfl.complete(ep);
-            pivot_flush(ep, prow, pcol, pkey, pend_n);
+            pivot_flush(ep, pent, pend_n);
         }
     }
     teardown(tmem_base);
