@@ -21,9 +21,33 @@ def c1():
 
 
 def pivot():
+    """The 3-product partition (KNN_PLAN_PIVOT_EXACT) and the automatic plan (the device
+    picks the single-product partition + fp32 re-evaluation for uniform data: plan 5)."""
     X = torch.from_numpy(datagen.points(16384, 32, "uniform", seed=2)).to(dev)
+    knn.set_plan(knn.PLAN_PIVOT_EXACT)
     knn.graph(X, 16)
     assert knn.last_plan() == 3
+    knn.set_plan(knn.PLAN_AUTO)
+    knn.graph(X, 16)
+    assert knn.last_plan() == 5, knn.last_plan()
+
+
+def hostpipe():
+    """knn_search_block_host's pipelined k-NNG (copy stream, chunked phases, gated kernels)."""
+    X = datagen.points(16384, 32, "uniform", seed=6)
+    Xp = torch.from_numpy(X).pin_memory().numpy()
+    knn.search_block_host(Xp, Xp, 16, self_shift=0)
+    assert knn.last_plan() == 5, knn.last_plan()
+
+
+def twopass():
+    """The two-pass warp select (k <= 32, >= 4 rows per SM): ragged rows, ties."""
+    g = np.random.Generator(np.random.Philox(7))
+    D = torch.from_numpy(g.random((600, 5000), dtype=np.float32)).to(dev)
+    knn.select(D, 32)
+    D[:, ::3] = 0.5
+    knn.select(D, 8)
+    assert knn.last_select_kernel()[0] == "two-pass warp per row"
 
 
 def pivotq():
@@ -63,7 +87,8 @@ def par3():
                                 g * per, min(N, (g + 1) * per) - g * per)
 
 
-cases = {"c1": c1, "pivot": pivot, "pivotq": pivotq, "selects": selects, "par3": par3}
+cases = {"c1": c1, "pivot": pivot, "hostpipe": hostpipe, "twopass": twopass, "pivotq": pivotq,
+         "selects": selects, "par3": par3}
 for name, fn in cases.items():
     if which in ("all", name):
         fn()
