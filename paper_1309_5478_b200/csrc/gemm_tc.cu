@@ -428,7 +428,7 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + ch0 * 32;
-            #pragma unroll 1
+            #pragma unroll 1  // (unrolling the two chunks of the 16-warp partition: 1.45 -> 1.59 ms)
             for (int ch = 0; ch < nch; ++ch) {
                 uint32_t r[32];
                 tmem_ld32(taddr + ch * 32, r);
