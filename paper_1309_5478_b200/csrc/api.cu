@@ -177,8 +177,11 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     samp_blk = samp_blk < 256 ? 256 : (samp_blk / 256) * 256;
     if (samp_blk > M) samp_blk = M;
 
+    // L2 pivot plans: per-point single-product bound terms (prep's split residuals, reading
+    // R21) instead of the constant worst-case bound
+    const bool bnd_ok = (pivot || pivotq) && metric <= KNN_L2;
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
-        flag = c.take<int32_t>(4);
+        flag = c.take<int32_t>(8);  // [0] flags, [1] plan, [2..3] candidates, [4] max eps2
         auto prep = [&](Prepared& p, int64_t n) {
             p.sqn = c.take<float>(round_up(n, knn::kColPad));
             p.rs = c.take<float>(round_up(n, knn::kColPad));
@@ -200,9 +203,22 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     int32_t* redo = nullptr;
     Prepared smp{};  // the pivot plans' column sample (gathered points)
     float *nsc_x = nullptr, *nsc_q = nullptr;  // single-product partition: scaled norms
+    float *eps_x = nullptr, *eps_q = nullptr, *ninf_x = nullptr, *ninf_q = nullptr;  // bound terms
+    float *bnd_x = nullptr, *bnd_q = nullptr;
     float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
+        if (bnd_ok) {
+            const int64_t np = round_up(N, knn::kColPad), mp = round_up(M, knn::kColPad);
+            eps_x = c.take<float>(np);
+            ninf_x = c.take<float>(np);
+            bnd_x = c.take<float>(np);
+            nsc_x = c.take<float>(np);
+            eps_q = same ? eps_x : c.take<float>(mp);
+            ninf_q = same ? ninf_x : c.take<float>(mp);
+            bnd_q = same ? bnd_x : c.take<float>(mp);
+            nsc_q = same ? nsc_x : c.take<float>(mp);
+        }
         if (!pivot) redo = c.take<int32_t>((size_t)(rows_blk > 0 && !pivotq ? rows_blk : M) + 1);
         if (pivot || pivotq) {
             const int64_t Sx = pivot ? Ssamp : Sq;
@@ -212,10 +228,6 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             smp.sqn = c.take<float>(round_up(Sx, knn::kColPad));
             smp.rs = c.take<float>(round_up(Sx, knn::kColPad));
             const int32_t cp = pivot ? cap : capq;
-            if (pivot) {
-                nsc_x = c.take<float>(round_up(N, knn::kColPad));
-                nsc_q = c.take<float>(round_up(M, knn::kColPad));
-            }
             thr = c.take<float>(round_up(M, knn::kColPad));
             cnt = c.take<int32_t>(M);
             cent = c.take<uint64_t>((size_t)M * cp);
@@ -226,31 +238,41 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     Carve carve{static_cast<char*>(ctx->ws)};
     layout_all(carve);
 
-    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 8 * sizeof(int32_t), s));
+    float* tmax2 = bnd_ok ? reinterpret_cast<float*>(flag + 4) : nullptr;
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s));
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, flag, metric, s, eps_x, tmax2));
         t.done();
     }
     if (!same) {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, metric, s));
+        KNN_CUDA(knn::launch_prep(Q, M, d, d_pad, pq.sqn, pq.rs, pq.hi, pq.lo, flag, metric, s, eps_q, tmax2));
         t.done();
+    }
+    if (bnd_ok) {  // nsc / ninf / bnd of every point, one t for the call
+        KNN_CUDA(knn::launch_bound_norms(px.sqn, eps_x, round_up(N, knn::kColPad), tmax2, d_pad, nsc_x, ninf_x,
+                                         bnd_x, s));
+        if (!same)
+            KNN_CUDA(knn::launch_bound_norms(pq.sqn, eps_q, round_up(M, knn::kColPad), tmax2, d_pad, nsc_q,
+                                             ninf_q, bnd_q, s));
+        ctx->launches += same ? 1 : 2;
     }
     if (pivot) {
         // 1. sample pass: per-row minima of 32-column chunks over the first Ssamp corpus
         //    points (written by the GEMM epilogue; no sample matrix), 2. pivots
         {
             ctx->launches++;  // (not timed separately)
-            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Ssamp, d_pad, smp.hi, smp.lo,
-                                               smp.sqn, smp.rs, smax, s));
+            // (L2: the sample's epilogue terms are the upper-bound norms ninf)
+            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, bnd_ok ? ninf_x : px.sqn, px.rs, N, Ssamp, d_pad,
+                                               smp.hi, smp.lo, smp.sqn, smp.rs, smax, s));
             for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
                 const int64_t R = M - r0 < samp_blk ? M - r0 : samp_blk;
-                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
-                                   smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
+                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, (bnd_ok ? ninf_q : pq.sqn) + r0,
+                                   pq.rs + r0, R, smp.hi, smp.lo, smp.sqn, smp.rs, Ssamp, d_pad};
                 Timed tg(ctx, KNN_KERNEL_GEMM, s);
                 KNN_CUDA(knn::launch_dist_tc_mins(op, Ssamp, metric, KNN_NO_SELF, D, ctx->pivot_margin,
-                                                  ctx->num_sms, s, smax));
+                                                  ctx->num_sms, s, smax, bnd_ok));
                 tg.done();
                 Timed tp(ctx, KNN_KERNEL_SELECT, s);  // the pivot select (a-S4 on the chunk minima)
                 KNN_CUDA(knn::launch_pivot_from_mins(D, Ssamp / 32, R, round_up(r0 + R, knn::kColPad) - r0,
@@ -271,16 +293,12 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         const bool p1_auto = p1_ok && ctx->pivot1 < 0;
         const bool one = p1_ok && ctx->pivot1 > 0;
         knn::TcOperands op1 = op;
-        const float F = knn::pivot1_margin(d_pad);
-        if (p1_ok) {  // the lower bound u_hh - F n_qx as the u of norms scaled by 1 - F
-            KNN_CUDA(knn::launch_scale_norms(px.sqn, nsc_x, round_up(N, knn::kColPad), 1.0f - F, s));
-            if (!same) KNN_CUDA(knn::launch_scale_norms(pq.sqn, nsc_q, round_up(M, knn::kColPad), 1.0f - F, s));
-            ctx->launches += same ? 1 : 2;
-            op1.qn = same ? nsc_x : nsc_q;
+        if (p1_ok) {  // the lower bound u_hh - F1_q ||q||^2 - F1_x ||x||^2: the u of the nsc norms
+            op1.qn = nsc_q;
             op1.xn = nsc_x;
         }
-        if (p1_auto) {
-            KNN_CUDA(knn::launch_pivot1_decide(thr, pq.sqn, M, px.sqn, N, F, ctx->pivot1_ratio, flag, s));
+        if (p1_auto) {  // window 2 (mean bq + mean bx) against the mean pivot
+            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd_q, M, bnd_x, N, 1.0f, ctx->pivot1_ratio, flag, s));
             ctx->launches++;
         }
         ctx->last_plan_auto1 = p1_auto;
@@ -297,7 +315,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         if (one || p1_auto)
             KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, M, k, idx_offset, Q, X, d, pq.sqn,
-                                                     px.sqn, thr, F, metric, out_idx, out_dist, flag, s,
+                                                     bnd_q, bnd_x, thr, metric, out_idx, out_dist, flag, s,
                                                      p1_auto ? 1 : -1));
         if (!one)
             KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, M, k, idx_offset, out_idx, out_dist, flag,
@@ -311,17 +329,17 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
         //    (the self pair +inf), 2. pivots, 3. partition GEMM, 4. exact select (k > 32)
         {
             ctx->launches++;  // (not timed separately)
-            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, Sq, d_pad, smp.hi, smp.lo,
-                                               smp.sqn, smp.rs, nullptr, s));
+            KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, bnd_ok ? ninf_x : px.sqn, px.rs, N, Sq, d_pad,
+                                               smp.hi, smp.lo, smp.sqn, smp.rs, nullptr, s));
             KNN_CUDA(cudaMemsetAsync(thr, 0xFF, round_up(M, knn::kColPad) * sizeof(float), s));  // pad: NaN
             KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)M * sizeof(int32_t), s));
             for (int64_t r0 = 0; r0 < M; r0 += samp_blk) {
                 const int64_t R = M - r0 < samp_blk ? M - r0 : samp_blk;
-                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, pq.sqn + r0, pq.rs + r0, R,
-                                   smp.hi, smp.lo, smp.sqn, smp.rs, Sq, d_pad};
+                knn::TcOperands op{pq.hi + r0 * d_pad, pq.lo + r0 * d_pad, (bnd_ok ? ninf_q : pq.sqn) + r0,
+                                   pq.rs + r0, R, smp.hi, smp.lo, smp.sqn, smp.rs, Sq, d_pad};
                 Timed tg(ctx, KNN_KERNEL_GEMM, s);
                 KNN_CUDA(knn::launch_dist_tc_sample(op, Sq, metric, KNN_NO_SELF, D, Sq, ctx->pivot_margin,
-                                                    ctx->num_sms, s));
+                                                    ctx->num_sms, s, bnd_ok));
                 tg.done();
                 Timed tp(ctx, KNN_KERNEL_SELECT, s);
                 KNN_CUDA(knn::launch_pivot_from_sample(D, R, Sq, Sq, rq, thr + r0, s));
@@ -622,14 +640,25 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     const bool p1_ok = metric <= KNN_L2 && ctx->plan != KNN_PLAN_PIVOT_EXACT && ctx->pivot1 != 0;
     const bool p1_auto = p1_ok && ctx->pivot1 < 0;
     const bool one = p1_ok && ctx->pivot1 > 0;
-    const float F = knn::pivot1_margin(d_pad);
+    // L2: per-point single-product bound terms (as in run_block; t from the sample, which is
+    // prepared first: any t > 0 gives a valid bound, the same t for every point of the call)
+    const bool bnd_ok = metric <= KNN_L2;
     Prepared px{}, smp{};
     float *D, *smax, *thr, *nsc = nullptr;
+    float *eps = nullptr, *ninf = nullptr, *bnd = nullptr, *s_eps = nullptr, *s_ninf = nullptr, *s_bnd = nullptr;
     int32_t *flag, *cnt;
     uint64_t* cent;
     auto ws_layout = [&](Carve& c) {
-        flag = c.take<int32_t>(4);
-        if (p1_ok) nsc = c.take<float>(round_up(N, knn::kColPad));
+        flag = c.take<int32_t>(8);  // [4]: max eps2 of the sample
+        if (bnd_ok) {
+            nsc = c.take<float>(round_up(N, knn::kColPad));
+            eps = c.take<float>(N);
+            ninf = c.take<float>(N);
+            bnd = c.take<float>(N);
+            s_eps = c.take<float>(S);
+            s_ninf = c.take<float>(S);
+            s_bnd = c.take<float>(S);
+        }
         px.sqn = c.take<float>(N);
         px.rs = c.take<float>(N);
         px.hi = c.take<__half>((size_t)N * d_pad);
@@ -683,12 +712,19 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         cudaStream_t cs;
         ~CopyGuard() { cudaStreamSynchronize(cs); }
     } cg{cs};
-    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    KNN_CUDA(cudaMemsetAsync(flag, 0, 8 * sizeof(int32_t), s));
     KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_chunk[nch], 0));
+    float* tmax2 = reinterpret_cast<float*>(flag + 4);
     {
         Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(xs, S, d, d_pad, smp.sqn, smp.rs, smp.hi, smp.lo, flag, metric, s));
+        KNN_CUDA(knn::launch_prep(xs, S, d, d_pad, smp.sqn, smp.rs, smp.hi, smp.lo, flag, metric, s, s_eps,
+                                  bnd_ok ? tmax2 : nullptr));
         t.done();
+    }
+    if (bnd_ok) {  // the sample's upper-bound norms replace its sqn terms in the sample pass
+        KNN_CUDA(knn::launch_bound_norms(smp.sqn, s_eps, S, tmax2, d_pad, nullptr, s_ninf, s_bnd, s));
+        KNN_CUDA(cudaMemcpyAsync(smp.sqn, s_ninf, (size_t)S * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        ctx->launches++;
     }
     KNN_CUDA(knn::launch_max_nonneg(smp.sqn, S, smax, s));
     ctx->launches++;
@@ -702,19 +738,20 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         {
             Timed t(ctx, KNN_KERNEL_PREP, s);
             KNN_CUDA(knn::launch_prep(x + c0 * d, R, d, d_pad, px.sqn + c0, px.rs + c0, px.hi + c0 * d_pad,
-                                      px.lo + c0 * d_pad, flag, metric, s));
+                                      px.lo + c0 * d_pad, flag, metric, s, bnd_ok ? eps + c0 : nullptr));
             t.done();
         }
-        if (p1_ok) {
-            KNN_CUDA(knn::launch_scale_norms(px.sqn + c0, nsc + c0, R, 1.0f - F, s));
+        if (bnd_ok) {  // with the sample's t (tmax2 is not raised by the chunks)
+            KNN_CUDA(knn::launch_bound_norms(px.sqn + c0, eps + c0, R, tmax2, d_pad, nsc + c0, ninf + c0, bnd + c0,
+                                             s));
             ctx->launches++;
         }
-        knn::TcOperands op{px.hi + c0 * d_pad, px.lo + c0 * d_pad, px.sqn + c0, px.rs + c0, R,
+        knn::TcOperands op{px.hi + c0 * d_pad, px.lo + c0 * d_pad, (bnd_ok ? ninf : px.sqn) + c0, px.rs + c0, R,
                            smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
         {
             Timed tg(ctx, KNN_KERNEL_GEMM, s);
             KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s,
-                                              smax));
+                                              smax, bnd_ok));
             tg.done();
         }
         {
@@ -724,7 +761,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
             tp.done();
         }
         if (c == 0 && p1_auto) {  // the device's choice, from the first chunk's rows and the sample
-            KNN_CUDA(knn::launch_pivot1_decide(thr, px.sqn, R, smp.sqn, S, F, ctx->pivot1_ratio, flag, s));
+            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd, R, s_bnd, S, 1.0f, ctx->pivot1_ratio, flag, s));
             ctx->launches++;
         }
         // the triangle's units whose column block lies in this chunk (rows and columns < c0 + R)
@@ -742,7 +779,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     {
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         if (one || p1_auto)
-            KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, N, k, 0, x, x, d, px.sqn, px.sqn, thr, F, metric,
+            KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, N, k, 0, x, x, d, px.sqn, bnd, bnd, thr, metric,
                                                      oi, od, flag, s, p1_auto ? 1 : -1));
         if (!one)
             KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, N, k, 0, oi, od, flag, s, p1_auto ? 0 : -1));

@@ -229,8 +229,8 @@ __device__ __forceinline__ void pivot_flush(const EpiArgs& ep, const uint4* pent
 // sample for k > 32), unclamped, in the u domain.
 enum { MODE_STORE = 0, MODE_PIVOT = 1, MODE_MINS = 2, MODE_SAMPLE = 3, MODE_NULL = 4, MODE_PIVOT1 = 5 };
 // MODE_PIVOT1: the partition from the single hi.hi product; the kept key is the lower bound
-// u_hh - F (||q||^2 + ||x||^2) <= the exact distance (computed as the u of norms scaled by
-// 1 - F, launch_scale_norms), so every element at or below the pivot is kept; the
+// u_hh - F1_q ||q||^2 - F1_x ||x||^2 <= the exact distance (computed as the u of the per-point
+// norms scaled by 1 - F1, prep.cu launch_bound_norms), so every element at or below the pivot is kept; the
 // candidate select re-evaluates the survivors exactly (select.cu).
 // MODE_NULL (diagnostic, knn_diag_mainloop): the epilogue only drains TMEM (tcgen05.ld) and
 // frees the accumulator, so the kernel runs at the mainloop's own rate.
@@ -980,7 +980,8 @@ cudaError_t launch_dist_tc_sym(const TcOperands& op, int32_t metric, float* D, i
 }
 
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
-                                float margin_override, int num_sms, cudaStream_t s, const float* xmax) {
+                                float margin_override, int num_sms, cudaStream_t s, const float* xmax,
+                                bool bounded_norms) {
     if (!xmax || self_shift != INT64_MIN) return cudaErrorInvalidValue;  // gathered samples only
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     // S sampled columns = S/256 full column blocks spread evenly over the op.N columns
@@ -997,8 +998,11 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
     // hi.hi product (prep.cu split, |lo| <= 2^-11 |x| per component): |2 q.x - 2 qh.xh| <=
     // (2^-10 (1 + 2^-10) + d 2^-23) 2|q||x| (the d term bounds fp32 accumulation), and
     // 2|q||x| <= ||q||^2 + ||x||^2; + 2^-20 covers the roundings of both u values.
-    float margin = (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
-                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
+    // bounded_norms: op.qn / op.xn already carry the per-point bound (launch_bound_norms'
+    // ninf = sqn (1 + Fs)), so no margin is added
+    float margin = bounded_norms ? 0.0f
+                                 : (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
+                                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;  // tests: force bad pivots
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, mins, op.M,
                nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns, xmax};
@@ -1039,7 +1043,8 @@ cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric,
 }
 
 cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,
-                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s) {
+                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s,
+                                  bool bounded_norms) {
     if (op.M == 0 || op.N == 0) return cudaSuccess;
     const int64_t ns = S / BN, nfull = op.N / BN;
     if (S % BN != 0 || ns < 1 || ns > nfull) return cudaErrorInvalidValue;
@@ -1052,8 +1057,10 @@ cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metri
         !tc_make_output_map(&md, Ds, op.M, S, ldS))
         return cudaErrorInvalidValue;
     // the same single-product error bound as the chunk-minimum sample (launch_dist_tc_mins)
-    float margin = (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
-                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
+    // (bounded_norms: the per-point bound is in op.qn / op.xn, launch_bound_norms' ninf)
+    float margin = bounded_norms ? 0.0f
+                                 : (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) +
+                                           op.d_pad * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
     if (!std::isnan(margin_override)) margin = margin_override;
     EpiArgs ep{op.qn, op.q_rs, op.M, op.xn, op.x_rs, op.N, metric, self_shift, Ds, ldS,
                nullptr, nullptr, nullptr, 0, nullptr, margin, nfull / ns};
@@ -1125,21 +1132,13 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
                                          s, unit_lo, unit_hi, 0.0f, col_major, gate);
 }
 
-float pivot1_margin(int32_t d_pad) {
-    // |u_hh - D| <= F (||q||^2 + ||x||^2) for the exact distance D of the fp32 inputs: the
-    // sample pass's bound (launch_dist_tc_mins) with one more d_pad 2^-23 for the fp32
-    // rounding of the two norms and of u, and 2^-20 for the lower bound's own roundings
-    return (float)(std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -10)) + 2.0 * d_pad * std::ldexp(1.0, -23) +
-                   std::ldexp(1.0, -19));
-}
-
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
                                   int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate,
                                   int64_t unit_lo, int64_t unit_hi, bool col_major) {
     if (metric_kind(metric) == 2) return cudaErrorInvalidValue;  // L2 metrics only
     return launch_pivot_impl<MODE_PIVOT1>(op, metric, self_shift, sym, thr, cnt, cent, cap, flag,
-                                          num_sms, s, unit_lo, unit_hi, pivot1_margin(op.d_pad), col_major, gate);
+                                          num_sms, s, unit_lo, unit_hi, 0.0f, col_major, gate);
 }
 
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s) {

@@ -35,9 +35,18 @@ constexpr int kColPad = 256;
 // ---------------------------------------------------------------- launchers --------
 // prep.cu: row norms (fp64 accumulate) + non-finite flag; optionally the scaled fp16
 // hi/lo split for the tensor-core GEMM (hi/lo may be null).
+// eps2 (optional, L2 metrics with the split): per point ||s x - hi||^2 / ||s x||^2 rounded
+// up (0 on the padding to kColPad); tmax2 (optional): atomically raised to the max eps2.
 cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
                         float* rscale, __half* hi, __half* lo, int32_t* flag, int32_t metric,
-                        cudaStream_t s);
+                        cudaStream_t s, float* eps2 = nullptr, float* tmax2 = nullptr);
+// Per-point single-product bound terms from prep's eps2 and the call's *tmax2 (prep.cu,
+// DESIGN.md §6.5): nsc = sqn (1 - F1) rounded down (the partition's lower-bound norms; may be null),
+// ninf = sqn (1 + Fs) rounded up (the sample's upper-bound norms; may be null), bnd =
+// sqn F1 rounded up (may be null).  |u_hh - D| <= Fs_q sqn_q + Fs_x sqn_x <= F1_q .. for
+// every pair of points prepared with the same *tmax2.
+cudaError_t launch_bound_norms(const float* sqn, const float* eps2, int64_t n, const float* tmax2, int32_t d_pad,
+                               float* nsc, float* ninf, float* bnd, cudaStream_t s);
 
 // prep.cu: the pivot plans' column sample: S points perm(j) = (j * sample_stride(N)) mod N,
 // their split operands and epilogue terms copied contiguously (column arrays padded).
@@ -80,18 +89,16 @@ cudaError_t launch_dist_tc_pivot(const TcOperands& op, int32_t metric, int64_t s
                                  int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false,
                                  int32_t gate = -1);
 // The same partition from the single hi.hi product (L2 metrics): kept iff the lower bound
-// L = u_hh - F (||q||^2 + ||x||^2) <= thr[row] (resp. thr[col]); the key is L.
-// F = pivot1_margin(d_pad) bounds |u_hh - D| / (||q||^2 + ||x||^2) for the exact D.
-// op.qn / op.xn must be the prep norms scaled by 1 - F (launch_scale_norms).
-cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s);
-float pivot1_margin(int32_t d_pad);
+// L = u_hh - F1_q ||q||^2 - F1_x ||x||^2 <= thr[row] (resp. thr[col]); the key is L.
+// op.qn / op.xn must be launch_bound_norms' nsc terms (prep norms scaled by 1 - F1).
 cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t self_shift, bool sym,
                                   const float* thr, int32_t* cnt, uint64_t* cent,
                                   int32_t cap, int32_t* flag, int num_sms, cudaStream_t s, int32_t gate = -1,
                                   int64_t unit_lo = -1, int64_t unit_hi = -1, bool col_major = false);
 // Device-side choice of the pivot plan's partition: flag[1] = 1 (single
 // product + re-evaluation) iff the single-product bound is narrow against the pivots,
-// 2 F (mean ||q||^2 + mean ||x||^2) <= ratio * mean(finite pivots), else 0 (3 products).
+// 2 F (mean qn + mean xn) <= ratio * mean(finite pivots), else 0 (3 products); the callers
+// pass the bnd terms of launch_bound_norms with F = 1.
 cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, const float* xn, int64_t N,
                                  float F, float ratio, int32_t* flag, cudaStream_t s);
 // Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
@@ -102,12 +109,15 @@ cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cud
 // spread evenly over them (block j * ((N/256) / (S/256))), so that ordered data (e.g. points
 // sorted by cluster) still gives every row a representative sample.
 // xmax: device pointer to an upper bound of the columns' sqn terms (the sample's max).
+// bounded_norms: op.qn / op.xn are launch_bound_norms' ninf terms (L2; no constant margin).
 cudaError_t launch_dist_tc_mins(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* mins,
-                                float margin_override, int num_sms, cudaStream_t s, const float* xmax);
+                                float margin_override, int num_sms, cudaStream_t s, const float* xmax,
+                                bool bounded_norms = false);
 // Quantile-pivot sample for k > 32: Ds[i][j] (ldS) = the single-product upper bound of u(i, j)
 // for corpus points j < op.N (self pair +inf), unclamped.
 cudaError_t launch_dist_tc_sample(const TcOperands& op, int64_t S, int32_t metric, int64_t self_shift, float* Ds,
-                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s);
+                                  int64_t ldS, float margin_override, int num_sms, cudaStream_t s,
+                                  bool bounded_norms = false);
 // select.cu: pivots = k-th smallest chunk minimum per row; exact select over candidates.
 // thr[M .. pad_end) (relative to thr) is zero-filled: the SYM partition reads whole 256-row
 // tiles of pivots; pad_end must not pass the caller's allocation (absolute limit).
@@ -126,12 +136,13 @@ cudaError_t launch_pivot_from_sample(const float* Ds, int64_t M, int64_t S, int6
                                      float* thr, cudaStream_t s);
 // Exact top-k (k <= 32, L2 metrics) of the single-product partition's lists (lower bounds):
 // re-evaluates the few candidates whose bounds reach the k-th upper bound in fp64 from the
-// fp32 inputs Q [M][d] / X [N][d]; qn / xn the prep norms, margin = pivot1_margin.
+// fp32 inputs Q [M][d] / X [N][d]; qn the rows' prep norms, bq / bx the rows' / columns'
+// launch_bound_norms bnd terms (U = L + 2 (bq + bx) >= D).
 // flag |= 2 when the partition is not certified exact for some row (the caller redoes).
 cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
-                                       const float* X, int32_t d, const float* qn, const float* xn,
-                                       const float* thr, float margin, int32_t metric, int32_t* out_idx,
+                                       const float* X, int32_t d, const float* qn, const float* bq,
+                                       const float* bx, const float* thr, int32_t metric, int32_t* out_idx,
                                        float* out_dist, int32_t* flag, cudaStream_t s, int32_t gate = -1);
 // redo: M + 1 int32 of workspace for the warp-per-row form (null: CTA per row only).
 cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint64_t* cent,

@@ -27,6 +27,7 @@
 #include "internal.cuh"
 
 #include <cfloat>
+#include <cmath>
 
 namespace knn {
 namespace {
@@ -36,7 +37,8 @@ constexpr int kWarpsPerBlock = 8;
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
             float* __restrict__ sqn, float* __restrict__ rscale, __half* __restrict__ hi,
-            __half* __restrict__ lo, int32_t* __restrict__ flag, int32_t metric) {
+            __half* __restrict__ lo, int32_t* __restrict__ flag, int32_t metric,
+            float* __restrict__ eps2, float* __restrict__ tmax2) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (row >= N) {
@@ -45,6 +47,7 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
         if (hi != nullptr && lane == 0 && row < round_up(N, (int64_t)kColPad)) {
             sqn[row] = 0.0f;
             rscale[row] = 0.0f;
+            if (eps2) eps2[row] = 0.0f;
         }
         return;
     }
@@ -107,16 +110,41 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
     }
     __half* h = hi + row * (int64_t)d_pad;
     __half* l = lo + row * (int64_t)d_pad;
+    // eps2 (L2 metrics): the row's split residual ratio ||s x - hi||^2 / ||s x||^2 in fp64
+    // from the exact scaled input (per-point bound of the single product)
+    const double sd = ldexp(1.0, sh);
+    double rr = 0.0, vv = 0.0;
     for (int t = lane; t < d_pad; t += 32) {
         float v = 0.0f;
+        float xv = 0.0f;
         if (t < d && finite) {
             // exact power-of-two scaling of x (or of the fp32-rounded centred value)
-            const float xv = metric == 3 && angular ? (float)((double)__ldg(x + t) - mean) : __ldg(x + t);
+            xv = metric == 3 && angular ? (float)((double)__ldg(x + t) - mean) : __ldg(x + t);
             v = xv * s1 * s2;
         }
         __half vh = __float2half_rn(v);
         h[t] = vh;
         l[t] = __float2half_rn(v - __half2float(vh));
+        if (eps2) {
+            const double vx = (double)xv * sd, r = vx - (double)__half2float(vh);
+            rr = fma(r, r, rr);
+            vv = fma(vx, vx, vv);
+        }
+    }
+    if (eps2) {
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rr += __shfl_xor_sync(0xFFFFFFFFu, rr, o);
+            vv += __shfl_xor_sync(0xFFFFFFFFu, vv, o);
+        }
+        if (lane == 0) {
+            // rounded up, with room for the fp64 sums' own rounding (d 2^-53 each)
+            const float e2 = vv > 0.0 ? __double2float_ru(rr / vv * (1.0 + 0x1p-30)) : 0.0f;
+            eps2[row] = e2;
+            // the call's t^2 = max eps2 (>= 0: int order); the read skips most atomics
+            if (tmax2 && e2 > *reinterpret_cast<volatile float*>(tmax2))
+                atomicMax(reinterpret_cast<int*>(tmax2), __float_as_int(e2));
+        }
     }
 }
 
@@ -124,10 +152,56 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
 
 cudaError_t launch_prep(const float* X, int64_t N, int32_t d, int32_t d_pad, float* sqn,
                         float* rscale, __half* hi, __half* lo, int32_t* flag, int32_t metric,
-                        cudaStream_t s) {
+                        cudaStream_t s, float* eps2, float* tmax2) {
     if (N == 0) return cudaSuccess;
+    if (eps2 && (hi == nullptr || metric > 1)) return cudaErrorInvalidValue;  // split, L2 metrics only
     dim3 grid((unsigned)ceil_div(hi != nullptr ? round_up(N, (int64_t)kColPad) : N, kWarpsPerBlock));
-    prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag, metric);
+    prep_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(X, N, d, d_pad, sqn, rscale, hi, lo, flag, metric, eps2,
+                                                     tmax2);
+    return cudaGetLastError();
+}
+
+namespace {
+// Per-point terms of the single-product bound (reading R21).  With v = s x
+// the exact scaled point, hi its fp16 split and e = ||v - hi|| / ||v|| (prep's eps2), for
+// any t > 0 (the same for every point of the call: t = sqrt(max eps2), at least 2^-13)
+//   2 |q||x| (e_q + e_x) <= (t + e_q^2 / t) ||q||^2 + (t + e_x^2 / t) ||x||^2     (AM-GM),
+//   2 |q||x| e_q e_x    <= 2^-11' (e_q ||q||^2 + e_x ||x||^2)         (every e <= 2^-11'),
+// so |2 q.x - 2 qh.xh / (s_q s_x)| <= B_q ||q||^2 + B_x ||x||^2 with the per-point
+// B = (t + e^2 / t)(1 + 2^-10) + 2^-11 (1 + 2^-9) e (the 1 + 2^-10 also covers the
+// 3-product value's rounded lo halves), and the accumulation / rounding terms of the
+// constant bound (gemm_tc.cu launch_dist_tc_mins) follow per point:
+//   Fs = B + gs (sample values: upper bounds),  F1 = B + g1 (partition lower bounds),
+//   gs = gamma (1 + 2^-9) + 2^-20,  g1 = 2 gamma (1 + 2^-9) + 2^-19,  gamma = d_pad 2^-23.
+// Outputs (fp64 arithmetic, directed roundings):  nsc = RD(sqn (1 - F1)) (the partition's
+// lower-bound norms), ninf = RU(sqn (1 + Fs)) (the sample's upper-bound norms),
+// bnd = RU(sqn F1) (half the width of the re-evaluation window, per point).
+__global__ void bound_norms_kernel(const float* __restrict__ sqn, const float* __restrict__ eps2, int64_t n,
+                                   const float* __restrict__ tmax2, double gs, double g1,
+                                   float* __restrict__ nsc, float* __restrict__ ninf, float* __restrict__ bnd) {
+    // (floor 2^-13: a call whose t-defining points happen to be fp16-exact, e.g. the
+    // pipelined k-NNG's sample, keeps every other point's F within ~2x the constant bound)
+    const double t = fmax(sqrt((double)__ldg(tmax2)), 0x1p-13);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double e2 = (double)eps2[i], q = (double)sqn[i];
+        const double B = (t + e2 / t) * (1.0 + 0x1p-10) + 0x1p-11 * (1.0 + 0x1p-9) * sqrt(e2);
+        const double F1 = B + g1;
+        if (nsc) nsc[i] = __double2float_rd(q * (1.0 - F1));
+        if (ninf) ninf[i] = __double2float_ru(q * (1.0 + B + gs));
+        if (bnd) bnd[i] = __double2float_ru(q * F1);
+    }
+}
+}  // namespace
+
+cudaError_t launch_bound_norms(const float* sqn, const float* eps2, int64_t n, const float* tmax2, int32_t d_pad,
+                               float* nsc, float* ninf, float* bnd, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const double gamma = d_pad * std::ldexp(1.0, -23);
+    const double gs = gamma * (1.0 + std::ldexp(1.0, -9)) + std::ldexp(1.0, -20);
+    const double g1 = 2.0 * gamma * (1.0 + std::ldexp(1.0, -9)) + std::ldexp(1.0, -19);
+    const int64_t blocks = ceil_div(n, (int64_t)256);
+    bound_norms_kernel<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(sqn, eps2, n, tmax2, gs, g1, nsc,
+                                                                               ninf, bnd);
     return cudaGetLastError();
 }
 
@@ -217,12 +291,7 @@ cudaError_t launch_max_nonneg(const float* v, int64_t n, float* out, cudaStream_
     return cudaGetLastError();
 }
 
-namespace {
-__global__ void scale_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n, float f) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i] * f;
-}
-}  // namespace
+
 
 namespace {
 // One CTA: sums of the row norms, the column norms and the finite pivots (double), then the
@@ -298,12 +367,6 @@ cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, c
     return cudaGetLastError();
 }
 
-// dst = f * src (the single-product partition's scaled norms; n includes the zero padding)
-cudaError_t launch_scale_norms(const float* src, float* dst, int64_t n, float f, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const int64_t blocks = ceil_div(n, (int64_t)256);
-    scale_kernel<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(src, dst, n, f);
-    return cudaGetLastError();
-}
+
 
 }  // namespace knn

@@ -2205,8 +2205,9 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
 }
 
 // Exact top-k (k <= 32) of the single-product partition (gemm_tc.cu MODE_PIVOT1, L2
-// metrics), warp per row.  The list holds lower bounds L = u_hh - F n_qx <= D (n_qx =
-// ||q||^2 + ||x||^2), so U = L + 2F n_qx >= D:
+// metrics), warp per row.  The list holds lower bounds L = u_hh - (F1_q ||q||^2 + F1_x
+// ||x||^2) <= D (per-point terms, prep.cu launch_bound_norms), so U = L + 2 (bq + bx) >= D
+// with b = RU(F1 ||.||^2):
 //  1. T = the k-th smallest U over the first <= 512 candidates: k candidates have D <= T,
 //     so the row's k nearest candidates (and their fp32 ties) all have L <= T;
 //  2. R = {L <= T (1 + 4 e) + slack} (e = the re-evaluation's error bound): typically k
@@ -2231,8 +2232,9 @@ __global__ void __launch_bounds__(256, KNN_CR_MINB)
 candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
                            int cap, int64_t M, int k, int64_t idx_offset,
                            const float* __restrict__ Q, const float* __restrict__ X, int d,
-                           const float* __restrict__ qn, const float* __restrict__ xn,
-                           const float* __restrict__ thr, float margin, float rerr, int metric, int vec,
+                           const float* __restrict__ qn, const float* __restrict__ bq,
+                           const float* __restrict__ bx, const float* __restrict__ thr, float rerr,
+                           int metric, int vec,
                            int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
                            int32_t* __restrict__ flag, int gate) {
     if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
@@ -2250,7 +2252,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
     if (lane == 0 && !(vec & 2)) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
     const uint32_t* ri = reinterpret_cast<const uint32_t*>(cent + row * cap);  // (key << 32 | col)
     const uint32_t* rk = ri + 1;
-    const float qnr = __ldg(qn + row), f2 = 2.0f * margin;
+    const float qnr = __ldg(qn + row), bqr = __ldg(bq + row);
     // 1. T
     const int n1 = n < 32 * CR_PER ? n : 32 * CR_PER;
     uint32_t v[CR_PER], lk[CR_PER], li[CR_PER];
@@ -2262,8 +2264,8 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
     }
     #pragma unroll
     for (int i = 0; i < CR_PER; ++i) {
-        const float xj = lane + 32 * i < n1 ? __ldg(xn + li[i]) : 0.0f;
-        v[i] = lk[i] == 0xFFFFFFFFu ? 0xFFFFFFFFu : ukey(fmaf(f2, qnr + xj, ukey_to_float(lk[i])));
+        const float bj = lane + 32 * i < n1 ? __ldg(bx + li[i]) : 0.0f;
+        v[i] = lk[i] == 0xFFFFFFFFu ? 0xFFFFFFFFu : ukey(__fmaf_ru(2.0f, __fadd_ru(bqr, bj), ukey_to_float(lk[i])));
     }
     sort16(v);
     #pragma unroll
@@ -3323,8 +3325,8 @@ cudaError_t launch_candidate_select_large(const int32_t* cnt, const uint64_t* ce
 
 cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
                                        int32_t cap, int64_t M, int32_t k, int64_t idx_offset, const float* Q,
-                                       const float* X, int32_t d, const float* qn, const float* xn,
-                                       const float* thr, float margin, int32_t metric, int32_t* out_idx,
+                                       const float* X, int32_t d, const float* qn, const float* bq,
+                                       const float* bx, const float* thr, int32_t metric, int32_t* out_idx,
                                        float* out_dist, int32_t* flag, cudaStream_t s, int32_t gate) {
     if (M == 0) return cudaSuccess;
     if (k < 1 || k > 32 || metric < 0 || metric > 1) return cudaErrorInvalidValue;
@@ -3334,7 +3336,7 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
     const int vec = ((d % 4 == 0) && ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(X)) & 15) == 0) |
                     (getenv_flag("KNN_RECOMP_STATS") ? 2 : 0);
     candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset, Q,
-                                                                       X, d, qn, xn, thr, margin, rerr, metric, vec,
+                                                                       X, d, qn, bq, bx, thr, rerr, metric, vec,
                                                                        out_idx, out_dist, flag, gate);
     return cudaGetLastError();
 }

@@ -640,7 +640,7 @@ def test_pivot1_single_product_partition_vs_oracle(N, d, k, metric, dist, nq, tm
     ex = np.take_along_axis(D64, gi[rows], axis=1)
     if metric == 1:
         ex = np.sqrt(ex)
-    if plan in (3, 4):
+    if plan in (5, 6):  # re-evaluated values: the fp32 sum of squared differences
         bound = ((d + 31) // 32 + 8) * 2.0 ** -24 * (0.5 if metric == 1 else 1.0) + 2.0 ** -24
         assert np.all(np.abs(gd[rows] - ex) <= bound * ex + 1e-30)
 
@@ -762,3 +762,27 @@ def test_host_pipelined_auto_plan_equals_device(N, d, k, metric):
     assert knn().last_plan() == 5, knn().last_plan()
     assert np.array_equal(hi, ref_i) and np.array_equal(hd.view(np.uint32), ref_d.view(np.uint32))
     e2e_check(X, X, hi, hd, k, np.arange(0, N, 131), True, metric=metric)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_per_point_bound_mixed_residuals(metric):
+    """Per-point single-product bound (reading R21): every 8th point is
+    fp16-exact after prep's power-of-two scaling (split residual e = 0) and the others are
+    random (e up to ~2^-12).  The host-pipelined call takes t from its sample (exactly those
+    fp16-exact points: t at its floor 2^-13), the device call from every point; both bounds
+    are valid for any t, so both calls keep the single-product partition without a redo and
+    return the device call's lists, which pass the oracle's E2E checks."""
+    N, d, k = 16384, 40, 12
+    X = datagen.points(N, d, "gauss", seed=4242)
+    X[::8] = X[::8].astype(np.float16).astype(np.float32)
+    X = np.ascontiguousarray(X)
+    kn = knn()
+    gi, gd = kn.graph(cuda(X), k, metric=metric)
+    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    assert kn.last_plan() == 5, kn.last_plan()
+    pinned_x = torch.from_numpy(X).pin_memory().numpy()
+    hi, hd = kn.search_block_host(pinned_x, pinned_x, k, metric=metric, self_shift=0)
+    assert kn.last_plan() == 5, kn.last_plan()  # (a redo would report the materialised plan)
+    assert np.array_equal(hi, gi) and np.array_equal(hd.view(np.uint32), gd.view(np.uint32))
+    rows = np.concatenate([np.arange(0, N, 97), np.arange(0, N, 8)[:64]])
+    e2e_check(X, X, gi, gd, k, np.unique(rows), True, metric=metric)
