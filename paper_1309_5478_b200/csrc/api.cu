@@ -181,7 +181,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     // R21) instead of the constant worst-case bound
     const bool bnd_ok = (pivot || pivotq) && metric <= KNN_L2;
     auto layout = [&](Carve& c, Prepared& pq, Prepared& px, float*& D, int32_t*& flag) {
-        flag = c.take<int32_t>(8);  // [0] flags, [1] plan, [2..3] candidates, [4] max eps2
+        flag = c.take<int32_t>(8);  // [0] flags, [1] plan, [2..3] candidates, [4] max eps2, [5] decide counter
         auto prep = [&](Prepared& p, int64_t n) {
             p.sqn = c.take<float>(round_up(n, knn::kColPad));
             p.rs = c.take<float>(round_up(n, knn::kColPad));
@@ -205,11 +205,13 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     float *nsc_x = nullptr, *nsc_q = nullptr;  // single-product partition: scaled norms
     float *eps_x = nullptr, *eps_q = nullptr, *ninf_x = nullptr, *ninf_q = nullptr;  // bound terms
     float *bnd_x = nullptr, *bnd_q = nullptr;
+    double* dec_part = nullptr;  // the plan decision's partial sums
     float* smax = nullptr;  // max of the sample's sqn terms
     auto layout_all = [&](Carve& c) {
         layout(c, pq, px, D, flag);
         if (bnd_ok) {
             const int64_t np = round_up(N, knn::kColPad), mp = round_up(M, knn::kColPad);
+            dec_part = c.take<double>(knn::pivot1_decide_ws_bytes() / sizeof(double));
             eps_x = c.take<float>(np);
             ninf_x = c.take<float>(np);
             bnd_x = c.take<float>(np);
@@ -298,7 +300,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
             op1.xn = nsc_x;
         }
         if (p1_auto) {  // window 2 (mean bq + mean bx) against the mean pivot
-            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd_q, M, bnd_x, N, 1.0f, ctx->pivot1_ratio, flag, s));
+            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd_q, M, bnd_x, N, 1.0f, ctx->pivot1_ratio, flag, dec_part,
+                                               reinterpret_cast<unsigned*>(flag + 5), s));
             ctx->launches++;
         }
         ctx->last_plan_auto1 = p1_auto;
@@ -646,10 +649,11 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     Prepared px{}, smp{};
     float *D, *smax, *thr, *nsc = nullptr;
     float *eps = nullptr, *ninf = nullptr, *bnd = nullptr, *s_eps = nullptr, *s_ninf = nullptr, *s_bnd = nullptr;
+    double* dec_part = nullptr;
     int32_t *flag, *cnt;
     uint64_t* cent;
     auto ws_layout = [&](Carve& c) {
-        flag = c.take<int32_t>(8);  // [4]: max eps2 of the sample
+        flag = c.take<int32_t>(8);  // [4]: max eps2 of the sample, [5]: decide counter
         if (bnd_ok) {
             nsc = c.take<float>(round_up(N, knn::kColPad));
             eps = c.take<float>(N);
@@ -658,6 +662,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
             s_eps = c.take<float>(S);
             s_ninf = c.take<float>(S);
             s_bnd = c.take<float>(S);
+            dec_part = c.take<double>(knn::pivot1_decide_ws_bytes() / sizeof(double));
         }
         px.sqn = c.take<float>(N);
         px.rs = c.take<float>(N);
@@ -761,7 +766,8 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
             tp.done();
         }
         if (c == 0 && p1_auto) {  // the device's choice, from the first chunk's rows and the sample
-            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd, R, s_bnd, S, 1.0f, ctx->pivot1_ratio, flag, s));
+            KNN_CUDA(knn::launch_pivot1_decide(thr, bnd, R, s_bnd, S, 1.0f, ctx->pivot1_ratio, flag, dec_part,
+                                               reinterpret_cast<unsigned*>(flag + 5), s));
             ctx->launches++;
         }
         // the triangle's units whose column block lies in this chunk (rows and columns < c0 + R)

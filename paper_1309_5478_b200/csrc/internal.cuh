@@ -99,8 +99,11 @@ cudaError_t launch_dist_tc_pivot1(const TcOperands& op, int32_t metric, int64_t 
 // product + re-evaluation) iff the single-product bound is narrow against the pivots,
 // 2 F (mean qn + mean xn) <= ratio * mean(finite pivots), else 0 (3 products); the callers
 // pass the bnd terms of launch_bound_norms with F = 1.
+// part: pivot1_decide_ws_bytes() of device scratch; counter: a device uint zeroed before the call.
+size_t pivot1_decide_ws_bytes();
 cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, const float* xn, int64_t N,
-                                 float F, float ratio, int32_t* flag, cudaStream_t s);
+                                 float F, float ratio, int32_t* flag, double* part, unsigned* counter,
+                                 cudaStream_t s);
 // Diagnostic: the 3-product GEMM with an epilogue that only drains TMEM (mainloop rate).
 cudaError_t launch_dist_tc_null(const TcOperands& op, bool sym, int num_sms, cudaStream_t s);
 // Pivot sample pass: mins[c][i] = min distance of query i over corpus points 32c..32c+31

@@ -294,23 +294,26 @@ cudaError_t launch_max_nonneg(const float* v, int64_t n, float* out, cudaStream_
 
 
 namespace {
-// One CTA: sums of the row norms, the column norms and the finite pivots (double), then the
-// decision.  (~65 k rows: a few microseconds.)
-__global__ void __launch_bounds__(1024) pivot1_decide_kernel(const float* __restrict__ thr,
-                                                            const float* __restrict__ qn, int64_t M,
-                                                            const float* __restrict__ xn, int64_t N, float F,
-                                                            float ratio, int32_t* __restrict__ flag) {
-    __shared__ double red[3][32];
-    // float4 loads with several in flight (the arrays are 16-byte aligned device carves);
-    // fp32 partial sums per thread (<= M / 4096 terms each), then fp64
+// Sums of the row terms, the column terms and the finite pivots, then the decision.
+// kDecBlocks CTAs each reduce a strided slice (fp32 partials per thread, <= M / 32768 terms
+// each, then fp64) into part[block]; the last CTA to finish (counter, zeroed by the
+// caller) adds the partials in block order (deterministic) and writes flag[1].
+constexpr int kDecBlocks = 128;
+__global__ void __launch_bounds__(256) pivot1_decide_kernel(const float* __restrict__ thr,
+                                                           const float* __restrict__ qn, int64_t M,
+                                                           const float* __restrict__ xn, int64_t N, float F,
+                                                           float ratio, int32_t* __restrict__ flag,
+                                                           double* __restrict__ part, unsigned* counter) {
+    __shared__ double red[4][8];
+    __shared__ bool last;
     float sq = 0.0f, sx = 0.0f, st = 0.0f;
     int nt = 0;
     const int64_t M4 = M / 4, N4 = N / 4;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     const float4* qn4 = reinterpret_cast<const float4*>(qn);
     const float4* th4 = reinterpret_cast<const float4*>(thr);
     const float4* xn4 = reinterpret_cast<const float4*>(xn);
-    #pragma unroll 4
-    for (int64_t i = threadIdx.x; i < M4; i += blockDim.x) {
+    for (int64_t i = t0; i < M4; i += nth) {
         const float4 a = qn4[i], t = th4[i];
         sq += (a.x + a.y) + (a.z + a.w);
         const float tv[4] = {t.x, t.y, t.z, t.w};
@@ -321,38 +324,42 @@ __global__ void __launch_bounds__(1024) pivot1_decide_kernel(const float* __rest
                 ++nt;
             }
     }
-    #pragma unroll 4
-    for (int64_t j = threadIdx.x; j < N4; j += blockDim.x) {
+    for (int64_t j = t0; j < N4; j += nth) {
         const float4 b = xn4[j];
         sx += (b.x + b.y) + (b.z + b.w);
     }
-    for (int64_t i = 4 * M4 + threadIdx.x; i < M; i += blockDim.x) {
+    for (int64_t i = 4 * M4 + t0; i < M; i += nth) {
         sq += qn[i];
         if (isfinite(thr[i])) {
             st += thr[i];
             ++nt;
         }
     }
-    for (int64_t j = 4 * N4 + threadIdx.x; j < N; j += blockDim.x) sx += xn[j];
-    double v[3] = {(double)sq, (double)sx, (double)st};
+    for (int64_t j = 4 * N4 + t0; j < N; j += nth) sx += xn[j];
+    double v[4] = {(double)sq, (double)sx, (double)st, (double)nt};
     #pragma unroll
-    for (int a = 0; a < 3; ++a) {
+    for (int a = 0; a < 4; ++a) {
         for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(0xFFFFFFFFu, v[a], o);
         if ((threadIdx.x & 31) == 0) red[a][threadIdx.x >> 5] = v[a];
     }
-    // finite-pivot count through the same reduction (as a double)
-    __shared__ double rcnt[32];
-    double c = (double)nt;
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-    if ((threadIdx.x & 31) == 0) rcnt[threadIdx.x >> 5] = c;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += red[threadIdx.x][w];
+        part[blockIdx.x * 4 + threadIdx.x] = acc;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
         double a = 0, b = 0, t = 0, n = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            a += red[0][w];
-            b += red[1][w];
-            t += red[2][w];
-            n += rcnt[w];
+        for (int k = 0; k < (int)gridDim.x; ++k) {
+            a += __ldcg(part + 4 * k);
+            b += __ldcg(part + 4 * k + 1);
+            t += __ldcg(part + 4 * k + 2);
+            n += __ldcg(part + 4 * k + 3);
         }
         const double width = 2.0 * (double)F * (a / (double)M + b / (double)N);
         flag[1] = (n > 0 && width <= (double)ratio * (t / n)) ? 1 : 0;
@@ -360,10 +367,13 @@ __global__ void __launch_bounds__(1024) pivot1_decide_kernel(const float* __rest
 }
 }  // namespace
 
+size_t pivot1_decide_ws_bytes() { return kDecBlocks * 4 * sizeof(double); }
+
 cudaError_t launch_pivot1_decide(const float* thr, const float* qn, int64_t M, const float* xn, int64_t N,
-                                 float F, float ratio, int32_t* flag, cudaStream_t s) {
+                                 float F, float ratio, int32_t* flag, double* part, unsigned* counter,
+                                 cudaStream_t s) {
     if (M == 0 || N == 0) return cudaSuccess;
-    pivot1_decide_kernel<<<1, 1024, 0, s>>>(thr, qn, M, xn, N, F, ratio, flag);
+    pivot1_decide_kernel<<<kDecBlocks, 256, 0, s>>>(thr, qn, M, xn, N, F, ratio, flag, part, counter);
     return cudaGetLastError();
 }
 

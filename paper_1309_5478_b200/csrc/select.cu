@@ -2225,72 +2225,115 @@ constexpr int CR_G = 8;
 #ifndef KNN_CR_ONEHALF
 #define KNN_CR_ONEHALF 1  // one 128-float slice of the candidates at a time (no spills)
 #endif
+#ifndef KNN_CR_T
+#define KNN_CR_T 8  // candidates per lane that the k-th upper bound T is taken from
+#endif
 #ifndef KNN_CR_MINB
 #define KNN_CR_MINB 4  // CTAs per SM of the re-evaluation (4: 64 registers)
 #endif
-__global__ void __launch_bounds__(256, KNN_CR_MINB)
-candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
-                           int cap, int64_t M, int k, int64_t idx_offset,
-                           const float* __restrict__ Q, const float* __restrict__ X, int d,
-                           const float* __restrict__ qn, const float* __restrict__ bq,
-                           const float* __restrict__ bx, const float* __restrict__ thr, float rerr,
-                           int metric, int vec,
-                           int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
-                           int32_t* __restrict__ flag, int gate) {
-    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
-    __shared__ uint32_t heads[8][CS_PER][33];
-    __shared__ uint32_t rlist[8][CR_RCAP];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t row = (int64_t)blockIdx.x * 8 + w;
-    if (row >= M) return;
-    int n = cnt[row];
-    if (n < k) {  // fewer than k lower bounds at or below the pivot: the partition is not exact
-        if (lane == 0) atomicOr(flag, 2);
-        return;
+// Step 1 of the re-evaluation: an upper bound T >= the k-th smallest U of the warp's
+// values v (ukey order, padding 0xFFFFFFFF; at least k valid).  32 buckets of power-of-two
+// width over [min, max] in the key domain (exact integer arithmetic), shared-memory counts,
+// a warp scan for the bucket b* holding the k-th; b*'s values (<= 32) sorted by a warp
+// bitonic network give the k-th exactly; a crowded b* gives its largest value (at least k
+// values are at or below it: still a valid T, one bucket looser).
+template <int PER>
+__device__ __forceinline__ uint32_t kth_upper(const uint32_t (&v)[PER], int k, uint32_t* hist, uint32_t* sbuf) {
+    const int lane = threadIdx.x & 31;
+    uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+    #pragma unroll
+    for (int i = 0; i < PER; ++i)
+        if (v[i] != 0xFFFFFFFFu) {
+            mn = min(mn, v[i]);
+            mx = max(mx, v[i]);
+        }
+    mn = __reduce_min_sync(FULL, mn);
+    mx = __reduce_max_sync(FULL, mx);
+    const uint32_t span = mx - mn;
+    if (span == 0) return mx;
+    const int sh = max(0, 27 - __clz(span));  // span >> sh <= 31
+    hist[lane] = 0u;
+    __syncwarp();
+    #pragma unroll
+    for (int i = 0; i < PER; ++i)
+        if (v[i] != 0xFFFFFFFFu) atomicAdd(hist + ((v[i] - mn) >> sh), 1u);
+    __syncwarp();
+    const uint32_t c = hist[lane];
+    uint32_t incl = c;
+    #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
     }
-    n = n < cap ? n : cap;
-    if (lane == 0 && !(vec & 2)) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
+    const int bs = __ffs(__ballot_sync(FULL, incl >= (uint32_t)k)) - 1;
+    const uint32_t cb = __shfl_sync(FULL, c, bs);
+    const int need = k - (int)__shfl_sync(FULL, incl - c, bs);  // rank in b*, 1..cb
+    if (cb > 32) {
+        uint32_t bm = 0u;
+        #pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (v[i] != 0xFFFFFFFFu && (int)((v[i] - mn) >> sh) <= bs) bm = max(bm, v[i]);
+        return __reduce_max_sync(FULL, bm);
+    }
+    int base = 0;
+    #pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const bool p = v[i] != 0xFFFFFFFFu && (int)((v[i] - mn) >> sh) == bs;
+        const uint32_t m = __ballot_sync(FULL, p);
+        if (p) sbuf[base + __popc(m & ws::lanemask_lt())] = v[i];
+        base += __popc(m);
+    }
+    __syncwarp();
+    uint32_t x = lane < (int)cb ? sbuf[lane] : 0xFFFFFFFFu;
+    #pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+        #pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t o = __shfl_xor_sync(FULL, x, stride);
+            const bool take_min = ((lane & stride) == 0) == ((lane & size) == 0);
+            x = take_min ? min(x, o) : max(x, o);
+        }
+    return __shfl_sync(FULL, x, need - 1);
+}
+
+template <int PER>
+__device__ __forceinline__ void recompute_row(int64_t row, int n, const uint64_t* __restrict__ cent, int cap,
+                                              int k, int64_t idx_offset, const float* __restrict__ Q,
+                                              const float* __restrict__ X, int d, const float* __restrict__ qn,
+                                              const float* __restrict__ bq, const float* __restrict__ bx,
+                                              const float* __restrict__ thr, float rerr, int metric, int vec,
+                                              int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
+                                              int32_t* __restrict__ flag, uint32_t* hist, uint32_t* sbuf,
+                                              uint32_t* rl) {
+    const int lane = threadIdx.x & 31;
     const uint32_t* ri = reinterpret_cast<const uint32_t*>(cent + row * cap);  // (key << 32 | col)
     const uint32_t* rk = ri + 1;
     const float qnr = __ldg(qn + row), bqr = __ldg(bq + row);
-    // 1. T
-    const int n1 = n < 32 * CR_PER ? n : 32 * CR_PER;
-    uint32_t v[CR_PER], lk[CR_PER], li[CR_PER];
+    // 1. T from the first <= 32 PER candidates (a subset's k-th U bounds the list's from above)
+    const int n1 = n < 32 * PER ? n : 32 * PER;
+    uint32_t v[PER], lk[PER], li[PER];
     #pragma unroll
-    for (int i = 0; i < CR_PER; ++i) {
+    for (int i = 0; i < PER; ++i) {
         const int pos = lane + 32 * i;
         lk[i] = pos < n1 ? __ldg(rk + 2 * pos) : 0xFFFFFFFFu;
         li[i] = pos < n1 ? __ldg(ri + 2 * pos) : 0u;
     }
     #pragma unroll
-    for (int i = 0; i < CR_PER; ++i) {
+    for (int i = 0; i < PER; ++i) {
         const float bj = lane + 32 * i < n1 ? __ldg(bx + li[i]) : 0.0f;
         v[i] = lk[i] == 0xFFFFFFFFu ? 0xFFFFFFFFu : ukey(__fmaf_ru(2.0f, __fadd_ru(bqr, bj), ukey_to_float(lk[i])));
     }
-    sort16(v);
-    #pragma unroll
-    for (int i = 0; i < CS_PER; ++i) heads[w][i][lane] = v[i];
-    __syncwarp();
-    uint32_t h = v[0], Tk = 0;
-    int p = 0;
-    for (int c = 0; c < k;) {
-        const uint32_t mn = __reduce_min_sync(FULL, h);
-        const bool mine = h == mn;
-        c += __popc(__ballot_sync(FULL, mine));
-        Tk = mn;
-        if (mine) h = ++p < CS_PER ? heads[w][p][lane] : 0xFFFFFFFFu;
-    }
-    const float T = ukey_to_float(Tk);
+    const float T = ukey_to_float(kth_upper<PER>(v, k, hist, sbuf));
     // every candidate whose re-evaluated value can reach the k-th re-evaluated value
     const uint32_t Tf = ukey(T + (4.0f * rerr + 0x1p-20f) * (fabsf(T) + qnr));
     // 2. R (the first 512 from registers)
     int nr = 0;
     #pragma unroll
-    for (int i = 0; i < CR_PER; ++i) {
+    for (int i = 0; i < PER; ++i) {
         const bool keep = lk[i] <= Tf;  // padding is 0xFFFFFFFF
         const uint32_t bm = __ballot_sync(FULL, keep);
         const int slot = nr + __popc(bm & ws::lanemask_lt());
-        if (keep && slot < CR_RCAP) rlist[w][slot] = li[i];
+        if (keep && slot < CR_RCAP) rl[slot] = li[i];
         nr += __popc(bm);
     }
     for (int base = n1; base < n; base += 32) {
@@ -2298,7 +2341,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
         const bool keep = pos < n && __ldg(rk + 2 * pos) <= Tf;
         const uint32_t bm = __ballot_sync(FULL, keep);
         const int slot = nr + __popc(bm & ws::lanemask_lt());
-        if (keep && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + 2 * pos);
+        if (keep && slot < CR_RCAP) rl[slot] = __ldg(ri + 2 * pos);
         nr += __popc(bm);
     }
     if (lane == 0 && (vec & 2))  // diagnostic (KNN_RECOMP_STATS): count |R| instead
@@ -2319,7 +2362,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
             const bool keep = pos < n && __ldg(rk + 2 * pos) <= Tf;
             const uint32_t bm = __ballot_sync(FULL, keep);
             const int slot = ridx + __popc(bm & ws::lanemask_lt()) - win * CR_RCAP;
-            if (keep && slot >= 0 && slot < CR_RCAP) rlist[w][slot] = __ldg(ri + 2 * pos);
+            if (keep && slot >= 0 && slot < CR_RCAP) rl[slot] = __ldg(ri + 2 * pos);
             ridx += __popc(bm);
         }
         __syncwarp();
@@ -2333,12 +2376,16 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
             #pragma unroll
             for (int u = 0; u < CR_G; ++u) {
                 const int c = g + t0 + u;
-                id[u] = rlist[w][c < nr ? c : g + t0];
+                id[u] = rl[c < nr ? c : g + t0];
                 xr[u] = X + (int64_t)id[u] * d;
             }
             float acc[CR_G];
+            uint64_t acc2[CR_G];
             #pragma unroll
-            for (int u = 0; u < CR_G; ++u) acc[u] = 0.0f;
+            for (int u = 0; u < CR_G; ++u) {
+                acc[u] = 0.0f;
+                acc2[u] = 0ull;
+            }
             if (vec & 1) {
 #if KNN_CR_ONEHALF
                 // one 128-float slice at a time: CR_G float4 loads in flight per lane (32
@@ -2349,15 +2396,20 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
                     float4 xv[CR_G];
                     #pragma unroll
                     for (int u = 0; u < CR_G; ++u) xv[u] = __ldg(reinterpret_cast<const float4*>(xr[u] + t));
+                    // two components per FADD2 / FFMA2 (even / odd partial sums per lane)
                     #pragma unroll
                     for (int u = 0; u < CR_G; ++u) {
-                        const float e0 = qv.x - xv[u].x, e1 = qv.y - xv[u].y;
-                        const float e2 = qv.z - xv[u].z, e3 = qv.w - xv[u].w;
-                        acc[u] = fmaf(e0, e0, acc[u]);
-                        acc[u] = fmaf(e1, e1, acc[u]);
-                        acc[u] = fmaf(e2, e2, acc[u]);
-                        acc[u] = fmaf(e3, e3, acc[u]);
+                        const uint64_t e01 = f2_sub(f2_pack(qv.x, qv.y), f2_pack(xv[u].x, xv[u].y));
+                        const uint64_t e23 = f2_sub(f2_pack(qv.z, qv.w), f2_pack(xv[u].z, xv[u].w));
+                        acc2[u] = f2_fma(e01, e01, acc2[u]);
+                        acc2[u] = f2_fma(e23, e23, acc2[u]);
                     }
+                }
+                #pragma unroll
+                for (int u = 0; u < CR_G; ++u) {
+                    float lo, hi;
+                    f2_unpack(acc2[u], lo, hi);
+                    acc[u] = lo + hi;
                 }
 #else
                 for (int t = 4 * lane; t < d; t += 256) {
@@ -2431,7 +2483,7 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
             const float su = __shfl_sync(FULL, tot, ((lane - t0) & 7) * 4);
             if (lane >= t0 && lane < t0 + CR_G && g + lane < nr) {
                 const float val = metric == 1 ? sqrtf(su) : su;
-                mine = (uint64_t)ukey(val) << 32 | rlist[w][g + lane];
+                mine = (uint64_t)ukey(val) << 32 | rl[g + lane];
             }
         }
         uint64_t b[1] = {mine};
@@ -2456,6 +2508,37 @@ candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __re
     if (lane < k) {
         out_idx[row * k + lane] = (int32_t)((int64_t)(uint32_t)best + idx_offset);
         out_dist[row * k + lane] = ukey_to_float((uint32_t)(best >> 32));
+    }
+}
+
+
+__global__ void __launch_bounds__(256, KNN_CR_MINB)
+candidate_recompute_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                           int cap, int64_t M, int k, int64_t idx_offset,
+                           const float* __restrict__ Q, const float* __restrict__ X, int d,
+                           const float* __restrict__ qn, const float* __restrict__ bq,
+                           const float* __restrict__ bx, const float* __restrict__ thr, float rerr,
+                           int metric, int vec,
+                           int32_t* __restrict__ out_idx, float* __restrict__ out_dist,
+                           int32_t* __restrict__ flag, int gate) {
+    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
+    __shared__ uint32_t hist[8][32], sbuf[8][32];
+    __shared__ uint32_t rlist[8][CR_RCAP];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // rows strided over a grid of a few CTAs per SM (a gated-off launch costs little)
+    for (int64_t row = (int64_t)blockIdx.x * 8 + w; row < M; row += (int64_t)gridDim.x * 8) {
+        int n = cnt[row];
+        if (n < k) {  // fewer than k lower bounds at or below the pivot: the partition is not exact
+            if (lane == 0) atomicOr(flag, 2);
+            continue;
+        }
+        n = n < cap ? n : cap;
+        if (lane == 0 && !(vec & 2)) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), (unsigned long long)n);
+        // (T from the first <= 256 candidates: longer lists get a slightly looser T, their
+        // remaining candidates join R through the scan of step 2)
+        recompute_row<KNN_CR_T>(row, n, cent, cap, k, idx_offset, Q, X, d, qn, bq, bx, thr, rerr, metric, vec, out_idx,
+                            out_dist, flag, hist[w], sbuf[w], rlist[w]);
+        __syncwarp();
     }
 }
 
@@ -3335,7 +3418,11 @@ cudaError_t launch_candidate_recompute(const int32_t* cnt, const uint64_t* cent,
     const float rerr = (float)(((d + 31) / 32 + 8) * std::ldexp(1.0, -24));
     const int vec = ((d % 4 == 0) && ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(X)) & 15) == 0) |
                     (getenv_flag("KNN_RECOMP_STATS") ? 2 : 0);
-    candidate_recompute_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset, Q,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>(ceil_div(M, 8), (int64_t)sms * KNN_CR_MINB);
+    candidate_recompute_kernel<<<(unsigned)blocks, 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset, Q,
                                                                        X, d, qn, bq, bx, thr, rerr, metric, vec,
                                                                        out_idx, out_dist, flag, gate);
     return cudaGetLastError();
