@@ -212,9 +212,16 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
  *     with the sign bit set, for values >= +0).  Asynchronous.  Directly after
  *     knn_graph_pivots on the same ctx, points, metric and stream it reuses the operands
  *     that call prepared (no second pass over X).
+ *     For k <= 32 and the L2 metrics (unless KNN_PLAN_PIVOT_EXACT or KNN_PIVOT1=0) it
+ *     queues, as knn_graph does, the single-product partition (keys = lower bounds of the
+ *     distance) next to the FP32-accurate one, the device choosing one from all N pivots
+ *     (thr must then hold every rank's pivots); the choice is kept in the ctx.
  *  3. knn_graph_gather_select: for rows [row0, row0+rows), concatenates the G ranks' lists
  *     (host arrays of G device pointers; peers' lists mapped with knn_ipc_open, read over
- *     NVLink inside the kernel) and runs the exact candidate select into out (rows×k).
+ *     NVLink inside the kernel) and runs the exact candidate select into out (rows×k) —
+ *     after a single-product partition on this ctx, the fp32 re-evaluation of the rows'
+ *     survivors from the points X and the pivots thr passed to knn_graph_partition (both
+ *     must still be alive).
  *     Blocking; returns KNN_ERR_INTERNAL when a list overflowed or a row's certificate
  *     failed (fewer than k candidates): the caller then falls back to another plan.
  * k <= N-1; N >= 16384 and 1 <= k <= 1024 (else KNN_ERR_UNSUPPORTED); tensor-core path. */

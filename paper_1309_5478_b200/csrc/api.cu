@@ -497,6 +497,7 @@ knn_status knn_ctx_destroy(knn_ctx_t ctx) {
     for (auto e : ctx->ev_chunk) cudaEventDestroy(e);
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
     if (ctx->pv_flag) cudaFree(ctx->pv_flag);
+    if (ctx->p3_buf) cudaFree(ctx->p3_buf);
     comm_release(ctx);
     delete ctx;
     return KNN_OK;
@@ -1153,6 +1154,54 @@ knn_status graph_shard_check(knn_ctx_t ctx, const float* X, int64_t N, int32_t d
     if (!metric_ok(ctx, metric, &st)) return st;
     return KNN_OK;
 }
+
+// The workspace prefix of knn_graph_pivots and knn_graph_partition (same offsets, so the
+// partition reuses what the pivots call prepared): flag, split operands and, L2, the
+// per-point bound terms (prep.cu launch_bound_norms; bnd goes to ctx->p3_buf).
+struct ShardPrep {
+    int32_t* flag = nullptr;
+    Prepared px{};
+    float *eps = nullptr, *nsc = nullptr, *ninf = nullptr;
+    double* dec = nullptr;
+};
+void shard_prefix(Carve& c, ShardPrep& p, int64_t N, int32_t d_pad, bool l2) {
+    p.flag = c.take<int32_t>(8);  // [0] flags, [1] plan, [2..3] candidates, [4] max eps2, [5] decide counter
+    p.px.sqn = c.take<float>(round_up(N, knn::kColPad));
+    p.px.rs = c.take<float>(round_up(N, knn::kColPad));
+    p.px.hi = c.take<__half>((size_t)N * d_pad);
+    p.px.lo = c.take<__half>((size_t)N * d_pad);
+    if (l2) {
+        p.eps = c.take<float>(round_up(N, knn::kColPad));
+        p.nsc = c.take<float>(round_up(N, knn::kColPad));
+        p.ninf = c.take<float>(round_up(N, knn::kColPad));
+        p.dec = c.take<double>(knn::pivot1_decide_ws_bytes() / sizeof(double));
+    }
+}
+
+// prep of all N points (+ L2: the bound terms, one t for the call; sqn and bnd copied to
+// ctx->p3_buf for knn_graph_gather_select)
+knn_status shard_prep(knn_ctx* ctx, const ShardPrep& p, const float* X, int64_t N, int32_t d, int32_t d_pad,
+                      int32_t metric, cudaStream_t s) {
+    const bool l2 = metric <= KNN_L2;
+    KNN_CUDA(cudaMemsetAsync(p.flag, 0, 8 * sizeof(int32_t), s));
+    KNN_TRY(ensure_pv_flag(ctx));
+    {
+        Timed t(ctx, KNN_KERNEL_PREP, s);
+        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, p.px.sqn, p.px.rs, p.px.hi, p.px.lo, ctx->pv_flag, metric, s,
+                                  l2 ? p.eps : nullptr, l2 ? reinterpret_cast<float*>(p.flag + 4) : nullptr));
+        t.done();
+    }
+    if (l2) {
+        const int64_t np = round_up(N, knn::kColPad);
+        KNN_TRY(ensure(ctx, &ctx->p3_buf, &ctx->p3_size, 2 * np * sizeof(float)));
+        float* bnd = static_cast<float*>(ctx->p3_buf) + np;
+        KNN_CUDA(knn::launch_bound_norms(p.px.sqn, p.eps, np, reinterpret_cast<float*>(p.flag + 4), d_pad, p.nsc,
+                                         p.ninf, bnd, s));
+        KNN_CUDA(cudaMemcpyAsync(ctx->p3_buf, p.px.sqn, np * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        ctx->launches++;
+    }
+    return KNN_OK;
+}
 }  // namespace
 
 knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric,
@@ -1168,15 +1217,13 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     const int64_t S = small ? round_up(N / ctx->pivot_div, 256)
                             : round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
     if (small && S / 32 < kk + 1) return fail(ctx, KNN_ERR_UNSUPPORTED, "sample too small for k");
-    Prepared px{}, smp{};
+    const bool l2 = metric <= KNN_L2;
+    ShardPrep sp;
+    Prepared smp{};
     float *D = nullptr, *smax = nullptr;
-    int32_t *flag = nullptr, *cnt = nullptr;
+    int32_t* cnt = nullptr;
     auto layout = [&](Carve& c) {
-        flag = c.take<int32_t>(4);
-        px.sqn = c.take<float>(round_up(N, knn::kColPad));
-        px.rs = c.take<float>(round_up(N, knn::kColPad));
-        px.hi = c.take<__half>((size_t)N * d_pad);
-        px.lo = c.take<__half>((size_t)N * d_pad);
+        shard_prefix(c, sp, N, d_pad, l2);
         smp.sqn = c.take<float>(round_up(S, knn::kColPad));
         smp.rs = c.take<float>(round_up(S, knn::kColPad));
         smp.hi = c.take<__half>((size_t)S * d_pad);
@@ -1190,28 +1237,27 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve);
-    KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    const Prepared& px = sp.px;
     KNN_TRY(ensure_pv_flag(ctx));
     KNN_CUDA(cudaMemsetAsync(ctx->pv_flag, 0, 4 * sizeof(int32_t), s));
-    {
-        Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, ctx->pv_flag, metric, s));
-        t.done();
-    }
+    KNN_TRY(shard_prep(ctx, sp, X, N, d, d_pad, metric, s));
     ctx->prep_X = X;  // knn_graph_partition may reuse px (same carve offsets, ws untouched)
     ctx->prep_N = N;
     ctx->prep_d = d;
     ctx->prep_metric = metric;
     ctx->launches++;
-    KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo, smp.sqn,
-                                       smp.rs, small ? smax : nullptr, s));
-    knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, px.sqn + row0, px.rs + row0, rows,
-                       smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
+    // (L2: the sample pass on the per-point upper-bound norms ninf)
+    KNN_CUDA(knn::launch_gather_sample(px.hi, px.lo, l2 ? sp.ninf : px.sqn, px.rs, N, S, d_pad, smp.hi, smp.lo,
+                                       smp.sqn, smp.rs, small ? smax : nullptr, s));
+    knn::TcOperands op{px.hi + row0 * d_pad, px.lo + row0 * d_pad, (l2 ? sp.ninf : px.sqn) + row0, px.rs + row0,
+                       rows, smp.hi, smp.lo, smp.sqn, smp.rs, S, d_pad};
     Timed tg(ctx, KNN_KERNEL_GEMM, s);
     if (small)
-        KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s, smax));
+        KNN_CUDA(knn::launch_dist_tc_mins(op, S, metric, KNN_NO_SELF, D, ctx->pivot_margin, ctx->num_sms, s, smax,
+                                          l2));
     else
-        KNN_CUDA(knn::launch_dist_tc_sample(op, S, metric, KNN_NO_SELF, D, S, ctx->pivot_margin, ctx->num_sms, s));
+        KNN_CUDA(knn::launch_dist_tc_sample(op, S, metric, KNN_NO_SELF, D, S, ctx->pivot_margin, ctx->num_sms, s,
+                                            l2));
     tg.done();
     Timed tp(ctx, KNN_KERNEL_SELECT, s);
     if (small) {
@@ -1236,39 +1282,66 @@ knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t
     KNN_TRY(set_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
-    Prepared px{};
-    int32_t* flag = nullptr;
-    auto layout = [&](Carve& c) {
-        flag = c.take<int32_t>(4);
-        px.sqn = c.take<float>(round_up(N, knn::kColPad));
-        px.rs = c.take<float>(round_up(N, knn::kColPad));
-        px.hi = c.take<__half>((size_t)N * d_pad);
-        px.lo = c.take<__half>((size_t)N * d_pad);
-    };
+    const bool l2 = metric <= KNN_L2;
+    ShardPrep sp;
+    auto layout = [&](Carve& c) { shard_prefix(c, sp, N, d_pad, l2); };
     Carve probe{nullptr};
     layout(probe);
     // the operands knn_graph_pivots prepared are still at the same offsets of ws if the
     // last ws user was that call on the same points (ensure() does not reallocate: this
     // call needs less workspace)
     const bool reuse = ctx->prep_X == X && ctx->prep_N == N && ctx->prep_d == d && ctx->prep_metric == metric &&
-                       probe.off + 256 <= ctx->ws_size;
+                       probe.off + 256 <= ctx->ws_size && (!l2 || (ctx->p3_buf && ctx->p3_size >= 2 * round_up(N, knn::kColPad) * sizeof(float)));
     KNN_TRY(ensure(ctx, &ctx->ws, &ctx->ws_size, probe.off + 256));
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve);
+    const Prepared& px = sp.px;
+    int32_t* flag = sp.flag;
     KNN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)N * sizeof(int32_t), s));
     if (!reuse) {
-        KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
-        KNN_TRY(ensure_pv_flag(ctx));
-        Timed t(ctx, KNN_KERNEL_PREP, s);
-        KNN_CUDA(knn::launch_prep(X, N, d, d_pad, px.sqn, px.rs, px.hi, px.lo, ctx->pv_flag, metric, s));
-        t.done();
+        KNN_TRY(shard_prep(ctx, sp, X, N, d, d_pad, metric, s));
+    } else {
+        KNN_CUDA(cudaMemsetAsync(flag, 0, 8 * sizeof(int32_t), s));
     }
+    ctx->prep_X = X;  // (ensure() above cleared it; the operands are those of X)
+    ctx->prep_N = N;
+    ctx->prep_d = d;
+    ctx->prep_metric = metric;
     knn::TcOperands op{px.hi, px.lo, px.sqn, px.rs, N, px.hi, px.lo, px.sqn, px.rs, N, d_pad};
+    // k <= 32, L2: the single-product partition as in the one-GPU call,
+    // chosen on the device from ALL N pivots (every rank takes the same decision: the same
+    // all-gathered pivots and bound terms) unless KNN_PLAN_PIVOT_EXACT / KNN_PIVOT1=0
+    const bool p1_ok = l2 && k <= 32 && ctx->plan != KNN_PLAN_PIVOT_EXACT && ctx->pivot1 != 0;
+    const bool p1_auto = p1_ok && ctx->pivot1 < 0, one = p1_ok && ctx->pivot1 > 0;
+    if (p1_auto) {
+        const float* bnd = static_cast<const float*>(ctx->p3_buf) + round_up(N, knn::kColPad);
+        // (the decision lives in ctx->pv_flag[1]: knn_graph_gather_select's workspace may
+        // be reallocated, pv_flag is not)
+        KNN_CUDA(knn::launch_pivot1_decide(thr, bnd, N, bnd, N, 1.0f, ctx->pivot1_ratio, ctx->pv_flag, sp.dec,
+                                           reinterpret_cast<unsigned*>(flag + 5), s));
+        ctx->launches++;
+    }
+    int32_t* pflag = p1_auto ? ctx->pv_flag : flag;  // the gated pair reads pv_flag[1]
     Timed tg(ctx, KNN_KERNEL_FUSED, s);
-    KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, 0, true, thr, cnt, cent, cap, flag, ctx->num_sms, s,
-                                       unit_lo, unit_hi));
+    if (p1_ok) {
+        knn::TcOperands op1 = op;
+        op1.qn = sp.nsc;
+        op1.xn = sp.nsc;
+        KNN_CUDA(knn::launch_dist_tc_pivot1(op1, metric, 0, true, thr, cnt, cent, cap, pflag, ctx->num_sms, s,
+                                            p1_auto ? 1 : -1, unit_lo, unit_hi));
+    }
+    if (!one)
+        KNN_CUDA(knn::launch_dist_tc_pivot(op, metric, 0, true, thr, cnt, cent, cap, pflag, ctx->num_sms, s,
+                                           unit_lo, unit_hi, false, p1_auto ? 0 : -1));
+    ctx->launches += p1_auto ? 1 : 0;
     tg.done();
-    ctx->last_plan = 3;
+    ctx->p3_state = p1_auto ? 1 : one ? 2 : 0;
+    ctx->p3_X = X;
+    ctx->p3_thr = thr;
+    ctx->p3_N = N;
+    ctx->p3_d = d;
+    ctx->p3_metric = metric;
+    ctx->last_plan = one ? 5 : 3;
     return KNN_OK;
 }
 
@@ -1298,12 +1371,31 @@ knn_status knn_graph_gather_select(knn_ctx_t ctx, int32_t G, const int32_t* cons
     Carve carve{static_cast<char*>(ctx->ws)};
     layout(carve);
     KNN_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
+    // the single-product partition's lists (lower bounds): re-evaluation from the points
+    const int p1 = ctx->p3_state != 0 && k <= 32 && ctx->p3_N == N && ctx->p3_X && ctx->p3_thr && ctx->p3_buf &&
+                           ctx->pv_flag
+                       ? ctx->p3_state : 0;
+    if (p1 == 1)  // the device's partition choice (knn_graph_partition) into flag[1]
+        KNN_CUDA(cudaMemcpyAsync(flag + 1, ctx->pv_flag + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     Timed tm(ctx, KNN_KERNEL_MERGE, s);
     KNN_CUDA(knn::launch_gather_lists(cnts, cents, G, cap, row0, rows, cap, cnt, cent, flag, s));
-    if (k <= 32)
+    if (p1) {
+        const int64_t np = round_up(N, knn::kColPad);
+        const float* sqn = static_cast<const float*>(ctx->p3_buf);
+        const float* bnd = sqn + np;
+        const int32_t d = ctx->p3_d;
+        KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, rows, k, 0, ctx->p3_X + row0 * d, ctx->p3_X, d,
+                                                 sqn + row0, bnd + row0, bnd, ctx->p3_thr + row0, ctx->p3_metric,
+                                                 out_idx, out_dist, flag, s, p1 == 1 ? 1 : -1));
+        if (p1 == 1)
+            KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, rows, k, 0, out_idx, out_dist, flag, s, 0));
+        ctx->last_plan = p1 == 1 ? 3 : 5;
+        ctx->last_plan_auto1 = p1 == 1;
+    } else if (k <= 32) {
         KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, rows, k, 0, out_idx, out_dist, flag, s));
-    else
+    } else {
         KNN_CUDA(knn::launch_candidate_select_large(cnt, cent, cap, rows, k, 0, out_idx, out_dist, flag, redo, s));
+    }
     tm.done();
     knn_status st = finish_blocking(ctx, s);
     drain_profile(ctx);

@@ -64,6 +64,17 @@ struct knn_ctx {
     // knn_graph_partition (a dedicated slice: the workspace flag is reset by every call),
     // reported by knn_graph_gather_select as KNN_ERR_NONFINITE
     int32_t* pv_flag = nullptr;
+    // Par-3 phases with the single-product partition (L2, k <= 32): knn_graph_partition
+    // queues the device-chosen pair (p3_state 1) or the single-product one alone (2);
+    // knn_graph_gather_select then re-evaluates from p3_X with the prep norms and bound terms
+    // kept in p3_buf ([sqn | bnd], roundup(N, 256) floats each) and the pivots p3_thr
+    int32_t p3_state = 0;
+    const float* p3_X = nullptr;
+    const float* p3_thr = nullptr;
+    int64_t p3_N = 0;
+    int32_t p3_d = 0, p3_metric = -1;
+    void* p3_buf = nullptr;
+    size_t p3_size = 0;
     // CUDA IPC mappings opened by knn_ipc_open: handle bytes -> mapped base
     std::vector<std::pair<std::string, void*>> ipc_open;
     // multi-GPU (shard.cu): communicator + the sharded calls' own buffers

@@ -2044,17 +2044,13 @@ __device__ __forceinline__ void sort16(uint32_t (&v)[CS_PER]) {
                 }
             }
 }
-__global__ void __launch_bounds__(256)
-candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
-                        int cap, int64_t M, int k,
-                        int64_t idx_offset, int32_t* __restrict__ out_idx,
-                        float* __restrict__ out_dist, int32_t* __restrict__ flag, int gate) {
-    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
-    __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
-    __shared__ uint32_t hist[8][256], skey[8][64], sidx[8][64];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t row = (int64_t)blockIdx.x * 8 + w;
-    if (row >= M) return;
+__device__ __forceinline__ void candidate_select_row(int64_t row, const int32_t* __restrict__ cnt,
+                                                     const uint64_t* __restrict__ cent, int cap, int k,
+                                                     int64_t idx_offset, int32_t* __restrict__ out_idx,
+                                                     float* __restrict__ out_dist, int32_t* __restrict__ flag,
+                                                     uint32_t (*heads_w)[33], uint32_t* hist_w, uint32_t* skey_w,
+                                                     uint32_t* sidx_w) {
+    const int lane = threadIdx.x & 31;
     int n = cnt[row];
     // certificate of the partition: k elements at or below the pivot means every element of
     // the true k nearest (ties included) is a candidate; otherwise redo (flag bit 2)
@@ -2092,16 +2088,16 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                 const float fmn = ukey_to_float(kmn), fmx = ukey_to_float(kmx);
                 const float scale = 32.0f / (fmx - fmn);
                 if (fmn >= 0.0f && fmx > fmn && isfinite(fmx) && isfinite(scale)) {
-                    hist[w][lane] = 0;
+                    hist_w[lane] = 0;
                     __syncwarp();
                     auto bucket = [&](uint32_t u) -> uint32_t {
                         return min((uint32_t)((ukey_to_float(u) - fmn) * scale), 31u);
                     };
                     #pragma unroll
                     for (int i = 0; i < CS_PER; ++i)
-                        if (lane + 32 * i < n) atomicAdd(&hist[w][bucket(uk[i])], 1u);
+                        if (lane + 32 * i < n) atomicAdd(&hist_w[bucket(uk[i])], 1u);
                     __syncwarp();
-                    const uint32_t c = hist[w][lane];
+                    const uint32_t c = hist_w[lane];
                     uint32_t incl = c;
                     #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
@@ -2118,8 +2114,8 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                             const uint32_t bm = __ballot_sync(FULL, p2);
                             if (p2) {
                                 const int pos = base + __popc(bm & ws::lanemask_lt());
-                                skey[w][pos] = uk[i];
-                                sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
+                                skey_w[pos] = uk[i];
+                                sidx_w[pos] = __ldg(ri + 2 * (lane + 32 * i));
                             }
                             base += __popc(bm);
                         }
@@ -2128,7 +2124,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                         #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int e = h * 32 + lane;
-                            b2[h] = e < base ? ((uint64_t)skey[w][e] << 32 | sidx[w][e]) : ~0ull;
+                            b2[h] = e < base ? ((uint64_t)skey_w[e] << 32 | sidx_w[e]) : ~0ull;
                         }
                         ws::warp_bitonic<2>(b2);
                         if (lane < k) {
@@ -2143,7 +2139,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
             for (int i = 0; i < CS_PER; ++i) v[i] = uk[i];
             sort16(v);
             #pragma unroll
-            for (int i = 0; i < CS_PER; ++i) heads[w][i][lane] = v[i];
+            for (int i = 0; i < CS_PER; ++i) heads_w[i][lane] = v[i];
             __syncwarp();
             uint32_t h = v[0], T = 0;
             int p = 0;
@@ -2152,7 +2148,7 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                 const bool mine = h == mn;
                 c += __popc(__ballot_sync(FULL, mine));
                 T = mn;
-                if (mine) h = ++p < CS_PER ? heads[w][p][lane] : 0xFFFFFFFFu;
+                if (mine) h = ++p < CS_PER ? heads_w[p][lane] : 0xFFFFFFFFu;
             }
             // compact the pairs with key < T (fewer than k), then those with key == T
             int base = 0;
@@ -2162,8 +2158,8 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                 const uint32_t bm = __ballot_sync(FULL, p2);
                 if (p2) {
                     const int pos = base + __popc(bm & ws::lanemask_lt());
-                    skey[w][pos] = uk[i];
-                    sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
+                    skey_w[pos] = uk[i];
+                    sidx_w[pos] = __ldg(ri + 2 * (lane + 32 * i));
                 }
                 base += __popc(bm);
             }
@@ -2174,23 +2170,23 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
                 const uint32_t bm = __ballot_sync(FULL, p2);
                 const int pos = base + eq + __popc(bm & ws::lanemask_lt());
                 if (p2 && pos < 32) {
-                    skey[w][pos] = T;
-                    sidx[w][pos] = __ldg(ri + 2 * (lane + 32 * i));
+                    skey_w[pos] = T;
+                    sidx_w[pos] = __ldg(ri + 2 * (lane + 32 * i));
                 }
                 eq += __popc(bm);
             }
             __syncwarp();
             if (base + eq <= 32) {  // every tie at T kept: the k best are among them
-                fk = skey[w];
-                fi = sidx[w];
+                fk = skey_w;
+                fi = sidx_w;
                 m = base + eq;
                 done = true;
             }
         }
         if (!done) {
-            ws::warp_select_k<2>(rk, ri, n, k, skey[w], sidx[w], hist[w]);
-            fk = skey[w];
-            fi = sidx[w];
+            ws::warp_select_k<2>(rk, ri, n, k, skey_w, sidx_w, hist_w);
+            fk = skey_w;
+            fi = sidx_w;
             m = k;
         }
     }
@@ -2201,6 +2197,24 @@ candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restr
         const uint32_t key = (uint32_t)(v[0] >> 32);
         out_idx[row * k + lane] = key == 0xFFFFFFFFu ? -1 : (int32_t)((int64_t)(uint32_t)v[0] + idx_offset);
         out_dist[row * k + lane] = key == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : ukey_to_float(key);
+    }
+}
+
+
+__global__ void __launch_bounds__(256)
+candidate_select_kernel(const int32_t* __restrict__ cnt, const uint64_t* __restrict__ cent,
+                        int cap, int64_t M, int k,
+                        int64_t idx_offset, int32_t* __restrict__ out_idx,
+                        float* __restrict__ out_dist, int32_t* __restrict__ flag, int gate) {
+    if (gate >= 0 && flag[1] != gate) return;  // the other partition ran (device plan choice)
+    __shared__ uint32_t heads[8][CS_PER][33];  // [warp][position][lane]
+    __shared__ uint32_t hist[8][256], skey[8][64], sidx[8][64];
+    const int w = threadIdx.x >> 5;
+    // rows strided over a grid of a few CTAs per SM (a gated-off launch costs little)
+    for (int64_t row = (int64_t)blockIdx.x * 8 + w; row < M; row += (int64_t)gridDim.x * 8) {
+        candidate_select_row(row, cnt, cent, cap, k, idx_offset, out_idx, out_dist, flag, heads[w], hist[w], skey[w],
+                             sidx[w]);
+        __syncwarp();
     }
 }
 
@@ -3289,7 +3303,11 @@ cudaError_t launch_candidate_select(const int32_t* cnt, const uint64_t* cent,
                                     int32_t gate) {
     if (M == 0) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
-    candidate_select_kernel<<<(unsigned)ceil_div(M, 8), 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>(ceil_div(M, 8), (int64_t)sms * 4);
+    candidate_select_kernel<<<(unsigned)blocks, 256, 0, s>>>(cnt, cent, cap, M, k, idx_offset,
                                                                     out_idx, out_dist, flag, gate);
     return cudaGetLastError();
 }

@@ -146,7 +146,8 @@ def _worker(rank, world, port, case, q):
     try:
         sharded.init()  # gloo group: the library's host-callback transport
         kn = knn()
-        kn.set_plan(kn.PLAN_PIVOT_EXACT)  # (the Par-1 fallback's blocks: as the reference)
+        if os.environ.get("KNN_TEST_AUTO_PLAN") != "1":
+            kn.set_plan(kn.PLAN_PIVOT_EXACT)  # (the Par-1 fallback's blocks: as the reference)
         assert kn.comm_info() == (2, rank, world)
         X = torch.from_numpy(datagen.points(N, d, "gauss", seed=93)).cuda()
         if rank != 0:
@@ -198,5 +199,89 @@ def test_two_processes_one_gpu(case):
     want_mode = knn().SHARD_MODES["query" if no_ipc else mode]
     for _, i, dd, m in res:
         assert m == want_mode
+        assert np.array_equal(i, ri.cpu().numpy())
+        assert np.array_equal(dd.view(np.uint32), rd.cpu().numpy().view(np.uint32))
+
+
+# ------------- Par-3 with the single-product partition (the automatic plan) ---
+@pytest.mark.parametrize("G,k,metric", [(2, 32, 0), (3, 10, 1), (1, 16, 0)])
+def test_emulated_ranks_auto_plan_equal_graph(G, k, metric):
+    """Under the automatic plan the Par-3 phases run the single-product partition (the
+    decision taken on the device from all N pivots, the same on every rank) and re-evaluate
+    each rank's rows from the points: bit-identical to the one-GPU automatic call, which
+    takes the same decision (both lists hold the same lower bounds; the re-evaluated values
+    do not depend on the list order)."""
+    kn = knn()
+    kn.set_plan(kn.PLAN_AUTO)
+    N, d = 17000, 40
+    X = torch.from_numpy(datagen.points(N, d, "uniform", seed=G * 100 + k + 7)).cuda()
+    ri, rd = reference(X, k, metric)
+    assert kn.last_plan() == 5, kn.last_plan()
+    npad = -(-N // 256) * 256
+    thr = torch.full((npad,), float("nan"), device="cuda")
+    per = -(-N // G)
+    for g in range(G):
+        lo, hi = g * per, min(N, (g + 1) * per)
+        kn.graph_pivots(X, k, lo, hi - lo, thr, metric=metric)
+    units = kn.graph_units(N)
+    cap = kn.graph_list_cap(k)
+    lists = []
+    for g in range(G):
+        ulo, uhi = units * g // G, units * (g + 1) // G
+        cnt = torch.zeros(N, dtype=torch.int32, device="cuda")
+        ce = torch.empty((N, cap), dtype=torch.int64, device="cuda")
+        kn.graph_partition(X, k, thr, ulo, uhi, cnt, ce, metric=metric)
+        lists.append((cnt, ce))
+    torch.cuda.synchronize()
+    parts_i, parts_d = [], []
+    for g in range(G):
+        lo, hi = g * per, min(N, (g + 1) * per)
+        i, dd = kn.graph_gather_select([l[0].data_ptr() for l in lists], [l[1].data_ptr() for l in lists], cap, N,
+                                       k, lo, hi - lo)
+        assert kn.last_plan() == 5, kn.last_plan()
+        parts_i.append(i)
+        parts_d.append(dd)
+    gi, gd = torch.cat(parts_i), torch.cat(parts_d)
+    assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_one_rank_sym_sharded_auto_plan(monkeypatch):
+    monkeypatch.setenv("KNN_SHARD_G1_PHASES", "1")
+    kn = knn()
+    kn.set_plan(kn.PLAN_AUTO)
+    kn.comm_destroy()
+    X = torch.from_numpy(datagen.points(20000, 64, "gauss", seed=777)).cuda()
+    ri, rd = reference(X, 24)
+    assert kn.last_plan() == 5, kn.last_plan()
+    for _ in range(2):
+        gi, gd = kn.graph_sharded(X, 24, mode="sym")
+        assert kn.last_shard_mode() == kn.SHARD_MODES["sym"]
+        assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+
+
+def test_two_processes_one_gpu_auto_plan(monkeypatch):
+    """The two-process Par-3 run (host transport, CUDA IPC list reads) under the automatic
+    plan: the single-product partition on both ranks, equal to the one-GPU automatic call."""
+    monkeypatch.setenv("KNN_TEST_AUTO_PLAN", "1")
+    kn = knn()
+    kn.set_plan(kn.PLAN_AUTO)
+    case = ("sym", 16384, 24, 16, False, False)
+    mode, N, d, k, no_ipc, search = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    for _, i, dd, _m in res:
+        assert dd is not None, i
+    X = torch.from_numpy(datagen.points(N, d, "gauss", seed=93)).cuda()
+    ri, rd = reference(X, k)
+    assert kn.last_plan() == 5, kn.last_plan()
+    for _, i, dd, m in res:
+        assert m == kn.SHARD_MODES["sym"]
         assert np.array_equal(i, ri.cpu().numpy())
         assert np.array_equal(dd.view(np.uint32), rd.cpu().numpy().view(np.uint32))
