@@ -305,8 +305,7 @@ def run_ours(args):
         traffic = {}
 
     plan_code = knn.last_plan()
-    div = int(os.environ.get("KNN_PIVOT_DIV", "8"))
-    S_samp = -(-(cols_w // div) // 256) * 256 if k <= 32 else -(-max(cols_w // div, 4096) // 256) * 256
+    S_samp = knn.pivot_sample_size(cols_w, k)  # the library's own sample size (N / 8..16)
 
     # committed ncu captures: the headline's kernels under their names, C4's GEMMs with a
     # "_c4" suffix (profiles/traffic.json)
@@ -370,7 +369,7 @@ def run_ours(args):
                ", single hi.hi product" if pivot1 else ""), "dist_tc_kernel", f_ms, f_n,
             products=1 if pivot1 else 3)))
     if g_n and pivot_plan:
-        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x N/8 sampled columns -> 32-column chunk minima)"
+        gr = tensor_roof("dist_tc_kernel<MINS> (pivot sample pass: rows x N/div sampled columns (div 8-16 by N) -> 32-column chunk minima)"
                          if k <= 32 else
                          f"dist_tc_kernel<SAMPLE> (quantile-pivot sample: single-product upper bounds, rows x {S_samp} columns)",
                          "dist_tc_kernel_sample", g_ms, g_n, products=1)

@@ -227,6 +227,11 @@ knn_status knn_merge_lists(knn_ctx_t ctx, const float* const* dist_lists,
  * k <= N-1; N >= 16384 and 1 <= k <= 1024 (else KNN_ERR_UNSUPPORTED); tensor-core path. */
 int64_t knn_graph_units(int64_t N);
 int32_t knn_graph_list_cap(int32_t k);
+/* The pivot plans' column-sample size for N corpus points and k: the
+ * chunk-minimum sample of k <= 32 (N / 8, 12 or 16 by N; env KNN_PIVOT_DIV overrides) or
+ * the quantile sample of k > 32, rounded up to 256 columns.  (Introspection: bench.py's
+ * flop accounting of the sample pass.) */
+int64_t knn_pivot_sample_size(knn_ctx_t ctx, int64_t N, int32_t k);
 knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k, int32_t metric,
                             int64_t row0, int64_t rows, float* thr, void* stream);
 knn_status knn_graph_partition(knn_ctx_t ctx, const float* X, int64_t N, int32_t d, int32_t k,

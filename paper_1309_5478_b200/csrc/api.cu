@@ -128,6 +128,15 @@ int32_t pivot_rank(int32_t kk, int64_t S, int64_t N, int64_t M) {
     return best;
 }
 
+// The chunk-minimum sample's divisor (k <= 32): S = N / div sampled columns.  The sample
+// pass costs ~N^2 / div, the partition's survivors grow as div / (sample rank) (DESIGN.md
+// §6.5); measured optimum (one B200, k = 32, d = 256): 8 at N = 16384, 12 at 65536 (2.24
+// -> 2.20 ms), 16 at 131072 (7.7 -> 7.4 ms).  KNN_PIVOT_DIV overrides.
+int32_t sample_div(const knn_ctx* ctx, int64_t N) {
+    if (ctx->pivot_div > 0) return ctx->pivot_div;
+    return N < 49152 ? 8 : N < 98304 ? 12 : 16;
+}
+
 // Queue the whole hot path for one block problem; asynchronous on `s`.
 knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
                      int32_t d, int32_t k, int32_t metric, int64_t self_shift, int64_t idx_offset,
@@ -137,7 +146,7 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
     // Pivot plan (PAPER.md:56 quickselect at matrix scale): per-row pivot = k-th smallest of
     // the minima of the 32-column chunks of a column sample (>= the row's k-th distance),
     // then the GEMM keeps only elements <= pivot.
-    const int64_t Ssamp = round_up(N / ctx->pivot_div, 256);
+    const int64_t Ssamp = round_up(N / sample_div(ctx, N), 256);
     // the sample is a permuted column subset that may contain the row's own point: one
     // more rank keeps k non-self elements at or below the pivot
     const int32_t kk = self_shift != KNN_NO_SELF ? k + 1 : k;
@@ -147,7 +156,8 @@ knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, in
                        ctx->plan != KNN_PLAN_MATERIALISED && Ssamp / 32 >= kk + 1;
     // Quantile pivot for k > 32 (the same quickselect partition; the pivot is a bucketed
     // order statistic of a single-product sample of Sq columns)
-    const int64_t Sq = round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
+    const int32_t qdiv = ctx->pivot_div > 0 ? ctx->pivot_div : 8;  // (k > 32: N / 8, at least 4096)
+    const int64_t Sq = round_up(N / qdiv > 4096 ? N / qdiv : 4096, 256);
     const bool pivotq = allow_pivot && tc && ctx->pivot_ok && k > 32 && N >= 16384 && M >= 256 &&
                         ctx->plan != KNN_PLAN_MATERIALISED && Sq <= (N / 256) * 256;
     int32_t rq = 0;
@@ -621,7 +631,7 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
     const bool tc = ctx->gemm_mode == 0 && ctx->tc_ok;
     if ((env && strcmp(env, "0") == 0) || !tc || !ctx->pivot_ok || !ctx->sym_ok ||
         ctx->plan == KNN_PLAN_MATERIALISED || k > 32 || N < 16384 || N % 2048 != 0 ||
-        ctx->pivot_div != 8)
+        (ctx->pivot_div > 0 && ctx->pivot_div != 8))
         return KNN_ERR_UNSUPPORTED;
     const int64_t S = N / 8;                    // sample: points 8j, j < S (a multiple of 256)
     const int64_t CH = N / 8 >= 8192 ? N / 8 : 8192;  // chunk rows (a multiple of 256)
@@ -1129,6 +1139,13 @@ int64_t knn_graph_units(int64_t N) {
     return n * (n + 1) / 2;
 }
 
+int64_t knn_pivot_sample_size(knn_ctx_t ctx, int64_t N, int32_t k) {
+    if (!ctx || N < 1) return 0;
+    if (k <= 32) return round_up(N / sample_div(ctx, N), 256);
+    const int32_t qdiv = ctx->pivot_div > 0 ? ctx->pivot_div : 8;
+    return round_up(N / qdiv > 4096 ? N / qdiv : 4096, 256);
+}
+
 int32_t knn_graph_list_cap(int32_t k) {
     return k <= 32 ? 2048 : (int32_t)round_up(3 * (int64_t)k > 2048 ? 3 * (int64_t)k : 2048, 256);
 }
@@ -1214,8 +1231,9 @@ knn_status knn_graph_pivots(knn_ctx_t ctx, const float* X, int64_t N, int32_t d,
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
     const int32_t kk = k + 1;  // the sample may hold the row's own point
     const bool small = k <= 32;
-    const int64_t S = small ? round_up(N / ctx->pivot_div, 256)
-                            : round_up(N / ctx->pivot_div > 4096 ? N / ctx->pivot_div : 4096, 256);
+    const int32_t qdiv = ctx->pivot_div > 0 ? ctx->pivot_div : 8;
+    const int64_t S = small ? round_up(N / sample_div(ctx, N), 256)
+                            : round_up(N / qdiv > 4096 ? N / qdiv : 4096, 256);
     if (small && S / 32 < kk + 1) return fail(ctx, KNN_ERR_UNSUPPORTED, "sample too small for k");
     const bool l2 = metric <= KNN_L2;
     ShardPrep sp;

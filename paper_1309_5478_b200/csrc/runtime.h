@@ -36,7 +36,7 @@ struct knn_ctx {
     bool sym_ok = true;        // env KNN_SYM=0 disables the symmetric k-NNG GEMM
     bool pivot_ok = true;      // env KNN_PIVOT=0 disables the pivot (partition) plan
     int32_t pivot_cap = 2048;  // candidates per row kept by the partition GEMM
-    int32_t pivot_div = 8;     // sample = the first N / pivot_div corpus points
+    int32_t pivot_div = 0;     // k <= 32 sample = N / pivot_div corpus points; 0: by N (sample_div)
     // k <= 32, L2 metrics: single-product partition + re-evaluation: -1 chosen
     // on the device per call (default), 1 always (env KNN_PIVOT1=1), 0 never (KNN_PIVOT1=0)
     int pivot1 = -1;
@@ -149,6 +149,8 @@ struct Prepared {
     __half* lo;
 };
 
+// The k <= 32 pivot sample's divisor for N corpus points (api.cu).
+int32_t sample_div(const knn_ctx* ctx, int64_t N);
 // Queue the whole hot path for one block problem (knn_search_block semantics); asynchronous.
 knn_status run_block(knn_ctx* ctx, const float* Q, int64_t M, const float* X, int64_t N,
                      int32_t d, int32_t k, int32_t metric, int64_t self_shift, int64_t idx_offset,

@@ -30,7 +30,7 @@ SYMBOLS = ["knn_abi_version", "knn_ctx_create", "knn_ctx_destroy", "knn_last_err
            "knn_gemm_path", "knn_set_plan", "knn_last_plan", "knn_last_candidates", "knn_profile_enable",
            "knn_profile_read", "knn_last_select_kernel", "knn_select_paper",
            "knn_search_streamed", "knn_merge_lists", "knn_ipc_export", "knn_ipc_open",
-           "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_graph_pivots",
+           "knn_ipc_close_all", "knn_graph_units", "knn_graph_list_cap", "knn_pivot_sample_size", "knn_graph_pivots",
            "knn_graph_partition", "knn_graph_gather_select", "knn_diag_mainloop",
            "knn_comm_unique_id", "knn_comm_init", "knn_comm_init_ops", "knn_comm_destroy", "knn_comm_info",
            "knn_shard_range", "knn_graph_sharded", "knn_search_sharded", "knn_last_shard_mode"]
@@ -102,6 +102,7 @@ def load_library():
             "knn_graph_units": (i64, [i64]),
             "knn_diag_mainloop": (st, [p, p, i64, i32, i32, i32, ctypes.POINTER(ctypes.c_double)]),
             "knn_graph_list_cap": (i32, [i32]),
+            "knn_pivot_sample_size": (i64, [p, i64, i32]),
             "knn_graph_pivots": (st, [p, p, i64, i32, i32, i32, i64, i64, p, p]),
             "knn_graph_partition": (st, [p, p, i64, i32, i32, i32, p, i64, i64, p, p, i32, p]),
             "knn_graph_gather_select": (st, [p, i32, p, p, i32, i64, i32, i64, i64, p, p, p]),
@@ -331,6 +332,11 @@ def merge_lists(dist_ptrs, idx_ptrs, row0, M, k, offsets=None, device=None, stre
 def graph_units(N):
     """Units (256x256 pair blocks) of the upper triangle of the k-NNG of N points."""
     return int(load_library().knn_graph_units(N))
+
+
+def pivot_sample_size(N, k, device=None):
+    """knn_pivot_sample_size: the pivot plans' column-sample size for N points and k."""
+    return int(load_library().knn_pivot_sample_size(context(device), N, k))
 
 
 def graph_list_cap(k):
