@@ -634,7 +634,12 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         (ctx->pivot_div > 0 && ctx->pivot_div != 8))
         return KNN_ERR_UNSUPPORTED;
     const int64_t S = N / 8;                    // sample: points 8j, j < S (a multiple of 256)
-    const int64_t CH = N / 8 >= 8192 ? N / 8 : 8192;  // chunk rows (a multiple of 256)
+    // chunk rows (a multiple of 256): N / 8, at least 8192.  (The last chunk's partition
+    // covers its columns against every row, ~2/n of the triangle after the last copy, but
+    // N / 16 measured slower: e2e 3.06 -> 3.38 ms at the headline; env KNN_PIPE_DIV.)
+    const char* pdv = getenv("KNN_PIPE_DIV");
+    const int64_t pdiv = pdv && atoi(pdv) >= 1 ? atoi(pdv) : 8;
+    const int64_t CH = round_up(N / pdiv >= 8192 ? N / pdiv : 8192, 256);
     const int nch = (int)ceil_div(N, CH);
     const int32_t d_pad = (int32_t)round_up(d, knn::kSplitKAlign);
     const int32_t cap = ctx->pivot_cap;
@@ -704,7 +709,8 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
             KNN_CUDA(cudaEventCreateWithFlags(&ctx->ev_free[b], cudaEventDisableTiming));
         }
     }
-    while ((int)ctx->ev_chunk.size() < nch + 2) {
+    constexpr int kOutChunks = 4;  // re-evaluation row chunks, each copied back as it ends
+    while ((int)ctx->ev_chunk.size() < nch + 3 + kOutChunks) {
         cudaEvent_t e = nullptr;
         KNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         ctx->ev_chunk.push_back(e);
@@ -793,16 +799,32 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         ctx->launches += p1_auto ? 1 : 0;
         tf.done();
     }
-    {
+    // the exact select / re-evaluation in row chunks, each chunk's results copied back on the
+    // copy stream while the next chunk computes (a failed certificate redoes the whole call
+    // below and copies again)
+    const int64_t RC = round_up(ceil_div(N, (int64_t)kOutChunks), (int64_t)256);
+    for (int oc = 0; oc * RC < N; ++oc) {
+        const int64_t r0 = oc * RC, R = N - r0 < RC ? N - r0 : RC;
         Timed tc2(ctx, KNN_KERNEL_MERGE, s);
         if (one || p1_auto)
-            KNN_CUDA(knn::launch_candidate_recompute(cnt, cent, cap, N, k, 0, x, x, d, px.sqn, bnd, bnd, thr, metric,
-                                                     oi, od, flag, s, p1_auto ? 1 : -1));
+            KNN_CUDA(knn::launch_candidate_recompute(cnt + r0, cent + r0 * cap, cap, R, k, 0, x + r0 * d, x, d,
+                                                     px.sqn + r0, bnd + r0, bnd, thr + r0, metric, oi + r0 * k,
+                                                     od + r0 * k, flag, s, p1_auto ? 1 : -1));
         if (!one)
-            KNN_CUDA(knn::launch_candidate_select(cnt, cent, cap, N, k, 0, oi, od, flag, s, p1_auto ? 0 : -1));
+            KNN_CUDA(knn::launch_candidate_select(cnt + r0, cent + r0 * cap, cap, R, k, 0, oi + r0 * k, od + r0 * k,
+                                                  flag, s, p1_auto ? 0 : -1));
         ctx->launches += p1_auto ? 1 : 0;
         tc2.done();
+        cudaEvent_t ev = ctx->ev_chunk[nch + 2 + oc];
+        KNN_CUDA(cudaEventRecord(ev, s));
+        KNN_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        KNN_CUDA(cudaMemcpyAsync(out_idx_host + r0 * k, oi + r0 * k, (size_t)R * k * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, cs));
+        KNN_CUDA(cudaMemcpyAsync(out_dist_host + r0 * k, od + r0 * k, (size_t)R * k * sizeof(float),
+                                 cudaMemcpyDeviceToHost, cs));
     }
+    KNN_CUDA(cudaEventRecord(ctx->ev_chunk[nch + 2 + kOutChunks], cs));
+    KNN_CUDA(cudaStreamWaitEvent(s, ctx->ev_chunk[nch + 2 + kOutChunks], 0));
     ctx->last_plan = one ? 5 : 3;
     ctx->last_plan_auto1 = p1_auto;
     knn_status st = finish_blocking(ctx, s);
@@ -810,11 +832,12 @@ knn_status host_graph_pipelined(knn_ctx* ctx, const float* X_host, int64_t N, in
         ctx->pivot_redos++;
         KNN_TRY(run_block(ctx, x, N, x, N, d, k, metric, 0, 0, oi, od, s, false));
         st = finish_blocking(ctx, s);
+        if (st != KNN_OK) return st;
+        KNN_CUDA(cudaMemcpyAsync(out_idx_host, oi, (size_t)N * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)N * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+        return finish_blocking(ctx, s);
     }
-    if (st != KNN_OK) return st;
-    KNN_CUDA(cudaMemcpyAsync(out_idx_host, oi, (size_t)N * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    KNN_CUDA(cudaMemcpyAsync(out_dist_host, od, (size_t)N * k * sizeof(float), cudaMemcpyDeviceToHost, s));
-    return finish_blocking(ctx, s);
+    return st;
 }
 
 knn_status knn_search_block_host(knn_ctx_t ctx, const float* Q_host, int64_t M,
