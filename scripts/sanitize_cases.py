@@ -85,6 +85,7 @@ def par3():
     for g in range(G):
         knn.graph_gather_select([l[0].data_ptr() for l in lists], [l[1].data_ptr() for l in lists], cap, N, k,
                                 g * per, min(N, (g + 1) * per) - g * per)
+        assert knn.last_plan() == 5, knn.last_plan()  # the single-product partition + re-evaluation
 
 
 cases = {"c1": c1, "pivot": pivot, "hostpipe": hostpipe, "twopass": twopass, "pivotq": pivotq,
