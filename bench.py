@@ -413,9 +413,36 @@ def run_ours(args):
         sel_rows = R_local if sym_shard else rows_w
         cs_name = ("candidate_recompute_kernel" if pivot1 else "candidate_select_kernel") if k <= 32 \
             else "candidate_select_warp_kernel"
-        rooflines.append((m_ms, hbm_roof(f"{cs_name} (exact select of the partition)",
-                                         cs_name, m_ms, m_n,
-                                         cands * 8.0 + sel_rows * (4.0 + k * 8.0))))
+        if pivot1:
+            # the re-evaluation gathers the fp32 rows of its ~40 survivors per row from L2: its
+            # roofline is the measured L2 gather rate of that pattern (tools/l2_gather_probe.cu,
+            # profiles/l2_gather_probe.json); |R| from one untimed call with the library's
+            # counter (KNN_RECOMP_STATS counts the re-evaluated set instead of the lists)
+            os.environ["KNN_RECOMP_STATS"] = "1"
+            step()
+            torch.cuda.synchronize()
+            reev = knn.last_candidates()
+            del os.environ["KNN_RECOMP_STATS"]
+            step()  # (restores the library's candidate count of a normal call)
+            torch.cuda.synchronize()
+            try:
+                with open(os.path.join(ROOT, "profiles", "l2_gather_probe.json")) as f:
+                    l2peak = json.load(f)["l2_gather_gbs"]
+            except Exception:
+                l2peak = None
+            r = hbm_roof(f"{cs_name} (exact select of the partition: fp32 re-evaluation of the survivors "
+                         f"near the k-th, rows gathered from L2)", cs_name, m_ms, m_n,
+                         reev * d * 4.0 + cands * 8.0 + sel_rows * (4.0 + k * 8.0))
+            if l2peak:
+                r.update({"bound": "l2", "peak": l2peak, "frac": r["achieved"] / l2peak,
+                          "peak_kind": "measured L2 gather rate, random 1 KB rows of a 64 MB L2-resident "
+                                       "matrix (profiles/l2_gather_probe.json)"})
+            r["reevaluated_per_row"] = reev / max(sel_rows, 1)
+            rooflines.append((m_ms, r))
+        else:
+            rooflines.append((m_ms, hbm_roof(f"{cs_name} (exact select of the partition)",
+                                             cs_name, m_ms, m_n,
+                                             cands * 8.0 + sel_rows * (4.0 + k * 8.0))))
         rooflines[-1][1]["candidates_per_row"] = cands / max(sel_rows, 1)
     if x_n:  # Par-2: the k-way merge of the ranks' partial lists of this rank's rows
         rooflines.append((x_ms, hbm_roof("merge_lists_kernel (a-S6, corpus-sharded k-way merge)",
