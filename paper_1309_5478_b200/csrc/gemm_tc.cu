@@ -173,23 +173,27 @@ template <int MODE, bool ARES = false>
 #define KNN_MINS_WARPS 8  // epilogue warps of the chunk-minimum sample pass (8 or 16)
 #endif
 #ifndef KNN_PV1_WARPS
-#define KNN_PV1_WARPS 16  // epilogue warps of the single-product partition (12 or 16)
+#define KNN_PV1_WARPS 16  // epilogue warps of the single-product partition (12, 16 or 20; 20 with
+                          // 80 registers, a 3-stage ring and 64-entry pending lists measured
+                          // slower: 1.42 -> 1.48 ms)
 #endif
 struct EpiCfg {
     static constexpr bool PV = MODE == 1 || MODE == 5;  // MODE_PIVOT, MODE_PIVOT1
     // the single-product partition is bound by its epilogue's latency: 16 warps (4 per TMEM
     // lane quadrant, 2 chunks each) over a 4-stage operand ring (the MMA is not its limit)
-    static constexpr bool PV16 = MODE == 5 && KNN_PV1_WARPS == 16;
-    static constexpr int WARPS = PV16 || (MODE == 2 && KNN_MINS_WARPS == 16) ? 16 : PV ? 12 : EPI_WARPS;
+    static constexpr bool PV20 = MODE == 5 && KNN_PV1_WARPS == 20;  // (5 per quadrant; one idles per tile)
+    static constexpr bool PV16 = MODE == 5 && (KNN_PV1_WARPS == 16 || PV20);
+    static constexpr int WARPS = PV20 ? 20 : PV16 || (MODE == 2 && KNN_MINS_WARPS == 16) ? 16 : PV ? 12 : EPI_WARPS;
     static constexpr int PARTS = WARPS / 4;
     static constexpr int CPW = (BN / 32 + PARTS - 1) / PARTS;  // chunks per warp (last: fewer)
     // PV staging: 32 rows of SROW floats (KNN_EPI_REG) or a swizzled 32x32 chunk
     static constexpr int STG_PV = KNN_EPI_REG ? 32 * SROW * 4 : STG_BYTES;
-    static constexpr int PEND = PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 96) : 128) : PEND_CAP;
+    static constexpr int PEND = PV20 ? 64 : PV16 ? 96 : PV ? (KNN_EPI_REG ? (CTA2 ? 160 : 96) : 128) : PEND_CAP;
     static constexpr int SLAB = PV ? STG_PV + 16 * PEND : MODE == 2 ? 0 : 2 * STG_BYTES;  // per warp
     static constexpr int NCOLS = PV16 ? 6 : PV ? 3 : NCOL;  // column-data ring slots
     static constexpr int THREADS = 64 + 32 * WARPS + 32;
-    static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE : PV16 ? 4 * (A_BYTES + B_TILE) : RING_BYTES;
+    static constexpr int RING = ARES ? 2 * ARES_PANEL + ARES_KB * B_TILE
+                                     : PV20 ? 3 * (A_BYTES + B_TILE) : PV16 ? 4 * (A_BYTES + B_TILE) : RING_BYTES;
     static constexpr int SMEM = RING + WARPS * SLAB + NCOLS * COL_BYTES + 1024 + 1024;
     static_assert(SMEM <= 232448, "shared memory");
     static_assert(SLAB % 16 == 0, "slab alignment");
@@ -427,6 +431,10 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
             const float* col_t = col_n + 2 * BN;
             mbar_wait(tfull0 + 8 * buf, tphase);
             tc_fence_after();
+            if (nch <= 0) {  // (E::PV20: this warp's share of the tile is empty; it still frees it)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+            }
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + ch0 * 32;
             #pragma unroll 1  // (unrolling the two chunks of the 16-warp partition: 1.45 -> 1.59 ms)
             for (int ch = 0; ch < nch; ++ch) {
