@@ -786,3 +786,60 @@ def test_per_point_bound_mixed_residuals(metric):
     assert np.array_equal(hi, gi) and np.array_equal(hd.view(np.uint32), gd.view(np.uint32))
     rows = np.concatenate([np.arange(0, N, 97), np.arange(0, N, 8)[:64]])
     e2e_check(X, X, gi, gd, k, np.unique(rows), True, metric=metric)
+
+
+_LISTS_CODE = """
+import sys, numpy as np, torch
+from paper_1309_5478_b200 import knn, datagen
+N, d, k, dist, mixed = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], int(sys.argv[5])
+X = datagen.points(N, d, dist, seed=N + 3 * d)
+if mixed:
+    X[::8] = X[::8].astype(np.float16).astype(np.float32)
+Xt = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+npad = -(-N // 256) * 256
+thr = torch.full((npad,), float("nan"), device="cuda")
+knn.graph_pivots(Xt, k, 0, N, thr)
+cap = knn.graph_list_cap(k)
+cnt = torch.zeros(N, dtype=torch.int32, device="cuda")
+ce = torch.empty((N, cap), dtype=torch.int64, device="cuda")
+knn.graph_partition(Xt, k, thr, 0, knn.graph_units(N), cnt, ce)
+torch.cuda.synchronize()
+np.save(sys.argv[6], X)
+np.save(sys.argv[7], thr.cpu().numpy())
+np.save(sys.argv[8], cnt.cpu().numpy())
+np.save(sys.argv[9], ce.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("N,d,k,dist,mixed", [(16384, 48, 16, "gauss", 0), (20000, 30, 10, "clusters", 0),
+                                              (16384, 40, 32, "uniform", 1)])
+def test_single_product_lists_are_sound(N, d, k, dist, mixed, tmp_path):
+    """The single-product partition (KNN_PIVOT1=1, readings R20/R21) read
+    straight from its lists (knn_graph_pivots + knn_graph_partition): every listed key L is a
+    lower bound of the exact distance of its pair (the oracle's fp64 value of the fp32
+    inputs), and every pair whose exact distance is at or below the row's pivot is listed
+    — the two properties the plan's exactness rests on — on data near the origin, far from
+    it (clusters: wide bounds) and with fp16-exact points mixed in (per-point residuals 0)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    paths = [str(tmp_path / f) for f in ("x.npy", "thr.npy", "cnt.npy", "ce.npy")]
+    subprocess.run([sys.executable, "-c", _LISTS_CODE, str(N), str(d), str(k), dist, str(mixed)] + paths,
+                   check=True, cwd=root, timeout=600, env=dict(os.environ, KNN_PIVOT1="1"))
+    X, thr, cnt, ce = (np.load(p) for p in paths)
+    cap = ce.shape[1]
+    assert np.all(cnt[:N] <= cap), "list overflow"
+    rows = np.unique(np.concatenate([[0, N - 1], np.arange(0, N, N // 61)]))
+    D64 = oracle.dist_rows(X, X, rows=rows)
+    for r, i in enumerate(rows):
+        n = int(cnt[i])
+        ent = ce[i, :n].view(np.uint64)
+        cols = (ent & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        keys = (ent >> np.uint64(32)).astype(np.uint32)
+        # the key is the IEEE bits of L >= +0 with the sign bit set (include/knn.h)
+        L = (keys & np.uint32(0x7FFFFFFF)).view(np.float32).astype(np.float64)
+        assert len(np.unique(cols)) == n and not np.any(cols == i), i
+        assert np.all(L <= D64[r, cols]), (i, float(np.max(L - D64[r, cols])))
+        # thr holds nextup(pivot): the partition keeps L < thr
+        pivot = float(np.nextafter(np.float32(thr[i]), np.float32(-np.inf)))
+        need = np.flatnonzero(D64[r] <= pivot)
+        need = need[need != i]
+        assert np.isin(need, cols).all(), (i, len(need), n)
