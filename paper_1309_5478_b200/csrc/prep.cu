@@ -70,12 +70,30 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
     }
     double s = 0.0;
     float amax = 0.0f;
-    for (int t = lane; t < d; t += 32) {
-        float v = __ldg(x + t);
-        finite &= isfinite(v);
-        const double c = (double)v - mean;
-        amax = fmaxf(amax, fabsf((float)c));
-        s += c * c;
+    // 16-byte loads when the rows allow (d % 4 == 0, X 16-byte aligned); same sums per lane
+    // order is not required: s is fp64 and rounded once (reading R15)
+    const bool vec4 = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    if (vec4) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int t = lane; t < d / 4; t += 32) {
+            const float4 q = __ldg(x4 + t);
+            const float vv[4] = {q.x, q.y, q.z, q.w};
+            #pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                finite &= isfinite(vv[e]);
+                const double c = (double)vv[e] - mean;
+                amax = fmaxf(amax, fabsf((float)c));
+                s = fma(c, c, s);
+            }
+        }
+    } else {
+        for (int t = lane; t < d; t += 32) {
+            float v = __ldg(x + t);
+            finite &= isfinite(v);
+            const double c = (double)v - mean;
+            amax = fmaxf(amax, fabsf((float)c));
+            s += c * c;
+        }
     }
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -114,6 +132,35 @@ prep_kernel(const float* __restrict__ X, int64_t N, int32_t d, int32_t d_pad,
     // from the exact scaled input (per-point bound of the single product)
     const double sd = ldexp(1.0, sh);
     double rr = 0.0, vv = 0.0;
+    if ((d & 7) == 0 && vec4 && !(metric == 3 && angular)) {
+        // 8 elements per lane per step: two 16-byte loads, one 16-byte store per half
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int g = lane; g < d_pad / 8; g += 32) {
+            float xv[8];
+            if (8 * g < d && finite) {
+                const float4 a = __ldg(x4 + 2 * g), b = __ldg(x4 + 2 * g + 1);
+                xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+                xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
+            } else {
+                #pragma unroll
+                for (int e = 0; e < 8; ++e) xv[e] = 0.0f;
+            }
+            __align__(16) __half hh[8], ll[8];
+            #pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float v = xv[e] * s1 * s2;  // exact power-of-two scaling
+                hh[e] = __float2half_rn(v);
+                ll[e] = __float2half_rn(v - __half2float(hh[e]));
+                if (eps2) {
+                    const double vx = (double)xv[e] * sd, r = vx - (double)__half2float(hh[e]);
+                    rr = fma(r, r, rr);
+                    vv = fma(vx, vx, vv);
+                }
+            }
+            *reinterpret_cast<uint4*>(h + 8 * g) = *reinterpret_cast<const uint4*>(hh);
+            *reinterpret_cast<uint4*>(l + 8 * g) = *reinterpret_cast<const uint4*>(ll);
+        }
+    } else
     for (int t = lane; t < d_pad; t += 32) {
         float v = 0.0f;
         float xv = 0.0f;
