@@ -399,17 +399,20 @@ __global__ void __launch_bounds__(256) pivot1_decide_kernel(const float* __restr
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last && threadIdx.x < 32) {  // one warp adds the partials in a fixed order (deterministic)
         __threadfence();
-        double a = 0, b = 0, t = 0, n = 0;
-        for (int k = 0; k < (int)gridDim.x; ++k) {
-            a += __ldcg(part + 4 * k);
-            b += __ldcg(part + 4 * k + 1);
-            t += __ldcg(part + 4 * k + 2);
-            n += __ldcg(part + 4 * k + 3);
+        const int lane = threadIdx.x;
+        double v4[4] = {0, 0, 0, 0};
+        for (int k = lane; k < (int)gridDim.x; k += 32)
+            #pragma unroll
+            for (int a = 0; a < 4; ++a) v4[a] += __ldcg(part + 4 * k + a);
+        #pragma unroll
+        for (int a = 0; a < 4; ++a)
+            for (int o = 16; o > 0; o >>= 1) v4[a] += __shfl_xor_sync(0xFFFFFFFFu, v4[a], o);
+        if (lane == 0) {
+            const double width = 2.0 * (double)F * (v4[0] / (double)M + v4[1] / (double)N);
+            flag[1] = (v4[3] > 0 && width <= (double)ratio * (v4[2] / v4[3])) ? 1 : 0;
         }
-        const double width = 2.0 * (double)F * (a / (double)M + b / (double)N);
-        flag[1] = (n > 0 && width <= (double)ratio * (t / n)) ? 1 : 0;
     }
 }
 }  // namespace
