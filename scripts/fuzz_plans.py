@@ -1,10 +1,15 @@
-"""Randomised cross-check: the automatic plan vs the materialised plan (bit-identical by
-design) over random shapes, metrics and distributions.  python scripts/fuzz_plans.py [n] [seed]"""
+"""Randomised cross-check over random shapes, metrics and distributions: the automatic plan
+vs the materialised plan, bit-identical by design for the FP32-accurate plans; when the device
+chose the single-product partition (plans 5 / 6: re-evaluated fp32 values, reading R20) both
+results are checked against the oracle on sampled rows instead (E2E checks of oracle.checks).
+python scripts/fuzz_plans.py [n] [seed]"""
 import os, sys, json, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_1309_5478_b200 import knn, datagen
+import oracle
+from oracle import checks
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
@@ -28,7 +33,17 @@ for case in range(n_cases):
         ri, rd = run()
     finally:
         knn.set_plan(knn.PLAN_AUTO)
-    ok = torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+    if plan in (5, 6):
+        Qn, Xn = Q.cpu().numpy(), X.cpu().numpy()
+        rows = np.unique(np.concatenate([[0, Qn.shape[0] - 1], rng.integers(0, Qn.shape[0], 14)]))
+        D64 = oracle.dist_rows(Qn, Xn, rows=rows, metric=metric)
+        ok = True
+        for i_, d_ in ((gi, gd), (ri, rd)):
+            res = checks.check_rows(i_.cpu().numpy()[rows], d_.cpu().numpy()[rows], D64, oracle.sqnorms(Qn)[rows],
+                                    oracle.sqnorms(Xn), rows, k, metric=metric, graph=not search)
+            ok = ok and res["failures"] == []
+    else:
+        ok = torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
     bad += not ok
     print(json.dumps({"case": case, "N": N, "M": Q.shape[0], "d": d, "k": k, "metric": metric, "dist": dist,
                       "search": search, "plan": plan, "equal": ok}), flush=True)
