@@ -2060,8 +2060,9 @@ __device__ __forceinline__ void candidate_select_row(int64_t row, const int32_t*
     // the row's entries (ukey << 32 | col): keys are the odd words, columns the even ones
     const uint32_t* ri = reinterpret_cast<const uint32_t*>(cent + row * cap);
     const uint32_t* rk = ri + 1;
-    const uint32_t* fk = rk;
-    const uint32_t* fi = ri;
+    const uint32_t* fk = rk;  // the kept pairs: the list itself (stride 2 words) when n <= k,
+    const uint32_t* fi = ri;  // else the compacted shared-memory copy (stride 1)
+    int fs = 2;
     int m = n;
     if (n > k) {
         bool done = false;
@@ -2179,6 +2180,7 @@ __device__ __forceinline__ void candidate_select_row(int64_t row, const int32_t*
             if (base + eq <= 32) {  // every tie at T kept: the k best are among them
                 fk = skey_w;
                 fi = sidx_w;
+                fs = 1;
                 m = base + eq;
                 done = true;
             }
@@ -2187,11 +2189,14 @@ __device__ __forceinline__ void candidate_select_row(int64_t row, const int32_t*
             ws::warp_select_k<2>(rk, ri, n, k, skey_w, sidx_w, hist_w);
             fk = skey_w;
             fi = sidx_w;
+            fs = 1;
             m = k;
         }
     }
-    // sort the m <= 32 kept pairs; slots past m are empty (-1, +inf)
-    uint64_t v[1] = {lane < m ? ((uint64_t)fk[lane] << 32 | fi[lane]) : ~0ull};
+    // sort the m <= 32 kept pairs; slots past m are empty (-1, +inf).  (n <= k reads the list's
+    // interleaved entries directly: stride 2 — a stride-1 read here returned garbage for rows
+    // with exactly k candidates, reachable since the per-point bound's tighter pivots.)
+    uint64_t v[1] = {lane < m ? ((uint64_t)fk[fs * lane] << 32 | fi[fs * lane]) : ~0ull};
     ws::warp_bitonic<1>(v);
     if (lane < k) {
         const uint32_t key = (uint32_t)(v[0] >> 32);

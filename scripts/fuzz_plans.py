@@ -36,7 +36,7 @@ for case in range(n_cases):
     if plan in (5, 6):
         Qn, Xn = Q.cpu().numpy(), X.cpu().numpy()
         rows = np.unique(np.concatenate([[0, Qn.shape[0] - 1], rng.integers(0, Qn.shape[0], 14)]))
-        D64 = oracle.dist_rows(Qn, Xn, rows=rows, metric=metric)
+        D64 = oracle.dist_rows(Qn, Xn, rows=rows, metric=0 if metric <= 1 else metric)  # (L2: squared)
         ok = True
         for i_, d_ in ((gi, gd), (ri, rd)):
             res = checks.check_rows(i_.cpu().numpy()[rows], d_.cpu().numpy()[rows], D64, oracle.sqnorms(Qn)[rows],

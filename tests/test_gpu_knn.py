@@ -843,3 +843,24 @@ def test_single_product_lists_are_sound(N, d, k, dist, mixed, tmp_path):
         need = np.flatnonzero(D64[r] <= pivot)
         need = need[need != i]
         assert np.isin(need, cols).all(), (i, len(need), n)
+
+
+@pytest.mark.parametrize("N,d,k,metric,dist,seed", [(44677, 3, 2, 0, "uniform", 1071), (36383, 3, 2, 0, "gauss", 1173),
+                                                    (34516, 7, 5, 3, "grid", 1194), (30639, 257, 2, 3, "gauss", 1043)])
+def test_pivot_plan_rows_with_exactly_k_candidates(N, d, k, metric, dist, seed):
+    """Regression (found by scripts/fuzz_plans.py): with the per-point bound's tighter pivots
+    some rows keep exactly k candidates, and the exact candidate select read that short list
+    with the wrong stride (garbage first neighbour).  The automatic plan must equal the
+    materialised plan bit for bit (plans 3 / 4 here: the FP32-accurate partition)."""
+    kn = knn()
+    X = cuda(datagen.points(N, d, dist, seed=seed))
+    gi, gd = kn.graph(X, k, metric=metric)
+    plan = kn.last_plan()
+    try:
+        kn.set_plan(kn.PLAN_MATERIALISED)
+        ri, rd = kn.graph(X, k, metric=metric)
+    finally:
+        kn.set_plan(kn.PLAN_AUTO)
+    if plan in (3, 4):
+        assert torch.equal(gi, ri) and torch.equal(gd.view(torch.int32), rd.view(torch.int32))
+    assert int(gi.min()) >= 0 and not torch.isnan(gd).any()
