@@ -520,9 +520,16 @@ dist_tc_kernel(const __grid_constant__ CUtensorMap map_qh, const __grid_constant
                         #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int c = 4 * c4 + 2 * h;
-                            const uint64_t p = f2_mul(f2_pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), cq2);
+                            const uint64_t acc2 = f2_pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+                            const uint64_t sj = h ? f2_pack(ss.z, ss.w) : f2_pack(ss.x, ss.y);
                             const uint64_t ns = f2_add(qn2, h ? f2_pack(nn.z, nn.w) : f2_pack(nn.x, nn.y));
-                            const uint64_t u2 = f2_fma(p, h ? f2_pack(ss.z, ss.w) : f2_pack(ss.x, ss.y), ns);
+                            // L2: fl(fl(acc cq) s_j + ns) — the scales are powers of two, so
+                            // the two orientations of a pair agree exactly.  Cosine / Pearson:
+                            // the scales are not, so the scale product is formed first,
+                            // fl(acc fl(cq s_j) + ns), symmetric in (q, x): the blocked and the
+                            // symmetric (mirrored) plans then give the same bits
+                            const uint64_t u2 = METRIC == 2 ? f2_fma(acc2, f2_mul(cq2, sj), ns)
+                                                            : f2_fma(f2_mul(acc2, cq2), sj, ns);
                             float u0, u1;
                             f2_unpack(u2, u0, u1);
                             // cosine: the sentinel clamp before any comparison (key <= T => u <= T)
