@@ -1,6 +1,7 @@
-"""Randomised cross-check of the other entry points against the device-resident k-NNG (all
-under the automatic plan, bit for bit): the host-pipelined call (knn_search_block_host),
-Par-3's phases with G = 2..3 emulated ranks, and the one-rank sharded call.
+"""Randomised cross-check of the other entry points against the device-resident k-NNG / search
+(all under the automatic plan, bit for bit): the host-pipelined call (knn_search_block_host),
+Par-3's phases with G = 2..3 emulated ranks, and the one-rank sharded calls (sym / query /
+corpus k-NNG, query / corpus search) through their phases.
 python scripts/fuzz_paths.py [n] [seed]"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,6 +35,12 @@ for case in range(n_cases):
     Xp = torch.from_numpy(X).pin_memory().numpy()
     res["host"] = same(ref, knn.search_block_host(Xp, Xp, k, metric=metric, self_shift=0))
     res["sym1"] = same(ref, knn.graph_sharded(Xt, k, mode="sym", metric=metric))
+    res["query1"] = same(ref, knn.graph_sharded(Xt, k, mode="query", metric=metric))
+    res["corpus1"] = same(ref, knn.graph_sharded(Xt, k, mode="corpus", metric=metric))
+    Qt = torch.from_numpy(datagen.points(int(rng.integers(300, 3000)), d, dist, seed=6000 + case)).cuda()
+    sref = knn.search(Qt, Xt, k)  # (knn_search / knn_search_sharded: squared L2, BJ's signature)
+    res["search_query1"] = same(sref, knn.search_sharded(Qt, Xt, k, mode="query"))
+    res["search_corpus1"] = same(sref, knn.search_sharded(Qt, Xt, k, mode="corpus"))
     G = int(rng.integers(2, 4))
     npad = -(-N // 256) * 256
     thr = torch.full((npad,), float("nan"), device="cuda")
