@@ -2332,10 +2332,11 @@ __device__ __forceinline__ void recompute_row(int64_t row, int n, const uint64_t
     const int n1 = n < 32 * PER ? n : 32 * PER;
     uint32_t v[PER], lk[PER], li[PER];
     #pragma unroll
-    for (int i = 0; i < PER; ++i) {
+    for (int i = 0; i < PER; ++i) {  // one 8-byte load per entry: x = column, y = key
         const int pos = lane + 32 * i;
-        lk[i] = pos < n1 ? __ldg(rk + 2 * pos) : 0xFFFFFFFFu;
-        li[i] = pos < n1 ? __ldg(ri + 2 * pos) : 0u;
+        const uint2 e = pos < n1 ? __ldg(reinterpret_cast<const uint2*>(ri) + pos) : make_uint2(0u, 0xFFFFFFFFu);
+        lk[i] = e.y;
+        li[i] = e.x;
     }
     #pragma unroll
     for (int i = 0; i < PER; ++i) {
